@@ -1,0 +1,180 @@
+"""fp64 CPU oracle for the GatedFWA hot path -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline``
+/ ``--impl reference`` leg may import this package.  It wraps
+``oracle/gfwa_oracle.c`` (plain C, fp64 loops, OpenMP over (b, h)) through
+ctypes and shares no code with ``paper_2512_07782_b200`` (neither imports the
+other).  Inputs are numpy/torch arrays; they are converted to float64 (the
+exact values the GPU saw, upcast) before the call.
+
+See ``gfwa_oracle.c`` for the paper citations of every function.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "gfwa_oracle.c")
+_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+_D = ctypes.POINTER(ctypes.c_double)
+_I64 = ctypes.c_int64
+
+
+def build(force: bool = False) -> str:
+    """Compile gfwa_oracle.c -> liboracle.so with gcc -O2 -fopenmp."""
+    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC):
+        tmp = _LIB_PATH + f".tmp{os.getpid()}"
+        subprocess.check_call(
+            ["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-std=c11", "-o", tmp, _SRC, "-lm"]
+        )
+        os.replace(tmp, _LIB_PATH)
+    return _LIB_PATH
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        lib = ctypes.CDLL(_LIB_PATH)
+        lib.oracle_num_threads.restype = ctypes.c_int
+        lib.oracle_attend_row.restype = ctypes.c_double
+        _lib = lib
+    return _lib
+
+
+def _f64(x) -> np.ndarray:
+    """Exact upcast of a torch tensor / numpy array to contiguous float64."""
+    try:
+        import torch
+
+        if isinstance(x, torch.Tensor):
+            x = x.detach().to("cpu", torch.float64).numpy()
+    except ImportError:  # pragma: no cover
+        pass
+    return np.ascontiguousarray(np.asarray(x, dtype=np.float64))
+
+
+def _p(a: np.ndarray | None):
+    if a is None:
+        return ctypes.cast(None, _D)
+    assert a.dtype == np.float64 and a.flags["C_CONTIGUOUS"]
+    return a.ctypes.data_as(_D)
+
+
+def num_threads() -> int:
+    return int(_load().oracle_num_threads())
+
+
+def gate_alpha(h, beta, eps: float = 1e-6) -> np.ndarray:
+    """alpha [B,H,N] from h, beta [B,N,H] (Eq. 9; Alg. 1 l.5-7)."""
+    h, beta = _f64(h), _f64(beta)
+    B, N, H = h.shape
+    out = np.empty((B, H, N))
+    _load().oracle_gate_alpha(_p(h), _p(beta), _I64(B), _I64(N), _I64(H), ctypes.c_double(eps), _p(out))
+    return out
+
+
+def gate_prefix(alpha, carry=None):
+    """U [B,H,N] = carry - cumsum(alpha) (Eq. 11), total [B,H] = sum alpha."""
+    alpha = _f64(alpha)
+    B, H, N = alpha.shape
+    U = np.empty((B, H, N))
+    total = np.empty((B, H))
+    c = None if carry is None else _f64(carry).reshape(B, H)
+    _load().oracle_gate_prefix(_p(alpha), _I64(B), _I64(N), _I64(H), _p(c), _p(U), _p(total))
+    return U, total
+
+
+def gate_prefix_hbeta(h, beta, eps: float = 1e-6, carry=None):
+    """Alg. 1 end to end: (h, beta) -> (U, total, alpha)."""
+    alpha = gate_alpha(h, beta, eps)
+    U, total = gate_prefix(alpha, carry)
+    return U, total, alpha
+
+
+def fwd(Q, K, V, U, w: int, scale: float | None = None):
+    """O [B,Nq,H,d], LSE [B,H,Nq] per Eq. 12 / Alg. 2.
+
+    Q [B,Nq,H,d]; K, V [B,Nkv,H,d]; U [B,H,Nkv]; queries are the last Nq keys.
+    """
+    Q, K, V, U = _f64(Q), _f64(K), _f64(V), _f64(U)
+    B, Nq, H, d = Q.shape
+    Nkv = K.shape[1]
+    scale = 1.0 / np.sqrt(d) if scale is None else scale
+    O = np.empty_like(Q)
+    LSE = np.empty((B, H, Nq))
+    _load().oracle_fwd(_I64(B), _I64(H), _I64(Nq), _I64(Nkv), _I64(d), _I64(w), ctypes.c_double(scale),
+                       _p(Q), _p(K), _p(V), _p(U), _p(O), _p(LSE))
+    return O, LSE
+
+
+def fwd_rows(Q, K, V, U, w: int, rows, scale: float | None = None):
+    """Eq. 12 evaluated only for the listed (b, h, t) rows -> (o [n,d], lse [n])."""
+    Q, K, V, U = _f64(Q), _f64(K), _f64(V), _f64(U)
+    B, Nq, H, d = Q.shape
+    Nkv = K.shape[1]
+    scale = 1.0 / np.sqrt(d) if scale is None else scale
+    r = np.ascontiguousarray(np.asarray(rows, dtype=np.int64).reshape(-1, 3))
+    n = r.shape[0]
+    o = np.empty((n, d))
+    lse = np.empty((n,))
+    _load().oracle_fwd_rows(_I64(B), _I64(H), _I64(Nq), _I64(Nkv), _I64(d), _I64(w), ctypes.c_double(scale),
+                            _p(Q), _p(K), _p(V), _p(U), _I64(n),
+                            r.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), _p(o), _p(lse))
+    return o, lse
+
+
+def attend_row(q, keys, vals, u, ut: float, scale: float | None = None):
+    """One query over an explicit key list (decode, reading C-16) -> (o [d], lse)."""
+    q, keys, vals, u = _f64(q), _f64(keys), _f64(vals), _f64(u)
+    d = q.shape[-1]
+    n = keys.shape[0]
+    scale = 1.0 / np.sqrt(d) if scale is None else scale
+    o = np.empty((d,))
+    lse = _load().oracle_attend_row(_I64(d), ctypes.c_double(scale), _p(q), _I64(n), _p(keys), _p(vals),
+                                    _p(u), ctypes.c_double(ut), _p(o))
+    return o, float(lse)
+
+
+def bwd(Q, K, V, U, dO, w: int, scale: float | None = None, dalpha_carry=None, want_dalpha: bool = True):
+    """Alg. E.2 densely -> dict(dQ, dK, dV, dU, dalpha)."""
+    Q, K, V, U, dO = _f64(Q), _f64(K), _f64(V), _f64(U), _f64(dO)
+    B, Nq, H, d = Q.shape
+    Nkv = K.shape[1]
+    scale = 1.0 / np.sqrt(d) if scale is None else scale
+    dQ = np.empty_like(Q)
+    dK = np.empty_like(K)
+    dV = np.empty_like(V)
+    dU = np.empty((B, H, Nkv))
+    dalpha = np.empty((B, H, Nkv)) if want_dalpha else None
+    c = None if dalpha_carry is None else _f64(dalpha_carry).reshape(B, H)
+    _load().oracle_bwd(_I64(B), _I64(H), _I64(Nq), _I64(Nkv), _I64(d), _I64(w), ctypes.c_double(scale),
+                       _p(Q), _p(K), _p(V), _p(U), _p(dO), _p(dQ), _p(dK), _p(dV), _p(dU), _p(dalpha), _p(c))
+    return {"dQ": dQ, "dK": dK, "dV": dV, "dU": dU, "dalpha": dalpha}
+
+
+def dalpha_scan(dU, carry=None) -> np.ndarray:
+    """dalpha = carry - reverse_cumsum(dU) over the last axis."""
+    dU = _f64(dU)
+    B, H, N = dU.shape
+    out = np.empty_like(dU)
+    c = None if carry is None else _f64(carry).reshape(B, H)
+    _load().oracle_dalpha(_p(dU), _I64(B), _I64(H), _I64(N), _p(c), _p(out))
+    return out
+
+
+def gate_chain(h, beta, dalpha, eps: float = 1e-6):
+    """(dh, dbeta) [B,N,H] from dalpha [B,H,N] (chain rule of Eq. 9)."""
+    h, beta, dalpha = _f64(h), _f64(beta), _f64(dalpha)
+    B, N, H = h.shape
+    dh = np.empty_like(h)
+    db = np.empty_like(h)
+    _load().oracle_gate_chain(_p(h), _p(beta), _p(dalpha), _I64(B), _I64(N), _I64(H), ctypes.c_double(eps),
+                              _p(dh), _p(db))
+    return dh, db
