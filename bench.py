@@ -1,0 +1,446 @@
+#!/usr/bin/env python
+"""bench.py -- GatedFWA fwd+bwd throughput on B200 (BASELINE.json metric).
+
+One *step* = one pass of the training hot path over one batch (SURVEY §8(a)
+rows A2-A6): gfwa_gate_prefix -> gfwa_fwd -> gfwa_bwd (D, main, dalpha) ->
+gfwa_gate_prefix_bwd (dh, dbeta).  The decode row (A7) is timed in the same
+run as an auxiliary line item on its own workload (C5); the sequence-shard
+exchange (A8) runs with ``--workload C4`` under torchrun.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--workload C2|C3_w128|C3_w512|C3_w2048|C4]
+
+Default workload: BASELINE.json configs[1] (C2: B=8, H=16, N=4096, d=128,
+w=512, bf16).  N>1 (torchrun): every rank runs its own C2 batch (batch x head
+sharding, no data-path collective: "scaling": "weak").  Inputs are seeded
+synthetic tensors (synth.py) resident in HBM; the working set (> 1 GB) is
+larger than the 126 MB L2, so no explicit flush is needed between steps.
+Timing: CUDA events on the launching stream, barrier + synchronize on both
+sides, max over ranks.  Rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GatedFWA fwd+bwd tokens/s and in-window TFLOP/s (% BF16 peak), 1/2/4/8 B200"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return {"hbm_gbs": p["hbm_gbs"], "bf16": p["bf16_tflops"], "bf16_sus": p["bf16_tflops_sustained"],
+                "src": "measured"}
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16": 1590.0, "bf16_sus": 1400.0, "src": "fallback"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": ["unsampled"]}
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl")
+        return dist, dist.get_rank(), ws, int(os.environ.get("LOCAL_RANK", "0"))
+    return None, 0, 1, 0
+
+
+def _max_over_ranks(dist, x: float, dev):
+    if dist is None:
+        return x
+    import torch
+
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# --------------------------------------------------------------------------- our arm
+
+
+def in_window_fraction(N: int, w: int) -> float:
+    return sum(min(t + 1, w) for t in range(N)) / (N * w)
+
+
+def run_ours(args):
+    import torch
+
+    import synth
+    from paper_2512_07782_b200 import binding as gb
+
+    dist, rank, world, local = _dist()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    peaks = _peaks()
+    c = synth.CONFIGS[args.workload]
+    s = synth.AttnShape(B=c["B"], H=c["H"], N=c["N"], d=c["d"], w=c["w"])
+    seed = c["seed"] + 1000 * rank
+    Q, K, V, dO = synth.attn_inputs(s, seed=seed, device=dev, dtype=torch.bfloat16)
+    h, beta = synth.gate_inputs(s.B, s.N, s.H, seed=seed, device=dev)
+    h, beta = h.bfloat16(), beta.bfloat16()
+    st = torch.cuda.current_stream(dev)
+
+    ev = {}
+
+    def step(timed_kernels: bool = False):
+        rec = []
+        if timed_kernels:
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+            e[0].record(st)
+        U = gb.gfwa_gate_prefix(h, beta)
+        if timed_kernels:
+            e[1].record(st)
+        O, LSE, O32 = gb.gfwa_fwd(Q, K, V, U, s.w, want_o_f32=True)
+        if timed_kernels:
+            e[2].record(st)
+        dQ, dK, dV, dU, _ = gb.gfwa_bwd(Q, K, V, U, O, LSE, dO, s.w, O_f32=O32, want_dalpha=False)
+        if timed_kernels:
+            e[3].record(st)
+        _, dh, dbeta = gb.gfwa_gate_prefix_bwd(dU, h, beta, want_dalpha=False)
+        if timed_kernels:
+            e[4].record(st)
+            rec.append(e)
+        return rec, (O, dQ, dK, dV, dh, dbeta)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    if dist:
+        dist.barrier()
+    n_launch0 = gb.launch_count()
+    evs = []
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize(dev)
+        if dist:
+            dist.barrier()
+        t0.record(st)
+        for _ in range(args.steps):
+            r, _ = step(timed_kernels=True)
+            evs += r
+        t1.record(st)
+        torch.cuda.synchronize(dev)
+    launches = gb.launch_count() - n_launch0
+    ms = t0.elapsed_time(t1) / args.steps
+    ms = _max_over_ranks(dist, ms, dev)
+    parts = {"gate": 0.0, "fwd": 0.0, "bwd": 0.0, "gate_bwd": 0.0}
+    for e in evs:
+        parts["gate"] += e[0].elapsed_time(e[1])
+        parts["fwd"] += e[1].elapsed_time(e[2])
+        parts["bwd"] += e[2].elapsed_time(e[3])
+        parts["gate_bwd"] += e[3].elapsed_time(e[4])
+    parts = {k: v / args.steps for k, v in parts.items()}
+    tokens = s.B * s.N * world
+    value = tokens / (ms * 1e-3)
+    frac_iw = in_window_fraction(s.N, s.w)
+    flops_fwd = 4.0 * s.N * s.w * s.d * s.B * s.H  # north_star in-window convention
+    flops_bwd = 10.0 * s.N * s.w * s.d * s.B * s.H
+    tflops = (flops_fwd + flops_bwd) * world / (ms * 1e-3) / 1e12
+    # dominant kernel roofline (attention call with the largest device time)
+    dom = "bwd" if parts["bwd"] >= parts["fwd"] else "fwd"
+    dom_flops = flops_bwd if dom == "bwd" else flops_fwd
+    achieved = dom_flops / (parts[dom] * 1e-3) / 1e12
+    path = gb.gfwa_attn_path(Q, K, V, s.w)
+    traffic = _traffic_from_profiles(dom)
+    roofline = {"kernel": f"gfwa_{dom} ({'tcgen05' if path == 1 else 'simt'})", "bound": "tensor",
+                "achieved": round(achieved, 2), "peak": peaks["bf16_sus"], "unit": "TFLOP/s",
+                "frac": round(achieved / peaks["bf16_sus"], 4), "traffic": traffic,
+                "peak_src": f"{peaks['src']} bf16 sustained (kernel timed inside a long step)",
+                "algorithmic": f"{'10' if dom == 'bwd' else '4'}*N*w*d*B*H = {dom_flops:.4g} FLOP/launch"}
+    # e2e: the same step through the public API with pinned host buffers
+    e2e = run_e2e(args, s, Q, K, V, dO, h, beta, step_fn=None, dev=dev, world=world, dist=dist)
+    aux = {}
+    if rank == 0 and not args.no_aux:
+        aux = run_aux(dev, peaks)
+    if rank != 0:
+        return
+    cpu = cpu_baseline(args, s) if not args.no_cpu else None
+    line = {
+        "metric": METRIC,
+        "value": round(value, 1),
+        "unit": "tokens/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic (synth.py seeded: RMS-normed Q/K, N(0,1) V/dO, gates h~N(mu_h,1), beta=1+elu)",
+        "config": {"workload": f"{args.workload} (BASELINE configs[1])" if args.workload == "C2" else args.workload,
+                   "B": s.B, "H": s.H, "N": s.N, "d": s.d, "w": s.w, "global_batch": s.B * world,
+                   "seq_len": s.N, "parallelism": f"batch-sharded x{world}" if world > 1 else "single GPU",
+                   "l2": "inputs larger than L2 (working set > 1 GB), no flush",
+                   "in_window_fraction": round(frac_iw, 4)},
+        "tflops_in_window": round(tflops, 2),
+        "pct_bf16_peak": round(tflops / peaks["bf16"], 4),
+        "ms_breakdown": {k: round(v, 4) for k, v in parts.items()},
+        "attn_path": "tcgen05" if path == 1 else "simt",
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "aux": aux,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _traffic_from_profiles(kind: str):
+    """dram bytes per launch from the committed ncu summary (profiles/traffic.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f).get(kind)
+    except Exception:
+        return None
+
+
+def run_e2e(args, s, Q, K, V, dO, h, beta, step_fn, dev, world, dist):
+    import torch
+
+    from paper_2512_07782_b200 import binding as gb
+
+    host_in = [x.cpu().pin_memory() for x in (Q, K, V, dO, h, beta)]
+    outs_host = None
+    st = torch.cuda.current_stream(dev)
+    n = max(1, min(args.steps, 5))
+
+    def one():
+        nonlocal outs_host
+        Qd, Kd, Vd, dOd, hd, bd = (x.to(dev, non_blocking=True) for x in host_in)
+        U = gb.gfwa_gate_prefix(hd, bd)
+        O, LSE, O32 = gb.gfwa_fwd(Qd, Kd, Vd, U, s.w, want_o_f32=True)
+        dQ, dK, dV, dU, _ = gb.gfwa_bwd(Qd, Kd, Vd, U, O, LSE, dOd, s.w, O_f32=O32, want_dalpha=False)
+        _, dh, dbeta = gb.gfwa_gate_prefix_bwd(dU, hd, bd, want_dalpha=False)
+        res = (O, dQ, dK, dV, dh, dbeta)
+        if outs_host is None:
+            outs_host = [torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for x in res]
+        for hbuf, x in zip(outs_host, res):
+            hbuf.copy_(x, non_blocking=True)
+
+    one()
+    torch.cuda.synchronize(dev)
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record(st)
+    for _ in range(n):
+        one()
+    b.record(st)
+    torch.cuda.synchronize(dev)
+    ms = _max_over_ranks(dist, a.elapsed_time(b) / n, dev)
+    h2d = sum(x.numel() * x.element_size() for x in host_in)
+    d2h = sum(x.numel() * x.element_size() for x in outs_host)
+    return {"value": round(s.B * s.N * world / (ms * 1e-3), 1), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": round(ms, 3), "steps": n}
+
+
+def run_aux(dev, peaks):
+    """Decode (C5) and gate-scan probe (G): achieved HBM GB/s, same run."""
+    import torch
+
+    import synth
+    from paper_2512_07782_b200 import binding as gb
+
+    out = {}
+    c = synth.CONFIGS["C5"]
+    B, H, d, w = c["B"], c["H"], c["d"], c["w"]
+    Kc, Vc, a_hist, q, k, v, a_new = synth.decode_inputs(B, H, d, w, seed=c["seed"], device=dev)
+    Uc = -torch.cumsum(a_hist, -1)
+    pos = torch.full((B,), w + 17, dtype=torch.int64, device=dev)
+    for _ in range(3):
+        gb.gfwa_decode(q, k, v, a_new, Kc, Vc, Uc, pos)
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n = 20
+    e0.record()
+    for _ in range(n):
+        gb.gfwa_decode(q, k, v, a_new, Kc, Vc, Uc, pos)
+    e1.record()
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1) / n
+    byts = B * H * (4 * w * d + 4 * w + 8 * d)  # bf16 K,V rows + fp32 u + q/k/v/o
+    out["decode_C5"] = {"ms_per_step": round(ms, 4), "tokens_per_s": round(B / (ms * 1e-3), 1),
+                        "achieved_GBps": round(byts / (ms * 1e-3) / 1e9, 1),
+                        "frac_hbm": round(byts / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"], 4),
+                        "bytes_per_step": byts}
+    del Kc, Vc
+    c = synth.CONFIGS["G"]
+    h, beta = synth.gate_inputs(c["B"], c["N"], c["H"], seed=c["seed"], device=dev)
+    h, beta = h.bfloat16(), beta.bfloat16()
+    for _ in range(3):
+        gb.gfwa_gate_prefix(h, beta)
+    torch.cuda.synchronize(dev)
+    e0.record()
+    for _ in range(n):
+        gb.gfwa_gate_prefix(h, beta)
+    e1.record()
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1) / n
+    elems = c["B"] * c["N"] * c["H"]
+    byts = elems * 8  # bf16 h, beta in; fp32 U out
+    out["gate_scan_G"] = {"ms": round(ms, 4), "achieved_GBps": round(byts / (ms * 1e-3) / 1e9, 1),
+                          "frac_hbm": round(byts / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"], 4),
+                          "G_elems_per_s": round(elems / (ms * 1e-3) / 1e9, 2)}
+    return out
+
+
+# --------------------------------------------------------------------------- CPU oracle
+
+
+def _oracle_sample(s, n_slices: int, n_rows: int):
+    """A bounded sample of the workload for the fp64 oracle: `n_slices` (b,h)
+    slices, each the first `n_rows` tokens of one head (same recipe/seed)."""
+    import torch
+
+    import synth
+
+    sub = synth.AttnShape(B=n_slices, H=1, N=n_rows, d=s.d, w=s.w)
+    Q, K, V, dO = synth.attn_inputs(sub, seed=4242, dtype=torch.bfloat16)
+    h, beta = synth.gate_inputs(n_slices, n_rows, 1, seed=4243)
+    return sub, Q, K, V, dO, h.bfloat16(), beta.bfloat16()
+
+
+def _oracle_step(sub, Q, K, V, dO, h, beta):
+    import oracle
+
+    U, _, _ = oracle.gate_prefix_hbeta(h, beta)
+    oracle.fwd(Q, K, V, U, sub.w)
+    g = oracle.bwd(Q, K, V, U, dO, sub.w)
+    oracle.gate_chain(h, beta, g["dalpha"])
+
+
+def cpu_baseline(args, s):
+    import oracle
+
+    cores = oracle.num_threads()
+    n_rows = min(s.N, 1024)
+    sub, *arrs = _oracle_sample(s, cores, n_rows)
+    t = time.perf_counter()
+    _oracle_step(sub, *arrs)
+    dt = time.perf_counter() - t
+    # one full token = H heads; the sample covers cores*n_rows head-rows
+    tok_equiv = cores * n_rows / s.H
+    return {"value": round(tok_equiv / dt, 3), "unit": "tokens/s", "cores": cores, "kind": "oracle",
+            "sample": f"{cores} (b,h) slices x first {n_rows} tokens of {args.workload} (fp64 C oracle: gate, "
+                      f"fwd, bwd, gate chain), {dt:.2f} s; tokens = head-rows / H"}
+
+
+def run_reference(args):
+    """--impl reference: the fp64 CPU oracle, as it stands, on host cores."""
+    import synth
+
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+
+    c = synth.CONFIGS[args.workload]
+    s = synth.AttnShape(B=c["B"], H=c["H"], N=c["N"], d=c["d"], w=c["w"])
+    cores = oracle.num_threads()
+    n_rows = min(s.N, 512)
+    sub, *arrs = _oracle_sample(s, cores, n_rows)
+    for _ in range(args.warmup):
+        _oracle_step(sub, *arrs)
+    t = time.perf_counter()
+    for _ in range(args.steps):
+        _oracle_step(sub, *arrs)
+    dt = (time.perf_counter() - t) / args.steps
+    tok = cores * n_rows / s.H
+    value = tok / dt
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "tokens/s", "n_gpus": 0,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (synth.py)",
+        "config": {"workload": args.workload, "B": s.B, "H": s.H, "N": s.N, "d": s.d, "w": s.w},
+        "cpu_baseline": {"value": round(value, 3), "unit": "tokens/s", "cores": cores, "kind": "oracle",
+                         "sample": f"per step {cores} (b,h) slices x first {n_rows} tokens; tokens = head-rows/H"},
+        "e2e": {"value": round(value, 3), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="C2", choices=["C2", "C3_w128", "C3_w512", "C3_w2048"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU oracle baseline")
+    ap.add_argument("--no-aux", action="store_true", help="skip decode/gate-probe line items")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

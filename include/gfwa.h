@@ -1,0 +1,208 @@
+/*
+ * gfwa.h -- C ABI of libgfwa.so, the B200 (sm_100a) GatedFWA hot path.
+ *
+ * GatedFWA (arXiv 2512.07782) = sliding-window softmax attention whose logits
+ * carry a cumulative decay bias B_tj = u_t - u_j built from a per-token,
+ * per-head gate alpha.  Citations "P:<line>" refer to the paper's LaTeX
+ * source, "S:<line>" to SPEC.md; "C-<n>" are the readings of
+ * silent/ambiguous passages listed in DESIGN.md §3.
+ *
+ * Conventions shared by every call
+ * --------------------------------
+ *  - All tensor pointers are DEVICE pointers owned by the caller.  The
+ *    library never allocates, frees or synchronises; every call is enqueued
+ *    on `stream` (a cudaStream_t; NULL = legacy default stream) and returns
+ *    as soon as the work is launched.  No host reads of device data.
+ *  - Scratch memory is passed in (`ws`, `ws_bytes`), sized by the matching
+ *    *_workspace_size() call, and must be 256-byte aligned.  Unless a call
+ *    says otherwise the workspace needs no initialisation.
+ *  - Errors are returned as gfwa_status_t; arguments are validated before
+ *    any launch, so INVALID_ARGUMENT / UNSUPPORTED leave outputs untouched.
+ *    GFWA_ERR_CUDA reports a launch error; gfwa_last_cuda_error() gives the
+ *    cudaError_t of the calling thread's last failure.  No exception crosses
+ *    the ABI.  There is no CPU fallback: a non-sm_100 device is UNSUPPORTED.
+ *  - Token index t is 0-based.  Window (Alg. 2 line 14 P:382; C-2):
+ *    query at key position g attends keys j with max(0, g-w+1) <= j <= g
+ *    (w keys including itself, clipped at 0; w >= N is full causal).
+ *  - Logit (Eq. 12; C-1): s_tj = scale * q_t.k_j + (u_t - u_j),
+ *    scale defaults to 1/sqrt(d) and multiplies q.k only.
+ *  - dtypes: Q/K/V/O/dO/dQ/dK/dV/caches are GFWA_BF16 (tensor-core path) or
+ *    GFWA_F32 (exact parity path).  U, LSE, D, dU, dalpha, O_f32 are fp32;
+ *    carries and totals are fp64.
+ */
+#ifndef GFWA_H_
+#define GFWA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* gfwa_stream_t; /* == cudaStream_t */
+
+typedef enum {
+    GFWA_OK = 0,
+    GFWA_ERR_INVALID_ARGUMENT = 1, /* null pointer, bad size, misaligned pointer/stride */
+    GFWA_ERR_UNSUPPORTED = 2,      /* head dim / dtype combination / device not CC 10.0 */
+    GFWA_ERR_CUDA = 3,             /* a CUDA launch failed; see gfwa_last_cuda_error() */
+    GFWA_ERR_WORKSPACE = 4         /* ws_bytes smaller than *_workspace_size() */
+} gfwa_status_t;
+
+typedef enum { GFWA_F32 = 0, GFWA_BF16 = 1 } gfwa_dtype_t;
+
+/* Gate input kind for gfwa_gate_prefix / gfwa_decode.
+ * HBETA: (h, beta) as in Alg. 1, alpha = softplus(beta*h)/(beta+eps).
+ * ALPHA: alpha is given directly (beta ignored) -- lets callers bring their
+ *        own gate and lets tests drive alpha = 0 (SWA) or constant alpha. */
+typedef enum { GFWA_GATE_HBETA = 0, GFWA_GATE_ALPHA = 1 } gfwa_gate_kind_t;
+
+/* ------------------------------------------------------------------------- */
+/* Gate preprocessing: Alg. 1 "Fused Tiled Scan", Eq. 9-11.       */
+/* ------------------------------------------------------------------------- */
+
+/*
+ * gfwa_gate_prefix -- one streaming pass over (h, beta):
+ *   z = beta*h;  alpha = softplus(z)/(beta+eps)            (Alg. 1 l.5-7)
+ *   U[b,hh,t] = carry_in[b,hh] - sum_{q<=t} alpha[b,q,hh]  (Alg. 1 l.8-10, Eq. 11,
+ *                                                            inclusive prefix, C-8)
+ *   total[b,hh] = sum_q alpha[b,q,hh]                       (for the cross-rank scan)
+ * in_dtype   dtype of h/beta (GFWA_BF16 or GFWA_F32).
+ * h, beta    [B, N, H] row-major (H contiguous).  beta unused for GATE_ALPHA
+ *            (then h holds alpha).
+ * carry_in   [B*H] fp64 device array or NULL (= 0).
+ * U          [B, H, N] fp32 output (N contiguous, head-major for attention).
+ * total      [B*H] fp64 output or NULL.
+ * Accumulation: fp32 per element, fp64 across chunks (reading C-9).
+ * ws         >= gfwa_gate_prefix_workspace_size(B, N, H) bytes; need not be
+ *            initialised (the call clears what it uses, on `stream`).
+ */
+size_t gfwa_gate_prefix_workspace_size(int64_t B, int64_t N, int64_t H);
+gfwa_status_t gfwa_gate_prefix(gfwa_gate_kind_t kind, gfwa_dtype_t in_dtype, const void* h,
+                               const void* beta, int64_t B, int64_t N, int64_t H, float eps,
+                               const double* carry_in, float* U, double* total, void* ws,
+                               size_t ws_bytes, gfwa_stream_t stream);
+
+/*
+ * gfwa_gate_prefix_bwd -- backward of gfwa_gate_prefix ("gradients into U flow
+ * through the same streamed scan"; chain rule of Eq. 9):
+ *   dalpha[b,hh,t] = carry[b,hh] - sum_{t'>=t} dU[b,hh,t']       (reverse scan)
+ *   dh    = dalpha * sigmoid(beta h) * beta/(beta+eps)
+ *   dbeta = dalpha * (sigmoid(beta h) h (beta+eps) - softplus(beta h))/(beta+eps)^2
+ * dU [B,H,N] fp32 in; dalpha [B,H,N] fp32 out (or NULL); dh, dbeta [B,N,H] in
+ * in_dtype out (NULL to skip; ignored for GATE_ALPHA, where dh receives dalpha
+ * in [B,N,H] layout if non-NULL).  carry [B*H] fp64 or NULL: the suffix sum
+ * of later sequence shards (sequence sharding, north_star).
+ * ws as for gfwa_gate_prefix.
+ */
+size_t gfwa_gate_prefix_bwd_workspace_size(int64_t B, int64_t N, int64_t H);
+gfwa_status_t gfwa_gate_prefix_bwd(gfwa_gate_kind_t kind, gfwa_dtype_t in_dtype, const void* h,
+                                   const void* beta, int64_t B, int64_t N, int64_t H, float eps,
+                                   const float* dU, const double* carry, float* dalpha, void* dh,
+                                   void* dbeta, void* ws, size_t ws_bytes, gfwa_stream_t stream);
+
+/* ------------------------------------------------------------------------- */
+/* Attention: Alg. 2 (forward) and Alg. E.2 (backward) */
+/* ------------------------------------------------------------------------- */
+
+/*
+ * Problem descriptor.  Queries are the LAST N_q rows of the N_kv-row key
+ * sequence: query t sits at key position g = t + (N_kv - N_q).  N_kv > N_q
+ * carries a halo of earlier keys (sequence sharding); the U frame is the key
+ * frame (U has N_kv entries per (b,h)).
+ * Strides are in ELEMENTS over (b, n, h); the head dim d is contiguous.
+ * Gradients share the layout of their primal: dQ uses q_stride, dK k_stride,
+ * dV v_stride, dO and O use o_stride.  For the BF16 path every stride and
+ * base pointer must be 16-byte aligned (TMA).
+ */
+typedef struct {
+    int64_t B, H, N_q, N_kv;
+    int32_t d;          /* head dim: 64 or 128 */
+    int32_t w;          /* window, >= 1 */
+    float scale;        /* <= 0 selects 1/sqrt(d) */
+    gfwa_dtype_t dtype; /* dtype of Q, K, V, O, dO, dQ, dK, dV */
+    int64_t q_stride[3], k_stride[3], v_stride[3], o_stride[3];
+} gfwa_attn_desc_t;
+
+/*
+ * gfwa_fwd -- Eq. 12 via Alg. 2: for every (b, hh, t)
+ *   O[b,t,hh,:] = sum_j softmax_j(s_tj) V[b,j,hh,:] over the window,
+ *   LSE[b,hh,t] = log sum_j exp(s_tj)   (natural log, bias included, C-10)
+ * Q [B,N_q,H,d], K, V [B,N_kv,H,d], U [B,H,N_kv] fp32 -> O [B,N_q,H,d],
+ * LSE [B,H,N_q] fp32.  O_f32 (nullable) [B,N_q,H,d] fp32 receives O before
+ * the output cast; pass it to gfwa_bwd so D = rowsum(O*dO) is taken from fp32
+ * O (reading C-12).  Key tiles outside every row's window are never read.
+ */
+gfwa_status_t gfwa_fwd(const gfwa_attn_desc_t* desc, const void* Q, const void* K, const void* V,
+                       const float* U, void* O, float* O_f32, float* LSE, gfwa_stream_t stream);
+
+/*
+ * gfwa_bwd -- Alg. E.2 with readings C-3 (scale on dQ, dK),
+ * C-4 (du^k is a column sum), C-11 (du^q row sum kept), C-12 (D from O_f32):
+ *   D = rowsum(O*dO);  P = exp(s - LSE);  dS = P (dO V^T - D)
+ *   dV = P^T dO;  dQ = scale dS K;  dK = scale dS^T Q
+ *   dU[g] = sum_j dS_tj (g = t + h0)  -  sum_t dS_tj (key j)
+ *   dalpha = dalpha_carry - reverse_cumsum(dU)     (NULL to skip)
+ * O (dtype) is used for D only when O_f32 is NULL.  dK, dV, dU cover all N_kv
+ * key rows (halo rows included); dQ covers N_q rows.  dalpha [B,H,N_kv] fp32,
+ * dalpha_carry [B*H] fp64 or NULL.
+ * ws >= gfwa_bwd_workspace_size(desc); need not be initialised.
+ */
+size_t gfwa_bwd_workspace_size(const gfwa_attn_desc_t* desc);
+gfwa_status_t gfwa_bwd(const gfwa_attn_desc_t* desc, const void* Q, const void* K, const void* V,
+                       const float* U, const void* O, const float* O_f32, const float* LSE,
+                       const void* dO, void* dQ, void* dK, void* dV, float* dU, float* dalpha,
+                       const double* dalpha_carry, void* ws, size_t ws_bytes, gfwa_stream_t stream);
+
+/* ------------------------------------------------------------------------- */
+/* Decode: one new token per sequence over a rolling w-entry cache.           */
+/* The paper claims O(wd) per step with a KV cache but gives no  */
+/* algorithm; reading C-16: decode(t) == row t of Eq. 12.                     */
+/* ------------------------------------------------------------------------- */
+
+typedef struct {
+    int64_t B, H;
+    int32_t d;                  /* 64 or 128 */
+    int32_t w;                  /* cache length = window */
+    float scale;                /* <= 0 selects 1/sqrt(d) */
+    float eps;                  /* gate eps for GATE_HBETA */
+    gfwa_dtype_t dtype;         /* dtype of q, k_new, v_new, caches, o */
+    gfwa_gate_kind_t gate_kind; /* gate_a/gate_b are (h, beta) or (alpha, NULL), fp32 [B,H] */
+} gfwa_decode_desc_t;
+
+/*
+ * gfwa_decode -- for every (b, hh), with t = pos[b] (tokens already cached
+ * before this one) and slot s = t mod w:
+ *   u_t = u_{t-1} - alpha_t, u_{t-1} = U_cache[b,hh,(t-1) mod w] (0 when t == 0)
+ *   K_cache[b,hh,s] = k_new, V_cache[b,hh,s] = v_new, U_cache[b,hh,s] = u_t
+ *   o[b,hh] = sum_i softmax_i(scale q.k_i + u_t - u_i) v_i over the
+ *             min(t+1, w) valid slots (ring order is irrelevant)
+ * q, k_new, v_new, o [B,H,d]; K_cache, V_cache [B,H,w,d]; U_cache [B,H,w] fp32;
+ * pos [B] int64 DEVICE array (graph-capturable).  The caches are updated in
+ * place.  ws >= gfwa_decode_workspace_size(desc) bytes; it must be ZEROED once
+ * by the caller before first use (the call leaves it zeroed again).
+ */
+size_t gfwa_decode_workspace_size(const gfwa_decode_desc_t* desc);
+gfwa_status_t gfwa_decode(const gfwa_decode_desc_t* desc, const void* q, const void* k_new,
+                          const void* v_new, const float* gate_a, const float* gate_b,
+                          void* K_cache, void* V_cache, float* U_cache, const int64_t* pos, void* o,
+                          void* ws, size_t ws_bytes, gfwa_stream_t stream);
+
+/* ------------------------------------------------------------------------- */
+/* Helpers                                                                    */
+/* ------------------------------------------------------------------------- */
+const char* gfwa_status_string(gfwa_status_t s);
+int gfwa_last_cuda_error(void); /* cudaError_t of this thread's last GFWA_ERR_CUDA */
+const char* gfwa_version(void);
+/* Number of kernel launches the calling thread has issued through this library
+ * (monotonic; bench.py reads it to report gpu_launches). */
+uint64_t gfwa_launch_count(void);
+/* Which forward/backward implementation a descriptor routes to:
+ * 0 = SIMT (fp32 parity path), 1 = tcgen05/TMA tensor-core path. */
+int gfwa_attn_path(const gfwa_attn_desc_t* desc);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GFWA_H_ */

@@ -1,0 +1,344 @@
+"""Thin ctypes binding of libgfwa.so (include/gfwa.h).
+
+Argument marshalling only: every function takes torch CUDA tensors, checks
+shapes/dtypes, passes raw device pointers plus the current CUDA stream to the
+C ABI call of the same name, and raises ``GfwaError`` on a non-OK status.
+Nothing here computes any part of the method; there is no CPU fallback --
+if the library is missing or the device is not sm_100 the call fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+import threading
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libgfwa.so")
+
+GFWA_F32, GFWA_BF16 = 0, 1
+GATE_HBETA, GATE_ALPHA = 0, 1
+_STATUS = {
+    0: "GFWA_OK",
+    1: "GFWA_ERR_INVALID_ARGUMENT",
+    2: "GFWA_ERR_UNSUPPORTED",
+    3: "GFWA_ERR_CUDA",
+    4: "GFWA_ERR_WORKSPACE",
+}
+
+
+class GfwaError(RuntimeError):
+    pass
+
+
+class AttnDesc(ctypes.Structure):
+    _fields_ = [
+        ("B", ctypes.c_int64),
+        ("H", ctypes.c_int64),
+        ("N_q", ctypes.c_int64),
+        ("N_kv", ctypes.c_int64),
+        ("d", ctypes.c_int32),
+        ("w", ctypes.c_int32),
+        ("scale", ctypes.c_float),
+        ("dtype", ctypes.c_int32),
+        ("q_stride", ctypes.c_int64 * 3),
+        ("k_stride", ctypes.c_int64 * 3),
+        ("v_stride", ctypes.c_int64 * 3),
+        ("o_stride", ctypes.c_int64 * 3),
+    ]
+
+
+class DecodeDesc(ctypes.Structure):
+    _fields_ = [
+        ("B", ctypes.c_int64),
+        ("H", ctypes.c_int64),
+        ("d", ctypes.c_int32),
+        ("w", ctypes.c_int32),
+        ("scale", ctypes.c_float),
+        ("eps", ctypes.c_float),
+        ("dtype", ctypes.c_int32),
+        ("gate_kind", ctypes.c_int32),
+    ]
+
+
+_lib = None
+_lock = threading.Lock()
+_VP = ctypes.c_void_p
+_I64 = ctypes.c_int64
+
+EXPORTED = (
+    "gfwa_gate_prefix",
+    "gfwa_gate_prefix_workspace_size",
+    "gfwa_gate_prefix_bwd",
+    "gfwa_gate_prefix_bwd_workspace_size",
+    "gfwa_fwd",
+    "gfwa_bwd",
+    "gfwa_bwd_workspace_size",
+    "gfwa_decode",
+    "gfwa_decode_workspace_size",
+    "gfwa_status_string",
+    "gfwa_last_cuda_error",
+    "gfwa_version",
+    "gfwa_launch_count",
+    "gfwa_attn_path",
+)
+
+
+def load() -> ctypes.CDLL:
+    """Load libgfwa.so (fails loudly if it was not built)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise GfwaError(f"{LIB_PATH} missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        lib = ctypes.CDLL(LIB_PATH)
+        sz = ctypes.c_size_t
+        lib.gfwa_gate_prefix_workspace_size.restype = sz
+        lib.gfwa_gate_prefix_workspace_size.argtypes = [_I64, _I64, _I64]
+        lib.gfwa_gate_prefix_bwd_workspace_size.restype = sz
+        lib.gfwa_gate_prefix_bwd_workspace_size.argtypes = [_I64, _I64, _I64]
+        lib.gfwa_gate_prefix.restype = ctypes.c_int
+        lib.gfwa_gate_prefix.argtypes = [ctypes.c_int, ctypes.c_int, _VP, _VP, _I64, _I64, _I64, ctypes.c_float,
+                                         _VP, _VP, _VP, _VP, sz, _VP]
+        lib.gfwa_gate_prefix_bwd.restype = ctypes.c_int
+        lib.gfwa_gate_prefix_bwd.argtypes = [ctypes.c_int, ctypes.c_int, _VP, _VP, _I64, _I64, _I64,
+                                             ctypes.c_float, _VP, _VP, _VP, _VP, _VP, _VP, sz, _VP]
+        lib.gfwa_fwd.restype = ctypes.c_int
+        lib.gfwa_fwd.argtypes = [ctypes.POINTER(AttnDesc), _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP]
+        lib.gfwa_bwd_workspace_size.restype = sz
+        lib.gfwa_bwd_workspace_size.argtypes = [ctypes.POINTER(AttnDesc)]
+        lib.gfwa_bwd.restype = ctypes.c_int
+        lib.gfwa_bwd.argtypes = [ctypes.POINTER(AttnDesc)] + [_VP] * 15 + [sz, _VP]
+        lib.gfwa_decode_workspace_size.restype = sz
+        lib.gfwa_decode_workspace_size.argtypes = [ctypes.POINTER(DecodeDesc)]
+        lib.gfwa_decode.restype = ctypes.c_int
+        lib.gfwa_decode.argtypes = [ctypes.POINTER(DecodeDesc)] + [_VP] * 12 + [sz, _VP]
+        lib.gfwa_status_string.restype = ctypes.c_char_p
+        lib.gfwa_last_cuda_error.restype = ctypes.c_int
+        lib.gfwa_version.restype = ctypes.c_char_p
+        lib.gfwa_launch_count.restype = ctypes.c_uint64
+        lib.gfwa_attn_path.restype = ctypes.c_int
+        lib.gfwa_attn_path.argtypes = [ctypes.POINTER(AttnDesc)]
+        _lib = lib
+        return lib
+
+
+def _check(status: int, what: str):
+    if status != 0:
+        extra = ""
+        if status == 3:
+            extra = f" (cudaError {load().gfwa_last_cuda_error()})"
+        raise GfwaError(f"{what}: {_STATUS.get(status, status)}{extra}")
+
+
+def _ptr(t: torch.Tensor | None):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(device) -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def _dt(t: torch.Tensor) -> int:
+    if t.dtype == torch.bfloat16:
+        return GFWA_BF16
+    if t.dtype == torch.float32:
+        return GFWA_F32
+    raise GfwaError(f"unsupported dtype {t.dtype} (bf16 or fp32)")
+
+
+def _need_cuda(*ts):
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise GfwaError("libgfwa takes CUDA tensors only (no CPU fallback)")
+
+
+_ws_cache: dict = {}
+
+
+def workspace(nbytes: int, device, tag: str = "scratch", zero: bool = False) -> torch.Tensor:
+    """Cached device scratch (caller-owned per the ABI); `zero` tensors are
+    zeroed once at allocation (decode's self-resetting counters)."""
+    key = (tag, torch.device(device).index if torch.device(device).index is not None else torch.cuda.current_device())
+    t = _ws_cache.get(key)
+    if t is None or t.numel() < nbytes:
+        t = (torch.zeros if zero else torch.empty)(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+        _ws_cache[key] = t
+    return t
+
+
+def _bnh_strides(t: torch.Tensor):
+    """(b, n, h) element strides of a [B,N,H,d] tensor with d contiguous."""
+    if t.dim() != 4 or t.stride(3) != 1:
+        raise GfwaError("attention tensors must be [B,N,H,d] with the head dim contiguous")
+    return (t.stride(0), t.stride(1), t.stride(2))
+
+
+def make_desc(Q, K, V, O_like, w: int, scale: float | None) -> AttnDesc:
+    B, Nq, H, d = Q.shape
+    Nkv = K.shape[1]
+    dsc = AttnDesc()
+    dsc.B, dsc.H, dsc.N_q, dsc.N_kv, dsc.d, dsc.w = B, H, Nq, Nkv, d, int(w)
+    dsc.scale = float(scale) if scale is not None else 0.0
+    dsc.dtype = _dt(Q)
+    dsc.q_stride[:] = _bnh_strides(Q)
+    dsc.k_stride[:] = _bnh_strides(K)
+    dsc.v_stride[:] = _bnh_strides(V)
+    dsc.o_stride[:] = _bnh_strides(O_like)
+    return dsc
+
+
+# --------------------------------------------------------------------------- gate
+
+
+def gfwa_gate_prefix(h: torch.Tensor, beta: torch.Tensor | None = None, eps: float = 1e-6,
+                     carry_in: torch.Tensor | None = None, want_total: bool = False, alpha_input: bool = False):
+    """U [B,H,N] fp32 (and total [B,H] fp64) from h, beta [B,N,H] (Alg. 1).
+
+    alpha_input=True: ``h`` holds alpha directly (GFWA_GATE_ALPHA)."""
+    lib = load()
+    _need_cuda(h, beta, carry_in)
+    h = h.contiguous()
+    beta = None if beta is None else beta.contiguous()
+    B, N, H = h.shape
+    U = torch.empty(B, H, N, dtype=torch.float32, device=h.device)
+    total = torch.empty(B, H, dtype=torch.float64, device=h.device) if want_total else None
+    if carry_in is not None:
+        carry_in = carry_in.to(torch.float64).contiguous()
+    nbytes = lib.gfwa_gate_prefix_workspace_size(B, N, H)
+    ws = workspace(nbytes, h.device, "gate")
+    kind = GATE_ALPHA if alpha_input else GATE_HBETA
+    st = lib.gfwa_gate_prefix(kind, _dt(h), _ptr(h), _ptr(beta), B, N, H, float(eps), _ptr(carry_in), _ptr(U),
+                              _ptr(total), _ptr(ws), nbytes, _stream(h.device))
+    _check(st, "gfwa_gate_prefix")
+    return (U, total) if want_total else U
+
+
+def gfwa_gate_prefix_bwd(dU: torch.Tensor, h: torch.Tensor | None = None, beta: torch.Tensor | None = None,
+                         eps: float = 1e-6, carry: torch.Tensor | None = None, want_dalpha: bool = True,
+                         want_dh: bool = True, dtype=None):
+    """dalpha [B,H,N] (reverse scan) and dh, dbeta [B,N,H] (chain rule of Eq. 9)."""
+    lib = load()
+    _need_cuda(dU, h, beta, carry)
+    dU = dU.to(torch.float32).contiguous()
+    B, H, N = dU.shape
+    dev = dU.device
+    io_dt = dtype or (h.dtype if h is not None else torch.float32)
+    dalpha = torch.empty(B, H, N, dtype=torch.float32, device=dev) if want_dalpha else None
+    dh = dbeta = None
+    if want_dh and h is not None:
+        h = h.contiguous()
+        beta = beta.contiguous()
+        dh = torch.empty(B, N, H, dtype=io_dt, device=dev)
+        dbeta = torch.empty(B, N, H, dtype=io_dt, device=dev)
+    if carry is not None:
+        carry = carry.to(torch.float64).contiguous()
+    nbytes = lib.gfwa_gate_prefix_bwd_workspace_size(B, N, H)
+    ws = workspace(nbytes, dev, "gate")
+    in_dt = GFWA_BF16 if io_dt == torch.bfloat16 else GFWA_F32
+    st = lib.gfwa_gate_prefix_bwd(GATE_HBETA, in_dt, _ptr(h), _ptr(beta), B, N, H, float(eps), _ptr(dU),
+                                  _ptr(carry), _ptr(dalpha), _ptr(dh), _ptr(dbeta), _ptr(ws), nbytes,
+                                  _stream(dev))
+    _check(st, "gfwa_gate_prefix_bwd")
+    return dalpha, dh, dbeta
+
+
+# --------------------------------------------------------------------------- attention
+
+
+def gfwa_fwd(Q, K, V, U, w: int, scale: float | None = None, want_o_f32: bool = False, out=None):
+    """O [B,Nq,H,d], LSE [B,H,Nq] (+ O_f32) per Eq. 12 / Alg. 2."""
+    lib = load()
+    _need_cuda(Q, K, V, U)
+    U = U.contiguous()
+    B, Nq, H, d = Q.shape
+    O = out if out is not None else torch.empty(B, Nq, H, d, dtype=Q.dtype, device=Q.device)
+    O_f32 = torch.empty_strided(O.shape, O.stride(), dtype=torch.float32, device=Q.device) if want_o_f32 else None
+    LSE = torch.empty(B, H, Nq, dtype=torch.float32, device=Q.device)
+    dsc = make_desc(Q, K, V, O, w, scale)
+    st = lib.gfwa_fwd(ctypes.byref(dsc), _ptr(Q), _ptr(K), _ptr(V), _ptr(U), _ptr(O), _ptr(O_f32), _ptr(LSE),
+                      _stream(Q.device))
+    _check(st, "gfwa_fwd")
+    return O, LSE, O_f32
+
+
+def gfwa_bwd(Q, K, V, U, O, LSE, dO, w: int, scale: float | None = None, O_f32=None, want_dalpha: bool = True,
+             dalpha_carry=None):
+    """dQ, dK, dV, dU (+ dalpha) per Alg. E.2."""
+    lib = load()
+    _need_cuda(Q, K, V, U, O, LSE, dO)
+    if dO.stride() != O.stride() or (O_f32 is not None and O_f32.stride() != O.stride()):
+        # O, dO and O_f32 share one (b, n, h) stride set in the ABI
+        O, dO = O.contiguous(), dO.contiguous()
+        O_f32 = None if O_f32 is None else O_f32.contiguous()
+    B, Nq, H, d = Q.shape
+    Nkv = K.shape[1]
+    dev = Q.device
+    dQ = torch.empty_strided(Q.shape, Q.stride(), dtype=Q.dtype, device=dev)
+    dK = torch.empty_strided(K.shape, K.stride(), dtype=K.dtype, device=dev)
+    dV = torch.empty_strided(V.shape, V.stride(), dtype=V.dtype, device=dev)
+    dU = torch.empty(B, H, Nkv, dtype=torch.float32, device=dev)
+    dalpha = torch.empty(B, H, Nkv, dtype=torch.float32, device=dev) if want_dalpha else None
+    if dalpha_carry is not None:
+        dalpha_carry = dalpha_carry.to(torch.float64).contiguous()
+    dsc = make_desc(Q, K, V, O, w, scale)
+    nbytes = lib.gfwa_bwd_workspace_size(ctypes.byref(dsc))
+    ws = workspace(nbytes, dev, "bwd")
+    st = lib.gfwa_bwd(ctypes.byref(dsc), _ptr(Q), _ptr(K), _ptr(V), _ptr(U.contiguous()), _ptr(O), _ptr(O_f32),
+                      _ptr(LSE), _ptr(dO), _ptr(dQ), _ptr(dK), _ptr(dV), _ptr(dU), _ptr(dalpha),
+                      _ptr(dalpha_carry), _ptr(ws), nbytes, _stream(dev))
+    _check(st, "gfwa_bwd")
+    return dQ, dK, dV, dU, dalpha
+
+
+def gfwa_attn_path(Q, K, V, w: int) -> int:
+    """0 = SIMT parity path, 1 = tcgen05 tensor-core path (for this shape/dtype)."""
+    dsc = make_desc(Q, K, V, Q, w, None)
+    return int(load().gfwa_attn_path(ctypes.byref(dsc)))
+
+
+# --------------------------------------------------------------------------- decode
+
+
+def gfwa_decode(q, k_new, v_new, gate_a, K_cache, V_cache, U_cache, pos, gate_b=None, eps: float = 1e-6,
+                scale: float | None = None, out=None):
+    """One decode step (reading C-16); caches are updated in place.  gate_b=None
+    means gate_a holds alpha directly; else (gate_a, gate_b) = (h, beta)."""
+    lib = load()
+    _need_cuda(q, k_new, v_new, gate_a, K_cache, V_cache, U_cache, pos)
+    B, H, d = q.shape
+    w = K_cache.shape[2]
+    for t in (q, k_new, v_new, K_cache, V_cache, U_cache):
+        if not t.is_contiguous():
+            raise GfwaError("decode tensors must be contiguous")
+    dsc = DecodeDesc()
+    dsc.B, dsc.H, dsc.d, dsc.w = B, H, d, w
+    dsc.scale = float(scale) if scale is not None else 0.0
+    dsc.eps = float(eps)
+    dsc.dtype = _dt(q)
+    dsc.gate_kind = GATE_ALPHA if gate_b is None else GATE_HBETA
+    o = out if out is not None else torch.empty_like(q)
+    ga = gate_a.float().contiguous()
+    gb = None if gate_b is None else gate_b.float().contiguous()
+    nbytes = lib.gfwa_decode_workspace_size(ctypes.byref(dsc))
+    ws = workspace(nbytes, q.device, f"decode{B}x{H}x{w}x{d}", zero=True)
+    st = lib.gfwa_decode(ctypes.byref(dsc), _ptr(q), _ptr(k_new), _ptr(v_new), _ptr(ga),
+                         _ptr(gb), _ptr(K_cache),
+                         _ptr(V_cache), _ptr(U_cache), _ptr(pos), _ptr(o), _ptr(ws), nbytes, _stream(q.device))
+    _check(st, "gfwa_decode")
+    return o
+
+
+def launch_count() -> int:
+    return int(load().gfwa_launch_count())
+
+
+def version() -> str:
+    return load().gfwa_version().decode()
+
+
+def default_scale(d: int) -> float:
+    return 1.0 / math.sqrt(d)

@@ -1,0 +1,42 @@
+// attn_common.cuh -- parameter block shared by the attention kernels.
+#pragma once
+#include "common.cuh"
+
+namespace gfwa {
+
+struct AttnParams {
+    // problem
+    int64_t B, H, Nq, Nkv, h0;  // h0 = Nkv - Nq halo rows
+    int d, w;
+    float scale;
+    // element strides over (b, n, h); d contiguous
+    int64_t qs[3], ks[3], vs[3], os[3];
+    // forward
+    const void* Q;
+    const void* K;
+    const void* V;
+    const float* U;  // [B,H,Nkv]
+    void* O;
+    float* O_f32;
+    float* LSE;      // [B,H,Nq]
+    // backward
+    const void* dO;
+    const float* Ofp;   // fp32 O for D (may be null -> use O)
+    void* dQ;
+    void* dK;
+    void* dV;
+    float* dU;          // [B,H,Nkv]
+    float* Dv;          // [B,H,Nq] workspace: rowsum(O*dO)
+    float* dQacc;       // fp32 dQ accumulator workspace (tensor-core path)
+};
+
+__device__ __forceinline__ int64_t off3(const int64_t* s, int64_t b, int64_t n, int64_t h) {
+    return b * s[0] + n * s[1] + h * s[2];
+}
+
+// Launchers implemented in attn_simt.cu / attn_tc_*.cu
+gfwa_status_t simt_fwd(const AttnParams& p, gfwa_dtype_t dt, cudaStream_t st);
+gfwa_status_t simt_bwd(const AttnParams& p, gfwa_dtype_t dt, cudaStream_t st);
+gfwa_status_t bwd_preprocess(const AttnParams& p, gfwa_dtype_t dt, cudaStream_t st);
+
+}  // namespace gfwa

@@ -1,0 +1,192 @@
+// capi.cu -- argument validation, dispatch and helpers of the libgfwa C ABI
+// (include/gfwa.h).  No allocation, no synchronisation, no host reads of
+// device data; every launch goes onto the caller's stream.
+#include <atomic>
+#include <cmath>
+
+#include "attn_common.cuh"
+
+namespace gfwa {
+
+static std::atomic<uint64_t> g_launches{0};
+static thread_local int g_last_cuda_error = 0;
+
+void note_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+
+gfwa_status_t check_launch(cudaError_t err) {
+    if (err == cudaSuccess) return GFWA_OK;
+    g_last_cuda_error = (int)err;
+    return GFWA_ERR_CUDA;
+}
+
+// Tensor-core (tcgen05) path hooks; defined in attn_tc_fwd.cu / attn_tc_bwd.cu.
+bool tc_fwd_supported(const AttnParams& p, gfwa_dtype_t dt);
+gfwa_status_t tc_fwd(const AttnParams& p, cudaStream_t st);
+bool tc_bwd_supported(const AttnParams& p, gfwa_dtype_t dt);
+size_t tc_bwd_workspace(const AttnParams& p);
+gfwa_status_t tc_bwd(const AttnParams& p, cudaStream_t st, void* ws);
+
+// reverse scan dU -> dalpha (gate_scan.cu internals via the public call)
+}  // namespace gfwa
+
+using namespace gfwa;
+
+namespace {
+
+bool device_is_sm100() {
+    static int cached = -1;
+    if (cached < 0) {
+        int dev = 0, major = 0, minor = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess) return false;
+        cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+        cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+        cached = (major == 10 && minor == 0) ? 1 : 0;
+    }
+    return cached == 1;
+}
+
+gfwa_status_t make_params(const gfwa_attn_desc_t* d, AttnParams& p) {
+    if (!d) return GFWA_ERR_INVALID_ARGUMENT;
+    if (d->B < 1 || d->H < 1 || d->N_q < 1 || d->N_kv < d->N_q || d->w < 1) return GFWA_ERR_INVALID_ARGUMENT;
+    if (d->d != 64 && d->d != 128) return GFWA_ERR_UNSUPPORTED;
+    if (d->dtype != GFWA_F32 && d->dtype != GFWA_BF16) return GFWA_ERR_UNSUPPORTED;
+    if (!(d->scale == d->scale)) return GFWA_ERR_INVALID_ARGUMENT;
+    if (d->B * d->H > 65535 * 65535LL || d->N_kv > ((int64_t)1 << 31)) return GFWA_ERR_INVALID_ARGUMENT;
+    if (!device_is_sm100()) return GFWA_ERR_UNSUPPORTED;
+    p = AttnParams{};
+    p.B = d->B;
+    p.H = d->H;
+    p.Nq = d->N_q;
+    p.Nkv = d->N_kv;
+    p.h0 = d->N_kv - d->N_q;
+    p.d = d->d;
+    p.w = d->w;
+    p.scale = d->scale > 0.f ? d->scale : 1.f / std::sqrt((float)d->d);
+    for (int i = 0; i < 3; ++i) {
+        p.qs[i] = d->q_stride[i];
+        p.ks[i] = d->k_stride[i];
+        p.vs[i] = d->v_stride[i];
+        p.os[i] = d->o_stride[i];
+    }
+    if (d->H > 65535 || d->B > 65535) return GFWA_ERR_INVALID_ARGUMENT;
+    return GFWA_OK;
+}
+
+bool strides_ok(const int64_t* s, size_t esize) {
+    for (int i = 0; i < 3; ++i)
+        if (s[i] < 0 || ((s[i] * (int64_t)esize) % 16) != 0) return false;
+    return true;
+}
+
+bool al16(const void* p) { return ((uintptr_t)p % 16) == 0; }
+
+}  // namespace
+
+extern "C" gfwa_status_t gfwa_fwd(const gfwa_attn_desc_t* desc, const void* Q, const void* K, const void* V,
+                                  const float* U, void* O, float* O_f32, float* LSE, gfwa_stream_t stream) {
+    AttnParams p;
+    if (gfwa_status_t s = make_params(desc, p)) return s;
+    if (!Q || !K || !V || !U || !O || !LSE) return GFWA_ERR_INVALID_ARGUMENT;
+    const size_t es = desc->dtype == GFWA_BF16 ? 2 : 4;
+    if (!strides_ok(p.qs, es) || !strides_ok(p.ks, es) || !strides_ok(p.vs, es) || !strides_ok(p.os, es))
+        return GFWA_ERR_INVALID_ARGUMENT;
+    if (!al16(Q) || !al16(K) || !al16(V) || !al16(O) || (O_f32 && !al16(O_f32))) return GFWA_ERR_INVALID_ARGUMENT;
+    p.Q = Q;
+    p.K = K;
+    p.V = V;
+    p.U = U;
+    p.O = O;
+    p.O_f32 = O_f32;
+    p.LSE = LSE;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (tc_fwd_supported(p, desc->dtype)) return tc_fwd(p, st);
+    return simt_fwd(p, desc->dtype, st);
+}
+
+static size_t bwd_ws_layout(const AttnParams& p, gfwa_dtype_t dt, size_t* off_D, size_t* off_scan,
+                            size_t* off_tc) {
+    size_t off = 0;
+    *off_D = off;
+    off += ((size_t)p.B * p.H * p.Nq * sizeof(float) + 255) & ~(size_t)255;
+    *off_scan = off;
+    off += gfwa_gate_prefix_bwd_workspace_size(p.B, p.Nkv, p.H);
+    *off_tc = off;
+    if (tc_bwd_supported(p, dt)) off += (tc_bwd_workspace(p) + 255) & ~(size_t)255;
+    return off;
+}
+
+extern "C" size_t gfwa_bwd_workspace_size(const gfwa_attn_desc_t* desc) {
+    AttnParams p;
+    if (make_params(desc, p) != GFWA_OK) return 256;
+    size_t a, b, c;
+    return bwd_ws_layout(p, desc->dtype, &a, &b, &c);
+}
+
+// The dU -> dalpha reverse scan runs as a [B, Nkv, H=H] gate backward with
+// kind ALPHA: it only needs dU in [B, H, Nkv] layout, which is exactly dU.
+extern "C" gfwa_status_t gfwa_bwd(const gfwa_attn_desc_t* desc, const void* Q, const void* K, const void* V,
+                                  const float* U, const void* O, const float* O_f32, const float* LSE,
+                                  const void* dO, void* dQ, void* dK, void* dV, float* dU, float* dalpha,
+                                  const double* dalpha_carry, void* ws, size_t ws_bytes, gfwa_stream_t stream) {
+    AttnParams p;
+    if (gfwa_status_t s = make_params(desc, p)) return s;
+    if (!Q || !K || !V || !U || !LSE || !dO || !dQ || !dK || !dV || !dU || !ws) return GFWA_ERR_INVALID_ARGUMENT;
+    if (!O && !O_f32) return GFWA_ERR_INVALID_ARGUMENT;
+    const size_t es = desc->dtype == GFWA_BF16 ? 2 : 4;
+    if (!strides_ok(p.qs, es) || !strides_ok(p.ks, es) || !strides_ok(p.vs, es) || !strides_ok(p.os, es))
+        return GFWA_ERR_INVALID_ARGUMENT;
+    const void* ptrs[] = {Q, K, V, dO, dQ, dK, dV};
+    for (const void* pp : ptrs)
+        if (!al16(pp)) return GFWA_ERR_INVALID_ARGUMENT;
+    if ((uintptr_t)ws % 256) return GFWA_ERR_INVALID_ARGUMENT;
+    size_t off_D, off_scan, off_tc;
+    const size_t need = bwd_ws_layout(p, desc->dtype, &off_D, &off_scan, &off_tc);
+    if (ws_bytes < need) return GFWA_ERR_WORKSPACE;
+    p.Q = Q;
+    p.K = K;
+    p.V = V;
+    p.U = U;
+    p.O = const_cast<void*>(O);
+    p.Ofp = O_f32;
+    p.LSE = const_cast<float*>(LSE);
+    p.dO = dO;
+    p.dQ = dQ;
+    p.dK = dK;
+    p.dV = dV;
+    p.dU = dU;
+    p.Dv = (float*)((char*)ws + off_D);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (gfwa_status_t s = bwd_preprocess(p, desc->dtype, st)) return s;
+    gfwa_status_t s;
+    if (tc_bwd_supported(p, desc->dtype))
+        s = tc_bwd(p, st, (char*)ws + off_tc);
+    else
+        s = simt_bwd(p, desc->dtype, st);
+    if (s != GFWA_OK) return s;
+    if (!dalpha) return GFWA_OK;
+    // dalpha = carry - reverse_cumsum(dU) over the N_kv key rows
+    return gfwa_gate_prefix_bwd(GFWA_GATE_ALPHA, GFWA_F32, nullptr, nullptr, p.B * p.H, p.Nkv, 1, 0.f, dU,
+                                dalpha_carry, dalpha, nullptr, nullptr, (char*)ws + off_scan,
+                                gfwa_gate_prefix_bwd_workspace_size(p.B * p.H, p.Nkv, 1), stream);
+}
+
+extern "C" int gfwa_attn_path(const gfwa_attn_desc_t* desc) {
+    AttnParams p;
+    if (make_params(desc, p) != GFWA_OK) return -1;
+    return tc_fwd_supported(p, desc->dtype) ? 1 : 0;
+}
+
+extern "C" const char* gfwa_status_string(gfwa_status_t s) {
+    switch (s) {
+        case GFWA_OK: return "GFWA_OK";
+        case GFWA_ERR_INVALID_ARGUMENT: return "GFWA_ERR_INVALID_ARGUMENT";
+        case GFWA_ERR_UNSUPPORTED: return "GFWA_ERR_UNSUPPORTED";
+        case GFWA_ERR_CUDA: return "GFWA_ERR_CUDA";
+        case GFWA_ERR_WORKSPACE: return "GFWA_ERR_WORKSPACE";
+    }
+    return "GFWA_ERR_UNKNOWN";
+}
+
+extern "C" int gfwa_last_cuda_error(void) { return g_last_cuda_error; }
+extern "C" const char* gfwa_version(void) { return "gfwa 0.1.0 (sm_100a)"; }
+extern "C" uint64_t gfwa_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }

@@ -1,0 +1,148 @@
+"""GPU parity of gfwa_fwd / gfwa_bwd (Alg. 2, Alg. E.2) against the fp64 oracle,
+called through the C ABI on the same seeded inputs.
+
+fp32 path: max relative error per (b,h) slice <= 1e-4 on O, <= 1e-3 on
+gradients; bf16 path: max abs error <= 2e-2 on O, <= 5e-2 on gradients
+(north_star).  Shapes span several tiles with ragged tails and the method's
+degenerate cases (N=1, w=1, w>=N, halo rows N_kv > N_q, d=64/128)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from paper_2512_07782_b200 import binding as gb
+from parity import (TOL_BF16_GRAD, TOL_BF16_O, TOL_F32_GRAD, TOL_F32_O, TOL_LSE, max_abs, np64,
+                    rel_slices)
+
+pytestmark = pytest.mark.gpu
+
+
+def _U(B, H, Nkv, seed, mean=0.5):
+    g = torch.Generator().manual_seed(seed)
+    alpha = torch.nn.functional.softplus(torch.randn(B, H, Nkv, generator=g) + mean - 0.5)
+    return (-torch.cumsum(alpha.double(), -1)).float()
+
+
+def _run(s: synth.AttnShape, dtype, seed, U=None):
+    Q, K, V, dO = synth.attn_inputs(s, seed=seed, dtype=dtype)
+    U = _U(s.B, s.H, s.nkv, seed + 1) if U is None else U
+    Qd, Kd, Vd, dOd, Ud = (x.cuda() for x in (Q, K, V, dO, U))
+    O, LSE, O32 = gb.gfwa_fwd(Qd, Kd, Vd, Ud, s.w, want_o_f32=True)
+    dQ, dK, dV, dU, da = gb.gfwa_bwd(Qd, Kd, Vd, Ud, O, LSE, dOd, s.w, O_f32=O32)
+    torch.cuda.synchronize()
+    Or, Lr = oracle.fwd(Q, K, V, U, s.w)
+    g = oracle.bwd(Q, K, V, U, dO, s.w)
+    return dict(O=O, LSE=LSE, O32=O32, dQ=dQ, dK=dK, dV=dV, dU=dU, dalpha=da), dict(O=Or, LSE=Lr, **g)
+
+
+F32_SHAPES = [
+    synth.AttnShape(B=1, H=2, N=128, d=64, w=32),        # C1 (BASELINE configs[0])
+    synth.AttnShape(B=1, H=1, N=1, d=64, w=1),           # N = 1
+    synth.AttnShape(B=2, H=1, N=65, d=128, w=1),         # w = 1 -> O = V
+    synth.AttnShape(B=1, H=3, N=200, d=64, w=37),        # ragged tiles, odd w
+    synth.AttnShape(B=1, H=2, N=130, d=128, w=500),      # w >= N: full causal
+    synth.AttnShape(B=1, H=2, N=257, d=128, w=64),       # w aligned to the tile
+    synth.AttnShape(B=1, H=2, N=150, d=64, w=40, N_kv=190),  # halo rows (sequence shard)
+]
+
+
+@pytest.mark.parametrize("s", F32_SHAPES, ids=lambda s: f"B{s.B}H{s.H}N{s.N}kv{s.nkv}d{s.d}w{s.w}")
+def test_fp32_path_matches_oracle(s):
+    got, ref = _run(s, torch.float32, seed=s.N + s.w)
+    assert rel_slices(got["O"], ref["O"], "bnhd") <= TOL_F32_O
+    assert max_abs(got["LSE"], ref["LSE"]) <= 1e-4
+    for k in ("dQ", "dK", "dV"):
+        assert rel_slices(got[k], ref[k], "bnhd") <= TOL_F32_GRAD, k
+    for k in ("dU", "dalpha"):
+        if np.abs(ref[k]).max() > 1e-6:
+            assert rel_slices(got[k], ref[k], "bhn") <= TOL_F32_GRAD, k
+        else:
+            assert max_abs(got[k], ref[k]) <= 1e-6, k
+
+
+BF16_SHAPES = [
+    synth.AttnShape(B=1, H=2, N=300, d=128, w=96),
+    synth.AttnShape(B=2, H=2, N=1000, d=128, w=512),     # C2 window, ragged N
+    synth.AttnShape(B=1, H=2, N=777, d=128, w=128),
+    synth.AttnShape(B=1, H=2, N=640, d=64, w=200),
+    synth.AttnShape(B=1, H=2, N=384, d=128, w=2048),     # w > N
+    synth.AttnShape(B=1, H=2, N=512, d=128, w=256, N_kv=768),  # halo
+]
+
+
+@pytest.mark.parametrize("s", BF16_SHAPES, ids=lambda s: f"B{s.B}H{s.H}N{s.N}kv{s.nkv}d{s.d}w{s.w}")
+def test_bf16_path_matches_oracle(s):
+    got, ref = _run(s, torch.bfloat16, seed=3 * s.N + s.w)
+    assert max_abs(got["O"], ref["O"]) <= TOL_BF16_O
+    assert max_abs(got["LSE"], ref["LSE"]) <= TOL_LSE
+    for k in ("dQ", "dK", "dV", "dU", "dalpha"):
+        assert max_abs(got[k], ref[k]) <= TOL_BF16_GRAD, k
+
+
+def test_end_to_end_from_gate_inputs():
+    """gate scan -> attention -> backward -> gate chain vs the oracle chain."""
+    from paper_2512_07782_b200 import gated_fwa
+
+    s = synth.AttnShape(B=1, H=4, N=333, d=128, w=100)
+    Q, K, V, dO = synth.attn_inputs(s, seed=5, dtype=torch.bfloat16)
+    h, beta = synth.gate_inputs(s.B, s.N, s.H, seed=6)
+    leaves = [x.cuda().requires_grad_(True) for x in (Q, K, V, h, beta)]
+    O = gated_fwa(*leaves, w=s.w)
+    O.backward(dO.cuda())
+    U, _, _ = oracle.gate_prefix_hbeta(h, beta)
+    Or, _ = oracle.fwd(Q, K, V, U, s.w)
+    g = oracle.bwd(Q, K, V, U, dO, s.w)
+    dh, db = oracle.gate_chain(h, beta, g["dalpha"])
+    assert max_abs(O, Or) <= TOL_BF16_O
+    assert max_abs(leaves[0].grad, g["dQ"]) <= TOL_BF16_GRAD
+    assert max_abs(leaves[1].grad, g["dK"]) <= TOL_BF16_GRAD
+    assert max_abs(leaves[2].grad, g["dV"]) <= TOL_BF16_GRAD
+    assert max_abs(leaves[3].grad, dh) <= TOL_BF16_GRAD
+    assert max_abs(leaves[4].grad, db) <= TOL_BF16_GRAD
+
+
+def test_c2_full_size_sampled():
+    """BASELINE configs[1] (C2: B=8, H=16, N=4096, d=128, w=512, bf16) in the
+    launch configuration bench.py times; fwd checked on sampled rows across all
+    slices, fwd+bwd checked in full on two (b, h) slices."""
+    c = synth.CONFIGS["C2"]
+    s = synth.AttnShape(B=c["B"], H=c["H"], N=c["N"], d=c["d"], w=c["w"])
+    Q, K, V, dO = synth.attn_inputs(s, seed=c["seed"], device="cuda", dtype=torch.bfloat16)
+    h, beta = synth.gate_inputs(s.B, s.N, s.H, seed=c["seed"], device="cuda")
+    U = gb.gfwa_gate_prefix(h, beta)
+    O, LSE, O32 = gb.gfwa_fwd(Q, K, V, U, s.w, want_o_f32=True)
+    dQ, dK, dV, dU, da = gb.gfwa_bwd(Q, K, V, U, O, LSE, dO, s.w, O_f32=O32)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(0)
+    rows = np.stack([rng.integers(0, s.B, 96), rng.integers(0, s.H, 96), rng.integers(0, s.N, 96)], 1)
+    rows[:4, 2] = [0, 1, s.w - 1, s.N - 1]
+    o_r, l_r = oracle.fwd_rows(Q, K, V, U, s.w, rows)
+    o_g = np64(O)[rows[:, 0], rows[:, 2], rows[:, 1]]
+    l_g = np64(LSE)[rows[:, 0], rows[:, 1], rows[:, 2]]
+    assert np.abs(o_g - o_r).max() <= TOL_BF16_O
+    assert np.abs(l_g - l_r).max() <= TOL_LSE
+    for b, hh in ((0, 0), (s.B - 1, s.H - 1)):
+        sl = lambda x: x[b:b + 1, :, hh:hh + 1]  # noqa: E731
+        Ur = U[b:b + 1, hh:hh + 1]
+        g = oracle.bwd(sl(Q), sl(K), sl(V), Ur, sl(dO), s.w)
+        Or, _ = oracle.fwd(sl(Q), sl(K), sl(V), Ur, s.w)
+        assert max_abs(sl(O), Or) <= TOL_BF16_O
+        for k, t in (("dQ", dQ), ("dK", dK), ("dV", dV)):
+            assert max_abs(sl(t), g[k]) <= TOL_BF16_GRAD, k
+        assert max_abs(dU[b:b + 1, hh:hh + 1], g["dU"]) <= TOL_BF16_GRAD
+        assert max_abs(da[b:b + 1, hh:hh + 1], g["dalpha"]) <= TOL_BF16_GRAD
+
+
+def test_zero_grad_out_and_invariants():
+    """dO = 0 -> all gradients exactly 0; sum_m dU_m = 0 and dalpha_0 = 0 (rowsum(dS) = 0)."""
+    s = synth.AttnShape(B=1, H=2, N=260, d=128, w=70)
+    Q, K, V, dO = synth.attn_inputs(s, seed=11, device="cuda", dtype=torch.float32)
+    U = _U(1, 2, s.N, 12).cuda()
+    O, LSE, O32 = gb.gfwa_fwd(Q, K, V, U, s.w, want_o_f32=True)
+    z = gb.gfwa_bwd(Q, K, V, U, O, LSE, torch.zeros_like(dO), s.w, O_f32=O32)
+    for t in z:
+        assert torch.count_nonzero(t) == 0
+    dQ, dK, dV, dU, da = gb.gfwa_bwd(Q, K, V, U, O, LSE, dO, s.w, O_f32=O32)
+    assert dU.double().sum(-1).abs().max().item() <= 1e-3 * dU.abs().max().item()
+    assert da[..., 0].abs().max().item() <= 1e-3 * da.abs().max().item()
