@@ -29,7 +29,7 @@ class GatedFWAFunction(torch.autograd.Function):
         Q, K, V, h, beta, U, O, LSE, O_f32 = ctx.saved_tensors
         dQ, dK, dV, dU, _ = B.gfwa_bwd(Q, K, V, U, O, LSE, dO.contiguous(), ctx.w, ctx.scale, O_f32=O_f32,
                                        want_dalpha=False)
-        _, dh, dbeta = B.gfwa_gate_prefix_bwd(dU, h, beta, ctx.eps, want_dalpha=False, dtype=h.dtype)
+        _, dh, dbeta = B.gfwa_gate_prefix_bwd(dU, h, beta, ctx.eps, want_dalpha=False)
         return dQ, dK, dV, dh, dbeta, None, None, None
 
 

@@ -115,7 +115,7 @@ def load() -> ctypes.CDLL:
         lib.gfwa_decode_workspace_size.restype = sz
         lib.gfwa_decode_workspace_size.argtypes = [ctypes.POINTER(DecodeDesc)]
         lib.gfwa_decode.restype = ctypes.c_int
-        lib.gfwa_decode.argtypes = [ctypes.POINTER(DecodeDesc)] + [_VP] * 12 + [sz, _VP]
+        lib.gfwa_decode.argtypes = [ctypes.POINTER(DecodeDesc)] + [_VP] * 11 + [sz, _VP]
         lib.gfwa_status_string.restype = ctypes.c_char_p
         lib.gfwa_last_cuda_error.restype = ctypes.c_int
         lib.gfwa_version.restype = ctypes.c_char_p
@@ -202,7 +202,7 @@ def gfwa_gate_prefix(h: torch.Tensor, beta: torch.Tensor | None = None, eps: flo
     lib = load()
     _need_cuda(h, beta, carry_in)
     h = h.contiguous()
-    beta = None if beta is None else beta.contiguous()
+    beta = None if beta is None else beta.to(h.dtype).contiguous()  # one in_dtype for both
     B, N, H = h.shape
     U = torch.empty(B, H, N, dtype=torch.float32, device=h.device)
     total = torch.empty(B, H, dtype=torch.float64, device=h.device) if want_total else None
@@ -219,19 +219,19 @@ def gfwa_gate_prefix(h: torch.Tensor, beta: torch.Tensor | None = None, eps: flo
 
 def gfwa_gate_prefix_bwd(dU: torch.Tensor, h: torch.Tensor | None = None, beta: torch.Tensor | None = None,
                          eps: float = 1e-6, carry: torch.Tensor | None = None, want_dalpha: bool = True,
-                         want_dh: bool = True, dtype=None):
+                         want_dh: bool = True):
     """dalpha [B,H,N] (reverse scan) and dh, dbeta [B,N,H] (chain rule of Eq. 9)."""
     lib = load()
     _need_cuda(dU, h, beta, carry)
     dU = dU.to(torch.float32).contiguous()
     B, H, N = dU.shape
     dev = dU.device
-    io_dt = dtype or (h.dtype if h is not None else torch.float32)
+    io_dt = h.dtype if h is not None else torch.float32  # dh, dbeta in the dtype of h, beta
     dalpha = torch.empty(B, H, N, dtype=torch.float32, device=dev) if want_dalpha else None
     dh = dbeta = None
     if want_dh and h is not None:
         h = h.contiguous()
-        beta = beta.contiguous()
+        beta = beta.to(io_dt).contiguous()
         dh = torch.empty(B, N, H, dtype=io_dt, device=dev)
         dbeta = torch.empty(B, N, H, dtype=io_dt, device=dev)
     if carry is not None:

@@ -22,8 +22,11 @@ def np64(x):
     return np.asarray(x, dtype=np.float64)
 
 
-def rel_slices(g, o, layout: str):
-    """max over (b, h) slices of max|g-o| / max|o|.  layout 'bnhd' or 'bhn'."""
+def rel_slices(g, o, layout: str, floor: float = 1e-3):
+    """max over (b, h) slices of max|g-o| / max(max|o|, floor).  layout 'bnhd' or 'bhn'.
+
+    The absolute floor (reading C-17) keeps exactly-zero reference slices
+    (e.g. dQ at N=1, where dS = 0 in exact arithmetic) from dividing by 0."""
     g, o = np64(g), np64(o)
     if layout == "bnhd":
         g = g.transpose(0, 2, 1, 3).reshape(g.shape[0] * g.shape[2], -1)
@@ -32,7 +35,7 @@ def rel_slices(g, o, layout: str):
         g = g.reshape(-1, g.shape[-1])
         o = o.reshape(-1, o.shape[-1])
     num = np.abs(g - o).max(axis=1)
-    den = np.maximum(np.abs(o).max(axis=1), 1e-30)
+    den = np.maximum(np.abs(o).max(axis=1), floor)
     return float((num / den).max())
 
 

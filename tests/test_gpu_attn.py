@@ -52,13 +52,13 @@ def test_fp32_path_matches_oracle(s):
     got, ref = _run(s, torch.float32, seed=s.N + s.w)
     assert rel_slices(got["O"], ref["O"], "bnhd") <= TOL_F32_O
     assert max_abs(got["LSE"], ref["LSE"]) <= 1e-4
-    for k in ("dQ", "dK", "dV"):
-        assert rel_slices(got[k], ref[k], "bnhd") <= TOL_F32_GRAD, k
-    for k in ("dU", "dalpha"):
-        if np.abs(ref[k]).max() > 1e-6:
-            assert rel_slices(got[k], ref[k], "bhn") <= TOL_F32_GRAD, k
+    for k, lay in (("dQ", "bnhd"), ("dK", "bnhd"), ("dV", "bnhd"), ("dU", "bhn"), ("dalpha", "bhn")):
+        if np.abs(ref[k]).max() == 0.0:
+            # degenerate cases (w = 1, N = 1): the exact gradient is identically 0
+            # (dS = P (dP - D) with P = 1, dP = D); only fp32 round-off of dP - D remains
+            assert max_abs(got[k], ref[k]) <= 1e-4, k
         else:
-            assert max_abs(got[k], ref[k]) <= 1e-6, k
+            assert rel_slices(got[k], ref[k], lay) <= TOL_F32_GRAD, k
 
 
 BF16_SHAPES = [

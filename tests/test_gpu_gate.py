@@ -70,11 +70,12 @@ def test_gate_prefix_bwd(B, N, H, dtype):
     h, beta = h.to(dtype), beta.to(dtype)
     dU = torch.randn(B, H, N, generator=torch.Generator().manual_seed(N))
     carry = torch.randn(B, H, dtype=torch.float64)
-    dalpha, dh, dbeta = gb.gfwa_gate_prefix_bwd(dU.cuda(), h.cuda(), beta.cuda(), 1e-6, carry=carry.cuda(),
-                                                dtype=torch.float32)
+    dalpha, dh, dbeta = gb.gfwa_gate_prefix_bwd(dU.cuda(), h.cuda(), beta.cuda(), 1e-6, carry=carry.cuda())
+    assert dh.dtype == dtype and dbeta.dtype == dtype
     dar = oracle.dalpha_scan(dU, carry)
     assert rel_slices(dalpha, dar, "bhn") <= TOL_U
     dhr, dbr = oracle.gate_chain(h, beta, dar, 1e-6)
-    scale = max(np.abs(dhr).max(), 1e-30)
-    assert np.abs(np64(dh) - dhr).max() / scale <= 1e-5
-    assert np.abs(np64(dbeta) - dbr).max() / max(np.abs(dbr).max(), 1e-30) <= 1e-5
+    # fp32 chain-rule math; bf16 outputs add one rounding (2^-8 relative)
+    tol = 1e-5 if dtype == torch.float32 else 8e-3
+    assert np.abs(np64(dh) - dhr).max() / max(np.abs(dhr).max(), 1e-30) <= tol
+    assert np.abs(np64(dbeta) - dbr).max() / max(np.abs(dbr).max(), 1e-30) <= tol
