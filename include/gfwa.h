@@ -202,6 +202,13 @@ uint64_t gfwa_launch_count(void);
  * 0 = SIMT (fp32 parity path), 1 = tcgen05/TMA tensor-core path. */
 int gfwa_attn_path(const gfwa_attn_desc_t* desc);
 
+/* Diagnostic: one 128x128x128 tile through the tensor-core primitives the
+ * attention kernels use (TMA 128B-swizzle loads, tcgen05 SS MMA S = Q K^T,
+ * bf16 P = S written to TMEM, tcgen05 TS MMA O = P V).  Q, K, V: [128,128]
+ * bf16 row-major device arrays; S_out, O_out: [128,128] fp32 device arrays. */
+gfwa_status_t gfwa_debug_tc_selftest(const void* Q, const void* K, const void* V, float* S_out, float* O_out,
+                                     gfwa_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -332,6 +332,19 @@ def gfwa_decode(q, k_new, v_new, gate_a, K_cache, V_cache, U_cache, pos, gate_b=
     return o
 
 
+def gfwa_debug_tc_selftest(Q, K, V):
+    """S = Q K^T and O = bf16(S) V on one 128x128 tile through the tcgen05 path."""
+    lib = load()
+    _need_cuda(Q, K, V)
+    S = torch.empty(128, 128, dtype=torch.float32, device=Q.device)
+    O = torch.empty_like(S)
+    f = lib.gfwa_debug_tc_selftest
+    f.restype = ctypes.c_int
+    f.argtypes = [_VP] * 6
+    _check(f(_ptr(Q), _ptr(K), _ptr(V), _ptr(S), _ptr(O), _stream(Q.device)), "gfwa_debug_tc_selftest")
+    return S, O
+
+
 def launch_count() -> int:
     return int(load().gfwa_launch_count())
 

@@ -1,0 +1,27 @@
+// tma_host.cuh -- host-side TMA tensor-map encoding for [B, N, H, d] bf16
+// tensors (d contiguous, arbitrary (b, n, h) element strides).
+#pragma once
+#include <cuda.h>
+#include <stdint.h>
+
+namespace gfwa {
+
+// Box = {64 d-elements (128 B, one swizzle row), 1 head, rows, 1 batch},
+// 128-byte swizzle, OOB rows zero-filled (ragged tails, halo edges).
+inline bool encode_bnhd_map(CUtensorMap* map, const void* base, int64_t B, int64_t N, int64_t H, int d,
+                            const int64_t* s /* element strides b, n, h */, int box_rows) {
+    cuuint64_t dims[4] = {(cuuint64_t)d, (cuuint64_t)H, (cuuint64_t)N, (cuuint64_t)B};
+    cuuint64_t strides[3] = {(cuuint64_t)(s[2] * 2), (cuuint64_t)(s[1] * 2), (cuuint64_t)(s[0] * 2)};
+    // size-1 dims may carry any stride; keep them legal (multiple of 16, non-zero)
+    for (int i = 0; i < 3; ++i)
+        if (strides[i] == 0) strides[i] = 16;
+    cuuint32_t box[4] = {64u, 1u, (cuuint32_t)box_rows, 1u};
+    cuuint32_t estr[4] = {1u, 1u, 1u, 1u};
+    CUresult r = cuTensorMapEncodeTiled(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims,
+                                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+}  // namespace gfwa
