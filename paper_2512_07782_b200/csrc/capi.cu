@@ -72,6 +72,17 @@ gfwa_status_t make_params(const gfwa_attn_desc_t* d, AttnParams& p) {
     return GFWA_OK;
 }
 
+// A thread that has only used another CUDA runtime (e.g. torch's autograd
+// worker) may have no current driver context; the TMA descriptor encoder is a
+// driver call, so bind the context that owns the caller's data first.
+void bind_context(const void* dev_ptr) {
+    CUcontext cur = nullptr;
+    if (cuCtxGetCurrent(&cur) == CUDA_SUCCESS && cur) return;
+    CUcontext ctx = nullptr;
+    if (cuPointerGetAttribute(&ctx, CU_POINTER_ATTRIBUTE_CONTEXT, (CUdeviceptr)dev_ptr) == CUDA_SUCCESS && ctx)
+        cuCtxSetCurrent(ctx);
+}
+
 bool strides_ok(const int64_t* s, size_t esize) {
     for (int i = 0; i < 3; ++i)
         if (s[i] < 0 || ((s[i] * (int64_t)esize) % 16) != 0) return false;
@@ -91,6 +102,7 @@ extern "C" gfwa_status_t gfwa_fwd(const gfwa_attn_desc_t* desc, const void* Q, c
     if (!strides_ok(p.qs, es) || !strides_ok(p.ks, es) || !strides_ok(p.vs, es) || !strides_ok(p.os, es))
         return GFWA_ERR_INVALID_ARGUMENT;
     if (!al16(Q) || !al16(K) || !al16(V) || !al16(O) || (O_f32 && !al16(O_f32))) return GFWA_ERR_INVALID_ARGUMENT;
+    bind_context(Q);
     p.Q = Q;
     p.K = K;
     p.V = V;
@@ -109,7 +121,7 @@ static size_t bwd_ws_layout(const AttnParams& p, gfwa_dtype_t dt, size_t* off_D,
     *off_D = off;
     off += ((size_t)p.B * p.H * p.Nq * sizeof(float) + 255) & ~(size_t)255;
     *off_scan = off;
-    off += gfwa_gate_prefix_bwd_workspace_size(p.B, p.Nkv, p.H);
+    off += gfwa_gate_prefix_bwd_workspace_size(p.B * p.H, p.Nkv, 1);  // the dalpha scan below
     *off_tc = off;
     if (tc_bwd_supported(p, dt)) off += (tc_bwd_workspace(p) + 255) & ~(size_t)255;
     return off;
@@ -130,18 +142,17 @@ extern "C" gfwa_status_t gfwa_bwd(const gfwa_attn_desc_t* desc, const void* Q, c
                                   const double* dalpha_carry, void* ws, size_t ws_bytes, gfwa_stream_t stream) {
     AttnParams p;
     if (gfwa_status_t s = make_params(desc, p)) return s;
-    if (!Q || !K || !V || !U || !LSE || !dO || !dQ || !dK || !dV || !dU || !ws) return GFWA_ERR_INVALID_ARGUMENT;
-    if (!O && !O_f32) return GFWA_ERR_INVALID_ARGUMENT;
+    GFWA_REQUIRE(Q && K && V && U && LSE && dO && dQ && dK && dV && dU && ws);
+    GFWA_REQUIRE(O || O_f32);
     const size_t es = desc->dtype == GFWA_BF16 ? 2 : 4;
-    if (!strides_ok(p.qs, es) || !strides_ok(p.ks, es) || !strides_ok(p.vs, es) || !strides_ok(p.os, es))
-        return GFWA_ERR_INVALID_ARGUMENT;
+    GFWA_REQUIRE(strides_ok(p.qs, es) && strides_ok(p.ks, es) && strides_ok(p.vs, es) && strides_ok(p.os, es));
     const void* ptrs[] = {Q, K, V, dO, dQ, dK, dV};
-    for (const void* pp : ptrs)
-        if (!al16(pp)) return GFWA_ERR_INVALID_ARGUMENT;
-    if ((uintptr_t)ws % 256) return GFWA_ERR_INVALID_ARGUMENT;
+    for (const void* pp : ptrs) GFWA_REQUIRE(al16(pp));
+    GFWA_REQUIRE((uintptr_t)ws % 256 == 0);
     size_t off_D, off_scan, off_tc;
     const size_t need = bwd_ws_layout(p, desc->dtype, &off_D, &off_scan, &off_tc);
     if (ws_bytes < need) return GFWA_ERR_WORKSPACE;
+    bind_context(Q);
     p.Q = Q;
     p.K = K;
     p.V = V;
@@ -156,12 +167,13 @@ extern "C" gfwa_status_t gfwa_bwd(const gfwa_attn_desc_t* desc, const void* Q, c
     p.dU = dU;
     p.Dv = (float*)((char*)ws + off_D);
     cudaStream_t st = (cudaStream_t)stream;
-    if (gfwa_status_t s = bwd_preprocess(p, desc->dtype, st)) return s;
     gfwa_status_t s;
-    if (tc_bwd_supported(p, desc->dtype))
-        s = tc_bwd(p, st, (char*)ws + off_tc);
-    else
+    if (tc_bwd_supported(p, desc->dtype)) {
+        s = tc_bwd(p, st, (char*)ws + off_tc);  // D, dQ/dU zeroing fused in its own pre kernel
+    } else {
+        if ((s = bwd_preprocess(p, desc->dtype, st)) != GFWA_OK) return s;
         s = simt_bwd(p, desc->dtype, st);
+    }
     if (s != GFWA_OK) return s;
     if (!dalpha) return GFWA_OK;
     // dalpha = carry - reverse_cumsum(dU) over the N_kv key rows

@@ -7,6 +7,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "../../include/gfwa.h"
 
 namespace gfwa {
@@ -18,6 +21,15 @@ void note_launch(int n = 1);
 // Records a CUDA error for gfwa_last_cuda_error(); returns GFWA_ERR_CUDA if err.
 gfwa_status_t check_launch(cudaError_t err);
 inline gfwa_status_t check_launch() { return check_launch(cudaGetLastError()); }
+
+// Argument check: returns INVALID_ARGUMENT; with GFWA_DEBUG set, says which.
+#define GFWA_REQUIRE(cond)                                                                       \
+    do {                                                                                         \
+        if (!(cond)) {                                                                           \
+            if (getenv("GFWA_DEBUG")) fprintf(stderr, "gfwa: %s:%d: failed %s\n", __FILE__, __LINE__, #cond); \
+            return GFWA_ERR_INVALID_ARGUMENT;                                                    \
+        }                                                                                        \
+    } while (0)
 
 // ---------------------------------------------------------------- device side
 
