@@ -3,6 +3,10 @@
 Each ``csrc/*.cu`` is compiled to an object in ``build/`` (in parallel), then
 linked into ``paper_2512_07782_b200/libgfwa.so``.  Flags:
 ``-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17``.
+
+``python _build.py --variant NAME -DX=Y ...`` builds an experiment variant into
+``paper_2512_07782_b200/variants/libgfwa_NAME.so`` (select it at run time with
+``GFWA_LIB=<path>``); the default library is unaffected.
 """
 from __future__ import annotations
 
@@ -32,39 +36,55 @@ FLAGS = ARCH + [
     os.path.join(ROOT, "include"),
 ]
 
+# per-file register caps: the tensor-core kernels run 10 warps / CTA (1 CTA/SM),
+# so up to 200 registers per thread are available to the softmax warps
+PER_FILE = {"attn_tc_fwd.cu": ["-maxrregcount=200"], "attn_tc_bwd.cu": ["-maxrregcount=200"]}
+
 
 def _deps_mtime() -> float:
     files = glob.glob(os.path.join(CSRC, "*")) + glob.glob(os.path.join(ROOT, "include", "*.h"))
     return max(os.path.getmtime(f) for f in files)
 
 
-def _compile(src: str) -> tuple[str, str]:
-    obj = os.path.join(BUILD, os.path.basename(src) + ".o")
-    cmd = [NVCC, *FLAGS, "-c", src, "-o", obj]
+def _compile(args) -> tuple[str, str]:
+    src, bdir, extra = args
+    obj = os.path.join(bdir, os.path.basename(src) + ".o")
+    cmd = [NVCC, *FLAGS, *PER_FILE.get(os.path.basename(src), []), *extra, "-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
     return obj, r.stderr
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= _deps_mtime():
-        return LIB
-    os.makedirs(BUILD, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, extra: list[str] | None = None,
+          variant: str | None = None) -> str:
+    extra = list(extra or [])
+    out = LIB if variant is None else os.path.join(PKG, "variants", f"libgfwa_{variant}.so")
+    bdir = BUILD if variant is None else os.path.join(BUILD, "variants", variant)
+    if not force and variant is None and os.path.exists(out) and os.path.getmtime(out) >= _deps_mtime():
+        return out
+    os.makedirs(bdir, exist_ok=True)
+    os.makedirs(os.path.dirname(out), exist_ok=True)
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
-        results = list(ex.map(_compile, srcs))
+        results = list(ex.map(_compile, [(s, bdir, extra) for s in srcs]))
     if verbose:
         for _, log in results:
             sys.stderr.write(log)
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = out + f".tmp{os.getpid()}"
     cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *[o for o, _ in results], "-lcuda"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    argv = sys.argv[1:]
+    variant = None
+    if "--variant" in argv:
+        variant = argv[argv.index("--variant") + 1]
+    defines = [a for a in argv if a.startswith("-D")]
+    print(build(force="--force" in argv or variant is not None, verbose="-v" in argv, extra=defines,
+                variant=variant))

@@ -16,7 +16,7 @@ import threading
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libgfwa.so")
+LIB_PATH = os.environ.get("GFWA_LIB") or os.path.join(_PKG, "libgfwa.so")  # GFWA_LIB: experiment variants
 
 GFWA_F32, GFWA_BF16 = 0, 1
 GATE_HBETA, GATE_ALPHA = 0, 1

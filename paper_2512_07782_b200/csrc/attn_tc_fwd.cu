@@ -3,22 +3,31 @@
 //
 // One CTA owns two 128-row query tiles of one (b, h) and streams the 128-key
 // K/V tiles of their joint window once, diagonal first (descending j):
-//   warp 9      TMA producer: Q0/Q1 once, then K_j / V_j into 2-stage rings
-//               (128B swizzle, OOB rows zero-filled -> ragged tails for free)
+//   warp 9      TMA producer: Q0/Q1 once, then K_j (3-stage ring, one tile
+//               ahead) and V_j (2-stage ring); 128B swizzle, OOB rows
+//               zero-filled -> ragged tails for free
 //   warp 8      MMA issuer (one elected lane): S_i = Q_i K_j^T (SS, fp32 in
 //               TMEM) and O_i += P_i V_j (TS: P read from TMEM), commits to
 //               mbarriers; tcgen05.commit tracks all earlier MMAs, so S_full
 //               of step n also certifies that PV of step n-1 has landed.
 //   warps 0-3/4-7  softmax for tile 0 / tile 1, one thread per query row:
-//               tcgen05.ld the S row, add the gate bias (u_q - u_k) (P:377-380,
-//               an outer difference of two u vectors, nothing N x w is ever
-//               materialised), window-mask only on diagonal / window-edge
-//               tiles, online softmax in fp32 with a lazy
-//               rescale (only when the running max grows by > 2^8), bf16 P
-//               back into the same TMEM columns, then the epilogue O / l and
-//               LSE = m + ln l.
+//               tcgen05.ld the S row, add the gate bias as an outer
+//               difference of two u vectors (nothing N x w is materialised),
+//               window-mask only on diagonal / window-edge tiles (P:381-383,
+//               a per-row column range turned into bit masks), online softmax
+//               in fp32 with packed f32x2 FMA/ADD and a lazy rescale (the
+//               reference max moves only when it grows by > 2^8), bf16 P back
+//               into the same TMEM columns; epilogue O / l staged in smem with
+//               the 128B swizzle and written by TMA stores, LSE = m + ln l
+//               (P:388).
 // TMEM: S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512) columns x 128 lanes.
 // Key tiles outside every row's window are never loaded.
+#include <vector>
+
+#ifndef GFWA_FWD_POLY
+#define GFWA_FWD_POLY 2
+#endif
+
 #include "attn_common.cuh"
 #include "sm100.cuh"
 #include "tma_host.cuh"
@@ -31,44 +40,68 @@ using namespace sm100;
 constexpr int BM = 128;          // query rows per tile
 constexpr int BN = 128;          // keys per tile
 constexpr int D = 128;           // head dim
-constexpr int NST = 2;           // K and V ring stages
+constexpr int NK = 3;            // K ring stages
+constexpr int NV = 2;            // V ring stages
 constexpr uint32_t kTileBytes = BM * D * 2;  // 32 KB bf16 tile
 constexpr int kThreads = 320;    // 8 softmax warps + MMA warp + TMA warp
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
+constexpr int kPolyPairs = GFWA_FWD_POLY;  // of every 4 column pairs, how many use exp2_poly2
 
 struct TcFwdParams {
     const float* U;
-    void* O;
-    float* O_f32;
     float* LSE;
     int64_t Nq, Nkv, h0, H;
     int w;
-    float sl2;  // scale * log2(e)
-    int64_t os0, os1, os2;
+    int store_f32;
+    float sl2;         // scale * log2(e)
+    long long* trace;  // diagnostics only (GFWA_TRACE_FWD): per-CTA clock64 stamps
 };
+
+#define GFWA_TR(slot)                                                                                         \
+    do {                                                                                                      \
+        if (p.trace)                                                                                          \
+            p.trace[((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 64 + (slot)] = clock64(); \
+    } while (0)
 
 struct __align__(8) Bars {
     uint64_t q_full[2];
-    uint64_t k_full[NST], k_empty[NST];
-    uint64_t v_full[NST], v_empty[NST];
+    uint64_t k_full[NK], k_empty[NK];
+    uint64_t v_full[NV], v_empty[NV];
     uint64_t s_full[2], p_ready[2], o_full[2];
 };
 
 __device__ __forceinline__ int64_t kv_tile_lo(int64_t g_lo, int w) { return max64(0, g_lo - w + 1) / BN; }
 
+// bits [lo, hi] (inclusive, clipped to the 32-bit word starting at column base)
+__device__ __forceinline__ uint32_t range_bits(int lo, int hi, int base) {
+    const int a = min(max(lo - base, 0), 32), z = min(max(hi - base + 1, 0), 32);
+    const uint32_t upto_z = z >= 32 ? 0xffffffffu : ((1u << z) - 1u);
+    const uint32_t below_a = a >= 32 ? 0xffffffffu : ((1u << a) - 1u);
+    return upto_z & ~below_a;
+}
+
 __global__ void __launch_bounds__(kThreads, 1)
     fwd_tc_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
-                  const __grid_constant__ CUtensorMap mv, const TcFwdParams p) {
-    extern __shared__ uint8_t smem_raw[];
+                  const __grid_constant__ CUtensorMap mv, const __grid_constant__ CUtensorMap mo,
+                  const __grid_constant__ CUtensorMap mo32, const TcFwdParams p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint8_t* Qs = smem;                            // 2 tiles
-    uint8_t* Ks = smem + 2 * kTileBytes;           // NST tiles
-    uint8_t* Vs = Ks + NST * kTileBytes;           // NST tiles
-    float* ukbuf = (float*)(Vs + NST * kTileBytes);  // [2][BN]
-    Bars* bars = (Bars*)(ukbuf + 2 * BN);
+    uint8_t* Ks = smem + 2 * kTileBytes;           // NK tiles
+    uint8_t* Vs = Ks + NK * kTileBytes;            // NV tiles
+    __shared__ __align__(16) float s_nbk[2][BN];  // negated key bias -(u_k - uref) log2e, per tile
+    Bars* bars = (Bars*)(Vs + NV * kTileBytes);
     uint32_t* tmem_sh = (uint32_t*)(bars + 1);
 
     const int warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+        GFWA_TR(0);
+        if (p.trace) {
+            uint32_t smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            p.trace[((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 64 + 63] = smid;
+        }
+    }
     const int64_t b = blockIdx.z, h = blockIdx.y;
     const int64_t r0 = (int64_t)blockIdx.x * 2 * BM;
     const bool act1 = r0 + BM < p.Nq;
@@ -91,9 +124,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&bars->p_ready[i], 4);
             mbar_init(&bars->o_full[i], 1);
         }
-        for (int s = 0; s < NST; ++s) {
+        for (int s = 0; s < NK; ++s) {
             mbar_init(&bars->k_full[s], 1);
             mbar_init(&bars->k_empty[s], 1);
+        }
+        for (int s = 0; s < NV; ++s) {
             mbar_init(&bars->v_full[s], 1);
             mbar_init(&bars->v_empty[s], 1);
         }
@@ -107,11 +142,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_prefetch(&mq);
         tma_prefetch(&mk);
         tma_prefetch(&mv);
+        tma_prefetch(&mo);
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_sh;
+    if (threadIdx.x == 0) GFWA_TR(1);
 
     if (warp == 9) {
         // ------------------------------------------------ TMA producer
@@ -124,19 +161,25 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tma_load_4d(Qs + i * kTileBytes + half * (kTileBytes / 2), &mq, &bars->q_full[i], half * 64,
                                 (int)h, (int)(r0 + i * BM), (int)b);
             }
-            int k = 0;
-            for (int64_t j = J_hi; j >= J_lo; --j, ++k) {
-                const int s = k % NST;
-                const uint32_t ph = ((k / NST) & 1) ^ 1;
-                mbar_wait(&bars->k_empty[s], ph);
+            // K runs one tile ahead of V: S(j) needs K_j long before PV(j) needs V_j
+            const int nk = (int)(J_hi - J_lo + 1);
+            auto load_k = [&](int k) {
+                const int s = k % NK;
+                mbar_wait(&bars->k_empty[s], ((k / NK) & 1) ^ 1);
                 mbar_expect_tx(&bars->k_full[s], kTileBytes);
                 for (int half = 0; half < 2; ++half)
                     tma_load_4d_hint(Ks + s * kTileBytes + half * (kTileBytes / 2), &mk, &bars->k_full[s],
-                                     half * 64, (int)h, (int)(j * BN), (int)b, pol_kv);
-                mbar_wait(&bars->v_empty[s], ph);
-                mbar_expect_tx(&bars->v_full[s], kTileBytes);
+                                     half * 64, (int)h, (int)((J_hi - k) * BN), (int)b, pol_kv);
+            };
+            load_k(0);
+            int k = 0;
+            for (int64_t j = J_hi; j >= J_lo; --j, ++k) {
+                const int sv = k % NV;
+                if (k + 1 < nk) load_k(k + 1);
+                mbar_wait(&bars->v_empty[sv], ((k / NV) & 1) ^ 1);
+                mbar_expect_tx(&bars->v_full[sv], kTileBytes);
                 for (int half = 0; half < 2; ++half)
-                    tma_load_4d_hint(Vs + s * kTileBytes + half * (kTileBytes / 2), &mv, &bars->v_full[s],
+                    tma_load_4d_hint(Vs + sv * kTileBytes + half * (kTileBytes / 2), &mv, &bars->v_full[sv],
                                      half * 64, (int)h, (int)(j * BN), (int)b, pol_kv);
             }
         }
@@ -152,18 +195,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (act1) mbar_wait(&bars->q_full[1], 0);
         int k = 0;
         for (int64_t j = J_hi; j >= J_lo; --j, ++k) {
-            const int s = k % NST;
-            mbar_wait(&bars->k_full[s], (k / NST) & 1);
+            const int s = k % NK;
+            mbar_wait(&bars->k_full[s], (k / NK) & 1);
+            if (k < 8 && (threadIdx.x & 31) == 0) GFWA_TR(2 + k);
             tc_fence_after();
             int pv_issued = 0;
             for (int i = 0; i < 2; ++i) {
                 if (!act[i] || j < jlo[i] || j > jhi[i]) continue;
                 if (prev[i] >= 0) {
-                    // O_i += P_i(prev) V_prev  (V of tile j+1 sits in stage (k-1) % NST)
+                    // O_i += P_i(prev) V_prev  (V of tile j+1 sits in stage (k-1) % NV)
                     mbar_wait(&bars->p_ready[i], pph[i]);
                     pph[i] ^= 1;
-                    const int vs = (k - 1) % NST;
-                    mbar_wait(&bars->v_full[vs], ((k - 1) / NST) & 1);
+                    const int vs = (k - 1) % NV;
+                    mbar_wait(&bars->v_full[vs], ((k - 1) / NV) & 1);
                     tc_fence_after();
                     if (elect_one()) {
                         const uint32_t vbase = smem_u32(Vs + vs * kTileBytes);
@@ -197,7 +241,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (pv_issued > 0) {
                     const int64_t jp = j + 1;
                     const int users = (jp >= jlo[0] && jp <= jhi[0]) + (act1 && jp >= jlo[1] && jp <= jhi[1]);
-                    if (pv_issued == users) tc_commit(&bars->v_empty[(k - 1) % NST]);
+                    if (pv_issued == users) tc_commit(&bars->v_empty[(k - 1) % NV]);
                 }
             }
             __syncwarp();
@@ -207,8 +251,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (!act[i]) continue;
             mbar_wait(&bars->p_ready[i], pph[i]);
             const int kj = (int)(J_hi - prev[i]);
-            const int vs = kj % NST;
-            mbar_wait(&bars->v_full[vs], (kj / NST) & 1);
+            const int vs = kj % NV;
+            mbar_wait(&bars->v_full[vs], (kj / NV) & 1);
             tc_fence_after();
             if (elect_one()) {
                 const uint32_t vbase = smem_u32(Vs + vs * kTileBytes);
@@ -230,61 +274,87 @@ __global__ void __launch_bounds__(kThreads, 1)
             const bool valid = t < p.Nq;
             const int64_t g = t + p.h0;
             const float* Ubh = p.U + (b * p.H + h) * p.Nkv;
-            const float uq = valid ? Ubh[g] : 0.f;
+            // Bias in log2 units relative to a per-CTA reference u (reading C-18):
+            // u_q - u_k = (u_q - uref) - (u_k - uref); each difference is formed in
+            // fp32 before scaling, and the row constant (u_q - uref) cancels in the
+            // softmax, so it only re-enters the LSE.
+            const float uref = Ubh[glo[0]];
+            const float bq = valid ? (Ubh[g] - uref) * kLog2e : 0.f;
             const uint32_t lane_addr = tmem + ((uint32_t)((warp & 3) * 32) << 16);
             const uint32_t scol = 128 * i;
-            float* uk = ukbuf + i * BN;
+            const uint64_t sl2x2 = f2pack(p.sl2, p.sl2);
             float m_used = -INFINITY, l = 0.f;
             uint32_t sph = 0;
             int n = 0;
+            float u_next = jhi[i] * BN + r < p.Nkv ? Ubh[jhi[i] * BN + r] : 0.f;
             for (int64_t j = jhi[i]; j >= jlo[i]; --j, ++n) {
-                // u of this key tile -> smem (WG-cooperative)
+                // -(u_k - uref) log2e of this key tile -> smem (WG-cooperative); the
+                // next tile's u is prefetched into a register meanwhile
                 named_bar_sync(1 + i, 128);
-                const int64_t kj = j * BN + r;
-                uk[r] = kj < p.Nkv ? Ubh[kj] : 0.f;
+                s_nbk[i][r] = (uref - u_next) * kLog2e;
+                if (j > jlo[i]) u_next = Ubh[(j - 1) * BN + r];
                 named_bar_sync(1 + i, 128);
                 mbar_wait(&bars->s_full[i], sph);
+                if (n < 8 && r == 0) GFWA_TR(16 + 24 * i + n);
                 sph ^= 1;
                 tc_fence_after();
-                float x[BN];
-                {
-                    uint32_t rr[32];
-#pragma unroll
-                    for (int c = 0; c < BN; c += 32) {
-                        tmem_ld32(lane_addr + scol + c, rr);
-                        tmem_wait_ld();
-#pragma unroll
-                        for (int e = 0; e < 32; ++e) x[c + e] = __uint_as_float(rr[e]);
-                    }
-                }
-                // logits in log2 units: scale*q.k + (u_q - u_k)  (difference first, C-18)
+                const bool trw = (i == 0 && n == 1 && (r == 0 || r == 96));
+                // x = scale*q.k - (u_k - uref) log2e   (Alg. 2 l.12-15), packed pairs.
+                // Two passes over 32-column TMEM chunks (max, then exp) keep ~64
+                // values live instead of 128: no spills, loads pipeline freely;
+                // re-reading TMEM is cheaper than holding the row in registers.
                 const bool interior = (j * BN + BN - 1 <= glo[i]) && (j * BN >= ghi[i] - p.w + 1);
-                float mt = -INFINITY;
-                if (interior) {
-#pragma unroll
-                    for (int c = 0; c < BN; c += 4) {
-                        const float4 u4 = *reinterpret_cast<const float4*>(uk + c);
-                        x[c + 0] = fmaf(x[c + 0], p.sl2, (uq - u4.x) * kLog2e);
-                        x[c + 1] = fmaf(x[c + 1], p.sl2, (uq - u4.y) * kLog2e);
-                        x[c + 2] = fmaf(x[c + 2], p.sl2, (uq - u4.z) * kLog2e);
-                        x[c + 3] = fmaf(x[c + 3], p.sl2, (uq - u4.w) * kLog2e);
-                        mt = fmaxf(mt, fmaxf(fmaxf(x[c], x[c + 1]), fmaxf(x[c + 2], x[c + 3])));
-                    }
-                } else {
+                uint32_t keep[4] = {~0u, ~0u, ~0u, ~0u};
+                if (!interior) {
+                    // keys in (g - w, g] and < N_kv, as columns of this tile
                     const int64_t kb = j * BN;
+                    const int hi = (int)min64(min64(g - kb, (int64_t)BN - 1), p.Nkv - 1 - kb);
+                    const int lo = (int)max64(g - p.w + 1 - kb, (int64_t)0);
 #pragma unroll
-                    for (int c = 0; c < BN; c += 4) {
-                        const float4 u4 = *reinterpret_cast<const float4*>(uk + c);
-                        const float uu[4] = {u4.x, u4.y, u4.z, u4.w};
+                    for (int c = 0; c < 4; ++c) keep[c] = range_bits(lo, hi, 32 * c);
+                }
+                const float* nbv = s_nbk[i];
+                auto logits = [&](const uint32_t (&raw)[32], int cb, uint64_t (&xp)[16]) {
 #pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const int64_t key = kb + c + e;
-                            const bool keep = key <= g && key > g - p.w && key < p.Nkv;
-                            x[c + e] = keep ? fmaf(x[c + e], p.sl2, (uq - uu[e]) * kLog2e) : -INFINITY;
-                            mt = fmaxf(mt, x[c + e]);
+                    for (int e = 0; e < 32; e += 4) {
+                        const float4 nb = *reinterpret_cast<const float4*>(nbv + cb + e);
+                        xp[e / 2] = ffma2(f2pack(__uint_as_float(raw[e]), __uint_as_float(raw[e + 1])), sl2x2,
+                                          f2pack(nb.x, nb.y));
+                        xp[e / 2 + 1] = ffma2(f2pack(__uint_as_float(raw[e + 2]), __uint_as_float(raw[e + 3])), sl2x2,
+                                              f2pack(nb.z, nb.w));
+                    }
+                    if (!interior) {
+                        const uint32_t kw = keep[cb >> 5];
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) {
+                            float a, z;
+                            f2unpack(xp[e], a, z);
+                            a = ((kw >> (2 * e)) & 1u) ? a : -INFINITY;
+                            z = ((kw >> (2 * e + 1)) & 1u) ? z : -INFINITY;
+                            xp[e] = f2pack(a, z);
                         }
                     }
+                };
+                float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+                for (int cb = 0; cb < BN; cb += 32) {
+                    uint32_t raw[32];
+                    tmem_ld32(lane_addr + scol + cb, raw);
+                    tmem_wait_ld();
+                    uint64_t xp[16];
+                    logits(raw, cb, xp);
+#pragma unroll
+                    for (int e = 0; e < 16; e += 2) {
+                        float a0, a1, b0, b1;
+                        f2unpack(xp[e], a0, a1);
+                        f2unpack(xp[e + 1], b0, b1);
+                        mx0 = fmaxf(mx0, fmaxf(a0, a1));
+                        mx1 = fmaxf(mx1, fmaxf(b0, b1));
+                    }
                 }
+                if (trw) GFWA_TR(10 + (r == 96));
+                const float mt = fmaxf(mx0, mx1);
+                if (trw) GFWA_TR(12 + (r == 96));
                 // lazy online softmax: move the reference max only when it grows by > 2^8
                 float corr = 1.f;
                 bool need = false;
@@ -297,19 +367,42 @@ __global__ void __launch_bounds__(kThreads, 1)
                     m_used = mt;
                 }
                 const float mref = (m_used == -INFINITY) ? 0.f : m_used;
-                float lsum = 0.f;
+                const uint64_t nm2 = f2pack(-mref, -mref);
+                uint64_t acc[4] = {0, 0, 0, 0};  // packed (0.f, 0.f)
 #pragma unroll
-                for (int c = 0; c < BN; c += 64) {
-                    uint32_t pk[32];
+                for (int cb = 0; cb < BN; cb += 32) {
+                    uint32_t raw[32];
+                    tmem_ld32(lane_addr + scol + cb, raw);
+                    tmem_wait_ld();
+                    uint64_t xp[16];
+                    logits(raw, cb, xp);
+                    uint32_t pk[16];
 #pragma unroll
-                    for (int e = 0; e < 32; ++e) {
-                        const float p0 = ex2(x[c + 2 * e] - mref), p1 = ex2(x[c + 2 * e + 1] - mref);
-                        lsum += p0 + p1;
+                    for (int e = 0; e < 16; ++e) {
+                        const uint64_t d = fadd2(xp[e], nm2);
+                        float p0, p1;
+                        if ((e & 3) < kPolyPairs) {
+                            // part of the exponentials on the FMA pipe: MUFU.EX2 is
+                            // co-critical with the tensor core on B200
+                            f2unpack(exp2_poly2(d), p0, p1);
+                        } else {
+                            float d0, d1;
+                            f2unpack(d, d0, d1);
+                            p0 = ex2(d0);
+                            p1 = ex2(d1);
+                        }
+                        acc[e & 3] = fadd2(acc[e & 3], f2pack(p0, p1));
                         pk[e] = pack_bf16x2(p0, p1);
                     }
-                    tmem_st32(lane_addr + scol + c / 2, pk);
+                    tmem_st16(lane_addr + scol + cb / 2, pk);  // P (bf16) over the S columns
                 }
-                l += lsum;
+                if (trw) GFWA_TR(14 + (r == 96));
+                {
+                    const uint64_t a01 = fadd2(acc[0], acc[1]), a23 = fadd2(acc[2], acc[3]);
+                    float s0, s1;
+                    f2unpack(fadd2(a01, a23), s0, s1);
+                    l += s0 + s1;
+                }
                 // rescale O_i (PV of the previous step is complete: S_full certified it)
                 if (__any_sync(0xffffffffu, need) && n > 0) {
                     uint32_t ob[32];
@@ -323,42 +416,66 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
                 tmem_wait_st();
+                if (trw) GFWA_TR(34 + (r == 96));
                 tc_fence_before();
                 __syncwarp();
                 if ((threadIdx.x & 31) == 0) mbar_arrive(&bars->p_ready[i]);
+                if (n < 8 && r == 0) GFWA_TR(24 + 24 * i + n);
+                if (trw && r == 96) GFWA_TR(38);
             }
-            // epilogue: O / l, LSE (Alg. 2 l.19-20)
+            // epilogue: O / l (Alg. 2 l.19-20) staged in smem (128B swizzle) and
+            // written with TMA stores; tile 0 stages in the K ring, tile 1 in the
+            // V ring + Q area (both idle once O_full fires)
             mbar_wait(&bars->o_full[i], 0);
+            if (r == 0) GFWA_TR(32 + 24 * i);
             tc_fence_after();
-            const float inv = 1.f / l;
-            __nv_bfloat16* orow = (__nv_bfloat16*)p.O + b * p.os0 + t * p.os1 + h * p.os2;
-            float* frow = p.O_f32 ? p.O_f32 + b * p.os0 + t * p.os1 + h * p.os2 : nullptr;
-#pragma unroll
-            for (int c = 0; c < D; c += 32) {
+            const float inv = l > 0.f ? 1.f / l : 0.f;
+            uint8_t* stg_bf = i == 0 ? Ks : Vs;
+            uint8_t* stg_f = i == 0 ? Ks + kTileBytes : Qs;
+            const uint32_t sb = smem_u32(stg_bf), sf = smem_u32(stg_f);
+#pragma unroll 1
+            for (int c = 0; c < 4; ++c) {
                 uint32_t ob[32];
-                tmem_ld32(lane_addr + 256 + scol + c, ob);
+                tmem_ld32(lane_addr + 256 + scol + 32 * c, ob);
                 tmem_wait_ld();
-                if (valid) {
-                    float v[32];
+                float v[32];
 #pragma unroll
-                    for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(ob[e]) * inv;
+                for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(ob[e]) * inv;
+                // bf16: columns [32c, 32c+32) = half c>>1, 16-B chunks (c&1)*4 + k
 #pragma unroll
-                    for (int e = 0; e < 32; e += 8) {
-                        uint4 pk;
-                        pk.x = pack_bf16x2(v[e + 0], v[e + 1]);
-                        pk.y = pack_bf16x2(v[e + 2], v[e + 3]);
-                        pk.z = pack_bf16x2(v[e + 4], v[e + 5]);
-                        pk.w = pack_bf16x2(v[e + 6], v[e + 7]);
-                        *reinterpret_cast<uint4*>(orow + c + e) = pk;
-                    }
-                    if (frow) {
+                for (int k = 0; k < 4; ++k) {
+                    const int chunk = ((c & 1) * 4 + k) ^ (r & 7);
+                    uint4 pkv;
+                    pkv.x = pack_bf16x2(v[8 * k + 0], v[8 * k + 1]);
+                    pkv.y = pack_bf16x2(v[8 * k + 2], v[8 * k + 3]);
+                    pkv.z = pack_bf16x2(v[8 * k + 4], v[8 * k + 5]);
+                    pkv.w = pack_bf16x2(v[8 * k + 6], v[8 * k + 7]);
+                    sts128(sb + (c >> 1) * (kTileBytes / 2) + r * 128 + chunk * 16, pkv);
+                }
+                if (p.store_f32) {
+                    // fp32: box c (32 columns, 128 B rows), 16-B pieces k
 #pragma unroll
-                        for (int e = 0; e < 32; e += 4)
-                            *reinterpret_cast<float4*>(frow + c + e) = make_float4(v[e], v[e + 1], v[e + 2], v[e + 3]);
+                    for (int k = 0; k < 8; ++k) {
+                        const int piece = k ^ (r & 7);
+                        sts128(sf + c * 16384 + r * 128 + piece * 16,
+                               make_uint4(__float_as_uint(v[4 * k]), __float_as_uint(v[4 * k + 1]),
+                                          __float_as_uint(v[4 * k + 2]), __float_as_uint(v[4 * k + 3])));
                     }
                 }
             }
-            if (valid) p.LSE[(b * p.H + h) * p.Nq + t] = (m_used + __log2f(l)) * kLn2;
+            if (valid) p.LSE[(b * p.H + h) * p.Nq + t] = (m_used + bq + __log2f(l)) * kLn2;
+            fence_proxy_async();
+            named_bar_sync(1 + i, 128);
+            if (r == 0) {
+                const int row0 = (int)(r0 + i * BM);
+                for (int half = 0; half < 2; ++half)
+                    tma_store_4d(&mo, stg_bf + half * (kTileBytes / 2), half * 64, (int)h, row0, (int)b);
+                if (p.store_f32)
+                    for (int c = 0; c < 4; ++c) tma_store_4d(&mo32, stg_f + c * 16384, c * 32, (int)h, row0, (int)b);
+                bulk_commit();
+                bulk_wait_read0();  // smem must stay valid until the bulk stores have read it
+                GFWA_TR(33 + 24 * i);
+            }
         }
     }
     tc_fence_before();
@@ -369,7 +486,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
-constexpr size_t kSmemBytes = 1024 + 2 * kTileBytes + 2 * NST * kTileBytes + 2 * BN * sizeof(float) + sizeof(Bars) + 16;
+// dynamic smem (+1 KB static s_nbk): 1024 alignment slack + Q, K ring, V ring + barriers
+constexpr size_t kSmemBytes = 1024 + 2 * kTileBytes + (NK + NV) * kTileBytes + sizeof(Bars) + 16;
 
 }  // namespace
 
@@ -381,33 +499,51 @@ bool tc_fwd_supported(const AttnParams& p, gfwa_dtype_t dt) {
 }
 
 gfwa_status_t tc_fwd(const AttnParams& p, cudaStream_t st) {
-    CUtensorMap mq, mk, mv;
-    if (!encode_bnhd_map(&mq, p.Q, p.B, p.Nq, p.H, D, p.qs, BM) ||
-        !encode_bnhd_map(&mk, p.K, p.B, p.Nkv, p.H, D, p.ks, BN) ||
-        !encode_bnhd_map(&mv, p.V, p.B, p.Nkv, p.H, D, p.vs, BN))
-        return GFWA_ERR_INVALID_ARGUMENT;
+    CUtensorMap mq, mk, mv, mo, mo32;
+    GFWA_REQUIRE(encode_bnhd_map(&mq, p.Q, p.B, p.Nq, p.H, D, p.qs, BM));
+    GFWA_REQUIRE(encode_bnhd_map(&mk, p.K, p.B, p.Nkv, p.H, D, p.ks, BN));
+    GFWA_REQUIRE(encode_bnhd_map(&mv, p.V, p.B, p.Nkv, p.H, D, p.vs, BN));
+    GFWA_REQUIRE(encode_bnhd_map(&mo, p.O, p.B, p.Nq, p.H, D, p.os, BM));
+    if (p.O_f32)
+        GFWA_REQUIRE(encode_bnhd_map_f32(&mo32, p.O_f32, p.B, p.Nq, p.H, D, p.os, BM));
+    else
+        mo32 = mo;  // unused
     TcFwdParams tp;
     tp.U = p.U;
-    tp.O = p.O;
-    tp.O_f32 = p.O_f32;
     tp.LSE = p.LSE;
     tp.Nq = p.Nq;
     tp.Nkv = p.Nkv;
     tp.h0 = p.h0;
     tp.H = p.H;
     tp.w = p.w;
+    tp.store_f32 = p.O_f32 != nullptr;
     tp.sl2 = p.scale * kLog2e;
-    tp.os0 = p.os[0];
-    tp.os1 = p.os[1];
-    tp.os2 = p.os[2];
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
         attr_set = true;
     }
     dim3 grid((unsigned)((p.Nq + 2 * BM - 1) / (2 * BM)), (unsigned)p.H, (unsigned)p.B);
-    fwd_tc_kernel<<<grid, kThreads, kSmemBytes, st>>>(mq, mk, mv, tp);
+    // diagnostics: GFWA_TRACE_FWD=<file> dumps per-CTA clock64 stamps (synchronous)
+    const char* trace_file = getenv("GFWA_TRACE_FWD");
+    const size_t n_cta = (size_t)grid.x * grid.y * grid.z;
+    tp.trace = nullptr;
+    if (trace_file) {
+        cudaMalloc(&tp.trace, n_cta * 64 * sizeof(long long));
+        cudaMemsetAsync(tp.trace, 0, n_cta * 64 * sizeof(long long), st);
+    }
+    fwd_tc_kernel<<<grid, kThreads, kSmemBytes, st>>>(mq, mk, mv, mo, mo32, tp);
     note_launch();
+    if (trace_file) {
+        std::vector<long long> hbuf(n_cta * 64);
+        cudaStreamSynchronize(st);
+        cudaMemcpy(hbuf.data(), tp.trace, hbuf.size() * sizeof(long long), cudaMemcpyDeviceToHost);
+        cudaFree(tp.trace);
+        if (FILE* f = fopen(trace_file, "wb")) {
+            fwrite(hbuf.data(), sizeof(long long), hbuf.size(), f);
+            fclose(f);
+        }
+    }
     return check_launch();
 }
 
