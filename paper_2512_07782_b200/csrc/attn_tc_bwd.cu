@@ -2,22 +2,27 @@
 // (sm_100a): Alg. E.2 with readings C-3, C-4, C-11, C-12.
 //
 // KV-major: one CTA owns a 128-key tile of one (b, h) (K and V resident in
-// smem) and walks the 128-query tiles whose windows reach it.
-// Per query tile, all five contractions run on tcgen05 with TMEM accumulators:
-//   S^T  = K Q^T          SS  -> TMEM [0,128)
-//   dP^T = V dO^T         SS  -> TMEM [128,256)
-//   (softmax-grad warps, one thread per key: P^T = exp(S - L), dS^T =
-//    P^T (dP^T - D); P^T, dS^T back to TMEM as bf16, dS^T also to smem)
-//   dV  += P^T dO         TS  (A = P^T from TMEM)        -> TMEM [256,384)
-//   dK  += dS^T Q         TS  (A = dS^T from TMEM)       -> TMEM [384,512)
-//   dQ_i = dS K           SS  (A = dS from smem, MN-major) -> TMEM [0,128)
-// The paper writes dQ back per tile; here the drain warps add it
-// into an fp32 dQ accumulator with vector reductions in L2.  du^k (the column
-// sum, C-4) accumulates in registers of the key thread; du^q (the paper's
-// rowsum(dS), kept per reading C-11) is a cross-thread sum over keys,
-// done in fp32 with a warp butterfly transpose-reduce plus a 4-warp smem
-// combine, so both sums see the same fp32 dS and sum_m dU_m telescopes to 0.
-// A separate Q-major kernel (the paper's second kernel) is avoided.
+// smem) and walks the 64-query steps whose windows reach it.
+// All five contractions run on tcgen05 with TMEM accumulators, pipelined
+// across steps with two TMEM buffers (S^T/dP^T of step n are produced while
+// the gradients of step n-1 are contracted):
+//   S^T  = K Q^T          SS  M=128 keys, N=64 queries   -> buf[n&1] cols [0,64)
+//   dP^T = V dO^T         SS                             -> buf[n&1] cols [64,128)
+//   (softmax-grad, 2 warpgroups x 32 queries, thread = key: P^T = exp(S - L),
+//    dS^T = P^T (dP^T - D); P^T and dS^T back to TMEM as bf16 over the columns
+//    they were read from, dS^T also to smem)
+//   dQ^T = K^T dS^T       SS  M=128 (d), 4 x N=16         -> the freed columns
+//   dV  += P^T dO         TS  (A = P^T from TMEM)         -> TMEM [256,384)
+//   dK  += dS^T Q         TS  (A = dS^T from TMEM)        -> TMEM [384,512)
+// The dQ^T tile is drained by a third warpgroup (thread = head-dim lane) into
+// an fp32 dQ accumulator with coalesced L2 reductions while the next step
+// runs (the paper writes dQ back per tile).  du^k (column sum, C-4)
+// accumulates per key thread; du^q (the paper's rowsum(dS), kept per
+// C-11) is a cross-thread sum over keys done in fp32 with a warp butterfly
+// transpose-reduce, so both sums see the same fp32 dS and sum_m dU_m
+// telescopes to zero.  dK, dV leave through smem + TMA stores.
+#include <vector>
+
 #include "attn_common.cuh"
 #include "sm100.cuh"
 #include "tma_host.cuh"
@@ -27,78 +32,98 @@ namespace {
 
 using namespace sm100;
 
-constexpr int BM = 128;  // queries per step
-constexpr int BN = 128;  // keys per CTA
+constexpr int BN = 128;   // keys per CTA
+constexpr int BMQ = 64;   // queries per step
 constexpr int D = 128;
-constexpr uint32_t kTile = 128 * 128 * 2;  // 32 KB bf16 tile
-constexpr int kThreads = 320;              // softmax-grad WG, dQ-drain WG, MMA warp, TMA warp
+constexpr int NQS = 3;    // Q/dO ring stages
+constexpr uint32_t kDQ = 32 * 128 * 4;    // 16 KB dQ staging: 32 queries x 128 d fp32
+constexpr uint32_t kKV = 128 * 128 * 2;   // 32 KB K or V tile
+constexpr uint32_t kQT = 64 * 128 * 2;    // 16 KB Q or dO tile
+constexpr uint32_t kDS = 128 * 64 * 2;    // 16 KB dS^T tile
+constexpr int kThreads = 448;             // 2 softmax-grad WGs, drain WG, MMA warp, TMA warp
 
 struct TcBwdParams {
     const float* U;
     const float* LSE;
     const float* Dv;
-    float* dQacc;   // [B, Nq, H, d] fp32, zeroed by the preprocess kernel
-    float* dU;      // [B, H, Nkv] fp32, zeroed by the preprocess kernel
-    void* dK;
-    void* dV;
+    float* dQacc;  // [B, Nq, H, d] fp32, zeroed by the preprocess kernel
+    float* dU;     // [B, H, Nkv] fp32, zeroed before the launch
     int64_t Nq, Nkv, h0, H;
     int w;
     float sl2, scale;
-    int64_t ks0, ks1, ks2, vs0, vs1, vs2;
+    long long* trace;  // diagnostics only (GFWA_TRACE_BWD): per-CTA clock64 stamps
 };
+
+#define GFWA_TR(slot)                                                                                         \
+    do {                                                                                                      \
+        if (p.trace)                                                                                          \
+            p.trace[((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 64 + (slot)] = clock64(); \
+    } while (0)
 
 struct __align__(8) Bars {
-    uint64_t kv_full, q_full, q_empty, st_full, ds_ready, dq_full, dq_drained, dkdv_full;
+    uint64_t kv_full;
+    uint64_t q_full[NQS], q_empty[NQS];
+    uint64_t st_full[2], ds_ready[2], dq_full[2], dq_drained[2];
+    uint64_t dkdv_full;
 };
 
-__device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {
-    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
-                 : "memory");
-}
 __device__ __forceinline__ void red_add(float* addr, float a) {
     asm volatile("red.global.add.f32 [%0], %1;" ::"l"(addr), "f"(a) : "memory");
+}
+
+__device__ __forceinline__ uint32_t range_bits(int lo, int hi, int base) {
+    const int a = min(max(lo - base, 0), 32), z = min(max(hi - base + 1, 0), 32);
+    const uint32_t upto_z = z >= 32 ? 0xffffffffu : ((1u << z) - 1u);
+    const uint32_t below_a = a >= 32 ? 0xffffffffu : ((1u << a) - 1u);
+    return upto_z & ~below_a;
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
     bwd_tc_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
                   const __grid_constant__ CUtensorMap mv, const __grid_constant__ CUtensorMap mdo,
+                  const __grid_constant__ CUtensorMap mdk, const __grid_constant__ CUtensorMap mdv,
+                  const __grid_constant__ CUtensorMap mdq,
                   const TcBwdParams p) {
-    extern __shared__ uint8_t smem_raw[];
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint8_t* Ks = smem;
-    uint8_t* Vs = Ks + kTile;
-    uint8_t* Qs = Vs + kTile;
-    uint8_t* dOs = Qs + kTile;
-    uint8_t* dSs = dOs + kTile;  // dS^T [keys][queries], MN-major A of the dQ MMA
-    float* redq = (float*)(dSs + kTile);  // [4 warps][BM] partial du^q
-    float* vlse = redq + 4 * BM;          // per-step query vectors (log2 units)
-    float* vD = vlse + BM;
-    float* vuq = vD + BM;
-    Bars* bars = (Bars*)(vuq + BM);
+    uint8_t* Vs = Ks + kKV;
+    uint8_t* Qs = Vs + kKV;              // NQS stages of [Q tile | dO tile]
+    uint8_t* dSs = Qs + NQS * 2 * kQT;   // 2 x dS^T tile
+    uint8_t* dQs = dSs + 2 * kDS;        // dQ staging: 4 x [32 queries][32 d] fp32, 128B swizzle
+    Bars* bars = (Bars*)(dQs + kDQ);
     uint32_t* tmem_sh = (uint32_t*)(bars + 1);
+    __shared__ __align__(16) float s_cq[NQS][BMQ];    // (u_q - uref) log2e - L_q log2e
+    __shared__ __align__(16) float s_D[NQS][BMQ];     // D_q = rowsum(O dO)
+    __shared__ float s_red[2][2][4][32];              // [parity][wg][warp][lane] du^q partials
 
-    const int warp = threadIdx.x >> 5;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t b = blockIdx.z, h = blockIdx.y;
-    const int64_t j0 = (int64_t)blockIdx.x * BN;  // first key of the tile
+    const int64_t j0 = (int64_t)blockIdx.x * BN;
     const int64_t j_last = min64(j0 + BN, p.Nkv) - 1;
     // Alg. E.2 l.12-14: queries whose window reaches this key tile
     const int64_t t_lo = max64(0, j0 - p.h0);
     const int64_t t_hi = min64(p.Nq - 1, j_last + p.w - 1 - p.h0);
-    const int64_t qt_lo = t_lo / BM, qt_hi = t_hi / BM;
-    const int nsteps = t_lo <= t_hi ? (int)(qt_hi - qt_lo + 1) : 0;
+    const int64_t qt_lo = t_lo / BMQ;
+    const int nsteps = t_lo <= t_hi ? (int)(t_hi / BMQ - qt_lo + 1) : 0;
+    const float* Ubh = p.U + (b * p.H + h) * p.Nkv;
 
     if (threadIdx.x == 0) {
         mbar_init(&bars->kv_full, 1);
-        mbar_init(&bars->q_full, 1);
-        mbar_init(&bars->q_empty, 1);
-        mbar_init(&bars->st_full, 1);
-        mbar_init(&bars->ds_ready, 4);
-        mbar_init(&bars->dq_full, 1);
-        mbar_init(&bars->dq_drained, 4);
+        for (int s = 0; s < NQS; ++s) {
+            mbar_init(&bars->q_full[s], 2);  // TMA bytes + the vector stores
+            mbar_init(&bars->q_empty[s], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&bars->st_full[i], 1);
+            mbar_init(&bars->ds_ready[i], 8);
+            mbar_init(&bars->dq_full[i], 1);
+            mbar_init(&bars->dq_drained[i], 4);
+        }
         mbar_init(&bars->dkdv_full, 1);
         fence_barrier_init();
     }
-    if (warp == 8) {
+    if (warp == 12) {
         tmem_alloc(tmem_sh, 512);
         tmem_relinquish();
     }
@@ -106,239 +131,310 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_sh;
+    const float uref = Ubh[j0];  // per-CTA bias reference (reading C-18)
+    if (threadIdx.x == 0) GFWA_TR(0);
 
-    if (warp == 9) {
-        // ------------------------------------------------ TMA producer
-        if (elect_one() && nsteps > 0) {
-            mbar_expect_tx(&bars->kv_full, 2 * kTile);
-            for (int half = 0; half < 2; ++half) {
-                tma_load_4d(Ks + half * (kTile / 2), &mk, &bars->kv_full, half * 64, (int)h, (int)j0, (int)b);
-                tma_load_4d(Vs + half * (kTile / 2), &mv, &bars->kv_full, half * 64, (int)h, (int)j0, (int)b);
-            }
-            for (int n = 0; n < nsteps; ++n) {
-                const int64_t t0 = (qt_lo + n) * BM;
-                mbar_wait(&bars->q_empty, (n & 1) ^ 1);
-                mbar_expect_tx(&bars->q_full, 2 * kTile);
+    if (warp == 13) {
+        // ------------------------------------------------ producer: TMA + per-step vectors
+        if (nsteps > 0) {
+            if (elect_one()) {
+                mbar_expect_tx(&bars->kv_full, 2 * kKV);
                 for (int half = 0; half < 2; ++half) {
-                    tma_load_4d(Qs + half * (kTile / 2), &mq, &bars->q_full, half * 64, (int)h, (int)t0, (int)b);
-                    tma_load_4d(dOs + half * (kTile / 2), &mdo, &bars->q_full, half * 64, (int)h, (int)t0,
-                                (int)b);
+                    tma_load_4d(Ks + half * (kKV / 2), &mk, &bars->kv_full, half * 64, (int)h, (int)j0, (int)b);
+                    tma_load_4d(Vs + half * (kKV / 2), &mv, &bars->kv_full, half * 64, (int)h, (int)j0, (int)b);
                 }
             }
+            __syncwarp();
+            for (int n = 0; n < nsteps; ++n) {
+                const int s = n % NQS;
+                const int64_t t0 = (qt_lo + n) * BMQ;
+                mbar_wait(&bars->q_empty[s], ((n / NQS) & 1) ^ 1);
+                if (elect_one()) {
+                    mbar_expect_tx(&bars->q_full[s], 2 * kQT);
+                    uint8_t* qd = Qs + s * 2 * kQT;
+                    for (int half = 0; half < 2; ++half) {
+                        tma_load_4d(qd + half * (kQT / 2), &mq, &bars->q_full[s], half * 64, (int)h, (int)t0, (int)b);
+                        tma_load_4d(qd + kQT + half * (kQT / 2), &mdo, &bars->q_full[s], half * 64, (int)h, (int)t0,
+                                    (int)b);
+                    }
+                }
+                for (int q = lane; q < BMQ; q += 32) {
+                    const int64_t t = t0 + q;
+                    const bool ok = t < p.Nq;
+                    const int64_t vi = (b * p.H + h) * p.Nq + t;
+                    s_cq[s][q] = ok ? (Ubh[t + p.h0] - uref) * kLog2e - p.LSE[vi] * kLog2e : 0.f;
+                    s_D[s][q] = ok ? p.Dv[vi] : 0.f;
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bars->q_full[s]);
+            }
         }
-    } else if (warp == 8) {
+    } else if (warp == 12) {
         // ------------------------------------------------ MMA issuer
-        const uint32_t id_kk = idesc_bf16(128, 128, false, false);  // S^T, dP^T
-        const uint32_t id_tm = idesc_bf16(128, 128, false, true);   // dV, dK (A in TMEM, B MN-major)
-        const uint32_t id_dq = idesc_bf16(128, 128, true, true);    // dQ (A, B MN-major)
+        const uint32_t id_st = idesc_bf16(128, BMQ, false, false);  // S^T, dP^T
+        const uint32_t id_tm = idesc_bf16(128, D, false, true);     // dV, dK (A in TMEM, B MN-major)
+        const uint32_t id_dq = idesc_bf16(128, 16, true, true);     // dQ^T quarters (A, B MN-major)
+        const uint32_t kb = smem_u32(Ks), vb = smem_u32(Vs);
         if (nsteps > 0) mbar_wait(&bars->kv_full, 0);
-        const uint32_t kb = smem_u32(Ks), vb = smem_u32(Vs), qb = smem_u32(Qs), ob = smem_u32(dOs),
-                       sb = smem_u32(dSs);
-        for (int n = 0; n < nsteps; ++n) {
-            mbar_wait(&bars->q_full, n & 1);
-            if (n > 0) mbar_wait(&bars->dq_drained, (n - 1) & 1);
+        auto mma2 = [&](int m) {  // gradients of step m
+            const int bm = m & 1, sm = m % NQS;
+            mbar_wait(&bars->ds_ready[bm], (m >> 1) & 1);
+            if (m < 8 && lane == 0) GFWA_TR(17 + m);
             tc_fence_after();
             if (elect_one()) {
+                const uint32_t buf = tmem + 128 * bm;
+                const uint32_t qb = smem_u32(Qs + sm * 2 * kQT), ob = qb + kQT, sb = smem_u32(dSs + bm * kDS);
+                // dQ^T = K^T dS^T, four 16-query column blocks into the freed columns
+                const uint32_t qcol[4] = {16, 48, 64 + 16, 64 + 48};
+#pragma unroll
+                for (int qq = 0; qq < 4; ++qq)
+#pragma unroll
+                    for (int kk = 0; kk < BN / 16; ++kk)
+                        mma_ss(buf + qcol[qq], sdesc_sw128(kb + kk * 2048, kKV / 2, 1024),
+                               sdesc_sw128(sb + qq * 32 + kk * 2048, 8192, 1024), id_dq, kk > 0 ? 1u : 0u);
+                tc_commit(&bars->dq_full[bm]);
+                // dV += P^T dO ; dK += dS^T Q   (16 queries = 8 TMEM columns per K step)
+#pragma unroll
+                for (int kk = 0; kk < BMQ / 16; ++kk) {
+                    const uint32_t acol = (kk >> 1) * 32 + (kk & 1) * 8;
+                    const uint32_t acc = (m > 0 || kk > 0) ? 1u : 0u;
+                    mma_ts(tmem + 256, buf + acol, sdesc_sw128(ob + kk * 2048, kQT / 2, 1024), id_tm, acc);
+                    mma_ts(tmem + 384, buf + 64 + acol, sdesc_sw128(qb + kk * 2048, kQT / 2, 1024), id_tm, acc);
+                }
+                tc_commit(&bars->q_empty[sm]);
+                if (m == nsteps - 1) tc_commit(&bars->dkdv_full);
+            }
+            __syncwarp();
+        };
+        for (int n = 0; n < nsteps; ++n) {
+            const int bn = n & 1, s = n % NQS;
+            mbar_wait(&bars->q_full[s], (n / NQS) & 1);
+            if (n >= 2) mbar_wait(&bars->dq_drained[bn], ((n - 2) >> 1) & 1);
+            tc_fence_after();
+            if (elect_one()) {
+                const uint32_t qb = smem_u32(Qs + s * 2 * kQT), ob = qb + kQT;
+                const uint32_t buf = tmem + 128 * bn;
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk) {
-                    const uint32_t off = (kk >> 2) * (kTile / 2) + (kk & 3) * 32;
-                    mma_ss(tmem + 0, sdesc_sw128(kb + off, 16, 1024), sdesc_sw128(qb + off, 16, 1024), id_kk,
-                           kk > 0);
-                    mma_ss(tmem + 128, sdesc_sw128(vb + off, 16, 1024), sdesc_sw128(ob + off, 16, 1024), id_kk,
-                           kk > 0);
+                    const uint32_t ka = (kk >> 2) * (kKV / 2) + (kk & 3) * 32;
+                    const uint32_t qa = (kk >> 2) * (kQT / 2) + (kk & 3) * 32;
+                    mma_ss(buf, sdesc_sw128(kb + ka, 16, 1024), sdesc_sw128(qb + qa, 16, 1024), id_st, kk > 0);
+                    mma_ss(buf + 64, sdesc_sw128(vb + ka, 16, 1024), sdesc_sw128(ob + qa, 16, 1024), id_st, kk > 0);
                 }
-                tc_commit(&bars->st_full);
+                tc_commit(&bars->st_full[bn]);
             }
             __syncwarp();
-            mbar_wait(&bars->ds_ready, n & 1);
-            tc_fence_after();
-            if (elect_one()) {
-#pragma unroll
-                for (int kk = 0; kk < BM / 16; ++kk) {
-                    // dV += P^T dO ; dK += dS^T Q  (A from TMEM, 16 queries = 8 columns)
-                    mma_ts(tmem + 256, tmem + 0 + 8 * kk, sdesc_sw128(ob + kk * 2048, kTile / 2, 1024), id_tm,
-                           (n > 0 || kk > 0) ? 1u : 0u);
-                    mma_ts(tmem + 384, tmem + 128 + 8 * kk, sdesc_sw128(qb + kk * 2048, kTile / 2, 1024), id_tm,
-                           (n > 0 || kk > 0) ? 1u : 0u);
-                }
-#pragma unroll
-                for (int kk = 0; kk < BN / 16; ++kk) {
-                    // dQ_i = dS K   (contract over the 128 keys)
-                    mma_ss(tmem + 0, sdesc_sw128(sb + kk * 2048, kTile / 2, 1024),
-                           sdesc_sw128(kb + kk * 2048, kTile / 2, 1024), id_dq, kk > 0);
-                }
-                tc_commit(&bars->dq_full);
-                tc_commit(&bars->q_empty);
-                if (n == nsteps - 1) tc_commit(&bars->dkdv_full);
-            }
-            __syncwarp();
+            if (n >= 1) mma2(n - 1);
         }
-    } else if (warp < 4) {
-        // ------------------------------------------------ softmax-grad WG: thread = key
-        const int kr = threadIdx.x;  // 0..127
+        if (nsteps > 0) mma2(nsteps - 1);
+    } else if (warp < 8) {
+        // ------------------------------------------------ softmax-grad: thread = key, 32 queries per WG
+        const int wg = warp >> 2;  // query columns [32 wg, 32 wg + 32) of each step
+        const int kr = threadIdx.x & 127;
         const int64_t j = j0 + kr;
         const bool kvalid = j < p.Nkv;
-        const float* Ubh = p.U + (b * p.H + h) * p.Nkv;
-        const float uk = kvalid ? Ubh[j] : 0.f;
-        const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
-        float colsum = 0.f;
+        const float nuk = kvalid ? -(Ubh[j] - uref) * kLog2e : 0.f;
+        const uint64_t sl2x2 = f2pack(p.sl2, p.sl2), nuk2 = f2pack(nuk, nuk);
+        const uint32_t lane_addr = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+        uint64_t colsum2 = 0;  // packed (0.f, 0.f)
         for (int n = 0; n < nsteps; ++n) {
-            const int64_t t0 = (qt_lo + n) * BM;
-            named_bar_sync(1, 128);
-            {
-                const int64_t t = t0 + kr;
-                const bool ok = t < p.Nq;
-                const int64_t vi = (b * p.H + h) * p.Nq + t;
-                vlse[kr] = ok ? p.LSE[vi] * kLog2e : 0.f;
-                vD[kr] = ok ? p.Dv[vi] : 0.f;
-                vuq[kr] = ok ? Ubh[t + p.h0] : 0.f;
-            }
-            named_bar_sync(1, 128);
-            mbar_wait(&bars->st_full, n & 1);
+            const int bn = n & 1, s = n % NQS;
+            const int64_t t0 = (qt_lo + n) * BMQ;
+            mbar_wait(&bars->st_full[bn], (n >> 1) & 1);
+            if (n < 8 && threadIdx.x == 0) GFWA_TR(1 + n);
             tc_fence_after();
-            // interior: every (key, query) pair of the tile lies inside the window
-            const bool interior = (j0 + BN - 1 <= t0 + p.h0) && (j0 > t0 + BM - 1 + p.h0 - p.w) &&
-                                  (t0 + BM <= p.Nq) && (j0 + BN <= p.Nkv);
-#pragma unroll 1
-            for (int c = 0; c < BM; c += 32) {
-                uint32_t sr[32], dr[32];
-                tmem_ld32(lane_addr + c, sr);
-                tmem_ld32(lane_addr + 128 + c, dr);
-                tmem_wait_ld();
-                float ds[32];
-                uint32_t pk[16], dk[16];
-#pragma unroll
-                for (int e = 0; e < 32; ++e) {
-                    const int q = c + e;
-                    // P = exp(scale q.k + (u_q - u_k) - L_q)  (P:1095-1100), log2 units
-                    float x = fmaf(__uint_as_float(sr[e]), p.sl2, (vuq[q] - uk) * kLog2e) - vlse[q];
-                    if (!interior) {
-                        const int64_t t = t0 + q, g = t + p.h0;
-                        const bool keep = t < p.Nq && kvalid && j <= g && j > g - p.w;
-                        x = keep ? x : -INFINITY;
-                    }
-                    const float pr = ex2(x);
-                    ds[e] = pr * (__uint_as_float(dr[e]) - vD[q]);  // dS = P (dP - D)
-                    colsum += ds[e];                                // du^k, fp32 (C-4)
-                    if (e & 1) {
-                        pk[e / 2] = pack_bf16x2(__uint_as_float(sr[e - 1]), pr);
-                        dk[e / 2] = pack_bf16x2(ds[e - 1], ds[e]);
-                    } else {
-                        sr[e] = __float_as_uint(pr);  // keep P of the even column for packing
-                    }
-                }
-                tmem_st16(lane_addr + c / 2, pk);        // P^T  -> cols [0, 64)
-                tmem_st16(lane_addr + 128 + c / 2, dk);  // dS^T -> cols [128, 192)
-                // dS^T row -> smem, 128B-swizzled MN-major layout (query chunk ^ key%8)
-#pragma unroll
-                for (int v = 0; v < 4; ++v) {
-                    const int q = c + v * 8;
-                    const int half = q >> 6, chunk = ((q & 63) >> 3) ^ (kr & 7);
-                    uint4 val = make_uint4(dk[v * 4 + 0], dk[v * 4 + 1], dk[v * 4 + 2], dk[v * 4 + 3]);
-                    *reinterpret_cast<uint4*>(dSs + half * (kTile / 2) + kr * 128 + chunk * 16) = val;
-                }
-                // du^q partial: sum of this warp's 32 keys for each of the 32 query
-                // columns, butterfly transpose-reduce -> lane l holds column c + l
-                const int lane = threadIdx.x & 31;
-#pragma unroll
-                for (int s = 16; s >= 1; s >>= 1) {
-                    const bool up = lane & s;
-#pragma unroll
-                    for (int e = 0; e < s; ++e) {
-                        const float send = up ? ds[e] : ds[e + s];
-                        const float keep = up ? ds[e + s] : ds[e];
-                        ds[e] = keep + __shfl_xor_sync(0xffffffffu, send, s);
-                    }
-                }
-                redq[warp * BM + c + lane] = ds[0];
+            const uint32_t scol = 128 * bn + 32 * wg;  // this WG's S^T columns (dP^T at +64)
+            // keys in (g - w, g] of each query g = t + h0, as a column range
+            const bool interior = (j0 + BN - 1 <= t0 + p.h0) && (j0 > t0 + BMQ - 1 + p.h0 - p.w) &&
+                                  (t0 + BMQ <= p.Nq) && (j0 + BN <= p.Nkv);
+            uint32_t keep = ~0u;
+            if (!interior) {
+                const int64_t qlo = j - p.h0 - t0, qhi = min64(j - p.h0 - t0 + p.w - 1, p.Nq - 1 - t0);
+                keep = kvalid ? range_bits((int)max64(qlo, -1), (int)min64(qhi, (int64_t)BMQ), 32 * wg) : 0u;
             }
+            const float* cq = &s_cq[s][32 * wg];
+            const float* Dq = &s_D[s][32 * wg];
+            float ds[32];
+            uint32_t pk[16], dk[16];
+#pragma unroll
+            for (int h16 = 0; h16 < 32; h16 += 16) {
+                // 16-column TMEM chunks keep the live register set small
+                uint32_t s16[16], d16[16];
+                tmem_ld16(lane_addr + scol + h16, s16);
+                tmem_ld16(lane_addr + scol + 64 + h16, d16);
+                tmem_wait_ld();
+#pragma unroll
+                for (int e = 0; e < 16; e += 4) {
+                    const float4 c4 = *reinterpret_cast<const float4*>(cq + h16 + e);
+                    const float4 d4 = *reinterpret_cast<const float4*>(Dq + h16 + e);
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                    const int a = e + 2 * u, e2 = h16 + a;
+                    // P = exp(scale q.k + (u_q - u_k) - L_q)  (P:1095-1100), log2 units
+                    uint64_t x = ffma2(f2pack(__uint_as_float(s16[a]), __uint_as_float(s16[a + 1])), sl2x2,
+                                       u == 0 ? f2pack(c4.x, c4.y) : f2pack(c4.z, c4.w));
+                    x = fadd2(x, nuk2);
+                    float x0, x1;
+                    f2unpack(x, x0, x1);
+                    if (!interior) {
+                        x0 = ((keep >> e2) & 1u) ? x0 : -INFINITY;
+                        x1 = ((keep >> (e2 + 1)) & 1u) ? x1 : -INFINITY;
+                    }
+                    const uint64_t pr = f2pack(ex2(x0), ex2(x1));
+                    // dS = P (dP - D)
+                    const uint64_t dpd = fadd2(f2pack(__uint_as_float(d16[a]), __uint_as_float(d16[a + 1])),
+                                               u == 0 ? f2pack(-d4.x, -d4.y) : f2pack(-d4.z, -d4.w));
+                    const uint64_t dsv = fmul2(pr, dpd);
+                    colsum2 = fadd2(colsum2, dsv);  // du^k, fp32 (C-4)
+                    float p0, p1;
+                    f2unpack(pr, p0, p1);
+                    f2unpack(dsv, ds[e2], ds[e2 + 1]);
+                    pk[e2 / 2] = pack_bf16x2(p0, p1);
+                    dk[e2 / 2] = pack_bf16x2(ds[e2], ds[e2 + 1]);
+                    }
+                }
+            }
+            tmem_st16(lane_addr + scol, pk);       // P^T  over the S^T columns it came from
+            tmem_st16(lane_addr + scol + 64, dk);  // dS^T over the dP^T columns
+            {  // dS^T row -> smem (128B-swizzled MN-major: row = key, 16-B chunk of 8 queries ^ key%8)
+                const uint32_t sb = smem_u32(dSs + bn * kDS) + kr * 128;
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    sts128(sb + (((4 * wg + c) ^ (kr & 7)) * 16),
+                           make_uint4(dk[4 * c], dk[4 * c + 1], dk[4 * c + 2], dk[4 * c + 3]));
+            }
+            // du^q partial over this warp's 32 keys: butterfly transpose-reduce -> lane l holds query 32 wg + l
+#pragma unroll
+            for (int sft = 16; sft >= 1; sft >>= 1) {
+                const bool up = lane & sft;
+#pragma unroll
+                for (int e = 0; e < sft; ++e) {
+                    const float send = up ? ds[e] : ds[e + sft];
+                    const float keepv = up ? ds[e + sft] : ds[e];
+                    ds[e] = keepv + __shfl_xor_sync(0xffffffffu, send, sft);
+                }
+            }
+            s_red[n & 1][wg][warp & 3][lane] = ds[0];
             tmem_wait_st();
             fence_proxy_async();
             tc_fence_before();
             __syncwarp();
-            if ((threadIdx.x & 31) == 0) mbar_arrive(&bars->ds_ready);
-            // du^q_t += rowsum(dS) at key position t + h0 (C-11), 4-warp combine
-            named_bar_sync(1, 128);
-            {
-                const int64_t t = t0 + kr;
-                const float rs = redq[kr] + redq[BM + kr] + redq[2 * BM + kr] + redq[3 * BM + kr];
+            if (lane == 0) mbar_arrive(&bars->ds_ready[bn]);
+            if (n < 8 && threadIdx.x == 0) GFWA_TR(9 + n);
+            // du^q_t += rowsum(dS) at key position t + h0 (C-11): combine the WG's 4 warps
+            named_bar_sync(1 + wg, 128);
+            if (kr < 32) {
+                const int64_t t = t0 + 32 * wg + kr;
+                const float rs = s_red[n & 1][wg][0][kr] + s_red[n & 1][wg][1][kr] + s_red[n & 1][wg][2][kr] +
+                                 s_red[n & 1][wg][3][kr];
                 if (t < p.Nq) red_add(p.dU + (b * p.H + h) * p.Nkv + t + p.h0, rs);
             }
         }
-        // epilogue: dK = scale * acc (C-3), dV, du^k = -colsum (C-4)
-        __nv_bfloat16* dkrow = (__nv_bfloat16*)p.dK + b * p.ks0 + j * p.ks1 + h * p.ks2;
-        __nv_bfloat16* dvrow = (__nv_bfloat16*)p.dV + b * p.vs0 + j * p.vs1 + h * p.vs2;
+        {
+            float c0, c1;
+            f2unpack(colsum2, c0, c1);
+            if (kvalid && nsteps > 0) red_add(p.dU + (b * p.H + h) * p.Nkv + j, -(c0 + c1));  // du^k (C-4)
+        }
+        // epilogue: WG0 -> dV, WG1 -> dK (scale, C-3), via smem + TMA store
+        uint8_t* stg = Qs + wg * 2 * kQT;  // the Q/dO stages are idle once dkdv_full fires
+        const uint32_t sg = smem_u32(stg);
+        const uint32_t acol = wg == 0 ? 256 : 384;
+        const float mul = wg == 0 ? 1.f : p.scale;
         if (nsteps > 0) {
             mbar_wait(&bars->dkdv_full, 0);
+            if (threadIdx.x == 0) GFWA_TR(41);
             tc_fence_after();
         }
 #pragma unroll 1
-        for (int c = 0; c < D; c += 32) {
-            uint32_t kr32[32], vr32[32];
+        for (int c = 0; c < 4; ++c) {
+            uint32_t v[32];
             if (nsteps > 0) {
-                tmem_ld32(lane_addr + 384 + c, kr32);
-                tmem_ld32(lane_addr + 256 + c, vr32);
+                tmem_ld32(lane_addr + acol + 32 * c, v);
                 tmem_wait_ld();
             } else {
 #pragma unroll
-                for (int e = 0; e < 32; ++e) kr32[e] = vr32[e] = 0u;
+                for (int e = 0; e < 32; ++e) v[e] = 0u;
             }
-            if (kvalid) {
 #pragma unroll
-                for (int e = 0; e < 32; e += 8) {
-                    uint4 a, v;
-                    a.x = pack_bf16x2(__uint_as_float(kr32[e + 0]) * p.scale, __uint_as_float(kr32[e + 1]) * p.scale);
-                    a.y = pack_bf16x2(__uint_as_float(kr32[e + 2]) * p.scale, __uint_as_float(kr32[e + 3]) * p.scale);
-                    a.z = pack_bf16x2(__uint_as_float(kr32[e + 4]) * p.scale, __uint_as_float(kr32[e + 5]) * p.scale);
-                    a.w = pack_bf16x2(__uint_as_float(kr32[e + 6]) * p.scale, __uint_as_float(kr32[e + 7]) * p.scale);
-                    v.x = pack_bf16x2(__uint_as_float(vr32[e + 0]), __uint_as_float(vr32[e + 1]));
-                    v.y = pack_bf16x2(__uint_as_float(vr32[e + 2]), __uint_as_float(vr32[e + 3]));
-                    v.z = pack_bf16x2(__uint_as_float(vr32[e + 4]), __uint_as_float(vr32[e + 5]));
-                    v.w = pack_bf16x2(__uint_as_float(vr32[e + 6]), __uint_as_float(vr32[e + 7]));
-                    *reinterpret_cast<uint4*>(dkrow + c + e) = a;
-                    *reinterpret_cast<uint4*>(dvrow + c + e) = v;
-                }
+            for (int k = 0; k < 4; ++k) {
+                const int chunk = ((c & 1) * 4 + k) ^ (kr & 7);
+                uint4 pkv;
+                pkv.x = pack_bf16x2(__uint_as_float(v[8 * k + 0]) * mul, __uint_as_float(v[8 * k + 1]) * mul);
+                pkv.y = pack_bf16x2(__uint_as_float(v[8 * k + 2]) * mul, __uint_as_float(v[8 * k + 3]) * mul);
+                pkv.z = pack_bf16x2(__uint_as_float(v[8 * k + 4]) * mul, __uint_as_float(v[8 * k + 5]) * mul);
+                pkv.w = pack_bf16x2(__uint_as_float(v[8 * k + 6]) * mul, __uint_as_float(v[8 * k + 7]) * mul);
+                sts128(sg + (c >> 1) * (kKV / 2) + kr * 128 + chunk * 16, pkv);
             }
         }
-        if (kvalid) red_add(p.dU + (b * p.H + h) * p.Nkv + j, -colsum);
-    } else if (warp < 8) {
-        // ------------------------------------------------ dQ drain WG: thread = query
-        const int qr = threadIdx.x - 128;
+        fence_proxy_async();
+        named_bar_sync(1 + wg, 128);
+        if (kr == 0) {
+            for (int half = 0; half < 2; ++half)
+                tma_store_4d(wg == 0 ? &mdv : &mdk, stg + half * (kKV / 2), half * 64, (int)h, (int)j0, (int)b);
+            bulk_commit();
+            bulk_wait_read0();
+            if (wg == 0) GFWA_TR(42);
+        }
+    } else if (warp < 12) {
+        // ------------------------------------------------ dQ drain: thread = head-dim lane
+        // dQ^T (TMEM, lane = d) -> smem [64 queries][128 d] fp32 (4 boxes of 32 d,
+        // 128B swizzle) -> TMA bulk reduce-add into the fp32 dQ accumulator: the
+        // L2 does the adds, no per-thread atomics.
+        const int dl = threadIdx.x - 256;  // 0..127
         const uint32_t lane_addr = tmem + ((uint32_t)((warp & 3) * 32) << 16);
-        for (int n = 0; n < nsteps; ++n) {
-            const int64_t t = (qt_lo + n) * BM + qr;
-            const bool valid = t < p.Nq;
-            mbar_wait(&bars->dq_full, n & 1);
+        const uint32_t qcol[4] = {16, 48, 64 + 16, 64 + 48};
+        const uint32_t sq = smem_u32(dQs) + (dl >> 5) * (kDQ / 4);  // this lane's 32-d box (4 KB)
+        for (int m = 0; m < nsteps; ++m) {
+            const int bm = m & 1;
+            const int64_t t0 = (qt_lo + m) * BMQ;
+            mbar_wait(&bars->dq_full[bm], (m >> 1) & 1);
+            if (m < 8 && dl == 0) GFWA_TR(25 + m);
             tc_fence_after();
-            float* dq = p.dQacc + ((b * p.Nq + t) * p.H + h) * D;
-#pragma unroll 1
-            for (int c = 0; c < D; c += 32) {
-                uint32_t r[32];
-                tmem_ld32(lane_addr + c, r);
-                tmem_wait_ld();
-                if (valid) {
+            uint32_t v[4][16];
 #pragma unroll
-                    for (int e = 0; e < 32; e += 4)
-                        red_add_v4(dq + c + e, __uint_as_float(r[e]), __uint_as_float(r[e + 1]),
-                                   __uint_as_float(r[e + 2]), __uint_as_float(r[e + 3]));
-                }
-            }
+            for (int qq = 0; qq < 4; ++qq) tmem_ld16(lane_addr + 128 * bm + qcol[qq], v[qq]);
+            tmem_wait_ld();
+            // all 64 queries are in registers: release the TMEM buffer first
             tc_fence_before();
             __syncwarp();
-            if ((threadIdx.x & 31) == 0) mbar_arrive(&bars->dq_drained);
+            if (lane == 0) mbar_arrive(&bars->dq_drained[bm]);
+            if (m < 8 && dl == 0) GFWA_TR(33 + m);
+            // two rounds of 32 queries through a 16 KB staging buffer;
+            // row = query, 16-B chunk (d%32)/4 ^ (query%8), word d%4
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+                if (dl == 0) bulk_wait_read0();  // the previous bulk reduce has read the buffer
+                named_bar_sync(3, 128);
+#pragma unroll
+                for (int qq = 2 * half; qq < 2 * half + 2; ++qq)
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) {
+                        const int q = 16 * (qq & 1) + e;  // row within the 32-query round
+                        sts32(sq + q * 128 + ((((dl & 31) >> 2) ^ (q & 7)) << 4) + (dl & 3) * 4,
+                              __uint_as_float(v[qq][e]));
+                    }
+                fence_proxy_async();
+                named_bar_sync(3, 128);
+                if (dl == 0) {
+                    for (int c = 0; c < 4; ++c)
+                        tma_reduce_add_4d(&mdq, dQs + c * (kDQ / 4), c * 32, (int)h, (int)(t0 + 32 * half), (int)b);
+                    bulk_commit();
+                }
+            }
         }
+        if (dl == 0) bulk_wait0();  // reductions complete before the CTA exits
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 8) {
+    if (warp == 12) {
         tc_fence_after();
         tmem_dealloc(tmem, 512);
     }
 }
 
-constexpr size_t kSmemBytes = 1024 + 5 * kTile + 7 * BM * sizeof(float) + sizeof(Bars) + 16;
+constexpr size_t kSmemBytes = 1024 + 2 * kKV + NQS * 2 * kQT + 2 * kDS + kDQ + sizeof(Bars) + 16;
 
-// dQacc, dU zeroing fused with D = rowsum(O dO); dQ = scale * dQacc -> bf16
+// dQacc zeroing fused with D = rowsum(O dO)  (Alg. E.2 l.7; O from O_f32, C-12)
 __global__ void __launch_bounds__(256) bwd_tc_pre_kernel(AttnParams p) {
     const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
@@ -366,6 +462,7 @@ __global__ void __launch_bounds__(256) bwd_tc_pre_kernel(AttnParams p) {
     *reinterpret_cast<float4*>(p.dQacc + ((b * p.Nq + t) * p.H + h) * D + c) = make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
+// dQ = scale * dQacc -> bf16 (C-3)
 __global__ void __launch_bounds__(256) bwd_tc_post_kernel(AttnParams p) {
     const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
@@ -375,7 +472,7 @@ __global__ void __launch_bounds__(256) bwd_tc_post_kernel(AttnParams p) {
     const int c = lane * 4;
     const float4 a = *reinterpret_cast<const float4*>(p.dQacc + ((b * p.Nq + t) * p.H + h) * D + c);
     uint2 o;
-    o.x = pack_bf16x2(a.x * p.scale, a.y * p.scale);  // dQ = scale dS K (C-3)
+    o.x = pack_bf16x2(a.x * p.scale, a.y * p.scale);
     o.y = pack_bf16x2(a.z * p.scale, a.w * p.scale);
     *reinterpret_cast<uint2*>((__nv_bfloat16*)p.dQ + b * p.qs[0] + t * p.qs[1] + h * p.qs[2] + c) = o;
 }
@@ -394,11 +491,15 @@ size_t tc_bwd_workspace(const AttnParams& p) { return (size_t)p.B * p.Nq * p.H *
 gfwa_status_t tc_bwd(const AttnParams& pin, cudaStream_t st, void* ws) {
     AttnParams p = pin;
     p.dQacc = (float*)ws;
-    CUtensorMap mq, mk, mv, mdo;
-    GFWA_REQUIRE(encode_bnhd_map(&mq, p.Q, p.B, p.Nq, p.H, D, p.qs, BM));
+    CUtensorMap mq, mk, mv, mdo, mdk, mdv, mdq;
+    GFWA_REQUIRE(encode_bnhd_map(&mq, p.Q, p.B, p.Nq, p.H, D, p.qs, BMQ));
     GFWA_REQUIRE(encode_bnhd_map(&mk, p.K, p.B, p.Nkv, p.H, D, p.ks, BN));
     GFWA_REQUIRE(encode_bnhd_map(&mv, p.V, p.B, p.Nkv, p.H, D, p.vs, BN));
-    GFWA_REQUIRE(encode_bnhd_map(&mdo, p.dO, p.B, p.Nq, p.H, D, p.os, BM));
+    GFWA_REQUIRE(encode_bnhd_map(&mdo, p.dO, p.B, p.Nq, p.H, D, p.os, BMQ));
+    GFWA_REQUIRE(encode_bnhd_map(&mdk, p.dK, p.B, p.Nkv, p.H, D, p.ks, BN));
+    GFWA_REQUIRE(encode_bnhd_map(&mdv, p.dV, p.B, p.Nkv, p.H, D, p.vs, BN));
+    const int64_t acc_s[3] = {p.Nq * p.H * D, p.H * D, D};  // dQacc [B, Nq, H, d] fp32
+    GFWA_REQUIRE(encode_bnhd_map_f32(&mdq, p.dQacc, p.B, p.Nq, p.H, D, acc_s, 32));
     const int64_t rows = p.B * p.Nq * p.H;
     const unsigned rgrid = (unsigned)((rows + 7) / 8);
     if (gfwa_status_t s = check_launch(cudaMemsetAsync(p.dU, 0, (size_t)p.B * p.H * p.Nkv * sizeof(float), st)))
@@ -412,8 +513,6 @@ gfwa_status_t tc_bwd(const AttnParams& pin, cudaStream_t st, void* ws) {
     tp.Dv = p.Dv;
     tp.dQacc = p.dQacc;
     tp.dU = p.dU;
-    tp.dK = p.dK;
-    tp.dV = p.dV;
     tp.Nq = p.Nq;
     tp.Nkv = p.Nkv;
     tp.h0 = p.h0;
@@ -421,20 +520,31 @@ gfwa_status_t tc_bwd(const AttnParams& pin, cudaStream_t st, void* ws) {
     tp.w = p.w;
     tp.sl2 = p.scale * kLog2e;
     tp.scale = p.scale;
-    tp.ks0 = p.ks[0];
-    tp.ks1 = p.ks[1];
-    tp.ks2 = p.ks[2];
-    tp.vs0 = p.vs[0];
-    tp.vs1 = p.vs[1];
-    tp.vs2 = p.vs[2];
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(bwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
         attr_set = true;
     }
     dim3 grid((unsigned)((p.Nkv + BN - 1) / BN), (unsigned)p.H, (unsigned)p.B);
-    bwd_tc_kernel<<<grid, kThreads, kSmemBytes, st>>>(mq, mk, mv, mdo, tp);
+    const char* trace_file = getenv("GFWA_TRACE_BWD");  // diagnostics (synchronous)
+    const size_t n_cta = (size_t)grid.x * grid.y * grid.z;
+    tp.trace = nullptr;
+    if (trace_file) {
+        cudaMalloc(&tp.trace, n_cta * 64 * sizeof(long long));
+        cudaMemsetAsync(tp.trace, 0, n_cta * 64 * sizeof(long long), st);
+    }
+    bwd_tc_kernel<<<grid, kThreads, kSmemBytes, st>>>(mq, mk, mv, mdo, mdk, mdv, mdq, tp);
     note_launch();
+    if (trace_file) {
+        std::vector<long long> hbuf(n_cta * 64);
+        cudaStreamSynchronize(st);
+        cudaMemcpy(hbuf.data(), tp.trace, hbuf.size() * sizeof(long long), cudaMemcpyDeviceToHost);
+        cudaFree(tp.trace);
+        if (FILE* f = fopen(trace_file, "wb")) {
+            fwrite(hbuf.data(), sizeof(long long), hbuf.size(), f);
+            fclose(f);
+        }
+    }
     if (gfwa_status_t s = check_launch()) return s;
     bwd_tc_post_kernel<<<rgrid, 256, 0, st>>>(p);
     note_launch();
