@@ -46,20 +46,27 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks/throttle reasons, sampled every 50 ms from before the
+    warm-up until after the timed region; each sample is stamped with the host
+    wall clock on arrival and summary() keeps those inside [t0, t1] of the timed
+    region (widened by one sampling period so a short region still gets its
+    neighbouring samples)."""
+
+    PERIOD_S = 0.05
 
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
         self.proc = None
-        self.lines = []
+        self.samples = []  # (host time, line)
+        self.window = None
 
-    def __enter__(self):
+    def start(self):
         q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", str(int(self.PERIOD_S * 1000))],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -69,10 +76,14 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.samples.append((time.time(), line.strip()))
 
-    def __exit__(self, *a):
+    def mark(self, t0: float, t1: float):
+        self.window = (t0 - self.PERIOD_S, t1 + self.PERIOD_S)
+
+    def stop(self):
         if self.proc is not None:
+            time.sleep(2 * self.PERIOD_S)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
@@ -82,7 +93,10 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        lo, hi = self.window if self.window else (-1e18, 1e18)
+        for ts, ln in self.samples:
+            if not lo <= ts <= hi:
+                continue
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 8:
                 continue
@@ -97,7 +111,8 @@ class ClockSampler:
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": ["unsampled"]}
         sm.sort()
-        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm),
+                "window_s": round(hi - lo, 3)}
 
 
 def _dist():
@@ -167,6 +182,8 @@ def run_ours(args):
             rec.append(e)
         return rec, (O, dQ, dK, dV, dh, dbeta)
 
+    clk = ClockSampler(local).start()
+    time.sleep(0.3)  # nvidia-smi needs a moment before its first sample
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize(dev)
@@ -176,16 +193,18 @@ def run_ours(args):
     evs = []
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        torch.cuda.synchronize(dev)
-        if dist:
-            dist.barrier()
-        t0.record(st)
-        for _ in range(args.steps):
-            r, _ = step(timed_kernels=True)
-            evs += r
-        t1.record(st)
-        torch.cuda.synchronize(dev)
+    torch.cuda.synchronize(dev)
+    if dist:
+        dist.barrier()
+    wall0 = time.time()
+    t0.record(st)
+    for _ in range(args.steps):
+        r, _ = step(timed_kernels=True)
+        evs += r
+    t1.record(st)
+    torch.cuda.synchronize(dev)
+    clk.mark(wall0, time.time())
+    clk.stop()
     launches = gb.launch_count() - n_launch0
     ms = t0.elapsed_time(t1) / args.steps
     ms = _max_over_ranks(dist, ms, dev)
@@ -251,6 +270,80 @@ def run_ours(args):
         "aux": aux,
     }
     print(json.dumps(line), flush=True)
+
+
+class _SoloRing:
+    """World of one: no neighbours (the N=1 run of the sequence-sharded step)."""
+
+    rank, world = 0, 1
+
+    def shift(self, send, recv_like, forward):
+        return None
+
+
+def run_seq(args):
+    """--workload C4: BASELINE configs[3] (B=1, H=32, N=131072, d=128, w=2048)
+    sequence-sharded over the ranks (S = N/P contiguous rows each, K/V/u halo
+    r -> r+1 and halo gradients r+1 -> r over NCCL P2P; strong scaling)."""
+    import torch
+
+    import synth
+    from paper_2512_07782_b200 import binding as gb
+    from paper_2512_07782_b200.dist import Ring, cuda_ops, sp_forward_backward
+
+    dist, rank, world, local = _dist()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    peaks = _peaks()
+    c = synth.CONFIGS["C4"]
+    Ng = c["N"]
+    S = Ng // world
+    s = synth.AttnShape(B=c["B"], H=c["H"], N=S, d=c["d"], w=c["w"])
+    seed = c["seed"] + 1000 * rank  # each rank draws its own rows (synthetic data)
+    Q, K, V, dO = synth.attn_inputs(s, seed=seed, device=dev, dtype=torch.bfloat16)
+    h, beta = synth.gate_inputs(s.B, S, s.H, seed=seed, device=dev)
+    h, beta = h.bfloat16(), beta.bfloat16()
+    ring = Ring() if world > 1 else _SoloRing()
+    ops = cuda_ops()
+    st = torch.cuda.current_stream(dev)
+
+    def step():
+        return sp_forward_backward(Q, K, V, h, beta, dO, s.w, ops, ring)
+
+    clk = ClockSampler(local).start()
+    time.sleep(0.3)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    if dist:
+        dist.barrier()
+    n0 = gb.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    wall0 = time.time()
+    e0.record(st)
+    for _ in range(args.steps):
+        step()
+    e1.record(st)
+    torch.cuda.synchronize(dev)
+    clk.mark(wall0, time.time())
+    clk.stop()
+    launches = gb.launch_count() - n0
+    ms = _max_over_ranks(dist, e0.elapsed_time(e1) / args.steps, dev)
+    fl = 14.0 * Ng * s.w * s.d * s.B * s.H  # fwd 4 + bwd 10 (north_star in-window count)
+    tflops = fl / (ms * 1e-3) / 1e12
+    if rank != 0:
+        return
+    print(json.dumps({
+        "metric": METRIC, "value": round(s.B * Ng / (ms * 1e-3), 1), "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (synth.py seeded per rank)",
+        "config": {"workload": "C4 (BASELINE configs[3])", "B": s.B, "H": s.H, "N": Ng, "rows_per_rank": S,
+                   "d": s.d, "w": s.w, "parallelism": f"sequence-sharded x{world} (w-row K/V/u halo, NCCL P2P)",
+                   "l2": "inputs larger than L2, no flush"},
+        "tflops_in_window": round(tflops, 2), "pct_bf16_peak": round(tflops / peaks["bf16"], 4),
+        "gpu_launches": launches, "clocks": clk.summary(),
+    }), flush=True)
 
 
 def _traffic_from_profiles(kind: str):
@@ -380,16 +473,24 @@ def cpu_baseline(args, s):
     import oracle
 
     cores = oracle.num_threads()
-    n_rows = min(s.N, 1024)
-    sub, *arrs = _oracle_sample(s, cores, n_rows)
-    t = time.perf_counter()
-    _oracle_step(sub, *arrs)
-    dt = time.perf_counter() - t
-    # one full token = H heads; the sample covers cores*n_rows head-rows
-    tok_equiv = cores * n_rows / s.H
+    # bounded sample: grow the number of (b, h) slices (full N each) until the
+    # fp64 oracle has run for >= 10 s of wall time or the whole workload is done
+    n_rows = s.N
+    slices, dt, done = cores, 0.0, 0
+    while True:
+        sub, *arrs = _oracle_sample(s, slices, n_rows)
+        t = time.perf_counter()
+        _oracle_step(sub, *arrs)
+        dt = time.perf_counter() - t
+        done = slices
+        if dt >= 10.0 or slices >= s.B * s.H:
+            break
+        slices = min(s.B * s.H, max(slices * 2, int(slices * 10.0 / max(dt, 1e-3))))
+    # one full token = H heads; the sample covers done*n_rows head-rows
+    tok_equiv = done * n_rows / s.H
     return {"value": round(tok_equiv / dt, 3), "unit": "tokens/s", "cores": cores, "kind": "oracle",
-            "sample": f"{cores} (b,h) slices x first {n_rows} tokens of {args.workload} (fp64 C oracle: gate, "
-                      f"fwd, bwd, gate chain), {dt:.2f} s; tokens = head-rows / H"}
+            "sample": f"{done} of {s.B * s.H} (b,h) slices x all {n_rows} tokens of {args.workload} (fp64 C oracle: "
+                      f"gate, fwd, bwd, gate chain), {dt:.2f} s; tokens = head-rows / H"}
 
 
 def run_reference(args):
@@ -431,7 +532,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="C2", choices=["C2", "C3_w128", "C3_w512", "C3_w2048"])
+    ap.add_argument("--workload", default="C2", choices=["C2", "C3_w128", "C3_w512", "C3_w2048", "C4"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU oracle baseline")
     ap.add_argument("--no-aux", action="store_true", help="skip decode/gate-probe line items")
     args = ap.parse_args()
@@ -439,7 +540,7 @@ def main():
     if args.impl == "reference":
         run_reference(args)
     else:
-        run_ours(args)
+        run_seq(args) if args.workload == "C4" else run_ours(args)
 
 
 if __name__ == "__main__":

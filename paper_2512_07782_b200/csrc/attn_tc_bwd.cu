@@ -257,12 +257,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             float ds[32];
             uint32_t pk[16], dk[16];
 #pragma unroll
+            uint32_t sall[32], dall[32];  // all four TMEM loads in flight before one wait
+            tmem_ld32(lane_addr + scol, sall);
+            tmem_ld32(lane_addr + scol + 64, dall);
+            tmem_wait_ld();
+            const bool trw = (n == 4 && threadIdx.x == 0);
+            if (trw) GFWA_TR(43);
             for (int h16 = 0; h16 < 32; h16 += 16) {
-                // 16-column TMEM chunks keep the live register set small
-                uint32_t s16[16], d16[16];
-                tmem_ld16(lane_addr + scol + h16, s16);
-                tmem_ld16(lane_addr + scol + 64 + h16, d16);
-                tmem_wait_ld();
+                const uint32_t* s16 = sall + h16;
+                const uint32_t* d16 = dall + h16;
 #pragma unroll
                 for (int e = 0; e < 16; e += 4) {
                     const float4 c4 = *reinterpret_cast<const float4*>(cq + h16 + e);
@@ -294,6 +297,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
             }
+            if (trw) GFWA_TR(44);
             tmem_st16(lane_addr + scol, pk);       // P^T  over the S^T columns it came from
             tmem_st16(lane_addr + scol + 64, dk);  // dS^T over the dP^T columns
             {  // dS^T row -> smem (128B-swizzled MN-major: row = key, 16-B chunk of 8 queries ^ key%8)
@@ -303,6 +307,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     sts128(sb + (((4 * wg + c) ^ (kr & 7)) * 16),
                            make_uint4(dk[4 * c], dk[4 * c + 1], dk[4 * c + 2], dk[4 * c + 3]));
             }
+            if (trw) GFWA_TR(45);
             // du^q partial over this warp's 32 keys: butterfly transpose-reduce -> lane l holds query 32 wg + l
 #pragma unroll
             for (int sft = 16; sft >= 1; sft >>= 1) {
@@ -315,11 +320,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
             s_red[n & 1][wg][warp & 3][lane] = ds[0];
+            if (trw) GFWA_TR(46);
             tmem_wait_st();
             fence_proxy_async();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&bars->ds_ready[bn]);
+            if (trw) GFWA_TR(47);
             if (n < 8 && threadIdx.x == 0) GFWA_TR(9 + n);
             // du^q_t += rowsum(dS) at key position t + h0 (C-11): combine the WG's 4 warps
             named_bar_sync(1 + wg, 128);
@@ -328,6 +335,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const float rs = s_red[n & 1][wg][0][kr] + s_red[n & 1][wg][1][kr] + s_red[n & 1][wg][2][kr] +
                                  s_red[n & 1][wg][3][kr];
                 if (t < p.Nq) red_add(p.dU + (b * p.H + h) * p.Nkv + t + p.h0, rs);
+                if (trw) GFWA_TR(48);
             }
         }
         {

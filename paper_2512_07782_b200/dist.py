@@ -1,0 +1,162 @@
+"""Sequence-sharded GatedFWA over P ranks (BASELINE.json north_star: long
+sequences "sequence-sharded across the 8 B200s of one box ... a halo of the
+previous w K/V rows plus the running gate-sum offset").
+
+Why this is the whole exchange: the window bounds every dependency to the
+previous w keys, so with w <= S = N/P rows per rank, rank r needs only
+rank r-1's last w K/V rows and their u values; the backward returns the halo's
+dK/dV/dU to rank r-1 and, through the straddle identity, the d-alpha carry.
+
+Frames:
+  * each rank scans its own gates with carry 0:  U_loc[i] = -sum_{q<=i} alpha_q
+    (global U = U_loc - P_r, P_r = sum of earlier ranks' totals; only the
+    optional global U needs the all-gather of totals);
+  * halo u values are sent in the receiver's frame:
+    u_halo = U_loc(r-1)[S-w:] - U_loc(r-1)[S-1]  (exact: the bias only uses
+    differences, and LSE is shift-invariant, C-10);
+  * backward: dU of the halo rows is added into rank r-1's last w rows and the
+    carry for rank r-1's reverse scan is  +sum_j dU_halo(j)  (Appendix A.1:
+    sum_{m >= s_r} dU_m = sum of the straddling dS = -sum_j dU_halo(j)).
+
+The compute backend is injectable (``Ops``): on GPUs it is libgfwa (the CUDA
+path); the CPU multi-process tests inject oracle adapters to check this host
+logic with the gloo backend.  Communication uses torch.distributed P2P
+(NCCL over NVLink on the box).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable
+
+import torch
+import torch.distributed as dist
+
+
+@dataclass
+class Ops:
+    gate_prefix: Callable   # (h, beta, eps) -> U [B,H,S] fp32 (carry 0)
+    fwd: Callable           # (Q, K, V, U, w) -> (O, LSE, O_f32)
+    bwd: Callable           # (Q, K, V, U, O, LSE, dO, w, O_f32) -> (dQ, dK, dV, dU)
+    gate_bwd: Callable      # (dU, h, beta, eps, carry fp64 [B,H] | None) -> (dalpha, dh, dbeta)
+
+
+def cuda_ops() -> Ops:
+    """The libgfwa (CUDA) backend."""
+    from . import binding as gb
+
+    def _fwd(Q, K, V, U, w):
+        return gb.gfwa_fwd(Q, K, V, U, w, want_o_f32=True)
+
+    def _bwd(Q, K, V, U, O, LSE, dO, w, O32):
+        dQ, dK, dV, dU, _ = gb.gfwa_bwd(Q, K, V, U, O, LSE, dO, w, O_f32=O32, want_dalpha=False)
+        return dQ, dK, dV, dU
+
+    def _gate_bwd(dU, h, beta, eps, carry):
+        return gb.gfwa_gate_prefix_bwd(dU, h, beta, eps, carry=carry)
+
+    return Ops(gate_prefix=lambda h, b, eps: gb.gfwa_gate_prefix(h, b, eps), fwd=_fwd, bwd=_bwd,
+               gate_bwd=_gate_bwd)
+
+
+class Ring:
+    """Neighbour exchange on a process group (rank r <-> r+1)."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        # gloo moves host tensors only: stage CUDA tensors through pinned host memory
+        self.stage = dist.get_backend(group) != "nccl"
+
+    def _glob(self, r):
+        return dist.get_global_rank(self.group, r) if self.group is not None else r
+
+    def shift(self, send: list[torch.Tensor] | None, recv_like: list[torch.Tensor] | None, forward: bool):
+        """forward=True: rank r sends to r+1 and receives from r-1 (else the reverse)."""
+        dst = self.rank + 1 if forward else self.rank - 1
+        src = self.rank - 1 if forward else self.rank + 1
+        ops = []
+        recv = None
+        dev = None
+        if send is not None and 0 <= dst < self.world:
+            if self.stage:
+                send = [t.cpu() for t in send]
+            ops += [dist.P2POp(dist.isend, t.contiguous(), self._glob(dst), self.group) for t in send]
+        if recv_like is not None and 0 <= src < self.world:
+            dev = recv_like[0].device
+            recv = [torch.empty_like(t, device="cpu" if self.stage else t.device) for t in recv_like]
+            ops += [dist.P2POp(dist.irecv, t, self._glob(src), self.group) for t in recv]
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+        if recv is not None and self.stage:
+            recv = [t.to(dev) for t in recv]
+        return recv
+
+
+@dataclass
+class ShardResult:
+    O: torch.Tensor
+    LSE: torch.Tensor
+    U_loc: torch.Tensor
+    dQ: torch.Tensor
+    dK: torch.Tensor
+    dV: torch.Tensor
+    dalpha: torch.Tensor
+    dh: torch.Tensor
+    dbeta: torch.Tensor
+
+
+def halo_pack(K, V, U_loc, w: int):
+    """Last w K/V rows and their u in the receiver's frame (U_loc[S-1] -> 0)."""
+    S = K.shape[1]
+    return [K[:, S - w:].contiguous(), V[:, S - w:].contiguous(),
+            (U_loc[..., S - w:] - U_loc[..., S - 1:S]).contiguous()]
+
+
+def global_offset(total: torch.Tensor, ring: Ring) -> torch.Tensor:
+    """P_r = sum of the earlier ranks' gate totals (exclusive scan, fp64)."""
+    allt = [torch.empty_like(total) for _ in range(ring.world)]
+    dist.all_gather(allt, total.contiguous(), group=ring.group)
+    out = torch.zeros_like(total)
+    for r in range(ring.rank):
+        out += allt[r]
+    return out
+
+
+def sp_forward_backward(Q, K, V, h, beta, dO, w: int, ops: Ops, ring: Ring, eps: float = 1e-6) -> ShardResult:
+    """One sequence-sharded training step on this rank's S rows.
+
+    Q, K, V, dO [B,S,H,d]; h, beta [B,S,H] (this rank's contiguous rows).
+    Requires w <= S (one-hop halo)."""
+    S = K.shape[1]
+    if w > S:
+        raise ValueError(f"sequence sharding needs w <= rows per rank ({w} > {S})")
+    r, P = ring.rank, ring.world
+    U_loc = ops.gate_prefix(h, beta, eps)
+    # forward halo r -> r+1 (K, V, u in the receiver's frame)
+    like = halo_pack(K, V, U_loc, w)
+    recv = ring.shift(like if r < P - 1 else None, like, forward=True)
+    if recv is not None:
+        Kx = torch.cat([recv[0], K], 1)
+        Vx = torch.cat([recv[1], V], 1)
+        Ux = torch.cat([recv[2], U_loc], -1).contiguous()
+        h0 = w
+    else:
+        Kx, Vx, Ux, h0 = K, V, U_loc, 0
+    O, LSE, O32 = ops.fwd(Q, Kx, Vx, Ux, w)
+    dQ, dKx, dVx, dUx = ops.bwd(Q, Kx, Vx, Ux, O, LSE, dO, w, O32)
+    # backward halo r -> r-1: gradients of the halo rows
+    back_like = [dKx[:, :w], dVx[:, :w], dUx[..., :w]] if h0 else [dKx[:, :w], dVx[:, :w], dUx[..., :w]]
+    back = ring.shift([t.contiguous() for t in back_like] if h0 else None, back_like, forward=False)
+    dK = dKx[:, h0:].contiguous()
+    dV = dVx[:, h0:].contiguous()
+    dU = dUx[..., h0:].contiguous()
+    carry = None
+    if back is not None:
+        dK[:, S - w:] += back[0]
+        dV[:, S - w:] += back[1]
+        dU[..., S - w:] += back[2]
+        carry = back[2].double().sum(-1)  # d-alpha carry = +sum_j dU_halo(j)
+    dalpha, dh, dbeta = ops.gate_bwd(dU, h, beta, eps, carry)
+    return ShardResult(O, LSE, U_loc, dQ, dK, dV, dalpha, dh, dbeta)

@@ -1,0 +1,110 @@
+"""Multi-process CPU test of the sequence-sharded orchestration
+(paper_2512_07782_b200.dist) with the gloo backend, world_size 2 and 3.
+
+The compute backend is injected with fp64 oracle adapters (test-only), so the
+check isolates the host logic: halo slicing, the receiver-frame u values, the
+reverse halo of dK/dV/dU and the d-alpha carry.  Every rank's outputs must
+equal the matching rows of the unsharded oracle run."""
+import os
+import tempfile
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+
+
+def _oracle_ops():
+    from paper_2512_07782_b200.dist import Ops
+
+    t = lambda a: torch.from_numpy(np.asarray(a))  # noqa: E731
+
+    def gate_prefix(h, beta, eps):
+        return t(oracle.gate_prefix_hbeta(h, beta, eps)[0])
+
+    def fwd(Q, K, V, U, w):
+        O, L = oracle.fwd(Q, K, V, U, w)
+        return t(O), t(L), None
+
+    def bwd(Q, K, V, U, O, LSE, dO, w, O32):
+        g = oracle.bwd(Q, K, V, U, dO, w, want_dalpha=False)
+        return t(g["dQ"]), t(g["dK"]), t(g["dV"]), t(g["dU"])
+
+    def gate_bwd(dU, h, beta, eps, carry):
+        da = oracle.dalpha_scan(dU, None if carry is None else carry.numpy())
+        dh, db = oracle.gate_chain(h, beta, da, eps)
+        return t(da), t(dh), t(db)
+
+    return Ops(gate_prefix=gate_prefix, fwd=fwd, bwd=bwd, gate_bwd=gate_bwd)
+
+
+def _inputs(B, N, H, d, seed):
+    g = torch.Generator().manual_seed(seed)
+    Q = torch.randn(B, N, H, d, generator=g, dtype=torch.float64)
+    K = torch.randn(B, N, H, d, generator=g, dtype=torch.float64)
+    V = torch.randn(B, N, H, d, generator=g, dtype=torch.float64)
+    dO = torch.randn(B, N, H, d, generator=g, dtype=torch.float64)
+    h = torch.randn(B, N, H, generator=g, dtype=torch.float64)
+    beta = 1.0 + torch.nn.functional.elu(0.5 * torch.randn(B, N, H, generator=g, dtype=torch.float64))
+    return Q, K, V, dO, h, beta
+
+
+def _worker(rank, world, port, outdir, B, N, H, d, w):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2512_07782_b200.dist import Ring, sp_forward_backward
+
+        Q, K, V, dO, h, beta = _inputs(B, N, H, d, 5)
+        S = N // world
+        sl = slice(rank * S, (rank + 1) * S)
+        res = sp_forward_backward(Q[:, sl], K[:, sl], V[:, sl], h[:, sl], beta[:, sl], dO[:, sl], w, _oracle_ops(),
+                                  Ring())
+        torch.save({k: getattr(res, k) for k in ("O", "LSE", "U_loc", "dQ", "dK", "dV", "dalpha", "dh", "dbeta")},
+                   os.path.join(outdir, f"r{rank}.pt"))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,N,w", [(2, 48, 10), (2, 40, 20), (3, 60, 7)])
+def test_sequence_sharded_matches_unsharded(world, N, w):
+    B, H, d = 1, 2, 8
+    port = 29500 + (os.getpid() % 2000)
+    with tempfile.TemporaryDirectory() as outdir:
+        mp.spawn(_worker, args=(world, port, outdir, B, N, H, d, w), nprocs=world, join=True)
+        Q, K, V, dO, h, beta = _inputs(B, N, H, d, 5)
+        U, _, _ = oracle.gate_prefix_hbeta(h, beta)
+        O, L = oracle.fwd(Q, K, V, U, w)
+        g = oracle.bwd(Q, K, V, U, dO, w)
+        dh, db = oracle.gate_chain(h, beta, g["dalpha"])
+        S = N // world
+        for r in range(world):
+            res = torch.load(os.path.join(outdir, f"r{r}.pt"))
+            sl = slice(r * S, (r + 1) * S)
+            assert np.allclose(res["O"].numpy(), O[:, sl], atol=1e-12)
+            assert np.allclose(res["LSE"].numpy(), L[..., sl], atol=1e-11)
+            assert np.allclose(res["dQ"].numpy(), g["dQ"][:, sl], atol=1e-11)
+            assert np.allclose(res["dK"].numpy(), g["dK"][:, sl], atol=1e-11)
+            assert np.allclose(res["dV"].numpy(), g["dV"][:, sl], atol=1e-11)
+            assert np.allclose(res["dalpha"].numpy(), g["dalpha"][..., sl], atol=1e-10)
+            assert np.allclose(res["dh"].numpy(), dh[:, sl], atol=1e-10)
+            assert np.allclose(res["dbeta"].numpy(), db[:, sl], atol=1e-10)
+            # local frame: global U = U_loc - (earlier ranks' totals)
+            off = U[..., r * S - 1] if r > 0 else 0.0
+            assert np.allclose(res["U_loc"].numpy() + (off[..., None] if r > 0 else 0.0), U[..., sl], atol=1e-11)
+
+
+def test_halo_larger_than_shard_is_rejected():
+    from paper_2512_07782_b200.dist import Ops, sp_forward_backward
+
+    class _R:
+        rank, world = 0, 2
+
+    Q = torch.zeros(1, 4, 1, 8)
+    with pytest.raises(ValueError):
+        sp_forward_backward(Q, Q, Q, Q[..., 0, 0:1].squeeze(-1), Q[..., 0, 0:1].squeeze(-1), Q, 5,
+                            Ops(None, None, None, None), _R())

@@ -18,3 +18,7 @@ for n in (0, 1, 2, 4):
 stat("last MMA2 -> dkdv_full", t[:, 41] - np.nanmax(m2, axis=1))
 stat("epilogue", t[:, 42] - t[:, 41])
 stat("total", t[:, 42] - start)
+s4 = t[:, 1 + 4]
+for name, a, b in (("st_full->LDTM done", s4, t[:, 43]), ("compute", t[:, 43], t[:, 44]), ("STTM+STS", t[:, 44], t[:, 45]),
+                   ("butterfly", t[:, 45], t[:, 46]), ("wait_st+fence+arrive", t[:, 46], t[:, 47]), ("combine", t[:, 47], t[:, 48])):
+    stat("step4 sg: " + name, b - a)
