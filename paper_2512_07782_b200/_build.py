@@ -72,7 +72,9 @@ def build(force: bool = False, verbose: bool = False, extra: list[str] | None = 
         for _, log in results:
             sys.stderr.write(log)
     tmp = out + f".tmp{os.getpid()}"
-    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *[o for o, _ in results], "-lcuda"]
+    # no -lcuda: driver entry points are resolved at run time (csrc/driver_api.cuh),
+    # so the library also loads on hosts without a driver
+    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *[o for o, _ in results]]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")

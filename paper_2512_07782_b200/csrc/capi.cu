@@ -5,6 +5,7 @@
 #include <cmath>
 
 #include "attn_common.cuh"
+#include "driver_api.cuh"
 
 namespace gfwa {
 
@@ -77,10 +78,10 @@ gfwa_status_t make_params(const gfwa_attn_desc_t* d, AttnParams& p) {
 // driver call, so bind the context that owns the caller's data first.
 void bind_context(const void* dev_ptr) {
     CUcontext cur = nullptr;
-    if (cuCtxGetCurrent(&cur) == CUDA_SUCCESS && cur) return;
+    if (drv::ctxGetCurrent(&cur) == CUDA_SUCCESS && cur) return;
     CUcontext ctx = nullptr;
-    if (cuPointerGetAttribute(&ctx, CU_POINTER_ATTRIBUTE_CONTEXT, (CUdeviceptr)dev_ptr) == CUDA_SUCCESS && ctx)
-        cuCtxSetCurrent(ctx);
+    if (drv::pointerGetAttribute(&ctx, CU_POINTER_ATTRIBUTE_CONTEXT, (CUdeviceptr)dev_ptr) == CUDA_SUCCESS && ctx)
+        drv::ctxSetCurrent(ctx);
 }
 
 bool strides_ok(const int64_t* s, size_t esize) {

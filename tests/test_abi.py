@@ -69,7 +69,7 @@ def test_null_pointers_rejected():
     assert lib.gfwa_fwd(ctypes.byref(d), None, None, None, None, None, None, None, None) in (1, 2)
     assert lib.gfwa_gate_prefix(0, 0, None, None, 1, 1, 1, 1e-6, None, None, None, None, 0, None) == 1
     dd = gb.DecodeDesc()
-    assert lib.gfwa_decode(ctypes.byref(dd), *([None] * 12), 0, None) == 1
+    assert lib.gfwa_decode(ctypes.byref(dd), *([None] * 11), 0, None) == 1
 
 
 def test_workspace_sizes_scale_with_problem():
