@@ -5,35 +5,41 @@
 // (P:271), every (b, head-group, chunk) tile is an independent CTA and the
 // carry is resolved with a single-pass *decoupled look-back*.  h and beta are
 // read once and U written once (the paper's I/O claim), all accesses
-// coalesced:
+// coalesced and vectorised:
 //   load    [T tokens x HG heads] tile of h, beta ([B,N,H], H contiguous),
-//           one batch of independent loads per thread (1024 threads)
+//           4 heads per load, one batch of independent loads per thread
 //   alpha   softplus(beta h)/(beta + eps) in fp32 -> smem [HG][T] (transpose,
 //           one pad word per lane run so the run reads are conflict-free)
-//   scan    one warp per head; lane l owns a run of R = T/32 tokens: serial
-//           fp32 prefix, run totals scanned across the warp in fp64
+//   scan    a warp owns HG/8 heads; lane l owns a run of R = T/32 tokens:
+//           serial fp32 prefix, run totals scanned across the warp in fp64
 //   carry   chunk aggregate published as one 64-bit word (fp64 value with the
 //           2-bit status in its lowest mantissa bits: a single relaxed load
-//           observes value and status together); all 32 heads look back
-//           concurrently, 32 predecessors per round
+//           observes value and status together); a warp looks back for all
+//           its heads at once, 32/(heads per warp) predecessors per round
 //   store   U [B,H,N] rows (N contiguous), 16-byte vector stores
-// The head-group size is a template parameter (power of two), so all tile
-// index math is shifts and masks.  The backward runs the same machinery right
-// to left on dU and fuses the chain rule into dh, dbeta.
+// 256-thread CTAs, 4 resident per SM, so one CTA's load phase overlaps the
+// others' scan and store phases (one 1024-thread CTA per SM left the memory
+// system idle during the scan: 0.38 TB/s).  The head-group size is a template
+// parameter (power of two), so all tile index math is shifts and masks.  The
+// backward runs the same machinery right to left on dU and fuses the
+// chain rule into dh, dbeta.
 #include <algorithm>
+#include <type_traits>
 
 #include "common.cuh"
 
 namespace gfwa {
 namespace {
 
-constexpr int kThreads = 1024;  // 32 warps: one per head of the group
+constexpr int kThreads = 256;  // 8 warps
 constexpr int kWarps = kThreads / 32;
+constexpr int kMinBlocks = 4;  // resident CTAs per SM (64 registers / thread)
+constexpr unsigned kFull = 0xffffffffu;
 
 struct ScanGeom {
     int HG;        // heads per CTA (<= 32)
     int log_hgp;   // log2 of the head-group slot count (power of two >= HG)
-    int log_t;     // log2 tokens per chunk (T >= 64)
+    int log_t;     // log2 tokens per chunk (128 <= T <= 1024, so 4 <= R <= 32)
     int n_hgroups; // ceil(H / HG)
     int n_chunks;  // ceil(N / T)
 };
@@ -43,11 +49,13 @@ ScanGeom scan_geom(int64_t B, int64_t N, int64_t H) {
     g.HG = H >= 32 ? 32 : (int)H;
     g.log_hgp = 0;
     while ((1 << g.log_hgp) < g.HG) ++g.log_hgp;
-    g.log_t = 13 - g.log_hgp;  // T * HGP = 8192 elements per tile
+    g.log_t = std::min(10, 13 - g.log_hgp);  // T * HGP <= 8192 elements per tile
     g.n_hgroups = (int)((H + g.HG - 1) / g.HG);
     // small problems: shorter chunks so every SM streams (the look-back makes
     // the chunk count free)
-    while (g.log_t > 6 && (int64_t)g.n_hgroups * ((N + (1 << g.log_t) - 1) >> g.log_t) * B < 2 * 148) --g.log_t;
+    while (g.log_t > 7 &&
+           (int64_t)g.n_hgroups * ((N + (1 << g.log_t) - 1) >> g.log_t) * B < kMinBlocks * 148)
+        --g.log_t;
     g.n_chunks = (int)((N + (1 << g.log_t) - 1) >> g.log_t);
     return g;
 }
@@ -84,55 +92,94 @@ __device__ __forceinline__ void publish(unsigned long long* p, double v, unsigne
     st_relaxed_u64(p, ((unsigned long long)__double_as_longlong(v) & ~3ull) | status);
 }
 
-__device__ __forceinline__ double warp_sum_d(double v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
-
-// Exclusive prefix over chunks 0..c-1 of this (sequence, head): warp-parallel
-// decoupled look-back, 32 predecessors per round.  Whole warp calls.
-__device__ double lookback(const unsigned long long* d, int c) {
+// Exclusive prefixes over chunks 0..c-1 (in processing order) for the HPW
+// heads j0, j0 + 8, ... a warp owns: the lanes form HPW groups of LPH =
+// 32/HPW, group i walks back over head j_i's descriptors LPH predecessors per
+// round until it meets an inclusive prefix.  Every lane returns its group's
+// prefix.  d points at (this sequence/head-group, chunk 0, head 0).  Whole
+// warp calls.
+template <int HPW>
+__device__ double lookback(const unsigned long long* d, int c, int j0, int nh) {
+    constexpr int LPH = 32 / HPW;
     const int lane = threadIdx.x & 31;
+    const int gi = lane / LPH, p = lane % LPH;
+    const int j = j0 + kWarps * gi;
+    const unsigned gmask = LPH == 32 ? kFull : (((1u << (LPH & 31)) - 1u) << (gi * LPH));
     double excl = 0.0;
     int pc = c - 1;
-    while (pc >= 0) {
-        const int q = pc - lane;
+    bool done = j >= nh || c == 0;  // uniform within a group
+    while (__any_sync(kFull, !done)) {
+        const int q = pc - p;
+        const bool act = !done && q >= 0;
         unsigned long long w = 0;
-        if (q >= 0) {
+        if (act) {
             do {
-                w = ld_relaxed_u64(d + (size_t)q * 32);
+                w = ld_relaxed_u64(d + (size_t)q * 32 + j);
             } while ((w & 3ull) == 0);
         }
-        const unsigned st = (unsigned)(w & 3ull);
-        const double v = q >= 0 ? __longlong_as_double((long long)(w & ~3ull)) : 0.0;
-        const unsigned pmask = __ballot_sync(0xffffffffu, q >= 0 && st == 2);
-        if (pmask) {
-            const int first = __ffs(pmask) - 1;  // closest chunk with an inclusive prefix
-            excl += warp_sum_d(lane <= first ? v : 0.0);
-            break;
-        }
-        excl += warp_sum_d(v);
-        pc -= 32;
+        const unsigned incl = __ballot_sync(kFull, act && (w & 3ull) == 2) & gmask;
+        double v = act ? __longlong_as_double((long long)(w & ~3ull)) : 0.0;
+        if (incl && p > __ffs(incl) - 1 - gi * LPH) v = 0.0;  // beyond the closest inclusive prefix
+#pragma unroll
+        for (int o = LPH / 2; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+        if (!done) excl += v;
+        done = done || incl != 0 || pc < LPH;
+        pc -= LPH;
     }
     return excl;
+}
+
+// 4 consecutive elements <-> fp32 (8-byte bf16 / 16-byte fp32 accesses)
+template <typename Tin>
+using Raw4 = std::conditional_t<sizeof(Tin) == 2, uint2, float4>;
+__device__ __forceinline__ void unpack4(uint2 r, float (&v)[4]) {
+    v[0] = __uint_as_float(r.x << 16);
+    v[1] = __uint_as_float(r.x & 0xffff0000u);
+    v[2] = __uint_as_float(r.y << 16);
+    v[3] = __uint_as_float(r.y & 0xffff0000u);
+}
+__device__ __forceinline__ void unpack4(float4 r, float (&v)[4]) {
+    v[0] = r.x;
+    v[1] = r.y;
+    v[2] = r.z;
+    v[3] = r.w;
+}
+__device__ __forceinline__ void store4(__nv_bfloat16* p, const float (&v)[4]) {
+    __nv_bfloat162 r[2] = {__floats2bfloat162_rn(v[0], v[1]), __floats2bfloat162_rn(v[2], v[3])};
+    *reinterpret_cast<uint2*>(p) = *reinterpret_cast<const uint2*>(r);
+}
+__device__ __forceinline__ void store4(float* p, const float (&v)[4]) {
+    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
 }
 
 template <typename Tin>
 __device__ __forceinline__ float load_in(const Tin* p) { return to_f32<Tin>(*p); }
 
+// alpha_t = softplus(beta_t h_t) / (beta_t + eps)  (Eq. 9, Alg. 1 l.6)
+__device__ __forceinline__ float alpha_of(float hv, float bv, float eps) {
+    return __fdividef(softplus_fast(bv * hv), bv + eps);
+}
+
 // smem index of token tt in a head row: one pad word per run of R tokens
 __device__ __forceinline__ int sk(int tt, int log_r) { return tt + (tt >> log_r); }
+
+// vectorised [B,N,H] tile access: all HGP heads present, rows 4-aligned
+template <int HGP, typename Tin>
+__device__ __forceinline__ bool tile_vec_ok(int nh, int64_t H, const Tin* a, const Tin* b) {
+    return HGP >= 4 && nh == HGP && (H & 3) == 0 && ((uintptr_t)a % (4 * sizeof(Tin))) == 0 &&
+           (b == nullptr || ((uintptr_t)b % (4 * sizeof(Tin))) == 0);
+}
 
 // ---------------------------------------------------------------- forward
 
 template <typename Tin, bool kAlphaIn, int LOG_HGP>
-__global__ void __launch_bounds__(kThreads) gate_prefix_kernel(
+__global__ void __launch_bounds__(kThreads, kMinBlocks) gate_prefix_kernel(
     const Tin* __restrict__ h, const Tin* __restrict__ beta, int64_t N, int64_t H, float eps,
     const double* __restrict__ carry_in, float* __restrict__ U, double* __restrict__ total, Lookback lb,
     ScanGeom g) {
     constexpr int HGP = 1 << LOG_HGP;
-    extern __shared__ float sA[];  // [HGP][pitch]
+    constexpr int HPW = HGP > kWarps ? HGP / kWarps : 1;  // heads per warp
+    extern __shared__ float sA[];                         // [HGP][pitch]
     __shared__ unsigned s_ticket;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) s_ticket = atomicAdd(lb.ticket, 1u);
@@ -151,78 +198,127 @@ __global__ void __launch_bounds__(kThreads) gate_prefix_kernel(
 
     // 1. tile load, alpha in fp32 (Alg. 1 l.4-7)
     const int64_t row0 = ((int64_t)b * N + t0) * H + hh0;
-    constexpr int kB = 8;
-    for (int e0 = tid; e0 < T * HGP; e0 += kThreads * kB) {
-        float hv[kB], bv[kB];
+    if (tile_vec_ok<HGP>(nh, H, h, kAlphaIn ? nullptr : beta)) {
+        constexpr int LOG_G4 = LOG_HGP >= 2 ? LOG_HGP - 2 : 0;  // 4-head groups per token
+        constexpr int kV = 8 / (int)sizeof(Tin);              // groups per thread per batch (64 B in flight)
+        const int ngrp = T << LOG_G4;
+        for (int e0 = tid; e0 < ngrp; e0 += kThreads * kV) {
+            Raw4<Tin> rh[kV], rb[kV];
 #pragma unroll
-        for (int k = 0; k < kB; ++k) {
-            const int e = e0 + k * kThreads;
-            const int tt = e >> LOG_HGP, j = e & (HGP - 1);
-            hv[k] = 0.f;
-            bv[k] = 1.f;
-            if (e < T * HGP && tt < nt && j < nh) {
-                const int64_t i = row0 + (int64_t)tt * H + j;
-                hv[k] = load_in(h + i);
-                if (!kAlphaIn) bv[k] = load_in(beta + i);
+            for (int k = 0; k < kV; ++k) {
+                const int e = e0 + k * kThreads;
+                const int tt = e >> LOG_G4, j4 = e & ((1 << LOG_G4) - 1);
+                if (e < ngrp && tt < nt) {
+                    const int64_t i = row0 + (int64_t)tt * H + 4 * j4;
+                    rh[k] = *reinterpret_cast<const Raw4<Tin>*>(h + i);
+                    if (!kAlphaIn) rb[k] = *reinterpret_cast<const Raw4<Tin>*>(beta + i);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < kV; ++k) {
+                const int e = e0 + k * kThreads;
+                const int tt = e >> LOG_G4, j4 = e & ((1 << LOG_G4) - 1);
+                if (e >= ngrp) continue;
+                float hv[4], bv[4], a[4];
+                unpack4(rh[k], hv);
+                if (!kAlphaIn) unpack4(rb[k], bv);
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    a[i] = tt >= nt ? 0.f : kAlphaIn ? hv[i] : alpha_of(hv[i], bv[i], eps);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) sA[(4 * j4 + i) * pitch + sk(tt, log_r)] = a[i];
             }
         }
+    } else {
+        constexpr int kB = 4;
+        for (int e0 = tid; e0 < T * HGP; e0 += kThreads * kB) {
+            float hv[kB], bv[kB];
 #pragma unroll
-        for (int k = 0; k < kB; ++k) {
-            const int e = e0 + k * kThreads;
-            const int tt = e >> LOG_HGP, j = e & (HGP - 1);
-            if (e < T * HGP) {
-                float a = 0.f;
-                if (tt < nt && j < nh) a = kAlphaIn ? hv[k] : __fdividef(softplus_fast(bv[k] * hv[k]), bv[k] + eps);
-                sA[j * pitch + sk(tt, log_r)] = a;
+            for (int k = 0; k < kB; ++k) {
+                const int e = e0 + k * kThreads;
+                const int tt = e >> LOG_HGP, j = e & (HGP - 1);
+                hv[k] = 0.f;
+                bv[k] = 1.f;
+                if (e < T * HGP && tt < nt && j < nh) {
+                    const int64_t i = row0 + (int64_t)tt * H + j;
+                    hv[k] = load_in(h + i);
+                    if (!kAlphaIn) bv[k] = load_in(beta + i);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < kB; ++k) {
+                const int e = e0 + k * kThreads;
+                const int tt = e >> LOG_HGP, j = e & (HGP - 1);
+                if (e < T * HGP) {
+                    float a = 0.f;
+                    if (tt < nt && j < nh) a = kAlphaIn ? hv[k] : alpha_of(hv[k], bv[k], eps);
+                    sA[j * pitch + sk(tt, log_r)] = a;
+                }
             }
         }
     }
     __syncthreads();
-    const int j = warp;  // one head per warp
-    if (j >= nh) return;
 
-    // 2. lane runs (fp32), their exclusive scan across the warp (fp64), chunk
-    //    aggregate published, look-back, inclusive published
-    const float* row = sA + j * pitch + lane * (R + 1);
-    float run = 0.f;
-    for (int k = 0; k < R; ++k) run += row[k];
-    double x = (double)run;
+    // 2. lane runs (fp32), their inclusive scan across the warp (fp64), chunk
+    //    aggregates published, look-back, inclusive prefixes published
+    unsigned long long* d = lb.desc + (size_t)(b * g.n_hgroups + hg) * g.n_chunks * 32;
+    float run[HPW];
+    double xs[HPW];
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const double y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-    }
-    const double agg = __shfl_sync(0xffffffffu, x, 31);
-    unsigned long long* d = lb.desc + ((size_t)(b * g.n_hgroups + hg) * g.n_chunks) * 32 + j;
-    if (lane == 0) publish(d + (size_t)c * 32, agg, c == 0 ? 2u : 1u);
-    const double excl = c == 0 ? 0.0 : lookback(d, c);
-    if (lane == 0) {
-        if (c > 0) publish(d + (size_t)c * 32, excl + agg, 2u);
-        if (total && c == g.n_chunks - 1) total[(int64_t)b * H + hh0 + j] = excl + agg;
-    }
-    // 3. U_t = carry - (prefix before this run) - (in-run fp32 prefix)  (Alg. 1 l.8-9)
-    const double carry = carry_in ? carry_in[(int64_t)b * H + hh0 + j] : 0.0;
-    const float cbase = (float)(carry - (excl + x - (double)run));
-    float* urow = U + ((int64_t)b * H + hh0 + j) * N + t0 + lane * R;
-    const int tl = lane * R;
-    float acc = 0.f;
-    if (tl + R <= nt && (R & 3) == 0 && ((uintptr_t)urow & 15) == 0) {
-        for (int k = 0; k < R; k += 4) {
-            float4 o;
-            acc += row[k];
-            o.x = cbase - acc;
-            acc += row[k + 1];
-            o.y = cbase - acc;
-            acc += row[k + 2];
-            o.z = cbase - acc;
-            acc += row[k + 3];
-            o.w = cbase - acc;
-            *reinterpret_cast<float4*>(urow + k) = o;
+    for (int i = 0; i < HPW; ++i) {
+        const int j = warp + kWarps * i;
+        run[i] = 0.f;
+        if (j < nh) {
+            const float* row = sA + j * pitch + lane * (R + 1);
+            for (int k = 0; k < R; ++k) run[i] += row[k];
         }
-    } else {
-        for (int k = 0; k < R; ++k) {
-            acc += row[k];
-            if (tl + k < nt) urow[k] = cbase - acc;
+        double x = (double)run[i];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double y = __shfl_up_sync(kFull, x, o);
+            if (lane >= o) x += y;
+        }
+        xs[i] = x;
+        const double agg = __shfl_sync(kFull, x, 31);
+        if (lane == 0 && j < nh) publish(d + (size_t)c * 32 + j, agg, c == 0 ? 2u : 1u);
+    }
+    const double ex = lookback<HPW>(d, c, warp, nh);
+
+    // 3. U_t = carry - (prefix before this run) - (in-run fp32 prefix)  (Alg. 1 l.8-9)
+    const int tl = lane * R;
+#pragma unroll
+    for (int i = 0; i < HPW; ++i) {
+        const int j = warp + kWarps * i;
+        if (j >= nh) continue;  // warp-uniform
+        const double excl = __shfl_sync(kFull, ex, i * (32 / HPW));
+        const double agg = __shfl_sync(kFull, xs[i], 31);
+        if (lane == 0) {
+            if (c > 0) publish(d + (size_t)c * 32 + j, excl + agg, 2u);
+            if (total && c == g.n_chunks - 1) total[(int64_t)b * H + hh0 + j] = excl + agg;
+        }
+        const double carry = carry_in ? carry_in[(int64_t)b * H + hh0 + j] : 0.0;
+        const float cbase = (float)(carry - (excl + xs[i] - (double)run[i]));
+        const float* row = sA + j * pitch + lane * (R + 1);
+        float* urow = U + ((int64_t)b * H + hh0 + j) * N + t0 + tl;
+        float acc = 0.f;
+        if (tl + R <= nt && ((uintptr_t)urow & 15) == 0) {
+            for (int k = 0; k < R; k += 4) {
+                float4 o;
+                acc += row[k];
+                o.x = cbase - acc;
+                acc += row[k + 1];
+                o.y = cbase - acc;
+                acc += row[k + 2];
+                o.z = cbase - acc;
+                acc += row[k + 3];
+                o.w = cbase - acc;
+                *reinterpret_cast<float4*>(urow + k) = o;
+            }
+        } else {
+            for (int k = 0; k < R; ++k) {
+                acc += row[k];
+                if (tl + k < nt) urow[k] = cbase - acc;
+            }
         }
     }
 }
@@ -230,11 +326,12 @@ __global__ void __launch_bounds__(kThreads) gate_prefix_kernel(
 // ---------------------------------------------------------------- backward
 
 template <typename Tin, bool kAlphaIn, int LOG_HGP>
-__global__ void __launch_bounds__(kThreads) gate_prefix_bwd_kernel(
+__global__ void __launch_bounds__(kThreads, kMinBlocks) gate_prefix_bwd_kernel(
     const Tin* __restrict__ h, const Tin* __restrict__ beta, int64_t N, int64_t H, float eps,
     const float* __restrict__ dU, const double* __restrict__ carry, float* __restrict__ dalpha,
     Tin* __restrict__ dh, Tin* __restrict__ dbeta, Lookback lb, ScanGeom g) {
     constexpr int HGP = 1 << LOG_HGP;
+    constexpr int HPW = HGP > kWarps ? HGP / kWarps : 1;
     extern __shared__ float sA[];  // [HGP][pitch]
     __shared__ unsigned s_ticket;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -252,57 +349,153 @@ __global__ void __launch_bounds__(kThreads) gate_prefix_bwd_kernel(
     const int hh0 = hg * g.HG;
     const int nh = min(g.HG, (int)(H - hh0));
     const int nt = (int)min64(T, N - t0);
+    const int tl = lane * R;
 
-    // 1. dU rows (N contiguous) -> smem, one batch of independent loads
-    constexpr int kB = 8;
-    for (int e0 = tid; e0 < T * HGP; e0 += kThreads * kB) {
-        float v[kB];
+    // 1. dU rows (N contiguous): lane l's run of R tokens straight into its
+    //    smem run (16-byte loads when aligned; conflict-free stores)
+#pragma unroll 1
+    for (int i = 0; i < HPW; ++i) {
+        const int j = warp + kWarps * i;
+        if (j >= nh) continue;
+        const float* src = dU + ((int64_t)b * H + hh0 + j) * N + t0 + tl;
+        float* row = sA + j * pitch + lane * (R + 1);
+        if (tl + R <= nt && ((uintptr_t)src & 15) == 0) {
+            float4 v[8];
 #pragma unroll
-        for (int k = 0; k < kB; ++k) {
-            const int e = e0 + k * kThreads;
-            const int j = e >> g.log_t, tt = e & (T - 1);
-            v[k] = (e < T * HGP && tt < nt && j < nh) ? dU[((int64_t)b * H + hh0 + j) * N + t0 + tt] : 0.f;
-        }
+            for (int k = 0; k < 8; ++k)
+                if (4 * k < R) v[k] = *reinterpret_cast<const float4*>(src + 4 * k);
 #pragma unroll
-        for (int k = 0; k < kB; ++k) {
-            const int e = e0 + k * kThreads;
-            if (e < T * HGP) sA[(e >> g.log_t) * pitch + sk(e & (T - 1), log_r)] = v[k];
+            for (int k = 0; k < 8; ++k)
+                if (4 * k < R) {
+                    row[4 * k] = v[k].x;
+                    row[4 * k + 1] = v[k].y;
+                    row[4 * k + 2] = v[k].z;
+                    row[4 * k + 3] = v[k].w;
+                }
+        } else {
+            for (int k = 0; k < R; ++k) row[k] = tl + k < nt ? src[k] : 0.f;
         }
     }
-    __syncthreads();
-    const int j = warp;
-    if (j < nh) {
-        // 2. reverse scan: dalpha_t = carry - sum_{t' >= t} dU_t'  (suffix sums)
-        float* row = sA + j * pitch + lane * (R + 1);
-        float run = 0.f;
-        for (int k = 0; k < R; ++k) run += row[k];
-        double x = (double)run;  // inclusive suffix scan of the lane runs
+    __syncwarp();
+
+    // 2. reverse scan: dalpha_t = carry - sum_{t' >= t} dU_t'  (suffix sums)
+    unsigned long long* d = lb.desc + (size_t)(b * g.n_hgroups + hg) * g.n_chunks * 32;
+    float run[HPW];
+    double xs[HPW];
+#pragma unroll
+    for (int i = 0; i < HPW; ++i) {
+        const int j = warp + kWarps * i;
+        run[i] = 0.f;
+        if (j < nh) {
+            const float* row = sA + j * pitch + lane * (R + 1);
+            for (int k = 0; k < R; ++k) run[i] += row[k];
+        }
+        double x = (double)run[i];  // inclusive suffix scan of the lane runs
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const double y = __shfl_down_sync(0xffffffffu, x, o);
+            const double y = __shfl_down_sync(kFull, x, o);
             if (lane + o < 32) x += y;
         }
-        const double agg = __shfl_sync(0xffffffffu, x, 0);
-        unsigned long long* d = lb.desc + ((size_t)(b * g.n_hgroups + hg) * g.n_chunks) * 32 + j;
-        if (lane == 0) publish(d + (size_t)rc * 32, agg, rc == 0 ? 2u : 1u);
-        const double excl = rc == 0 ? 0.0 : lookback(d, rc);
-        if (lane == 0 && rc > 0) publish(d + (size_t)rc * 32, excl + agg, 2u);
+        xs[i] = x;
+        const double agg = __shfl_sync(kFull, x, 0);
+        if (lane == 0 && j < nh) publish(d + (size_t)rc * 32 + j, agg, rc == 0 ? 2u : 1u);
+    }
+    const double ex = lookback<HPW>(d, rc, warp, nh);
+#pragma unroll
+    for (int i = 0; i < HPW; ++i) {
+        const int j = warp + kWarps * i;
+        if (j >= nh) continue;  // warp-uniform
+        const double excl = __shfl_sync(kFull, ex, i * (32 / HPW));
+        const double agg = __shfl_sync(kFull, xs[i], 0);
+        if (lane == 0 && rc > 0) publish(d + (size_t)rc * 32 + j, excl + agg, 2u);
         const double cr = carry ? carry[(int64_t)b * H + hh0 + j] : 0.0;
-        const float cbase = (float)(cr - (excl + x - (double)run));
-        float* arow = dalpha ? dalpha + ((int64_t)b * H + hh0 + j) * N + t0 + lane * R : nullptr;
-        const int tl = lane * R;
+        const float cbase = (float)(cr - (excl + xs[i] - (double)run[i]));
+        float* row = sA + j * pitch + lane * (R + 1);
+        float* arow = dalpha ? dalpha + ((int64_t)b * H + hh0 + j) * N + t0 + tl : nullptr;
         float acc = 0.f;
-        for (int k = R - 1; k >= 0; --k) {
-            acc += row[k];
-            const float da = cbase - acc;
-            row[k] = da;  // kept for the chain rule
-            if (arow && tl + k < nt) arow[k] = da;
+        if (arow && tl + R <= nt && ((uintptr_t)arow & 15) == 0) {
+            for (int k = R - 4; k >= 0; k -= 4) {
+                float4 o;
+                acc += row[k + 3];
+                o.w = cbase - acc;
+                acc += row[k + 2];
+                o.z = cbase - acc;
+                acc += row[k + 1];
+                o.y = cbase - acc;
+                acc += row[k];
+                o.x = cbase - acc;
+                row[k] = o.x;  // kept for the chain rule
+                row[k + 1] = o.y;
+                row[k + 2] = o.z;
+                row[k + 3] = o.w;
+                *reinterpret_cast<float4*>(arow + k) = o;
+            }
+        } else {
+            for (int k = R - 1; k >= 0; --k) {
+                acc += row[k];
+                const float da = cbase - acc;
+                row[k] = da;
+                if (arow && tl + k < nt) arow[k] = da;
+            }
         }
     }
     if (!dh && !dbeta) return;
     __syncthreads();
-    // 3. chain rule through Eq. 9 into dh, dbeta ([B,N,H], coalesced)
+
+    // 3. chain rule through Eq. 9 into dh, dbeta ([B,N,H], coalesced):
+    //    d alpha/dh = beta sigma(beta h)/(beta+eps),
+    //    d alpha/dbeta = (h sigma(beta h)(beta+eps) - softplus(beta h))/(beta+eps)^2
     const int64_t row0 = ((int64_t)b * N + t0) * H + hh0;
+    if (tile_vec_ok<HGP>(nh, H, kAlphaIn ? dh : h, kAlphaIn ? nullptr : beta) &&
+        (!dh || ((uintptr_t)dh % (4 * sizeof(Tin))) == 0) &&
+        (!dbeta || ((uintptr_t)dbeta % (4 * sizeof(Tin))) == 0)) {
+        constexpr int LOG_G4 = LOG_HGP >= 2 ? LOG_HGP - 2 : 0;
+        constexpr int kV = 4 / (int)sizeof(Tin);
+        const int ngrp = T << LOG_G4;
+        for (int e0 = tid; e0 < ngrp; e0 += kThreads * kV) {
+            Raw4<Tin> rh[kV], rb[kV];
+            if (!kAlphaIn) {
+#pragma unroll
+                for (int k = 0; k < kV; ++k) {
+                    const int e = e0 + k * kThreads;
+                    const int tt = e >> LOG_G4, j4 = e & ((1 << LOG_G4) - 1);
+                    if (e < ngrp && tt < nt) {
+                        const int64_t i = row0 + (int64_t)tt * H + 4 * j4;
+                        rh[k] = *reinterpret_cast<const Raw4<Tin>*>(h + i);
+                        rb[k] = *reinterpret_cast<const Raw4<Tin>*>(beta + i);
+                    }
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < kV; ++k) {
+                const int e = e0 + k * kThreads;
+                const int tt = e >> LOG_G4, j4 = e & ((1 << LOG_G4) - 1);
+                if (e >= ngrp || tt >= nt) continue;
+                const int64_t i = row0 + (int64_t)tt * H + 4 * j4;
+                float da[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) da[q] = sA[(4 * j4 + q) * pitch + sk(tt, log_r)];
+                if (kAlphaIn) {
+                    if (dh) store4(dh + i, da);
+                } else {
+                    float hv[4], bv[4], gh[4], gb[4];
+                    unpack4(rh[k], hv);
+                    unpack4(rb[k], bv);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const float z = bv[q] * hv[q], be = bv[q] + eps, sg = sigmoid_fast(z);
+                        const float rbe = __fdividef(1.f, be);
+                        gh[q] = da[q] * sg * bv[q] * rbe;
+                        gb[q] = da[q] * (sg * hv[q] * be - softplus_fast(z)) * (rbe * rbe);
+                    }
+                    if (dh) store4(dh + i, gh);
+                    if (dbeta) store4(dbeta + i, gb);
+                }
+            }
+        }
+        return;
+    }
+    constexpr int kB = 4;
     for (int e0 = tid; e0 < T * HGP; e0 += kThreads * kB) {
         float hv[kB], bv[kB];
 #pragma unroll
@@ -340,7 +533,7 @@ template <typename Tin, bool kAlpha, int L>
 void launch_fwd_t(const void* h, const void* beta, int64_t B, int64_t N, int64_t H, float eps,
                   const double* carry_in, float* U, double* total, const Lookback& lb, const ScanGeom& g,
                   cudaStream_t st) {
-    const size_t smem = (size_t)(1 << L) * ((1 << g.log_t) + 33) * sizeof(float);
+    const size_t smem = (size_t)(1 << L) * ((1 << g.log_t) + 33) * sizeof(float);  // <= 37 KB
     auto k = gate_prefix_kernel<Tin, kAlpha, L>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k<<<(unsigned)(B * g.n_hgroups * g.n_chunks), kThreads, smem, st>>>((const Tin*)h, (const Tin*)beta, N, H, eps,
@@ -351,7 +544,7 @@ template <typename Tin, bool kAlpha, int L>
 void launch_bwd_t(const void* h, const void* beta, int64_t B, int64_t N, int64_t H, float eps, const float* dU,
                   const double* carry, float* dalpha, void* dh, void* dbeta, const Lookback& lb, const ScanGeom& g,
                   cudaStream_t st) {
-    const size_t smem = (size_t)(1 << L) * ((1 << g.log_t) + 33) * sizeof(float);
+    const size_t smem = (size_t)(1 << L) * ((1 << g.log_t) + 33) * sizeof(float);  // <= 37 KB
     auto k = gate_prefix_bwd_kernel<Tin, kAlpha, L>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k<<<(unsigned)(B * g.n_hgroups * g.n_chunks), kThreads, smem, st>>>(
