@@ -3,29 +3,33 @@
 //
 // One CTA owns two 128-row query tiles of one (b, h) and streams the 128-key
 // K/V tiles of their joint window once, diagonal first (descending j):
-//   warp 9      TMA producer: Q0/Q1 once, then K_j (3-stage ring, one tile
-//               ahead) and V_j (2-stage ring); 128B swizzle, OOB rows
-//               zero-filled -> ragged tails for free
-//   warp 8      MMA issuer (one elected lane): S_i = Q_i K_j^T (SS, fp32 in
+//   warp 17     TMA producer: Q0/Q1 once, then K_j and V_j (2-stage rings, K
+//               one tile ahead of V); 128B swizzle, OOB rows zero-filled ->
+//               ragged tails for free
+//   warp 16     MMA issuer (one elected lane): S_i = Q_i K_j^T (SS, fp32 in
 //               TMEM) and O_i += P_i V_j (TS: P read from TMEM), commits to
 //               mbarriers; tcgen05.commit tracks all earlier MMAs, so S_full
 //               of step n also certifies that PV of step n-1 has landed.
-//   warps 0-3/4-7  softmax for tile 0 / tile 1, one thread per query row:
-//               tcgen05.ld the S row, add the gate bias as an outer
-//               difference of two u vectors (nothing N x w is materialised),
-//               window-mask only on diagonal / window-edge tiles (P:381-383,
-//               a per-row column range turned into bit masks), online softmax
-//               in fp32 with packed f32x2 FMA/ADD and a lazy rescale (the
-//               reference max moves only when it grows by > 2^8), bf16 P back
-//               into the same TMEM columns; epilogue O / l staged in smem with
-//               the 128B swizzle and written by TMA stores, LSE = m + ln l
-//               (P:388).
+//   warps 0-7 / 8-15  softmax for tile 0 / tile 1; a query row is shared by
+//               two threads (warps w and w+4: same TMEM lane quadrant, 64
+//               columns each, held in registers after one tcgen05.ld pair):
+//               add the gate bias as an outer difference of two u
+//               vectors (nothing N x w is materialised), window-mask only on
+//               diagonal / window-edge tiles (a per-row column range
+//               turned into bit masks), row max exchanged through smem, online
+//               softmax in fp32 with packed f32x2 FMA/ADD, 3-input max and a
+//               lazy rescale (the reference max moves only when it grows by
+//               > 2^8), bf16 P back into the same TMEM columns; epilogue O / l
+//               staged in smem with the 128B swizzle and written by TMA stores,
+//               LSE = m + ln l.
+//   warps 18-19 idle (complete the third warpgroup: setmaxnreg moves the
+//               MMA/TMA warpgroup's registers to the softmax warpgroups)
 // TMEM: S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512) columns x 128 lanes.
 // Key tiles outside every row's window are never loaded.
 #include <vector>
 
 #ifndef GFWA_FWD_POLY
-#define GFWA_FWD_POLY 2
+#define GFWA_FWD_POLY 1
 #endif
 
 #include "attn_common.cuh"
@@ -40,10 +44,14 @@ using namespace sm100;
 constexpr int BM = 128;          // query rows per tile
 constexpr int BN = 128;          // keys per tile
 constexpr int D = 128;           // head dim
-constexpr int NK = 3;            // K ring stages
-constexpr int NV = 2;            // V ring stages
+constexpr int NK = 2;            // K ring stages (2 x 32 KB: also the fp32 epilogue stage of tile 0)
+constexpr int NV = 2;            // V ring stages (2 x 32 KB: also the fp32 epilogue stage of tile 1)
 constexpr uint32_t kTileBytes = BM * D * 2;  // 32 KB bf16 tile
-constexpr int kThreads = 320;    // 8 softmax warps + MMA warp + TMA warp
+constexpr int kThreads = 640;    // 16 softmax warps (2 per row quadrant per tile), MMA, TMA, 2 idle
+constexpr int kMmaWarp = 16, kTmaWarp = 17;
+constexpr int kSoftmaxRegs = 112;  // softmax warpgroups hold 64 fp32 S values per thread in registers
+// (the CTA pool is the launch allocation, 640 x 96: 512 x 112 + 128 x 32 fits it exactly)
+constexpr int kOtherRegs = 32;     // MMA / TMA warpgroup
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 constexpr int kPolyPairs = GFWA_FWD_POLY;  // of every 4 column pairs, how many use exp2_poly2
 
@@ -90,6 +98,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* Ks = smem + 2 * kTileBytes;           // NK tiles
     uint8_t* Vs = Ks + NK * kTileBytes;            // NV tiles
     __shared__ __align__(16) float s_nbk[2][BN];  // negated key bias -(u_k - uref) log2e, per tile
+    __shared__ float s_mx[2][2][BM];              // per tile, column half, row: max / row-sum exchange
     Bars* bars = (Bars*)(Vs + NV * kTileBytes);
     uint32_t* tmem_sh = (uint32_t*)(bars + 1);
 
@@ -121,7 +130,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int i = 0; i < 2; ++i) {
             mbar_init(&bars->q_full[i], 1);
             mbar_init(&bars->s_full[i], 1);
-            mbar_init(&bars->p_ready[i], 4);
+            mbar_init(&bars->p_ready[i], 8);
             mbar_init(&bars->o_full[i], 1);
         }
         for (int s = 0; s < NK; ++s) {
@@ -134,11 +143,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         fence_barrier_init();
     }
-    if (warp == 8) {
+    if (warp == kMmaWarp) {
         tmem_alloc(tmem_sh, 512);
         tmem_relinquish();
     }
-    if (warp == 9 && elect_one()) {
+    if (warp == kTmaWarp && elect_one()) {
         tma_prefetch(&mq);
         tma_prefetch(&mk);
         tma_prefetch(&mv);
@@ -149,8 +158,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     const uint32_t tmem = *tmem_sh;
     if (threadIdx.x == 0) GFWA_TR(1);
-
-    if (warp == 9) {
+    // registers move from the MMA/TMA warpgroup to the two softmax warpgroups
+    if (warp >= kMmaWarp) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kOtherRegs));
+    if (warp == kTmaWarp) {
         // ------------------------------------------------ TMA producer
         if (elect_one()) {
             const uint64_t pol_kv = policy_evict_last();  // K/V tiles are re-read by ~w/128 neighbours
@@ -183,7 +193,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                      half * 64, (int)h, (int)(j * BN), (int)b, pol_kv);
             }
         }
-    } else if (warp == 8) {
+    } else if (warp == kMmaWarp) {
         // ------------------------------------------------ MMA issuer
         const uint32_t idesc_qk = idesc_bf16(BM, BN, false, false);
         const uint32_t idesc_pv = idesc_bf16(BM, D, false, true);
@@ -265,10 +275,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             __syncwarp();
         }
-    } else {
+    } else if (warp < kMmaWarp) {
         // ------------------------------------------------ softmax warpgroups
-        const int i = warp >> 2;  // query tile
-        const int r = threadIdx.x & 127;
+        // tile i = warp >> 3; a row r is shared by two threads (warps w and
+        // w + 4 of the tile, same TMEM lane quadrant), each owning 64 columns
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kSoftmaxRegs));
+        const int i = warp >> 3;
+        const int hf = (warp >> 2) & 1;  // column half
+        const int r = (warp & 3) * 32 + (threadIdx.x & 31);
+        const int c0 = 64 * hf;
         if (i == 0 || act1) {
             const int64_t t = r0 + i * BM + r;
             const bool valid = t < p.Nq;
@@ -283,79 +298,81 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t lane_addr = tmem + ((uint32_t)((warp & 3) * 32) << 16);
             const uint32_t scol = 128 * i;
             const uint64_t sl2x2 = f2pack(p.sl2, p.sl2);
+            const int64_t jlo_i = i ? jlo[1] : jlo[0], jhi_i = i ? jhi[1] : jhi[0];
+            const int64_t glo_i = i ? glo[1] : glo[0], ghi_i = i ? ghi[1] : ghi[0];
             float m_used = -INFINITY, l = 0.f;
             uint32_t sph = 0;
             int n = 0;
-            float u_next = jhi[i] * BN + r < p.Nkv ? Ubh[jhi[i] * BN + r] : 0.f;
-            for (int64_t j = jhi[i]; j >= jlo[i]; --j, ++n) {
-                // -(u_k - uref) log2e of this key tile -> smem (WG-cooperative); the
-                // next tile's u is prefetched into a register meanwhile
-                named_bar_sync(1 + i, 128);
-                s_nbk[i][r] = (uref - u_next) * kLog2e;
-                if (j > jlo[i]) u_next = Ubh[(j - 1) * BN + r];
-                named_bar_sync(1 + i, 128);
+            // the hf == 0 half keeps the key-bias vector: u of the next key tile prefetched
+            float u_next = hf == 0 && jhi_i * BN + r < p.Nkv ? Ubh[jhi_i * BN + r] : 0.f;
+            for (int64_t j = jhi_i; j >= jlo_i; --j, ++n) {
+                // -(u_k - uref) log2e of this key tile -> smem (tile-cooperative)
+                named_bar_sync(1 + i, 256);
+                if (hf == 0) {
+                    s_nbk[i][r] = (uref - u_next) * kLog2e;
+                    if (j > jlo_i) u_next = Ubh[(j - 1) * BN + r];
+                }
+                named_bar_sync(1 + i, 256);
                 mbar_wait(&bars->s_full[i], sph);
-                if (n < 8 && r == 0) GFWA_TR(16 + 24 * i + n);
+                if (n < 8 && r == 0 && hf == 0) GFWA_TR(16 + 24 * i + n);
                 sph ^= 1;
                 tc_fence_after();
-                const bool trw = (i == 0 && n == 1 && (r == 0 || r == 96));
-                // x = scale*q.k - (u_k - uref) log2e   (Alg. 2 l.12-15), packed pairs.
-                // Two passes over 32-column TMEM chunks (max, then exp) keep ~64
-                // values live instead of 128: no spills, loads pipeline freely;
-                // re-reading TMEM is cheaper than holding the row in registers.
-                const bool interior = (j * BN + BN - 1 <= glo[i]) && (j * BN >= ghi[i] - p.w + 1);
-                uint32_t keep[4] = {~0u, ~0u, ~0u, ~0u};
+                const bool trw = (i == 0 && n == 1 && hf == 0 && (r == 0 || r == 96));
+                const bool interior = (j * BN + BN - 1 <= glo_i) && (j * BN >= ghi_i - p.w + 1);
+                uint32_t keep[2] = {~0u, ~0u};
                 if (!interior) {
                     // keys in (g - w, g] and < N_kv, as columns of this tile
                     const int64_t kb = j * BN;
                     const int hi = (int)min64(min64(g - kb, (int64_t)BN - 1), p.Nkv - 1 - kb);
                     const int lo = (int)max64(g - p.w + 1 - kb, (int64_t)0);
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) keep[c] = range_bits(lo, hi, 32 * c);
+                    for (int c = 0; c < 2; ++c) keep[c] = range_bits(lo, hi, c0 + 32 * c);
                 }
-                const float* nbv = s_nbk[i];
-                auto logits = [&](const uint32_t (&raw)[32], int cb, uint64_t (&xp)[16]) {
-#pragma unroll
-                    for (int e = 0; e < 32; e += 4) {
-                        const float4 nb = *reinterpret_cast<const float4*>(nbv + cb + e);
-                        xp[e / 2] = ffma2(f2pack(__uint_as_float(raw[e]), __uint_as_float(raw[e + 1])), sl2x2,
-                                          f2pack(nb.x, nb.y));
-                        xp[e / 2 + 1] = ffma2(f2pack(__uint_as_float(raw[e + 2]), __uint_as_float(raw[e + 3])), sl2x2,
-                                              f2pack(nb.z, nb.w));
-                    }
-                    if (!interior) {
-                        const uint32_t kw = keep[cb >> 5];
-#pragma unroll
-                        for (int e = 0; e < 16; ++e) {
-                            float a, z;
-                            f2unpack(xp[e], a, z);
-                            a = ((kw >> (2 * e)) & 1u) ? a : -INFINITY;
-                            z = ((kw >> (2 * e + 1)) & 1u) ? z : -INFINITY;
-                            xp[e] = f2pack(a, z);
-                        }
-                    }
-                };
-                float mx0 = -INFINITY, mx1 = -INFINITY;
-#pragma unroll
-                for (int cb = 0; cb < BN; cb += 32) {
-                    uint32_t raw[32];
-                    tmem_ld32(lane_addr + scol + cb, raw);
-                    tmem_wait_ld();
-                    uint64_t xp[16];
-                    logits(raw, cb, xp);
-#pragma unroll
-                    for (int e = 0; e < 16; e += 2) {
-                        float a0, a1, b0, b1;
-                        f2unpack(xp[e], a0, a1);
-                        f2unpack(xp[e + 1], b0, b1);
-                        mx0 = fmaxf(mx0, fmaxf(a0, a1));
-                        mx1 = fmaxf(mx1, fmaxf(b0, b1));
-                    }
-                }
+                const float* nbv = s_nbk[i] + c0;
+                // this thread's 64 S values in registers (two loads, one wait), the
+                // logits x = scale*q.k - (u_k - uref) log2e (Alg. 2 l.12-15) in place
+                // as packed pairs; max and exp both run from registers
+                uint32_t raw[64];
+                tmem_ld32(lane_addr + scol + c0, *reinterpret_cast<uint32_t(*)[32]>(raw));
+                tmem_ld32(lane_addr + scol + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(raw + 32));
+                tmem_wait_ld();
                 if (trw) GFWA_TR(10 + (r == 96));
-                const float mt = fmaxf(mx0, mx1);
+                uint64_t xp[32];
+#pragma unroll
+                for (int e = 0; e < 64; e += 4) {
+                    const float4 nb = *reinterpret_cast<const float4*>(nbv + e);
+                    xp[e / 2] = ffma2(f2pack(__uint_as_float(raw[e]), __uint_as_float(raw[e + 1])), sl2x2,
+                                      f2pack(nb.x, nb.y));
+                    xp[e / 2 + 1] = ffma2(f2pack(__uint_as_float(raw[e + 2]), __uint_as_float(raw[e + 3])), sl2x2,
+                                          f2pack(nb.z, nb.w));
+                }
+                if (!interior) {
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) {
+                        const uint32_t kw = keep[e >> 4];
+                        const int bit = 2 * (e & 15);
+                        float a, z;
+                        f2unpack(xp[e], a, z);
+                        a = ((kw >> bit) & 1u) ? a : -INFINITY;
+                        z = ((kw >> (bit + 1)) & 1u) ? z : -INFINITY;
+                        xp[e] = f2pack(a, z);
+                    }
+                }
+                float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+                for (int e = 0; e < 32; ++e) {
+                    float a, z;
+                    f2unpack(xp[e], a, z);
+                    mx[e & 3] = fmax3(mx[e & 3], a, z);
+                }
+                // row max = max over both halves (exchanged through smem)
+                s_mx[i][hf][r] = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+                if (trw) GFWA_TR(58 + (r == 96));
+                named_bar_sync(3 + i, 256);
+                const float mt = fmaxf(s_mx[i][0][r], s_mx[i][1][r]);
                 if (trw) GFWA_TR(12 + (r == 96));
-                // lazy online softmax: move the reference max only when it grows by > 2^8
+                // lazy online softmax: move the reference max only when it grows by
+                // > 2^8 (both halves take the same decision from the same values)
                 float corr = 1.f;
                 bool need = false;
                 if (mt > m_used + kRescaleThreshold) {
@@ -370,16 +387,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint64_t nm2 = f2pack(-mref, -mref);
                 uint64_t acc[4] = {0, 0, 0, 0};  // packed (0.f, 0.f)
 #pragma unroll
-                for (int cb = 0; cb < BN; cb += 32) {
-                    uint32_t raw[32];
-                    tmem_ld32(lane_addr + scol + cb, raw);
-                    tmem_wait_ld();
-                    uint64_t xp[16];
-                    logits(raw, cb, xp);
+                for (int cb = 0; cb < 64; cb += 32) {
                     uint32_t pk[16];
 #pragma unroll
                     for (int e = 0; e < 16; ++e) {
-                        const uint64_t d = fadd2(xp[e], nm2);
+                        const uint64_t d = fadd2(xp[cb / 2 + e], nm2);
                         float p0, p1;
                         if ((e & 3) < kPolyPairs) {
                             // part of the exponentials on the FMA pipe: MUFU.EX2 is
@@ -394,25 +406,25 @@ __global__ void __launch_bounds__(kThreads, 1)
                         acc[e & 3] = fadd2(acc[e & 3], f2pack(p0, p1));
                         pk[e] = pack_bf16x2(p0, p1);
                     }
-                    tmem_st16(lane_addr + scol + cb / 2, pk);  // P (bf16) over the S columns
+                    tmem_st16(lane_addr + scol + (c0 + cb) / 2, pk);  // P (bf16) over the S columns
                 }
                 if (trw) GFWA_TR(14 + (r == 96));
                 {
                     const uint64_t a01 = fadd2(acc[0], acc[1]), a23 = fadd2(acc[2], acc[3]);
                     float s0, s1;
                     f2unpack(fadd2(a01, a23), s0, s1);
-                    l += s0 + s1;
+                    l += s0 + s1;  // this half's share of the row sum
                 }
-                // rescale O_i (PV of the previous step is complete: S_full certified it)
+                // rescale this half of O_i (PV of the previous step is complete: S_full certified it)
                 if (__any_sync(0xffffffffu, need) && n > 0) {
                     uint32_t ob[32];
 #pragma unroll
-                    for (int c = 0; c < D; c += 32) {
-                        tmem_ld32(lane_addr + 256 + scol + c, ob);
+                    for (int c = 0; c < 64; c += 32) {
+                        tmem_ld32(lane_addr + 256 + scol + c0 + c, ob);
                         tmem_wait_ld();
 #pragma unroll
                         for (int e = 0; e < 32; ++e) ob[e] = __float_as_uint(__uint_as_float(ob[e]) * corr);
-                        tmem_st32(lane_addr + 256 + scol + c, ob);
+                        tmem_st32(lane_addr + 256 + scol + c0 + c, ob);
                     }
                 }
                 tmem_wait_st();
@@ -420,21 +432,25 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc_fence_before();
                 __syncwarp();
                 if ((threadIdx.x & 31) == 0) mbar_arrive(&bars->p_ready[i]);
-                if (n < 8 && r == 0) GFWA_TR(24 + 24 * i + n);
+                if (n < 8 && r == 0 && hf == 0) GFWA_TR(24 + 24 * i + n);
                 if (trw && r == 96) GFWA_TR(38);
             }
             // epilogue: O / l (Alg. 2 l.19-20) staged in smem (128B swizzle) and
-            // written with TMA stores; tile 0 stages in the K ring, tile 1 in the
-            // V ring + Q area (both idle once O_full fires)
+            // written with TMA stores: bf16 in the tile's own Q slot, fp32 in the
+            // K ring (tile 0: every S MMA precedes O_full[0]) or the V ring (tile 1:
+            // last to finish)
+            s_mx[i][hf][r] = l;
             mbar_wait(&bars->o_full[i], 0);
-            if (r == 0) GFWA_TR(32 + 24 * i);
+            if (r == 0 && hf == 0) GFWA_TR(32 + 24 * i);
             tc_fence_after();
-            const float inv = l > 0.f ? 1.f / l : 0.f;
-            uint8_t* stg_bf = i == 0 ? Ks : Vs;
-            uint8_t* stg_f = i == 0 ? Ks + kTileBytes : Qs;
+            named_bar_sync(3 + i, 256);
+            const float lt = s_mx[i][0][r] + s_mx[i][1][r];
+            const float inv = lt > 0.f ? 1.f / lt : 0.f;
+            uint8_t* stg_bf = Qs + i * kTileBytes;
+            uint8_t* stg_f = i == 0 ? Ks : Vs;
             const uint32_t sb = smem_u32(stg_bf), sf = smem_u32(stg_f);
 #pragma unroll 1
-            for (int c = 0; c < 4; ++c) {
+            for (int c = 2 * hf; c < 2 * hf + 2; ++c) {
                 uint32_t ob[32];
                 tmem_ld32(lane_addr + 256 + scol + 32 * c, ob);
                 tmem_wait_ld();
@@ -463,10 +479,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
             }
-            if (valid) p.LSE[(b * p.H + h) * p.Nq + t] = (m_used + bq + __log2f(l)) * kLn2;
+            if (valid && hf == 0) p.LSE[(b * p.H + h) * p.Nq + t] = (m_used + bq + __log2f(lt)) * kLn2;
             fence_proxy_async();
-            named_bar_sync(1 + i, 128);
-            if (r == 0) {
+            named_bar_sync(1 + i, 256);
+            if (r == 0 && hf == 0) {
                 const int row0 = (int)(r0 + i * BM);
                 for (int half = 0; half < 2; ++half)
                     tma_store_4d(&mo, stg_bf + half * (kTileBytes / 2), half * 64, (int)h, row0, (int)b);
@@ -480,7 +496,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 8) {
+    if (warp == kMmaWarp) {
         tc_fence_after();
         tmem_dealloc(tmem, 512);
     }

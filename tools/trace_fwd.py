@@ -30,8 +30,10 @@ stat("k_full gaps k3-k2", kf[:, 3] - kf[:, 2])
 sf1 = t[:, 17].astype(float)
 for w, off in ((0, 0), (3, 1)):
     a, b_, c, d = (t[:, s + off].astype(float) for s in (10, 12, 14, 34))
+    e = t[:, 58 + off].astype(float)
     stat(f"w{w}: S_full->LDTM done", a - sf1)
-    stat(f"w{w}: LDTM->max done", b_ - a)
+    stat(f"w{w}: LDTM->own max", e - a)
+    stat(f"w{w}: own max->exchange done", b_ - e)
     stat(f"w{w}: max->exp/STTM done", c - b_)
     stat(f"w{w}: exp->wait_st done", d - c)
 stat("w3: P arrive - w0 S_full", t[:, 38].astype(float) - sf1)
