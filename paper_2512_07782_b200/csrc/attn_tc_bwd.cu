@@ -9,9 +9,10 @@
 //   S^T  = K Q^T          SS  M=128 keys, N=64 queries   -> buf[n&1] cols [0,64)
 //   dP^T = V dO^T         SS                             -> buf[n&1] cols [64,128)
 //   (softmax-grad, 2 warpgroups x 32 queries, thread = key: P^T = exp(S - L),
-//    dS^T = P^T (dP^T - D); P^T and dS^T back to TMEM as bf16 over the columns
-//    they were read from, dS^T also to smem)
-//   dQ^T = K^T dS^T       SS  M=128 (d), 4 x N=16         -> the freed columns
+//    dS^T = P^T (dP^T - D); after both warpgroups hold their columns in
+//    registers, P^T and dS^T go back to TMEM as bf16, packed into [0,32) and
+//    [32,64), dS^T also to smem)
+//   dQ^T = K^T dS^T       SS  M=128 (d), N=64             -> the freed [64,128)
 //   dV  += P^T dO         TS  (A = P^T from TMEM)         -> TMEM [256,384)
 //   dK  += dS^T Q         TS  (A = dS^T from TMEM)        -> TMEM [384,512)
 // The dQ^T tile is drained by a third warpgroup (thread = head-dim lane) into
@@ -173,7 +174,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ------------------------------------------------ MMA issuer
         const uint32_t id_st = idesc_bf16(128, BMQ, false, false);  // S^T, dP^T
         const uint32_t id_tm = idesc_bf16(128, D, false, true);     // dV, dK (A in TMEM, B MN-major)
-        const uint32_t id_dq = idesc_bf16(128, 16, true, true);     // dQ^T quarters (A, B MN-major)
+        const uint32_t id_dq = idesc_bf16(128, BMQ, true, true);    // dQ^T (A, B MN-major)
         const uint32_t kb = smem_u32(Ks), vb = smem_u32(Vs);
         if (nsteps > 0) mbar_wait(&bars->kv_full, 0);
         auto mma2 = [&](int m) {  // gradients of step m
@@ -184,22 +185,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (elect_one()) {
                 const uint32_t buf = tmem + 128 * bm;
                 const uint32_t qb = smem_u32(Qs + sm * 2 * kQT), ob = qb + kQT, sb = smem_u32(dSs + bm * kDS);
-                // dQ^T = K^T dS^T, four 16-query column blocks into the freed columns
-                const uint32_t qcol[4] = {16, 48, 64 + 16, 64 + 48};
+                // dQ^T = K^T dS^T, one N = 64 chain into the freed columns [64,128)
 #pragma unroll
-                for (int qq = 0; qq < 4; ++qq)
-#pragma unroll
-                    for (int kk = 0; kk < BN / 16; ++kk)
-                        mma_ss(buf + qcol[qq], sdesc_sw128(kb + kk * 2048, kKV / 2, 1024),
-                               sdesc_sw128(sb + qq * 32 + kk * 2048, 8192, 1024), id_dq, kk > 0 ? 1u : 0u);
+                for (int kk = 0; kk < BN / 16; ++kk)
+                    mma_ss(buf + 64, sdesc_sw128(kb + kk * 2048, kKV / 2, 1024),
+                           sdesc_sw128(sb + kk * 2048, 8192, 1024), id_dq, kk > 0 ? 1u : 0u);
                 tc_commit(&bars->dq_full[bm]);
-                // dV += P^T dO ; dK += dS^T Q   (16 queries = 8 TMEM columns per K step)
+                // dV += P^T dO ; dK += dS^T Q   (P^T in columns [0,32), dS^T in [32,64):
+                // 16 queries = 8 TMEM columns per K step)
 #pragma unroll
                 for (int kk = 0; kk < BMQ / 16; ++kk) {
-                    const uint32_t acol = (kk >> 1) * 32 + (kk & 1) * 8;
                     const uint32_t acc = (m > 0 || kk > 0) ? 1u : 0u;
-                    mma_ts(tmem + 256, buf + acol, sdesc_sw128(ob + kk * 2048, kQT / 2, 1024), id_tm, acc);
-                    mma_ts(tmem + 384, buf + 64 + acol, sdesc_sw128(qb + kk * 2048, kQT / 2, 1024), id_tm, acc);
+                    mma_ts(tmem + 256, buf + 8 * kk, sdesc_sw128(ob + kk * 2048, kQT / 2, 1024), id_tm, acc);
+                    mma_ts(tmem + 384, buf + 32 + 8 * kk, sdesc_sw128(qb + kk * 2048, kQT / 2, 1024), id_tm, acc);
                 }
                 tc_commit(&bars->q_empty[sm]);
                 if (m == nsteps - 1) tc_commit(&bars->dkdv_full);
@@ -261,6 +259,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             tmem_ld32(lane_addr + scol, sall);
             tmem_ld32(lane_addr + scol + 64, dall);
             tmem_wait_ld();
+            // both warpgroups hold their S^T / dP^T columns in registers before
+            // either packs P^T, dS^T into [0,64): dQ^T then gets [64,128) whole
+            tc_fence_before();
+            named_bar_sync(5, 256);
+            tc_fence_after();
             const bool trw = (n == 4 && threadIdx.x == 0);
             if (trw) GFWA_TR(43);
             for (int h16 = 0; h16 < 32; h16 += 16) {
@@ -298,8 +301,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
             if (trw) GFWA_TR(44);
-            tmem_st16(lane_addr + scol, pk);       // P^T  over the S^T columns it came from
-            tmem_st16(lane_addr + scol + 64, dk);  // dS^T over the dP^T columns
+            tmem_st16(lane_addr + 128 * bn + 16 * wg, pk);       // P^T  -> columns [0,32)
+            tmem_st16(lane_addr + 128 * bn + 32 + 16 * wg, dk);  // dS^T -> columns [32,64)
             {  // dS^T row -> smem (128B-swizzled MN-major: row = key, 16-B chunk of 8 queries ^ key%8)
                 const uint32_t sb = smem_u32(dSs + bn * kDS) + kr * 128;
 #pragma unroll
@@ -390,7 +393,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // L2 does the adds, no per-thread atomics.
         const int dl = threadIdx.x - 256;  // 0..127
         const uint32_t lane_addr = tmem + ((uint32_t)((warp & 3) * 32) << 16);
-        const uint32_t qcol[4] = {16, 48, 64 + 16, 64 + 48};
+        const uint32_t qcol[4] = {64, 80, 96, 112};  // dQ^T: columns [64,128) of the buffer
         const uint32_t sq = smem_u32(dQs) + (dl >> 5) * (kDQ / 4);  // this lane's 32-d box (4 KB)
         for (int m = 0; m < nsteps; ++m) {
             const int bm = m & 1;
