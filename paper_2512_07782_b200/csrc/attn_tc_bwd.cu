@@ -42,6 +42,10 @@ constexpr uint32_t kKV = 128 * 128 * 2;   // 32 KB K or V tile
 constexpr uint32_t kQT = 64 * 128 * 2;    // 16 KB Q or dO tile
 constexpr uint32_t kDS = 128 * 64 * 2;    // 16 KB dS^T tile
 constexpr int kThreads = 448;             // 2 softmax-grad WGs, drain WG, MMA warp, TMA warp
+#ifndef GFWA_BWD_POLY
+#define GFWA_BWD_POLY 0
+#endif
+constexpr int kBwdPoly = GFWA_BWD_POLY;  // of every 2 column pairs, how many use exp2_poly2
 
 struct TcBwdParams {
     const float* U;
@@ -286,7 +290,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                         x0 = ((keep >> e2) & 1u) ? x0 : -INFINITY;
                         x1 = ((keep >> (e2 + 1)) & 1u) ? x1 : -INFINITY;
                     }
-                    const uint64_t pr = f2pack(ex2(x0), ex2(x1));
+                    uint64_t pr;
+                    if (u < kBwdPoly) {
+                        // part of the exponentials on the FMA pipe: MUFU, SHFL and LDS
+                        // share the MIO queue, which bounds this loop
+                        pr = exp2_poly2(f2pack(x0, x1));
+                        if (!interior) {
+                            float q0, q1;
+                            f2unpack(pr, q0, q1);
+                            pr = f2pack(((keep >> e2) & 1u) ? q0 : 0.f, ((keep >> (e2 + 1)) & 1u) ? q1 : 0.f);
+                        }
+                    } else {
+                        pr = f2pack(ex2(x0), ex2(x1));
+                    }
                     // dS = P (dP - D)
                     const uint64_t dpd = fadd2(f2pack(__uint_as_float(d16[a]), __uint_as_float(d16[a + 1])),
                                                u == 0 ? f2pack(-d4.x, -d4.y) : f2pack(-d4.z, -d4.w));
