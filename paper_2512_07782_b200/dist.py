@@ -105,6 +105,7 @@ class ShardResult:
     dalpha: torch.Tensor
     dh: torch.Tensor
     dbeta: torch.Tensor
+    dU: torch.Tensor = None  # this rank's rows, halo contributions of rank r+1 added
 
 
 def halo_pack(K, V, U_loc, w: int):
@@ -159,4 +160,4 @@ def sp_forward_backward(Q, K, V, h, beta, dO, w: int, ops: Ops, ring: Ring, eps:
         dU[..., S - w:] += back[2]
         carry = back[2].double().sum(-1)  # d-alpha carry = +sum_j dU_halo(j)
     dalpha, dh, dbeta = ops.gate_bwd(dU, h, beta, eps, carry)
-    return ShardResult(O, LSE, U_loc, dQ, dK, dV, dalpha, dh, dbeta)
+    return ShardResult(O, LSE, U_loc, dQ, dK, dV, dalpha, dh, dbeta, dU)
