@@ -1,30 +1,31 @@
 // attn_tc_fwd.cu -- GatedFWA forward on the 5th-generation tensor cores
 // (sm_100a): Alg. 2 re-designed for tcgen05/TMEM/TMA.
 //
-// One CTA owns two 128-row query tiles of one (b, h) and streams the 128-key
-// K/V tiles of their joint window once, diagonal first (descending j):
-//   warp 17     TMA producer: Q0/Q1 once, then K_j and V_j (2-stage rings, K
-//               one tile ahead of V); 128B swizzle, OOB rows zero-filled ->
-//               ragged tails for free
-//   warp 16     MMA issuer (one elected lane): S_i = Q_i K_j^T (SS, fp32 in
-//               TMEM) and O_i += P_i V_j (TS: P read from TMEM), commits to
-//               mbarriers; tcgen05.commit tracks all earlier MMAs, so S_full
-//               of step n also certifies that PV of step n-1 has landed.
-//   warps 0-7 / 8-15  softmax for tile 0 / tile 1; a query row is shared by
-//               two threads (warps w and w+4: same TMEM lane quadrant, 64
-//               columns each, held in registers after one tcgen05.ld pair):
-//               add the gate bias as an outer difference of two u
-//               vectors (nothing N x w is materialised), window-mask only on
-//               diagonal / window-edge tiles (a per-row column range
-//               turned into bit masks), row max exchanged through smem, online
-//               softmax in fp32 with packed f32x2 FMA/ADD, 3-input max and a
-//               lazy rescale (the reference max moves only when it grows by
-//               > 2^8), bf16 P back into the same TMEM columns; epilogue O / l
-//               staged in smem with the 128B swizzle and written by TMA stores,
-//               LSE = m + ln l.
-//   warps 18-19 idle (complete the third warpgroup: setmaxnreg moves the
-//               MMA/TMA warpgroup's registers to the softmax warpgroups)
-// TMEM: S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512) columns x 128 lanes.
+// One CTA owns one 128-row query tile of one (b, h) and streams the 128-key
+// K/V tiles of its window, diagonal first (descending j).  TWO CTAs share an
+// SM (98 KB smem, 256 TMEM columns each): while one runs its softmax the other's
+// MMAs keep the tensor core busy, and one CTA's prologue (Q, K loads, first S)
+// and epilogue overlap the other's main loop -- without a persistent scheduler.
+//   warp 5      TMA producer: Q once, then K_j, V_j (one stage each: K_{j+1}
+//               streams in during the softmax of step j, V_j during the S MMA);
+//               128B swizzle, OOB rows zero-filled -> ragged tails for free
+//   warp 4      MMA issuer (one elected lane): S = Q K_j^T (SS, fp32 in TMEM)
+//               and O += P V_j (TS: bf16 P read from TMEM); tcgen05.commit
+//               tracks all earlier MMAs, so S_full of step n also certifies
+//               that PV of step n-1 has landed.
+//   warps 0-3   softmax, one thread per query row holding its 128 S values in
+//               registers (four tcgen05.ld, one wait; setmaxnreg gives this
+//               warpgroup 224 registers): add the gate bias as an
+//               outer difference of two u vectors (nothing N x w is
+//               materialised), window-mask only on diagonal / window-edge tiles
+//               (a per-row column range turned into bit masks), online
+//               softmax in fp32 with packed f32x2 FMA/ADD, 3-input max and a lazy
+//               rescale (the reference max moves only when it grows by > 2^8),
+//               part of exp2 on the FMA pipe, bf16 P back over the S columns;
+//               epilogue O / l staged in smem with the 128B swizzle and written
+//               by TMA stores, LSE = m + ln l.
+//   warps 6-7   idle (complete the second warpgroup for setmaxnreg)
+// TMEM (256 columns per CTA): S [0,128), O [128,256) x 128 lanes.
 // Key tiles outside every row's window are never loaded.
 #include <vector>
 
@@ -44,14 +45,11 @@ using namespace sm100;
 constexpr int BM = 128;          // query rows per tile
 constexpr int BN = 128;          // keys per tile
 constexpr int D = 128;           // head dim
-constexpr int NK = 2;            // K ring stages (2 x 32 KB: also the fp32 epilogue stage of tile 0)
-constexpr int NV = 2;            // V ring stages (2 x 32 KB: also the fp32 epilogue stage of tile 1)
 constexpr uint32_t kTileBytes = BM * D * 2;  // 32 KB bf16 tile
-constexpr int kThreads = 640;    // 16 softmax warps (2 per row quadrant per tile), MMA, TMA, 2 idle
-constexpr int kMmaWarp = 16, kTmaWarp = 17;
-constexpr int kSoftmaxRegs = 112;  // softmax warpgroups hold 64 fp32 S values per thread in registers
-// (the CTA pool is the launch allocation, 640 x 96: 512 x 112 + 128 x 32 fits it exactly)
-constexpr int kOtherRegs = 32;     // MMA / TMA warpgroup
+constexpr int kThreads = 256;    // softmax warpgroup + (MMA, TMA, 2 idle)
+constexpr int kMmaWarp = 4, kTmaWarp = 5;
+constexpr int kSoftmaxRegs = 224;  // CTA pool at (256, 2): 256 x 128; 128 x 224 + 128 x 32 fits it
+constexpr int kOtherRegs = 32;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 constexpr int kPolyPairs = GFWA_FWD_POLY;  // of every 4 column pairs, how many use exp2_poly2
 
@@ -72,10 +70,7 @@ struct TcFwdParams {
     } while (0)
 
 struct __align__(8) Bars {
-    uint64_t q_full[2];
-    uint64_t k_full[NK], k_empty[NK];
-    uint64_t v_full[NV], v_empty[NV];
-    uint64_t s_full[2], p_ready[2], o_full[2];
+    uint64_t q_full, k_full, k_empty, v_full, v_empty, s_full, p_ready, o_full;
 };
 
 __device__ __forceinline__ int64_t kv_tile_lo(int64_t g_lo, int w) { return max64(0, g_lo - w + 1) / BN; }
@@ -88,18 +83,17 @@ __device__ __forceinline__ uint32_t range_bits(int lo, int hi, int base) {
     return upto_z & ~below_a;
 }
 
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, 2)
     fwd_tc_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
                   const __grid_constant__ CUtensorMap mv, const __grid_constant__ CUtensorMap mo,
                   const __grid_constant__ CUtensorMap mo32, const TcFwdParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    uint8_t* Qs = smem;                            // 2 tiles
-    uint8_t* Ks = smem + 2 * kTileBytes;           // NK tiles
-    uint8_t* Vs = Ks + NK * kTileBytes;            // NV tiles
-    __shared__ __align__(16) float s_nbk[2][BN];  // negated key bias -(u_k - uref) log2e, per tile
-    __shared__ float s_mx[2][2][BM];              // per tile, column half, row: max / row-sum exchange
-    Bars* bars = (Bars*)(Vs + NV * kTileBytes);
+    uint8_t* Qs = smem;
+    uint8_t* Ks = Qs + kTileBytes;
+    uint8_t* Vs = Ks + kTileBytes;
+    __shared__ __align__(16) float s_nbk[BN];  // negated key bias -(u_k - uref) log2e
+    Bars* bars = (Bars*)(Vs + kTileBytes);
     uint32_t* tmem_sh = (uint32_t*)(bars + 1);
 
     const int warp = threadIdx.x >> 5;
@@ -112,39 +106,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     }
     const int64_t b = blockIdx.z, h = blockIdx.y;
-    const int64_t r0 = (int64_t)blockIdx.x * 2 * BM;
-    const bool act1 = r0 + BM < p.Nq;
-    // Alg. 2 l.7-9 per query tile: key positions g = t + h0
-    int64_t jlo[2], jhi[2], glo[2], ghi[2];
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-        glo[i] = r0 + i * BM + p.h0;
-        ghi[i] = min64(r0 + i * BM + BM - 1, p.Nq - 1) + p.h0;
-        jlo[i] = kv_tile_lo(glo[i], p.w);
-        jhi[i] = ghi[i] / BN;
-    }
-    const int64_t J_hi = act1 ? jhi[1] : jhi[0];
-    const int64_t J_lo = jlo[0];
+    const int64_t r0 = (int64_t)blockIdx.x * BM;
+    // Alg. 2 l.7-9: key positions g = t + h0
+    const int64_t glo = r0 + p.h0, ghi = min64(r0 + BM - 1, p.Nq - 1) + p.h0;
+    const int64_t jlo = kv_tile_lo(glo, p.w), jhi = ghi / BN;
 
     if (threadIdx.x == 0) {
-        for (int i = 0; i < 2; ++i) {
-            mbar_init(&bars->q_full[i], 1);
-            mbar_init(&bars->s_full[i], 1);
-            mbar_init(&bars->p_ready[i], 8);
-            mbar_init(&bars->o_full[i], 1);
-        }
-        for (int s = 0; s < NK; ++s) {
-            mbar_init(&bars->k_full[s], 1);
-            mbar_init(&bars->k_empty[s], 1);
-        }
-        for (int s = 0; s < NV; ++s) {
-            mbar_init(&bars->v_full[s], 1);
-            mbar_init(&bars->v_empty[s], 1);
-        }
+        mbar_init(&bars->q_full, 1);
+        mbar_init(&bars->k_full, 1);
+        mbar_init(&bars->k_empty, 1);
+        mbar_init(&bars->v_full, 1);
+        mbar_init(&bars->v_empty, 1);
+        mbar_init(&bars->s_full, 1);
+        mbar_init(&bars->p_ready, 4);
+        mbar_init(&bars->o_full, 1);
         fence_barrier_init();
     }
     if (warp == kMmaWarp) {
-        tmem_alloc(tmem_sh, 512);
+        tmem_alloc(tmem_sh, 256);
         tmem_relinquish();
     }
     if (warp == kTmaWarp && elect_one()) {
@@ -158,352 +137,283 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     const uint32_t tmem = *tmem_sh;
     if (threadIdx.x == 0) GFWA_TR(1);
-    // registers move from the MMA/TMA warpgroup to the two softmax warpgroups
-    if (warp >= kMmaWarp) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kOtherRegs));
+    // registers move from the MMA/TMA warpgroup to the softmax warpgroup
+    if (warp >= 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kOtherRegs));
+
     if (warp == kTmaWarp) {
         // ------------------------------------------------ TMA producer
         if (elect_one()) {
             const uint64_t pol_kv = policy_evict_last();  // K/V tiles are re-read by ~w/128 neighbours
-            for (int i = 0; i < 2; ++i) {
-                if (i == 1 && !act1) break;
-                mbar_expect_tx(&bars->q_full[i], kTileBytes);
-                for (int half = 0; half < 2; ++half)
-                    tma_load_4d(Qs + i * kTileBytes + half * (kTileBytes / 2), &mq, &bars->q_full[i], half * 64,
-                                (int)h, (int)(r0 + i * BM), (int)b);
-            }
-            // K runs one tile ahead of V: S(j) needs K_j long before PV(j) needs V_j
-            const int nk = (int)(J_hi - J_lo + 1);
-            auto load_k = [&](int k) {
-                const int s = k % NK;
-                mbar_wait(&bars->k_empty[s], ((k / NK) & 1) ^ 1);
-                mbar_expect_tx(&bars->k_full[s], kTileBytes);
-                for (int half = 0; half < 2; ++half)
-                    tma_load_4d_hint(Ks + s * kTileBytes + half * (kTileBytes / 2), &mk, &bars->k_full[s],
-                                     half * 64, (int)h, (int)((J_hi - k) * BN), (int)b, pol_kv);
-            };
-            load_k(0);
+            mbar_expect_tx(&bars->q_full, kTileBytes);
+            for (int half = 0; half < 2; ++half)
+                tma_load_4d(Qs + half * (kTileBytes / 2), &mq, &bars->q_full, half * 64, (int)h, (int)r0, (int)b);
             int k = 0;
-            for (int64_t j = J_hi; j >= J_lo; --j, ++k) {
-                const int sv = k % NV;
-                if (k + 1 < nk) load_k(k + 1);
-                mbar_wait(&bars->v_empty[sv], ((k / NV) & 1) ^ 1);
-                mbar_expect_tx(&bars->v_full[sv], kTileBytes);
+            for (int64_t j = jhi; j >= jlo; --j, ++k) {
+                mbar_wait(&bars->k_empty, (k & 1) ^ 1);
+                mbar_expect_tx(&bars->k_full, kTileBytes);
                 for (int half = 0; half < 2; ++half)
-                    tma_load_4d_hint(Vs + sv * kTileBytes + half * (kTileBytes / 2), &mv, &bars->v_full[sv],
-                                     half * 64, (int)h, (int)(j * BN), (int)b, pol_kv);
+                    tma_load_4d_hint(Ks + half * (kTileBytes / 2), &mk, &bars->k_full, half * 64, (int)h,
+                                     (int)(j * BN), (int)b, pol_kv);
+                mbar_wait(&bars->v_empty, (k & 1) ^ 1);
+                mbar_expect_tx(&bars->v_full, kTileBytes);
+                for (int half = 0; half < 2; ++half)
+                    tma_load_4d_hint(Vs + half * (kTileBytes / 2), &mv, &bars->v_full, half * 64, (int)h,
+                                     (int)(j * BN), (int)b, pol_kv);
             }
         }
     } else if (warp == kMmaWarp) {
         // ------------------------------------------------ MMA issuer
         const uint32_t idesc_qk = idesc_bf16(BM, BN, false, false);
         const uint32_t idesc_pv = idesc_bf16(BM, D, false, true);
-        const bool act[2] = {true, act1};
-        uint32_t pph[2] = {0, 0};
-        int64_t prev[2] = {-1, -1};
-        bool first_pv[2] = {true, true};
-        mbar_wait(&bars->q_full[0], 0);
-        if (act1) mbar_wait(&bars->q_full[1], 0);
+        const uint32_t qbase = smem_u32(Qs), kbase = smem_u32(Ks), vbase = smem_u32(Vs);
+        mbar_wait(&bars->q_full, 0);
         int k = 0;
-        for (int64_t j = J_hi; j >= J_lo; --j, ++k) {
-            const int s = k % NK;
-            mbar_wait(&bars->k_full[s], (k / NK) & 1);
+        for (int64_t j = jhi; j >= jlo; --j, ++k) {
+            if (k > 0) {
+                // O += P(k-1) V(k-1), then V's stage is free
+                mbar_wait(&bars->p_ready, (k - 1) & 1);
+                mbar_wait(&bars->v_full, (k - 1) & 1);
+                tc_fence_after();
+                if (elect_one()) {
+#pragma unroll
+                    for (int kk = 0; kk < BN / 16; ++kk)
+                        mma_ts(tmem + 128, tmem + 8 * kk, sdesc_sw128(vbase + kk * 2048, kTileBytes / 2, 1024),
+                               idesc_pv, (k > 1 || kk > 0) ? 1u : 0u);
+                    tc_commit(&bars->v_empty);
+                }
+                __syncwarp();
+            }
+            // S = Q K_j^T (over the P just consumed: tcgen05 MMAs run in issue order)
+            mbar_wait(&bars->k_full, k & 1);
             if (k < 8 && (threadIdx.x & 31) == 0) GFWA_TR(2 + k);
             tc_fence_after();
-            int pv_issued = 0;
-            for (int i = 0; i < 2; ++i) {
-                if (!act[i] || j < jlo[i] || j > jhi[i]) continue;
-                if (prev[i] >= 0) {
-                    // O_i += P_i(prev) V_prev  (V of tile j+1 sits in stage (k-1) % NV)
-                    mbar_wait(&bars->p_ready[i], pph[i]);
-                    pph[i] ^= 1;
-                    const int vs = (k - 1) % NV;
-                    mbar_wait(&bars->v_full[vs], ((k - 1) / NV) & 1);
-                    tc_fence_after();
-                    if (elect_one()) {
-                        const uint32_t vbase = smem_u32(Vs + vs * kTileBytes);
-#pragma unroll
-                        for (int kk = 0; kk < BN / 16; ++kk)
-                            mma_ts(tmem + 256 + 128 * i, tmem + 128 * i + 8 * kk,
-                                   sdesc_sw128(vbase + kk * 2048, kTileBytes / 2, 1024), idesc_pv,
-                                   (first_pv[i] && kk == 0) ? 0u : 1u);
-                    }
-                    __syncwarp();
-                    first_pv[i] = false;
-                    ++pv_issued;
-                }
-                // S_i = Q_i K_j^T
-                if (elect_one()) {
-                    const uint32_t qbase = smem_u32(Qs + i * kTileBytes), kbase = smem_u32(Ks + s * kTileBytes);
-#pragma unroll
-                    for (int kk = 0; kk < D / 16; ++kk) {
-                        const uint32_t off = (kk >> 2) * (kTileBytes / 2) + (kk & 3) * 32;
-                        mma_ss(tmem + 128 * i, sdesc_sw128(qbase + off, 16, 1024),
-                               sdesc_sw128(kbase + off, 16, 1024), idesc_qk, kk > 0 ? 1u : 0u);
-                    }
-                    tc_commit(&bars->s_full[i]);
-                }
-                __syncwarp();
-                prev[i] = j;
-            }
             if (elect_one()) {
-                tc_commit(&bars->k_empty[s]);
-                // release V_{j+1} once every query tile that uses it has issued its PV
-                if (pv_issued > 0) {
-                    const int64_t jp = j + 1;
-                    const int users = (jp >= jlo[0] && jp <= jhi[0]) + (act1 && jp >= jlo[1] && jp <= jhi[1]);
-                    if (pv_issued == users) tc_commit(&bars->v_empty[(k - 1) % NV]);
+#pragma unroll
+                for (int kk = 0; kk < D / 16; ++kk) {
+                    const uint32_t off = (kk >> 2) * (kTileBytes / 2) + (kk & 3) * 32;
+                    mma_ss(tmem, sdesc_sw128(qbase + off, 16, 1024), sdesc_sw128(kbase + off, 16, 1024), idesc_qk,
+                           kk > 0 ? 1u : 0u);
                 }
+                tc_commit(&bars->s_full);
+                tc_commit(&bars->k_empty);
             }
             __syncwarp();
         }
-        // flush: last PV of every tile, then signal the epilogue
-        for (int i = 0; i < 2; ++i) {
-            if (!act[i]) continue;
-            mbar_wait(&bars->p_ready[i], pph[i]);
-            const int kj = (int)(J_hi - prev[i]);
-            const int vs = kj % NV;
-            mbar_wait(&bars->v_full[vs], (kj / NV) & 1);
-            tc_fence_after();
-            if (elect_one()) {
-                const uint32_t vbase = smem_u32(Vs + vs * kTileBytes);
+        // last PV, then O is final
+        mbar_wait(&bars->p_ready, (k - 1) & 1);
+        mbar_wait(&bars->v_full, (k - 1) & 1);
+        tc_fence_after();
+        if (elect_one()) {
 #pragma unroll
-                for (int kk = 0; kk < BN / 16; ++kk)
-                    mma_ts(tmem + 256 + 128 * i, tmem + 128 * i + 8 * kk,
-                           sdesc_sw128(vbase + kk * 2048, kTileBytes / 2, 1024), idesc_pv,
-                           (first_pv[i] && kk == 0) ? 0u : 1u);
-                tc_commit(&bars->o_full[i]);
-            }
-            __syncwarp();
+            for (int kk = 0; kk < BN / 16; ++kk)
+                mma_ts(tmem + 128, tmem + 8 * kk, sdesc_sw128(vbase + kk * 2048, kTileBytes / 2, 1024), idesc_pv,
+                       (k > 1 || kk > 0) ? 1u : 0u);
+            tc_commit(&bars->o_full);
         }
-    } else if (warp < kMmaWarp) {
-        // ------------------------------------------------ softmax warpgroups
-        // tile i = warp >> 3; a row r is shared by two threads (warps w and
-        // w + 4 of the tile, same TMEM lane quadrant), each owning 64 columns
+        __syncwarp();
+    } else if (warp < 4) {
+        // ------------------------------------------------ softmax warpgroup
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kSoftmaxRegs));
-        const int i = warp >> 3;
-        const int hf = (warp >> 2) & 1;  // column half
-        const int r = (warp & 3) * 32 + (threadIdx.x & 31);
-        const int c0 = 64 * hf;
-        if (i == 0 || act1) {
-            const int64_t t = r0 + i * BM + r;
-            const bool valid = t < p.Nq;
-            const int64_t g = t + p.h0;
-            const float* Ubh = p.U + (b * p.H + h) * p.Nkv;
-            // Bias in log2 units relative to a per-CTA reference u (reading C-18):
-            // u_q - u_k = (u_q - uref) - (u_k - uref); each difference is formed in
-            // fp32 before scaling, and the row constant (u_q - uref) cancels in the
-            // softmax, so it only re-enters the LSE.
-            const float uref = Ubh[glo[0]];
-            const float bq = valid ? (Ubh[g] - uref) * kLog2e : 0.f;
-            const uint32_t lane_addr = tmem + ((uint32_t)((warp & 3) * 32) << 16);
-            const uint32_t scol = 128 * i;
-            const uint64_t sl2x2 = f2pack(p.sl2, p.sl2);
-            const int64_t jlo_i = i ? jlo[1] : jlo[0], jhi_i = i ? jhi[1] : jhi[0];
-            const int64_t glo_i = i ? glo[1] : glo[0], ghi_i = i ? ghi[1] : ghi[0];
-            float m_used = -INFINITY, l = 0.f;
-            uint32_t sph = 0;
-            int n = 0;
-            // the hf == 0 half keeps the key-bias vector: u of the next key tile prefetched
-            float u_next = hf == 0 && jhi_i * BN + r < p.Nkv ? Ubh[jhi_i * BN + r] : 0.f;
-            for (int64_t j = jhi_i; j >= jlo_i; --j, ++n) {
-                // -(u_k - uref) log2e of this key tile -> smem (tile-cooperative)
-                named_bar_sync(1 + i, 256);
-                if (hf == 0) {
-                    s_nbk[i][r] = (uref - u_next) * kLog2e;
-                    if (j > jlo_i) u_next = Ubh[(j - 1) * BN + r];
-                }
-                named_bar_sync(1 + i, 256);
-                mbar_wait(&bars->s_full[i], sph);
-                if (n < 8 && r == 0 && hf == 0) GFWA_TR(16 + 24 * i + n);
-                sph ^= 1;
-                tc_fence_after();
-                const bool trw = (i == 0 && n == 1 && hf == 0 && (r == 0 || r == 96));
-                const bool interior = (j * BN + BN - 1 <= glo_i) && (j * BN >= ghi_i - p.w + 1);
-                uint32_t keep[2] = {~0u, ~0u};
-                if (!interior) {
-                    // keys in (g - w, g] and < N_kv, as columns of this tile
-                    const int64_t kb = j * BN;
-                    const int hi = (int)min64(min64(g - kb, (int64_t)BN - 1), p.Nkv - 1 - kb);
-                    const int lo = (int)max64(g - p.w + 1 - kb, (int64_t)0);
+        const int r = threadIdx.x & 127;
+        const int64_t t = r0 + r;
+        const bool valid = t < p.Nq;
+        const int64_t g = t + p.h0;
+        const float* Ubh = p.U + (b * p.H + h) * p.Nkv;
+        // Bias in log2 units relative to a per-CTA reference u (reading C-18):
+        // u_q - u_k = (u_q - uref) - (u_k - uref); each difference is formed in
+        // fp32 before scaling, and the row constant (u_q - uref) cancels in the
+        // softmax, so it only re-enters the LSE.
+        const float uref = Ubh[glo];
+        const float bq = valid ? (Ubh[g] - uref) * kLog2e : 0.f;
+        const uint32_t lane_addr = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+        const uint64_t sl2x2 = f2pack(p.sl2, p.sl2);
+        float m_used = -INFINITY, l = 0.f;
+        int n = 0;
+        float u_next = jhi * BN + r < p.Nkv ? Ubh[jhi * BN + r] : 0.f;
+        for (int64_t j = jhi; j >= jlo; --j, ++n) {
+            // -(u_k - uref) log2e of this key tile -> smem (WG-cooperative); the
+            // next tile's u is prefetched into a register meanwhile
+            named_bar_sync(1, 128);
+            s_nbk[r] = (uref - u_next) * kLog2e;
+            if (j > jlo) u_next = (j - 1) * BN + r < p.Nkv ? Ubh[(j - 1) * BN + r] : 0.f;
+            named_bar_sync(1, 128);
+            mbar_wait(&bars->s_full, n & 1);
+            if (n < 8 && r == 0) GFWA_TR(16 + n);
+            tc_fence_after();
+            const bool trw = (n == 1 && (r == 0 || r == 96));
+            const bool interior = (j * BN + BN - 1 <= glo) && (j * BN >= ghi - p.w + 1);
+            uint32_t keep[4] = {~0u, ~0u, ~0u, ~0u};
+            if (!interior) {
+                // keys in (g - w, g] and < N_kv, as columns of this tile
+                const int64_t kb = j * BN;
+                const int hi = (int)min64(min64(g - kb, (int64_t)BN - 1), p.Nkv - 1 - kb);
+                const int lo = (int)max64(g - p.w + 1 - kb, (int64_t)0);
 #pragma unroll
-                    for (int c = 0; c < 2; ++c) keep[c] = range_bits(lo, hi, c0 + 32 * c);
-                }
-                const float* nbv = s_nbk[i] + c0;
-                // this thread's 64 S values in registers (two loads, one wait), the
-                // logits x = scale*q.k - (u_k - uref) log2e (Alg. 2 l.12-15) in place
-                // as packed pairs; max and exp both run from registers
-                uint32_t raw[64];
-                tmem_ld32(lane_addr + scol + c0, *reinterpret_cast<uint32_t(*)[32]>(raw));
-                tmem_ld32(lane_addr + scol + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(raw + 32));
-                tmem_wait_ld();
-                if (trw) GFWA_TR(10 + (r == 96));
-                uint64_t xp[32];
+                for (int c = 0; c < 4; ++c) keep[c] = range_bits(lo, hi, 32 * c);
+            }
+            // the whole S row in registers: four loads, one wait, then the logits
+            // x = scale*q.k - (u_k - uref) log2e (Alg. 2 l.12-15) in place as
+            // packed pairs; max and exp both run from registers
+            uint32_t raw[BN];
 #pragma unroll
-                for (int e = 0; e < 64; e += 4) {
-                    const float4 nb = *reinterpret_cast<const float4*>(nbv + e);
-                    xp[e / 2] = ffma2(f2pack(__uint_as_float(raw[e]), __uint_as_float(raw[e + 1])), sl2x2,
-                                      f2pack(nb.x, nb.y));
-                    xp[e / 2 + 1] = ffma2(f2pack(__uint_as_float(raw[e + 2]), __uint_as_float(raw[e + 3])), sl2x2,
-                                          f2pack(nb.z, nb.w));
-                }
-                if (!interior) {
+            for (int cb = 0; cb < BN; cb += 32)
+                tmem_ld32(lane_addr + cb, *reinterpret_cast<uint32_t(*)[32]>(raw + cb));
+            tmem_wait_ld();
+            if (trw) GFWA_TR(10 + (r == 96));
+            uint64_t xp[BN / 2];
 #pragma unroll
-                    for (int e = 0; e < 32; ++e) {
-                        const uint32_t kw = keep[e >> 4];
-                        const int bit = 2 * (e & 15);
-                        float a, z;
-                        f2unpack(xp[e], a, z);
-                        a = ((kw >> bit) & 1u) ? a : -INFINITY;
-                        z = ((kw >> (bit + 1)) & 1u) ? z : -INFINITY;
-                        xp[e] = f2pack(a, z);
-                    }
-                }
-                float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+            for (int e = 0; e < BN; e += 4) {
+                const float4 nb = *reinterpret_cast<const float4*>(s_nbk + e);
+                xp[e / 2] = ffma2(f2pack(__uint_as_float(raw[e]), __uint_as_float(raw[e + 1])), sl2x2,
+                                  f2pack(nb.x, nb.y));
+                xp[e / 2 + 1] = ffma2(f2pack(__uint_as_float(raw[e + 2]), __uint_as_float(raw[e + 3])), sl2x2,
+                                      f2pack(nb.z, nb.w));
+            }
+            if (!interior) {
 #pragma unroll
-                for (int e = 0; e < 32; ++e) {
+                for (int e = 0; e < BN / 2; ++e) {
+                    const uint32_t kw = keep[e >> 4];
+                    const int bit = 2 * (e & 15);
                     float a, z;
                     f2unpack(xp[e], a, z);
-                    mx[e & 3] = fmax3(mx[e & 3], a, z);
+                    a = ((kw >> bit) & 1u) ? a : -INFINITY;
+                    z = ((kw >> (bit + 1)) & 1u) ? z : -INFINITY;
+                    xp[e] = f2pack(a, z);
                 }
-                // row max = max over both halves (exchanged through smem)
-                s_mx[i][hf][r] = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
-                if (trw) GFWA_TR(58 + (r == 96));
-                named_bar_sync(3 + i, 256);
-                const float mt = fmaxf(s_mx[i][0][r], s_mx[i][1][r]);
-                if (trw) GFWA_TR(12 + (r == 96));
-                // lazy online softmax: move the reference max only when it grows by
-                // > 2^8 (both halves take the same decision from the same values)
-                float corr = 1.f;
-                bool need = false;
-                if (mt > m_used + kRescaleThreshold) {
-                    if (m_used != -INFINITY) {
-                        corr = ex2(m_used - mt);
-                        need = true;
-                    }
-                    l *= corr;
-                    m_used = mt;
-                }
-                const float mref = (m_used == -INFINITY) ? 0.f : m_used;
-                const uint64_t nm2 = f2pack(-mref, -mref);
-                uint64_t acc[4] = {0, 0, 0, 0};  // packed (0.f, 0.f)
-#pragma unroll
-                for (int cb = 0; cb < 64; cb += 32) {
-                    uint32_t pk[16];
-#pragma unroll
-                    for (int e = 0; e < 16; ++e) {
-                        const uint64_t d = fadd2(xp[cb / 2 + e], nm2);
-                        float p0, p1;
-                        if ((e & 3) < kPolyPairs) {
-                            // part of the exponentials on the FMA pipe: MUFU.EX2 is
-                            // co-critical with the tensor core on B200
-                            f2unpack(exp2_poly2(d), p0, p1);
-                        } else {
-                            float d0, d1;
-                            f2unpack(d, d0, d1);
-                            p0 = ex2(d0);
-                            p1 = ex2(d1);
-                        }
-                        acc[e & 3] = fadd2(acc[e & 3], f2pack(p0, p1));
-                        pk[e] = pack_bf16x2(p0, p1);
-                    }
-                    tmem_st16(lane_addr + scol + (c0 + cb) / 2, pk);  // P (bf16) over the S columns
-                }
-                if (trw) GFWA_TR(14 + (r == 96));
-                {
-                    const uint64_t a01 = fadd2(acc[0], acc[1]), a23 = fadd2(acc[2], acc[3]);
-                    float s0, s1;
-                    f2unpack(fadd2(a01, a23), s0, s1);
-                    l += s0 + s1;  // this half's share of the row sum
-                }
-                // rescale this half of O_i (PV of the previous step is complete: S_full certified it)
-                if (__any_sync(0xffffffffu, need) && n > 0) {
-                    uint32_t ob[32];
-#pragma unroll
-                    for (int c = 0; c < 64; c += 32) {
-                        tmem_ld32(lane_addr + 256 + scol + c0 + c, ob);
-                        tmem_wait_ld();
-#pragma unroll
-                        for (int e = 0; e < 32; ++e) ob[e] = __float_as_uint(__uint_as_float(ob[e]) * corr);
-                        tmem_st32(lane_addr + 256 + scol + c0 + c, ob);
-                    }
-                }
-                tmem_wait_st();
-                if (trw) GFWA_TR(34 + (r == 96));
-                tc_fence_before();
-                __syncwarp();
-                if ((threadIdx.x & 31) == 0) mbar_arrive(&bars->p_ready[i]);
-                if (n < 8 && r == 0 && hf == 0) GFWA_TR(24 + 24 * i + n);
-                if (trw && r == 96) GFWA_TR(38);
             }
-            // epilogue: O / l (Alg. 2 l.19-20) staged in smem (128B swizzle) and
-            // written with TMA stores: bf16 in the tile's own Q slot, fp32 in the
-            // K ring (tile 0: every S MMA precedes O_full[0]) or the V ring (tile 1:
-            // last to finish)
-            s_mx[i][hf][r] = l;
-            mbar_wait(&bars->o_full[i], 0);
-            if (r == 0 && hf == 0) GFWA_TR(32 + 24 * i);
-            tc_fence_after();
-            named_bar_sync(3 + i, 256);
-            const float lt = s_mx[i][0][r] + s_mx[i][1][r];
-            const float inv = lt > 0.f ? 1.f / lt : 0.f;
-            uint8_t* stg_bf = Qs + i * kTileBytes;
-            uint8_t* stg_f = i == 0 ? Ks : Vs;
-            const uint32_t sb = smem_u32(stg_bf), sf = smem_u32(stg_f);
-#pragma unroll 1
-            for (int c = 2 * hf; c < 2 * hf + 2; ++c) {
+            float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+            for (int e = 0; e < BN / 2; ++e) {
+                float a, z;
+                f2unpack(xp[e], a, z);
+                mx[e & 3] = fmax3(mx[e & 3], a, z);
+            }
+            const float mt = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+            if (trw) GFWA_TR(12 + (r == 96));
+            // lazy online softmax: move the reference max only when it grows by > 2^8
+            float corr = 1.f;
+            bool need = false;
+            if (mt > m_used + kRescaleThreshold) {
+                if (m_used != -INFINITY) {
+                    corr = ex2(m_used - mt);
+                    need = true;
+                }
+                l *= corr;
+                m_used = mt;
+            }
+            const float mref = (m_used == -INFINITY) ? 0.f : m_used;
+            const uint64_t nm2 = f2pack(-mref, -mref);
+            uint64_t acc[4] = {0, 0, 0, 0};  // packed (0.f, 0.f)
+#pragma unroll
+            for (int cb = 0; cb < BN; cb += 32) {
+                uint32_t pk[16];
+#pragma unroll
+                for (int e = 0; e < 16; ++e) {
+                    const uint64_t d = fadd2(xp[cb / 2 + e], nm2);
+                    float p0, p1;
+                    if ((e & 3) < kPolyPairs) {
+                        // part of the exponentials on the FMA pipe: MUFU.EX2 is
+                        // co-critical with the tensor core on B200
+                        f2unpack(exp2_poly2(d), p0, p1);
+                    } else {
+                        float d0, d1;
+                        f2unpack(d, d0, d1);
+                        p0 = ex2(d0);
+                        p1 = ex2(d1);
+                    }
+                    acc[e & 3] = fadd2(acc[e & 3], f2pack(p0, p1));
+                    pk[e] = pack_bf16x2(p0, p1);
+                }
+                tmem_st16(lane_addr + cb / 2, pk);  // P (bf16) over the S columns
+            }
+            if (trw) GFWA_TR(14 + (r == 96));
+            {
+                const uint64_t a01 = fadd2(acc[0], acc[1]), a23 = fadd2(acc[2], acc[3]);
+                float s0, s1;
+                f2unpack(fadd2(a01, a23), s0, s1);
+                l += s0 + s1;
+            }
+            // rescale O (PV of the previous step is complete: S_full certified it)
+            if (__any_sync(0xffffffffu, need) && n > 0) {
                 uint32_t ob[32];
-                tmem_ld32(lane_addr + 256 + scol + 32 * c, ob);
-                tmem_wait_ld();
-                float v[32];
 #pragma unroll
-                for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(ob[e]) * inv;
-                // bf16: columns [32c, 32c+32) = half c>>1, 16-B chunks (c&1)*4 + k
+                for (int c = 0; c < D; c += 32) {
+                    tmem_ld32(lane_addr + 128 + c, ob);
+                    tmem_wait_ld();
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const int chunk = ((c & 1) * 4 + k) ^ (r & 7);
-                    uint4 pkv;
-                    pkv.x = pack_bf16x2(v[8 * k + 0], v[8 * k + 1]);
-                    pkv.y = pack_bf16x2(v[8 * k + 2], v[8 * k + 3]);
-                    pkv.z = pack_bf16x2(v[8 * k + 4], v[8 * k + 5]);
-                    pkv.w = pack_bf16x2(v[8 * k + 6], v[8 * k + 7]);
-                    sts128(sb + (c >> 1) * (kTileBytes / 2) + r * 128 + chunk * 16, pkv);
-                }
-                if (p.store_f32) {
-                    // fp32: box c (32 columns, 128 B rows), 16-B pieces k
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) {
-                        const int piece = k ^ (r & 7);
-                        sts128(sf + c * 16384 + r * 128 + piece * 16,
-                               make_uint4(__float_as_uint(v[4 * k]), __float_as_uint(v[4 * k + 1]),
-                                          __float_as_uint(v[4 * k + 2]), __float_as_uint(v[4 * k + 3])));
-                    }
+                    for (int e = 0; e < 32; ++e) ob[e] = __float_as_uint(__uint_as_float(ob[e]) * corr);
+                    tmem_st32(lane_addr + 128 + c, ob);
                 }
             }
-            if (valid && hf == 0) p.LSE[(b * p.H + h) * p.Nq + t] = (m_used + bq + __log2f(lt)) * kLn2;
-            fence_proxy_async();
-            named_bar_sync(1 + i, 256);
-            if (r == 0 && hf == 0) {
-                const int row0 = (int)(r0 + i * BM);
-                for (int half = 0; half < 2; ++half)
-                    tma_store_4d(&mo, stg_bf + half * (kTileBytes / 2), half * 64, (int)h, row0, (int)b);
-                if (p.store_f32)
-                    for (int c = 0; c < 4; ++c) tma_store_4d(&mo32, stg_f + c * 16384, c * 32, (int)h, row0, (int)b);
-                bulk_commit();
-                bulk_wait_read0();  // smem must stay valid until the bulk stores have read it
-                GFWA_TR(33 + 24 * i);
+            tmem_wait_st();
+            if (trw) GFWA_TR(34 + (r == 96));
+            tc_fence_before();
+            __syncwarp();
+            if ((threadIdx.x & 31) == 0) mbar_arrive(&bars->p_ready);
+            if (n < 8 && r == 0) GFWA_TR(24 + n);
+            if (trw && r == 96) GFWA_TR(38);
+        }
+        // epilogue: O / l (Alg. 2 l.19-20) staged in smem (128B swizzle: bf16 in the
+        // Q slot, fp32 in the K and V slots -- all idle once O_full fires) and
+        // written with TMA stores
+        mbar_wait(&bars->o_full, 0);
+        if (r == 0) GFWA_TR(32);
+        tc_fence_after();
+        const float inv = l > 0.f ? 1.f / l : 0.f;
+        const uint32_t sbf = smem_u32(Qs), sf = smem_u32(Ks);
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+            uint32_t ob[32];
+            tmem_ld32(lane_addr + 128 + 32 * c, ob);
+            tmem_wait_ld();
+            float v[32];
+#pragma unroll
+            for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(ob[e]) * inv;
+            // bf16: columns [32c, 32c+32) = half c>>1, 16-B chunks (c&1)*4 + k
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int chunk = ((c & 1) * 4 + k) ^ (r & 7);
+                uint4 pkv;
+                pkv.x = pack_bf16x2(v[8 * k + 0], v[8 * k + 1]);
+                pkv.y = pack_bf16x2(v[8 * k + 2], v[8 * k + 3]);
+                pkv.z = pack_bf16x2(v[8 * k + 4], v[8 * k + 5]);
+                pkv.w = pack_bf16x2(v[8 * k + 6], v[8 * k + 7]);
+                sts128(sbf + (c >> 1) * (kTileBytes / 2) + r * 128 + chunk * 16, pkv);
             }
+            if (p.store_f32) {
+                // fp32: box c (32 columns, 128 B rows), 16-B pieces k
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const int piece = k ^ (r & 7);
+                    sts128(sf + c * 16384 + r * 128 + piece * 16,
+                           make_uint4(__float_as_uint(v[4 * k]), __float_as_uint(v[4 * k + 1]),
+                                      __float_as_uint(v[4 * k + 2]), __float_as_uint(v[4 * k + 3])));
+                }
+            }
+        }
+        if (valid) p.LSE[(b * p.H + h) * p.Nq + t] = (m_used + bq + __log2f(l)) * kLn2;
+        fence_proxy_async();
+        named_bar_sync(1, 128);
+        if (r == 0) {
+            for (int half = 0; half < 2; ++half)
+                tma_store_4d(&mo, Qs + half * (kTileBytes / 2), half * 64, (int)h, (int)r0, (int)b);
+            if (p.store_f32)
+                for (int c = 0; c < 4; ++c) tma_store_4d(&mo32, Ks + c * 16384, c * 32, (int)h, (int)r0, (int)b);
+            bulk_commit();
+            bulk_wait_read0();  // smem must stay valid until the bulk stores have read it
+            GFWA_TR(33);
         }
     }
     tc_fence_before();
     __syncthreads();
     if (warp == kMmaWarp) {
         tc_fence_after();
-        tmem_dealloc(tmem, 512);
+        tmem_dealloc(tmem, 256);
     }
 }
 
-// dynamic smem (+1 KB static s_nbk): 1024 alignment slack + Q, K ring, V ring + barriers
-constexpr size_t kSmemBytes = 1024 + 2 * kTileBytes + (NK + NV) * kTileBytes + sizeof(Bars) + 16;
+// dynamic smem: 1024 alignment slack + Q, K, V + barriers (2 CTAs per SM)
+constexpr size_t kSmemBytes = 1024 + 3 * kTileBytes + sizeof(Bars) + 16;
 
 }  // namespace
 
@@ -539,7 +449,7 @@ gfwa_status_t tc_fwd(const AttnParams& p, cudaStream_t st) {
         cudaFuncSetAttribute(fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
         attr_set = true;
     }
-    dim3 grid((unsigned)((p.Nq + 2 * BM - 1) / (2 * BM)), (unsigned)p.H, (unsigned)p.B);
+    dim3 grid((unsigned)((p.Nq + BM - 1) / BM), (unsigned)p.H, (unsigned)p.B);
     // diagnostics: GFWA_TRACE_FWD=<file> dumps per-CTA clock64 stamps (synchronous)
     const char* trace_file = getenv("GFWA_TRACE_FWD");
     const size_t n_cta = (size_t)grid.x * grid.y * grid.z;
