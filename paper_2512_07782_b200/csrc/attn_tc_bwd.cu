@@ -489,7 +489,46 @@ __global__ void __launch_bounds__(256) bwd_tc_pre_kernel(AttnParams p) {
     *reinterpret_cast<float4*>(p.dQacc + ((b * p.Nq + t) * p.H + h) * D + c) = make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
-// dQ = scale * dQacc -> bf16 (C-3)
+// D = rowsum(O_f32 dO) and zeroing of dQacc, fast path for contiguous O_f32 / dO:
+// a warp per row (grid-stride, 32-bit index math), the zeroing as flat 32-byte stores
+__global__ void __launch_bounds__(256) bwd_tc_pre_flat_kernel(const float* __restrict__ of,
+                                                             const __nv_bfloat16* __restrict__ dO,
+                                                             float* __restrict__ Dv, float* __restrict__ acc,
+                                                             uint32_t rows, uint32_t H, uint32_t Nq) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < rows; row += nw) {
+        const float4 o = __ldcs(reinterpret_cast<const float4*>(of + (size_t)row * D) + lane);
+        const uint2 g2 = __ldcs(reinterpret_cast<const uint2*>(dO + (size_t)row * D) + lane);
+        const float2 g01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&g2.x));
+        const float2 g23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&g2.y));
+        float a = o.x * g01.x + o.y * g01.y + o.z * g23.x + o.w * g23.y;
+        a = warp_sum(a);
+        if (lane == 0) {
+            const uint32_t hh = row % H, bt = row / H, t = bt % Nq, b = bt / Nq;
+            Dv[((size_t)b * H + hh) * Nq + t] = a;
+        }
+        reinterpret_cast<float4*>(acc + (size_t)row * D)[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+}
+
+// dQ = scale * dQacc -> bf16 (C-3), flat fast path for a contiguous dQ: 8 elements
+// per thread (32-byte loads, 16-byte stores), grid-stride, no index division
+__global__ void __launch_bounds__(256) bwd_tc_post_flat_kernel(const float* __restrict__ acc,
+                                                              __nv_bfloat16* __restrict__ dq, int64_t n8, float scale) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
+        const float4 a = __ldcs(reinterpret_cast<const float4*>(acc) + 2 * i);
+        const float4 c = __ldcs(reinterpret_cast<const float4*>(acc) + 2 * i + 1);
+        uint4 o;
+        o.x = pack_bf16x2(a.x * scale, a.y * scale);
+        o.y = pack_bf16x2(a.z * scale, a.w * scale);
+        o.z = pack_bf16x2(c.x * scale, c.y * scale);
+        o.w = pack_bf16x2(c.z * scale, c.w * scale);
+        reinterpret_cast<uint4*>(dq)[i] = o;
+    }
+}
+
+// dQ = scale * dQacc -> bf16 (C-3), general strides
 __global__ void __launch_bounds__(256) bwd_tc_post_kernel(AttnParams p) {
     const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
@@ -531,7 +570,19 @@ gfwa_status_t tc_bwd(const AttnParams& pin, cudaStream_t st, void* ws) {
     const unsigned rgrid = (unsigned)((rows + 7) / 8);
     if (gfwa_status_t s = check_launch(cudaMemsetAsync(p.dU, 0, (size_t)p.B * p.H * p.Nkv * sizeof(float), st)))
         return s;
-    bwd_tc_pre_kernel<<<rgrid, 256, 0, st>>>(p);
+    static int n_sm = 0;
+    if (n_sm == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const bool o_flat = p.Ofp && p.os[2] == D && p.os[1] == p.H * D && p.os[0] == p.Nq * p.H * D &&
+                        rows < ((int64_t)1 << 31);
+    if (o_flat)
+        bwd_tc_pre_flat_kernel<<<(unsigned)min64((rows + 7) / 8, (int64_t)n_sm * 16), 256, 0, st>>>(
+            p.Ofp, (const __nv_bfloat16*)p.dO, p.Dv, p.dQacc, (uint32_t)rows, (uint32_t)p.H, (uint32_t)p.Nq);
+    else
+        bwd_tc_pre_kernel<<<rgrid, 256, 0, st>>>(p);
     note_launch();
     if (gfwa_status_t s = check_launch()) return s;
     TcBwdParams tp;
@@ -573,7 +624,14 @@ gfwa_status_t tc_bwd(const AttnParams& pin, cudaStream_t st, void* ws) {
         }
     }
     if (gfwa_status_t s = check_launch()) return s;
-    bwd_tc_post_kernel<<<rgrid, 256, 0, st>>>(p);
+    const bool dq_flat = p.qs[2] == D && p.qs[1] == p.H * D && p.qs[0] == p.Nq * p.H * D;
+    if (dq_flat) {
+        const int64_t n8 = rows * D / 8;
+        const unsigned g = (unsigned)min64((n8 + 255) / 256, (int64_t)n_sm * 8);
+        bwd_tc_post_flat_kernel<<<g, 256, 0, st>>>(p.dQacc, (__nv_bfloat16*)p.dQ, n8, p.scale);
+    } else {
+        bwd_tc_post_kernel<<<rgrid, 256, 0, st>>>(p);
+    }
     note_launch();
     return check_launch();
 }

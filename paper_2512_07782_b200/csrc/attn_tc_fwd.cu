@@ -30,7 +30,7 @@
 #include <vector>
 
 #ifndef GFWA_FWD_POLY
-#define GFWA_FWD_POLY 1
+#define GFWA_FWD_POLY 0
 #endif
 
 #include "attn_common.cuh"
