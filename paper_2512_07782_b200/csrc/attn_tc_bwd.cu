@@ -20,7 +20,8 @@
 // runs (the paper writes dQ back per tile).  du^k (column sum, C-4)
 // accumulates per key thread; du^q (the paper's rowsum(dS), kept per
 // C-11) is a cross-thread sum over keys done in fp32 with a warp butterfly
-// transpose-reduce, so both sums see the same fp32 dS and sum_m dU_m
+// transpose-reduce (after dS is handed to the MMA warp) and a cross-warp sum by
+// the drain warpgroup, so both sums see the same fp32 dS and sum_m dU_m
 // telescopes to zero.  dK, dV leave through smem + TMA stores.
 #include <vector>
 
@@ -37,11 +38,15 @@ constexpr int BN = 128;   // keys per CTA
 constexpr int BMQ = 64;   // queries per step
 constexpr int D = 128;
 constexpr int NQS = 3;    // Q/dO ring stages
-constexpr uint32_t kDQ = 32 * 128 * 4;    // 16 KB dQ staging: 32 queries x 128 d fp32
+constexpr uint32_t kDQ = 32 * 128 * 4;    // 16 KB dQ staging: 4 warps x 2 x (16 queries x 32 d) fp32
+constexpr uint32_t kDQW = 16 * 32 * 4;    // 2 KB: one drain warp's box
 constexpr uint32_t kKV = 128 * 128 * 2;   // 32 KB K or V tile
 constexpr uint32_t kQT = 64 * 128 * 2;    // 16 KB Q or dO tile
 constexpr uint32_t kDS = 128 * 64 * 2;    // 16 KB dS^T tile
 constexpr int kThreads = 448;             // 2 softmax-grad WGs, drain WG, MMA warp, TMA warp
+#ifndef GFWA_BWD_NODQ
+#define GFWA_BWD_NODQ 0  // experiment only: skip the dQ reductions
+#endif
 #ifndef GFWA_BWD_POLY
 #define GFWA_BWD_POLY 0
 #endif
@@ -68,7 +73,7 @@ struct TcBwdParams {
 struct __align__(8) Bars {
     uint64_t kv_full;
     uint64_t q_full[NQS], q_empty[NQS];
-    uint64_t st_full[2], ds_ready[2], dq_full[2], dq_drained[2];
+    uint64_t st_full[2], ds_ready[2], dq_full[2], dq_drained[2], red_ready[2], red_free[2];
     uint64_t dkdv_full;
 };
 
@@ -95,7 +100,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* Vs = Ks + kKV;
     uint8_t* Qs = Vs + kKV;              // NQS stages of [Q tile | dO tile]
     uint8_t* dSs = Qs + NQS * 2 * kQT;   // 2 x dS^T tile
-    uint8_t* dQs = dSs + 2 * kDS;        // dQ staging: 4 x [32 queries][32 d] fp32, 128B swizzle
+    uint8_t* dQs = dSs + 2 * kDS;        // dQ staging: per drain warp 2 x [16 queries][32 d] fp32, 128B swizzle
     Bars* bars = (Bars*)(dQs + kDQ);
     uint32_t* tmem_sh = (uint32_t*)(bars + 1);
     __shared__ __align__(16) float s_cq[NQS][BMQ];    // (u_q - uref) log2e - L_q log2e
@@ -124,6 +129,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&bars->ds_ready[i], 8);
             mbar_init(&bars->dq_full[i], 1);
             mbar_init(&bars->dq_drained[i], 4);
+            mbar_init(&bars->red_ready[i], 8);
+            mbar_init(&bars->red_free[i], 2);
         }
         mbar_init(&bars->dkdv_full, 1);
         fence_barrier_init();
@@ -327,7 +334,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                            make_uint4(dk[4 * c], dk[4 * c + 1], dk[4 * c + 2], dk[4 * c + 3]));
             }
             if (trw) GFWA_TR(45);
-            // du^q partial over this warp's 32 keys: butterfly transpose-reduce -> lane l holds query 32 wg + l
+            tmem_wait_st();
+            fence_proxy_async();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bars->ds_ready[bn]);
+            if (n < 8 && threadIdx.x == 0) GFWA_TR(9 + n);
+            if (trw) GFWA_TR(46);
+            // du^q partial over this warp's 32 keys, off the MMA's critical path (the
+            // gradient contractions of step n are already running): butterfly
+            // transpose-reduce -> lane l holds query 32 wg + l; the drain warpgroup
+            // sums the 4 warps' partials and issues the red.add (C-11)
 #pragma unroll
             for (int sft = 16; sft >= 1; sft >>= 1) {
                 const bool up = lane & sft;
@@ -338,24 +355,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ds[e] = keepv + __shfl_xor_sync(0xffffffffu, send, sft);
                 }
             }
-            s_red[n & 1][wg][warp & 3][lane] = ds[0];
-            if (trw) GFWA_TR(46);
-            tmem_wait_st();
-            fence_proxy_async();
-            tc_fence_before();
+            if (n >= 2) mbar_wait(&bars->red_free[bn], ((n - 2) >> 1) & 1);
+            s_red[bn][wg][warp & 3][lane] = ds[0];
             __syncwarp();
-            if (lane == 0) mbar_arrive(&bars->ds_ready[bn]);
+            if (lane == 0) mbar_arrive(&bars->red_ready[bn]);
             if (trw) GFWA_TR(47);
-            if (n < 8 && threadIdx.x == 0) GFWA_TR(9 + n);
-            // du^q_t += rowsum(dS) at key position t + h0 (C-11): combine the WG's 4 warps
-            named_bar_sync(1 + wg, 128);
-            if (kr < 32) {
-                const int64_t t = t0 + 32 * wg + kr;
-                const float rs = s_red[n & 1][wg][0][kr] + s_red[n & 1][wg][1][kr] + s_red[n & 1][wg][2][kr] +
-                                 s_red[n & 1][wg][3][kr];
-                if (t < p.Nq) red_add(p.dU + (b * p.H + h) * p.Nkv + t + p.h0, rs);
-                if (trw) GFWA_TR(48);
-            }
         }
         {
             float c0, c1;
@@ -404,13 +408,29 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp < 12) {
         // ------------------------------------------------ dQ drain: thread = head-dim lane
-        // dQ^T (TMEM, lane = d) -> smem [64 queries][128 d] fp32 (4 boxes of 32 d,
-        // 128B swizzle) -> TMA bulk reduce-add into the fp32 dQ accumulator: the
-        // L2 does the adds, no per-thread atomics.
+        // dQ^T (TMEM, lane = d) -> smem [16 queries][32 d] fp32 boxes (128B swizzle) ->
+        // TMA bulk reduce-add into the fp32 dQ accumulator: the L2 does the adds, no
+        // per-thread atomics.  Each drain warp stages its own 32 d (double-buffered
+        // 2 KB boxes) and issues its own reduces, so no cross-warp barrier.
         const int dl = threadIdx.x - 256;  // 0..127
         const uint32_t lane_addr = tmem + ((uint32_t)((warp & 3) * 32) << 16);
         const uint32_t qcol[4] = {64, 80, 96, 112};  // dQ^T: columns [64,128) of the buffer
-        const uint32_t sq = smem_u32(dQs) + (dl >> 5) * (kDQ / 4);  // this lane's 32-d box (4 KB)
+        uint8_t* wbox = dQs + (warp & 3) * 2 * kDQW;
+        // du^q_t += rowsum(dS) at key position t + h0 (C-11): the 4 per-warp
+        // partials of each softmax-grad warpgroup (threads dl < 64, one query each)
+        auto combine_duq = [&](int mm) {
+            if (dl < BMQ) {
+                const int bq = mm & 1;
+                mbar_wait(&bars->red_ready[bq], (mm >> 1) & 1);
+                const int wq = dl >> 5, lq = dl & 31;
+                const float rs =
+                    s_red[bq][wq][0][lq] + s_red[bq][wq][1][lq] + s_red[bq][wq][2][lq] + s_red[bq][wq][3][lq];
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bars->red_free[bq]);
+                const int64_t t = (qt_lo + mm) * BMQ + dl;
+                if (t < p.Nq) red_add(p.dU + (b * p.H + h) * p.Nkv + t + p.h0, rs);
+            }
+        };
         for (int m = 0; m < nsteps; ++m) {
             const int bm = m & 1;
             const int64_t t0 = (qt_lo + m) * BMQ;
@@ -426,30 +446,28 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&bars->dq_drained[bm]);
             if (m < 8 && dl == 0) GFWA_TR(33 + m);
-            // two rounds of 32 queries through a 16 KB staging buffer;
-            // row = query, 16-B chunk (d%32)/4 ^ (query%8), word d%4
+            if (m > 0) combine_duq(m - 1);  // the previous step's partials are in smem by now
+            // four rounds of 16 queries; row = query (128 B = this warp's 32 d),
+            // 16-B chunk (d%32)/4 ^ (query%8), word d%4
 #pragma unroll
-            for (int half = 0; half < 2; ++half) {
-                if (dl == 0) bulk_wait_read0();  // the previous bulk reduce has read the buffer
-                named_bar_sync(3, 128);
+            for (int r = 0; r < 4; ++r) {
+                if (lane == 0) bulk_wait_read1();  // the reduce two rounds back has read this box
+                __syncwarp();
+                const uint32_t sq = smem_u32(wbox + (r & 1) * kDQW);
 #pragma unroll
-                for (int qq = 2 * half; qq < 2 * half + 2; ++qq)
-#pragma unroll
-                    for (int e = 0; e < 16; ++e) {
-                        const int q = 16 * (qq & 1) + e;  // row within the 32-query round
-                        sts32(sq + q * 128 + ((((dl & 31) >> 2) ^ (q & 7)) << 4) + (dl & 3) * 4,
-                              __uint_as_float(v[qq][e]));
-                    }
+                for (int e = 0; e < 16; ++e)
+                    sts32(sq + e * 128 + ((((lane >> 2) ^ e) & 7) << 4) + (lane & 3) * 4, __uint_as_float(v[r][e]));
                 fence_proxy_async();
-                named_bar_sync(3, 128);
-                if (dl == 0) {
-                    for (int c = 0; c < 4; ++c)
-                        tma_reduce_add_4d(&mdq, dQs + c * (kDQ / 4), c * 32, (int)h, (int)(t0 + 32 * half), (int)b);
+                __syncwarp();
+                if (lane == 0 && !GFWA_BWD_NODQ) {
+                    tma_reduce_add_4d(&mdq, wbox + (r & 1) * kDQW, 32 * (warp & 3), (int)h, (int)(t0 + 16 * r), (int)b);
                     bulk_commit();
                 }
             }
+            if (m < 8 && dl == 0) GFWA_TR(49 + m);
         }
-        if (dl == 0) bulk_wait0();  // reductions complete before the CTA exits
+        if (nsteps > 0) combine_duq(nsteps - 1);
+        if (lane == 0) bulk_wait0();  // reductions complete before the CTA exits
     }
     tc_fence_before();
     __syncthreads();
@@ -565,7 +583,7 @@ gfwa_status_t tc_bwd(const AttnParams& pin, cudaStream_t st, void* ws) {
     GFWA_REQUIRE(encode_bnhd_map(&mdk, p.dK, p.B, p.Nkv, p.H, D, p.ks, BN));
     GFWA_REQUIRE(encode_bnhd_map(&mdv, p.dV, p.B, p.Nkv, p.H, D, p.vs, BN));
     const int64_t acc_s[3] = {p.Nq * p.H * D, p.H * D, D};  // dQacc [B, Nq, H, d] fp32
-    GFWA_REQUIRE(encode_bnhd_map_f32(&mdq, p.dQacc, p.B, p.Nq, p.H, D, acc_s, 32));
+    GFWA_REQUIRE(encode_bnhd_map_f32(&mdq, p.dQacc, p.B, p.Nq, p.H, D, acc_s, 16));
     const int64_t rows = p.B * p.Nq * p.H;
     const unsigned rgrid = (unsigned)((rows + 7) / 8);
     if (gfwa_status_t s = check_launch(cudaMemsetAsync(p.dU, 0, (size_t)p.B * p.H * p.Nkv * sizeof(float), st)))

@@ -43,4 +43,22 @@ inline bool encode_bnhd_map_f32(CUtensorMap* map, const void* base, int64_t B, i
     return r == CUDA_SUCCESS;
 }
 
+// fp32 [B, H, d, Nq] map (queries contiguous, row pitch nq_pitch elements, a
+// multiple of 4) with box {32 queries (128 B), d rows, 1, 1}, 128B swizzle: the
+// transposed dQ accumulator of the tensor-core backward (a drain thread owns one
+// d row of the dQ^T tile, so it stages whole 16-byte query runs).
+inline bool encode_bhdn_map_f32(CUtensorMap* map, const void* base, int64_t B, int64_t H, int d, int64_t Nq,
+                                int64_t nq_pitch, int box_q = 32, int box_d = 0) {
+    cuuint64_t dims[4] = {(cuuint64_t)Nq, (cuuint64_t)d, (cuuint64_t)H, (cuuint64_t)B};
+    cuuint64_t strides[3] = {(cuuint64_t)(nq_pitch * 4), (cuuint64_t)(nq_pitch * 4 * d),
+                             (cuuint64_t)(nq_pitch * 4 * d * H)};
+    cuuint32_t box[4] = {(cuuint32_t)box_q, (cuuint32_t)(box_d > 0 ? box_d : d), 1u, 1u};
+    cuuint32_t estr[4] = {1u, 1u, 1u, 1u};
+    CUresult r = drv::tensorMapEncodeTiled(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<void*>(base), dims,
+                                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                        box_q == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 }  // namespace gfwa

@@ -15,10 +15,12 @@ for n in (0, 1, 2, 4):
     stat(f"step{n}: MMA2 start -> dq_full", dq[:, n] - m2[:, n])
     stat(f"step{n}: drain (dq_full->drained)", dr[:, n] - dq[:, n])
     stat(f"step{n}: st(n) -> st(n+1)", st[:, n + 1] - st[:, n])
+    stat(f"step{n}: drain staging+reduce issue", t[:, 49 + n] - dr[:, n])
+    stat(f"step{n}: drain loop (dq_full n -> n+1)", dq[:, n + 1] - dq[:, n])
 stat("last MMA2 -> dkdv_full", t[:, 41] - np.nanmax(m2, axis=1))
 stat("epilogue", t[:, 42] - t[:, 41])
 stat("total", t[:, 42] - start)
 s4 = t[:, 1 + 4]
 for name, a, b in (("st_full->LDTM done", s4, t[:, 43]), ("compute", t[:, 43], t[:, 44]), ("STTM+STS", t[:, 44], t[:, 45]),
-                   ("butterfly", t[:, 45], t[:, 46]), ("wait_st+fence+arrive", t[:, 46], t[:, 47]), ("combine", t[:, 47], t[:, 48])):
+                   ("wait_st+fence+arrive", t[:, 45], t[:, 46]), ("butterfly+partials", t[:, 46], t[:, 47])):
     stat("step4 sg: " + name, b - a)
