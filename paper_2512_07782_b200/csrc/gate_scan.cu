@@ -42,6 +42,7 @@ struct ScanGeom {
     int log_t;     // log2 tokens per chunk (128 <= T <= 1024, so 4 <= R <= 32)
     int n_hgroups; // ceil(H / HG)
     int n_chunks;  // ceil(N / T)
+    int n_seq;     // B * n_hgroups independent scans
 };
 
 ScanGeom scan_geom(int64_t B, int64_t N, int64_t H) {
@@ -57,6 +58,7 @@ ScanGeom scan_geom(int64_t B, int64_t N, int64_t H) {
            (int64_t)g.n_hgroups * ((N + (1 << g.log_t) - 1) >> g.log_t) * B < kMinBlocks * 148)
         --g.log_t;
     g.n_chunks = (int)((N + (1 << g.log_t) - 1) >> g.log_t);
+    g.n_seq = (int)(B * g.n_hgroups);
     return g;
 }
 
@@ -185,8 +187,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) gate_prefix_kernel(
     if (tid == 0) s_ticket = atomicAdd(lb.ticket, 1u);
     __syncthreads();
     const unsigned tk = s_ticket;
-    const int c = (int)(tk % g.n_chunks);
-    const int rest = (int)(tk / g.n_chunks);
+    // chunk-outer ticket order: a wave spans every sequence's leading chunks, so
+    // look-back chains are as short as the wave allows
+    const int c = (int)(tk / (unsigned)g.n_seq);
+    const int rest = (int)(tk % (unsigned)g.n_seq);
     const int hg = rest % g.n_hgroups;
     const int b = rest / g.n_hgroups;
     const int T = 1 << g.log_t, log_r = g.log_t - 5, R = T >> 5;
@@ -338,9 +342,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) gate_prefix_bwd_kernel(
     if (tid == 0) s_ticket = atomicAdd(lb.ticket, 1u);
     __syncthreads();
     const unsigned tk = s_ticket;
-    const int rc = (int)(tk % g.n_chunks);  // order of processing: right to left
+    const int rc = (int)(tk / (unsigned)g.n_seq);  // order of processing: right to left, chunk-outer
     const int c = g.n_chunks - 1 - rc;
-    const int rest = (int)(tk / g.n_chunks);
+    const int rest = (int)(tk % (unsigned)g.n_seq);
     const int hg = rest % g.n_hgroups;
     const int b = rest / g.n_hgroups;
     const int T = 1 << g.log_t, log_r = g.log_t - 5, R = T >> 5;
