@@ -153,3 +153,50 @@ def test_zero_grad_out_and_invariants():
     dQ, dK, dV, dU, da = gb.gfwa_bwd(Q, K, V, U, O, LSE, dO, s.w, O_f32=O32)
     assert dU.double().sum(-1).abs().max().item() <= 1e-3 * dU.abs().max().item()
     assert da[..., 0].abs().max().item() <= 1e-3 * da.abs().max().item()
+
+
+def _sampled_full_size(s: synth.AttnShape, seed: int, n_rows: int, bwd_slices, halo: int = 0):
+    """Forward on sampled rows across all slices, fwd+bwd in full on the given
+    (b, h) slices, at a BASELINE shape in the launch configuration bench.py times."""
+    Q, K, V, dO = synth.attn_inputs(s, seed=seed, device="cuda", dtype=torch.bfloat16)
+    h, beta = synth.gate_inputs(s.B, s.nkv, s.H, seed=seed, device="cuda")
+    U = gb.gfwa_gate_prefix(h, beta)
+    O, LSE, O32 = gb.gfwa_fwd(Q, K, V, U, s.w, want_o_f32=True)
+    dQ, dK, dV, dU, da = gb.gfwa_bwd(Q, K, V, U, O, LSE, dO, s.w, O_f32=O32)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(seed)
+    rows = np.stack([rng.integers(0, s.B, n_rows), rng.integers(0, s.H, n_rows), rng.integers(0, s.N, n_rows)], 1)
+    rows[:4, 2] = [0, 1, min(s.w, s.N) - 1, s.N - 1]
+    o_r, l_r = oracle.fwd_rows(Q, K, V, U, s.w, rows)
+    o_g = np64(O)[rows[:, 0], rows[:, 2], rows[:, 1]]
+    l_g = np64(LSE)[rows[:, 0], rows[:, 1], rows[:, 2]]
+    assert np.abs(o_g - o_r).max() <= TOL_BF16_O
+    assert np.abs(l_g - l_r).max() <= TOL_LSE
+    for b, hh in bwd_slices:
+        sl = lambda x: x[b:b + 1, :, hh:hh + 1]  # noqa: E731
+        Ur = U[b:b + 1, hh:hh + 1]
+        g = oracle.bwd(sl(Q), sl(K), sl(V), Ur, sl(dO), s.w)
+        for k, t in (("dQ", dQ), ("dK", dK), ("dV", dV)):
+            assert max_abs(sl(t), g[k]) <= TOL_BF16_GRAD, k
+        assert max_abs(dU[b:b + 1, hh:hh + 1], g["dU"]) <= TOL_BF16_GRAD
+        # d-alpha sums up to N per-row gradients (reading C-22)
+        tol_da = TOL_BF16_GRAD * max(1.0, (s.nkv / 1024) ** 0.5)
+        assert max_abs(da[b:b + 1, hh:hh + 1], g["dalpha"]) <= tol_da
+
+
+@pytest.mark.parametrize("wl", ["C3_w128", "C3_w512", "C3_w2048"])
+def test_c3_window_sweep_full_size_sampled(wl):
+    """BASELINE configs[2] (H=32, N=8192, d=128, w in {128, 512, 2048}, bf16)."""
+    c = synth.CONFIGS[wl]
+    s = synth.AttnShape(B=c["B"], H=c["H"], N=c["N"], d=c["d"], w=c["w"])
+    slices = [(0, 0), (0, c["H"] - 1)] if c["w"] <= 512 else [(0, c["H"] - 1)]  # oracle bwd is O(N w d)
+    _sampled_full_size(s, c["seed"], 64, slices)
+
+
+def test_c4_rank_shard_full_size_sampled():
+    """BASELINE configs[3] at P=8: one rank's launch (S = 16384 query rows after a
+    w = 2048 halo, N_kv = S + w, H = 32) -- the call the sequence-sharded step makes."""
+    c = synth.CONFIGS["C4"]
+    S = c["N"] // 8
+    s = synth.AttnShape(B=c["B"], H=c["H"], N=S, d=c["d"], w=c["w"], N_kv=S + c["w"])
+    _sampled_full_size(s, c["seed"], 64, [(0, 5)])
