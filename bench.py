@@ -256,7 +256,7 @@ def run_ours(args):
     dom_flops = flops_bwd if dom == "bwd" else flops_fwd
     achieved = dom_flops / (parts[dom] * 1e-3) / 1e12
     path = gb.gfwa_attn_path(Q, K, V, s.w)
-    traffic = _traffic_from_profiles(dom)
+    traffic = _traffic_from_profiles(dom, args.workload)
     roofline = {"kernel": f"gfwa_{dom} ({'tcgen05' if path == 1 else 'simt'})", "bound": "tensor",
                 "achieved": round(achieved, 2), "peak": peaks["bf16_sus"], "unit": "TFLOP/s",
                 "frac": round(achieved / peaks["bf16_sus"], 4), "traffic": traffic,
@@ -376,11 +376,12 @@ def run_seq(args):
     }), flush=True)
 
 
-def _traffic_from_profiles(kind: str):
-    """dram bytes per launch from the committed ncu summary (profiles/traffic.json)."""
+def _traffic_from_profiles(kind: str, workload: str):
+    """dram bytes per launch of this workload's call from the committed ncu summary
+    (profiles/traffic.json, one entry per workload); null if that workload was not profiled."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            return json.load(f).get(kind)
+            return json.load(f).get(workload, {}).get(kind)
     except Exception:
         return None
 

@@ -23,6 +23,8 @@
 // parameter (power of two), so all tile index math is shifts and masks.  The
 // backward runs the same machinery right to left on dU and fuses the
 // chain rule into dh, dbeta.
+#include <cstdio>
+#include <cstdlib>
 #include <algorithm>
 #include <type_traits>
 
@@ -35,6 +37,9 @@ constexpr int kThreads = 256;  // 8 warps
 constexpr int kWarps = kThreads / 32;
 constexpr int kMinBlocks = 4;  // resident CTAs per SM (64 registers / thread)
 constexpr unsigned kFull = 0xffffffffu;
+#ifndef GFWA_GATE_SMALL_LOG
+#define GFWA_GATE_SMALL_LOG 22  // below 2^22 (b, t, h) elements the scan is latency-bound
+#endif
 
 struct ScanGeom {
     int HG;        // heads per CTA (<= 32)
@@ -48,6 +53,21 @@ struct ScanGeom {
 ScanGeom scan_geom(int64_t B, int64_t N, int64_t H) {
     ScanGeom g;
     g.HG = H >= 32 ? 32 : (int)H;
+    const char* ge = getenv("GFWA_GATE_GEOM");  // experiments: "log2(HG),log2(T)"
+    if (ge || B * N * H < ((int64_t)1 << GFWA_GATE_SMALL_LOG)) {
+        // latency regime (LM shapes): the look-back chain, not HBM, sets the time,
+        // so use long chunks (T = 512, measured best of 128..1024) and narrow 4-head groups for parallelism
+        int lh = 2, lt = 9;
+        if (ge) sscanf(ge, "%d,%d", &lh, &lt);
+        g.HG = (int)std::min<int64_t>(H, (int64_t)1 << lh);
+        g.log_hgp = 0;
+        while ((1 << g.log_hgp) < g.HG) ++g.log_hgp;
+        g.log_t = std::max(7, std::min(lt, std::min(10, 13 - g.log_hgp)));
+        g.n_hgroups = (int)((H + g.HG - 1) / g.HG);
+        g.n_chunks = (int)((N + (1 << g.log_t) - 1) >> g.log_t);
+        g.n_seq = (int)(B * g.n_hgroups);
+        return g;
+    }
     g.log_hgp = 0;
     while ((1 << g.log_hgp) < g.HG) ++g.log_hgp;
     g.log_t = std::min(10, 13 - g.log_hgp);  // T * HGP <= 8192 elements per tile

@@ -1,7 +1,7 @@
 """Summarise an ncu launch list (gpu__time_duration + dram bytes per launch) by
 kernel, and optionally write profiles/traffic.json for bench.py's roofline.
 
-  python tools/ncu_launches.py gpurun_out/r01/launches_bench.csv [--traffic profiles/traffic.json]
+  python tools/ncu_launches.py gpurun_out/r01/launches_bench.csv [--traffic profiles/traffic.json [--workload C2]]
 """
 import collections
 import csv
@@ -41,7 +41,14 @@ def main():
         tr = {k: int(v) for k, v in tr.items() if v}
         tr["_note"] = ("dram__bytes_read.sum + dram__bytes_write.sum per launch of the gfwa_fwd / gfwa_bwd call "
                        "(sum over the call's kernels), from " + sys.argv[1])
-        json.dump(tr, open(path, "w"), indent=1)
+        wl = sys.argv[sys.argv.index("--workload") + 1] if "--workload" in sys.argv else "C2"
+        try:
+            allt = json.load(open(path))
+        except Exception:
+            allt = {}
+        allt = {k: v for k, v in allt.items() if isinstance(v, dict)}  # per-workload entries only
+        allt[wl] = tr
+        json.dump(allt, open(path, "w"), indent=1)
         print("wrote", path, tr)
 
 
