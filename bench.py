@@ -490,9 +490,28 @@ def run_aux(dev, peaks):
     e1.record()
     torch.cuda.synchronize(dev)
     ms2 = e0.elapsed_time(e1) / n
-    out["gate_preproc_compare_G"] = {"pytorch_two_kernel_ms": round(ms2, 4), "fused_scan_ms": round(ms, 4),
-                                     "speedup": round(ms2 / ms, 2),
-                                     "paper_context": "A100 Triton: 1-pass 0.3 ms vs PyTorch 2.9 ms at N=64K (P:527)"}
+    # the paper's own two designs on B200 (C ABI comparison variants): 1-pass with one
+    # program per head and an on-chip carry, Scan-Then-Propagate (App. E.1)
+    var_ms = {}
+    for v in (1, 2):
+        for _ in range(3):
+            gb.gfwa_gate_prefix_variant(v, h, beta)
+        torch.cuda.synchronize(dev)
+        e0.record()
+        for _ in range(n):
+            gb.gfwa_gate_prefix_variant(v, h, beta)
+        e1.record()
+        torch.cuda.synchronize(dev)
+        var_ms[v] = e0.elapsed_time(e1) / n
+    gel = lambda t: round(elems / (t * 1e-3) / 1e9, 2)  # noqa: E731  (b, t, h) elements/s, G
+    out["gate_preproc_compare_G"] = {
+        "pytorch_two_kernel_ms": round(ms2, 4), "one_program_per_head_ms": round(var_ms[1], 4),
+        "scan_then_propagate_ms": round(var_ms[2], 4), "decoupled_lookback_ms": round(ms, 4),
+        "G_elems_per_s": {"pytorch_two_kernel": gel(ms2), "one_program_per_head": gel(var_ms[1]),
+                          "scan_then_propagate": gel(var_ms[2]), "decoupled_lookback": gel(ms)},
+        "speedup_vs_pytorch": round(ms2 / ms, 2),
+        "paper_context": ("A100 Triton: 1-pass 0.3 ms vs PyTorch 2.9 ms at N=64K (P:527); "
+                          "1-pass ~28.5 vs Scan-Then-Propagate ~20.1 billion tokens/s (P:1061)")}
     return out
 
 

@@ -102,6 +102,28 @@ gfwa_status_t gfwa_gate_prefix_bwd(gfwa_gate_kind_t kind, gfwa_dtype_t in_dtype,
                                    const float* dU, const double* carry, float* dalpha, void* dh,
                                    void* dbeta, void* ws, size_t ws_bytes, gfwa_stream_t stream);
 
+/*
+ * gfwa_gate_prefix_variant -- the two preprocessing designs the paper compares
+ * its kernel with, for the benchmark of SURVEY §8(f) f2.  NOT
+ * the product path: same output as gfwa_gate_prefix with GATE_HBETA and no
+ * carry (U[b,hh,t] = -sum_{q<=t} alpha, fp32 in-run / fp64 across runs, C-9).
+ *   variant 1  Alg. 1 as the paper launches it: one CTA per (b, head)
+ *              walking the time axis in 1024-token chunks with an on-chip
+ *              carry (serial across chunks); reads h, beta once.
+ *   variant 2  Scan-Then-Propagate, App. E.1: chunk sums, a scan
+ *              of the chunk sums, then a re-read of h, beta that writes U;
+ *              H <= 32 (else GFWA_ERR_UNSUPPORTED).
+ * h, beta    [B, N, H] in in_dtype (GFWA_BF16 or GFWA_F32); U [B, H, N] fp32.
+ * ws         >= gfwa_gate_prefix_variant_workspace_size(variant, B, N, H)
+ *            bytes (variant 2: chunk sums and offsets, fp64); caller-owned.
+ * Errors: INVALID_ARGUMENT (variant not 1/2, null pointers, sizes < 1),
+ * UNSUPPORTED (dtype, H > 32 for variant 2), WORKSPACE, CUDA.
+ */
+size_t gfwa_gate_prefix_variant_workspace_size(int variant, int64_t B, int64_t N, int64_t H);
+gfwa_status_t gfwa_gate_prefix_variant(int variant, gfwa_dtype_t in_dtype, const void* h, const void* beta,
+                                       int64_t B, int64_t N, int64_t H, float eps, float* U, void* ws,
+                                       size_t ws_bytes, gfwa_stream_t stream);
+
 /* ------------------------------------------------------------------------- */
 /* Attention: Alg. 2 (forward) and Alg. E.2 (backward) */
 /* ------------------------------------------------------------------------- */

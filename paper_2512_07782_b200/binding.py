@@ -70,6 +70,8 @@ _I64 = ctypes.c_int64
 
 EXPORTED = (
     "gfwa_gate_prefix",
+    "gfwa_gate_prefix_variant",
+    "gfwa_gate_prefix_variant_workspace_size",
     "gfwa_gate_prefix_workspace_size",
     "gfwa_gate_prefix_bwd",
     "gfwa_gate_prefix_bwd_workspace_size",
@@ -106,6 +108,11 @@ def load() -> ctypes.CDLL:
         lib.gfwa_gate_prefix_bwd.restype = ctypes.c_int
         lib.gfwa_gate_prefix_bwd.argtypes = [ctypes.c_int, ctypes.c_int, _VP, _VP, _I64, _I64, _I64,
                                              ctypes.c_float, _VP, _VP, _VP, _VP, _VP, _VP, sz, _VP]
+        lib.gfwa_gate_prefix_variant_workspace_size.restype = sz
+        lib.gfwa_gate_prefix_variant_workspace_size.argtypes = [ctypes.c_int, _I64, _I64, _I64]
+        lib.gfwa_gate_prefix_variant.restype = ctypes.c_int
+        lib.gfwa_gate_prefix_variant.argtypes = [ctypes.c_int, ctypes.c_int, _VP, _VP, _I64, _I64, _I64,
+                                                 ctypes.c_float, _VP, _VP, sz, _VP]
         lib.gfwa_fwd.restype = ctypes.c_int
         lib.gfwa_fwd.argtypes = [ctypes.POINTER(AttnDesc), _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP]
         lib.gfwa_bwd_workspace_size.restype = sz
@@ -215,6 +222,25 @@ def gfwa_gate_prefix(h: torch.Tensor, beta: torch.Tensor | None = None, eps: flo
                               _ptr(total), _ptr(ws), nbytes, _stream(h.device))
     _check(st, "gfwa_gate_prefix")
     return (U, total) if want_total else U
+
+
+def gfwa_gate_prefix_variant(variant: int, h: torch.Tensor, beta: torch.Tensor, eps: float = 1e-6):
+    """U [B,H,N] by one of the paper's comparison designs:
+    1 = one program per head with an on-chip carry, 2 = Scan-Then-Propagate
+    (App. E.1).  Benchmark/parity use only; the product call is
+    gfwa_gate_prefix."""
+    lib = load()
+    _need_cuda(h, beta)
+    h = h.contiguous()
+    beta = beta.to(h.dtype).contiguous()
+    B, N, H = h.shape
+    U = torch.empty(B, H, N, dtype=torch.float32, device=h.device)
+    nbytes = lib.gfwa_gate_prefix_variant_workspace_size(variant, B, N, H)
+    ws = workspace(nbytes, h.device, f"gate_v{variant}")
+    st = lib.gfwa_gate_prefix_variant(variant, _dt(h), _ptr(h), _ptr(beta), B, N, H, float(eps), _ptr(U), _ptr(ws),
+                                      nbytes, _stream(h.device))
+    _check(st, "gfwa_gate_prefix_variant")
+    return U
 
 
 def gfwa_gate_prefix_bwd(dU: torch.Tensor, h: torch.Tensor | None = None, beta: torch.Tensor | None = None,

@@ -79,3 +79,34 @@ def test_gate_prefix_bwd(B, N, H, dtype):
     tol = 1e-5 if dtype == torch.float32 else 8e-3
     assert np.abs(np64(dh) - dhr).max() / max(np.abs(dhr).max(), 1e-30) <= tol
     assert np.abs(np64(dbeta) - dbr).max() / max(np.abs(dbr).max(), 1e-30) <= tol
+
+
+VARIANT_SHAPES = [(1, 1, 1), (2, 7, 3), (2, 1000, 5), (3, 4097, 16), (1, 20000, 32), (1, 2049, 48)]
+
+
+@pytest.mark.parametrize("variant", [1, 2])
+@pytest.mark.parametrize("B,N,H", VARIANT_SHAPES)
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_gate_prefix_comparison_variants(variant, B, N, H, dtype):
+    """The paper's comparison designs: one program per head
+    with an on-chip carry and Scan-Then-Propagate (App. E.1) compute
+    the same U as the oracle (Alg. 1); variant 2 rejects H > 32."""
+    h, beta = synth.gate_inputs(B, N, H, seed=B * 11 + N + H)
+    h, beta = h.to(dtype), beta.to(dtype)
+    if variant == 2 and H > 32:
+        with pytest.raises(RuntimeError):
+            gb.gfwa_gate_prefix_variant(variant, h.cuda(), beta.cuda())
+        return
+    U = gb.gfwa_gate_prefix_variant(variant, h.cuda(), beta.cuda())
+    Ur, _, _ = oracle.gate_prefix_hbeta(h, beta, 1e-6)
+    assert rel_slices(U, Ur, "bhn") <= TOL_U
+
+
+@pytest.mark.parametrize("variant", [1, 2])
+def test_gate_prefix_comparison_variants_probe_G(variant):
+    c = synth.CONFIGS["G"]
+    h, beta = synth.gate_inputs(c["B"], c["N"], c["H"], seed=c["seed"], device="cuda")
+    h, beta = h.bfloat16(), beta.bfloat16()
+    U = gb.gfwa_gate_prefix_variant(variant, h, beta)
+    Ur, _, _ = oracle.gate_prefix_hbeta(h, beta)
+    assert rel_slices(U, Ur, "bhn") <= TOL_U
