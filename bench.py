@@ -455,6 +455,26 @@ def run_aux(dev, peaks):
                         "frac_hbm": round(byts / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"], 4),
                         "bytes_per_step": byts}
     del Kc, Vc
+    # GQA decode: groups of 4 query heads share a K/V head
+    c = synth.CONFIGS["C5_gqa4"]
+    B, H, Hk = c["B"], c["H"], c["H_kv"]
+    Kc, Vc, a_hist, q, k, v, a_new = synth.decode_inputs(B, H, d, w, seed=c["seed"], device=dev, H_kv=Hk)
+    Uc = -torch.cumsum(a_hist, -1)
+    for _ in range(3):
+        gb.gfwa_decode(q, k, v, a_new, Kc, Vc, Uc, pos)
+    torch.cuda.synchronize(dev)
+    e0.record()
+    for _ in range(n):
+        gb.gfwa_decode(q, k, v, a_new, Kc, Vc, Uc, pos)
+    e1.record()
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1) / n
+    byts = B * Hk * 4 * w * d + B * H * (4 * w + 4 * d) + B * Hk * 4 * d  # K,V rows once per group; u, q, o per head
+    out["decode_C5_gqa4"] = {"ms_per_step": round(ms, 4), "tokens_per_s": round(B / (ms * 1e-3), 1),
+                             "achieved_GBps": round(byts / (ms * 1e-3) / 1e9, 1),
+                             "frac_hbm": round(byts / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"], 4),
+                             "bytes_per_step": byts, "H_kv": Hk}
+    del Kc, Vc
     c = synth.CONFIGS["G"]
     h, beta = synth.gate_inputs(c["B"], c["N"], c["H"], seed=c["seed"], device=dev)
     h, beta = h.bfloat16(), beta.bfloat16()

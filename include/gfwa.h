@@ -191,16 +191,20 @@ typedef struct {
     float eps;                  /* gate eps for GATE_HBETA */
     gfwa_dtype_t dtype;         /* dtype of q, k_new, v_new, caches, o */
     gfwa_gate_kind_t gate_kind; /* gate_a/gate_b are (h, beta) or (alpha, NULL), fp32 [B,H] */
+    int64_t H_kv;               /* K/V heads (GQA): H % H_kv == 0, H/H_kv in {1,2,4,8}; 0 = H */
 } gfwa_decode_desc_t;
 
 /*
  * gfwa_decode -- for every (b, hh), with t = pos[b] (tokens already cached
  * before this one) and slot s = t mod w:
  *   u_t = u_{t-1} - alpha_t, u_{t-1} = U_cache[b,hh,(t-1) mod w] (0 when t == 0)
- *   K_cache[b,hh,s] = k_new, V_cache[b,hh,s] = v_new, U_cache[b,hh,s] = u_t
+ *   K_cache[b,kv(hh),s] = k_new, V_cache[b,kv(hh),s] = v_new, U_cache[b,hh,s] = u_t
  *   o[b,hh] = sum_i softmax_i(scale q.k_i + u_t - u_i) v_i over the
  *             min(t+1, w) valid slots (ring order is irrelevant)
- * q, k_new, v_new, o [B,H,d]; K_cache, V_cache [B,H,w,d]; U_cache [B,H,w] fp32;
+ * GQA (heads_per_gqa_group): query head hh reads
+ * K/V head hh / (H / H_kv); the gate and U stay per query head.
+ * q, o [B,H,d]; k_new, v_new [B,H_kv,d]; K_cache, V_cache [B,H_kv,w,d];
+ * U_cache [B,H,w] fp32;
  * pos [B] int64 DEVICE array (graph-capturable).  The caches are updated in
  * place.  ws >= gfwa_decode_workspace_size(desc) bytes; it must be ZEROED once
  * by the caller before first use (the call leaves it zeroed again).

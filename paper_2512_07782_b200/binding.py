@@ -60,6 +60,7 @@ class DecodeDesc(ctypes.Structure):
         ("eps", ctypes.c_float),
         ("dtype", ctypes.c_int32),
         ("gate_kind", ctypes.c_int32),
+        ("H_kv", ctypes.c_int64),
     ]
 
 
@@ -336,12 +337,12 @@ def gfwa_decode(q, k_new, v_new, gate_a, K_cache, V_cache, U_cache, pos, gate_b=
     lib = load()
     _need_cuda(q, k_new, v_new, gate_a, K_cache, V_cache, U_cache, pos)
     B, H, d = q.shape
-    w = K_cache.shape[2]
+    Hkv, w = K_cache.shape[1], K_cache.shape[2]  # Hkv < H: GQA groups of H // Hkv query heads
     for t in (q, k_new, v_new, K_cache, V_cache, U_cache):
         if not t.is_contiguous():
             raise GfwaError("decode tensors must be contiguous")
     dsc = DecodeDesc()
-    dsc.B, dsc.H, dsc.d, dsc.w = B, H, d, w
+    dsc.B, dsc.H, dsc.d, dsc.w, dsc.H_kv = B, H, d, w, Hkv
     dsc.scale = float(scale) if scale is not None else 0.0
     dsc.eps = float(eps)
     dsc.dtype = _dt(q)
@@ -350,7 +351,7 @@ def gfwa_decode(q, k_new, v_new, gate_a, K_cache, V_cache, U_cache, pos, gate_b=
     ga = gate_a.float().contiguous()
     gb = None if gate_b is None else gate_b.float().contiguous()
     nbytes = lib.gfwa_decode_workspace_size(ctypes.byref(dsc))
-    ws = workspace(nbytes, q.device, f"decode{B}x{H}x{w}x{d}", zero=True)
+    ws = workspace(nbytes, q.device, f"decode{B}x{H}x{Hkv}x{w}x{d}", zero=True)
     st = lib.gfwa_decode(ctypes.byref(dsc), _ptr(q), _ptr(k_new), _ptr(v_new), _ptr(ga),
                          _ptr(gb), _ptr(K_cache),
                          _ptr(V_cache), _ptr(U_cache), _ptr(pos), _ptr(o), _ptr(ws), nbytes, _stream(q.device))

@@ -67,21 +67,24 @@ def attn_inputs(s: AttnShape, seed: int, device="cpu", dtype=torch.float32, with
     return Q, K, V, dO
 
 
-def decode_inputs(B: int, H: int, d: int, w: int, seed: int, device="cpu", dtype=torch.bfloat16):
+def decode_inputs(B: int, H: int, d: int, w: int, seed: int, device="cpu", dtype=torch.bfloat16,
+                  H_kv: int | None = None):
     """A pre-filled ring cache plus one new token (config C5 recipe).
 
-    Returns K_cache, V_cache [B,H,w,d] (dtype), alpha_hist [B,H,w] fp32 (the
-    gates of the w cached tokens, oldest first), q, k_new, v_new [B,H,d] and
-    alpha_new [B,H] fp32.  The caller turns alpha_hist into U_cache with its
-    own scan (here: the oracle or the library), so no gate math lives here.
+    Returns K_cache, V_cache [B,H_kv,w,d] (dtype), alpha_hist [B,H,w] fp32 (the
+    gates of the w cached tokens, oldest first), q [B,H,d], k_new, v_new
+    [B,H_kv,d] and alpha_new [B,H] fp32 (H_kv < H: GQA, groups of H // H_kv
+    query heads share a K/V head).  The caller turns alpha_hist into U_cache
+    with its own scan (here: the oracle or the library), so no gate math lives here.
     """
+    Hk = H if H_kv is None else H_kv
     g = _gen(seed + 104729, device)
-    Kc = _rms_rows(torch.randn(B, H, w, d, generator=g, device=device)).to(dtype)
-    Vc = torch.randn(B, H, w, d, generator=g, device=device).to(dtype)
+    Kc = _rms_rows(torch.randn(B, Hk, w, d, generator=g, device=device)).to(dtype)
+    Vc = torch.randn(B, Hk, w, d, generator=g, device=device).to(dtype)
     alpha_hist = torch.nn.functional.softplus(torch.randn(B, H, w, generator=g, device=device))
     q = _rms_rows(torch.randn(B, H, d, generator=g, device=device)).to(dtype)
-    k = _rms_rows(torch.randn(B, H, d, generator=g, device=device)).to(dtype)
-    v = torch.randn(B, H, d, generator=g, device=device).to(dtype)
+    k = _rms_rows(torch.randn(B, Hk, d, generator=g, device=device)).to(dtype)
+    v = torch.randn(B, Hk, d, generator=g, device=device).to(dtype)
     alpha_new = torch.nn.functional.softplus(torch.randn(B, H, generator=g, device=device))
     return Kc, Vc, alpha_hist, q, k, v, alpha_new
 
@@ -95,5 +98,7 @@ CONFIGS = {
     "C3_w2048": dict(B=1, H=32, N=8192, d=128, w=2048, dtype="bf16", seed=1003),
     "C4": dict(B=1, H=32, N=131072, d=128, w=2048, dtype="bf16", seed=1004),
     "C5": dict(B=64, H=32, d=128, w=2048, dtype="bf16", seed=1005),
+    # C5 with GQA groups of 4 query heads per K/V head (heads_per_gqa_group = 4)
+    "C5_gqa4": dict(B=64, H=32, H_kv=8, d=128, w=2048, dtype="bf16", seed=1005),
     "G": dict(B=4, N=131072, H=32, dtype="bf16", seed=1006),
 }

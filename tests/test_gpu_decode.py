@@ -81,3 +81,75 @@ def test_decode_C5_full_size_sampled():
         assert np.abs(np64(o[b, hh]) - o_ref).max() <= TOL_BF16_O
     # the replaced slot now holds the new token
     assert torch.equal(Kc_ring[:, :, t % w], k) and torch.equal(Vc_ring[:, :, t % w], v)
+
+
+@pytest.mark.parametrize("dtype,d,w,steps,G", [(torch.bfloat16, 128, 33, 50, 4), (torch.float32, 64, 16, 30, 2),
+                                               (torch.bfloat16, 64, 20, 25, 8), (torch.bfloat16, 128, 1, 4, 4)])
+def test_decode_gqa_sequence_equals_prefill_rows(dtype, d, w, steps, G):
+    """GQA decode (SURVEY 8(f) f3): query head hh reads K/V head hh // G; every
+    step equals the oracle forward row with K/V expanded to the query heads
+    (the definition of grouped-query attention), gates per query head."""
+    B, H = 2, 8
+    Hk = H // G
+    s = synth.AttnShape(B=B, H=Hk, N=steps, d=d, w=w)
+    _, K, V, _ = synth.attn_inputs(s, seed=steps + 3 * w, dtype=dtype, with_grad_out=False)
+    sq = synth.AttnShape(B=B, H=H, N=steps, d=d, w=w)
+    Q, _, _, _ = synth.attn_inputs(sq, seed=steps + 5 * w, dtype=dtype, with_grad_out=False)
+    h, beta = synth.gate_inputs(B, steps, H, seed=w + G)
+    Kc = torch.zeros(B, Hk, w, d, dtype=dtype, device="cuda")
+    Vc = torch.zeros_like(Kc)
+    Uc = torch.zeros(B, H, w, dtype=torch.float32, device="cuda")
+    outs = []
+    for t in range(steps):
+        pos = torch.full((B,), t, dtype=torch.int64, device="cuda")
+        o = gb.gfwa_decode(Q[:, t].cuda().contiguous(), K[:, t].cuda().contiguous(), V[:, t].cuda().contiguous(),
+                           h[:, t].cuda(), Kc, Vc, Uc, pos, gate_b=beta[:, t].cuda())
+        outs.append(np64(o))
+    got = np.stack(outs, 1)  # [B, steps, H, d]
+    U, _, _ = oracle.gate_prefix_hbeta(h, beta)
+    ref, _ = oracle.fwd(Q, K.repeat_interleave(G, dim=2), V.repeat_interleave(G, dim=2), U, w)
+    if dtype == torch.float32:
+        assert np.abs(got - ref).max() / np.abs(ref).max() <= TOL_F32_O
+    else:
+        assert np.abs(got - ref).max() <= TOL_BF16_O
+    for t in range(max(0, steps - w), steps):
+        assert torch.equal(Kc[:, :, t % w].cpu(), K[:, t].to(dtype))
+
+
+def test_decode_C5_gqa4_full_size_sampled():
+    """C5 with GQA groups of 4 (B=64, H=32, H_kv=8, d=128, w=2048, bf16), wrapped
+    ring (pos = w + 17); 48 sampled (b, h) rows vs the oracle."""
+    c = synth.CONFIGS["C5_gqa4"]
+    B, H, Hk, d, w = c["B"], c["H"], c["H_kv"], c["d"], c["w"]
+    G = H // Hk
+    Kc, Vc, a_hist, q, k, v, a_new = synth.decode_inputs(B, H, d, w, seed=c["seed"], device="cuda", H_kv=Hk)
+    t = w + 17
+    U_hist, _ = oracle.gate_prefix(a_hist)
+    slots = np.arange(t - w, t) % w
+    Uc = np.zeros((B, H, w))
+    Uc[:, :, slots] = U_hist
+    idx = torch.from_numpy(slots).cuda()
+    Kc_ring, Vc_ring = torch.empty_like(Kc), torch.empty_like(Vc)
+    Kc_ring[:, :, idx] = Kc
+    Vc_ring[:, :, idx] = Vc
+    Uc_t = torch.from_numpy(Uc).float().cuda()
+    Uc_used = np64(Uc_t)
+    pos = torch.full((B,), t, dtype=torch.int64, device="cuda")
+    o = gb.gfwa_decode(q, k, v, a_new, Kc_ring, Vc_ring, Uc_t, pos)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(2)
+    a_new_np = np64(a_new)
+    order = [(tok % w) for tok in range(t - w + 1, t)]
+    for _ in range(48):
+        b, hh = int(rng.integers(0, B)), int(rng.integers(0, H))
+        kh = hh // G
+        keys = np.concatenate([np64(Kc_ring[b, kh, order]), np64(k[b, kh])[None]])
+        vals = np.concatenate([np64(Vc_ring[b, kh, order]), np64(v[b, kh])[None]])
+        ut = Uc_used[b, hh, (t - 1) % w] - a_new_np[b, hh]
+        u = np.concatenate([Uc_used[b, hh, order], [ut]])
+        o_ref, _ = oracle.attend_row(np64(q[b, hh]), keys, vals, u, ut)
+        assert np.abs(np64(o[b, hh]) - o_ref).max() <= TOL_BF16_O
+    assert torch.equal(Kc_ring[:, :, t % w], k) and torch.equal(Vc_ring[:, :, t % w], v)
+    # every query head's u_t was written to its own U_cache slot
+    ut_all = Uc_used[:, :, (t - 1) % w] - a_new_np
+    assert np.allclose(np64(Uc_t[:, :, t % w]), ut_all, rtol=1e-6, atol=1e-5)
