@@ -38,7 +38,7 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kMinBlocks = 4;  // resident CTAs per SM (64 registers / thread)
 constexpr unsigned kFull = 0xffffffffu;
 #ifndef GFWA_GATE_SMALL_LOG
-#define GFWA_GATE_SMALL_LOG 22  // below 2^22 (b, t, h) elements the scan is latency-bound
+#define GFWA_GATE_SMALL_LOG 22  // below 2^22 (b, t, h) elements: the LM-shape geometry
 #endif
 
 struct ScanGeom {
@@ -51,32 +51,20 @@ struct ScanGeom {
 };
 
 ScanGeom scan_geom(int64_t B, int64_t N, int64_t H) {
+    // The look-back chain, not HBM, sets the time at every measured size, so
+    // chunks are long and head groups narrow (measured on B200, ncu):
+    // LM shapes (< 2^22 (b, t, h) elements): 4-head groups x 512 tokens;
+    // probe G: 8-head groups x 1024 tokens (32 x 256 before: 80 -> 65 us fwd,
+    // 127 -> 93 us bwd).  T * HGP <= 8192 (the fp32 alpha tile in smem).
     ScanGeom g;
-    g.HG = H >= 32 ? 32 : (int)H;
-    const char* ge = getenv("GFWA_GATE_GEOM");  // experiments: "log2(HG),log2(T)"
-    if (ge || B * N * H < ((int64_t)1 << GFWA_GATE_SMALL_LOG)) {
-        // latency regime (LM shapes): the look-back chain, not HBM, sets the time,
-        // so use long chunks (T = 512, measured best of 128..1024) and narrow 4-head groups for parallelism
-        int lh = 2, lt = 9;
-        if (ge) sscanf(ge, "%d,%d", &lh, &lt);
-        g.HG = (int)std::min<int64_t>(H, (int64_t)1 << lh);
-        g.log_hgp = 0;
-        while ((1 << g.log_hgp) < g.HG) ++g.log_hgp;
-        g.log_t = std::max(7, std::min(lt, std::min(10, 13 - g.log_hgp)));
-        g.n_hgroups = (int)((H + g.HG - 1) / g.HG);
-        g.n_chunks = (int)((N + (1 << g.log_t) - 1) >> g.log_t);
-        g.n_seq = (int)(B * g.n_hgroups);
-        return g;
-    }
+    const bool small = B * N * H < ((int64_t)1 << GFWA_GATE_SMALL_LOG);
+    int lh = small ? 2 : 3, lt = small ? 9 : 10;
+    if (const char* ge = getenv("GFWA_GATE_GEOM")) sscanf(ge, "%d,%d", &lh, &lt);  // experiments
+    g.HG = (int)std::min<int64_t>(H, (int64_t)1 << std::min(std::max(lh, 0), 5));
     g.log_hgp = 0;
     while ((1 << g.log_hgp) < g.HG) ++g.log_hgp;
-    g.log_t = std::min(10, 13 - g.log_hgp);  // T * HGP <= 8192 elements per tile
+    g.log_t = std::max(7, std::min(lt, std::min(10, 13 - g.log_hgp)));
     g.n_hgroups = (int)((H + g.HG - 1) / g.HG);
-    // small problems: shorter chunks so every SM streams (the look-back makes
-    // the chunk count free)
-    while (g.log_t > 7 &&
-           (int64_t)g.n_hgroups * ((N + (1 << g.log_t) - 1) >> g.log_t) * B < kMinBlocks * 148)
-        --g.log_t;
     g.n_chunks = (int)((N + (1 << g.log_t) - 1) >> g.log_t);
     g.n_seq = (int)(B * g.n_hgroups);
     return g;
