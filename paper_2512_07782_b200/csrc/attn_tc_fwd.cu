@@ -361,14 +361,21 @@ __global__ void __launch_bounds__(kThreads, 2)
         tc_fence_after();
         const float inv = l > 0.f ? 1.f / l : 0.f;
         const uint32_t sbf = smem_u32(Qs), sf = smem_u32(Ks);
+        // two halves of 64 columns: both TMEM loads of a half in flight before one
+        // wait, and the half's bulk stores issued as soon as it is staged, so the
+        // second half's staging overlaps the first half's store read-out
 #pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
-            uint32_t ob[32];
-            tmem_ld32(lane_addr + 128 + 32 * c, ob);
+        for (int hf = 0; hf < 2; ++hf) {
+            uint32_t ob[2][32];
+            tmem_ld32(lane_addr + 128 + 64 * hf, ob[0]);
+            tmem_ld32(lane_addr + 128 + 64 * hf + 32, ob[1]);
             tmem_wait_ld();
+#pragma unroll
+            for (int cc = 0; cc < 2; ++cc) {
+            const int c = 2 * hf + cc;
             float v[32];
 #pragma unroll
-            for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(ob[e]) * inv;
+            for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(ob[cc][e]) * inv;
             // bf16: columns [32c, 32c+32) = half c>>1, 16-B chunks (c&1)*4 + k
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
@@ -390,16 +397,19 @@ __global__ void __launch_bounds__(kThreads, 2)
                                       __float_as_uint(v[4 * k + 2]), __float_as_uint(v[4 * k + 3])));
                 }
             }
+            }
+            fence_proxy_async();
+            named_bar_sync(1, 128);
+            if (r == 0) {
+                tma_store_4d(&mo, Qs + hf * (kTileBytes / 2), hf * 64, (int)h, (int)r0, (int)b);
+                if (p.store_f32)
+                    for (int c = 2 * hf; c < 2 * hf + 2; ++c)
+                        tma_store_4d(&mo32, Ks + c * 16384, c * 32, (int)h, (int)r0, (int)b);
+                bulk_commit();
+            }
         }
         if (valid) p.LSE[(b * p.H + h) * p.Nq + t] = (m_used + bq + __log2f(l)) * kLn2;
-        fence_proxy_async();
-        named_bar_sync(1, 128);
         if (r == 0) {
-            for (int half = 0; half < 2; ++half)
-                tma_store_4d(&mo, Qs + half * (kTileBytes / 2), half * 64, (int)h, (int)r0, (int)b);
-            if (p.store_f32)
-                for (int c = 0; c < 4; ++c) tma_store_4d(&mo32, Ks + c * 16384, c * 32, (int)h, (int)r0, (int)b);
-            bulk_commit();
             bulk_wait_read0();  // smem must stay valid until the bulk stores have read it
             GFWA_TR(33);
         }

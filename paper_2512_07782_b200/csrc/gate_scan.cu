@@ -309,7 +309,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) gate_prefix_kernel(
             if (total && c == g.n_chunks - 1) total[(int64_t)b * H + hh0 + j] = excl + agg;
         }
         const double carry = carry_in ? carry_in[(int64_t)b * H + hh0 + j] : 0.0;
-        const float cbase = (float)(carry - (excl + xs[i] - (double)run[i]));
+        // carry-side base in fp64; the final subtraction is done in fp64 too, so a
+        // result much smaller than the carry (cancellation) is rounded only once
+        const double cbase = carry - (excl + xs[i] - (double)run[i]);
         const float* row = sA + j * pitch + lane * (R + 1);
         float* urow = U + ((int64_t)b * H + hh0 + j) * N + t0 + tl;
         float acc = 0.f;
@@ -317,19 +319,19 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) gate_prefix_kernel(
             for (int k = 0; k < R; k += 4) {
                 float4 o;
                 acc += row[k];
-                o.x = cbase - acc;
+                o.x = (float)(cbase - (double)acc);
                 acc += row[k + 1];
-                o.y = cbase - acc;
+                o.y = (float)(cbase - (double)acc);
                 acc += row[k + 2];
-                o.z = cbase - acc;
+                o.z = (float)(cbase - (double)acc);
                 acc += row[k + 3];
-                o.w = cbase - acc;
+                o.w = (float)(cbase - (double)acc);
                 *reinterpret_cast<float4*>(urow + k) = o;
             }
         } else {
             for (int k = 0; k < R; ++k) {
                 acc += row[k];
-                if (tl + k < nt) urow[k] = cbase - acc;
+                if (tl + k < nt) urow[k] = (float)(cbase - (double)acc);
             }
         }
     }
@@ -421,7 +423,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) gate_prefix_bwd_kernel(
         const double agg = __shfl_sync(kFull, xs[i], 0);
         if (lane == 0 && rc > 0) publish(d + (size_t)rc * 32 + j, excl + agg, 2u);
         const double cr = carry ? carry[(int64_t)b * H + hh0 + j] : 0.0;
-        const float cbase = (float)(cr - (excl + xs[i] - (double)run[i]));
+        const double cbase = cr - (excl + xs[i] - (double)run[i]);  // fp64, as in the forward
         float* row = sA + j * pitch + lane * (R + 1);
         float* arow = dalpha ? dalpha + ((int64_t)b * H + hh0 + j) * N + t0 + tl : nullptr;
         float acc = 0.f;
@@ -429,13 +431,13 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) gate_prefix_bwd_kernel(
             for (int k = R - 4; k >= 0; k -= 4) {
                 float4 o;
                 acc += row[k + 3];
-                o.w = cbase - acc;
+                o.w = (float)(cbase - (double)acc);
                 acc += row[k + 2];
-                o.z = cbase - acc;
+                o.z = (float)(cbase - (double)acc);
                 acc += row[k + 1];
-                o.y = cbase - acc;
+                o.y = (float)(cbase - (double)acc);
                 acc += row[k];
-                o.x = cbase - acc;
+                o.x = (float)(cbase - (double)acc);
                 row[k] = o.x;  // kept for the chain rule
                 row[k + 1] = o.y;
                 row[k + 2] = o.z;
@@ -445,7 +447,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) gate_prefix_bwd_kernel(
         } else {
             for (int k = R - 1; k >= 0; --k) {
                 acc += row[k];
-                const float da = cbase - acc;
+                const float da = (float)(cbase - (double)acc);
                 row[k] = da;
                 if (arow && tl + k < nt) arow[k] = da;
             }

@@ -69,7 +69,7 @@ def test_gate_prefix_bwd(B, N, H, dtype):
     h, beta = synth.gate_inputs(B, N, H, seed=N + 3)
     h, beta = h.to(dtype), beta.to(dtype)
     dU = torch.randn(B, H, N, generator=torch.Generator().manual_seed(N))
-    carry = torch.randn(B, H, dtype=torch.float64)
+    carry = torch.randn(B, H, dtype=torch.float64, generator=torch.Generator().manual_seed(N + 1))
     dalpha, dh, dbeta = gb.gfwa_gate_prefix_bwd(dU.cuda(), h.cuda(), beta.cuda(), 1e-6, carry=carry.cuda())
     assert dh.dtype == dtype and dbeta.dtype == dtype
     dar = oracle.dalpha_scan(dU, carry)
