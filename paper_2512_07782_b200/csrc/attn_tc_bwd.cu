@@ -376,33 +376,41 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (threadIdx.x == 0) GFWA_TR(41);
             tc_fence_after();
         }
+        // two halves of 64 columns: both TMEM loads of a half in flight before one
+        // wait, each half's TMA store issued as soon as it is staged
 #pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
-            uint32_t v[32];
+        for (int hf = 0; hf < 2; ++hf) {
+            uint32_t v2[2][32];
             if (nsteps > 0) {
-                tmem_ld32(lane_addr + acol + 32 * c, v);
+                tmem_ld32(lane_addr + acol + 64 * hf, v2[0]);
+                tmem_ld32(lane_addr + acol + 64 * hf + 32, v2[1]);
                 tmem_wait_ld();
             } else {
 #pragma unroll
-                for (int e = 0; e < 32; ++e) v[e] = 0u;
+                for (int e = 0; e < 32; ++e) v2[0][e] = v2[1][e] = 0u;
             }
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const int chunk = ((c & 1) * 4 + k) ^ (kr & 7);
-                uint4 pkv;
-                pkv.x = pack_bf16x2(__uint_as_float(v[8 * k + 0]) * mul, __uint_as_float(v[8 * k + 1]) * mul);
-                pkv.y = pack_bf16x2(__uint_as_float(v[8 * k + 2]) * mul, __uint_as_float(v[8 * k + 3]) * mul);
-                pkv.z = pack_bf16x2(__uint_as_float(v[8 * k + 4]) * mul, __uint_as_float(v[8 * k + 5]) * mul);
-                pkv.w = pack_bf16x2(__uint_as_float(v[8 * k + 6]) * mul, __uint_as_float(v[8 * k + 7]) * mul);
-                sts128(sg + (c >> 1) * (kKV / 2) + kr * 128 + chunk * 16, pkv);
+            for (int cc = 0; cc < 2; ++cc) {
+                const uint32_t* v = v2[cc];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int chunk = (cc * 4 + k) ^ (kr & 7);
+                    uint4 pkv;
+                    pkv.x = pack_bf16x2(__uint_as_float(v[8 * k + 0]) * mul, __uint_as_float(v[8 * k + 1]) * mul);
+                    pkv.y = pack_bf16x2(__uint_as_float(v[8 * k + 2]) * mul, __uint_as_float(v[8 * k + 3]) * mul);
+                    pkv.z = pack_bf16x2(__uint_as_float(v[8 * k + 4]) * mul, __uint_as_float(v[8 * k + 5]) * mul);
+                    pkv.w = pack_bf16x2(__uint_as_float(v[8 * k + 6]) * mul, __uint_as_float(v[8 * k + 7]) * mul);
+                    sts128(sg + hf * (kKV / 2) + kr * 128 + chunk * 16, pkv);
+                }
+            }
+            fence_proxy_async();
+            named_bar_sync(1 + wg, 128);
+            if (kr == 0) {
+                tma_store_4d(wg == 0 ? &mdv : &mdk, stg + hf * (kKV / 2), hf * 64, (int)h, (int)j0, (int)b);
+                bulk_commit();
             }
         }
-        fence_proxy_async();
-        named_bar_sync(1 + wg, 128);
         if (kr == 0) {
-            for (int half = 0; half < 2; ++half)
-                tma_store_4d(wg == 0 ? &mdv : &mdk, stg + half * (kKV / 2), half * 64, (int)h, (int)j0, (int)b);
-            bulk_commit();
             bulk_wait_read0();
             if (wg == 0) GFWA_TR(42);
         }
