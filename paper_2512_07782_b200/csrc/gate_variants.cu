@@ -59,6 +59,51 @@ __device__ __forceinline__ double cta_scan(double x, double* s_w, double& total)
     return before + inc - x;
 }
 
+// alpha of a contiguous [nt tokens x H heads] tile (h, beta in [B,N,H]) into
+// the transposed smem tile sA[head][token] (one pad word per 8-token run):
+// 16-byte loads, four per thread in flight, when the tile is 16-byte aligned
+constexpr int kV2Pitch = kV2Chunk + kV2Chunk / 8 + 1;
+template <typename Tin>
+__device__ __forceinline__ void load_alpha_tile(const Tin* h, const Tin* beta, int64_t base, int nt, int H,
+                                                float eps, float* sA) {
+    constexpr int V = 16 / sizeof(Tin);  // elements per 16-byte vector
+    const int n = nt * H;
+    const bool vec = ((((uintptr_t)(h + base)) | ((uintptr_t)(beta + base))) & 15) == 0;
+    int done = 0;
+    if (vec) {
+        const int nv = n / V;
+        for (int i0 = threadIdx.x; i0 < nv; i0 += 4 * kThreads) {
+            uint4 hv[4], bv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int i = i0 + u * kThreads;
+                if (i < nv) {
+                    hv[u] = __ldcs(reinterpret_cast<const uint4*>(h + base) + i);
+                    bv[u] = __ldcs(reinterpret_cast<const uint4*>(beta + base) + i);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int i = i0 + u * kThreads;
+                if (i >= nv) break;
+                const Tin* hp = reinterpret_cast<const Tin*>(&hv[u]);
+                const Tin* bp = reinterpret_cast<const Tin*>(&bv[u]);
+#pragma unroll
+                for (int k = 0; k < V; ++k) {
+                    const int e = i * V + k, t = e / H, j = e % H;
+                    const float hv1 = to_f32<Tin>(hp[k]), bv1 = to_f32<Tin>(bp[k]);
+                    sA[j * kV2Pitch + t + (t >> 3)] = __fdividef(softplus_fast(bv1 * hv1), bv1 + eps);
+                }
+            }
+        }
+        done = nv * V;
+    }
+    for (int e = done + threadIdx.x; e < kV2Chunk * H; e += kThreads) {
+        const int t = e / H, j = e % H;
+        sA[j * kV2Pitch + t + (t >> 3)] = e < n ? alpha_at(h, beta, base + e, eps) : 0.f;
+    }
+}
+
 // ------------------------------------------------------------------ variant 1
 template <typename Tin>
 __global__ void __launch_bounds__(kThreads) gate_v1_kernel(const Tin* __restrict__ h, const Tin* __restrict__ beta,
@@ -97,41 +142,41 @@ template <typename Tin>
 __global__ void __launch_bounds__(kThreads) gate_v2_reduce_kernel(const Tin* __restrict__ h,
                                                                  const Tin* __restrict__ beta, int64_t N, int64_t H,
                                                                  float eps, double* __restrict__ S, int n_chunks) {
-    __shared__ float s_sum[kV2MaxH];
+    __shared__ float sA[kV2MaxH * kV2Pitch];
     const int c = blockIdx.x;
     const int64_t b = blockIdx.y, t0 = (int64_t)c * kV2Chunk;
     const int nt = (int)min64(kV2Chunk, N - t0);
-    if (threadIdx.x < H) s_sum[threadIdx.x] = 0.f;
+    load_alpha_tile(h, beta, (b * N + t0) * H, nt, (int)H, eps, sA);
     __syncthreads();
-    const int64_t base = (b * N + t0) * H;
-    const int n = nt * (int)H;
-    // consecutive threads read consecutive (t, h) elements (H contiguous)
-    float acc = 0.f;
-    int jprev = (int)(threadIdx.x % H);
-    for (int e = threadIdx.x; e < n; e += kThreads) {
-        const int j = (int)(e % H);
-        if (j != jprev) {
-            atomicAdd(&s_sum[jprev], acc);
-            acc = 0.f;
-            jprev = j;
-        }
-        acc += alpha_at(h, beta, base + e, eps);
+    // a warp per head: lane l sums its 8-token run, then the warp sums the runs
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int j = warp; j < H; j += kThreads / 32) {
+        const float* row = sA + j * kV2Pitch + lane * (kV2Chunk / 32 + 1);
+        float run = 0.f;
+#pragma unroll
+        for (int k = 0; k < kV2Chunk / 32; ++k) run += row[k];
+        double x = run;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        if (lane == 0) S[(b * H + j) * n_chunks + c] = x;
     }
-    atomicAdd(&s_sum[jprev], acc);
-    __syncthreads();
-    if (threadIdx.x < H) S[(b * H + threadIdx.x) * n_chunks + c] = (double)s_sum[threadIdx.x];
 }
 
-// phase 2: O[b, h, c] = sum_{c' < c} S[b, h, c']  (exclusive cumsum along time)
-__global__ void gate_v2_scan_kernel(const double* __restrict__ S, double* __restrict__ O, int64_t BH, int n_chunks) {
-    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= BH) return;
-    const double* s = S + r * n_chunks;
-    double* o = O + r * n_chunks;
-    double acc = 0.0;
-    for (int c = 0; c < n_chunks; ++c) {
-        o[c] = acc;
-        acc += s[c];
+// phase 2: O[b, h, c] = sum_{c' < c} S[b, h, c']  (exclusive cumsum along time,
+// P:1040-1042): one CTA per (b, h) row, a CTA-wide scan per 256 chunk sums
+__global__ void __launch_bounds__(kThreads) gate_v2_scan_kernel(const double* __restrict__ S, double* __restrict__ O,
+                                                               int n_chunks) {
+    __shared__ double s_w[kThreads / 32];
+    const double* srow = S + (int64_t)blockIdx.x * n_chunks;
+    double* orow = O + (int64_t)blockIdx.x * n_chunks;
+    double carry = 0.0;
+    for (int c0 = 0; c0 < n_chunks; c0 += kThreads) {
+        const int c = c0 + threadIdx.x;
+        const double x = c < n_chunks ? srow[c] : 0.0;
+        double total;
+        const double excl = cta_scan(x, s_w, total);
+        if (c < n_chunks) orow[c] = carry + excl;
+        carry += total;
     }
 }
 
@@ -142,16 +187,12 @@ __global__ void __launch_bounds__(kThreads) gate_v2_propagate_kernel(const Tin* 
                                                                     int64_t H, float eps,
                                                                     const double* __restrict__ O,
                                                                     float* __restrict__ U, int n_chunks) {
-    constexpr int kPitch = kV2Chunk + kV2Chunk / 8 + 1;  // one pad word per 8-token run: conflict-free runs
+    constexpr int kPitch = kV2Pitch;
     __shared__ float sA[kV2MaxH * kPitch];  // [head][token], transposed from [token][head]
     const int c = blockIdx.x;
     const int64_t b = blockIdx.y, t0 = (int64_t)c * kV2Chunk;
     const int nt = (int)min64(kV2Chunk, N - t0);
-    const int64_t base = (b * N + t0) * H;
-    for (int e = threadIdx.x; e < kV2Chunk * (int)H; e += kThreads) {
-        const int t = e / (int)H, j = e % (int)H;
-        sA[j * kPitch + t + (t >> 3)] = t < nt ? alpha_at(h, beta, base + e, eps) : 0.f;
-    }
+    load_alpha_tile(h, beta, (b * N + t0) * H, nt, (int)H, eps, sA);
     __syncthreads();
     // a warp per head; lane l owns tokens [8l, 8l + 8) of the chunk
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -194,7 +235,7 @@ void launch_variant(int variant, const void* h, const void* beta, int64_t B, int
     gate_v2_reduce_kernel<Tin><<<dim3((unsigned)n_chunks, (unsigned)B), kThreads, 0, st>>>(hp, bp, N, H, eps, S,
                                                                                             n_chunks);
     note_launch();
-    gate_v2_scan_kernel<<<(unsigned)((B * H + 127) / 128), 128, 0, st>>>(S, O, B * H, n_chunks);
+    gate_v2_scan_kernel<<<(unsigned)(B * H), kThreads, 0, st>>>(S, O, n_chunks);
     note_launch();
     gate_v2_propagate_kernel<Tin><<<dim3((unsigned)n_chunks, (unsigned)B), kThreads, 0, st>>>(hp, bp, N, H, eps, O,
                                                                                               U, n_chunks);
