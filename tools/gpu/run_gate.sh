@@ -1,8 +1,5 @@
-timeout 600 python -m pytest tests/test_gpu_gate.py -x -q 2>&1 | tail -1
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/lv.csv python -c "
-import sys; sys.path.insert(0,'.')
-import torch, synth
-from paper_2512_07782_b200 import binding as gb
-c=synth.CONFIGS['G']; h,b=synth.gate_inputs(c['B'],c['N'],c['H'],seed=1,device='cuda'); h,b=h.bfloat16(),b.bfloat16()
-for _ in range(2): gb.gfwa_gate_prefix_variant(2,h,b)
-torch.cuda.synchronize()" > /dev/null 2>&1; python tools/ncu_launches.py gpurun_out/lv.csv | grep gate_v2
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -1
+python bench.py --no-cpu --steps 10 > gpurun_out/b.log 2>&1; python - <<'P'
+import json; d=json.loads(open("gpurun_out/b.log").read().strip().splitlines()[-1]); print(d["ms_breakdown"], d["ms_per_step"], d["value"]); print(d["aux"]["gate_scan_G"]); print(d["aux"]["gate_preproc_compare_G"]); print(d["aux"]["decode_C5_gqa4"])
+P
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/lg.csv python profiles/prof_gate.py > /dev/null 2>&1; python tools/ncu_launches.py gpurun_out/lg.csv | grep gate
