@@ -116,12 +116,16 @@ class ClockSampler:
 
 
 def _dist():
+    """One process per GPU (torchrun env).  NCCL for the plumbing; GFWA_BENCH_BACKEND=gloo
+    exercises the multi-rank code path on a single-GPU box (ranks share cuda:0)."""
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     if ws > 1:
+        import torch
         import torch.distributed as dist
 
-        dist.init_process_group("nccl")
-        return dist, dist.get_rank(), ws, int(os.environ.get("LOCAL_RANK", "0"))
+        dist.init_process_group(os.environ.get("GFWA_BENCH_BACKEND", "nccl"))
+        local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
+        return dist, dist.get_rank(), ws, local
     return None, 0, 1, 0
 
 
@@ -130,7 +134,8 @@ def _max_over_ranks(dist, x: float, dev):
         return x
     import torch
 
-    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    on_dev = dist.get_backend() == "nccl"
+    t = torch.tensor([x], dtype=torch.float64, device=dev if on_dev else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -593,6 +598,9 @@ def run_reference(args):
         return
     import oracle
 
+    # torchrun exports OMP_NUM_THREADS=1; the oracle runs on all of this host's cores
+    oracle.set_num_threads(len(os.sched_getaffinity(0)))
+
     c = synth.CONFIGS[args.workload]
     s = synth.AttnShape(B=c["B"], H=c["H"], N=c["N"], d=c["d"], w=c["w"])
     cores = oracle.num_threads()
@@ -607,7 +615,8 @@ def run_reference(args):
     tok = cores * n_rows / s.H
     value = tok / dt
     print(json.dumps({
-        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "tokens/s", "n_gpus": 0,
+        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "tokens/s", "n_gpus": args.gpus,
+        "device": "host CPU (fp64 oracle; rank 0 only)",
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (synth.py)",
         "config": {"workload": args.workload, "B": s.B, "H": s.H, "N": s.N, "d": s.d, "w": s.w},

@@ -71,6 +71,11 @@ def num_threads() -> int:
     return int(_load().oracle_num_threads())
 
 
+def set_num_threads(n: int) -> None:
+    """OpenMP threads of the oracle loops (torchrun exports OMP_NUM_THREADS=1)."""
+    _load().oracle_set_num_threads(ctypes.c_int(int(n)))
+
+
 def gate_alpha(h, beta, eps: float = 1e-6) -> np.ndarray:
     """alpha [B,H,N] from h, beta [B,N,H] (Eq. 9; Alg. 1 l.5-7)."""
     h, beta = _f64(h), _f64(beta)

@@ -52,6 +52,15 @@ int oracle_num_threads(void) {
 #endif
 }
 
+/* thread count for the OpenMP loops (benchmark plumbing; no arithmetic) */
+void oracle_set_num_threads(int n) {
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
+
 /* softplus(z) = log(1 + e^z).  Alg. 1 line 6 writes
  * nu + log(e^{z-nu} + e^{-nu}), nu = max(z,0); reading C-6: the same value
  * written as max(z,0) + log1p(exp(-|z|)) so that z << 0 keeps relative
