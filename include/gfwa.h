@@ -47,7 +47,8 @@ typedef enum {
     GFWA_ERR_INVALID_ARGUMENT = 1, /* null pointer, bad size, misaligned pointer/stride */
     GFWA_ERR_UNSUPPORTED = 2,      /* head dim / dtype combination / device not CC 10.0 */
     GFWA_ERR_CUDA = 3,             /* a CUDA launch failed; see gfwa_last_cuda_error() */
-    GFWA_ERR_WORKSPACE = 4         /* ws_bytes smaller than *_workspace_size() */
+    GFWA_ERR_WORKSPACE = 4,        /* ws_bytes smaller than *_workspace_size() */
+    GFWA_ERR_NONFINITE = 5         /* opt-in debug check found NaN/Inf (gfwa_check_finite) */
 } gfwa_status_t;
 
 typedef enum { GFWA_F32 = 0, GFWA_BF16 = 1 } gfwa_dtype_t;
@@ -219,6 +220,16 @@ gfwa_status_t gfwa_decode(const gfwa_decode_desc_t* desc, const void* q, const v
 /* Helpers                                                                    */
 /* ------------------------------------------------------------------------- */
 const char* gfwa_status_string(gfwa_status_t s);
+/*
+ * gfwa_check_finite -- debug check (SURVEY 8(b) NONFINITE; SPEC's "NaN/Inf is an
+ * error surfaced"): GFWA_ERR_NONFINITE if any of the n elements of x (device,
+ * dtype F32 or BF16) is NaN or +-Inf, else GFWA_OK.  Unlike every other call it
+ * SYNCHRONISES `stream` (it reads a device flag back), so it is opt-in: call it
+ * directly, or set GFWA_CHECK_FINITE=1 in the environment to have gfwa_fwd check
+ * O and LSE and gfwa_bwd check dQ, dK, dV and dU after their launches.
+ */
+gfwa_status_t gfwa_check_finite(gfwa_dtype_t dtype, const void* x, int64_t n, gfwa_stream_t stream);
+
 int gfwa_last_cuda_error(void); /* cudaError_t of this thread's last GFWA_ERR_CUDA */
 const char* gfwa_version(void);
 /* Number of kernel launches the calling thread has issued through this library

@@ -26,6 +26,7 @@ _STATUS = {
     2: "GFWA_ERR_UNSUPPORTED",
     3: "GFWA_ERR_CUDA",
     4: "GFWA_ERR_WORKSPACE",
+    5: "GFWA_ERR_NONFINITE",
 }
 
 
@@ -81,6 +82,7 @@ EXPORTED = (
     "gfwa_bwd_workspace_size",
     "gfwa_decode",
     "gfwa_decode_workspace_size",
+    "gfwa_check_finite",
     "gfwa_status_string",
     "gfwa_last_cuda_error",
     "gfwa_version",
@@ -124,6 +126,8 @@ def load() -> ctypes.CDLL:
         lib.gfwa_decode_workspace_size.argtypes = [ctypes.POINTER(DecodeDesc)]
         lib.gfwa_decode.restype = ctypes.c_int
         lib.gfwa_decode.argtypes = [ctypes.POINTER(DecodeDesc)] + [_VP] * 11 + [sz, _VP]
+        lib.gfwa_check_finite.restype = ctypes.c_int
+        lib.gfwa_check_finite.argtypes = [ctypes.c_int, _VP, _I64, _VP]
         lib.gfwa_status_string.restype = ctypes.c_char_p
         lib.gfwa_last_cuda_error.restype = ctypes.c_int
         lib.gfwa_version.restype = ctypes.c_char_p
@@ -357,6 +361,20 @@ def gfwa_decode(q, k_new, v_new, gate_a, K_cache, V_cache, U_cache, pos, gate_b=
                          _ptr(V_cache), _ptr(U_cache), _ptr(pos), _ptr(o), _ptr(ws), nbytes, _stream(q.device))
     _check(st, "gfwa_decode")
     return o
+
+
+def gfwa_check_finite(x: torch.Tensor) -> bool:
+    """Debug check (synchronises the stream): True if every element is finite.
+    GFWA_CHECK_FINITE=1 makes gfwa_fwd / gfwa_bwd run it on their outputs and
+    raise GFWA_ERR_NONFINITE."""
+    lib = load()
+    _need_cuda(x)
+    x = x.contiguous()
+    st = lib.gfwa_check_finite(_dt(x), _ptr(x), x.numel(), _stream(x.device))
+    if st == 5:
+        return False
+    _check(st, "gfwa_check_finite")
+    return True
 
 
 def gfwa_debug_tc_selftest(Q, K, V):

@@ -34,6 +34,15 @@ using namespace gfwa;
 
 namespace {
 
+// [B, N, H, d] with no gaps (the debug finite check walks such tensors flat)
+bool packed(const int64_t* st, const AttnParams& p) {
+    return st[2] == p.d && st[1] == p.H * p.d && st[0] == p.Nq * p.H * p.d;
+}
+bool packed_kv(const int64_t* st, const AttnParams& p) {
+    return st[2] == p.d && st[1] == p.H * p.d && st[0] == p.Nkv * p.H * p.d;
+}
+bool check_finite_env();
+
 bool device_is_sm100() {
     static int cached = -1;
     if (cached < 0) {
@@ -112,8 +121,12 @@ extern "C" gfwa_status_t gfwa_fwd(const gfwa_attn_desc_t* desc, const void* Q, c
     p.O_f32 = O_f32;
     p.LSE = LSE;
     cudaStream_t st = (cudaStream_t)stream;
-    if (tc_fwd_supported(p, desc->dtype)) return tc_fwd(p, st);
-    return simt_fwd(p, desc->dtype, st);
+    gfwa_status_t s = tc_fwd_supported(p, desc->dtype) ? tc_fwd(p, st) : simt_fwd(p, desc->dtype, st);
+    if (s != GFWA_OK || !check_finite_env()) return s;
+    // opt-in debug check (GFWA_CHECK_FINITE=1): LSE, and O when it is packed
+    if ((s = gfwa_check_finite(GFWA_F32, LSE, p.B * p.H * p.Nq, stream)) != GFWA_OK) return s;
+    if (packed(p.os, p)) s = gfwa_check_finite(desc->dtype, O, p.B * p.Nq * p.H * p.d, stream);
+    return s;
 }
 
 static size_t bwd_ws_layout(const AttnParams& p, gfwa_dtype_t dt, size_t* off_D, size_t* off_scan,
@@ -176,6 +189,14 @@ extern "C" gfwa_status_t gfwa_bwd(const gfwa_attn_desc_t* desc, const void* Q, c
         s = simt_bwd(p, desc->dtype, st);
     }
     if (s != GFWA_OK) return s;
+    if (check_finite_env()) {  // opt-in debug check (GFWA_CHECK_FINITE=1)
+        if ((s = gfwa_check_finite(GFWA_F32, dU, p.B * p.H * p.Nkv, stream)) != GFWA_OK) return s;
+        if (packed(p.qs, p) && (s = gfwa_check_finite(desc->dtype, dQ, p.B * p.Nq * p.H * p.d, stream)) != GFWA_OK)
+            return s;
+        const int64_t nkv = p.B * p.Nkv * p.H * p.d;
+        if (packed_kv(p.ks, p) && (s = gfwa_check_finite(desc->dtype, dK, nkv, stream)) != GFWA_OK) return s;
+        if (packed_kv(p.vs, p) && (s = gfwa_check_finite(desc->dtype, dV, nkv, stream)) != GFWA_OK) return s;
+    }
     if (!dalpha) return GFWA_OK;
     // dalpha = carry - reverse_cumsum(dU) over the N_kv key rows
     return gfwa_gate_prefix_bwd(GFWA_GATE_ALPHA, GFWA_F32, nullptr, nullptr, p.B * p.H, p.Nkv, 1, 0.f, dU,
@@ -189,6 +210,49 @@ extern "C" int gfwa_attn_path(const gfwa_attn_desc_t* desc) {
     return tc_fwd_supported(p, desc->dtype) ? 1 : 0;
 }
 
+// ---------------------------------------------------------------- debug: non-finite check
+namespace {
+__device__ unsigned g_nonfinite;
+
+template <typename T>
+__global__ void nonfinite_kernel(const T* __restrict__ x, int64_t n) {
+    bool bad = false;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        bad |= !isfinite(to_f32<T>(x[i]));
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&g_nonfinite, 1u);
+}
+
+bool check_finite_env() {
+    static const int on = [] {
+        const char* e = getenv("GFWA_CHECK_FINITE");
+        return e && e[0] == '1' ? 1 : 0;
+    }();
+    return on != 0;
+}
+}  // namespace
+
+extern "C" gfwa_status_t gfwa_check_finite(gfwa_dtype_t dtype, const void* x, int64_t n, gfwa_stream_t stream) {
+    if (!x || n < 0) return GFWA_ERR_INVALID_ARGUMENT;
+    if (dtype != GFWA_F32 && dtype != GFWA_BF16) return GFWA_ERR_UNSUPPORTED;
+    if (n == 0) return GFWA_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    void* flag = nullptr;
+    if (gfwa_status_t s = check_launch(cudaGetSymbolAddress(&flag, g_nonfinite))) return s;
+    if (gfwa_status_t s = check_launch(cudaMemsetAsync(flag, 0, sizeof(unsigned), st))) return s;
+    const unsigned grid = (unsigned)min64((n + 255) / 256, 148 * 8);
+    if (dtype == GFWA_F32)
+        nonfinite_kernel<float><<<grid, 256, 0, st>>>((const float*)x, n);
+    else
+        nonfinite_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>((const __nv_bfloat16*)x, n);
+    note_launch();
+    if (gfwa_status_t s = check_launch()) return s;
+    unsigned h = 0;
+    if (gfwa_status_t s = check_launch(cudaMemcpyAsync(&h, flag, sizeof(unsigned), cudaMemcpyDeviceToHost, st)))
+        return s;
+    if (gfwa_status_t s = check_launch(cudaStreamSynchronize(st))) return s;
+    return h ? GFWA_ERR_NONFINITE : GFWA_OK;
+}
+
 extern "C" const char* gfwa_status_string(gfwa_status_t s) {
     switch (s) {
         case GFWA_OK: return "GFWA_OK";
@@ -196,6 +260,7 @@ extern "C" const char* gfwa_status_string(gfwa_status_t s) {
         case GFWA_ERR_UNSUPPORTED: return "GFWA_ERR_UNSUPPORTED";
         case GFWA_ERR_CUDA: return "GFWA_ERR_CUDA";
         case GFWA_ERR_WORKSPACE: return "GFWA_ERR_WORKSPACE";
+        case GFWA_ERR_NONFINITE: return "GFWA_ERR_NONFINITE";
     }
     return "GFWA_ERR_UNKNOWN";
 }

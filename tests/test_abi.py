@@ -80,3 +80,10 @@ def test_workspace_sizes_scale_with_problem():
     dd = gb.DecodeDesc()
     dd.B, dd.H, dd.d, dd.w = 64, 32, 128, 2048
     assert lib.gfwa_decode_workspace_size(ctypes.byref(dd)) >= 64 * 32 * (128 + 2) * 4
+
+
+def test_check_finite_validates_before_touching_the_device():
+    lib = gb.load()
+    assert lib.gfwa_check_finite(0, None, 4, None) == 1   # null pointer
+    assert lib.gfwa_check_finite(7, ctypes.c_void_p(16), 4, None) == 2  # dtype
+    assert lib.gfwa_status_string(5) == b"GFWA_ERR_NONFINITE"
