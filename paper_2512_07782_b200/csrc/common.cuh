@@ -79,13 +79,22 @@ __device__ __forceinline__ float sigmoid_f(float z) { return 1.f / (1.f + expf(-
 // t = s^2 <= 1/9 through s^13 (truncation 3e-8 relative).  Relative error
 // ~1e-7 over the whole range: the fp32 gate path stays inside the 1e-6
 // relative target on U (sums of positive terms keep the relative error).
-__device__ __forceinline__ float softplus_fast(float z) {
-    // u = 2^y, y = -|z| log2(e) split exactly as n + f (n integer, |f| <= 1/2)
-    // so the argument rounding does not grow with |z|
+// u = exp(-|z|) in (0, 1]: -|z| log2(e) split exactly as n + f (n integer,
+// |f| <= 1/2) so the argument rounding does not grow with |z|.  n is rounded
+// with the 1.5 * 2^23 magic add (FMA pipe) and read back from the mantissa
+// bits, so the only XU instruction is the MUFU.EX2.
+__device__ __forceinline__ float exp_neg_abs(float z) {
+    const float kMagic = 12582912.0f;  // 1.5 * 2^23
     const float x = fmaxf(-fabsf(z), -87.f);
-    const float n = rintf(x * 1.4426950408889634f);
+    const float tm = fmaf(x, 1.4426950408889634f, kMagic);  // rint(x log2e) in the low mantissa bits
+    const float n = tm - kMagic;
     const float f = fmaf(x, 1.4426950408889634f, -n) + x * 1.925963033500041e-08f;  // log2(e) - fp32(log2(e))
-    const float u = __int_as_float(__float_as_int(exp2f_approx(f)) + ((int)n << 23));  // n >= -126: normal
+    const int ni = __float_as_int(tm) - __float_as_int(kMagic);                     // n >= -126: normal result
+    return __int_as_float(__float_as_int(exp2f_approx(f)) + (ni << 23));
+}
+
+// log1p(u) for u in (0, 1]: 2 atanh(s), s = u/(2+u) in [0, 1/3], odd series in t = s^2
+__device__ __forceinline__ float log1p_unit(float u) {
     const float s = __fdividef(u, 2.f + u);
     const float t = s * s;
     float p = 1.f / 13.f;
@@ -95,7 +104,17 @@ __device__ __forceinline__ float softplus_fast(float z) {
     p = fmaf(p, t, 1.f / 5.f);
     p = fmaf(p, t, 1.f / 3.f);
     p = fmaf(p, t, 1.f);
-    return fmaxf(z, 0.f) + 2.f * s * p;
+    return 2.f * s * p;
+}
+
+__device__ __forceinline__ float softplus_fast(float z) { return fmaxf(z, 0.f) + log1p_unit(exp_neg_abs(z)); }
+
+// softplus(z) and sigmoid(z) from one u = exp(-|z|) (the gate chain rule needs both)
+__device__ __forceinline__ void softplus_sigmoid_fast(float z, float& sp, float& sg) {
+    const float u = exp_neg_abs(z);
+    sp = fmaxf(z, 0.f) + log1p_unit(u);
+    const float r = __fdividef(1.f, 1.f + u);
+    sg = z >= 0.f ? r : u * r;
 }
 
 // sigmoid(z) from u = exp(-|z|): 1/(1+u) or u/(1+u) (no cancellation)

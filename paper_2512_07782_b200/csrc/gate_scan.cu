@@ -497,10 +497,12 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) gate_prefix_bwd_kernel(
                     unpack4(rb[k], bv);
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
-                        const float z = bv[q] * hv[q], be = bv[q] + eps, sg = sigmoid_fast(z);
+                        const float z = bv[q] * hv[q], be = bv[q] + eps;
+                        float sp, sg;
+                        softplus_sigmoid_fast(z, sp, sg);
                         const float rbe = __fdividef(1.f, be);
                         gh[q] = da[q] * sg * bv[q] * rbe;
-                        gb[q] = da[q] * (sg * hv[q] * be - softplus_fast(z)) * (rbe * rbe);
+                        gb[q] = da[q] * (sg * hv[q] * be - sp) * (rbe * rbe);
                     }
                     if (dh) store4(dh + i, gh);
                     if (dbeta) store4(dbeta + i, gb);
@@ -534,10 +536,12 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) gate_prefix_bwd_kernel(
             if (kAlphaIn) {
                 if (dh) dh[i] = from_f32<Tin>(da);
             } else {
-                const float z = bv[k] * hv[k], be = bv[k] + eps, sg = sigmoid_fast(z);
+                const float z = bv[k] * hv[k], be = bv[k] + eps;
+                float sp, sg;
+                softplus_sigmoid_fast(z, sp, sg);
                 const float rbe = __fdividef(1.f, be);
                 if (dh) dh[i] = from_f32<Tin>(da * sg * bv[k] * rbe);
-                if (dbeta) dbeta[i] = from_f32<Tin>(da * (sg * hv[k] * be - softplus_fast(z)) * (rbe * rbe));
+                if (dbeta) dbeta[i] = from_f32<Tin>(da * (sg * hv[k] * be - sp) * (rbe * rbe));
             }
         }
     }
