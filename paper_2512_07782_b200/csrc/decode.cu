@@ -77,6 +77,17 @@ __device__ __forceinline__ uint4 ld_stream(const void* p) {
 }
 
 // one K/V head per query head (G = 1): the streaming kernel of round 1
+// per-lane asynchronous 16-byte global->smem copies (LDGSTS): rows stream into a
+// shared-memory ring without holding registers, many iterations ahead
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+    const int n = pred ? 16 : 0;  // src-size 0 zero-fills (no global read)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(n) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 template <typename T, int D>
 __global__ void __launch_bounds__(kThreads) decode_mha_kernel(DecodeParams p) {
     constexpr int E = Vec<T>::E;           // elements per 16-byte vector
@@ -235,11 +246,12 @@ __global__ void __launch_bounds__(kThreads) decode_mha_kernel(DecodeParams p) {
 }
 
 // GQA: G query heads per K/V head
-#ifndef GFWA_DEC_NB
-#define GFWA_DEC_NB 2
+#ifndef GFWA_DEC_RING
+#define GFWA_DEC_RING 8
 #endif
+constexpr int kRing = GFWA_DEC_RING;  // ring depth: iterations in flight per lane
 #ifndef GFWA_DEC_MINB
-#define GFWA_DEC_MINB 8
+#define GFWA_DEC_MINB 6
 #endif
 template <typename T, int D, int G>
 __global__ void __launch_bounds__(kThreads, GFWA_DEC_MINB) decode_gqa_kernel(DecodeParams p) {
@@ -251,6 +263,8 @@ __global__ void __launch_bounds__(kThreads, GFWA_DEC_MINB) decode_gqa_kernel(Dec
     __shared__ float s_m[kWarps][G], s_l[kWarps][G];
     __shared__ float s_ut[G];
     __shared__ bool s_last;
+    constexpr int R_ = (G >= 8 && D == 128) ? kRing / 2 : kRing;  // static smem stays under 48 KB
+    __shared__ uint4 s_ring[kWarps][R_][32];  // per-warp row ring (16 B per lane per iteration)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int split = blockIdx.x;
@@ -307,20 +321,27 @@ __global__ void __launch_bounds__(kThreads, GFWA_DEC_MINB) decode_gqa_kernel(Dec
     float mloc[G];
 #pragma unroll
     for (int g = 0; g < G; ++g) mloc[g] = -INFINITY;
-    constexpr int NB = GFWA_DEC_NB;  // rows in flight per lane group (memory-level parallelism)
+    // K and V rows stream through a per-warp shared-memory ring: lane li of row
+    // group sub copies its own 16-byte piece of row s = base + sub, kRing
+    // iterations ahead, and later reads back only that piece (no cross-lane hazard)
     constexpr int STEP = kWarps * RPW;
-    for (int sb = s0 + warp * RPW + sub; sb - sub < s1; sb += STEP * NB) {
-        uint4 kr[NB];
+    const int base0 = s0 + warp * RPW;
+    const int niter = base0 < s1 ? (s1 - base0 + STEP - 1) / STEP : 0;  // warp-uniform
+    uint4* ring = &s_ring[warp][0][0];
+    auto issue = [&](const T* cache, const T* newrow, int it) {
+        const int s = base0 + it * STEP + sub;
+        const bool ok = it < niter && s < s1;
+        const T* src = (s == slot_new) ? newrow : cache + (int64_t)(ok ? s : s0) * D;
+        cp_async16(&ring[(it % R_) * 32 + lane], src + li * E, ok);
+        cp_async_commit();
+    };
 #pragma unroll
-        for (int u = 0; u < NB; ++u) {
-            const int s = sb + u * STEP;
-            kr[u] = make_uint4(0u, 0u, 0u, 0u);
-            if (s < s1) kr[u] = ld_stream(((s == slot_new) ? knew : Kc + (int64_t)s * D) + li * E);
-        }
-#pragma unroll
-        for (int u = 0; u < NB; ++u) {
-        const int s = sb + u * STEP;
-        if (s - sub >= s1) break;  // warp-uniform
+    for (int it = 0; it < R_ - 1; ++it) issue(Kc, knew, it);
+    for (int it = 0; it < niter; ++it) {
+        issue(Kc, knew, it + R_ - 1);
+        cp_async_wait<R_ - 1>();  // this lane's piece of iteration `it` has landed
+        const uint4 kq = ring[(it % R_) * 32 + lane];
+        const int s = base0 + it * STEP + sub;
         const bool ok = s < s1;
         float acc[G];
 #pragma unroll
@@ -328,7 +349,7 @@ __global__ void __launch_bounds__(kThreads, GFWA_DEC_MINB) decode_gqa_kernel(Dec
         if (ok) {
             if constexpr (sizeof(T) == 2) {
                 // bf16: element pairs as packed fp32x2 (FFMA2), half the FMA issue slots
-                const uint32_t kw[4] = {kr[u].x, kr[u].y, kr[u].z, kr[u].w};
+                const uint32_t kw[4] = {kq.x, kq.y, kq.z, kq.w};
 #pragma unroll
                 for (int g = 0; g < G; ++g) {
                     uint64_t a2 = 0ull;
@@ -341,7 +362,7 @@ __global__ void __launch_bounds__(kThreads, GFWA_DEC_MINB) decode_gqa_kernel(Dec
                 }
             } else {
                 float kf[E];
-                unpack<T>(kr[u], kf);
+                unpack<T>(kq, kf);
 #pragma unroll
                 for (int g = 0; g < G; ++g)
 #pragma unroll
@@ -368,8 +389,8 @@ __global__ void __launch_bounds__(kThreads, GFWA_DEC_MINB) decode_gqa_kernel(Dec
             const int g = li / (LPR / G);
             s_score[g][s - s0] = fmaf(acc[0], sl2, s_score[g][s - s0]);
         }
-        }
     }
+    cp_async_wait<0>();
     __syncthreads();
     // per-head max over the CTA's slots
 #pragma unroll
@@ -395,49 +416,45 @@ __global__ void __launch_bounds__(kThreads, GFWA_DEC_MINB) decode_gqa_kernel(Dec
 #pragma unroll
         for (int e = 0; e < E; ++e) of[g][e] = 0.f;
     }
-    for (int sb = s0 + warp * RPW + sub; sb - sub < s1; sb += STEP * NB) {
-        uint4 vr[NB];
 #pragma unroll
-        for (int u = 0; u < NB; ++u) {
-            const int s = sb + u * STEP;
-            vr[u] = make_uint4(0u, 0u, 0u, 0u);
-            if (s < s1) vr[u] = ld_stream(((s == slot_new) ? vnew : Vc + (int64_t)s * D) + li * E);
-        }
+    for (int it = 0; it < R_ - 1; ++it) issue(Vc, vnew, it);
+    for (int it = 0; it < niter; ++it) {
+        issue(Vc, vnew, it + R_ - 1);
+        cp_async_wait<R_ - 1>();
+        const uint4 vq = ring[(it % R_) * 32 + lane];
+        const int s = base0 + it * STEP + sub;
+        if (s < s1) {
+            if constexpr (sizeof(T) == 2) {
+                const uint32_t vw[4] = {vq.x, vq.y, vq.z, vq.w};
+                uint64_t v2[4];
 #pragma unroll
-        for (int u = 0; u < NB; ++u) {
-            const int s = sb + u * STEP;
-            if (s < s1) {
-                if constexpr (sizeof(T) == 2) {
-                    const uint32_t vw[4] = {vr[u].x, vr[u].y, vr[u].z, vr[u].w};
-                    uint64_t v2[4];
+                for (int i = 0; i < 4; ++i) v2[i] = sm100::bf2_to_f2(vw[i]);
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) v2[i] = sm100::bf2_to_f2(vw[i]);
+                for (int g = 0; g < G; ++g) {
+                    const float pr = exp2f(s_score[g][s - s0] - m[g]);
+                    const uint64_t p2 = sm100::f2pack(pr, pr);
 #pragma unroll
-                    for (int g = 0; g < G; ++g) {
-                        const float pr = exp2f(s_score[g][s - s0] - m[g]);
-                        const uint64_t p2 = sm100::f2pack(pr, pr);
-#pragma unroll
-                        for (int i = 0; i < 4; ++i) {
-                            uint64_t o2 = sm100::f2pack(of[g][2 * i], of[g][2 * i + 1]);
-                            o2 = sm100::ffma2(p2, v2[i], o2);
-                            sm100::f2unpack(o2, of[g][2 * i], of[g][2 * i + 1]);
-                        }
-                        if (li == 0) lloc[g] += pr;
+                    for (int i = 0; i < 4; ++i) {
+                        uint64_t o2 = sm100::f2pack(of[g][2 * i], of[g][2 * i + 1]);
+                        o2 = sm100::ffma2(p2, v2[i], o2);
+                        sm100::f2unpack(o2, of[g][2 * i], of[g][2 * i + 1]);
                     }
-                } else {
-                    float vf[E];
-                    unpack<T>(vr[u], vf);
+                    if (li == 0) lloc[g] += pr;
+                }
+            } else {
+                float vf[E];
+                unpack<T>(vq, vf);
 #pragma unroll
-                    for (int g = 0; g < G; ++g) {
-                        const float pr = exp2f(s_score[g][s - s0] - m[g]);
+                for (int g = 0; g < G; ++g) {
+                    const float pr = exp2f(s_score[g][s - s0] - m[g]);
 #pragma unroll
-                        for (int e = 0; e < E; ++e) of[g][e] = fmaf(pr, vf[e], of[g][e]);
-                        if (li == 0) lloc[g] += pr;
-                    }
+                    for (int e = 0; e < E; ++e) of[g][e] = fmaf(pr, vf[e], of[g][e]);
+                    if (li == 0) lloc[g] += pr;
                 }
             }
         }
     }
+    cp_async_wait<0>();
     // reduce over the RPW rows of the warp (lanes with equal li)
 #pragma unroll
     for (int g = 0; g < G; ++g) {
