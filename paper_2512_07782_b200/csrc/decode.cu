@@ -4,10 +4,11 @@
 // last min(t+1, w) tokens, so the ring order of the cache is irrelevant.
 //
 // HBM-bound split-KV design (flash-decoding): grid = (splits, H_kv, B); each
-// CTA streams its contiguous slot range of K_cache then V_cache once with
-// 16-byte vector loads, keeps the partial (m, l, o) of every query head of its
-// KV group, and the last CTA of each (b, kv head) merges the partials by LSE
-// (atomic ticket, self-resetting counter).  The slot being replaced (t mod w)
+// CTA streams its contiguous slot range of K_cache then V_cache once through a
+// per-warp cp.async shared-memory ring (16-byte pieces, 8 iterations in flight
+// per lane without holding registers), keeps the partial (m, l, o) of every
+// query head of its KV group, and the last CTA of each (b, kv head) merges the
+// partials by LSE (atomic ticket, self-resetting counter).  The slot being replaced (t mod w)
 // is never read from the cache: its owner CTA uses k_new/v_new directly and
 // writes them back, so the in-place update cannot race with the readers (no
 // other CTA touches that slot).
@@ -68,15 +69,6 @@ __device__ __forceinline__ void unpack(const uint4& u, float* f) {
     }
 }
 
-__device__ __forceinline__ uint4 ld_stream(const void* p) {
-    uint4 r;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-                 : "l"(p));
-    return r;
-}
-
-// one K/V head per query head (G = 1): the streaming kernel of round 1
 // per-lane asynchronous 16-byte global->smem copies (LDGSTS): rows stream into a
 // shared-memory ring without holding registers, many iterations ahead
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
@@ -88,164 +80,7 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-template <typename T, int D>
-__global__ void __launch_bounds__(kThreads) decode_mha_kernel(DecodeParams p) {
-    constexpr int E = Vec<T>::E;           // elements per 16-byte vector
-    constexpr int LPR = D / E;             // lanes per cache row
-    constexpr int RPW = 32 / LPR;          // rows per warp iteration
-    __shared__ float s_score[kMaxSlotsPerCta];
-    __shared__ float s_red[kWarps][D];
-    __shared__ float s_m[kWarps], s_l[kWarps];
-    __shared__ bool s_last;
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int split = blockIdx.x;
-    const int64_t h = blockIdx.y, b = blockIdx.z, bh = b * p.H + h;
-    const int64_t t = p.pos[b];
-    const int w = p.w;
-    const int n_valid = (int)min64(t + 1, w);
-    const int slot_new = (int)(t % w);
-    const int s0 = split * p.slots_per_cta;
-    const int s1 = min(s0 + p.slots_per_cta, n_valid);
-
-    // u_t = u_{t-1} - alpha_t, u_{t-1} from the ring (0 before the first token)
-    const float u_prev = t > 0 ? p.Uc[bh * w + (int)((t - 1) % w)] : 0.f;
-    float alpha;
-    if (p.gate_kind == GFWA_GATE_ALPHA) {
-        alpha = p.gate_a[bh];
-    } else {
-        const float hv = p.gate_a[bh], bv = p.gate_b[bh];
-        alpha = softplus_f(bv * hv) / (bv + p.eps);
-    }
-    const float u_t = u_prev - alpha;
-
-    const T* qrow = (const T*)p.q + bh * D;
-    const T* Kc = (const T*)p.Kc + bh * (int64_t)w * D;
-    const T* Vc = (const T*)p.Vc + bh * (int64_t)w * D;
-    const T* knew = (const T*)p.k_new + bh * D;
-    const T* vnew = (const T*)p.v_new + bh * D;
-    const float* Uc = p.Uc + bh * w;
-    const int sub = lane / LPR, li = lane % LPR;  // row within the warp iteration, lane in row
-
-    float qf[E];
-    unpack<T>(*reinterpret_cast<const uint4*>(qrow + li * E), qf);
-    const float sl2 = p.scale * kLog2e;
-
-    // pass 1: scores (log2 units) s_i = scale q.k_i + (u_t - u_i)
-    float mloc = -INFINITY;
-    for (int s = s0 + warp * RPW + sub; s - sub < s1; s += kWarps * RPW) {
-        const bool ok = s < s1;
-        float acc = 0.f;
-        float ui = u_t;
-        if (ok) {
-            const T* krow = (s == slot_new) ? knew : Kc + (int64_t)s * D;
-            float kf[E];
-            unpack<T>(ld_stream(krow + li * E), kf);
-#pragma unroll
-            for (int e = 0; e < E; ++e) acc = fmaf(qf[e], kf[e], acc);
-            if (s != slot_new) ui = Uc[s];
-        }
-#pragma unroll
-        for (int o = LPR / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (ok && li == 0) {
-            const float sc = fmaf(acc, sl2, (u_t - ui) * kLog2e);
-            s_score[s - s0] = sc;
-            mloc = fmaxf(mloc, sc);
-        }
-    }
-    mloc = warp_max(mloc);
-    if (lane == 0) s_m[warp] = mloc;
-    __syncthreads();
-    float m = s_m[0];
-#pragma unroll
-    for (int i = 1; i < kWarps; ++i) m = fmaxf(m, s_m[i]);
-
-    // pass 2: o_part = sum_i exp2(s_i - m) v_i, l = sum_i exp2(s_i - m)
-    float of[E];
-#pragma unroll
-    for (int e = 0; e < E; ++e) of[e] = 0.f;
-    float lloc = 0.f;
-    for (int s = s0 + warp * RPW + sub; s - sub < s1; s += kWarps * RPW) {
-        if (s < s1) {
-            const float pr = exp2f(s_score[s - s0] - m);
-            const T* vrow = (s == slot_new) ? vnew : Vc + (int64_t)s * D;
-            float vf[E];
-            unpack<T>(ld_stream(vrow + li * E), vf);
-#pragma unroll
-            for (int e = 0; e < E; ++e) of[e] = fmaf(pr, vf[e], of[e]);
-            if (li == 0) lloc += pr;
-        }
-    }
-    // reduce over the RPW rows of the warp (lanes with equal li)
-#pragma unroll
-    for (int o = LPR; o < 32; o <<= 1) {
-#pragma unroll
-        for (int e = 0; e < E; ++e) of[e] += __shfl_xor_sync(0xffffffffu, of[e], o);
-    }
-    lloc = warp_sum(lloc);
-    if (sub == 0) {
-#pragma unroll
-        for (int e = 0; e < E; ++e) s_red[warp][li * E + e] = of[e];
-    }
-    if (lane == 0) s_l[warp] = lloc;
-    __syncthreads();
-
-    // partial of this split -> workspace
-    float* part = p.part + (bh * p.splits + split) * (int64_t)(D + 2);
-    for (int c = threadIdx.x; c < D; c += kThreads) {
-        float acc = 0.f;
-#pragma unroll
-        for (int i = 0; i < kWarps; ++i) acc += s_red[i][c];
-        part[c] = acc;
-    }
-    if (threadIdx.x == 0) {
-        float l = 0.f;
-        for (int i = 0; i < kWarps; ++i) l += s_l[i];
-        part[D] = (s0 < s1) ? m : -INFINITY;
-        part[D + 1] = l;
-    }
-    // owner of the new slot writes the token into the ring (no reader races)
-    if (slot_new >= s0 && slot_new < s0 + p.slots_per_cta) {
-        T* kd = (T*)p.Kc + bh * (int64_t)w * D + (int64_t)slot_new * D;
-        T* vd = (T*)p.Vc + bh * (int64_t)w * D + (int64_t)slot_new * D;
-        for (int c = threadIdx.x; c < D; c += kThreads) {
-            kd[c] = knew[c];
-            vd[c] = vnew[c];
-        }
-        if (threadIdx.x == 0) p.Uc[bh * w + slot_new] = u_t;
-    }
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const unsigned prev = atomicAdd(p.counter + bh, 1u);
-        s_last = (prev == (unsigned)p.splits - 1);
-    }
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    // LSE merge of the split partials (natural layout: o = sum o_i 2^(m_i-M) / L)
-    const float* pb = p.part + bh * p.splits * (int64_t)(D + 2);
-    float M = -INFINITY;
-    for (int i = 0; i < p.splits; ++i) M = fmaxf(M, __ldcg(pb + i * (D + 2) + D));
-    float L = 0.f;
-    for (int i = 0; i < p.splits; ++i) {
-        const float mi = __ldcg(pb + i * (D + 2) + D);
-        if (mi != -INFINITY) L += __ldcg(pb + i * (D + 2) + D + 1) * exp2f(mi - M);
-    }
-    const float invL = 1.f / L;
-    T* orow = (T*)p.o + bh * D;
-    for (int c = threadIdx.x; c < D; c += kThreads) {
-        float acc = 0.f;
-        for (int i = 0; i < p.splits; ++i) {
-            const float mi = __ldcg(pb + i * (D + 2) + D);
-            if (mi != -INFINITY) acc += __ldcg(pb + i * (D + 2) + c) * exp2f(mi - M);
-        }
-        orow[c] = from_f32<T>(acc * invL);
-    }
-    if (threadIdx.x == 0) p.counter[bh] = 0u;  // leave the workspace zeroed
-}
-
-// GQA: G query heads per K/V head
+// G query heads per K/V head (G = 1: multi-head attention, one K/V head per query head)
 #ifndef GFWA_DEC_RING
 #define GFWA_DEC_RING 8
 #endif
@@ -254,7 +89,7 @@ constexpr int kRing = GFWA_DEC_RING;  // ring depth: iterations in flight per la
 #define GFWA_DEC_MINB 6
 #endif
 template <typename T, int D, int G>
-__global__ void __launch_bounds__(kThreads, GFWA_DEC_MINB) decode_gqa_kernel(DecodeParams p) {
+__global__ void __launch_bounds__(kThreads, GFWA_DEC_MINB) decode_kernel(DecodeParams p) {
     constexpr int E = Vec<T>::E;           // elements per 16-byte vector
     constexpr int LPR = D / E;             // lanes per cache row
     constexpr int RPW = 32 / LPR;          // rows per warp iteration
@@ -569,10 +404,10 @@ extern "C" size_t gfwa_decode_workspace_size(const gfwa_decode_desc_t* d) {
 template <typename T, int D>
 static void launch_decode(dim3 grid, const DecodeParams& p, int G, cudaStream_t st) {
     switch (G) {
-        case 1: decode_mha_kernel<T, D><<<grid, kThreads, 0, st>>>(p); break;
-        case 2: decode_gqa_kernel<T, D, 2><<<grid, kThreads, 0, st>>>(p); break;
-        case 4: decode_gqa_kernel<T, D, 4><<<grid, kThreads, 0, st>>>(p); break;
-        default: decode_gqa_kernel<T, D, 8><<<grid, kThreads, 0, st>>>(p); break;
+        case 1: decode_kernel<T, D, 1><<<grid, kThreads, 0, st>>>(p); break;
+        case 2: decode_kernel<T, D, 2><<<grid, kThreads, 0, st>>>(p); break;
+        case 4: decode_kernel<T, D, 4><<<grid, kThreads, 0, st>>>(p); break;
+        default: decode_kernel<T, D, 8><<<grid, kThreads, 0, st>>>(p); break;
     }
 }
 
