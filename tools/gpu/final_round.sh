@@ -14,5 +14,6 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 
 ncu --set full --import-source on --clock-control none -k regex:gate_prefix_kernel -c 1 -o $O/gate_fwd python profiles/prof_gate.py > /dev/null 2>&1
 ncu --set full --import-source on --clock-control none -k regex:gate_prefix_bwd -c 1 -o $O/gate_bwd python profiles/prof_gate.py > /dev/null 2>&1
 ncu --set full --import-source on --clock-control none -k regex:decode_kernel -c 1 -o $O/decode_gqa python profiles/prof_decode_gqa.py > /dev/null 2>&1
+ncu --set full --import-source on --clock-control none -k regex:decode_kernel -c 1 -o $O/decode python profiles/prof_decode.py > /dev/null 2>&1
 ncu --set full --import-source on --clock-control none -k regex:bwd_tc_kernel -c 1 -o $O/bwd python profiles/prof_step.py > /dev/null 2>&1
 ls $O
