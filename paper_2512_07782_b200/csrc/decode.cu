@@ -143,13 +143,26 @@ __global__ void __launch_bounds__(kThreads, GFWA_DEC_MINB) decode_kernel(DecodeP
     // bias (u_t - u_i) log2e of every (head, slot) of this CTA, loaded coalesced up front
     // (a per-row u load inside pass 1 would stall the in-order warp on every row)
     const int nsl = max(s1 - s0, 0);
-    for (int i = threadIdx.x; i < G * nsl; i += kThreads) {
-        const int g = i / nsl, j = i % nsl, s = s0 + j;
-        float ut = u_t[0];
+    constexpr int kU = 8;  // independent u loads in flight per thread
+    for (int i0 = threadIdx.x; i0 < G * nsl; i0 += kThreads * kU) {
+        float uv[kU];
 #pragma unroll
-        for (int gg = 1; gg < G; ++gg)
-            if (g == gg) ut = u_t[gg];
-        s_score[g][j] = (s == slot_new) ? 0.f : (ut - __ldg(p.Uc + (bh0 + g) * w + s)) * kLog2e;
+        for (int k = 0; k < kU; ++k) {
+            const int i = i0 + k * kThreads;
+            uv[k] = 0.f;
+            if (i < G * nsl) uv[k] = __ldg(p.Uc + (bh0 + i / nsl) * w + s0 + i % nsl);
+        }
+#pragma unroll
+        for (int k = 0; k < kU; ++k) {
+            const int i = i0 + k * kThreads;
+            if (i >= G * nsl) break;
+            const int g = i / nsl, j = i % nsl;
+            float ut = u_t[0];
+#pragma unroll
+            for (int gg = 1; gg < G; ++gg)
+                if (g == gg) ut = u_t[gg];
+            s_score[g][j] = (s0 + j == slot_new) ? 0.f : (ut - uv[k]) * kLog2e;
+        }
     }
     __syncthreads();
     // pass 1: scores (log2 units) s_i = scale q.k_i + (u_t - u_i), each K row read once for G queries
