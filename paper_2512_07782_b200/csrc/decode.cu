@@ -255,6 +255,18 @@ __global__ void __launch_bounds__(kThreads, GFWA_DEC_MINB) decode_kernel(DecodeP
 #pragma unroll
         for (int i = 1; i < kWarps; ++i) m[g] = fmaxf(m[g], s_m[i][g]);
     }
+    // G > 1: p_i = exp2(s_i - m) once per (head, slot), in place: the 16 lanes of a row
+    // then read it as a shared-memory broadcast instead of each evaluating G exponentials
+    constexpr bool kPre = G > 1;
+    for (int i = threadIdx.x; kPre && i < G * nsl; i += kThreads) {
+        const int g = i / nsl, j = i % nsl;
+        float mg = m[0];
+#pragma unroll
+        for (int gg = 1; gg < G; ++gg)
+            if (g == gg) mg = m[gg];
+        s_score[g][j] = exp2f(s_score[g][j] - mg);
+    }
+    if (kPre) __syncthreads();
 
     // pass 2: o_part = sum_i exp2(s_i - m) v_i, l = sum_i exp2(s_i - m), each V row read once
     float of[G][E], lloc[G];
@@ -279,7 +291,7 @@ __global__ void __launch_bounds__(kThreads, GFWA_DEC_MINB) decode_kernel(DecodeP
                 for (int i = 0; i < 4; ++i) v2[i] = sm100::bf2_to_f2(vw[i]);
 #pragma unroll
                 for (int g = 0; g < G; ++g) {
-                    const float pr = exp2f(s_score[g][s - s0] - m[g]);
+                    const float pr = kPre ? s_score[g][s - s0] : exp2f(s_score[g][s - s0] - m[g]);
                     const uint64_t p2 = sm100::f2pack(pr, pr);
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
@@ -294,7 +306,7 @@ __global__ void __launch_bounds__(kThreads, GFWA_DEC_MINB) decode_kernel(DecodeP
                 unpack<T>(vq, vf);
 #pragma unroll
                 for (int g = 0; g < G; ++g) {
-                    const float pr = exp2f(s_score[g][s - s0] - m[g]);
+                    const float pr = kPre ? s_score[g][s - s0] : exp2f(s_score[g][s - s0] - m[g]);
 #pragma unroll
                     for (int e = 0; e < E; ++e) of[g][e] = fmaf(pr, vf[e], of[g][e]);
                     if (li == 0) lloc[g] += pr;
