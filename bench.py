@@ -272,6 +272,13 @@ def run_ours(args):
     aux = {}
     if rank == 0 and not args.no_aux:
         aux = run_aux(dev, peaks)
+    if not args.no_aux and args.workload == "C2":
+        # the north_star's sequence-sharded C4 step on the same ranks (strong scaling
+        # of one N = 131072 sequence; a few steps, max over ranks)
+        seq = measure_seq(3, 3, dist, rank, world, local, dev)
+        if rank == 0:
+            aux["seq_sharded_C4"] = {k: seq[k] for k in ("ms_per_step", "tokens_per_s", "tflops_in_window", "steps")}
+            aux["seq_sharded_C4"]["parallelism"] = seq["config"]["parallelism"]
     if rank != 0:
         return
     cpu = cpu_baseline(args, s) if not args.no_cpu else None
@@ -322,14 +329,33 @@ def run_seq(args):
     r -> r+1 and halo gradients r+1 -> r over NCCL P2P; strong scaling)."""
     import torch
 
-    import synth
-    from paper_2512_07782_b200 import binding as gb
-    from paper_2512_07782_b200.dist import Ring, cuda_ops, sp_forward_backward
-
     dist, rank, world, local = _dist()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     peaks = _peaks()
+    r = measure_seq(args.steps, args.warmup, dist, rank, world, local, dev, sample_clocks=True)
+    if rank != 0:
+        return
+    print(json.dumps({
+        "metric": METRIC, "value": r["tokens_per_s"], "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (synth.py seeded per rank)",
+        "config": r["config"],
+        "tflops_in_window": r["tflops_in_window"], "pct_bf16_peak": round(r["tflops_in_window"] / peaks["bf16"], 4),
+        "gpu_launches": r["gpu_launches"], "clocks": r.get("clocks"),
+    }), flush=True)
+
+
+def measure_seq(steps, warmup, dist, rank, world, local, dev, sample_clocks=False):
+    """One C4 sequence-sharded training step timed over all ranks (max over ranks);
+    every rank must call it (halo P2P and the max are collective)."""
+    import torch
+
+    import synth
+    from paper_2512_07782_b200 import binding as gb
+    from paper_2512_07782_b200.dist import Ring, cuda_ops, sp_forward_backward
+
     c = synth.CONFIGS["C4"]
     Ng = c["N"]
     S = Ng // world
@@ -345,9 +371,10 @@ def run_seq(args):
     def step():
         return sp_forward_backward(Q, K, V, h, beta, dO, s.w, ops, ring)
 
-    clk = ClockSampler(local).start()
-    time.sleep(0.3)
-    for _ in range(args.warmup):
+    clk = ClockSampler(local).start() if sample_clocks else None
+    if clk:
+        time.sleep(0.3)
+    for _ in range(warmup):
         step()
     torch.cuda.synchronize(dev)
     if dist:
@@ -356,29 +383,27 @@ def run_seq(args):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     wall0 = time.time()
     e0.record(st)
-    for _ in range(args.steps):
+    for _ in range(steps):
         step()
     e1.record(st)
     torch.cuda.synchronize(dev)
-    clk.mark(wall0, time.time())
-    clk.stop()
+    out = {}
+    if clk:
+        clk.mark(wall0, time.time())
+        clk.stop()
+        out["clocks"] = clk.summary()
     launches = gb.launch_count() - n0
-    ms = _max_over_ranks(dist, e0.elapsed_time(e1) / args.steps, dev)
+    ms = _max_over_ranks(dist, e0.elapsed_time(e1) / steps, dev)
     fl = 14.0 * Ng * s.w * s.d * s.B * s.H  # fwd 4 + bwd 10 (north_star in-window count)
-    tflops = fl / (ms * 1e-3) / 1e12
-    if rank != 0:
-        return
-    print(json.dumps({
-        "metric": METRIC, "value": round(s.B * Ng / (ms * 1e-3), 1), "unit": "tokens/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
-        "data": "synthetic (synth.py seeded per rank)",
+    out.update({
+        "ms_per_step": round(ms, 4), "tokens_per_s": round(s.B * Ng / (ms * 1e-3), 1),
+        "tflops_in_window": round(fl / (ms * 1e-3) / 1e12, 2), "gpu_launches": launches, "steps": steps,
         "config": {"workload": "C4 (BASELINE configs[3])", "B": s.B, "H": s.H, "N": Ng, "rows_per_rank": S,
                    "d": s.d, "w": s.w, "parallelism": f"sequence-sharded x{world} (w-row K/V/u halo, NCCL P2P)",
-                   "l2": "inputs larger than L2, no flush"},
-        "tflops_in_window": round(tflops, 2), "pct_bf16_peak": round(tflops / peaks["bf16"], 4),
-        "gpu_launches": launches, "clocks": clk.summary(),
-    }), flush=True)
+                   "l2": "inputs larger than L2, no flush"}})
+    del Q, K, V, dO, h, beta
+    torch.cuda.empty_cache()
+    return out
 
 
 def _traffic_from_profiles(kind: str, workload: str):
