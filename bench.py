@@ -354,7 +354,7 @@ def measure_seq(steps, warmup, dist, rank, world, local, dev, sample_clocks=Fals
 
     import synth
     from paper_2512_07782_b200 import binding as gb
-    from paper_2512_07782_b200.dist import Ring, cuda_ops, sp_forward_backward
+    from paper_2512_07782_b200.dist import Ring, alloc_kv_ext, cuda_ops, sp_forward_backward
 
     c = synth.CONFIGS["C4"]
     Ng = c["N"]
@@ -367,9 +367,10 @@ def measure_seq(steps, warmup, dist, rank, world, local, dev, sample_clocks=Fals
     ring = Ring() if world > 1 else _SoloRing()
     ops = cuda_ops()
     st = torch.cuda.current_stream(dev)
+    kv_ext, K, V = alloc_kv_ext(K, V, s.w)  # K/V resident behind a w-row halo slot
 
     def step():
-        return sp_forward_backward(Q, K, V, h, beta, dO, s.w, ops, ring)
+        return sp_forward_backward(Q, K, V, h, beta, dO, s.w, ops, ring, kv_ext=kv_ext)
 
     clk = ClockSampler(local).start() if sample_clocks else None
     if clk:
@@ -401,7 +402,7 @@ def measure_seq(steps, warmup, dist, rank, world, local, dev, sample_clocks=Fals
         "config": {"workload": "C4 (BASELINE configs[3])", "B": s.B, "H": s.H, "N": Ng, "rows_per_rank": S,
                    "d": s.d, "w": s.w, "parallelism": f"sequence-sharded x{world} (w-row K/V/u halo, NCCL P2P)",
                    "l2": "inputs larger than L2, no flush"}})
-    del Q, K, V, dO, h, beta
+    del Q, K, V, dO, h, beta, kv_ext
     torch.cuda.empty_cache()
     return out
 

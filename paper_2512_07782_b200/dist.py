@@ -125,11 +125,27 @@ def global_offset(total: torch.Tensor, ring: Ring) -> torch.Tensor:
     return out
 
 
-def sp_forward_backward(Q, K, V, h, beta, dO, w: int, ops: Ops, ring: Ring, eps: float = 1e-6) -> ShardResult:
+def alloc_kv_ext(K: torch.Tensor, V: torch.Tensor, w: int):
+    """[halo; local] K/V buffers of S + w rows holding a copy of the local K, V in
+    rows [w, S + w).  Pass them as ``kv_ext`` (and the returned local views as
+    K, V) so every step receives the halo in place and the attention calls run
+    on views: no per-step concatenation of the S local rows."""
+    B, S, H, d = K.shape
+    Kx = torch.empty(B, S + w, H, d, dtype=K.dtype, device=K.device)
+    Vx = torch.empty_like(Kx)
+    Kx[:, w:].copy_(K)
+    Vx[:, w:].copy_(V)
+    return (Kx, Vx), Kx[:, w:], Vx[:, w:]
+
+
+def sp_forward_backward(Q, K, V, h, beta, dO, w: int, ops: Ops, ring: Ring, eps: float = 1e-6,
+                        kv_ext=None) -> ShardResult:
     """One sequence-sharded training step on this rank's S rows.
 
     Q, K, V, dO [B,S,H,d]; h, beta [B,S,H] (this rank's contiguous rows).
-    Requires w <= S (one-hop halo)."""
+    Requires w <= S (one-hop halo).  kv_ext = (K_ext, V_ext) from alloc_kv_ext
+    (K, V then being their local views) avoids copying the local rows every step;
+    dK, dV are then returned as views of the backward's [halo; local] outputs."""
     S = K.shape[1]
     if w > S:
         raise ValueError(f"sequence sharding needs w <= rows per rank ({w} > {S})")
@@ -139,8 +155,13 @@ def sp_forward_backward(Q, K, V, h, beta, dO, w: int, ops: Ops, ring: Ring, eps:
     like = halo_pack(K, V, U_loc, w)
     recv = ring.shift(like if r < P - 1 else None, like, forward=True)
     if recv is not None:
-        Kx = torch.cat([recv[0], K], 1)
-        Vx = torch.cat([recv[1], V], 1)
+        if kv_ext is not None:
+            Kx, Vx = kv_ext  # the w halo rows land in front of the resident local rows
+            Kx[:, :w].copy_(recv[0])
+            Vx[:, :w].copy_(recv[1])
+        else:
+            Kx = torch.cat([recv[0], K], 1)
+            Vx = torch.cat([recv[1], V], 1)
         Ux = torch.cat([recv[2], U_loc], -1).contiguous()
         h0 = w
     else:
@@ -148,10 +169,13 @@ def sp_forward_backward(Q, K, V, h, beta, dO, w: int, ops: Ops, ring: Ring, eps:
     O, LSE, O32 = ops.fwd(Q, Kx, Vx, Ux, w)
     dQ, dKx, dVx, dUx = ops.bwd(Q, Kx, Vx, Ux, O, LSE, dO, w, O32)
     # backward halo r -> r-1: gradients of the halo rows
-    back_like = [dKx[:, :w], dVx[:, :w], dUx[..., :w]] if h0 else [dKx[:, :w], dVx[:, :w], dUx[..., :w]]
+    back_like = [dKx[:, :w], dVx[:, :w], dUx[..., :w]]
     back = ring.shift([t.contiguous() for t in back_like] if h0 else None, back_like, forward=False)
-    dK = dKx[:, h0:].contiguous()
-    dV = dVx[:, h0:].contiguous()
+    if kv_ext is not None:
+        dK, dV = dKx[:, h0:], dVx[:, h0:]  # views: no copy of the S local rows
+    else:
+        dK = dKx[:, h0:].contiguous()
+        dV = dVx[:, h0:].contiguous()
     dU = dUx[..., h0:].contiguous()
     carry = None
     if back is not None:

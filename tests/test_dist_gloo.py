@@ -52,30 +52,34 @@ def _inputs(B, N, H, d, seed):
     return Q, K, V, dO, h, beta
 
 
-def _worker(rank, world, port, outdir, B, N, H, d, w):
+def _worker(rank, world, port, outdir, B, N, H, d, w, use_ext=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from paper_2512_07782_b200.dist import Ring, sp_forward_backward
+        from paper_2512_07782_b200.dist import Ring, alloc_kv_ext, sp_forward_backward
 
         Q, K, V, dO, h, beta = _inputs(B, N, H, d, 5)
         S = N // world
         sl = slice(rank * S, (rank + 1) * S)
-        res = sp_forward_backward(Q[:, sl], K[:, sl], V[:, sl], h[:, sl], beta[:, sl], dO[:, sl], w, _oracle_ops(),
-                                  Ring())
+        Kl, Vl, kv_ext = K[:, sl], V[:, sl], None
+        if use_ext:  # [halo; local] buffers: the halo lands in place, no per-step concatenation
+            kv_ext, Kl, Vl = alloc_kv_ext(Kl, Vl, w)
+        res = sp_forward_backward(Q[:, sl], Kl, Vl, h[:, sl], beta[:, sl], dO[:, sl], w, _oracle_ops(),
+                                  Ring(), kv_ext=kv_ext)
         torch.save({k: getattr(res, k) for k in ("O", "LSE", "U_loc", "dQ", "dK", "dV", "dalpha", "dh", "dbeta")},
                    os.path.join(outdir, f"r{rank}.pt"))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,N,w", [(2, 48, 10), (2, 40, 20), (3, 60, 7)])
-def test_sequence_sharded_matches_unsharded(world, N, w):
+@pytest.mark.parametrize("world,N,w,use_ext", [(2, 48, 10, False), (2, 40, 20, False), (3, 60, 7, False),
+                                               (2, 48, 10, True), (3, 60, 7, True)])
+def test_sequence_sharded_matches_unsharded(world, N, w, use_ext):
     B, H, d = 1, 2, 8
-    port = 29500 + (os.getpid() % 2000)
+    port = 29500 + (os.getpid() % 2000) + (7 if use_ext else 0)
     with tempfile.TemporaryDirectory() as outdir:
-        mp.spawn(_worker, args=(world, port, outdir, B, N, H, d, w), nprocs=world, join=True)
+        mp.spawn(_worker, args=(world, port, outdir, B, N, H, d, w, use_ext), nprocs=world, join=True)
         Q, K, V, dO, h, beta = _inputs(B, N, H, d, 5)
         U, _, _ = oracle.gate_prefix_hbeta(h, beta)
         O, L = oracle.fwd(Q, K, V, U, w)

@@ -27,19 +27,22 @@ def _inputs():
     return Q, K, V, dO, h, beta
 
 
-def _worker(rank, world, port, outdir):
+def _worker(rank, world, port, outdir, use_ext=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from paper_2512_07782_b200.dist import Ring, cuda_ops, sp_forward_backward
+        from paper_2512_07782_b200.dist import Ring, alloc_kv_ext, cuda_ops, sp_forward_backward
 
         torch.cuda.set_device(0)
         Q, K, V, dO, h, beta = _inputs()
         S = N // world
         sl = slice(rank * S, (rank + 1) * S)
         cu = lambda x: x[:, sl].contiguous().cuda()  # noqa: E731
-        res = sp_forward_backward(cu(Q), cu(K), cu(V), cu(h), cu(beta), cu(dO), W, cuda_ops(), Ring())
+        Kl, Vl, kv_ext = cu(K), cu(V), None
+        if use_ext:  # [halo; local] resident buffers (the bench's C4 path)
+            kv_ext, Kl, Vl = alloc_kv_ext(Kl, Vl, W)
+        res = sp_forward_backward(cu(Q), Kl, Vl, cu(h), cu(beta), cu(dO), W, cuda_ops(), Ring(), kv_ext=kv_ext)
         torch.cuda.synchronize()
         torch.save({k: getattr(res, k).float().cpu() for k in ("O", "dQ", "dK", "dV", "dU", "dalpha")},
                    os.path.join(outdir, f"r{rank}.pt"))
@@ -47,11 +50,12 @@ def _worker(rank, world, port, outdir):
         dist.destroy_process_group()
 
 
-def test_sequence_sharded_cuda_matches_oracle():
+@pytest.mark.parametrize("use_ext", [False, True])
+def test_sequence_sharded_cuda_matches_oracle(use_ext):
     world = 2
-    port = 31500 + (os.getpid() % 2000)
+    port = 31500 + (os.getpid() % 2000) + (11 if use_ext else 0)
     with tempfile.TemporaryDirectory() as outdir:
-        mp.spawn(_worker, args=(world, port, outdir), nprocs=world, join=True)
+        mp.spawn(_worker, args=(world, port, outdir, use_ext), nprocs=world, join=True)
         Q, K, V, dO, h, beta = _inputs()
         U, _, _ = oracle.gate_prefix_hbeta(h, beta)
         O, _ = oracle.fwd(Q, K, V, U, W)
