@@ -322,6 +322,12 @@ class _SoloRing:
     def shift(self, send, recv_like, forward):
         return None
 
+    def start(self, send, recv_like, forward):
+        return None
+
+    def finish(self, handle):
+        return None
+
 
 def run_seq(args):
     """--workload C4: BASELINE configs[3] (B=1, H=32, N=131072, d=128, w=2048)

@@ -280,14 +280,21 @@ def gfwa_gate_prefix_bwd(dU: torch.Tensor, h: torch.Tensor | None = None, beta: 
 # --------------------------------------------------------------------------- attention
 
 
-def gfwa_fwd(Q, K, V, U, w: int, scale: float | None = None, want_o_f32: bool = False, out=None):
-    """O [B,Nq,H,d], LSE [B,H,Nq] (+ O_f32) per Eq. 12 / Alg. 2."""
+def gfwa_fwd(Q, K, V, U, w: int, scale: float | None = None, want_o_f32: bool = False, out=None, out_f32=None):
+    """O [B,Nq,H,d], LSE [B,H,Nq] (+ O_f32) per Eq. 12 / Alg. 2.
+    out / out_f32: caller tensors (views allowed) receiving O and O_f32; O_f32
+    must share O's element strides (the ABI's one stride set)."""
     lib = load()
     _need_cuda(Q, K, V, U)
     U = U.contiguous()
     B, Nq, H, d = Q.shape
     O = out if out is not None else torch.empty(B, Nq, H, d, dtype=Q.dtype, device=Q.device)
-    O_f32 = torch.empty_strided(O.shape, O.stride(), dtype=torch.float32, device=Q.device) if want_o_f32 else None
+    if out_f32 is not None:
+        if out_f32.stride() != O.stride() or out_f32.dtype != torch.float32:
+            raise GfwaError("out_f32 must be fp32 with the strides of O")
+        O_f32 = out_f32
+    else:
+        O_f32 = torch.empty_strided(O.shape, O.stride(), dtype=torch.float32, device=Q.device) if want_o_f32 else None
     LSE = torch.empty(B, H, Nq, dtype=torch.float32, device=Q.device)
     dsc = make_desc(Q, K, V, O, w, scale)
     st = lib.gfwa_fwd(ctypes.byref(dsc), _ptr(Q), _ptr(K), _ptr(V), _ptr(U), _ptr(O), _ptr(O_f32), _ptr(LSE),

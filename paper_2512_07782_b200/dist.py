@@ -38,6 +38,9 @@ class Ops:
     fwd: Callable           # (Q, K, V, U, w) -> (O, LSE, O_f32)
     bwd: Callable           # (Q, K, V, U, O, LSE, dO, w, O_f32) -> (dQ, dK, dV, dU)
     gate_bwd: Callable      # (dU, h, beta, eps, carry fp64 [B,H] | None) -> (dalpha, dh, dbeta)
+    # (Q, K, V, U, w, O_out, O32_out | None) -> LSE: the forward written into caller views
+    # (lets the step run the interior queries while the halo is in flight); None: no split
+    fwd_into: Callable | None = None
 
 
 def cuda_ops() -> Ops:
@@ -54,8 +57,11 @@ def cuda_ops() -> Ops:
     def _gate_bwd(dU, h, beta, eps, carry):
         return gb.gfwa_gate_prefix_bwd(dU, h, beta, eps, carry=carry)
 
+    def _fwd_into(Q, K, V, U, w, O_out, O32_out):
+        return gb.gfwa_fwd(Q, K, V, U, w, out=O_out, out_f32=O32_out)[1]
+
     return Ops(gate_prefix=lambda h, b, eps: gb.gfwa_gate_prefix(h, b, eps), fwd=_fwd, bwd=_bwd,
-               gate_bwd=_gate_bwd)
+               gate_bwd=_gate_bwd, fwd_into=_fwd_into)
 
 
 class Ring:
@@ -73,6 +79,11 @@ class Ring:
 
     def shift(self, send: list[torch.Tensor] | None, recv_like: list[torch.Tensor] | None, forward: bool):
         """forward=True: rank r sends to r+1 and receives from r-1 (else the reverse)."""
+        return self.finish(self.start(send, recv_like, forward))
+
+    def start(self, send, recv_like, forward: bool):
+        """Post the exchange of shift() and return a handle for finish(); with NCCL the
+        transfer runs on NCCL's stream while the caller enqueues independent work."""
         dst = self.rank + 1 if forward else self.rank - 1
         src = self.rank - 1 if forward else self.rank + 1
         ops = []
@@ -86,9 +97,13 @@ class Ring:
             dev = recv_like[0].device
             recv = [torch.empty_like(t, device="cpu" if self.stage else t.device) for t in recv_like]
             ops += [dist.P2POp(dist.irecv, t, self._glob(src), self.group) for t in recv]
-        if ops:
-            for req in dist.batch_isend_irecv(ops):
-                req.wait()
+        reqs = dist.batch_isend_irecv(ops) if ops else []
+        return reqs, recv, dev
+
+    def finish(self, handle):
+        reqs, recv, dev = handle
+        for req in reqs:
+            req.wait()  # NCCL: the current stream waits for the transfer (no host block)
         if recv is not None and self.stage:
             recv = [t.to(dev) for t in recv]
         return recv
@@ -153,7 +168,17 @@ def sp_forward_backward(Q, K, V, h, beta, dO, w: int, ops: Ops, ring: Ring, eps:
     U_loc = ops.gate_prefix(h, beta, eps)
     # forward halo r -> r+1 (K, V, u in the receiver's frame)
     like = halo_pack(K, V, U_loc, w)
-    recv = ring.shift(like if r < P - 1 else None, like, forward=True)
+    handle = ring.start(like if r < P - 1 else None, like, forward=True)
+    split = kv_ext is not None and ops.fwd_into is not None and r > 0 and 2 * w <= S
+    if split:
+        # queries [w, S) see only local keys: run them while the halo is in flight,
+        # then the first w queries over [halo; local[:w]] (the ABI's halo convention)
+        O = torch.empty_like(Q)
+        O32 = torch.empty_strided(O.shape, O.stride(), dtype=torch.float32, device=O.device) \
+            if O.is_cuda else None
+        LSE = torch.empty(Q.shape[0], Q.shape[2], S, dtype=torch.float32, device=Q.device)
+        LSE[..., w:] = ops.fwd_into(Q[:, w:], K, V, U_loc, w, O[:, w:], None if O32 is None else O32[:, w:])
+    recv = ring.finish(handle)
     if recv is not None:
         if kv_ext is not None:
             Kx, Vx = kv_ext  # the w halo rows land in front of the resident local rows
@@ -166,7 +191,11 @@ def sp_forward_backward(Q, K, V, h, beta, dO, w: int, ops: Ops, ring: Ring, eps:
         h0 = w
     else:
         Kx, Vx, Ux, h0 = K, V, U_loc, 0
-    O, LSE, O32 = ops.fwd(Q, Kx, Vx, Ux, w)
+    if split:
+        LSE[..., :w] = ops.fwd_into(Q[:, :w], Kx[:, :2 * w], Vx[:, :2 * w], Ux[..., :2 * w].contiguous(), w,
+                                    O[:, :w], None if O32 is None else O32[:, :w])
+    else:
+        O, LSE, O32 = ops.fwd(Q, Kx, Vx, Ux, w)
     dQ, dKx, dVx, dUx = ops.bwd(Q, Kx, Vx, Ux, O, LSE, dO, w, O32)
     # backward halo r -> r-1: gradients of the halo rows
     back_like = [dKx[:, :w], dVx[:, :w], dUx[..., :w]]

@@ -38,7 +38,12 @@ def _oracle_ops():
         dh, db = oracle.gate_chain(h, beta, da, eps)
         return t(da), t(dh), t(db)
 
-    return Ops(gate_prefix=gate_prefix, fwd=fwd, bwd=bwd, gate_bwd=gate_bwd)
+    def fwd_into(Q, K, V, U, w, O_out, O32_out):
+        O, L = oracle.fwd(Q, K, V, U, w)
+        O_out.copy_(t(O))
+        return t(L)
+
+    return Ops(gate_prefix=gate_prefix, fwd=fwd, bwd=bwd, gate_bwd=gate_bwd, fwd_into=fwd_into)
 
 
 def _inputs(B, N, H, d, seed):
