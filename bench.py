@@ -281,7 +281,7 @@ def run_ours(args):
             aux["seq_sharded_C4"]["parallelism"] = seq["config"]["parallelism"]
     if rank != 0:
         return
-    cpu = cpu_baseline(args, s) if not args.no_cpu else None
+    cpu = cpu_baseline(args, s) if (not args.no_cpu and world == 1) else None  # rank 0 at N=1 only
     line = {
         "metric": METRIC,
         "value": round(value, 1),
