@@ -520,9 +520,12 @@ __global__ void __launch_bounds__(256) bwd_tc_pre_kernel(AttnParams p) {
 __global__ void __launch_bounds__(256) bwd_tc_pre_flat_kernel(const float* __restrict__ of,
                                                              const __nv_bfloat16* __restrict__ dO,
                                                              float* __restrict__ Dv, float* __restrict__ acc,
-                                                             uint32_t rows, uint32_t H, uint32_t Nq) {
+                                                             uint32_t rows, uint32_t H, uint32_t Nq,
+                                                             float* __restrict__ dU, uint32_t n_du) {
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    // dU accumulates red.adds in the main kernel: zero it here (no separate memset launch)
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_du; i += gridDim.x * blockDim.x) dU[i] = 0.f;
     for (uint32_t row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < rows; row += nw) {
         const float4 o = __ldcs(reinterpret_cast<const float4*>(of + (size_t)row * D) + lane);
         const uint2 g2 = __ldcs(reinterpret_cast<const uint2*>(dO + (size_t)row * D) + lane);
@@ -594,21 +597,23 @@ gfwa_status_t tc_bwd(const AttnParams& pin, cudaStream_t st, void* ws) {
     GFWA_REQUIRE(encode_bnhd_map_f32(&mdq, p.dQacc, p.B, p.Nq, p.H, D, acc_s, 16));
     const int64_t rows = p.B * p.Nq * p.H;
     const unsigned rgrid = (unsigned)((rows + 7) / 8);
-    if (gfwa_status_t s = check_launch(cudaMemsetAsync(p.dU, 0, (size_t)p.B * p.H * p.Nkv * sizeof(float), st)))
-        return s;
     static int n_sm = 0;
     if (n_sm == 0) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
     }
+    const int64_t n_du = p.B * p.H * p.Nkv;
     const bool o_flat = p.Ofp && p.os[2] == D && p.os[1] == p.H * D && p.os[0] == p.Nq * p.H * D &&
-                        rows < ((int64_t)1 << 31);
-    if (o_flat)
+                        rows < ((int64_t)1 << 31) && n_du < ((int64_t)1 << 31);
+    if (o_flat) {
         bwd_tc_pre_flat_kernel<<<(unsigned)min64((rows + 7) / 8, (int64_t)n_sm * 16), 256, 0, st>>>(
-            p.Ofp, (const __nv_bfloat16*)p.dO, p.Dv, p.dQacc, (uint32_t)rows, (uint32_t)p.H, (uint32_t)p.Nq);
-    else
+            p.Ofp, (const __nv_bfloat16*)p.dO, p.Dv, p.dQacc, (uint32_t)rows, (uint32_t)p.H, (uint32_t)p.Nq, p.dU,
+            (uint32_t)n_du);
+    } else {
+        if (gfwa_status_t s = check_launch(cudaMemsetAsync(p.dU, 0, (size_t)n_du * sizeof(float), st))) return s;
         bwd_tc_pre_kernel<<<rgrid, 256, 0, st>>>(p);
+    }
     note_launch();
     if (gfwa_status_t s = check_launch()) return s;
     TcBwdParams tp;
