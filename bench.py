@@ -175,7 +175,7 @@ def run_ours(args):
         U = gb.gfwa_gate_prefix(h, beta)
         if timed_kernels:
             e[1].record(st)
-        O, LSE, O32 = gb.gfwa_fwd(Q, K, V, U, s.w, want_o_f32=True)
+        O, LSE, O32 = gb.gfwa_fwd(Q, K, V, U, s.w, want_o_f32=True, prepare_bwd=True)
         if timed_kernels:
             e[2].record(st)
         dQ, dK, dV, dU, _ = gb.gfwa_bwd(Q, K, V, U, O, LSE, dO, s.w, O_f32=O32, want_dalpha=False)
@@ -444,7 +444,7 @@ def run_e2e(args, s, Q, K, V, dO, h, beta, step_fn, dev, world, dist):
     def compute(bufs):
         Qd, Kd, Vd, dOd, hd, bd = bufs
         U = gb.gfwa_gate_prefix(hd, bd)
-        O, LSE, O32 = gb.gfwa_fwd(Qd, Kd, Vd, U, s.w, want_o_f32=True)
+        O, LSE, O32 = gb.gfwa_fwd(Qd, Kd, Vd, U, s.w, want_o_f32=True, prepare_bwd=True)
         dQ, dK, dV, dU, _ = gb.gfwa_bwd(Qd, Kd, Vd, U, O, LSE, dOd, s.w, O_f32=O32, want_dalpha=False)
         _, dh, dbeta = gb.gfwa_gate_prefix_bwd(dU, hd, bd, want_dalpha=False)
         return (O, dQ, dK, dV, dh, dbeta)

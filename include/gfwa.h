@@ -172,6 +172,20 @@ gfwa_status_t gfwa_fwd(const gfwa_attn_desc_t* desc, const void* Q, const void* 
  * dalpha_carry [B*H] fp64 or NULL.
  * ws >= gfwa_bwd_workspace_size(desc); need not be initialised.
  */
+/*
+ * gfwa_fwd_train -- gfwa_fwd for a training step whose backward will run on
+ * bwd_ws (>= gfwa_bwd_workspace_size(desc) bytes, 256-byte aligned): on the
+ * tensor-core path the forward's epilogue also zeroes the backward's fp32 dQ
+ * accumulator inside bwd_ws and marks bwd_ws, so the next gfwa_bwd on it (same
+ * desc) skips that zeroing pass (268 MB at BASELINE configs[1]).  bwd_ws must
+ * not be modified in between; the backward consumes the mark, so a later
+ * gfwa_bwd without a new gfwa_fwd_train zeroes as usual.  Other paths: exactly
+ * gfwa_fwd.  Errors as gfwa_fwd, plus WORKSPACE.
+ */
+gfwa_status_t gfwa_fwd_train(const gfwa_attn_desc_t* desc, const void* Q, const void* K, const void* V,
+                             const float* U, void* O, float* O_f32, float* LSE, void* bwd_ws,
+                             size_t bwd_ws_bytes, gfwa_stream_t stream);
+
 size_t gfwa_bwd_workspace_size(const gfwa_attn_desc_t* desc);
 gfwa_status_t gfwa_bwd(const gfwa_attn_desc_t* desc, const void* Q, const void* K, const void* V,
                        const float* U, const void* O, const float* O_f32, const float* LSE,

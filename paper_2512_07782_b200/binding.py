@@ -78,6 +78,7 @@ EXPORTED = (
     "gfwa_gate_prefix_bwd",
     "gfwa_gate_prefix_bwd_workspace_size",
     "gfwa_fwd",
+    "gfwa_fwd_train",
     "gfwa_bwd",
     "gfwa_bwd_workspace_size",
     "gfwa_decode",
@@ -118,6 +119,8 @@ def load() -> ctypes.CDLL:
                                                  ctypes.c_float, _VP, _VP, sz, _VP]
         lib.gfwa_fwd.restype = ctypes.c_int
         lib.gfwa_fwd.argtypes = [ctypes.POINTER(AttnDesc), _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP]
+        lib.gfwa_fwd_train.restype = ctypes.c_int
+        lib.gfwa_fwd_train.argtypes = [ctypes.POINTER(AttnDesc), _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, sz, _VP]
         lib.gfwa_bwd_workspace_size.restype = sz
         lib.gfwa_bwd_workspace_size.argtypes = [ctypes.POINTER(AttnDesc)]
         lib.gfwa_bwd.restype = ctypes.c_int
@@ -280,10 +283,13 @@ def gfwa_gate_prefix_bwd(dU: torch.Tensor, h: torch.Tensor | None = None, beta: 
 # --------------------------------------------------------------------------- attention
 
 
-def gfwa_fwd(Q, K, V, U, w: int, scale: float | None = None, want_o_f32: bool = False, out=None, out_f32=None):
+def gfwa_fwd(Q, K, V, U, w: int, scale: float | None = None, want_o_f32: bool = False, out=None, out_f32=None,
+             prepare_bwd: bool = False):
     """O [B,Nq,H,d], LSE [B,H,Nq] (+ O_f32) per Eq. 12 / Alg. 2.
     out / out_f32: caller tensors (views allowed) receiving O and O_f32; O_f32
-    must share O's element strides (the ABI's one stride set)."""
+    must share O's element strides (the ABI's one stride set).
+    prepare_bwd: gfwa_fwd_train on the workspace gfwa_bwd will use (the forward
+    zeroes the backward's dQ accumulator; the next gfwa_bwd skips that pass)."""
     lib = load()
     _need_cuda(Q, K, V, U)
     U = U.contiguous()
@@ -297,6 +303,13 @@ def gfwa_fwd(Q, K, V, U, w: int, scale: float | None = None, want_o_f32: bool = 
         O_f32 = torch.empty_strided(O.shape, O.stride(), dtype=torch.float32, device=Q.device) if want_o_f32 else None
     LSE = torch.empty(B, H, Nq, dtype=torch.float32, device=Q.device)
     dsc = make_desc(Q, K, V, O, w, scale)
+    if prepare_bwd:
+        nbytes = lib.gfwa_bwd_workspace_size(ctypes.byref(dsc))
+        ws = workspace(nbytes, Q.device, "bwd")  # the tensor gfwa_bwd below takes
+        st = lib.gfwa_fwd_train(ctypes.byref(dsc), _ptr(Q), _ptr(K), _ptr(V), _ptr(U), _ptr(O), _ptr(O_f32),
+                                _ptr(LSE), _ptr(ws), nbytes, _stream(Q.device))
+        _check(st, "gfwa_fwd_train")
+        return O, LSE, O_f32
     st = lib.gfwa_fwd(ctypes.byref(dsc), _ptr(Q), _ptr(K), _ptr(V), _ptr(U), _ptr(O), _ptr(O_f32), _ptr(LSE),
                       _stream(Q.device))
     _check(st, "gfwa_fwd")

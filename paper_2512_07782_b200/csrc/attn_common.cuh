@@ -28,7 +28,18 @@ struct AttnParams {
     float* dU;          // [B,H,Nkv]
     float* Dv;          // [B,H,Nq] workspace: rowsum(O*dO)
     float* dQacc;       // fp32 dQ accumulator workspace (tensor-core path)
+    // gfwa_fwd_train: the forward zeroes the backward's dQ accumulator in its
+    // epilogue and marks the workspace (token) so the backward skips that pass
+    float* zero_acc;               // [B, Nq, H, d] fp32 region to zero (null: none)
+    unsigned long long* token;     // prepared-workspace token slot (device)
+    unsigned long long token_val;  // value identifying this problem's preparation
 };
+
+// token marking a backward workspace whose dQ accumulator the forward already zeroed
+inline unsigned long long prep_token(const AttnParams& p) {
+    return 0x4746574174726E21ull ^ ((unsigned long long)p.B << 48) ^ ((unsigned long long)p.H << 32) ^
+           ((unsigned long long)p.Nq << 8) ^ (unsigned long long)p.d;
+}
 
 __device__ __forceinline__ int64_t off3(const int64_t* s, int64_t b, int64_t n, int64_t h) {
     return b * s[0] + n * s[1] + h * s[2];

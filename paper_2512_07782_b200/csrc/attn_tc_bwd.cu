@@ -62,6 +62,7 @@ struct TcBwdParams {
     int w;
     float sl2, scale;
     long long* trace;  // diagnostics only (GFWA_TRACE_BWD): per-CTA clock64 stamps
+    unsigned long long* token;  // prepared-workspace token: consumed (cleared) by this kernel
 };
 
 #define GFWA_TR(slot)                                                                                         \
@@ -144,6 +145,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     const uint32_t tmem = *tmem_sh;
     const float uref = Ubh[j0];  // per-CTA bias reference (reading C-18)
+    // the pre kernel has read the token (stream order): clear it, so the next backward
+    // on this workspace zeroes its accumulator unless a new gfwa_fwd_train prepares it
+    if (p.token && threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) *p.token = 0ull;
     if (threadIdx.x == 0) GFWA_TR(0);
 
     if (warp == 13) {
@@ -512,7 +516,8 @@ __global__ void __launch_bounds__(256) bwd_tc_pre_kernel(AttnParams p) {
     }
     acc = warp_sum(acc);
     if (lane == 0) p.Dv[(b * p.H + h) * p.Nq + t] = acc;
-    *reinterpret_cast<float4*>(p.dQacc + ((b * p.Nq + t) * p.H + h) * D + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (!(p.token && *p.token == p.token_val))  // not already zeroed by gfwa_fwd_train
+        *reinterpret_cast<float4*>(p.dQacc + ((b * p.Nq + t) * p.H + h) * D + c) = make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
 // D = rowsum(O_f32 dO) and zeroing of dQacc, fast path for contiguous O_f32 / dO:
@@ -521,9 +526,13 @@ __global__ void __launch_bounds__(256) bwd_tc_pre_flat_kernel(const float* __res
                                                              const __nv_bfloat16* __restrict__ dO,
                                                              float* __restrict__ Dv, float* __restrict__ acc,
                                                              uint32_t rows, uint32_t H, uint32_t Nq,
-                                                             float* __restrict__ dU, uint32_t n_du) {
+                                                             float* __restrict__ dU, uint32_t n_du,
+                                                             const unsigned long long* __restrict__ token,
+                                                             unsigned long long token_val) {
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    // gfwa_fwd_train already zeroed the accumulator (its token is in the workspace)
+    const bool zero = !(token && *token == token_val);
     // dU accumulates red.adds in the main kernel: zero it here (no separate memset launch)
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_du; i += gridDim.x * blockDim.x) dU[i] = 0.f;
     for (uint32_t row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < rows; row += nw) {
@@ -537,7 +546,7 @@ __global__ void __launch_bounds__(256) bwd_tc_pre_flat_kernel(const float* __res
             const uint32_t hh = row % H, bt = row / H, t = bt % Nq, b = bt / Nq;
             Dv[((size_t)b * H + hh) * Nq + t] = a;
         }
-        reinterpret_cast<float4*>(acc + (size_t)row * D)[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (zero) reinterpret_cast<float4*>(acc + (size_t)row * D)[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
 }
 
@@ -609,7 +618,7 @@ gfwa_status_t tc_bwd(const AttnParams& pin, cudaStream_t st, void* ws) {
     if (o_flat) {
         bwd_tc_pre_flat_kernel<<<(unsigned)min64((rows + 7) / 8, (int64_t)n_sm * 16), 256, 0, st>>>(
             p.Ofp, (const __nv_bfloat16*)p.dO, p.Dv, p.dQacc, (uint32_t)rows, (uint32_t)p.H, (uint32_t)p.Nq, p.dU,
-            (uint32_t)n_du);
+            (uint32_t)n_du, p.token, p.token_val);
     } else {
         if (gfwa_status_t s = check_launch(cudaMemsetAsync(p.dU, 0, (size_t)n_du * sizeof(float), st))) return s;
         bwd_tc_pre_kernel<<<rgrid, 256, 0, st>>>(p);
@@ -629,6 +638,7 @@ gfwa_status_t tc_bwd(const AttnParams& pin, cudaStream_t st, void* ws) {
     tp.w = p.w;
     tp.sl2 = p.scale * kLog2e;
     tp.scale = p.scale;
+    tp.token = p.token;
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(bwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);

@@ -59,6 +59,9 @@ struct TcFwdParams {
     int64_t Nq, Nkv, h0, H;
     int w;
     int store_f32;
+    float* zero_acc;   // gfwa_fwd_train: the dQ accumulator [B, Nq, H, d] whose rows of this tile are zeroed
+    unsigned long long* token;
+    unsigned long long token_val;
     float sl2;         // scale * log2(e)
     long long* trace;  // diagnostics only (GFWA_TRACE_FWD): per-CTA clock64 stamps
 };
@@ -84,7 +87,8 @@ __device__ __forceinline__ uint32_t range_bits(int lo, int hi, int base) {
 }
 
 __global__ void __launch_bounds__(kThreads, 2)
-    fwd_tc_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
+    fwd_tc_kernel(const __grid_constant__ CUtensorMap mzq, const __grid_constant__ CUtensorMap mq,
+                  const __grid_constant__ CUtensorMap mk,
                   const __grid_constant__ CUtensorMap mv, const __grid_constant__ CUtensorMap mo,
                   const __grid_constant__ CUtensorMap mo32, const TcFwdParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -413,6 +417,23 @@ __global__ void __launch_bounds__(kThreads, 2)
             bulk_wait_read0();  // smem must stay valid until the bulk stores have read it
             GFWA_TR(33);
         }
+        if (p.zero_acc) {
+            // gfwa_fwd_train: zero this tile's 128 rows of the backward's fp32 dQ
+            // accumulator from a zeroed 16 KB smem box (the Q slot, idle now): four
+            // TMA stores of {32 d, 128 rows}
+            named_bar_sync(1, 128);  // the O stores have finished reading the Q slot
+            const uint32_t z = smem_u32(Qs) + r * 128;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) sts128(z + k * 16, make_uint4(0u, 0u, 0u, 0u));
+            fence_proxy_async();
+            named_bar_sync(1, 128);
+            if (r == 0) {
+                for (int c = 0; c < 4; ++c) tma_store_4d(&mzq, Qs, c * 32, (int)h, (int)r0, (int)b);
+                bulk_commit();
+                if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) *p.token = p.token_val;
+                bulk_wait_read0();
+            }
+        }
     }
     tc_fence_before();
     __syncthreads();
@@ -435,8 +456,14 @@ bool tc_fwd_supported(const AttnParams& p, gfwa_dtype_t dt) {
 }
 
 gfwa_status_t tc_fwd(const AttnParams& p, cudaStream_t st) {
-    CUtensorMap mq, mk, mv, mo, mo32;
+    CUtensorMap mq, mk, mv, mo, mo32, mzq;
     GFWA_REQUIRE(encode_bnhd_map(&mq, p.Q, p.B, p.Nq, p.H, D, p.qs, BM));
+    if (p.zero_acc) {
+        const int64_t acc_s[3] = {p.Nq * p.H * D, p.H * D, D};  // the backward's dQ accumulator layout
+        GFWA_REQUIRE(encode_bnhd_map_f32(&mzq, p.zero_acc, p.B, p.Nq, p.H, D, acc_s, BM));
+    } else {
+        mzq = mq;  // unused
+    }
     GFWA_REQUIRE(encode_bnhd_map(&mk, p.K, p.B, p.Nkv, p.H, D, p.ks, BN));
     GFWA_REQUIRE(encode_bnhd_map(&mv, p.V, p.B, p.Nkv, p.H, D, p.vs, BN));
     GFWA_REQUIRE(encode_bnhd_map(&mo, p.O, p.B, p.Nq, p.H, D, p.os, BM));
@@ -453,6 +480,9 @@ gfwa_status_t tc_fwd(const AttnParams& p, cudaStream_t st) {
     tp.H = p.H;
     tp.w = p.w;
     tp.store_f32 = p.O_f32 != nullptr;
+    tp.zero_acc = p.zero_acc;
+    tp.token = p.token;
+    tp.token_val = p.token_val;
     tp.sl2 = p.scale * kLog2e;
     static bool attr_set = false;
     if (!attr_set) {
@@ -468,7 +498,7 @@ gfwa_status_t tc_fwd(const AttnParams& p, cudaStream_t st) {
         cudaMalloc(&tp.trace, n_cta * 64 * sizeof(long long));
         cudaMemsetAsync(tp.trace, 0, n_cta * 64 * sizeof(long long), st);
     }
-    fwd_tc_kernel<<<grid, kThreads, kSmemBytes, st>>>(mq, mk, mv, mo, mo32, tp);
+    fwd_tc_kernel<<<grid, kThreads, kSmemBytes, st>>>(mzq, mq, mk, mv, mo, mo32, tp);
     note_launch();
     if (trace_file) {
         std::vector<long long> hbuf(n_cta * 64);

@@ -43,6 +43,14 @@ bool packed_kv(const int64_t* st, const AttnParams& p) {
 }
 bool check_finite_env();
 
+// gfwa_fwd_train hands its preparation to the shared gfwa_fwd body (per thread)
+struct Prepare {
+    float* zero_acc = nullptr;
+    unsigned long long* token = nullptr;
+    unsigned long long token_val = 0;
+};
+thread_local Prepare g_prepare;
+
 bool device_is_sm100() {
     static int cached = -1;
     if (cached < 0) {
@@ -120,6 +128,9 @@ extern "C" gfwa_status_t gfwa_fwd(const gfwa_attn_desc_t* desc, const void* Q, c
     p.O = O;
     p.O_f32 = O_f32;
     p.LSE = LSE;
+    p.zero_acc = g_prepare.zero_acc;
+    p.token = g_prepare.token;
+    p.token_val = g_prepare.token_val;
     cudaStream_t st = (cudaStream_t)stream;
     gfwa_status_t s = tc_fwd_supported(p, desc->dtype) ? tc_fwd(p, st) : simt_fwd(p, desc->dtype, st);
     if (s != GFWA_OK || !check_finite_env()) return s;
@@ -129,16 +140,49 @@ extern "C" gfwa_status_t gfwa_fwd(const gfwa_attn_desc_t* desc, const void* Q, c
     return s;
 }
 
+// [D | dalpha scan | dQ accumulator | token]; the token slot marks a workspace
+// whose accumulator gfwa_fwd_train already zeroed (tensor-core path only)
+extern "C" gfwa_status_t gfwa_fwd_train(const gfwa_attn_desc_t* desc, const void* Q, const void* K,
+                                        const void* V, const float* U, void* O, float* O_f32, float* LSE,
+                                        void* bwd_ws, size_t bwd_ws_bytes, gfwa_stream_t stream);
+
 static size_t bwd_ws_layout(const AttnParams& p, gfwa_dtype_t dt, size_t* off_D, size_t* off_scan,
-                            size_t* off_tc) {
+                            size_t* off_tc, size_t* off_tok = nullptr) {
     size_t off = 0;
     *off_D = off;
     off += ((size_t)p.B * p.H * p.Nq * sizeof(float) + 255) & ~(size_t)255;
     *off_scan = off;
     off += gfwa_gate_prefix_bwd_workspace_size(p.B * p.H, p.Nkv, 1);  // the dalpha scan below
     *off_tc = off;
-    if (tc_bwd_supported(p, dt)) off += (tc_bwd_workspace(p) + 255) & ~(size_t)255;
+    if (off_tok) *off_tok = 0;
+    if (tc_bwd_supported(p, dt)) {
+        off += (tc_bwd_workspace(p) + 255) & ~(size_t)255;
+        if (off_tok) *off_tok = off;
+        off += 256;
+    }
     return off;
+}
+
+// gfwa_fwd plus the preparation of the backward's workspace: on the tensor-core
+// path the forward's epilogue zeroes the dQ accumulator (the writes overlap the
+// compute-bound forward) and sets the token, so gfwa_bwd skips its zeroing pass.
+extern "C" gfwa_status_t gfwa_fwd_train(const gfwa_attn_desc_t* desc, const void* Q, const void* K,
+                                        const void* V, const float* U, void* O, float* O_f32, float* LSE,
+                                        void* bwd_ws, size_t bwd_ws_bytes, gfwa_stream_t stream) {
+    AttnParams p;
+    if (gfwa_status_t s = make_params(desc, p)) return s;
+    if (!bwd_ws || (uintptr_t)bwd_ws % 256) return GFWA_ERR_INVALID_ARGUMENT;
+    size_t off_D, off_scan, off_tc, off_tok;
+    const size_t need = bwd_ws_layout(p, desc->dtype, &off_D, &off_scan, &off_tc, &off_tok);
+    if (bwd_ws_bytes < need) return GFWA_ERR_WORKSPACE;
+    if (!off_tok || !tc_fwd_supported(p, desc->dtype))  // no accumulator to prepare: plain forward
+        return gfwa_fwd(desc, Q, K, V, U, O, O_f32, LSE, stream);
+    g_prepare.zero_acc = (float*)((char*)bwd_ws + off_tc);
+    g_prepare.token = (unsigned long long*)((char*)bwd_ws + off_tok);
+    g_prepare.token_val = prep_token(p);
+    const gfwa_status_t s = gfwa_fwd(desc, Q, K, V, U, O, O_f32, LSE, stream);
+    g_prepare = Prepare{};
+    return s;
 }
 
 extern "C" size_t gfwa_bwd_workspace_size(const gfwa_attn_desc_t* desc) {
@@ -163,9 +207,11 @@ extern "C" gfwa_status_t gfwa_bwd(const gfwa_attn_desc_t* desc, const void* Q, c
     const void* ptrs[] = {Q, K, V, dO, dQ, dK, dV};
     for (const void* pp : ptrs) GFWA_REQUIRE(al16(pp));
     GFWA_REQUIRE((uintptr_t)ws % 256 == 0);
-    size_t off_D, off_scan, off_tc;
-    const size_t need = bwd_ws_layout(p, desc->dtype, &off_D, &off_scan, &off_tc);
+    size_t off_D, off_scan, off_tc, off_tok;
+    const size_t need = bwd_ws_layout(p, desc->dtype, &off_D, &off_scan, &off_tc, &off_tok);
     if (ws_bytes < need) return GFWA_ERR_WORKSPACE;
+    p.token = off_tok ? (unsigned long long*)((char*)ws + off_tok) : nullptr;
+    p.token_val = prep_token(p);
     bind_context(Q);
     p.Q = Q;
     p.K = K;

@@ -200,3 +200,25 @@ def test_c4_rank_shard_full_size_sampled():
     S = c["N"] // 8
     s = synth.AttnShape(B=c["B"], H=c["H"], N=S, d=c["d"], w=c["w"], N_kv=S + c["w"])
     _sampled_full_size(s, c["seed"], 64, [(0, 5)])
+
+
+def test_fwd_train_prepares_the_backward_workspace():
+    """gfwa_fwd_train zeroes the backward's dQ accumulator in the forward's
+    epilogue and marks the workspace; the backward consumes the mark.  The
+    gradients must equal the plain path's, also for a second backward on the
+    same (now dirty, unmarked) workspace without a new preparation."""
+    s = synth.AttnShape(B=2, H=3, N=700, d=128, w=200)
+    Q, K, V, dO = synth.attn_inputs(s, seed=31, device="cuda", dtype=torch.bfloat16)
+    h, beta = synth.gate_inputs(s.B, s.N, s.H, seed=32, device="cuda")
+    U = gb.gfwa_gate_prefix(h, beta)
+    O, LSE, O32 = gb.gfwa_fwd(Q, K, V, U, s.w, want_o_f32=True)
+    ref = gb.gfwa_bwd(Q, K, V, U, O, LSE, dO, s.w, O_f32=O32)
+    O2, LSE2, O322 = gb.gfwa_fwd(Q, K, V, U, s.w, want_o_f32=True, prepare_bwd=True)
+    assert torch.equal(O, O2) and torch.equal(LSE, LSE2) and torch.equal(O32, O322)
+    got = gb.gfwa_bwd(Q, K, V, U, O2, LSE2, dO, s.w, O_f32=O322)
+    again = gb.gfwa_bwd(Q, K, V, U, O2, LSE2, dO, s.w, O_f32=O322)  # mark consumed: zeroes itself
+    torch.cuda.synchronize()
+    for a, b, c in zip(ref[:4], got[:4], again[:4]):
+        tol = 1e-2 * max(1.0, a.float().abs().max().item())  # fp32 reduce order only (bf16 outputs)
+        assert (a.float() - b.float()).abs().max().item() <= tol
+        assert (a.float() - c.float()).abs().max().item() <= tol
