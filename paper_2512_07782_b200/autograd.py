@@ -19,7 +19,8 @@ class GatedFWAFunction(torch.autograd.Function):
     @staticmethod
     def forward(ctx, Q, K, V, h, beta, w: int, eps: float, scale):
         U = B.gfwa_gate_prefix(h, beta, eps)
-        O, LSE, O_f32 = B.gfwa_fwd(Q, K, V, U, w, scale, want_o_f32=True)
+        # a backward will follow: let the forward zero its dQ accumulator (gfwa_fwd_train)
+        O, LSE, O_f32 = B.gfwa_fwd(Q, K, V, U, w, scale, want_o_f32=True, prepare_bwd=any(ctx.needs_input_grad))
         ctx.save_for_backward(Q, K, V, h, beta, U, O, LSE, O_f32)
         ctx.w, ctx.eps, ctx.scale = w, eps, scale
         return O
