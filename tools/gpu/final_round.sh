@@ -10,7 +10,7 @@ python bench.py --workload C3_w128 --no-cpu --no-aux > $O/bench_c3_128.log 2>&1
 python bench.py --workload C4 --steps 3 --warmup 3 > $O/bench_c4_p1.log 2>&1
 python bench.py --impl reference --steps 2 --warmup 3 > $O/bench_ref.log 2>&1
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
-    --log-file $O/launches_bench.csv python bench.py --steps 2 --warmup 1 --no-cpu > /dev/null 2>&1
+    --log-file $O/launches_bench.csv python bench.py --steps 2 --warmup 1 --no-cpu --no-aux > /dev/null 2>&1
 ncu --set full --import-source on --clock-control none -k regex:gate_prefix_kernel -c 1 -o $O/gate_fwd python profiles/prof_gate.py > /dev/null 2>&1
 ncu --set full --import-source on --clock-control none -k regex:gate_prefix_bwd -c 1 -o $O/gate_bwd python profiles/prof_gate.py > /dev/null 2>&1
 ncu --set full --import-source on --clock-control none -k regex:decode_kernel -c 1 -o $O/decode_gqa python profiles/prof_decode_gqa.py > /dev/null 2>&1
