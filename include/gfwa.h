@@ -175,8 +175,9 @@ gfwa_status_t gfwa_fwd(const gfwa_attn_desc_t* desc, const void* Q, const void* 
 /*
  * gfwa_fwd_train -- gfwa_fwd for a training step whose backward will run on
  * bwd_ws (>= gfwa_bwd_workspace_size(desc) bytes, 256-byte aligned): on the
- * tensor-core path the forward's epilogue also zeroes the backward's fp32 dQ
- * accumulator inside bwd_ws and marks bwd_ws, so the next gfwa_bwd on it (same
+ * tensor-core path the forward (its TMA producer warp, once its loads are
+ * issued) also zeroes the backward's fp32 dQ accumulator inside bwd_ws and
+ * marks bwd_ws, so the next gfwa_bwd on it (same
  * desc) skips that zeroing pass (268 MB at BASELINE configs[1]).  bwd_ws must
  * not be modified in between; the backward consumes the mark, so a later
  * gfwa_bwd without a new gfwa_fwd_train zeroes as usual.  Other paths: exactly

@@ -46,6 +46,7 @@ constexpr int BM = 128;          // query rows per tile
 constexpr int BN = 128;          // keys per tile
 constexpr int D = 128;           // head dim
 constexpr uint32_t kTileBytes = BM * D * 2;  // 32 KB bf16 tile
+constexpr uint32_t kZeroBytes = 64 * 32 * 4;   // 8 KB: one {32 d, 64 rows} fp32 box of zeros
 constexpr int kThreads = 256;    // softmax warpgroup + (MMA, TMA, 2 idle)
 constexpr int kMmaWarp = 4, kTmaWarp = 5;
 constexpr int kSoftmaxRegs = 224;  // CTA pool at (256, 2): 256 x 128; 128 x 224 + 128 x 32 fits it
@@ -97,7 +98,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     uint8_t* Ks = Qs + kTileBytes;
     uint8_t* Vs = Ks + kTileBytes;
     __shared__ __align__(16) float s_nbk[BN];  // negated key bias -(u_k - uref) log2e
-    Bars* bars = (Bars*)(Vs + kTileBytes);
+    uint8_t* Zs = Vs + kTileBytes;  // 8 KB of zeros (gfwa_fwd_train)
+    Bars* bars = (Bars*)(Zs + kZeroBytes);
     uint32_t* tmem_sh = (uint32_t*)(bars + 1);
 
     const int warp = threadIdx.x >> 5;
@@ -164,6 +166,25 @@ __global__ void __launch_bounds__(kThreads, 2)
                     tma_load_4d_hint(Vs + half * (kTileBytes / 2), &mv, &bars->v_full, half * 64, (int)h,
                                      (int)(j * BN), (int)b, pol_kv);
             }
+        }
+        __syncwarp();
+        if (p.zero_acc) {
+            // gfwa_fwd_train: this idle warp zeroes the tile's 128 rows of the backward's
+            // fp32 dQ accumulator with TMA stores of an 8 KB zero box, while the
+            // other warps finish the tile (the writes overlap the compute)
+            const uint32_t zb = smem_u32(Zs) + (threadIdx.x & 31) * 256;
+#pragma unroll
+            for (int k2 = 0; k2 < 16; ++k2) sts128(zb + k2 * 16, make_uint4(0u, 0u, 0u, 0u));
+            fence_proxy_async();
+            __syncwarp();
+            if ((threadIdx.x & 31) == 0) {
+                for (int rh = 0; rh < 2; ++rh)
+                    for (int c = 0; c < 4; ++c) tma_store_4d(&mzq, Zs, c * 32, (int)h, (int)(r0 + 64 * rh), (int)b);
+                bulk_commit();
+                if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) *p.token = p.token_val;
+                bulk_wait_read0();  // the zero box stays valid until read
+            }
+            __syncwarp();
         }
     } else if (warp == kMmaWarp) {
         // ------------------------------------------------ MMA issuer
@@ -417,23 +438,6 @@ __global__ void __launch_bounds__(kThreads, 2)
             bulk_wait_read0();  // smem must stay valid until the bulk stores have read it
             GFWA_TR(33);
         }
-        if (p.zero_acc) {
-            // gfwa_fwd_train: zero this tile's 128 rows of the backward's fp32 dQ
-            // accumulator from a zeroed 16 KB smem box (the Q slot, idle now): four
-            // TMA stores of {32 d, 128 rows}
-            named_bar_sync(1, 128);  // the O stores have finished reading the Q slot
-            const uint32_t z = smem_u32(Qs) + r * 128;
-#pragma unroll
-            for (int k = 0; k < 8; ++k) sts128(z + k * 16, make_uint4(0u, 0u, 0u, 0u));
-            fence_proxy_async();
-            named_bar_sync(1, 128);
-            if (r == 0) {
-                for (int c = 0; c < 4; ++c) tma_store_4d(&mzq, Qs, c * 32, (int)h, (int)r0, (int)b);
-                bulk_commit();
-                if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) *p.token = p.token_val;
-                bulk_wait_read0();
-            }
-        }
     }
     tc_fence_before();
     __syncthreads();
@@ -444,7 +448,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 }
 
 // dynamic smem: 1024 alignment slack + Q, K, V + barriers (2 CTAs per SM)
-constexpr size_t kSmemBytes = 1024 + 3 * kTileBytes + sizeof(Bars) + 16;
+constexpr size_t kSmemBytes = 1024 + 3 * kTileBytes + kZeroBytes + sizeof(Bars) + 16;
 
 }  // namespace
 
@@ -460,7 +464,7 @@ gfwa_status_t tc_fwd(const AttnParams& p, cudaStream_t st) {
     GFWA_REQUIRE(encode_bnhd_map(&mq, p.Q, p.B, p.Nq, p.H, D, p.qs, BM));
     if (p.zero_acc) {
         const int64_t acc_s[3] = {p.Nq * p.H * D, p.H * D, D};  // the backward's dQ accumulator layout
-        GFWA_REQUIRE(encode_bnhd_map_f32(&mzq, p.zero_acc, p.B, p.Nq, p.H, D, acc_s, BM));
+        GFWA_REQUIRE(encode_bnhd_map_f32(&mzq, p.zero_acc, p.B, p.Nq, p.H, D, acc_s, 64));
     } else {
         mzq = mq;  // unused
     }
