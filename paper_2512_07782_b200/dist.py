@@ -48,7 +48,9 @@ def cuda_ops() -> Ops:
     from . import binding as gb
 
     def _fwd(Q, K, V, U, w):
-        return gb.gfwa_fwd(Q, K, V, U, w, want_o_f32=True)
+        # the step's backward follows on the same problem: gfwa_fwd_train zeroes its
+        # dQ accumulator inside the forward (the token keeps other orders safe)
+        return gb.gfwa_fwd(Q, K, V, U, w, want_o_f32=True, prepare_bwd=True)
 
     def _bwd(Q, K, V, U, O, LSE, dO, w, O32):
         dQ, dK, dV, dU, _ = gb.gfwa_bwd(Q, K, V, U, O, LSE, dO, w, O_f32=O32, want_dalpha=False)
