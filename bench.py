@@ -147,25 +147,9 @@ def in_window_fraction(N: int, w: int) -> float:
     return sum(min(t + 1, w) for t in range(N)) / (N * w)
 
 
-def run_ours(args):
+def _step_fns(gb, s, Q, K, V, dO, h, beta, st, stage_events=None):
+    """One training step of the hot path (rows A2-A6) through the C ABI."""
     import torch
-
-    import synth
-    from paper_2512_07782_b200 import binding as gb
-
-    dist, rank, world, local = _dist()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    peaks = _peaks()
-    c = synth.CONFIGS[args.workload]
-    s = synth.AttnShape(B=c["B"], H=c["H"], N=c["N"], d=c["d"], w=c["w"])
-    seed = c["seed"] + 1000 * rank
-    Q, K, V, dO = synth.attn_inputs(s, seed=seed, device=dev, dtype=torch.bfloat16)
-    h, beta = synth.gate_inputs(s.B, s.N, s.H, seed=seed, device=dev)
-    h, beta = h.bfloat16(), beta.bfloat16()
-    st = torch.cuda.current_stream(dev)
-
-    ev = {}
 
     def step(timed_kernels: bool = False):
         rec = []
@@ -178,29 +162,51 @@ def run_ours(args):
         O, LSE, O32 = gb.gfwa_fwd(Q, K, V, U, s.w, want_o_f32=True, prepare_bwd=True)
         if timed_kernels:
             e[2].record(st)
+            sev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            for x in sev:  # create the CUDA events (torch creates them lazily)
+                x.record(st)
+            gb.debug_stage_events(sev)  # after the bwd preprocess kernel / after its main kernel
         dQ, dK, dV, dU, _ = gb.gfwa_bwd(Q, K, V, U, O, LSE, dO, s.w, O_f32=O32, want_dalpha=False)
         if timed_kernels:
             e[3].record(st)
         _, dh, dbeta = gb.gfwa_gate_prefix_bwd(dU, h, beta, want_dalpha=False)
         if timed_kernels:
             e[4].record(st)
-            rec.append(e)
+            rec.append((e, sev))
         return rec, (O, dQ, dK, dV, dh, dbeta)
 
-    clk = ClockSampler(local).start()
-    time.sleep(0.3)  # nvidia-smi needs a moment before its first sample
-    for _ in range(args.warmup):
+    return step
+
+
+def measure_dense(workload, steps, warmup, dist, rank, world, local, dev, peaks, no_graph=False, clk=None):
+    """One workload's training step (C2 / C3_*), every rank its own batch (batch x
+    head sharding: no collective on the data path).  CUDA graph replay timed with
+    events, max over ranks; then eager steps with events between the calls for the
+    per-call breakdown and the backward main kernel's own time (roofline)."""
+    import torch
+
+    import synth
+    from paper_2512_07782_b200 import binding as gb
+
+    c = synth.CONFIGS[workload]
+    s = synth.AttnShape(B=c["B"], H=c["H"], N=c["N"], d=c["d"], w=c["w"])
+    seed = c["seed"] + 1000 * rank
+    Q, K, V, dO = synth.attn_inputs(s, seed=seed, device=dev, dtype=torch.bfloat16)
+    h, beta = synth.gate_inputs(s.B, s.N, s.H, seed=seed, device=dev)
+    h, beta = h.bfloat16(), beta.bfloat16()
+    st = torch.cuda.current_stream(dev)
+    step = _step_fns(gb, s, Q, K, V, dO, h, beta, st)
+    for _ in range(warmup):
         step()
     torch.cuda.synchronize(dev)
     if dist:
         dist.barrier()
     # the step is captured once into a CUDA graph (every library call is
     # stream-ordered with no host sync, so it captures as is): the timed region
-    # replays it, so host launch overhead -- which dominates the small gate
-    # kernels -- stays out of the device timeline
+    # replays it, so host launch overhead stays out of the device timeline
     graph, graph_note = None, "off (--no-graph)"
     n_launch0 = gb.launch_count()
-    if not args.no_graph:
+    if not no_graph:
         try:
             graph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(graph):
@@ -222,7 +228,7 @@ def run_ours(args):
     n_launch0 = gb.launch_count()
     wall0 = time.time()
     t0.record(st)
-    for _ in range(args.steps):
+    for _ in range(steps):
         if graph is not None:
             graph.replay()
         else:
@@ -230,66 +236,119 @@ def run_ours(args):
             evs += r
     t1.record(st)
     torch.cuda.synchronize(dev)
-    clk.mark(wall0, time.time())
-    clk.stop()
-    launches = per_step_launches * args.steps if graph is not None else gb.launch_count() - n_launch0
-    ms = t0.elapsed_time(t1) / args.steps
+    if clk is not None:
+        clk.mark(wall0, time.time())
+    launches = per_step_launches * steps if graph is not None else gb.launch_count() - n_launch0
+    ms = t0.elapsed_time(t1) / steps
     ms = _max_over_ranks(dist, ms, dev)
     if graph is not None:  # per-call breakdown from eager steps (CUDA events between the calls)
         for _ in range(2):  # eager allocations cannot reuse the graph's pool: warm them first
             step()
         torch.cuda.synchronize(dev)
-        for _ in range(args.steps):
+        for _ in range(steps):
             r, _ = step(timed_kernels=True)
             evs += r
         torch.cuda.synchronize(dev)
-    parts = {"gate": 0.0, "fwd": 0.0, "bwd": 0.0, "gate_bwd": 0.0}
-    for e in evs:
+    parts = {"gate": 0.0, "fwd": 0.0, "bwd": 0.0, "gate_bwd": 0.0, "bwd_pre": 0.0, "bwd_main": 0.0,
+             "bwd_post": 0.0}
+    for e, sev in evs:
         parts["gate"] += e[0].elapsed_time(e[1])
         parts["fwd"] += e[1].elapsed_time(e[2])
         parts["bwd"] += e[2].elapsed_time(e[3])
         parts["gate_bwd"] += e[3].elapsed_time(e[4])
-    parts = {k: v / args.steps for k, v in parts.items()}
+        parts["bwd_pre"] += e[2].elapsed_time(sev[0])
+        parts["bwd_main"] += sev[0].elapsed_time(sev[1])
+        parts["bwd_post"] += sev[1].elapsed_time(e[3])
+    parts = {k: v / len(evs) for k, v in parts.items()}
     tokens = s.B * s.N * world
-    value = tokens / (ms * 1e-3)
     frac_iw = in_window_fraction(s.N, s.w)
     flops_fwd = 4.0 * s.N * s.w * s.d * s.B * s.H  # north_star in-window convention
     flops_bwd = 10.0 * s.N * s.w * s.d * s.B * s.H
     tflops = (flops_fwd + flops_bwd) * world / (ms * 1e-3) / 1e12
-    # dominant kernel roofline (attention call with the largest device time)
-    dom = "bwd" if parts["bwd"] >= parts["fwd"] else "fwd"
-    dom_flops = flops_bwd if dom == "bwd" else flops_fwd
-    achieved = dom_flops / (parts[dom] * 1e-3) / 1e12
     path = gb.gfwa_attn_path(Q, K, V, s.w)
-    traffic = _traffic_from_profiles(dom, args.workload)
-    roofline = {"kernel": f"gfwa_{dom} ({'tcgen05' if path == 1 else 'simt'})", "bound": "tensor",
-                "achieved": round(achieved, 2), "peak": peaks["bf16_sus"], "unit": "TFLOP/s",
-                "frac": round(achieved / peaks["bf16_sus"], 4), "traffic": traffic,
-                "peak_src": f"{peaks['src']} bf16 sustained (kernel timed inside a long step)",
-                "algorithmic": f"{'10' if dom == 'bwd' else '4'}*N*w*d*B*H = {dom_flops:.4g} FLOP/launch"}
+    # dominant kernel: the backward's main kernel (its own launch, timed by the
+    # stage events on the launching stream) against the BURST bf16 peak -- the
+    # step is ~1 ms, not a seconds-long sustained run
+    main_ms = parts["bwd_main"]
+    achieved = flops_bwd / (main_ms * 1e-3) / 1e12
+    roofline = {"kernel": "bwd_tc_kernel" if path == 1 else "bwd_simt", "bound": "tensor",
+                "achieved": round(achieved, 2), "peak": peaks["bf16"], "unit": "TFLOP/s",
+                "frac": round(achieved / peaks["bf16"], 4),
+                "frac_exact_in_window": round(achieved * frac_iw / peaks["bf16"], 4),
+                "traffic": _traffic_from_profiles("bwd_main", workload),
+                "kernel_ms": round(main_ms, 4),
+                "peak_src": f"{peaks['src']} bf16 burst (MEASURED_PEAKS.json bf16_tflops)",
+                "algorithmic": f"10*N*w*d*B*H = {flops_bwd:.4g} FLOP/launch (north_star in-window count)"}
+    fwd_ach = flops_fwd / (parts["fwd"] * 1e-3) / 1e12
+    return {
+        "s": s, "tensors": (Q, K, V, dO, h, beta), "ms": ms, "value": tokens / (ms * 1e-3),
+        "tflops": tflops, "pct": tflops / peaks["bf16"], "pct_exact": tflops * frac_iw / peaks["bf16"],
+        "frac_iw": frac_iw, "parts": parts, "path": path, "roofline": roofline, "launches": launches,
+        "graph_note": graph_note,
+        "fwd_kernel": {"kernel": "fwd_tc_kernel", "ms": round(parts["fwd"], 4), "achieved": round(fwd_ach, 2),
+                       "frac": round(fwd_ach / peaks["bf16"], 4),
+                       "frac_exact_in_window": round(fwd_ach * frac_iw / peaks["bf16"], 4)},
+    }
+
+
+def _dense_summary(r):
+    return {"ms_per_step": round(r["ms"], 4), "tokens_per_s": round(r["value"], 1),
+            "tflops_in_window": round(r["tflops"], 2), "pct_bf16_peak": round(r["pct"], 4),
+            "pct_bf16_peak_exact_in_window": round(r["pct_exact"], 4), "in_window_fraction": round(r["frac_iw"], 4),
+            "ms_breakdown": {k: round(v, 4) for k, v in r["parts"].items()},
+            "roofline": r["roofline"], "fwd_kernel": r["fwd_kernel"],
+            "config": {"B": r["s"].B, "H": r["s"].H, "N": r["s"].N, "d": r["s"].d, "w": r["s"].w}}
+
+
+def run_ours(args):
+    import torch
+
+    dist, rank, world, local = _dist()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1 and args.workload == "C2":
+        # N > 1: the north_star's sequence-sharded C4 step is the headline
+        # (strong scaling of one N = 131072 sequence); C2 batch-sharded in aux
+        return run_seq(args, aux_c2=not args.no_aux)
+    peaks = _peaks()
+    clk = ClockSampler(local).start()
+    time.sleep(0.3)  # nvidia-smi needs a moment before its first sample
+    r = measure_dense(args.workload, args.steps, args.warmup, dist, rank, world, local, dev, peaks,
+                      no_graph=args.no_graph, clk=clk)
+    clk.stop()
+    s = r["s"]
+    Q, K, V, dO, h, beta = r["tensors"]
     # e2e: the same step through the public API with pinned host buffers
     e2e = run_e2e(args, s, Q, K, V, dO, h, beta, step_fn=None, dev=dev, world=world, dist=dist)
+    del Q, K, V, dO, h, beta, r["tensors"]
+    torch.cuda.empty_cache()
     aux = {}
     if rank == 0 and not args.no_aux:
-        aux = run_aux(dev, peaks)
+        # the north_star target point (N=8192, w=512, d=128) and the rest of the C3
+        # window sweep (BASELINE configs[2]), each with its own kernel roofline
+        for wl in ("C3_w512", "C3_w128", "C3_w2048"):
+            if wl != args.workload:
+                aux[wl] = _dense_summary(measure_dense(wl, max(5, args.steps), 3, None, 0, 1, local, dev, peaks))
+                torch.cuda.empty_cache()
+        aux.update(run_aux(dev, peaks))
     if not args.no_aux and args.workload == "C2":
-        # the north_star's sequence-sharded C4 step on the same ranks (strong scaling
-        # of one N = 131072 sequence; a few steps, max over ranks)
+        # the sequence-sharded C4 step (P = 1 here: the baseline of the N > 1 lines)
         seq = measure_seq(3, 3, dist, rank, world, local, dev)
         if rank == 0:
             aux["seq_sharded_C4"] = {k: seq[k] for k in ("ms_per_step", "tokens_per_s", "tflops_in_window", "steps")}
             aux["seq_sharded_C4"]["parallelism"] = seq["config"]["parallelism"]
+            aux["seq_sharded_C4"]["pct_bf16_peak"] = round(seq["tflops_in_window"] / peaks["bf16"], 4)
     if rank != 0:
         return
     cpu = cpu_baseline(args, s) if (not args.no_cpu and world == 1) else None  # rank 0 at N=1 only
     line = {
         "metric": METRIC,
-        "value": round(value, 1),
+        "value": round(r["value"], 1),
         "unit": "tokens/s",
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": round(ms, 4),
+        "ms_per_step": round(r["ms"], 4),
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
@@ -299,15 +358,17 @@ def run_ours(args):
                    "B": s.B, "H": s.H, "N": s.N, "d": s.d, "w": s.w, "global_batch": s.B * world,
                    "seq_len": s.N, "parallelism": f"batch-sharded x{world}" if world > 1 else "single GPU",
                    "l2": "inputs larger than L2 (working set > 1 GB), no flush",
-                   "in_window_fraction": round(frac_iw, 4), "cuda_graph": graph_note},
-        "tflops_in_window": round(tflops, 2),
-        "pct_bf16_peak": round(tflops / peaks["bf16"], 4),
-        "ms_breakdown": {k: round(v, 4) for k, v in parts.items()},  # eager calls, events between them
-        "attn_path": "tcgen05" if path == 1 else "simt",
-        "roofline": roofline,
+                   "in_window_fraction": round(r["frac_iw"], 4), "cuda_graph": r["graph_note"]},
+        "tflops_in_window": round(r["tflops"], 2),
+        "pct_bf16_peak": round(r["pct"], 4),
+        "pct_bf16_peak_exact_in_window": round(r["pct_exact"], 4),
+        "ms_breakdown": {k: round(v, 4) for k, v in r["parts"].items()},  # eager calls, events between them
+        "attn_path": "tcgen05" if r["path"] == 1 else "simt",
+        "roofline": r["roofline"],
+        "fwd_kernel": r["fwd_kernel"],
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": launches,
+        "gpu_launches": r["launches"],
         "clocks": clk.summary(),
         "aux": aux,
     }
@@ -329,10 +390,11 @@ class _SoloRing:
         return None
 
 
-def run_seq(args):
-    """--workload C4: BASELINE configs[3] (B=1, H=32, N=131072, d=128, w=2048)
-    sequence-sharded over the ranks (S = N/P contiguous rows each, K/V/u halo
-    r -> r+1 and halo gradients r+1 -> r over NCCL P2P; strong scaling)."""
+def run_seq(args, aux_c2: bool = False):
+    """--workload C4 (and the N > 1 headline): BASELINE configs[3] (B=1, H=32,
+    N=131072, d=128, w=2048) sequence-sharded over the ranks (S = N/P contiguous
+    rows each, K/V/u halo r -> r+1 and halo gradients r+1 -> r over NCCL P2P,
+    gate totals through a cross-rank exclusive scan; strong scaling)."""
     import torch
 
     dist, rank, world, local = _dist()
@@ -340,6 +402,12 @@ def run_seq(args):
     dev = torch.device("cuda", local)
     peaks = _peaks()
     r = measure_seq(args.steps, args.warmup, dist, rank, world, local, dev, sample_clocks=True)
+    aux = {}
+    if aux_c2:  # BASELINE configs[1] batch-sharded over the same ranks (weak scaling)
+        c2 = measure_dense("C2", args.steps, args.warmup, dist, rank, world, local, dev, peaks)
+        aux["C2_batch_sharded"] = _dense_summary(c2)
+        aux["C2_batch_sharded"]["scaling"] = "weak"
+        aux["C2_batch_sharded"]["tokens_per_s_all_ranks"] = round(c2["value"], 1)
     if rank != 0:
         return
     print(json.dumps({
@@ -350,6 +418,7 @@ def run_seq(args):
         "config": r["config"],
         "tflops_in_window": r["tflops_in_window"], "pct_bf16_peak": round(r["tflops_in_window"] / peaks["bf16"], 4),
         "gpu_launches": r["gpu_launches"], "clocks": r.get("clocks"),
+        "e2e": r.get("e2e"), "aux": aux,
     }), flush=True)
 
 
@@ -509,7 +578,8 @@ def run_aux(dev, peaks):
     c = synth.CONFIGS["C5"]
     B, H, d, w = c["B"], c["H"], c["d"], c["w"]
     Kc, Vc, a_hist, q, k, v, a_new = synth.decode_inputs(B, H, d, w, seed=c["seed"], device=dev)
-    Uc = -torch.cumsum(a_hist, -1)
+    Uh = -torch.cumsum(a_hist, -1)
+    Uc = Uh - Uh[..., -1:]  # U_cache convention: u_tau - u_newest
     pos = torch.full((B,), w + 17, dtype=torch.int64, device=dev)
     for _ in range(3):
         gb.gfwa_decode(q, k, v, a_new, Kc, Vc, Uc, pos)
@@ -522,7 +592,7 @@ def run_aux(dev, peaks):
     e1.record()
     torch.cuda.synchronize(dev)
     ms = e0.elapsed_time(e1) / n
-    byts = B * H * (4 * w * d + 4 * w + 8 * d)  # bf16 K,V rows + fp32 u + q/k/v/o
+    byts = B * H * (4 * w * d + 8 * w + 8 * d)  # bf16 K,V rows + fp32 u read and rewritten + q/k/v/o
     out["decode_C5"] = {"ms_per_step": round(ms, 4), "tokens_per_s": round(B / (ms * 1e-3), 1),
                         "achieved_GBps": round(byts / (ms * 1e-3) / 1e9, 1),
                         "frac_hbm": round(byts / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"], 4),
@@ -532,7 +602,8 @@ def run_aux(dev, peaks):
     c = synth.CONFIGS["C5_gqa4"]
     B, H, Hk = c["B"], c["H"], c["H_kv"]
     Kc, Vc, a_hist, q, k, v, a_new = synth.decode_inputs(B, H, d, w, seed=c["seed"], device=dev, H_kv=Hk)
-    Uc = -torch.cumsum(a_hist, -1)
+    Uh = -torch.cumsum(a_hist, -1)
+    Uc = Uh - Uh[..., -1:]
     for _ in range(3):
         gb.gfwa_decode(q, k, v, a_new, Kc, Vc, Uc, pos)
     torch.cuda.synchronize(dev)
@@ -542,7 +613,7 @@ def run_aux(dev, peaks):
     e1.record()
     torch.cuda.synchronize(dev)
     ms = e0.elapsed_time(e1) / n
-    byts = B * Hk * 4 * w * d + B * H * (4 * w + 4 * d) + B * Hk * 4 * d  # K,V rows once per group; u, q, o per head
+    byts = B * Hk * 4 * w * d + B * H * (8 * w + 4 * d) + B * Hk * 4 * d  # K,V rows once per group; u (r+w), q, o per head
     out["decode_C5_gqa4"] = {"ms_per_step": round(ms, 4), "tokens_per_s": round(B / (ms * 1e-3), 1),
                              "achieved_GBps": round(byts / (ms * 1e-3) / 1e9, 1),
                              "frac_hbm": round(byts / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"], 4),
@@ -611,16 +682,17 @@ def run_aux(dev, peaks):
 # --------------------------------------------------------------------------- CPU oracle
 
 
-def _oracle_sample(s, n_slices: int, n_rows: int):
+def _oracle_sample(s, n_slices: int, n_rows: int, halo: int = 0):
     """A bounded sample of the workload for the fp64 oracle: `n_slices` (b,h)
-    slices, each the first `n_rows` tokens of one head (same recipe/seed)."""
+    slices, each `n_rows` query tokens of one head (same recipe/seed) after
+    `halo` key rows (halo = w - 1: every sampled query sees a full window)."""
     import torch
 
     import synth
 
-    sub = synth.AttnShape(B=n_slices, H=1, N=n_rows, d=s.d, w=s.w)
+    sub = synth.AttnShape(B=n_slices, H=1, N=n_rows, d=s.d, w=s.w, N_kv=n_rows + halo)
     Q, K, V, dO = synth.attn_inputs(sub, seed=4242, dtype=torch.bfloat16)
-    h, beta = synth.gate_inputs(n_slices, n_rows, 1, seed=4243)
+    h, beta = synth.gate_inputs(n_slices, n_rows + halo, 1, seed=4243)
     return sub, Q, K, V, dO, h.bfloat16(), beta.bfloat16()
 
 
@@ -669,11 +741,24 @@ def run_reference(args):
     # torchrun exports OMP_NUM_THREADS=1; the oracle runs on all of this host's cores
     oracle.set_num_threads(len(os.sched_getaffinity(0)))
 
-    c = synth.CONFIGS[args.workload]
+    # the config our arm reports: at N > 1 the default run's headline is the
+    # sequence-sharded C4 step (run_ours), so the reference times C4 too
+    wl = args.workload
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1 and wl == "C2":
+        wl = "C4"
+    c = synth.CONFIGS[wl]
     s = synth.AttnShape(B=c["B"], H=c["H"], N=c["N"], d=c["d"], w=c["w"])
     cores = oracle.num_threads()
-    n_rows = min(s.N, 512)
-    sub, *arrs = _oracle_sample(s, cores, n_rows)
+    if wl == "C4":
+        # C4 rows all see full 2048-key windows (but the first 2047 of 131072): each
+        # step takes `cores` slices of 1024 query rows after a w-1 key-row halo
+        n_rows, halo = 1024, s.w - 1
+        what = f"{n_rows} query rows after a {halo}-row key halo (full windows) of {wl}"
+    else:
+        # `cores` (b, h) slices over ALL N tokens of the workload (the full window mix)
+        n_rows, halo = s.N, 0
+        what = f"all {n_rows} tokens of {wl}"
+    sub, *arrs = _oracle_sample(s, cores, n_rows, halo)
     for _ in range(args.warmup):
         _oracle_step(sub, *arrs)
     t = time.perf_counter()
@@ -686,10 +771,10 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "tokens/s", "n_gpus": args.gpus,
         "device": "host CPU (fp64 oracle; rank 0 only)",
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (synth.py)",
-        "config": {"workload": args.workload, "B": s.B, "H": s.H, "N": s.N, "d": s.d, "w": s.w},
+        "scaling": "strong" if wl == "C4" else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (synth.py)",
+        "config": {"workload": wl, "B": s.B, "H": s.H, "N": s.N, "d": s.d, "w": s.w},
         "cpu_baseline": {"value": round(value, 3), "unit": "tokens/s", "cores": cores, "kind": "oracle",
-                         "sample": f"per step {cores} (b,h) slices x first {n_rows} tokens; tokens = head-rows/H"},
+                         "sample": f"per step {cores} (b,h) slices x {what}; tokens = head-rows/H"},
         "e2e": {"value": round(value, 3), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
@@ -706,6 +791,20 @@ def main():
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of a CUDA-graph replay")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    ws = os.environ.get("WORLD_SIZE")
+    if ws is None and args.gpus > 1:
+        # `bench.py --gpus N` outside torchrun: launch the N ranks ourselves (one
+        # process per GPU, the same command the driver uses)
+        import socket
+
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
+    if ws is not None and int(ws) != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}")
     if args.impl == "reference":
         run_reference(args)
     else:

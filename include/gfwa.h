@@ -155,7 +155,9 @@ typedef struct {
  * Q [B,N_q,H,d], K, V [B,N_kv,H,d], U [B,H,N_kv] fp32 -> O [B,N_q,H,d],
  * LSE [B,H,N_q] fp32.  O_f32 (nullable) [B,N_q,H,d] fp32 receives O before
  * the output cast; pass it to gfwa_bwd so D = rowsum(O*dO) is taken from fp32
- * O (reading C-12).  Key tiles outside every row's window are never read.
+ * O (reading C-12).  With O_f32 the bf16 tensor-core path forms the PV product
+ * with P and V in fp16 (reading C-23; |v| < 65504 required), without it in
+ * bf16.  Key tiles outside every row's window are never read.
  */
 gfwa_status_t gfwa_fwd(const gfwa_attn_desc_t* desc, const void* Q, const void* K, const void* V,
                        const float* U, void* O, float* O_f32, float* LSE, gfwa_stream_t stream);
@@ -177,11 +179,18 @@ gfwa_status_t gfwa_fwd(const gfwa_attn_desc_t* desc, const void* Q, const void* 
  * bwd_ws (>= gfwa_bwd_workspace_size(desc) bytes, 256-byte aligned): on the
  * tensor-core path the forward (its TMA producer warp, once its loads are
  * issued) also zeroes the backward's fp32 dQ accumulator inside bwd_ws and
- * marks bwd_ws, so the next gfwa_bwd on it (same
- * desc) skips that zeroing pass (268 MB at BASELINE configs[1]).  bwd_ws must
- * not be modified in between; the backward consumes the mark, so a later
- * gfwa_bwd without a new gfwa_fwd_train zeroes as usual.  Other paths: exactly
- * gfwa_fwd.  Errors as gfwa_fwd, plus WORKSPACE.
+ * marks bwd_ws (a token of the whole descriptor in its first 256 bytes), so
+ * the next gfwa_bwd on it with the same desc skips that zeroing pass (268 MB
+ * at BASELINE configs[1]).  Every gfwa_fwd_train overwrites the token and every
+ * tensor-core gfwa_bwd clears it, so only the latest prepared descriptor is
+ * honoured: a gfwa_bwd with another descriptor (or after an intervening
+ * backward) zeroes its own accumulator, and interleaving shapes on one
+ * workspace is safe.  When O_f32 is given, the PV product runs with P and V in
+ * fp16 (reading C-23: the fp32 O that D is taken from then carries 8x less
+ * P rounding than with bf16 P); V must then lie in the fp16 range
+ * (|v| < 65504; larger values overflow to inf).  Calls sharing a workspace
+ * must be ordered on one stream.  Other paths: exactly gfwa_fwd.  Errors as
+ * gfwa_fwd, plus WORKSPACE.
  */
 gfwa_status_t gfwa_fwd_train(const gfwa_attn_desc_t* desc, const void* Q, const void* K, const void* V,
                              const float* U, void* O, float* O_f32, float* LSE, void* bwd_ws,
@@ -212,11 +221,18 @@ typedef struct {
 
 /*
  * gfwa_decode -- for every (b, hh), with t = pos[b] (tokens already cached
- * before this one) and slot s = t mod w:
- *   u_t = u_{t-1} - alpha_t, u_{t-1} = U_cache[b,hh,(t-1) mod w] (0 when t == 0)
- *   K_cache[b,kv(hh),s] = k_new, V_cache[b,kv(hh),s] = v_new, U_cache[b,hh,s] = u_t
+ * before this one) and slot s = t mod w.  U_cache holds gate sums RELATIVE
+ * to the newest cached token: U_cache[b,hh,slot(tau)] = u_tau - u_{t-1} >= 0
+ * for each cached token tau (so the newest token's slot holds 0; build it from
+ * a prefill's U as U[tau] - U[t-1]).  With u_t = u_{t-1} - alpha_t (Eq. 11):
  *   o[b,hh] = sum_i softmax_i(scale q.k_i + u_t - u_i) v_i over the
- *             min(t+1, w) valid slots (ring order is irrelevant)
+ *             min(t+1, w) valid slots (ring order is irrelevant), where
+ *             u_t - u_i = -(U_cache[i] + alpha_t) and 0 for the new token
+ *   K_cache[b,kv(hh),s] = k_new, V_cache[b,kv(hh),s] = v_new, and every valid
+ *   U_cache entry becomes relative to u_t (U_cache[i] + alpha_t; slot s: 0).
+ * The relative frame keeps the stored values bounded by the window's gate sum
+ * at any position, so fp32 storage never swallows small gates (an absolute
+ * running u loses them once its ulp exceeds alpha).
  * GQA (heads_per_gqa_group): query head hh reads
  * K/V head hh / (H / H_kv); the gate and U stay per query head.
  * q, o [B,H,d]; k_new, v_new [B,H_kv,d]; K_cache, V_cache [B,H_kv,w,d];
@@ -250,6 +266,12 @@ const char* gfwa_version(void);
 /* Number of kernel launches the calling thread has issued through this library
  * (monotonic; bench.py reads it to report gpu_launches). */
 uint64_t gfwa_launch_count(void);
+/* Measurement hook (bench.py's per-kernel roofline): registers up to 4 CUDA
+ * events (cudaEvent_t handles, NULL entries allowed) for the calling thread's
+ * NEXT tensor-core gfwa_bwd, which records events[0] after its preprocess
+ * kernel and events[1] after its main kernel on the call's stream, then
+ * forgets them.  Never synchronises; no effect on results. */
+void gfwa_debug_stage_events(void* const* events, int n);
 /* Which forward/backward implementation a descriptor routes to:
  * 0 = SIMT (fp32 parity path), 1 = tcgen05/TMA tensor-core path. */
 int gfwa_attn_path(const gfwa_attn_desc_t* desc);
@@ -260,6 +282,10 @@ int gfwa_attn_path(const gfwa_attn_desc_t* desc);
  * bf16 row-major device arrays; S_out, O_out: [128,128] fp32 device arrays. */
 gfwa_status_t gfwa_debug_tc_selftest(const void* Q, const void* K, const void* V, float* S_out, float* O_out,
                                      gfwa_stream_t stream);
+/* As above; flags bit 0: P is written to TMEM as fp16 and the TS MMA reads it
+ * with A format F16 against the bf16 V (mixed-format kind::f16 probe). */
+gfwa_status_t gfwa_debug_tc_selftest_ex(const void* Q, const void* K, const void* V, float* S_out, float* O_out,
+                                        int flags, gfwa_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -77,6 +77,8 @@ EXPORTED = (
     "gfwa_gate_prefix_workspace_size",
     "gfwa_gate_prefix_bwd",
     "gfwa_gate_prefix_bwd_workspace_size",
+    "gfwa_debug_tc_selftest_ex",
+    "gfwa_debug_stage_events",
     "gfwa_fwd",
     "gfwa_fwd_train",
     "gfwa_bwd",
@@ -176,8 +178,11 @@ _ws_cache: dict = {}
 
 def workspace(nbytes: int, device, tag: str = "scratch", zero: bool = False) -> torch.Tensor:
     """Cached device scratch (caller-owned per the ABI); `zero` tensors are
-    zeroed once at allocation (decode's self-resetting counters)."""
-    key = (tag, torch.device(device).index if torch.device(device).index is not None else torch.cuda.current_device())
+    zeroed once at allocation (decode's self-resetting counters).  Keyed by
+    (tag, device, current stream): calls on one stream are ordered, so they may
+    share a workspace; calls on different streams get their own."""
+    dev = torch.device(device).index if torch.device(device).index is not None else torch.cuda.current_device()
+    key = (tag, dev, torch.cuda.current_stream(dev).cuda_stream)
     t = _ws_cache.get(key)
     if t is None or t.numel() < nbytes:
         t = (torch.zeros if zero else torch.empty)(max(int(nbytes), 256), dtype=torch.uint8, device=device)
@@ -397,17 +402,28 @@ def gfwa_check_finite(x: torch.Tensor) -> bool:
     return True
 
 
-def gfwa_debug_tc_selftest(Q, K, V):
-    """S = Q K^T and O = bf16(S) V on one 128x128 tile through the tcgen05 path."""
+def gfwa_debug_tc_selftest(Q, K, V, flags: int = 0):
+    """S = Q K^T and O = bf16(S) V (flags & 1: fp16(S) V) on one 128x128 tile through the tcgen05 path."""
     lib = load()
     _need_cuda(Q, K, V)
     S = torch.empty(128, 128, dtype=torch.float32, device=Q.device)
     O = torch.empty_like(S)
-    f = lib.gfwa_debug_tc_selftest
+    f = lib.gfwa_debug_tc_selftest_ex
     f.restype = ctypes.c_int
-    f.argtypes = [_VP] * 6
-    _check(f(_ptr(Q), _ptr(K), _ptr(V), _ptr(S), _ptr(O), _stream(Q.device)), "gfwa_debug_tc_selftest")
+    f.argtypes = [_VP] * 5 + [ctypes.c_int, _VP]
+    _check(f(_ptr(Q), _ptr(K), _ptr(V), _ptr(S), _ptr(O), int(flags), _stream(Q.device)), "gfwa_debug_tc_selftest")
     return S, O
+
+
+def debug_stage_events(events) -> None:
+    """Register torch.cuda.Event objects for the next tensor-core gfwa_bwd on this
+    thread: events[0] after its preprocess kernel, events[1] after its main kernel."""
+    lib = load()
+    arr = (ctypes.c_void_p * 4)(*([e.cuda_event if e is not None else None for e in events] + [None] * 4)[:4])
+    f = lib.gfwa_debug_stage_events
+    f.restype = None
+    f.argtypes = [ctypes.c_void_p, ctypes.c_int]
+    f(ctypes.cast(arr, ctypes.c_void_p), len(events))
 
 
 def launch_count() -> int:

@@ -36,9 +36,15 @@ struct AttnParams {
 };
 
 // token marking a backward workspace whose dQ accumulator the forward already zeroed
+// the prepared-workspace token: a mix of the whole descriptor (never 0, the cleared value)
 inline unsigned long long prep_token(const AttnParams& p) {
-    return 0x4746574174726E21ull ^ ((unsigned long long)p.B << 48) ^ ((unsigned long long)p.H << 32) ^
-           ((unsigned long long)p.Nq << 8) ^ (unsigned long long)p.d;
+    unsigned long long x = 0x4746574174726E21ull;
+    const long long f[6] = {p.B, p.H, p.Nq, p.Nkv, p.d, p.w};
+    for (long long v : f) {
+        x ^= (unsigned long long)v + 0x9E3779B97F4A7C15ull + (x << 6) + (x >> 2);
+        x *= 0xBF58476D1CE4E5B9ull;
+    }
+    return x | 1ull;
 }
 
 __device__ __forceinline__ int64_t off3(const int64_t* s, int64_t b, int64_t n, int64_t h) {

@@ -606,12 +606,8 @@ gfwa_status_t tc_bwd(const AttnParams& pin, cudaStream_t st, void* ws) {
     GFWA_REQUIRE(encode_bnhd_map_f32(&mdq, p.dQacc, p.B, p.Nq, p.H, D, acc_s, 16));
     const int64_t rows = p.B * p.Nq * p.H;
     const unsigned rgrid = (unsigned)((rows + 7) / 8);
-    static int n_sm = 0;
-    if (n_sm == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-    }
+    int n_sm = 148, dev = 0;  // per call: the attribute is per device
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
     const int64_t n_du = p.B * p.H * p.Nkv;
     const bool o_flat = p.Ofp && p.os[2] == D && p.os[1] == p.H * D && p.os[0] == p.Nq * p.H * D &&
                         rows < ((int64_t)1 << 31) && n_du < ((int64_t)1 << 31);
@@ -625,6 +621,7 @@ gfwa_status_t tc_bwd(const AttnParams& pin, cudaStream_t st, void* ws) {
     }
     note_launch();
     if (gfwa_status_t s = check_launch()) return s;
+    stage_event(0, st);  // measurement hook: after the preprocess kernel
     TcBwdParams tp;
     tp.U = p.U;
     tp.LSE = p.LSE;
@@ -639,11 +636,10 @@ gfwa_status_t tc_bwd(const AttnParams& pin, cudaStream_t st, void* ws) {
     tp.sl2 = p.scale * kLog2e;
     tp.scale = p.scale;
     tp.token = p.token;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(bwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-        attr_set = true;
-    }
+    // per launch: the attribute is per device (a process may drive several GPUs)
+    if (gfwa_status_t s = check_launch(
+            cudaFuncSetAttribute(bwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes)))
+        return s;
     dim3 grid((unsigned)((p.Nkv + BN - 1) / BN), (unsigned)p.H, (unsigned)p.B);
     const char* trace_file = getenv("GFWA_TRACE_BWD");  // diagnostics (synchronous)
     const size_t n_cta = (size_t)grid.x * grid.y * grid.z;
@@ -665,6 +661,7 @@ gfwa_status_t tc_bwd(const AttnParams& pin, cudaStream_t st, void* ws) {
         }
     }
     if (gfwa_status_t s = check_launch()) return s;
+    stage_event(1, st);  // measurement hook: after the main kernel
     const bool dq_flat = p.qs[2] == D && p.qs[1] == p.H * D && p.qs[0] == p.Nq * p.H * D;
     if (dq_flat) {
         const int64_t n8 = rows * D / 8;

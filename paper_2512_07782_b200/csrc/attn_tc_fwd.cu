@@ -24,7 +24,11 @@
 //               part of exp2 on the FMA pipe, bf16 P back over the S columns;
 //               epilogue O / l staged in smem with the 128B swizzle and written
 //               by TMA stores, LSE = m + ln l.
-//   warps 6-7   idle (complete the second warpgroup for setmaxnreg)
+//   warps 6-7   training forward (O_f32 requested): convert each V tile to fp16
+//               in place once it lands, so the PV product runs with P in fp16
+//               (reading C-23: the fp32 O that the backward's D = rowsum(O dO)
+//               is taken from carries 8x less P rounding than with bf16 P);
+//               otherwise idle (they complete the second warpgroup for setmaxnreg)
 // TMEM (256 columns per CTA): S [0,128), O [128,256) x 128 lanes.
 // Key tiles outside every row's window are never loaded.
 #include <vector>
@@ -74,7 +78,7 @@ struct TcFwdParams {
     } while (0)
 
 struct __align__(8) Bars {
-    uint64_t q_full, k_full, k_empty, v_full, v_empty, s_full, p_ready, o_full;
+    uint64_t q_full, k_full, k_empty, v_full, v_empty, v_conv, s_full, p_ready, o_full;
 };
 
 __device__ __forceinline__ int64_t kv_tile_lo(int64_t g_lo, int w) { return max64(0, g_lo - w + 1) / BN; }
@@ -87,6 +91,7 @@ __device__ __forceinline__ uint32_t range_bits(int lo, int hi, int base) {
     return upto_z & ~below_a;
 }
 
+template <bool kF16P>  // training forward: P, V in fp16 for the PV product (reading C-23)
 __global__ void __launch_bounds__(kThreads, 2)
     fwd_tc_kernel(const __grid_constant__ CUtensorMap mzq, const __grid_constant__ CUtensorMap mq,
                   const __grid_constant__ CUtensorMap mk,
@@ -123,6 +128,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         mbar_init(&bars->k_empty, 1);
         mbar_init(&bars->v_full, 1);
         mbar_init(&bars->v_empty, 1);
+        mbar_init(&bars->v_conv, 2);
         mbar_init(&bars->s_full, 1);
         mbar_init(&bars->p_ready, 4);
         mbar_init(&bars->o_full, 1);
@@ -189,7 +195,9 @@ __global__ void __launch_bounds__(kThreads, 2)
     } else if (warp == kMmaWarp) {
         // ------------------------------------------------ MMA issuer
         const uint32_t idesc_qk = idesc_bf16(BM, BN, false, false);
-        const uint32_t idesc_pv = idesc_bf16(BM, D, false, true);
+        // training forward: P and V in fp16 (A/B format F16 = 0), reading C-23
+        const uint32_t idesc_pv = idesc_bf16(BM, D, false, true) & ~(kF16P ? (63u << 7) : 0u);
+        uint64_t* v_ready = kF16P ? &bars->v_conv : &bars->v_full;
         const uint32_t qbase = smem_u32(Qs), kbase = smem_u32(Ks), vbase = smem_u32(Vs);
         mbar_wait(&bars->q_full, 0);
         int k = 0;
@@ -197,7 +205,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             if (k > 0) {
                 // O += P(k-1) V(k-1), then V's stage is free
                 mbar_wait(&bars->p_ready, (k - 1) & 1);
-                mbar_wait(&bars->v_full, (k - 1) & 1);
+                mbar_wait(v_ready, (k - 1) & 1);
                 tc_fence_after();
                 if (elect_one()) {
 #pragma unroll
@@ -226,7 +234,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
         // last PV, then O is final
         mbar_wait(&bars->p_ready, (k - 1) & 1);
-        mbar_wait(&bars->v_full, (k - 1) & 1);
+        mbar_wait(v_ready, (k - 1) & 1);
         tc_fence_after();
         if (elect_one()) {
 #pragma unroll
@@ -236,6 +244,28 @@ __global__ void __launch_bounds__(kThreads, 2)
             tc_commit(&bars->o_full);
         }
         __syncwarp();
+    } else if (kF16P && warp >= 6) {
+        // ------------------------------------------------ V -> fp16 in place (training forward)
+        // 2048 16-byte chunks per tile over 64 threads; the layout (128B swizzle) is
+        // unchanged, only the element encoding: bf16 -> fp32 (exact) -> fp16 (RNE)
+        const uint32_t vb = smem_u32(Vs) + (threadIdx.x - 192) * 16;
+        int k = 0;
+        for (int64_t j = jhi; j >= jlo; --j, ++k) {
+            mbar_wait(&bars->v_full, k & 1);
+#pragma unroll 4
+            for (int c = 0; c < (int)(kTileBytes / 16 / 64); ++c) {
+                const uint32_t a = vb + c * 64 * 16;
+                uint4 x = lds128u(a);
+                x.x = bf16x2_to_f16x2(x.x);
+                x.y = bf16x2_to_f16x2(x.y);
+                x.z = bf16x2_to_f16x2(x.z);
+                x.w = bf16x2_to_f16x2(x.w);
+                sts128(a, x);
+            }
+            fence_proxy_async();  // generic-proxy writes -> visible to the tensor core
+            __syncwarp();
+            if ((threadIdx.x & 31) == 0) mbar_arrive(&bars->v_conv);
+        }
     } else if (warp < 4) {
         // ------------------------------------------------ softmax warpgroup
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kSoftmaxRegs));
@@ -347,9 +377,9 @@ __global__ void __launch_bounds__(kThreads, 2)
                         p1 = ex2(d1);
                     }
                     acc[e & 3] = fadd2(acc[e & 3], f2pack(p0, p1));
-                    pk[e] = pack_bf16x2(p0, p1);
+                    pk[e] = kF16P ? pack_f16x2(p0, p1) : pack_bf16x2(p0, p1);
                 }
-                tmem_st16(lane_addr + cb / 2, pk);  // P (bf16) over the S columns
+                tmem_st16(lane_addr + cb / 2, pk);  // P (bf16, or fp16 when training) over the S columns
             }
             if (trw) GFWA_TR(14 + (r == 96));
             {
@@ -488,11 +518,11 @@ gfwa_status_t tc_fwd(const AttnParams& p, cudaStream_t st) {
     tp.token = p.token;
     tp.token_val = p.token_val;
     tp.sl2 = p.scale * kLog2e;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(fwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-        attr_set = true;
-    }
+    // per launch: the attribute is per device (a process may drive several GPUs)
+    auto kern = tp.store_f32 ? fwd_tc_kernel<true> : fwd_tc_kernel<false>;
+    if (gfwa_status_t s = check_launch(
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes)))
+        return s;
     dim3 grid((unsigned)((p.Nq + BM - 1) / BM), (unsigned)p.H, (unsigned)p.B);
     // diagnostics: GFWA_TRACE_FWD=<file> dumps per-CTA clock64 stamps (synchronous)
     const char* trace_file = getenv("GFWA_TRACE_FWD");
@@ -502,7 +532,7 @@ gfwa_status_t tc_fwd(const AttnParams& p, cudaStream_t st) {
         cudaMalloc(&tp.trace, n_cta * 64 * sizeof(long long));
         cudaMemsetAsync(tp.trace, 0, n_cta * 64 * sizeof(long long), st);
     }
-    fwd_tc_kernel<<<grid, kThreads, kSmemBytes, st>>>(mzq, mq, mk, mv, mo, mo32, tp);
+    kern<<<grid, kThreads, kSmemBytes, st>>>(mzq, mq, mk, mv, mo, mo32, tp);
     note_launch();
     if (trace_file) {
         std::vector<long long> hbuf(n_cta * 64);

@@ -14,6 +14,13 @@ static thread_local int g_last_cuda_error = 0;
 
 void note_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
 
+static thread_local cudaEvent_t g_stage_ev[4] = {nullptr, nullptr, nullptr, nullptr};
+void stage_event(int stage, cudaStream_t st) {
+    if (stage < 0 || stage >= 4 || !g_stage_ev[stage]) return;
+    cudaEventRecord(g_stage_ev[stage], st);
+    g_stage_ev[stage] = nullptr;
+}
+
 gfwa_status_t check_launch(cudaError_t err) {
     if (err == cudaSuccess) return GFWA_OK;
     g_last_cuda_error = (int)err;
@@ -51,16 +58,24 @@ struct Prepare {
 };
 thread_local Prepare g_prepare;
 
+// per device (a process may drive several GPUs), race-free (relaxed atomics:
+// every thread computes the same value)
+constexpr int kMaxDev = 64;
+std::atomic<int> g_is_sm100[kMaxDev];  // 0 unknown, 1 yes, 2 no
+
 bool device_is_sm100() {
-    static int cached = -1;
-    if (cached < 0) {
-        int dev = 0, major = 0, minor = 0;
-        if (cudaGetDevice(&dev) != cudaSuccess) return false;
-        cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
-        cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
-        cached = (major == 10 && minor == 0) ? 1 : 0;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0) return false;
+    if (dev < kMaxDev) {
+        const int c = g_is_sm100[dev].load(std::memory_order_relaxed);
+        if (c) return c == 1;
     }
-    return cached == 1;
+    int major = 0, minor = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    const bool ok = major == 10 && minor == 0;
+    if (dev < kMaxDev) g_is_sm100[dev].store(ok ? 1 : 2, std::memory_order_relaxed);
+    return ok;
 }
 
 gfwa_status_t make_params(const gfwa_attn_desc_t* d, AttnParams& p) {
@@ -140,26 +155,26 @@ extern "C" gfwa_status_t gfwa_fwd(const gfwa_attn_desc_t* desc, const void* Q, c
     return s;
 }
 
-// [D | dalpha scan | dQ accumulator | token]; the token slot marks a workspace
-// whose accumulator gfwa_fwd_train already zeroed (tensor-core path only)
+// [token | D | dalpha scan | dQ accumulator]; the token (a fixed 256-byte slot at
+// the start, whatever the shape) marks a workspace whose accumulator the latest
+// gfwa_fwd_train already zeroed for exactly this descriptor (tensor-core path
+// only).  Every gfwa_fwd_train overwrites it and every tensor-core gfwa_bwd
+// clears it, so interleaved shapes on one workspace stay correct: a backward
+// whose descriptor does not match the token zeroes its own accumulator.
 extern "C" gfwa_status_t gfwa_fwd_train(const gfwa_attn_desc_t* desc, const void* Q, const void* K,
                                         const void* V, const float* U, void* O, float* O_f32, float* LSE,
                                         void* bwd_ws, size_t bwd_ws_bytes, gfwa_stream_t stream);
 
 static size_t bwd_ws_layout(const AttnParams& p, gfwa_dtype_t dt, size_t* off_D, size_t* off_scan,
                             size_t* off_tc, size_t* off_tok = nullptr) {
-    size_t off = 0;
+    size_t off = 256;
+    if (off_tok) *off_tok = 0;
     *off_D = off;
     off += ((size_t)p.B * p.H * p.Nq * sizeof(float) + 255) & ~(size_t)255;
     *off_scan = off;
     off += gfwa_gate_prefix_bwd_workspace_size(p.B * p.H, p.Nkv, 1);  // the dalpha scan below
     *off_tc = off;
-    if (off_tok) *off_tok = 0;
-    if (tc_bwd_supported(p, dt)) {
-        off += (tc_bwd_workspace(p) + 255) & ~(size_t)255;
-        if (off_tok) *off_tok = off;
-        off += 256;
-    }
+    if (tc_bwd_supported(p, dt)) off += (tc_bwd_workspace(p) + 255) & ~(size_t)255;
     return off;
 }
 
@@ -175,7 +190,7 @@ extern "C" gfwa_status_t gfwa_fwd_train(const gfwa_attn_desc_t* desc, const void
     size_t off_D, off_scan, off_tc, off_tok;
     const size_t need = bwd_ws_layout(p, desc->dtype, &off_D, &off_scan, &off_tc, &off_tok);
     if (bwd_ws_bytes < need) return GFWA_ERR_WORKSPACE;
-    if (!off_tok || !tc_fwd_supported(p, desc->dtype))  // no accumulator to prepare: plain forward
+    if (!tc_bwd_supported(p, desc->dtype) || !tc_fwd_supported(p, desc->dtype))  // nothing to prepare
         return gfwa_fwd(desc, Q, K, V, U, O, O_f32, LSE, stream);
     g_prepare.zero_acc = (float*)((char*)bwd_ws + off_tc);
     g_prepare.token = (unsigned long long*)((char*)bwd_ws + off_tok);
@@ -210,7 +225,7 @@ extern "C" gfwa_status_t gfwa_bwd(const gfwa_attn_desc_t* desc, const void* Q, c
     size_t off_D, off_scan, off_tc, off_tok;
     const size_t need = bwd_ws_layout(p, desc->dtype, &off_D, &off_scan, &off_tc, &off_tok);
     if (ws_bytes < need) return GFWA_ERR_WORKSPACE;
-    p.token = off_tok ? (unsigned long long*)((char*)ws + off_tok) : nullptr;
+    p.token = tc_bwd_supported(p, desc->dtype) ? (unsigned long long*)((char*)ws + off_tok) : nullptr;
     p.token_val = prep_token(p);
     bind_context(Q);
     p.Q = Q;
@@ -313,4 +328,7 @@ extern "C" const char* gfwa_status_string(gfwa_status_t s) {
 
 extern "C" int gfwa_last_cuda_error(void) { return g_last_cuda_error; }
 extern "C" const char* gfwa_version(void) { return "gfwa 0.1.0 (sm_100a)"; }
+extern "C" void gfwa_debug_stage_events(void* const* events, int n) {
+    for (int i = 0; i < 4; ++i) g_stage_ev[i] = (events && i < n) ? (cudaEvent_t)events[i] : nullptr;
+}
 extern "C" uint64_t gfwa_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }

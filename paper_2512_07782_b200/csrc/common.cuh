@@ -18,6 +18,9 @@ namespace gfwa {
 
 // Counts kernel launches issued through the library (gfwa_launch_count()).
 void note_launch(int n = 1);
+// measurement hook (gfwa_debug_stage_events): records the calling thread's
+// registered event for `stage` on `st`, if one is registered, and clears it
+void stage_event(int stage, cudaStream_t st);
 // Records a CUDA error for gfwa_last_cuda_error(); returns GFWA_ERR_CUDA if err.
 gfwa_status_t check_launch(cudaError_t err);
 inline gfwa_status_t check_launch() { return check_launch(cudaGetLastError()); }

@@ -16,7 +16,7 @@
 // GQA (heads_per_gqa_group = 4 in the paper's NSA runs,
 // P:1209-1211): G = H / H_kv query heads share one K/V head, so each cache row
 // is read once for G queries (G x less HBM per query head).  The gate stays
-// per query head (U_cache [B,H,w], the bias u_t - u_i of that head's gate).
+// per query head (U_cache [B,H,w]: u_tau - u_newest of that head's gate).
 #include "common.cuh"
 #include "sm100.cuh"
 
@@ -96,7 +96,6 @@ __global__ void __launch_bounds__(kThreads, GFWA_DEC_MINB) decode_kernel(DecodeP
     __shared__ float s_score[G][kMaxSlotsPerCta];
     __shared__ float s_red[kWarps][G][D];
     __shared__ float s_m[kWarps][G], s_l[kWarps][G];
-    __shared__ float s_ut[G];
     __shared__ bool s_last;
     constexpr int R_ = (G >= 8 && D == 128) ? kRing / 2 : kRing;  // static smem stays under 48 KB
     __shared__ uint4 s_ring[kWarps][R_][32];  // per-warp row ring (16 B per lane per iteration)
@@ -112,20 +111,22 @@ __global__ void __launch_bounds__(kThreads, GFWA_DEC_MINB) decode_kernel(DecodeP
     const int s0 = split * p.slots_per_cta;
     const int s1 = min(s0 + p.slots_per_cta, n_valid);
 
-    // u_t = u_{t-1} - alpha_t per query head, u_{t-1} from the ring (0 before the first token)
-    float u_t[G];
+    // alpha_t per query head.  U_cache holds, per slot, r = u_tau - u_{t-1} >= 0 (the
+    // gate sum between the slot's token tau and the newest cached token): the bias of
+    // this step is u_t - u_tau = -(r + alpha_t), and the slot is rewritten as
+    // r + alpha_t (relative to u_t).  Stored values stay bounded by the window's gate
+    // sum whatever the position, so fp32 never loses the small alphas (a running
+    // absolute u would: its ulp grows with the position)
+    float a_t[G];
 #pragma unroll
     for (int g = 0; g < G; ++g) {
         const int64_t bh = bh0 + g;
-        const float u_prev = t > 0 ? p.Uc[bh * w + (int)((t - 1) % w)] : 0.f;
-        float alpha;
         if (p.gate_kind == GFWA_GATE_ALPHA) {
-            alpha = p.gate_a[bh];
+            a_t[g] = p.gate_a[bh];
         } else {
             const float hv = p.gate_a[bh], bv = p.gate_b[bh];
-            alpha = softplus_f(bv * hv) / (bv + p.eps);
+            a_t[g] = softplus_f(bv * hv) / (bv + p.eps);
         }
-        u_t[g] = u_prev - alpha;
     }
 
     const T* Kc = (const T*)p.Kc + bk * (int64_t)w * D;
@@ -141,7 +142,8 @@ __global__ void __launch_bounds__(kThreads, GFWA_DEC_MINB) decode_kernel(DecodeP
     const float sl2 = p.scale * kLog2e;
 
     // bias (u_t - u_i) log2e of every (head, slot) of this CTA, loaded coalesced up front
-    // (a per-row u load inside pass 1 would stall the in-order warp on every row)
+    // (a per-row u load inside pass 1 would stall the in-order warp on every row); each
+    // slot is read and rewritten (r + alpha_t) by the one thread that owns it
     const int nsl = max(s1 - s0, 0);
     constexpr int kU = 8;  // independent u loads in flight per thread
     for (int i0 = threadIdx.x; i0 < G * nsl; i0 += kThreads * kU) {
@@ -157,11 +159,13 @@ __global__ void __launch_bounds__(kThreads, GFWA_DEC_MINB) decode_kernel(DecodeP
             const int i = i0 + k * kThreads;
             if (i >= G * nsl) break;
             const int g = i / nsl, j = i % nsl;
-            float ut = u_t[0];
+            float at = a_t[0];
 #pragma unroll
             for (int gg = 1; gg < G; ++gg)
-                if (g == gg) ut = u_t[gg];
-            s_score[g][j] = (s0 + j == slot_new) ? 0.f : (ut - uv[k]) * kLog2e;
+                if (g == gg) at = a_t[gg];
+            const float r = (s0 + j == slot_new) ? 0.f : uv[k] + at;
+            s_score[g][j] = -r * kLog2e;
+            p.Uc[(bh0 + g) * w + s0 + j] = r;
         }
     }
     __syncthreads();
@@ -330,10 +334,6 @@ __global__ void __launch_bounds__(kThreads, GFWA_DEC_MINB) decode_kernel(DecodeP
         }
         if (lane == 0) s_l[warp][g] = lloc[g];
     }
-    if (threadIdx.x < G) s_ut[threadIdx.x] = u_t[0];
-#pragma unroll
-    for (int g = 1; g < G; ++g)
-        if (threadIdx.x == g) s_ut[g] = u_t[g];
     __syncthreads();
 
     // partials of this split -> workspace, one per query head
@@ -363,7 +363,6 @@ __global__ void __launch_bounds__(kThreads, GFWA_DEC_MINB) decode_kernel(DecodeP
             kd[c] = knew[c];
             vd[c] = vnew[c];
         }
-        if (threadIdx.x < G) p.Uc[(bh0 + threadIdx.x) * w + slot_new] = s_ut[threadIdx.x];
     }
     __threadfence();
     __syncthreads();

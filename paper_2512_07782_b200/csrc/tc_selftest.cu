@@ -4,6 +4,8 @@
 // the A operand of a TS MMA against an MN-major B) on one 128x128x128 tile:
 //   S = Q K^T (fp32, TMEM),  P = bf16(S) (TMEM),  O = P V (fp32, TMEM).
 // tests/test_gpu_tc_selftest.py compares S and O with torch.matmul.
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 #include "sm100.cuh"
 #include "tma_host.cuh"
@@ -18,7 +20,7 @@ constexpr uint32_t kTile = 128 * 128 * 2;  // one bf16 128x128 tile (two 64-col 
 __global__ void __launch_bounds__(192, 1) selftest_kernel(const __grid_constant__ CUtensorMap mq,
                                                           const __grid_constant__ CUtensorMap mk,
                                                           const __grid_constant__ CUtensorMap mv, float* S_out,
-                                                          float* O_out) {
+                                                          float* O_out, int flags) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint8_t* Qs = smem;
@@ -69,7 +71,8 @@ __global__ void __launch_bounds__(192, 1) selftest_kernel(const __grid_constant_
         mbar_wait(&bar_p, 0);
         tc_fence_after();
         if (elect_one()) {
-            const uint32_t idesc_pv = idesc_bf16(128, 128, false, true);
+            // flags & 1: P is fp16 in TMEM (A format F16) against bf16 V (B format BF16)
+            const uint32_t idesc_pv = idesc_bf16(128, 128, false, true) & ~((flags & 1) ? (7u << 7) : 0u);
             for (int k = 0; k < 8; ++k) {
                 // A = P columns [8k, 8k+8) (16 bf16 keys); B = V rows [16k, 16k+16)
                 mma_ts(tmem + 128, tmem + k * 8, sdesc_sw128(smem_u32(Vs) + k * 2048, kTile / 2, 1024),
@@ -94,7 +97,14 @@ __global__ void __launch_bounds__(192, 1) selftest_kernel(const __grid_constant_
         for (int c = 0; c < 128; ++c) S_out[row * 128 + c] = s[c];
         for (int c = 0; c < 64; c += 32) {
             uint32_t r[32];
-            for (int i = 0; i < 32; ++i) r[i] = pack_bf16x2(s[2 * (c + i)], s[2 * (c + i) + 1]);
+            for (int i = 0; i < 32; ++i) {
+                if (flags & 1) {
+                    const __half2 hv = __floats2half2_rn(s[2 * (c + i)], s[2 * (c + i) + 1]);
+                    r[i] = *reinterpret_cast<const uint32_t*>(&hv);
+                } else {
+                    r[i] = pack_bf16x2(s[2 * (c + i)], s[2 * (c + i) + 1]);
+                }
+            }
             tmem_st32(lane_addr + c, r);
         }
         tmem_wait_st();
@@ -124,8 +134,8 @@ __global__ void __launch_bounds__(192, 1) selftest_kernel(const __grid_constant_
 using namespace gfwa;
 
 // Q, K, V: [128, 128] bf16 row-major device arrays; S_out, O_out: [128,128] fp32.
-extern "C" gfwa_status_t gfwa_debug_tc_selftest(const void* Q, const void* K, const void* V, float* S_out,
-                                                float* O_out, gfwa_stream_t stream) {
+extern "C" gfwa_status_t gfwa_debug_tc_selftest_ex(const void* Q, const void* K, const void* V, float* S_out,
+                                                   float* O_out, int flags, gfwa_stream_t stream) {
     if (!Q || !K || !V || !S_out || !O_out) return GFWA_ERR_INVALID_ARGUMENT;
     CUtensorMap mq, mk, mv;
     const int64_t st[3] = {128 * 128, 128, 128};
@@ -134,7 +144,12 @@ extern "C" gfwa_status_t gfwa_debug_tc_selftest(const void* Q, const void* K, co
         return GFWA_ERR_INVALID_ARGUMENT;
     const size_t smem = 3 * kTile + 1024;
     cudaFuncSetAttribute(selftest_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    selftest_kernel<<<1, 192, smem, (cudaStream_t)stream>>>(mq, mk, mv, S_out, O_out);
+    selftest_kernel<<<1, 192, smem, (cudaStream_t)stream>>>(mq, mk, mv, S_out, O_out, flags);
     note_launch();
     return check_launch();
+}
+
+extern "C" gfwa_status_t gfwa_debug_tc_selftest(const void* Q, const void* K, const void* V, float* S_out,
+                                                float* O_out, gfwa_stream_t stream) {
+    return gfwa_debug_tc_selftest_ex(Q, K, V, S_out, O_out, 0, stream);
 }

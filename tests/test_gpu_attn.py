@@ -68,11 +68,22 @@ BF16_SHAPES = [
     synth.AttnShape(B=1, H=2, N=640, d=64, w=200),
     synth.AttnShape(B=1, H=2, N=384, d=128, w=2048),     # w > N
     synth.AttnShape(B=1, H=2, N=512, d=128, w=256, N_kv=768),  # halo
+    # the method's degenerate cases on the tensor-core path
+    synth.AttnShape(B=1, H=2, N=1, d=128, w=1),           # N = 1: O = v_0, gradients 0 but dV
+    synth.AttnShape(B=2, H=2, N=200, d=128, w=1),         # w = 1: O = V
+    synth.AttnShape(B=1, H=3, N=37, d=128, w=33),         # sub-tile N, odd w
+    synth.AttnShape(B=1, H=2, N=300, d=128, w=250, N_kv=500),  # halo of 200 rows (not tile-aligned)
+    synth.AttnShape(B=1, H=2, N=390, d=128, w=1000),      # w >= N with a ragged tail
+    synth.AttnShape(B=1, H=2, N=129, d=128, w=129, N_kv=129 + 70),  # ragged halo, w = N
 ]
 
 
 @pytest.mark.parametrize("s", BF16_SHAPES, ids=lambda s: f"B{s.B}H{s.H}N{s.N}kv{s.nkv}d{s.d}w{s.w}")
 def test_bf16_path_matches_oracle(s):
+    Q = torch.empty(s.B, s.N, s.H, s.d, dtype=torch.bfloat16, device="cuda")
+    K = torch.empty(s.B, s.nkv, s.H, s.d, dtype=torch.bfloat16, device="cuda")
+    if s.d == 128:
+        assert gb.gfwa_attn_path(Q, K, K, s.w) == 1, "bf16 d=128 must run on the tcgen05 kernels"
     got, ref = _run(s, torch.bfloat16, seed=3 * s.N + s.w)
     assert max_abs(got["O"], ref["O"]) <= TOL_BF16_O
     assert max_abs(got["LSE"], ref["LSE"]) <= TOL_LSE
@@ -155,6 +166,29 @@ def test_zero_grad_out_and_invariants():
     assert da[..., 0].abs().max().item() <= 1e-3 * da.abs().max().item()
 
 
+def test_bf16_tc_invariants():
+    """On the tensor-core backward: dO = 0 -> every gradient exactly 0; sum_m dU_m = 0
+    and dalpha_0 = 0 (rowsum(dS) = 0; du^q and du^k are summed from
+    the same fp32 dS, reading C-11, so the telescoping holds to fp32 round-off)."""
+    s = synth.AttnShape(B=2, H=4, N=1500, d=128, w=300)
+    Q, K, V, dO = synth.attn_inputs(s, seed=13, device="cuda", dtype=torch.bfloat16)
+    assert gb.gfwa_attn_path(Q, K, V, s.w) == 1
+    h, beta = synth.gate_inputs(s.B, s.N, s.H, seed=14, device="cuda")
+    U = gb.gfwa_gate_prefix(h, beta)
+    O, LSE, O32 = gb.gfwa_fwd(Q, K, V, U, s.w, want_o_f32=True)
+    z = gb.gfwa_bwd(Q, K, V, U, O, LSE, torch.zeros_like(dO), s.w, O_f32=O32)
+    for t in z:
+        assert torch.count_nonzero(t) == 0
+    dQ, dK, dV, dU, da = gb.gfwa_bwd(Q, K, V, U, O, LSE, dO, s.w, O_f32=O32)
+    # fp32 round-off of sums of ~N w terms of size |dS| <= max|dU|
+    bound = 1e-4 * dU.abs().max().item()
+    assert dU.double().sum(-1).abs().max().item() <= bound
+    assert da[..., 0].abs().max().item() <= bound
+    # dalpha is the exact reverse scan of dU (P:276)
+    scan = -torch.flip(torch.cumsum(torch.flip(dU.double(), [-1]), -1), [-1])
+    assert (da.double() - scan).abs().max().item() <= 1e-5 * max(1.0, scan.abs().max().item())
+
+
 def _sampled_full_size(s: synth.AttnShape, seed: int, n_rows: int, bwd_slices, halo: int = 0):
     """Forward on sampled rows across all slices, fwd+bwd in full on the given
     (b, h) slices, at a BASELINE shape in the launch configuration bench.py times."""
@@ -179,9 +213,9 @@ def _sampled_full_size(s: synth.AttnShape, seed: int, n_rows: int, bwd_slices, h
         for k, t in (("dQ", dQ), ("dK", dK), ("dV", dV)):
             assert max_abs(sl(t), g[k]) <= TOL_BF16_GRAD, k
         assert max_abs(dU[b:b + 1, hh:hh + 1], g["dU"]) <= TOL_BF16_GRAD
-        # d-alpha sums up to N per-row gradients (reading C-22)
-        tol_da = TOL_BF16_GRAD * max(1.0, (s.nkv / 1024) ** 0.5)
-        assert max_abs(da[b:b + 1, hh:hh + 1], g["dalpha"]) <= tol_da
+        e_da = max_abs(da[b:b + 1, hh:hh + 1], g["dalpha"])
+        print(f"dalpha max abs error b{b} h{hh}: {e_da:.4f}")
+        assert e_da <= TOL_BF16_GRAD
 
 
 @pytest.mark.parametrize("wl", ["C3_w128", "C3_w512", "C3_w2048"])
@@ -222,3 +256,32 @@ def test_fwd_train_prepares_the_backward_workspace():
         tol = 1e-2 * max(1.0, a.float().abs().max().item())  # fp32 reduce order only (bf16 outputs)
         assert (a.float() - b.float()).abs().max().item() <= tol
         assert (a.float() - c.float()).abs().max().item() <= tol
+
+
+def test_fwd_train_interleaved_shapes_share_one_workspace():
+    """two prepared forwards of different shapes on the one cached
+    workspace, then their backwards in reverse order (as autograd runs them).
+    The token names the whole descriptor at a fixed offset: Y's backward finds
+    its own token, X's finds it cleared and zeroes its accumulator itself."""
+    sx = synth.AttnShape(B=2, H=3, N=900, d=128, w=300)
+    sy = synth.AttnShape(B=1, H=2, N=500, d=128, w=128)
+    out = {}
+    for name, s, seed in (("X", sx, 41), ("Y", sy, 43)):
+        Q, K, V, dO = synth.attn_inputs(s, seed=seed, device="cuda", dtype=torch.bfloat16)
+        h, beta = synth.gate_inputs(s.B, s.N, s.H, seed=seed + 1, device="cuda")
+        U = gb.gfwa_gate_prefix(h, beta)
+        ref_o = gb.gfwa_fwd(Q, K, V, U, s.w, want_o_f32=True)
+        ref = gb.gfwa_bwd(Q, K, V, U, *ref_o[:2], dO, s.w, O_f32=ref_o[2])
+        out[name] = (Q, K, V, U, dO, s, [r.clone() for r in ref[:4]])
+    prep = {}
+    for name in ("X", "Y"):
+        Q, K, V, U, dO, s, _ = out[name]
+        prep[name] = gb.gfwa_fwd(Q, K, V, U, s.w, want_o_f32=True, prepare_bwd=True)
+    for name in ("Y", "X"):
+        Q, K, V, U, dO, s, ref = out[name]
+        O, LSE, O32 = prep[name]
+        got = gb.gfwa_bwd(Q, K, V, U, O, LSE, dO, s.w, O_f32=O32)
+        torch.cuda.synchronize()
+        for a, b in zip(ref, got[:4]):
+            tol = 1e-2 * max(1.0, a.float().abs().max().item())  # fp32 reduce order only
+            assert (a.float() - b.float()).abs().max().item() <= tol, name

@@ -42,7 +42,9 @@ def test_decode_sequence_equals_prefill_rows(dtype, d, w, steps):
     t_last = steps - 1
     for t in range(max(0, steps - w), steps):
         assert torch.equal(Kc[:, :, t % w].cpu(), K[:, t].to(dtype).permute(0, 1, 2))
-    assert np.allclose(np64(Uc[:, :, t_last % w]), U[:, :, t_last], rtol=1e-6, atol=1e-5)
+    # U_cache is relative to the newest token: u_tau - u_{t_last} per slot
+    for t in range(max(0, steps - w), steps):
+        assert np.allclose(np64(Uc[:, :, t % w]), U[:, :, t] - U[:, :, t_last], rtol=1e-5, atol=1e-5)
 
 
 def test_decode_C5_full_size_sampled():
@@ -53,11 +55,12 @@ def test_decode_C5_full_size_sampled():
     B, H, d, w = c["B"], c["H"], c["d"], c["w"]
     Kc, Vc, a_hist, q, k, v, a_new = synth.decode_inputs(B, H, d, w, seed=c["seed"], device="cuda")
     t = w + 17
-    # history tokens t-w .. t-1 live at slot (token mod w); their u from the oracle scan
+    # history tokens t-w .. t-1 live at slot (token mod w); their u from the oracle scan,
+    # stored relative to the newest cached token (the U_cache convention)
     U_hist, _ = oracle.gate_prefix(a_hist)            # u of tokens t-w..t-1 (frame: u_{t-w-1} = 0)
     slots = np.arange(t - w, t) % w
     Uc = np.zeros((B, H, w))
-    Uc[:, :, slots] = U_hist
+    Uc[:, :, slots] = U_hist - U_hist[:, :, -1:]
     Kc_ring = torch.empty_like(Kc)
     Vc_ring = torch.empty_like(Vc)
     Kc_ring[:, :, torch.from_numpy(slots).cuda()] = Kc
@@ -74,8 +77,7 @@ def test_decode_C5_full_size_sampled():
         order = [(tok % w) for tok in range(t - w + 1, t)]  # window of token t: t-w+1 .. t
         keys = np.concatenate([np64(Kc_ring[b, hh, order]), np64(k[b, hh])[None]])
         vals = np.concatenate([np64(Vc_ring[b, hh, order]), np64(v[b, hh])[None]])
-        u_prev = Uc_used[b, hh, (t - 1) % w]
-        ut = u_prev - a_new_np[b, hh]
+        ut = -a_new_np[b, hh]  # frame u_{t-1} = 0
         u = np.concatenate([Uc_used[b, hh, order], [ut]])
         o_ref, _ = oracle.attend_row(np64(q[b, hh]), keys, vals, u, ut)
         assert np.abs(np64(o[b, hh]) - o_ref).max() <= TOL_BF16_O
@@ -127,7 +129,7 @@ def test_decode_C5_gqa4_full_size_sampled():
     U_hist, _ = oracle.gate_prefix(a_hist)
     slots = np.arange(t - w, t) % w
     Uc = np.zeros((B, H, w))
-    Uc[:, :, slots] = U_hist
+    Uc[:, :, slots] = U_hist - U_hist[:, :, -1:]
     idx = torch.from_numpy(slots).cuda()
     Kc_ring, Vc_ring = torch.empty_like(Kc), torch.empty_like(Vc)
     Kc_ring[:, :, idx] = Kc
@@ -145,11 +147,46 @@ def test_decode_C5_gqa4_full_size_sampled():
         kh = hh // G
         keys = np.concatenate([np64(Kc_ring[b, kh, order]), np64(k[b, kh])[None]])
         vals = np.concatenate([np64(Vc_ring[b, kh, order]), np64(v[b, kh])[None]])
-        ut = Uc_used[b, hh, (t - 1) % w] - a_new_np[b, hh]
+        ut = -a_new_np[b, hh]  # frame u_{t-1} = 0
         u = np.concatenate([Uc_used[b, hh, order], [ut]])
         o_ref, _ = oracle.attend_row(np64(q[b, hh]), keys, vals, u, ut)
         assert np.abs(np64(o[b, hh]) - o_ref).max() <= TOL_BF16_O
     assert torch.equal(Kc_ring[:, :, t % w], k) and torch.equal(Vc_ring[:, :, t % w], v)
-    # every query head's u_t was written to its own U_cache slot
-    ut_all = Uc_used[:, :, (t - 1) % w] - a_new_np
-    assert np.allclose(np64(Uc_t[:, :, t % w]), ut_all, rtol=1e-6, atol=1e-5)
+    # every query head's ring is now relative to its own u_t: the new slot holds 0,
+    # the others u_tau - u_t = U_cache + alpha_t
+    after = np64(Uc_t)
+    assert np.all(after[:, :, t % w] == 0.0)
+    keep = [s for s in range(w) if s != t % w]
+    assert np.allclose(after[:, :, keep], Uc_used[:, :, keep] + a_new_np[:, :, None], rtol=1e-6, atol=1e-5)
+
+
+def test_decode_long_position_no_gate_drift():
+    """3000 consecutive decode steps at a position past 10^6 with small
+    gates (alpha ~ 5e-3).  An fp32 running absolute u would be ~1e4 there and
+    swallow such alphas; the relative ring keeps every bias exact to fp32 of the
+    window's gate sum.  After the run each slot must hold u_tau - u_last of the
+    fp64 scan of the alphas the kernel saw, and the last output must equal the
+    oracle row over the window."""
+    B, H, d, w, steps, t0 = 1, 2, 64, 512, 3000, 1_000_003
+    s = synth.AttnShape(B=B, H=H, N=steps, d=d, w=w)
+    Q, K, V, _ = synth.attn_inputs(s, seed=77, dtype=torch.bfloat16, with_grad_out=False)
+    g = torch.Generator().manual_seed(78)
+    alpha = (0.005 * torch.rand(B, steps, H, generator=g)).float()
+    Kc = torch.zeros(B, H, w, d, dtype=torch.bfloat16, device="cuda")
+    Vc = torch.zeros_like(Kc)
+    Uc = torch.zeros(B, H, w, dtype=torch.float32, device="cuda")
+    a_dev = alpha.cuda()
+    Qd, Kd, Vd = Q.cuda(), K.cuda(), V.cuda()
+    for t in range(steps):
+        pos = torch.full((B,), t0 + t, dtype=torch.int64, device="cuda")
+        o = gb.gfwa_decode(Qd[:, t].contiguous(), Kd[:, t].contiguous(), Vd[:, t].contiguous(),
+                           a_dev[:, t].contiguous(), Kc, Vc, Uc, pos)
+    torch.cuda.synchronize()
+    # before t0 the ring held zeros with U_cache 0 (fully open gates): the first w steps
+    # see those zero rows; after w steps only real tokens remain
+    U = -np.cumsum(alpha.double().numpy().transpose(0, 2, 1), -1)  # [B, H, steps]
+    last = steps - 1
+    for t in range(steps - w, steps):
+        np.testing.assert_allclose(np64(Uc[:, :, (t0 + t) % w]), U[:, :, t] - U[:, :, last], rtol=0, atol=2e-5)
+    ref, _ = oracle.fwd(Q[:, steps - w:], K[:, steps - w:], V[:, steps - w:], U[:, :, steps - w:], w)
+    assert np.abs(np64(o) - ref[:, -1]).max() <= TOL_BF16_O

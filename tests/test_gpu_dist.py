@@ -68,13 +68,11 @@ def test_sequence_sharded_cuda_matches_oracle(use_ext):
             for k in ("dQ", "dK", "dV"):
                 assert np.abs(res[r][k].numpy() - g[k][:, sl]).max() <= TOL_BF16_GRAD, k
             assert np.abs(res[r]["dU"].numpy() - g["dU"][..., sl]).max() <= TOL_BF16_GRAD
-        # d-alpha (reading C-22): the reverse cumulative sum of dU over up to N
-        # terms, so bf16 rounding of the per-row gradients accumulates in it; the
-        # per-row gradient dU carries the bf16 tolerance above, and the sharded
-        # d-alpha must equal the exact (fp64) reverse scan of the gathered dU --
-        # which checks the cross-rank carry
+        # the sharded d-alpha must equal the exact (fp64) reverse scan of the
+        # gathered dU -- which checks the cross-rank carry -- and the oracle's
+        # d-alpha at north_star's gradient tolerance
         dU_all = np.concatenate([res[r]["dU"].numpy().astype(np.float64) for r in range(world)], -1)
         da_scan = -np.flip(np.cumsum(np.flip(dU_all, -1), -1), -1)
         da_all = np.concatenate([res[r]["dalpha"].numpy().astype(np.float64) for r in range(world)], -1)
         assert np.abs(da_all - da_scan).max() <= 1e-5 * max(1.0, np.abs(da_scan).max())
-        assert np.abs(da_all - g["dalpha"]).max() <= TOL_BF16_GRAD * np.sqrt(N / 1024)
+        assert np.abs(da_all - g["dalpha"]).max() <= TOL_BF16_GRAD
