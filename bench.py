@@ -159,14 +159,14 @@ def _step_fns(gb, s, Q, K, V, dO, h, beta, st, stage_events=None):
         U = gb.gfwa_gate_prefix(h, beta)
         if timed_kernels:
             e[1].record(st)
-        O, LSE, O32 = gb.gfwa_fwd(Q, K, V, U, s.w, want_o_f32=True, prepare_bwd=True)
+        O, LSE, Olo = gb.gfwa_fwd(Q, K, V, U, s.w, want_o_lo=True, prepare_bwd=True)
         if timed_kernels:
             e[2].record(st)
             sev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
             for x in sev:  # create the CUDA events (torch creates them lazily)
                 x.record(st)
             gb.debug_stage_events(sev)  # after the bwd preprocess kernel / after its main kernel
-        dQ, dK, dV, dU, _ = gb.gfwa_bwd(Q, K, V, U, O, LSE, dO, s.w, O_f32=O32, want_dalpha=False)
+        dQ, dK, dV, dU, _ = gb.gfwa_bwd(Q, K, V, U, O, LSE, dO, s.w, O_lo=Olo, want_dalpha=False)
         if timed_kernels:
             e[3].record(st)
         _, dh, dbeta = gb.gfwa_gate_prefix_bwd(dU, h, beta, want_dalpha=False)
@@ -513,8 +513,8 @@ def run_e2e(args, s, Q, K, V, dO, h, beta, step_fn, dev, world, dist):
     def compute(bufs):
         Qd, Kd, Vd, dOd, hd, bd = bufs
         U = gb.gfwa_gate_prefix(hd, bd)
-        O, LSE, O32 = gb.gfwa_fwd(Qd, Kd, Vd, U, s.w, want_o_f32=True, prepare_bwd=True)
-        dQ, dK, dV, dU, _ = gb.gfwa_bwd(Qd, Kd, Vd, U, O, LSE, dOd, s.w, O_f32=O32, want_dalpha=False)
+        O, LSE, Olo = gb.gfwa_fwd(Qd, Kd, Vd, U, s.w, want_o_lo=True, prepare_bwd=True)
+        dQ, dK, dV, dU, _ = gb.gfwa_bwd(Qd, Kd, Vd, U, O, LSE, dOd, s.w, O_lo=Olo, want_dalpha=False)
         _, dh, dbeta = gb.gfwa_gate_prefix_bwd(dU, hd, bd, want_dalpha=False)
         return (O, dQ, dK, dV, dh, dbeta)
 

@@ -27,7 +27,8 @@
  *  - Logit (Eq. 12; C-1): s_tj = scale * q_t.k_j + (u_t - u_j),
  *    scale defaults to 1/sqrt(d) and multiplies q.k only.
  *  - dtypes: Q/K/V/O/dO/dQ/dK/dV/caches are GFWA_BF16 (tensor-core path) or
- *    GFWA_F32 (exact parity path).  U, LSE, D, dU, dalpha, O_f32 are fp32;
+ *    GFWA_F32 (exact parity path).  U, LSE, D, dU, dalpha are fp32; O_lo
+ *    (the bf16 residual of O's output cast) is bf16;
  *    carries and totals are fp64.
  */
 #ifndef GFWA_H_
@@ -153,23 +154,28 @@ typedef struct {
  *   O[b,t,hh,:] = sum_j softmax_j(s_tj) V[b,j,hh,:] over the window,
  *   LSE[b,hh,t] = log sum_j exp(s_tj)   (natural log, bias included, C-10)
  * Q [B,N_q,H,d], K, V [B,N_kv,H,d], U [B,H,N_kv] fp32 -> O [B,N_q,H,d],
- * LSE [B,H,N_q] fp32.  O_f32 (nullable) [B,N_q,H,d] fp32 receives O before
- * the output cast; pass it to gfwa_bwd so D = rowsum(O*dO) is taken from fp32
- * O (reading C-12).  With O_f32 the bf16 tensor-core path forms the PV product
- * with P and V in fp16 (reading C-23; |v| < 65504 required), without it in
- * bf16.  Key tiles outside every row's window are never read.
+ * LSE [B,H,N_q] fp32.  O_lo (nullable; BF16 dtype only, same layout and
+ * strides as O) receives the bf16 residual of the output cast,
+ * O_lo = bf16(O_fp32 - O), so O + O_lo carries the fp32 O to ~2^-17 relative;
+ * pass it to gfwa_bwd so D = rowsum(O*dO) is taken from it (reading C-12;
+ * SURVEY C-12's bf16-residual alternative to an fp32 O: half the bytes).
+ * With O_lo the tensor-core path forms the PV product with P and V in fp16
+ * (reading C-23; |v| < 65504 required), without it in bf16.  Key tiles
+ * outside every row's window are never read.  INVALID_ARGUMENT if O_lo is
+ * given with dtype F32 (an fp32 O is exact).
  */
 gfwa_status_t gfwa_fwd(const gfwa_attn_desc_t* desc, const void* Q, const void* K, const void* V,
-                       const float* U, void* O, float* O_f32, float* LSE, gfwa_stream_t stream);
+                       const float* U, void* O, void* O_lo, float* LSE, gfwa_stream_t stream);
 
 /*
  * gfwa_bwd -- Alg. E.2 with readings C-3 (scale on dQ, dK),
- * C-4 (du^k is a column sum), C-11 (du^q row sum kept), C-12 (D from O_f32):
+ * C-4 (du^k is a column sum), C-11 (du^q row sum kept), C-12 (D from O + O_lo):
  *   D = rowsum(O*dO);  P = exp(s - LSE);  dS = P (dO V^T - D)
  *   dV = P^T dO;  dQ = scale dS K;  dK = scale dS^T Q
  *   dU[g] = sum_j dS_tj (g = t + h0)  -  sum_t dS_tj (key j)
  *   dalpha = dalpha_carry - reverse_cumsum(dU)     (NULL to skip)
- * O (dtype) is used for D only when O_f32 is NULL.  dK, dV, dU cover all N_kv
+ * D = rowsum((O + O_lo) * dO) when O_lo is given (BF16), else rowsum(O * dO);
+ * O, O_lo and dO share O's strides.  dK, dV, dU cover all N_kv
  * key rows (halo rows included); dQ covers N_q rows.  dalpha [B,H,N_kv] fp32,
  * dalpha_carry [B*H] fp64 or NULL.
  * ws >= gfwa_bwd_workspace_size(desc); need not be initialised.
@@ -185,20 +191,20 @@ gfwa_status_t gfwa_fwd(const gfwa_attn_desc_t* desc, const void* Q, const void* 
  * tensor-core gfwa_bwd clears it, so only the latest prepared descriptor is
  * honoured: a gfwa_bwd with another descriptor (or after an intervening
  * backward) zeroes its own accumulator, and interleaving shapes on one
- * workspace is safe.  When O_f32 is given, the PV product runs with P and V in
- * fp16 (reading C-23: the fp32 O that D is taken from then carries 8x less
+ * workspace is safe.  When O_lo is given, the PV product runs with P and V in
+ * fp16 (reading C-23: the O + O_lo that D is taken from then carries 8x less
  * P rounding than with bf16 P); V must then lie in the fp16 range
  * (|v| < 65504; larger values overflow to inf).  Calls sharing a workspace
  * must be ordered on one stream.  Other paths: exactly gfwa_fwd.  Errors as
  * gfwa_fwd, plus WORKSPACE.
  */
 gfwa_status_t gfwa_fwd_train(const gfwa_attn_desc_t* desc, const void* Q, const void* K, const void* V,
-                             const float* U, void* O, float* O_f32, float* LSE, void* bwd_ws,
+                             const float* U, void* O, void* O_lo, float* LSE, void* bwd_ws,
                              size_t bwd_ws_bytes, gfwa_stream_t stream);
 
 size_t gfwa_bwd_workspace_size(const gfwa_attn_desc_t* desc);
 gfwa_status_t gfwa_bwd(const gfwa_attn_desc_t* desc, const void* Q, const void* K, const void* V,
-                       const float* U, const void* O, const float* O_f32, const float* LSE,
+                       const float* U, const void* O, const void* O_lo, const float* LSE,
                        const void* dO, void* dQ, void* dK, void* dV, float* dU, float* dalpha,
                        const double* dalpha_carry, void* ws, size_t ws_bytes, gfwa_stream_t stream);
 

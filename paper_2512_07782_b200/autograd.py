@@ -2,7 +2,7 @@
 
 ``gated_fwa(Q, K, V, h, beta, w)`` runs, on the current CUDA stream,
   gfwa_gate_prefix  (Alg. 1)          -> U
-  gfwa_fwd          (Alg. 2)          -> O, LSE, O_f32
+  gfwa_fwd          (Alg. 2)          -> O, LSE, O_lo
 and its backward runs
   gfwa_bwd          (Alg. E.2, C-12)  -> dQ, dK, dV, dU
   gfwa_gate_prefix_bwd (P:276, Eq. 9) -> dh, dbeta
@@ -20,15 +20,15 @@ class GatedFWAFunction(torch.autograd.Function):
     def forward(ctx, Q, K, V, h, beta, w: int, eps: float, scale):
         U = B.gfwa_gate_prefix(h, beta, eps)
         # a backward will follow: let the forward zero its dQ accumulator (gfwa_fwd_train)
-        O, LSE, O_f32 = B.gfwa_fwd(Q, K, V, U, w, scale, want_o_f32=True, prepare_bwd=any(ctx.needs_input_grad))
-        ctx.save_for_backward(Q, K, V, h, beta, U, O, LSE, O_f32)
+        O, LSE, O_lo = B.gfwa_fwd(Q, K, V, U, w, scale, want_o_lo=True, prepare_bwd=any(ctx.needs_input_grad))
+        ctx.save_for_backward(Q, K, V, h, beta, U, O, LSE, O_lo)
         ctx.w, ctx.eps, ctx.scale = w, eps, scale
         return O
 
     @staticmethod
     def backward(ctx, dO):
-        Q, K, V, h, beta, U, O, LSE, O_f32 = ctx.saved_tensors
-        dQ, dK, dV, dU, _ = B.gfwa_bwd(Q, K, V, U, O, LSE, dO.contiguous(), ctx.w, ctx.scale, O_f32=O_f32,
+        Q, K, V, h, beta, U, O, LSE, O_lo = ctx.saved_tensors
+        dQ, dK, dV, dU, _ = B.gfwa_bwd(Q, K, V, U, O, LSE, dO.contiguous(), ctx.w, ctx.scale, O_lo=O_lo,
                                        want_dalpha=False)
         _, dh, dbeta = B.gfwa_gate_prefix_bwd(dU, h, beta, ctx.eps, want_dalpha=False)
         return dQ, dK, dV, dh, dbeta, None, None, None

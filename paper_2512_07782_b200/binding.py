@@ -288,11 +288,13 @@ def gfwa_gate_prefix_bwd(dU: torch.Tensor, h: torch.Tensor | None = None, beta: 
 # --------------------------------------------------------------------------- attention
 
 
-def gfwa_fwd(Q, K, V, U, w: int, scale: float | None = None, want_o_f32: bool = False, out=None, out_f32=None,
+def gfwa_fwd(Q, K, V, U, w: int, scale: float | None = None, want_o_lo: bool = False, out=None, out_lo=None,
              prepare_bwd: bool = False):
-    """O [B,Nq,H,d], LSE [B,H,Nq] (+ O_f32) per Eq. 12 / Alg. 2.
-    out / out_f32: caller tensors (views allowed) receiving O and O_f32; O_f32
-    must share O's element strides (the ABI's one stride set).
+    """O [B,Nq,H,d], LSE [B,H,Nq] (+ O_lo) per Eq. 12 / Alg. 2.
+    O_lo (bf16 only; None for fp32, whose O is exact): the bf16 residual of the
+    output cast, bf16(O_exact - O), for the backward's D (reading C-12).
+    out / out_lo: caller tensors (views allowed) receiving O and O_lo; O_lo must
+    share O's element strides (the ABI's one stride set).
     prepare_bwd: gfwa_fwd_train on the workspace gfwa_bwd will use (the forward
     zeroes the backward's dQ accumulator; the next gfwa_bwd skips that pass)."""
     lib = load()
@@ -300,36 +302,38 @@ def gfwa_fwd(Q, K, V, U, w: int, scale: float | None = None, want_o_f32: bool = 
     U = U.contiguous()
     B, Nq, H, d = Q.shape
     O = out if out is not None else torch.empty(B, Nq, H, d, dtype=Q.dtype, device=Q.device)
-    if out_f32 is not None:
-        if out_f32.stride() != O.stride() or out_f32.dtype != torch.float32:
-            raise GfwaError("out_f32 must be fp32 with the strides of O")
-        O_f32 = out_f32
-    else:
-        O_f32 = torch.empty_strided(O.shape, O.stride(), dtype=torch.float32, device=Q.device) if want_o_f32 else None
+    O_lo = None
+    if Q.dtype == torch.bfloat16:
+        if out_lo is not None:
+            if out_lo.stride() != O.stride() or out_lo.dtype != torch.bfloat16:
+                raise GfwaError("out_lo must be bf16 with the strides of O")
+            O_lo = out_lo
+        elif want_o_lo:
+            O_lo = torch.empty_strided(O.shape, O.stride(), dtype=torch.bfloat16, device=Q.device)
     LSE = torch.empty(B, H, Nq, dtype=torch.float32, device=Q.device)
     dsc = make_desc(Q, K, V, O, w, scale)
     if prepare_bwd:
         nbytes = lib.gfwa_bwd_workspace_size(ctypes.byref(dsc))
         ws = workspace(nbytes, Q.device, "bwd")  # the tensor gfwa_bwd below takes
-        st = lib.gfwa_fwd_train(ctypes.byref(dsc), _ptr(Q), _ptr(K), _ptr(V), _ptr(U), _ptr(O), _ptr(O_f32),
+        st = lib.gfwa_fwd_train(ctypes.byref(dsc), _ptr(Q), _ptr(K), _ptr(V), _ptr(U), _ptr(O), _ptr(O_lo),
                                 _ptr(LSE), _ptr(ws), nbytes, _stream(Q.device))
         _check(st, "gfwa_fwd_train")
-        return O, LSE, O_f32
-    st = lib.gfwa_fwd(ctypes.byref(dsc), _ptr(Q), _ptr(K), _ptr(V), _ptr(U), _ptr(O), _ptr(O_f32), _ptr(LSE),
+        return O, LSE, O_lo
+    st = lib.gfwa_fwd(ctypes.byref(dsc), _ptr(Q), _ptr(K), _ptr(V), _ptr(U), _ptr(O), _ptr(O_lo), _ptr(LSE),
                       _stream(Q.device))
     _check(st, "gfwa_fwd")
-    return O, LSE, O_f32
+    return O, LSE, O_lo
 
 
-def gfwa_bwd(Q, K, V, U, O, LSE, dO, w: int, scale: float | None = None, O_f32=None, want_dalpha: bool = True,
+def gfwa_bwd(Q, K, V, U, O, LSE, dO, w: int, scale: float | None = None, O_lo=None, want_dalpha: bool = True,
              dalpha_carry=None):
-    """dQ, dK, dV, dU (+ dalpha) per Alg. E.2."""
+    """dQ, dK, dV, dU (+ dalpha) per Alg. E.2; D = rowsum((O + O_lo) dO)."""
     lib = load()
     _need_cuda(Q, K, V, U, O, LSE, dO)
-    if dO.stride() != O.stride() or (O_f32 is not None and O_f32.stride() != O.stride()):
-        # O, dO and O_f32 share one (b, n, h) stride set in the ABI
+    if dO.stride() != O.stride() or (O_lo is not None and O_lo.stride() != O.stride()):
+        # O, dO and O_lo share one (b, n, h) stride set in the ABI
         O, dO = O.contiguous(), dO.contiguous()
-        O_f32 = None if O_f32 is None else O_f32.contiguous()
+        O_lo = None if O_lo is None else O_lo.contiguous()
     B, Nq, H, d = Q.shape
     Nkv = K.shape[1]
     dev = Q.device
@@ -343,7 +347,7 @@ def gfwa_bwd(Q, K, V, U, O, LSE, dO, w: int, scale: float | None = None, O_f32=N
     dsc = make_desc(Q, K, V, O, w, scale)
     nbytes = lib.gfwa_bwd_workspace_size(ctypes.byref(dsc))
     ws = workspace(nbytes, dev, "bwd")
-    st = lib.gfwa_bwd(ctypes.byref(dsc), _ptr(Q), _ptr(K), _ptr(V), _ptr(U.contiguous()), _ptr(O), _ptr(O_f32),
+    st = lib.gfwa_bwd(ctypes.byref(dsc), _ptr(Q), _ptr(K), _ptr(V), _ptr(U.contiguous()), _ptr(O), _ptr(O_lo),
                       _ptr(LSE), _ptr(dO), _ptr(dQ), _ptr(dK), _ptr(dV), _ptr(dU), _ptr(dalpha),
                       _ptr(dalpha_carry), _ptr(ws), nbytes, _stream(dev))
     _check(st, "gfwa_bwd")

@@ -17,11 +17,11 @@ struct AttnParams {
     const void* V;
     const float* U;  // [B,H,Nkv]
     void* O;
-    float* O_f32;
+    void* O_lo;         // bf16 residual of the output cast, bf16(O_exact - O) (nullable; C-12)
     float* LSE;      // [B,H,Nq]
     // backward
     const void* dO;
-    const float* Ofp;   // fp32 O for D (may be null -> use O)
+    const void* Olo;    // that residual for D = rowsum((O + O_lo) dO) (may be null -> use O)
     void* dQ;
     void* dK;
     void* dV;

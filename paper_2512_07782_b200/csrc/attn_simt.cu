@@ -134,12 +134,13 @@ __global__ void __launch_bounds__(kThreads) fwd_simt_kernel(AttnParams p) {
         if (t >= p.Nq) continue;
         const float inv = 1.f / l[i];
         T* orow = (T*)p.O + off3(p.os, b, t, h);
-        float* frow = p.O_f32 ? p.O_f32 + off3(p.os, b, t, h) : nullptr;
+        T* lrow = p.O_lo ? (T*)p.O_lo + off3(p.os, b, t, h) : nullptr;
 #pragma unroll
         for (int x = 0; x < D / 32; ++x) {
             const float v = o[i][x] * inv;
-            orow[lane + 32 * x] = from_f32<T>(v);
-            if (frow) frow[lane + 32 * x] = v;
+            const T hi = from_f32<T>(v);
+            orow[lane + 32 * x] = hi;
+            if (lrow) lrow[lane + 32 * x] = from_f32<T>(v - to_f32<T>(hi));  // residual of the cast (C-12)
         }
         if (lane == 0) p.LSE[(b * p.H + h) * p.Nq + t] = (m[i] + log2f(l[i])) * kLn2;
     }
@@ -148,7 +149,7 @@ __global__ void __launch_bounds__(kThreads) fwd_simt_kernel(AttnParams p) {
 // --------------------------------------------------------- backward: D = rowsum(O dO)
 template <typename T>
 __global__ void __launch_bounds__(256) bwd_pre_kernel(AttnParams p) {
-    // one warp per (b, t, h) row; Alg. E.2 l.7, O from O_f32 when given (C-12)
+    // one warp per (b, t, h) row; Alg. E.2 l.7, O + O_lo when given (C-12)
     const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     const int64_t total = p.B * p.Nq * p.H;
@@ -157,9 +158,10 @@ __global__ void __launch_bounds__(256) bwd_pre_kernel(AttnParams p) {
     const int64_t oo = off3(p.os, b, t, h);
     const T* dO = (const T*)p.dO + oo;
     float acc = 0.f;
-    if (p.Ofp) {
-        const float* o = p.Ofp + oo;
-        for (int c = lane; c < p.d; c += 32) acc = fmaf(o[c], to_f32<T>(dO[c]), acc);
+    if (p.Olo) {
+        const T* o = (const T*)p.O + oo;
+        const T* ol = (const T*)p.Olo + oo;
+        for (int c = lane; c < p.d; c += 32) acc = fmaf(to_f32<T>(o[c]) + to_f32<T>(ol[c]), to_f32<T>(dO[c]), acc);
     } else {
         const T* o = (const T*)p.O + oo;
         for (int c = lane; c < p.d; c += 32) acc = fmaf(to_f32<T>(o[c]), to_f32<T>(dO[c]), acc);

@@ -491,7 +491,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 constexpr size_t kSmemBytes = 1024 + 2 * kKV + NQS * 2 * kQT + 2 * kDS + kDQ + sizeof(Bars) + 16;
 
-// dQacc zeroing fused with D = rowsum(O dO)  (Alg. E.2 l.7; O from O_f32, C-12)
+// dQacc zeroing fused with D = rowsum(O dO)  (Alg. E.2 l.7; O + O_lo, C-12)
 __global__ void __launch_bounds__(256) bwd_tc_pre_kernel(AttnParams p) {
     const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
@@ -505,24 +505,29 @@ __global__ void __launch_bounds__(256) bwd_tc_pre_kernel(AttnParams p) {
     const uint2 g2 = *reinterpret_cast<const uint2*>(dO + c);
     const float2 g01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&g2.x));
     const float2 g23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&g2.y));
-    if (p.Ofp) {
-        const float4 o = *reinterpret_cast<const float4*>(p.Ofp + oo + c);
-        acc = o.x * g01.x + o.y * g01.y + o.z * g23.x + o.w * g23.y;
-    } else {
-        const uint2 o2 = *reinterpret_cast<const uint2*>((const __nv_bfloat16*)p.O + oo + c);
-        const float2 o01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&o2.x));
-        const float2 o23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&o2.y));
-        acc = o01.x * g01.x + o01.y * g01.y + o23.x * g23.x + o23.y * g23.y;
+    const uint2 o2 = *reinterpret_cast<const uint2*>((const __nv_bfloat16*)p.O + oo + c);
+    float2 o01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&o2.x));
+    float2 o23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&o2.y));
+    if (p.Olo) {
+        const uint2 l2 = *reinterpret_cast<const uint2*>((const __nv_bfloat16*)p.Olo + oo + c);
+        const float2 l01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&l2.x));
+        const float2 l23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&l2.y));
+        o01.x += l01.x;
+        o01.y += l01.y;
+        o23.x += l23.x;
+        o23.y += l23.y;
     }
+    acc = o01.x * g01.x + o01.y * g01.y + o23.x * g23.x + o23.y * g23.y;
     acc = warp_sum(acc);
     if (lane == 0) p.Dv[(b * p.H + h) * p.Nq + t] = acc;
     if (!(p.token && *p.token == p.token_val))  // not already zeroed by gfwa_fwd_train
         *reinterpret_cast<float4*>(p.dQacc + ((b * p.Nq + t) * p.H + h) * D + c) = make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
-// D = rowsum(O_f32 dO) and zeroing of dQacc, fast path for contiguous O_f32 / dO:
+// D = rowsum((O + O_lo) dO) and zeroing of dQacc, fast path for contiguous O, O_lo, dO:
 // a warp per row (grid-stride, 32-bit index math), the zeroing as flat 32-byte stores
-__global__ void __launch_bounds__(256) bwd_tc_pre_flat_kernel(const float* __restrict__ of,
+__global__ void __launch_bounds__(256) bwd_tc_pre_flat_kernel(const __nv_bfloat16* __restrict__ o,
+                                                             const __nv_bfloat16* __restrict__ olo,
                                                              const __nv_bfloat16* __restrict__ dO,
                                                              float* __restrict__ Dv, float* __restrict__ acc,
                                                              uint32_t rows, uint32_t H, uint32_t Nq,
@@ -535,12 +540,16 @@ __global__ void __launch_bounds__(256) bwd_tc_pre_flat_kernel(const float* __res
     const bool zero = !(token && *token == token_val);
     // dU accumulates red.adds in the main kernel: zero it here (no separate memset launch)
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_du; i += gridDim.x * blockDim.x) dU[i] = 0.f;
+    auto f4 = [](uint2 v) {
+        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.x));
+        const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.y));
+        return make_float4(a.x, a.y, b.x, b.y);
+    };
     for (uint32_t row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < rows; row += nw) {
-        const float4 o = __ldcs(reinterpret_cast<const float4*>(of + (size_t)row * D) + lane);
-        const uint2 g2 = __ldcs(reinterpret_cast<const uint2*>(dO + (size_t)row * D) + lane);
-        const float2 g01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&g2.x));
-        const float2 g23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&g2.y));
-        float a = o.x * g01.x + o.y * g01.y + o.z * g23.x + o.w * g23.y;
+        const float4 oh = f4(__ldcs(reinterpret_cast<const uint2*>(o + (size_t)row * D) + lane));
+        const float4 ol = f4(__ldcs(reinterpret_cast<const uint2*>(olo + (size_t)row * D) + lane));
+        const float4 g = f4(__ldcs(reinterpret_cast<const uint2*>(dO + (size_t)row * D) + lane));
+        float a = (oh.x + ol.x) * g.x + (oh.y + ol.y) * g.y + (oh.z + ol.z) * g.z + (oh.w + ol.w) * g.w;
         a = warp_sum(a);
         if (lane == 0) {
             const uint32_t hh = row % H, bt = row / H, t = bt % Nq, b = bt / Nq;
@@ -609,11 +618,11 @@ gfwa_status_t tc_bwd(const AttnParams& pin, cudaStream_t st, void* ws) {
     int n_sm = 148, dev = 0;  // per call: the attribute is per device
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
     const int64_t n_du = p.B * p.H * p.Nkv;
-    const bool o_flat = p.Ofp && p.os[2] == D && p.os[1] == p.H * D && p.os[0] == p.Nq * p.H * D &&
+    const bool o_flat = p.Olo && p.os[2] == D && p.os[1] == p.H * D && p.os[0] == p.Nq * p.H * D &&
                         rows < ((int64_t)1 << 31) && n_du < ((int64_t)1 << 31);
     if (o_flat) {
         bwd_tc_pre_flat_kernel<<<(unsigned)min64((rows + 7) / 8, (int64_t)n_sm * 16), 256, 0, st>>>(
-            p.Ofp, (const __nv_bfloat16*)p.dO, p.Dv, p.dQacc, (uint32_t)rows, (uint32_t)p.H, (uint32_t)p.Nq, p.dU,
+            (const __nv_bfloat16*)p.O, (const __nv_bfloat16*)p.Olo, (const __nv_bfloat16*)p.dO, p.Dv, p.dQacc, (uint32_t)rows, (uint32_t)p.H, (uint32_t)p.Nq, p.dU,
             (uint32_t)n_du, p.token, p.token_val);
     } else {
         if (gfwa_status_t s = check_launch(cudaMemsetAsync(p.dU, 0, (size_t)n_du * sizeof(float), st))) return s;

@@ -1,87 +1,119 @@
 // attn_tc_fwd.cu -- GatedFWA forward on the 5th-generation tensor cores
 // (sm_100a): Alg. 2 re-designed for tcgen05/TMEM/TMA.
 //
-// One CTA owns one 128-row query tile of one (b, h) and streams the 128-key
-// K/V tiles of its window, diagonal first (descending j).  TWO CTAs share an
-// SM (98 KB smem, 256 TMEM columns each): while one runs its softmax the other's
-// MMAs keep the tensor core busy, and one CTA's prologue (Q, K loads, first S)
-// and epilogue overlap the other's main loop -- without a persistent scheduler.
-//   warp 5      TMA producer: Q once, then K_j, V_j (one stage each: K_{j+1}
-//               streams in during the softmax of step j, V_j during the S MMA);
-//               128B swizzle, OOB rows zero-filled -> ragged tails for free
-//   warp 4      MMA issuer (one elected lane): S = Q K_j^T (SS, fp32 in TMEM)
-//               and O += P V_j (TS: bf16 P read from TMEM); tcgen05.commit
-//               tracks all earlier MMAs, so S_full of step n also certifies
-//               that PV of step n-1 has landed.
-//   warps 0-3   softmax, one thread per query row holding its 128 S values in
-//               registers (four tcgen05.ld, one wait; setmaxnreg gives this
-//               warpgroup 224 registers): add the gate bias as an
-//               outer difference of two u vectors (nothing N x w is
-//               materialised), window-mask only on diagonal / window-edge tiles
-//               (a per-row column range turned into bit masks), online
-//               softmax in fp32 with packed f32x2 FMA/ADD, 3-input max and a lazy
-//               rescale (the reference max moves only when it grows by > 2^8),
-//               part of exp2 on the FMA pipe, bf16 P back over the S columns;
-//               epilogue O / l staged in smem with the 128B swizzle and written
-//               by TMA stores, LSE = m + ln l.
-//   warps 6-7   training forward (O_f32 requested): convert each V tile to fp16
-//               in place once it lands, so the PV product runs with P in fp16
-//               (reading C-23: the fp32 O that the backward's D = rowsum(O dO)
-//               is taken from carries 8x less P rounding than with bf16 P);
-//               otherwise idle (they complete the second warpgroup for setmaxnreg)
-// TMEM (256 columns per CTA): S [0,128), O [128,256) x 128 lanes.
+// Persistent, warp-specialised, one CTA per SM.  A work item is a PAIR of
+// 128-row query tiles (A = rows [r0, r0+128), B = [r0+128, r0+256)) of one
+// (b, h); both share every 128-key K/V tile of their (overlapping) windows, so
+// each K/V tile is staged once per 256 query rows.  The key tiles of the item
+// are walked diagonal-first (descending j); the first one only feeds B (its
+// diagonal), the last only A (its window edge).
+//
+//   warp 13     TMA producer: Q_A, Q_B per item (a slot is refilled as soon as
+//               the tile's last S MMA has read it), K_j and V_j through one ring
+//               of three tile slots (evict-last: re-read by ~w/128 neighbouring
+//               items);
+//               gfwa_fwd_train: also zeroes the item's rows of the backward's dQ
+//               accumulator with coalesced stores (the lanes are idle otherwise)
+//   warp 12     MMA issuer (one elected lane), ping-pong over the two tiles:
+//                 O_A += P_A V_{n-1};  S_A = Q_A K_n^T;
+//                 O_B += P_B V_{n-1};  S_B = Q_B K_n^T
+//               (P lives over its S columns, so a tile's next S is issued after
+//               its PV; while the tensor core runs one tile's pair the other
+//               tile's softmax runs)
+//   warps 0-3   softmax of tile A, warps 4-7 of tile B: one thread per query row
+//               holding its 128 S values in registers (one tcgen05.ld wait), the
+//               gate bias as an outer difference of two u vectors (P:377-380,
+//               nothing N x w is materialised), window masks only on diagonal /
+//               edge tiles with fully masked 32-key chunks skipped
+//               (no exponentials), online softmax in fp32 with a lazy rescale
+//               (the reference max moves only when it grows by > 2^8; the rare
+//               rescale of O runs in TMEM by the row's own thread), 16-bit P
+//               written back over the S columns.  LSE = m + ln l.
+//   warps 8-11  epilogue: O / l -> bf16 O (staged in a 32 KB buffer) and, in
+//               the training forward, its bf16 residual O_lo = bf16(O/l - O)
+//               (staged in a 32 KB buffer; O + O_lo carries O to ~2^-17, which
+//               is what the backward's D = rowsum(O dO) needs, reading C-12),
+//               written by TMA stores
+//   warps 14-15 training forward: the in-place fp16 conversion of every V tile
+//               (reading C-23: P and V in fp16 for the PV product, so the fp32 O
+//               that D = rowsum(O dO) is taken from carries 8x less P rounding
+//               than with bf16 P)
+// TMEM (512 columns): S_A [0,128), S_B [128,256), O_A [256,384), O_B [384,512).
 // Key tiles outside every row's window are never loaded.
-#include <vector>
+#include "attn_common.cuh"
+#include "sm100.cuh"
+#include "tma_host.cuh"
 
 #ifndef GFWA_FWD_POLY
 #define GFWA_FWD_POLY 0
 #endif
-
-#include "attn_common.cuh"
-#include "sm100.cuh"
-#include "tma_host.cuh"
+#ifndef GFWA_FWD_TRACE
+#define GFWA_FWD_TRACE 0  // diagnostics build only: clock64 stamps per role into a device array
+#endif
 
 namespace gfwa {
 namespace {
 
 using namespace sm100;
 
-constexpr int BM = 128;          // query rows per tile
-constexpr int BN = 128;          // keys per tile
-constexpr int D = 128;           // head dim
-constexpr uint32_t kTileBytes = BM * D * 2;  // 32 KB bf16 tile
-constexpr uint32_t kZeroBytes = 64 * 32 * 4;   // 8 KB: one {32 d, 64 rows} fp32 box of zeros
-constexpr int kThreads = 256;    // softmax warpgroup + (MMA, TMA, 2 idle)
-constexpr int kMmaWarp = 4, kTmaWarp = 5;
-constexpr int kSoftmaxRegs = 224;  // CTA pool at (256, 2): 256 x 128; 128 x 224 + 128 x 32 fits it
-constexpr int kOtherRegs = 32;
+constexpr int BM = 128;  // query rows per tile (two tiles per item)
+constexpr int BN = 128;  // keys per tile
+constexpr int D = 128;   // head dim
+constexpr uint32_t kTile = BM * D * 2;  // 32 KB bf16 tile
+// 4 full warpgroups (setmaxnreg acts per warpgroup; the CTA register pool is
+// 512 x 128 = 64K): softmax A, softmax B, epilogue, {MMA, TMA, 2 V-convert warps}
+constexpr int kThreads = 512;
+constexpr int kEpiWarp0 = 8, kMmaWarp = 12, kTmaWarp = 13, kCvtWarp0 = 14;
+constexpr int kSoftmaxRegs = 184, kEpiRegs = 72, kOtherRegs = 72;  // 256*184 + 128*72 + 128*72 = 65536
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 constexpr int kPolyPairs = GFWA_FWD_POLY;  // of every 4 column pairs, how many use exp2_poly2
+
+// dynamic shared memory (1024-aligned base)
+constexpr uint32_t kOffQ = 0;                    // Q_A, Q_B
+constexpr uint32_t kOffKV = 2 * kTile;           // one K/V ring of 3 tile slots: K_0 V_0 K_1 V_1 ...
+constexpr int kSlots = 3;
+constexpr uint32_t kOffE = 5 * kTile;            // 32 KB staging of the O tile, 32 KB of the O_lo tile
+constexpr uint32_t kOffNbk = 7 * kTile;          // [2 tiles][128] fp32 key biases
+constexpr uint32_t kOffLinv = kOffNbk + 2 * BN * 4;  // [2 tiles][128] 1/l
+constexpr uint32_t kOffBars = kOffLinv + 2 * BM * 4;
+constexpr size_t kSmemBytes = kOffBars + 256;
+
+struct __align__(8) Bars {
+    uint64_t q_full[2], q_empty[2];
+    // a slot alternates K and V fills: each kind completes its own barrier, so a
+    // consumer of one kind never sees a phase of the other (parity aliasing)
+    uint64_t k_full[kSlots], v_full[kSlots], kv_empty[kSlots], v_ready[kSlots];
+    uint64_t s_full[2], p_ready[2], o_full[2], o_free[2], l_ready[2];
+    uint32_t tmem;
+};
+static_assert(sizeof(Bars) <= 256, "barrier block");
 
 struct TcFwdParams {
     const float* U;
     float* LSE;
-    int64_t Nq, Nkv, h0, H;
+    int64_t Nq, Nkv, h0, H, B;
     int w;
-    int store_f32;
-    float* zero_acc;   // gfwa_fwd_train: the dQ accumulator [B, Nq, H, d] whose rows of this tile are zeroed
+    int store_lo;
+    int n_items, n_pairs;
+    float* zero_acc;  // gfwa_fwd_train: the dQ accumulator [B, Nq, H, d] whose item rows are zeroed
     unsigned long long* token;
     unsigned long long token_val;
-    float sl2;         // scale * log2(e)
-    long long* trace;  // diagnostics only (GFWA_TRACE_FWD): per-CTA clock64 stamps
+    float sl2;  // scale * log2(e)
 };
 
-#define GFWA_TR(slot)                                                                                         \
-    do {                                                                                                      \
-        if (p.trace)                                                                                          \
-            p.trace[((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 64 + (slot)] = clock64(); \
+#if GFWA_FWD_TRACE
+constexpr int kTrMax = 512;  // stamps per (CTA, role)
+__device__ long long g_fwd_trace[148 * 8 * kTrMax];
+#define FTR(role, k)                                                                          \
+    do {                                                                                      \
+        if ((k) < kTrMax && blockIdx.x < 148)                                                 \
+            g_fwd_trace[((int)blockIdx.x * 8 + (role)) * kTrMax + (k)] = clock64();          \
     } while (0)
-
-struct __align__(8) Bars {
-    uint64_t q_full, k_full, k_empty, v_full, v_empty, v_conv, s_full, p_ready, o_full;
-};
-
-__device__ __forceinline__ int64_t kv_tile_lo(int64_t g_lo, int w) { return max64(0, g_lo - w + 1) / BN; }
+#else
+#define FTR(role, k) \
+    do {             \
+    } while (0)
+#endif
 
 // bits [lo, hi] (inclusive, clipped to the 32-bit word starting at column base)
 __device__ __forceinline__ uint32_t range_bits(int lo, int hi, int base) {
@@ -91,51 +123,81 @@ __device__ __forceinline__ uint32_t range_bits(int lo, int hi, int base) {
     return upto_z & ~below_a;
 }
 
-template <bool kF16P>  // training forward: P, V in fp16 for the PV product (reading C-23)
-__global__ void __launch_bounds__(kThreads, 2)
-    fwd_tc_kernel(const __grid_constant__ CUtensorMap mzq, const __grid_constant__ CUtensorMap mq,
-                  const __grid_constant__ CUtensorMap mk,
-                  const __grid_constant__ CUtensorMap mv, const __grid_constant__ CUtensorMap mo,
-                  const __grid_constant__ CUtensorMap mo32, const TcFwdParams p) {
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    uint8_t* Qs = smem;
-    uint8_t* Ks = Qs + kTileBytes;
-    uint8_t* Vs = Ks + kTileBytes;
-    __shared__ __align__(16) float s_nbk[BN];  // negated key bias -(u_k - uref) log2e
-    uint8_t* Zs = Vs + kTileBytes;  // 8 KB of zeros (gfwa_fwd_train)
-    Bars* bars = (Bars*)(Zs + kZeroBytes);
-    uint32_t* tmem_sh = (uint32_t*)(bars + 1);
+// The geometry of one work item: rows of tiles A and B, their key-tile ranges
+// (Alg. 2 l.7-9 with key positions g = t + h0), and the union walked by the item.
+// 32-bit positions (N_kv < 2^31 is checked on the host); per-tile fields are
+// read with explicit selects so nothing lands in local memory.
+struct Item {
+    int b, h, r0;
+    int glo0, glo1, ghi0, ghi1;  // key positions of the tile's first / last valid query row
+    int jlo0, jlo1, jhi0, jhi1;  // key tiles needed by tile X (empty tile: jlo > jhi)
+    int jtop;                    // first key tile of the walk (descending)
+    int nsteps;
+    bool has0, has1;
+    __device__ __forceinline__ bool has(int x) const { return x ? has1 : has0; }
+    __device__ __forceinline__ int jlo(int x) const { return x ? jlo1 : jlo0; }
+    __device__ __forceinline__ int jhi(int x) const { return x ? jhi1 : jhi0; }
+    __device__ __forceinline__ int glo(int x) const { return x ? glo1 : glo0; }
+    __device__ __forceinline__ int ghi(int x) const { return x ? ghi1 : ghi0; }
+    __device__ __forceinline__ bool uses(int x, int j) const { return has(x) && j >= jlo(x) && j <= jhi(x); }
+};
 
-    const int warp = threadIdx.x >> 5;
-    if (threadIdx.x == 0) {
-        GFWA_TR(0);
-        if (p.trace) {
-            uint32_t smid;
-            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-            p.trace[((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 64 + 63] = smid;
-        }
+__device__ __forceinline__ Item make_item(const TcFwdParams& p, int idx) {
+    Item it;
+    const int pair = idx % p.n_pairs;
+    const int bh = idx / p.n_pairs;
+    it.h = bh % (int)p.H;
+    it.b = bh / (int)p.H;
+    it.r0 = pair * 2 * BM;
+    const int Nq = (int)p.Nq, h0 = (int)p.h0;
+    it.has0 = it.r0 < Nq;
+    it.has1 = it.r0 + BM < Nq;
+    it.glo0 = it.r0 + h0;
+    it.glo1 = it.r0 + BM + h0;
+    it.ghi0 = min(it.r0 + BM - 1, Nq - 1) + h0;
+    it.ghi1 = min(it.r0 + 2 * BM - 1, Nq - 1) + h0;
+    it.jlo0 = max(0, it.glo0 - p.w + 1) / BN;
+    it.jlo1 = max(0, it.glo1 - p.w + 1) / BN;
+    it.jhi0 = it.ghi0 / BN;
+    it.jhi1 = it.ghi1 / BN;
+    if (!it.has1) {
+        it.jlo1 = 1;
+        it.jhi1 = 0;
     }
-    const int64_t b = blockIdx.z, h = blockIdx.y;
-    const int64_t r0 = (int64_t)blockIdx.x * BM;
-    // Alg. 2 l.7-9: key positions g = t + h0
-    const int64_t glo = r0 + p.h0, ghi = min64(r0 + BM - 1, p.Nq - 1) + p.h0;
-    const int64_t jlo = kv_tile_lo(glo, p.w), jhi = ghi / BN;
+    it.jtop = it.has1 ? it.jhi1 : it.jhi0;
+    it.nsteps = it.jtop - it.jlo0 + 1;
+    return it;
+}
 
+template <bool kF16P>  // training forward (O_lo wanted): P, V in fp16 for the PV product (reading C-23)
+__global__ void __launch_bounds__(kThreads, 1)
+    fwd_tc_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
+                  const __grid_constant__ CUtensorMap mv, const __grid_constant__ CUtensorMap mo,
+                  const __grid_constant__ CUtensorMap mol, const TcFwdParams p) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    Bars* bars = (Bars*)(smem + kOffBars);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
-        mbar_init(&bars->q_full, 1);
-        mbar_init(&bars->k_full, 1);
-        mbar_init(&bars->k_empty, 1);
-        mbar_init(&bars->v_full, 1);
-        mbar_init(&bars->v_empty, 1);
-        mbar_init(&bars->v_conv, 2);
-        mbar_init(&bars->s_full, 1);
-        mbar_init(&bars->p_ready, 4);
-        mbar_init(&bars->o_full, 1);
+        if (smem_u32(smem) & 1023u) __trap();  // the 128B-swizzle tiles need a 1024-aligned base
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&bars->q_full[i], 1);
+            mbar_init(&bars->q_empty[i], 1);  // the tile's last S MMA
+            mbar_init(&bars->s_full[i], 1);
+            mbar_init(&bars->p_ready[i], 4);
+            mbar_init(&bars->o_full[i], 1);
+            mbar_init(&bars->o_free[i], 4);
+            mbar_init(&bars->l_ready[i], 4);
+        }
+        for (int i = 0; i < kSlots; ++i) {
+            mbar_init(&bars->k_full[i], 1);
+            mbar_init(&bars->v_full[i], 1);
+            mbar_init(&bars->kv_empty[i], 1);
+            mbar_init(&bars->v_ready[i], 2);  // the two convert warps
+        }
         fence_barrier_init();
     }
     if (warp == kMmaWarp) {
-        tmem_alloc(tmem_sh, 256);
+        tmem_alloc(&bars->tmem, 512);
         tmem_relinquish();
     }
     if (warp == kTmaWarp && elect_one()) {
@@ -147,340 +209,439 @@ __global__ void __launch_bounds__(kThreads, 2)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tmem = *tmem_sh;
-    if (threadIdx.x == 0) GFWA_TR(1);
-    // registers move from the MMA/TMA warpgroup to the softmax warpgroup
-    if (warp >= 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kOtherRegs));
+    const uint32_t tmem = bars->tmem;
+
+    if (warp >= kEpiWarp0 && warp < kMmaWarp) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kEpiRegs));
+    } else if (warp >= kMmaWarp) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kOtherRegs));
+    }
 
     if (warp == kTmaWarp) {
-        // ------------------------------------------------ TMA producer
-        if (elect_one()) {
-            const uint64_t pol_kv = policy_evict_last();  // K/V tiles are re-read by ~w/128 neighbours
-            mbar_expect_tx(&bars->q_full, kTileBytes);
-            for (int half = 0; half < 2; ++half)
-                tma_load_4d(Qs + half * (kTileBytes / 2), &mq, &bars->q_full, half * 64, (int)h, (int)r0, (int)b);
-            int k = 0;
-            for (int64_t j = jhi; j >= jlo; --j, ++k) {
-                mbar_wait(&bars->k_empty, (k & 1) ^ 1);
-                mbar_expect_tx(&bars->k_full, kTileBytes);
-                for (int half = 0; half < 2; ++half)
-                    tma_load_4d_hint(Ks + half * (kTileBytes / 2), &mk, &bars->k_full, half * 64, (int)h,
-                                     (int)(j * BN), (int)b, pol_kv);
-                mbar_wait(&bars->v_empty, (k & 1) ^ 1);
-                mbar_expect_tx(&bars->v_full, kTileBytes);
-                for (int half = 0; half < 2; ++half)
-                    tma_load_4d_hint(Vs + half * (kTileBytes / 2), &mv, &bars->v_full, half * 64, (int)h,
-                                     (int)(j * BN), (int)b, pol_kv);
-            }
-        }
-        __syncwarp();
-        if (p.zero_acc) {
-            // gfwa_fwd_train: this idle warp zeroes the tile's 128 rows of the backward's
-            // fp32 dQ accumulator with TMA stores of an 8 KB zero box, while the
-            // other warps finish the tile (the writes overlap the compute)
-            const uint32_t zb = smem_u32(Zs) + (threadIdx.x & 31) * 256;
+        // ------------------------------------------------------------ TMA producer
+        const uint64_t pol_kv = policy_evict_last();
+        uint32_t fq[2] = {0, 0}, kc = 0;
+        for (int idx = blockIdx.x; idx < p.n_items; idx += gridDim.x) {
+            const Item it = make_item(p, idx);
+            bool q_loaded[2] = {false, false};
+            for (int n = 0; n < it.nsteps; ++n) {
+                const int j = it.jtop - n;
 #pragma unroll
-            for (int k2 = 0; k2 < 16; ++k2) sts128(zb + k2 * 16, make_uint4(0u, 0u, 0u, 0u));
-            fence_proxy_async();
-            __syncwarp();
-            if ((threadIdx.x & 31) == 0) {
-                for (int rh = 0; rh < 2; ++rh)
-                    for (int c = 0; c < 4; ++c) tma_store_4d(&mzq, Zs, c * 32, (int)h, (int)(r0 + 64 * rh), (int)b);
-                bulk_commit();
-                if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) *p.token = p.token_val;
-                bulk_wait_read0();  // the zero box stays valid until read
+                for (int x = 1; x >= 0; --x)
+                    if (it.uses(x, j) && !q_loaded[x]) {  // Q_X just before its first key tile
+                        mbar_wait_park(&bars->q_empty[x], (fq[x] & 1) ^ 1);
+                        if (elect_one()) {
+                            mbar_expect_tx(&bars->q_full[x], kTile);
+                            uint8_t* dst = smem + kOffQ + x * kTile;
+                            for (int half = 0; half < 2; ++half)
+                                tma_load_4d(dst + half * (kTile / 2), &mq, &bars->q_full[x], half * 64, it.h,
+                                            it.r0 + x * BM, it.b);
+                        }
+                        __syncwarp();
+                        ++fq[x];
+                        q_loaded[x] = true;
+                    }
+                // K_j then V_j into the next two ring slots (load m = 2g, 2g + 1 of step g)
+#pragma unroll
+                for (int kv = 0; kv < 2; ++kv) {
+                    const uint32_t m = 2 * kc + kv, sl = m % kSlots;
+                    mbar_wait_park(&bars->kv_empty[sl], ((m / kSlots) & 1) ^ 1);
+                    if (kv == 0 && lane == 0) FTR(6, (int)kc);
+                    if (elect_one()) {
+                        uint64_t* full = kv ? &bars->v_full[sl] : &bars->k_full[sl];
+                        mbar_expect_tx(full, kTile);
+                        for (int half = 0; half < 2; ++half)
+                            tma_load_4d_hint(smem + kOffKV + sl * kTile + half * (kTile / 2), kv ? &mv : &mk, full,
+                                             half * 64, it.h, j * BN, it.b, pol_kv);
+                    }
+                    __syncwarp();
+                }
+                ++kc;
             }
-            __syncwarp();
+            if (p.zero_acc) {
+                // gfwa_fwd_train: zero this item's rows of the backward's fp32 dQ
+                // accumulator [B, Nq, H, d] (one 512-byte row per warp store)
+                const int r1 = min(it.r0 + 2 * BM, (int)p.Nq);
+                for (int t = it.r0; t < r1; ++t) {
+                    float4* row = reinterpret_cast<float4*>(
+                        p.zero_acc + (((int64_t)it.b * p.Nq + t) * p.H + it.h) * D);
+                    row[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+            }
         }
+        if (p.zero_acc && blockIdx.x == 0 && lane == 0) *p.token = p.token_val;
     } else if (warp == kMmaWarp) {
-        // ------------------------------------------------ MMA issuer
+        // ------------------------------------------------------------ MMA issuer
         const uint32_t idesc_qk = idesc_bf16(BM, BN, false, false);
-        // training forward: P and V in fp16 (A/B format F16 = 0), reading C-23
         const uint32_t idesc_pv = idesc_bf16(BM, D, false, true) & ~(kF16P ? (63u << 7) : 0u);
-        uint64_t* v_ready = kF16P ? &bars->v_conv : &bars->v_full;
-        const uint32_t qbase = smem_u32(Qs), kbase = smem_u32(Ks), vbase = smem_u32(Vs);
-        mbar_wait(&bars->q_full, 0);
-        int k = 0;
-        for (int64_t j = jhi; j >= jlo; --j, ++k) {
-            if (k > 0) {
-                // O += P(k-1) V(k-1), then V's stage is free
-                mbar_wait(&bars->p_ready, (k - 1) & 1);
-                mbar_wait(v_ready, (k - 1) & 1);
-                tc_fence_after();
-                if (elect_one()) {
+
+        uint32_t kc = 0, cp[2] = {0, 0}, nit[2] = {0, 0}, fq[2] = {0, 0};
+        for (int idx = blockIdx.x; idx < p.n_items; idx += gridDim.x) {
+            const Item it = make_item(p, idx);
+            bool first_pv[2] = {true, true};
+            for (int n = 0; n <= it.nsteps; ++n) {
+                const int j = it.jtop - n;  // this step's key tile (n < nsteps)
+                // this step's K is ring load 2 kc, the previous step's V is load 2 kc - 1
+                const uint32_t mk_ = 2 * kc, mv_ = 2 * kc - 1;
+                const uint32_t sk = mk_ % kSlots, sv = mv_ % kSlots;
+                bool v_waited = false, k_waited = false;
 #pragma unroll
-                    for (int kk = 0; kk < BN / 16; ++kk)
-                        mma_ts(tmem + 128, tmem + 8 * kk, sdesc_sw128(vbase + kk * 2048, kTileBytes / 2, 1024),
-                               idesc_pv, (k > 1 || kk > 0) ? 1u : 0u);
-                    tc_commit(&bars->v_empty);
+                for (int x = 0; x < 2; ++x) {
+                    // O_X += P_X V_{n-1} (Alg. 2 l.16-17)
+                    if (n > 0 && it.uses(x, j + 1)) {
+                        mbar_wait_park(&bars->p_ready[x], cp[x] & 1);
+                        ++cp[x];
+                        if (first_pv[x]) mbar_wait_park(&bars->o_free[x], (nit[x] & 1) ^ 1);  // epilogue read O_X
+                        if (!v_waited) {
+                            // one phase per V fill of the slot: V loads m = 2g + 1 land in slot
+                            // m % 3 every 6 loads, so this is fill m / 6 of the slot
+                            mbar_wait_park(kF16P ? &bars->v_ready[sv] : &bars->v_full[sv], (mv_ / (2 * kSlots)) & 1);
+                            v_waited = true;
+                        }
+                        tc_fence_after();
+                        if (lane == 0) FTR(2, (int)(2 * (cp[0] + cp[1])));
+                        if (elect_one()) {
+                            const uint32_t vb = smem_u32(smem + kOffKV + sv * kTile);
+#pragma unroll
+                            for (int kk = 0; kk < BN / 16; ++kk)
+                                mma_ts(tmem + 256 + 128 * x, tmem + 128 * x + 8 * kk,
+                                       sdesc_sw128(vb + kk * 2048, kTile / 2, 1024), idesc_pv,
+                                       (!first_pv[x] || kk > 0) ? 1u : 0u);
+                            if (j + 1 == it.jlo(x)) tc_commit(&bars->o_full[x]);
+                        }
+                        __syncwarp();
+                        first_pv[x] = false;
+                    }
+                    // S_X = Q_X K_n^T (Alg. 2 l.11-12), over the P just consumed: tcgen05
+                    // MMAs of one thread execute in issue order
+                    if (n < it.nsteps && it.uses(x, j)) {
+                        if (!k_waited) {
+                            mbar_wait_park(&bars->k_full[sk], (mk_ / (2 * kSlots)) & 1);  // K fill m / 6 of the slot
+                            k_waited = true;
+                        }
+                        if (j == it.jhi(x)) mbar_wait_park(&bars->q_full[x], fq[x]++ & 1);
+                        tc_fence_after();
+                        if (lane == 0) FTR(3 + x, (int)kc);
+                        if (elect_one()) {
+                            const uint32_t qb = smem_u32(smem + kOffQ + x * kTile);
+                            const uint32_t kb = smem_u32(smem + kOffKV + sk * kTile);
+#pragma unroll
+                            for (int kk = 0; kk < D / 16; ++kk) {
+                                const uint32_t off = (kk >> 2) * (kTile / 2) + (kk & 3) * 32;
+                                mma_ss(tmem + 128 * x, sdesc_sw128(qb + off, 16, 1024),
+                                       sdesc_sw128(kb + off, 16, 1024), idesc_qk, kk > 0 ? 1u : 0u);
+                            }
+                            tc_commit(&bars->s_full[x]);
+                            if (j == it.jlo(x)) tc_commit(&bars->q_empty[x]);
+                        }
+                        __syncwarp();
+                    }
+                }
+                if (elect_one()) {
+                    if (n < it.nsteps) tc_commit(&bars->kv_empty[sk]);  // both S of this step issued
+                    if (n > 0) tc_commit(&bars->kv_empty[sv]);        // both PV of the previous step issued
                 }
                 __syncwarp();
+                if (n < it.nsteps) ++kc;
             }
-            // S = Q K_j^T (over the P just consumed: tcgen05 MMAs run in issue order)
-            mbar_wait(&bars->k_full, k & 1);
-            if (k < 8 && (threadIdx.x & 31) == 0) GFWA_TR(2 + k);
-            tc_fence_after();
-            if (elect_one()) {
-#pragma unroll
-                for (int kk = 0; kk < D / 16; ++kk) {
-                    const uint32_t off = (kk >> 2) * (kTileBytes / 2) + (kk & 3) * 32;
-                    mma_ss(tmem, sdesc_sw128(qbase + off, 16, 1024), sdesc_sw128(kbase + off, 16, 1024), idesc_qk,
-                           kk > 0 ? 1u : 0u);
-                }
-                tc_commit(&bars->s_full);
-                tc_commit(&bars->k_empty);
-            }
-            __syncwarp();
+            for (int x = 0; x < 2; ++x)
+                if (it.has(x)) ++nit[x];
         }
-        // last PV, then O is final
-        mbar_wait(&bars->p_ready, (k - 1) & 1);
-        mbar_wait(v_ready, (k - 1) & 1);
-        tc_fence_after();
-        if (elect_one()) {
-#pragma unroll
-            for (int kk = 0; kk < BN / 16; ++kk)
-                mma_ts(tmem + 128, tmem + 8 * kk, sdesc_sw128(vbase + kk * 2048, kTileBytes / 2, 1024), idesc_pv,
-                       (k > 1 || kk > 0) ? 1u : 0u);
-            tc_commit(&bars->o_full);
-        }
-        __syncwarp();
-    } else if (kF16P && warp >= 6) {
-        // ------------------------------------------------ V -> fp16 in place (training forward)
-        // 2048 16-byte chunks per tile over 64 threads; the layout (128B swizzle) is
-        // unchanged, only the element encoding: bf16 -> fp32 (exact) -> fp16 (RNE)
-        const uint32_t vb = smem_u32(Vs) + (threadIdx.x - 192) * 16;
-        int k = 0;
-        for (int64_t j = jhi; j >= jlo; --j, ++k) {
-            mbar_wait(&bars->v_full, k & 1);
-#pragma unroll 4
-            for (int c = 0; c < (int)(kTileBytes / 16 / 64); ++c) {
-                const uint32_t a = vb + c * 64 * 16;
-                uint4 x = lds128u(a);
-                x.x = bf16x2_to_f16x2(x.x);
-                x.y = bf16x2_to_f16x2(x.y);
-                x.z = bf16x2_to_f16x2(x.z);
-                x.w = bf16x2_to_f16x2(x.w);
-                sts128(a, x);
-            }
-            fence_proxy_async();  // generic-proxy writes -> visible to the tensor core
-            __syncwarp();
-            if ((threadIdx.x & 31) == 0) mbar_arrive(&bars->v_conv);
-        }
-    } else if (warp < 4) {
-        // ------------------------------------------------ softmax warpgroup
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kSoftmaxRegs));
-        const int r = threadIdx.x & 127;
-        const int64_t t = r0 + r;
-        const bool valid = t < p.Nq;
-        const int64_t g = t + p.h0;
-        const float* Ubh = p.U + (b * p.H + h) * p.Nkv;
-        // Bias in log2 units relative to a per-CTA reference u (reading C-18):
-        // u_q - u_k = (u_q - uref) - (u_k - uref); each difference is formed in
-        // fp32 before scaling, and the row constant (u_q - uref) cancels in the
-        // softmax, so it only re-enters the LSE.
-        const float uref = Ubh[glo];
-        const float bq = valid ? (Ubh[g] - uref) * kLog2e : 0.f;
-        const uint32_t lane_addr = tmem + ((uint32_t)((warp & 3) * 32) << 16);
-        const uint64_t sl2x2 = f2pack(p.sl2, p.sl2);
-        float m_used = -INFINITY, l = 0.f;
-        int n = 0;
-        float u_next = jhi * BN + r < p.Nkv ? Ubh[jhi * BN + r] : 0.f;
-        for (int64_t j = jhi; j >= jlo; --j, ++n) {
-            // -(u_k - uref) log2e of this key tile -> smem (WG-cooperative); the
-            // next tile's u is prefetched into a register meanwhile
-            named_bar_sync(1, 128);
-            s_nbk[r] = (uref - u_next) * kLog2e;
-            if (j > jlo) u_next = (j - 1) * BN + r < p.Nkv ? Ubh[(j - 1) * BN + r] : 0.f;
-            named_bar_sync(1, 128);
-            mbar_wait(&bars->s_full, n & 1);
-            if (n < 8 && r == 0) GFWA_TR(16 + n);
-            tc_fence_after();
-            const bool trw = (n == 1 && (r == 0 || r == 96));
-            const bool interior = (j * BN + BN - 1 <= glo) && (j * BN >= ghi - p.w + 1);
-            uint32_t keep[4] = {~0u, ~0u, ~0u, ~0u};
-            if (!interior) {
-                // keys in (g - w, g] and < N_kv, as columns of this tile
-                const int64_t kb = j * BN;
-                const int hi = (int)min64(min64(g - kb, (int64_t)BN - 1), p.Nkv - 1 - kb);
-                const int lo = (int)max64(g - p.w + 1 - kb, (int64_t)0);
-#pragma unroll
-                for (int c = 0; c < 4; ++c) keep[c] = range_bits(lo, hi, 32 * c);
-            }
-            // the whole S row in registers: four loads, one wait, then the logits
-            // x = scale*q.k - (u_k - uref) log2e (Alg. 2 l.12-15) in place as
-            // packed pairs; max and exp both run from registers
-            uint32_t raw[BN];
-#pragma unroll
-            for (int cb = 0; cb < BN; cb += 32)
-                tmem_ld32(lane_addr + cb, *reinterpret_cast<uint32_t(*)[32]>(raw + cb));
-            tmem_wait_ld();
-            if (trw) GFWA_TR(10 + (r == 96));
-            uint64_t xp[BN / 2];
-#pragma unroll
-            for (int e = 0; e < BN; e += 4) {
-                const float4 nb = *reinterpret_cast<const float4*>(s_nbk + e);
-                xp[e / 2] = ffma2(f2pack(__uint_as_float(raw[e]), __uint_as_float(raw[e + 1])), sl2x2,
-                                  f2pack(nb.x, nb.y));
-                xp[e / 2 + 1] = ffma2(f2pack(__uint_as_float(raw[e + 2]), __uint_as_float(raw[e + 3])), sl2x2,
-                                      f2pack(nb.z, nb.w));
-            }
-            if (!interior) {
-#pragma unroll
-                for (int e = 0; e < BN / 2; ++e) {
-                    const uint32_t kw = keep[e >> 4];
-                    const int bit = 2 * (e & 15);
-                    float a, z;
-                    f2unpack(xp[e], a, z);
-                    a = ((kw >> bit) & 1u) ? a : -INFINITY;
-                    z = ((kw >> (bit + 1)) & 1u) ? z : -INFINITY;
-                    xp[e] = f2pack(a, z);
-                }
-            }
-            float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-            for (int e = 0; e < BN / 2; ++e) {
-                float a, z;
-                f2unpack(xp[e], a, z);
-                mx[e & 3] = fmax3(mx[e & 3], a, z);
-            }
-            const float mt = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
-            if (trw) GFWA_TR(12 + (r == 96));
-            // lazy online softmax: move the reference max only when it grows by > 2^8
-            float corr = 1.f;
-            bool need = false;
-            if (mt > m_used + kRescaleThreshold) {
-                if (m_used != -INFINITY) {
-                    corr = ex2(m_used - mt);
-                    need = true;
-                }
-                l *= corr;
-                m_used = mt;
-            }
-            const float mref = (m_used == -INFINITY) ? 0.f : m_used;
-            const uint64_t nm2 = f2pack(-mref, -mref);
-            uint64_t acc[4] = {0, 0, 0, 0};  // packed (0.f, 0.f)
-#pragma unroll
-            for (int cb = 0; cb < BN; cb += 32) {
-                uint32_t pk[16];
-#pragma unroll
-                for (int e = 0; e < 16; ++e) {
-                    const uint64_t d = fadd2(xp[cb / 2 + e], nm2);
-                    float p0, p1;
-                    if ((e & 3) < kPolyPairs) {
-                        // part of the exponentials on the FMA pipe: MUFU.EX2 is
-                        // co-critical with the tensor core on B200
-                        f2unpack(exp2_poly2(d), p0, p1);
-                    } else {
-                        float d0, d1;
-                        f2unpack(d, d0, d1);
-                        p0 = ex2(d0);
-                        p1 = ex2(d1);
+    } else if (warp >= kCvtWarp0) {
+        // ------------------------------------------------------------ V -> fp16 in place (training)
+        // the layout (128B swizzle) is unchanged, only the element encoding:
+        // bf16 -> fp32 (exact) -> fp16 (RNE); 2048 16-byte chunks over 64 threads
+        if (kF16P) {
+            const int ct = threadIdx.x - kCvtWarp0 * 32;
+            uint32_t kc = 0;
+            for (int idx = blockIdx.x; idx < p.n_items; idx += gridDim.x) {
+                const Item it = make_item(p, idx);
+                for (int n = 0; n < it.nsteps; ++n, ++kc) {
+                    const uint32_t m = 2 * kc + 1, sl = m % kSlots;  // this step's V: ring load 2 kc + 1
+                    mbar_wait_park(&bars->v_full[sl], (m / (2 * kSlots)) & 1);
+                    const uint32_t vb = smem_u32(smem + kOffKV + sl * kTile) + ct * 16;
+#pragma unroll 8
+                    for (int c = 0; c < (int)(kTile / 16 / 64); ++c) {
+                        const uint32_t a = vb + c * 64 * 16;
+                        uint4 q4 = lds128u(a);
+                        q4.x = bf16x2_to_f16x2(q4.x);
+                        q4.y = bf16x2_to_f16x2(q4.y);
+                        q4.z = bf16x2_to_f16x2(q4.z);
+                        q4.w = bf16x2_to_f16x2(q4.w);
+                        sts128(a, q4);
                     }
-                    acc[e & 3] = fadd2(acc[e & 3], f2pack(p0, p1));
-                    pk[e] = kF16P ? pack_f16x2(p0, p1) : pack_bf16x2(p0, p1);
+                    fence_proxy_async();  // generic-proxy writes -> visible to the tensor core
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&bars->v_ready[sl]);
                 }
-                tmem_st16(lane_addr + cb / 2, pk);  // P (bf16, or fp16 when training) over the S columns
             }
-            if (trw) GFWA_TR(14 + (r == 96));
-            {
-                const uint64_t a01 = fadd2(acc[0], acc[1]), a23 = fadd2(acc[2], acc[3]);
-                float s0, s1;
-                f2unpack(fadd2(a01, a23), s0, s1);
-                l += s0 + s1;
-            }
-            // rescale O (PV of the previous step is complete: S_full certified it)
-            if (__any_sync(0xffffffffu, need) && n > 0) {
-                uint32_t ob[32];
+        }
+    } else if (warp < kEpiWarp0) {
+        // ------------------------------------------------------------ softmax (tile x)
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kSoftmaxRegs));
+        const int x = warp >> 2;
+        const int r = threadIdx.x & 127;
+        const uint32_t lane_addr = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+        const uint32_t s_col = 128 * x, o_col = 256 + 128 * x;
+        float* nbk = reinterpret_cast<float*>(smem + kOffNbk) + x * BN;
+        float* linv = reinterpret_cast<float*>(smem + kOffLinv) + x * BM;
+        const uint64_t sl2x2 = f2pack(p.sl2, p.sl2);
+        uint32_t cs = 0;
+        for (int idx = blockIdx.x; idx < p.n_items; idx += gridDim.x) {
+            const Item it = make_item(p, idx);
+            if (!it.has(x)) continue;
+            const float* Ubh = p.U + ((int64_t)it.b * p.H + it.h) * p.Nkv;
+            const int t = it.r0 + x * BM + r;
+            const bool valid = t < (int)p.Nq;
+            const int g = t + (int)p.h0;
+            const int Nkv = (int)p.Nkv;
+            const int glo_x = it.glo(x), ghi_x = it.ghi(x), jlo_x = it.jlo(x), jt = it.jhi(x);
+            // bias in log2 units relative to the item's reference u (reading C-18): the
+            // row constant (u_q - uref) cancels in the softmax and re-enters the LSE
+            const float uref = Ubh[it.glo0];
+            const float bq = valid ? (Ubh[g] - uref) * kLog2e : 0.f;
+            float m_used = -INFINITY, l = 0.f;
+            float u_next = jt * BN + r < Nkv ? Ubh[jt * BN + r] : 0.f;
+            for (int j = jt; j >= jlo_x; --j, ++cs) {
+                // -(u_k - uref) log2e of this key tile -> smem (WG-cooperative, after every
+                // thread finished the previous tile); the next tile's u is prefetched
+                float* nb_cur = nbk;
+                named_bar_sync(1 + x, 128);
+                nb_cur[r] = (uref - u_next) * kLog2e;
+                if (j > jlo_x) u_next = (j - 1) * BN + r < Nkv ? Ubh[(j - 1) * BN + r] : 0.f;
+                named_bar_sync(1 + x, 128);
+                if (r == 0) FTR(x, 3 * (int)cs);
+                mbar_wait_park(&bars->s_full[x], cs & 1);
+                if (r == 0) FTR(x, 3 * (int)cs + 1);
+                tc_fence_after();
+                const bool interior = (j * BN + BN - 1 <= glo_x) && (j * BN >= ghi_x - p.w + 1) && (j * BN + BN <= Nkv);
+                uint32_t keep[4] = {~0u, ~0u, ~0u, ~0u};
+                bool live[4] = {true, true, true, true};  // warp-uniform: chunk has a kept key in some row
+                if (!interior) {
+                    // keys in (g - w, g] and < N_kv, as columns of this tile
+                    const int kb = j * BN;
+                    const int hi = min(min(g - kb, BN - 1), Nkv - 1 - kb);
+                    const int lo = max(g - p.w + 1 - kb, 0);
 #pragma unroll
-                for (int c = 0; c < D; c += 32) {
-                    tmem_ld32(lane_addr + 128 + c, ob);
+                    for (int c = 0; c < 4; ++c) {
+                        keep[c] = range_bits(lo, hi, 32 * c);
+                        live[c] = __any_sync(0xffffffffu, keep[c] != 0u);
+                    }
+                }
+                // two passes over the S row in TMEM, 64 columns in registers at a time (both
+                // softmax warpgroups fit the register file).  Pass 1 forms the logits
+                // x = scale*q.k - (u_k - uref) log2e (Alg. 2 l.12-15, masked to -inf
+                // outside the window), keeps the row max and writes x back over S;
+                // pass 2 reads x and only exponentiates.
+                float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+                for (int h2 = 0; h2 < 2; ++h2) {
+                    if (!(h2 ? (live[2] || live[3]) : (live[0] || live[1]))) continue;
+                    uint32_t raw[64];
+                    tmem_ld32(lane_addr + s_col + 64 * h2, *reinterpret_cast<uint32_t(*)[32]>(raw));
+                    tmem_ld32(lane_addr + s_col + 64 * h2 + 32, *reinterpret_cast<uint32_t(*)[32]>(raw + 32));
                     tmem_wait_ld();
 #pragma unroll
-                    for (int e = 0; e < 32; ++e) ob[e] = __float_as_uint(__uint_as_float(ob[e]) * corr);
-                    tmem_st32(lane_addr + 128 + c, ob);
+                    for (int e = 0; e < 64; e += 4) {
+                        const float4 nbv = *reinterpret_cast<const float4*>(nb_cur + 64 * h2 + e);
+                        const uint64_t x01 = ffma2(f2pack(__uint_as_float(raw[e]), __uint_as_float(raw[e + 1])),
+                                                   sl2x2, f2pack(nbv.x, nbv.y));
+                        const uint64_t x23 = ffma2(f2pack(__uint_as_float(raw[e + 2]), __uint_as_float(raw[e + 3])),
+                                                   sl2x2, f2pack(nbv.z, nbv.w));
+                        float a0, a1, a2, a3;
+                        f2unpack(x01, a0, a1);
+                        f2unpack(x23, a2, a3);
+                        if (!interior) {
+                            const int c = 64 * h2 + e;
+                            const uint32_t kw = h2 ? ((e >> 5) ? keep[3] : keep[2]) : ((e >> 5) ? keep[1] : keep[0]);
+                            const int bit = c & 31;
+                            a0 = ((kw >> bit) & 1u) ? a0 : -INFINITY;
+                            a1 = ((kw >> (bit + 1)) & 1u) ? a1 : -INFINITY;
+                            a2 = ((kw >> (bit + 2)) & 1u) ? a2 : -INFINITY;
+                            a3 = ((kw >> (bit + 3)) & 1u) ? a3 : -INFINITY;
+                        }
+                        mx[(e >> 2) & 3] = fmax3(mx[(e >> 2) & 3], fmaxf(a0, a1), fmaxf(a2, a3));
+                        raw[e] = __float_as_uint(a0);
+                        raw[e + 1] = __float_as_uint(a1);
+                        raw[e + 2] = __float_as_uint(a2);
+                        raw[e + 3] = __float_as_uint(a3);
+                    }
+                    tmem_st32(lane_addr + s_col + 64 * h2, *reinterpret_cast<uint32_t(*)[32]>(raw));
+                    tmem_st32(lane_addr + s_col + 64 * h2 + 32, *reinterpret_cast<uint32_t(*)[32]>(raw + 32));
                 }
-            }
-            tmem_wait_st();
-            if (trw) GFWA_TR(34 + (r == 96));
-            tc_fence_before();
-            __syncwarp();
-            if ((threadIdx.x & 31) == 0) mbar_arrive(&bars->p_ready);
-            if (n < 8 && r == 0) GFWA_TR(24 + n);
-            if (trw && r == 96) GFWA_TR(38);
-        }
-        // epilogue: O / l (Alg. 2 l.19-20) staged in smem (128B swizzle: bf16 in the
-        // Q slot, fp32 in the K and V slots -- all idle once O_full fires) and
-        // written with TMA stores
-        mbar_wait(&bars->o_full, 0);
-        if (r == 0) GFWA_TR(32);
-        tc_fence_after();
-        const float inv = l > 0.f ? 1.f / l : 0.f;
-        const uint32_t sbf = smem_u32(Qs), sf = smem_u32(Ks);
-        // two halves of 64 columns: both TMEM loads of a half in flight before one
-        // wait, and the half's bulk stores issued as soon as it is staged, so the
-        // second half's staging overlaps the first half's store read-out
+                const float mt = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+                // lazy online softmax: move the reference max only when it grows by > 2^8
+                float corr = 1.f;
+                bool need = false;
+                if (mt > m_used + kRescaleThreshold) {
+                    if (m_used != -INFINITY) {
+                        corr = ex2(m_used - mt);
+                        need = true;
+                    }
+                    l *= corr;
+                    m_used = mt;
+                }
+                const float mref = (m_used == -INFINITY) ? 0.f : m_used;
+                const uint64_t nm2 = f2pack(-mref, -mref);
+                float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+                tmem_wait_st();  // pass 1's x is in TMEM
+#pragma unroll
+                for (int h2 = 0; h2 < 2; ++h2) {
+                    const bool any = h2 ? (live[2] || live[3]) : (live[0] || live[1]);
+                    uint32_t xr[64];
+                    if (any) {
+                        tmem_ld32(lane_addr + s_col + 64 * h2, *reinterpret_cast<uint32_t(*)[32]>(xr));
+                        tmem_ld32(lane_addr + s_col + 64 * h2 + 32, *reinterpret_cast<uint32_t(*)[32]>(xr + 32));
+                        tmem_wait_ld();
+                    }
+#pragma unroll
+                    for (int cb = 0; cb < 2; ++cb) {
+                        uint32_t pk[16];
+                        if (h2 ? (cb ? live[3] : live[2]) : (cb ? live[1] : live[0])) {
+#pragma unroll
+                            for (int e = 0; e < 16; ++e) {
+                                const int k = 32 * cb + 2 * e;
+                                const uint64_t d = fadd2(f2pack(__uint_as_float(xr[k]), __uint_as_float(xr[k + 1])), nm2);
+                                float p0, p1;
+                                if ((e & 3) < kPolyPairs) {
+                                    f2unpack(exp2_poly2(d), p0, p1);
+                                } else {
+                                    float d0, d1;
+                                    f2unpack(d, d0, d1);
+                                    p0 = ex2(d0);
+                                    p1 = ex2(d1);
+                                }
+                                acc[(2 * e) & 7] += p0;
+                                acc[(2 * e + 1) & 7] += p1;
+                                pk[e] = kF16P ? pack_f16x2(p0, p1) : pack_bf16x2(p0, p1);
+                            }
+                        } else {
+#pragma unroll
+                            for (int e = 0; e < 16; ++e) pk[e] = 0u;
+                        }
+                        // P (16-bit) over the S columns: keys [64 h2 + 32 cb, +32) -> 16 columns
+                        tmem_st16(lane_addr + s_col + 32 * h2 + 16 * cb, pk);
+                    }
+                }
+                l += ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+                // rescale O (the PV of the previous step is complete: S_full certified it)
+                if (__any_sync(0xffffffffu, need)) {
+                    uint32_t ob[32];
 #pragma unroll 1
-        for (int hf = 0; hf < 2; ++hf) {
-            uint32_t ob[2][32];
-            tmem_ld32(lane_addr + 128 + 64 * hf, ob[0]);
-            tmem_ld32(lane_addr + 128 + 64 * hf + 32, ob[1]);
-            tmem_wait_ld();
+                    for (int c = 0; c < D; c += 32) {
+                        tmem_ld32(lane_addr + o_col + c, ob);
+                        tmem_wait_ld();
 #pragma unroll
-            for (int cc = 0; cc < 2; ++cc) {
-            const int c = 2 * hf + cc;
-            float v[32];
-#pragma unroll
-            for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(ob[cc][e]) * inv;
-            // bf16: columns [32c, 32c+32) = half c>>1, 16-B chunks (c&1)*4 + k
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const int chunk = ((c & 1) * 4 + k) ^ (r & 7);
-                uint4 pkv;
-                pkv.x = pack_bf16x2(v[8 * k + 0], v[8 * k + 1]);
-                pkv.y = pack_bf16x2(v[8 * k + 2], v[8 * k + 3]);
-                pkv.z = pack_bf16x2(v[8 * k + 4], v[8 * k + 5]);
-                pkv.w = pack_bf16x2(v[8 * k + 6], v[8 * k + 7]);
-                sts128(sbf + (c >> 1) * (kTileBytes / 2) + r * 128 + chunk * 16, pkv);
+                        for (int e = 0; e < 32; ++e) ob[e] = __float_as_uint(__uint_as_float(ob[e]) * corr);
+                        tmem_st32(lane_addr + o_col + c, ob);
+                    }
+                }
+                tmem_wait_st();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bars->p_ready[x]);
+                if (r == 0) FTR(x, 3 * (int)cs + 2);
             }
-            if (p.store_f32) {
-                // fp32: box c (32 columns, 128 B rows), 16-B pieces k
+            // Alg. 2 l.19-20: 1/l for the epilogue, LSE = m + ln l (natural log, bias included)
+            linv[r] = l > 0.f ? 1.f / l : 0.f;
+            if (valid) p.LSE[((int64_t)it.b * p.H + it.h) * p.Nq + t] = (m_used + bq + __log2f(l)) * kLn2;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bars->l_ready[x]);
+        }
+    } else {
+        // ------------------------------------------------------------ epilogue (+ V -> fp16)
+        const int r = threadIdx.x & 127;
+        const int ew = warp - kEpiWarp0;  // == warp & 3: TMEM lanes [32 ew, 32 ew + 32)
+        const uint32_t lane_addr = tmem + ((uint32_t)(ew * 32) << 16);
+        const float* linv_all = reinterpret_cast<const float*>(smem + kOffLinv);
+        uint32_t nit0 = 0, nit1 = 0;
+        auto epilogue = [&](const Item& it, int x) {
+            const uint32_t ph = (x ? nit1 : nit0) & 1;
+            if (r == 0) FTR(5, (int)(4 * (nit0 + nit1)));
+            mbar_wait_park(&bars->o_full[x], ph);
+            mbar_wait_park(&bars->l_ready[x], ph);
+            if (r == 0) FTR(5, (int)(4 * (nit0 + nit1)) + 1);
+            tc_fence_after();
+            const float inv = linv_all[x * BM + r];
+            uint8_t* ehi = smem + kOffE;
+            const uint32_t sbf = smem_u32(ehi), sf = smem_u32(ehi + kTile);
+            const uint32_t o_col = 256 + 128 * x;
+            // four rounds of 32 columns: O (bf16) into the Q slot, O_lo into E; each
+            // 64-column half is stored as soon as it is staged
+#pragma unroll 1
+            for (int cq = 0; cq < 4; ++cq) {
+                uint32_t ob[32];
+                tmem_ld32(lane_addr + o_col + 32 * cq, ob);
+                tmem_wait_ld();
+                if (cq == 3) {  // all of O_X has been read: release its columns
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&bars->o_free[x]);
+                }
+                const int hf = cq >> 1, cc = cq & 1;
 #pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    const int piece = k ^ (r & 7);
-                    sts128(sf + c * 16384 + r * 128 + piece * 16,
-                           make_uint4(__float_as_uint(v[4 * k]), __float_as_uint(v[4 * k + 1]),
-                                      __float_as_uint(v[4 * k + 2]), __float_as_uint(v[4 * k + 3])));
+                for (int k = 0; k < 4; ++k) {
+                    const int chunk = (cc * 4 + k) ^ (r & 7);
+                    uint32_t hw[4], lw[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const float v0 = __uint_as_float(ob[8 * k + 2 * e]) * inv;
+                        const float v1 = __uint_as_float(ob[8 * k + 2 * e + 1]) * inv;
+                        hw[e] = pack_bf16x2(v0, v1);
+                        if (p.store_lo) {
+                            float h0, h1;
+                            f2unpack(bf2_to_f2(hw[e]), h0, h1);
+                            lw[e] = pack_bf16x2(v0 - h0, v1 - h1);
+                        }
+                    }
+                    const uint32_t off = hf * (kTile / 2) + r * 128 + chunk * 16;
+                    sts128(sbf + off, make_uint4(hw[0], hw[1], hw[2], hw[3]));
+                    if (p.store_lo) sts128(sf + off, make_uint4(lw[0], lw[1], lw[2], lw[3]));
+                }
+                if (cc == 1) {
+                    fence_proxy_async();
+                    named_bar_sync(3, 128);
+                    if (r == 0) {
+                        const int row0 = it.r0 + x * BM;
+                        tma_store_4d(&mo, ehi + hf * (kTile / 2), hf * 64, it.h, row0, it.b);
+                        if (p.store_lo) tma_store_4d(&mol, ehi + kTile + hf * (kTile / 2), hf * 64, it.h, row0, it.b);
+                        bulk_commit();
+                    }
                 }
             }
-            }
-            fence_proxy_async();
-            named_bar_sync(1, 128);
             if (r == 0) {
-                tma_store_4d(&mo, Qs + hf * (kTileBytes / 2), hf * 64, (int)h, (int)r0, (int)b);
-                if (p.store_f32)
-                    for (int c = 2 * hf; c < 2 * hf + 2; ++c)
-                        tma_store_4d(&mo32, Ks + c * 16384, c * 32, (int)h, (int)r0, (int)b);
-                bulk_commit();
+                bulk_wait_read0();  // the staging buffers are reusable once the stores have read them
+                FTR(5, (int)(4 * (nit0 + nit1)) + 2);
             }
-        }
-        if (valid) p.LSE[(b * p.H + h) * p.Nq + t] = (m_used + bq + __log2f(l)) * kLn2;
-        if (r == 0) {
-            bulk_wait_read0();  // smem must stay valid until the bulk stores have read it
-            GFWA_TR(33);
+            named_bar_sync(3, 128);
+            if (x)
+                ++nit1;
+            else
+                ++nit0;
+        };
+        for (int idx = blockIdx.x; idx < p.n_items; idx += gridDim.x) {
+            const Item it = make_item(p, idx);
+            if (it.has1) epilogue(it, 1);  // B's last key tile comes before A's
+            if (it.has0) epilogue(it, 0);
         }
     }
     tc_fence_before();
     __syncthreads();
     if (warp == kMmaWarp) {
         tc_fence_after();
-        tmem_dealloc(tmem, 256);
+        tmem_dealloc(tmem, 512);
     }
 }
 
-// dynamic smem: 1024 alignment slack + Q, K, V + barriers (2 CTAs per SM)
-constexpr size_t kSmemBytes = 1024 + 3 * kTileBytes + kZeroBytes + sizeof(Bars) + 16;
-
 }  // namespace
+
+#if GFWA_FWD_TRACE
+// diagnostics build only: copy the stamp array out (148 x 8 x kTrMax int64)
+extern "C" int gfwa_debug_fwd_trace(long long* host, size_t n) {
+    if (n > sizeof(g_fwd_trace) / sizeof(long long)) n = sizeof(g_fwd_trace) / sizeof(long long);
+    return (int)cudaMemcpyFromSymbol(host, g_fwd_trace, n * sizeof(long long));
+}
+#endif
 
 bool tc_fwd_supported(const AttnParams& p, gfwa_dtype_t dt) {
     if (dt != GFWA_BF16 || p.d != D) return false;
@@ -490,21 +651,15 @@ bool tc_fwd_supported(const AttnParams& p, gfwa_dtype_t dt) {
 }
 
 gfwa_status_t tc_fwd(const AttnParams& p, cudaStream_t st) {
-    CUtensorMap mq, mk, mv, mo, mo32, mzq;
+    CUtensorMap mq, mk, mv, mo, mol;
     GFWA_REQUIRE(encode_bnhd_map(&mq, p.Q, p.B, p.Nq, p.H, D, p.qs, BM));
-    if (p.zero_acc) {
-        const int64_t acc_s[3] = {p.Nq * p.H * D, p.H * D, D};  // the backward's dQ accumulator layout
-        GFWA_REQUIRE(encode_bnhd_map_f32(&mzq, p.zero_acc, p.B, p.Nq, p.H, D, acc_s, 64));
-    } else {
-        mzq = mq;  // unused
-    }
     GFWA_REQUIRE(encode_bnhd_map(&mk, p.K, p.B, p.Nkv, p.H, D, p.ks, BN));
     GFWA_REQUIRE(encode_bnhd_map(&mv, p.V, p.B, p.Nkv, p.H, D, p.vs, BN));
     GFWA_REQUIRE(encode_bnhd_map(&mo, p.O, p.B, p.Nq, p.H, D, p.os, BM));
-    if (p.O_f32)
-        GFWA_REQUIRE(encode_bnhd_map_f32(&mo32, p.O_f32, p.B, p.Nq, p.H, D, p.os, BM));
+    if (p.O_lo)
+        GFWA_REQUIRE(encode_bnhd_map(&mol, p.O_lo, p.B, p.Nq, p.H, D, p.os, BM));
     else
-        mo32 = mo;  // unused
+        mol = mo;  // unused
     TcFwdParams tp;
     tp.U = p.U;
     tp.LSE = p.LSE;
@@ -512,38 +667,29 @@ gfwa_status_t tc_fwd(const AttnParams& p, cudaStream_t st) {
     tp.Nkv = p.Nkv;
     tp.h0 = p.h0;
     tp.H = p.H;
+    tp.B = p.B;
     tp.w = p.w;
-    tp.store_f32 = p.O_f32 != nullptr;
+    tp.store_lo = p.O_lo != nullptr;
     tp.zero_acc = p.zero_acc;
     tp.token = p.token;
     tp.token_val = p.token_val;
     tp.sl2 = p.scale * kLog2e;
+    tp.n_pairs = (int)((p.Nq + 2 * BM - 1) / (2 * BM));
+    const int64_t n_items = (int64_t)tp.n_pairs * p.H * p.B;
+    if (n_items >= ((int64_t)1 << 31) || p.Nkv + 2 * BM >= ((int64_t)1 << 31)) return GFWA_ERR_INVALID_ARGUMENT;
+    tp.n_items = (int)n_items;
+    int dev = 0, n_sm = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
     // per launch: the attribute is per device (a process may drive several GPUs)
-    auto kern = tp.store_f32 ? fwd_tc_kernel<true> : fwd_tc_kernel<false>;
+    auto kern = tp.store_lo ? fwd_tc_kernel<true> : fwd_tc_kernel<false>;
     if (gfwa_status_t s = check_launch(
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes)))
         return s;
-    dim3 grid((unsigned)((p.Nq + BM - 1) / BM), (unsigned)p.H, (unsigned)p.B);
-    // diagnostics: GFWA_TRACE_FWD=<file> dumps per-CTA clock64 stamps (synchronous)
-    const char* trace_file = getenv("GFWA_TRACE_FWD");
-    const size_t n_cta = (size_t)grid.x * grid.y * grid.z;
-    tp.trace = nullptr;
-    if (trace_file) {
-        cudaMalloc(&tp.trace, n_cta * 64 * sizeof(long long));
-        cudaMemsetAsync(tp.trace, 0, n_cta * 64 * sizeof(long long), st);
-    }
-    kern<<<grid, kThreads, kSmemBytes, st>>>(mzq, mq, mk, mv, mo, mo32, tp);
+    int64_t cap = n_sm;
+    if (const char* e = getenv("GFWA_FWD_GRID")) cap = max64(1, atoll(e));  // diagnostics: fewer CTAs, more items each
+    const unsigned grid = (unsigned)min64(n_items, cap);
+    kern<<<grid, kThreads, kSmemBytes, st>>>(mq, mk, mv, mo, mol, tp);
     note_launch();
-    if (trace_file) {
-        std::vector<long long> hbuf(n_cta * 64);
-        cudaStreamSynchronize(st);
-        cudaMemcpy(hbuf.data(), tp.trace, hbuf.size() * sizeof(long long), cudaMemcpyDeviceToHost);
-        cudaFree(tp.trace);
-        if (FILE* f = fopen(trace_file, "wb")) {
-            fwrite(hbuf.data(), sizeof(long long), hbuf.size(), f);
-            fclose(f);
-        }
-    }
     return check_launch();
 }
 

@@ -127,21 +127,22 @@ bool al16(const void* p) { return ((uintptr_t)p % 16) == 0; }
 }  // namespace
 
 extern "C" gfwa_status_t gfwa_fwd(const gfwa_attn_desc_t* desc, const void* Q, const void* K, const void* V,
-                                  const float* U, void* O, float* O_f32, float* LSE, gfwa_stream_t stream) {
+                                  const float* U, void* O, void* O_lo, float* LSE, gfwa_stream_t stream) {
     AttnParams p;
     if (gfwa_status_t s = make_params(desc, p)) return s;
     if (!Q || !K || !V || !U || !O || !LSE) return GFWA_ERR_INVALID_ARGUMENT;
     const size_t es = desc->dtype == GFWA_BF16 ? 2 : 4;
     if (!strides_ok(p.qs, es) || !strides_ok(p.ks, es) || !strides_ok(p.vs, es) || !strides_ok(p.os, es))
         return GFWA_ERR_INVALID_ARGUMENT;
-    if (!al16(Q) || !al16(K) || !al16(V) || !al16(O) || (O_f32 && !al16(O_f32))) return GFWA_ERR_INVALID_ARGUMENT;
+    if (!al16(Q) || !al16(K) || !al16(V) || !al16(O) || (O_lo && !al16(O_lo))) return GFWA_ERR_INVALID_ARGUMENT;
+    if (O_lo && desc->dtype != GFWA_BF16) return GFWA_ERR_INVALID_ARGUMENT;  // an fp32 O is exact already
     bind_context(Q);
     p.Q = Q;
     p.K = K;
     p.V = V;
     p.U = U;
     p.O = O;
-    p.O_f32 = O_f32;
+    p.O_lo = O_lo;
     p.LSE = LSE;
     p.zero_acc = g_prepare.zero_acc;
     p.token = g_prepare.token;
@@ -162,7 +163,7 @@ extern "C" gfwa_status_t gfwa_fwd(const gfwa_attn_desc_t* desc, const void* Q, c
 // clears it, so interleaved shapes on one workspace stay correct: a backward
 // whose descriptor does not match the token zeroes its own accumulator.
 extern "C" gfwa_status_t gfwa_fwd_train(const gfwa_attn_desc_t* desc, const void* Q, const void* K,
-                                        const void* V, const float* U, void* O, float* O_f32, float* LSE,
+                                        const void* V, const float* U, void* O, void* O_lo, float* LSE,
                                         void* bwd_ws, size_t bwd_ws_bytes, gfwa_stream_t stream);
 
 static size_t bwd_ws_layout(const AttnParams& p, gfwa_dtype_t dt, size_t* off_D, size_t* off_scan,
@@ -182,7 +183,7 @@ static size_t bwd_ws_layout(const AttnParams& p, gfwa_dtype_t dt, size_t* off_D,
 // path the forward's epilogue zeroes the dQ accumulator (the writes overlap the
 // compute-bound forward) and sets the token, so gfwa_bwd skips its zeroing pass.
 extern "C" gfwa_status_t gfwa_fwd_train(const gfwa_attn_desc_t* desc, const void* Q, const void* K,
-                                        const void* V, const float* U, void* O, float* O_f32, float* LSE,
+                                        const void* V, const float* U, void* O, void* O_lo, float* LSE,
                                         void* bwd_ws, size_t bwd_ws_bytes, gfwa_stream_t stream) {
     AttnParams p;
     if (gfwa_status_t s = make_params(desc, p)) return s;
@@ -191,11 +192,11 @@ extern "C" gfwa_status_t gfwa_fwd_train(const gfwa_attn_desc_t* desc, const void
     const size_t need = bwd_ws_layout(p, desc->dtype, &off_D, &off_scan, &off_tc, &off_tok);
     if (bwd_ws_bytes < need) return GFWA_ERR_WORKSPACE;
     if (!tc_bwd_supported(p, desc->dtype) || !tc_fwd_supported(p, desc->dtype))  // nothing to prepare
-        return gfwa_fwd(desc, Q, K, V, U, O, O_f32, LSE, stream);
+        return gfwa_fwd(desc, Q, K, V, U, O, O_lo, LSE, stream);
     g_prepare.zero_acc = (float*)((char*)bwd_ws + off_tc);
     g_prepare.token = (unsigned long long*)((char*)bwd_ws + off_tok);
     g_prepare.token_val = prep_token(p);
-    const gfwa_status_t s = gfwa_fwd(desc, Q, K, V, U, O, O_f32, LSE, stream);
+    const gfwa_status_t s = gfwa_fwd(desc, Q, K, V, U, O, O_lo, LSE, stream);
     g_prepare = Prepare{};
     return s;
 }
@@ -210,13 +211,14 @@ extern "C" size_t gfwa_bwd_workspace_size(const gfwa_attn_desc_t* desc) {
 // The dU -> dalpha reverse scan runs as a [B, Nkv, H=H] gate backward with
 // kind ALPHA: it only needs dU in [B, H, Nkv] layout, which is exactly dU.
 extern "C" gfwa_status_t gfwa_bwd(const gfwa_attn_desc_t* desc, const void* Q, const void* K, const void* V,
-                                  const float* U, const void* O, const float* O_f32, const float* LSE,
+                                  const float* U, const void* O, const void* O_lo, const float* LSE,
                                   const void* dO, void* dQ, void* dK, void* dV, float* dU, float* dalpha,
                                   const double* dalpha_carry, void* ws, size_t ws_bytes, gfwa_stream_t stream) {
     AttnParams p;
     if (gfwa_status_t s = make_params(desc, p)) return s;
     GFWA_REQUIRE(Q && K && V && U && LSE && dO && dQ && dK && dV && dU && ws);
-    GFWA_REQUIRE(O || O_f32);
+    GFWA_REQUIRE(O);
+    GFWA_REQUIRE(!O_lo || (desc->dtype == GFWA_BF16 && al16(O_lo)));
     const size_t es = desc->dtype == GFWA_BF16 ? 2 : 4;
     GFWA_REQUIRE(strides_ok(p.qs, es) && strides_ok(p.ks, es) && strides_ok(p.vs, es) && strides_ok(p.os, es));
     const void* ptrs[] = {Q, K, V, dO, dQ, dK, dV};
@@ -233,7 +235,7 @@ extern "C" gfwa_status_t gfwa_bwd(const gfwa_attn_desc_t* desc, const void* Q, c
     p.V = V;
     p.U = U;
     p.O = const_cast<void*>(O);
-    p.Ofp = O_f32;
+    p.Olo = O_lo;
     p.LSE = const_cast<float*>(LSE);
     p.dO = dO;
     p.dQ = dQ;

@@ -27,7 +27,7 @@ inline bool encode_bnhd_map(CUtensorMap* map, const void* base, int64_t B, int64
 }
 
 // fp32 [B, N, H, d] map with box {32 d-elements (128 B), 1, rows, 1}, 128B swizzle
-// (epilogue stores of O_f32 and the dQ reduce-add).
+// (the dQ reduce-add).
 inline bool encode_bnhd_map_f32(CUtensorMap* map, const void* base, int64_t B, int64_t N, int64_t H, int d,
                                 const int64_t* s, int box_rows) {
     cuuint64_t dims[4] = {(cuuint64_t)d, (cuuint64_t)H, (cuuint64_t)N, (cuuint64_t)B};

@@ -35,10 +35,10 @@ import torch.distributed as dist
 @dataclass
 class Ops:
     gate_prefix: Callable   # (h, beta, eps) -> U [B,H,S] fp32 (carry 0)
-    fwd: Callable           # (Q, K, V, U, w) -> (O, LSE, O_f32)
-    bwd: Callable           # (Q, K, V, U, O, LSE, dO, w, O_f32) -> (dQ, dK, dV, dU)
+    fwd: Callable           # (Q, K, V, U, w) -> (O, LSE, O_lo)
+    bwd: Callable           # (Q, K, V, U, O, LSE, dO, w, O_lo) -> (dQ, dK, dV, dU)
     gate_bwd: Callable      # (dU, h, beta, eps, carry fp64 [B,H] | None) -> (dalpha, dh, dbeta)
-    # (Q, K, V, U, w, O_out, O32_out | None) -> LSE: the forward written into caller views
+    # (Q, K, V, U, w, O_out, Olo_out | None) -> LSE: the forward written into caller views
     # (lets the step run the interior queries while the halo is in flight); None: no split
     fwd_into: Callable | None = None
 
@@ -50,17 +50,17 @@ def cuda_ops() -> Ops:
     def _fwd(Q, K, V, U, w):
         # the step's backward follows on the same problem: gfwa_fwd_train zeroes its
         # dQ accumulator inside the forward (the token keeps other orders safe)
-        return gb.gfwa_fwd(Q, K, V, U, w, want_o_f32=True, prepare_bwd=True)
+        return gb.gfwa_fwd(Q, K, V, U, w, want_o_lo=True, prepare_bwd=True)
 
-    def _bwd(Q, K, V, U, O, LSE, dO, w, O32):
-        dQ, dK, dV, dU, _ = gb.gfwa_bwd(Q, K, V, U, O, LSE, dO, w, O_f32=O32, want_dalpha=False)
+    def _bwd(Q, K, V, U, O, LSE, dO, w, Olo):
+        dQ, dK, dV, dU, _ = gb.gfwa_bwd(Q, K, V, U, O, LSE, dO, w, O_lo=Olo, want_dalpha=False)
         return dQ, dK, dV, dU
 
     def _gate_bwd(dU, h, beta, eps, carry):
         return gb.gfwa_gate_prefix_bwd(dU, h, beta, eps, carry=carry)
 
-    def _fwd_into(Q, K, V, U, w, O_out, O32_out):
-        return gb.gfwa_fwd(Q, K, V, U, w, out=O_out, out_f32=O32_out)[1]
+    def _fwd_into(Q, K, V, U, w, O_out, Olo_out):
+        return gb.gfwa_fwd(Q, K, V, U, w, out=O_out, out_lo=Olo_out)[1]
 
     return Ops(gate_prefix=lambda h, b, eps: gb.gfwa_gate_prefix(h, b, eps), fwd=_fwd, bwd=_bwd,
                gate_bwd=_gate_bwd, fwd_into=_fwd_into)
@@ -176,10 +176,11 @@ def sp_forward_backward(Q, K, V, h, beta, dO, w: int, ops: Ops, ring: Ring, eps:
         # queries [w, S) see only local keys: run them while the halo is in flight,
         # then the first w queries over [halo; local[:w]] (the ABI's halo convention)
         O = torch.empty_like(Q)
-        O32 = torch.empty_strided(O.shape, O.stride(), dtype=torch.float32, device=O.device) \
-            if O.is_cuda else None
+        # the bf16 residual of the output cast for the backward's D (reading C-12)
+        Olo = torch.empty_strided(O.shape, O.stride(), dtype=torch.bfloat16, device=O.device) \
+            if (O.is_cuda and O.dtype == torch.bfloat16) else None
         LSE = torch.empty(Q.shape[0], Q.shape[2], S, dtype=torch.float32, device=Q.device)
-        LSE[..., w:] = ops.fwd_into(Q[:, w:], K, V, U_loc, w, O[:, w:], None if O32 is None else O32[:, w:])
+        LSE[..., w:] = ops.fwd_into(Q[:, w:], K, V, U_loc, w, O[:, w:], None if Olo is None else Olo[:, w:])
     recv = ring.finish(handle)
     if recv is not None:
         if kv_ext is not None:
@@ -195,10 +196,10 @@ def sp_forward_backward(Q, K, V, h, beta, dO, w: int, ops: Ops, ring: Ring, eps:
         Kx, Vx, Ux, h0 = K, V, U_loc, 0
     if split:
         LSE[..., :w] = ops.fwd_into(Q[:, :w], Kx[:, :2 * w], Vx[:, :2 * w], Ux[..., :2 * w].contiguous(), w,
-                                    O[:, :w], None if O32 is None else O32[:, :w])
+                                    O[:, :w], None if Olo is None else Olo[:, :w])
     else:
-        O, LSE, O32 = ops.fwd(Q, Kx, Vx, Ux, w)
-    dQ, dKx, dVx, dUx = ops.bwd(Q, Kx, Vx, Ux, O, LSE, dO, w, O32)
+        O, LSE, Olo = ops.fwd(Q, Kx, Vx, Ux, w)
+    dQ, dKx, dVx, dUx = ops.bwd(Q, Kx, Vx, Ux, O, LSE, dO, w, Olo)
     # backward halo r -> r-1: gradients of the halo rows
     back_like = [dKx[:, :w], dVx[:, :w], dUx[..., :w]]
     back = ring.shift([t.contiguous() for t in back_like] if h0 else None, back_like, forward=False)

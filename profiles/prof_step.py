@@ -25,8 +25,8 @@ def main():
     h, beta = h.bfloat16(), beta.bfloat16()
     for _ in range(2):
         U = gb.gfwa_gate_prefix(h, beta)
-        O, LSE, O32 = gb.gfwa_fwd(Q, K, V, U, s.w, want_o_f32=True)
-        dQ, dK, dV, dU, _ = gb.gfwa_bwd(Q, K, V, U, O, LSE, dO, s.w, O_f32=O32, want_dalpha=False)
+        O, LSE, Olo = gb.gfwa_fwd(Q, K, V, U, s.w, want_o_lo=True)
+        dQ, dK, dV, dU, _ = gb.gfwa_bwd(Q, K, V, U, O, LSE, dO, s.w, O_lo=Olo, want_dalpha=False)
         gb.gfwa_gate_prefix_bwd(dU, h, beta, want_dalpha=False)
     torch.cuda.synchronize()
 

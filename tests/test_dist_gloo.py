@@ -29,7 +29,7 @@ def _oracle_ops():
         O, L = oracle.fwd(Q, K, V, U, w)
         return t(O), t(L), None
 
-    def bwd(Q, K, V, U, O, LSE, dO, w, O32):
+    def bwd(Q, K, V, U, O, LSE, dO, w, Olo):
         g = oracle.bwd(Q, K, V, U, dO, w, want_dalpha=False)
         return t(g["dQ"]), t(g["dK"]), t(g["dV"]), t(g["dU"])
 
@@ -38,7 +38,7 @@ def _oracle_ops():
         dh, db = oracle.gate_chain(h, beta, da, eps)
         return t(da), t(dh), t(db)
 
-    def fwd_into(Q, K, V, U, w, O_out, O32_out):
+    def fwd_into(Q, K, V, U, w, O_out, Olo_out):
         O, L = oracle.fwd(Q, K, V, U, w)
         O_out.copy_(t(O))
         return t(L)

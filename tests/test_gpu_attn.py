@@ -28,12 +28,12 @@ def _run(s: synth.AttnShape, dtype, seed, U=None):
     Q, K, V, dO = synth.attn_inputs(s, seed=seed, dtype=dtype)
     U = _U(s.B, s.H, s.nkv, seed + 1) if U is None else U
     Qd, Kd, Vd, dOd, Ud = (x.cuda() for x in (Q, K, V, dO, U))
-    O, LSE, O32 = gb.gfwa_fwd(Qd, Kd, Vd, Ud, s.w, want_o_f32=True)
-    dQ, dK, dV, dU, da = gb.gfwa_bwd(Qd, Kd, Vd, Ud, O, LSE, dOd, s.w, O_f32=O32)
+    O, LSE, Olo = gb.gfwa_fwd(Qd, Kd, Vd, Ud, s.w, want_o_lo=True)
+    dQ, dK, dV, dU, da = gb.gfwa_bwd(Qd, Kd, Vd, Ud, O, LSE, dOd, s.w, O_lo=Olo)
     torch.cuda.synchronize()
     Or, Lr = oracle.fwd(Q, K, V, U, s.w)
     g = oracle.bwd(Q, K, V, U, dO, s.w)
-    return dict(O=O, LSE=LSE, O32=O32, dQ=dQ, dK=dK, dV=dV, dU=dU, dalpha=da), dict(O=Or, LSE=Lr, **g)
+    return dict(O=O, LSE=LSE, Olo=Olo, dQ=dQ, dK=dK, dV=dV, dU=dU, dalpha=da), dict(O=Or, LSE=Lr, **g)
 
 
 F32_SHAPES = [
@@ -129,8 +129,8 @@ def test_c2_full_size_sampled():
     Q, K, V, dO = synth.attn_inputs(s, seed=c["seed"], device="cuda", dtype=torch.bfloat16)
     h, beta = synth.gate_inputs(s.B, s.N, s.H, seed=c["seed"], device="cuda")
     U = gb.gfwa_gate_prefix(h, beta)
-    O, LSE, O32 = gb.gfwa_fwd(Q, K, V, U, s.w, want_o_f32=True)
-    dQ, dK, dV, dU, da = gb.gfwa_bwd(Q, K, V, U, O, LSE, dO, s.w, O_f32=O32)
+    O, LSE, Olo = gb.gfwa_fwd(Q, K, V, U, s.w, want_o_lo=True)
+    dQ, dK, dV, dU, da = gb.gfwa_bwd(Q, K, V, U, O, LSE, dO, s.w, O_lo=Olo)
     torch.cuda.synchronize()
     rng = np.random.default_rng(0)
     rows = np.stack([rng.integers(0, s.B, 96), rng.integers(0, s.H, 96), rng.integers(0, s.N, 96)], 1)
@@ -157,11 +157,11 @@ def test_zero_grad_out_and_invariants():
     s = synth.AttnShape(B=1, H=2, N=260, d=128, w=70)
     Q, K, V, dO = synth.attn_inputs(s, seed=11, device="cuda", dtype=torch.float32)
     U = _U(1, 2, s.N, 12).cuda()
-    O, LSE, O32 = gb.gfwa_fwd(Q, K, V, U, s.w, want_o_f32=True)
-    z = gb.gfwa_bwd(Q, K, V, U, O, LSE, torch.zeros_like(dO), s.w, O_f32=O32)
+    O, LSE, Olo = gb.gfwa_fwd(Q, K, V, U, s.w, want_o_lo=True)
+    z = gb.gfwa_bwd(Q, K, V, U, O, LSE, torch.zeros_like(dO), s.w, O_lo=Olo)
     for t in z:
         assert torch.count_nonzero(t) == 0
-    dQ, dK, dV, dU, da = gb.gfwa_bwd(Q, K, V, U, O, LSE, dO, s.w, O_f32=O32)
+    dQ, dK, dV, dU, da = gb.gfwa_bwd(Q, K, V, U, O, LSE, dO, s.w, O_lo=Olo)
     assert dU.double().sum(-1).abs().max().item() <= 1e-3 * dU.abs().max().item()
     assert da[..., 0].abs().max().item() <= 1e-3 * da.abs().max().item()
 
@@ -175,11 +175,11 @@ def test_bf16_tc_invariants():
     assert gb.gfwa_attn_path(Q, K, V, s.w) == 1
     h, beta = synth.gate_inputs(s.B, s.N, s.H, seed=14, device="cuda")
     U = gb.gfwa_gate_prefix(h, beta)
-    O, LSE, O32 = gb.gfwa_fwd(Q, K, V, U, s.w, want_o_f32=True)
-    z = gb.gfwa_bwd(Q, K, V, U, O, LSE, torch.zeros_like(dO), s.w, O_f32=O32)
+    O, LSE, Olo = gb.gfwa_fwd(Q, K, V, U, s.w, want_o_lo=True)
+    z = gb.gfwa_bwd(Q, K, V, U, O, LSE, torch.zeros_like(dO), s.w, O_lo=Olo)
     for t in z:
         assert torch.count_nonzero(t) == 0
-    dQ, dK, dV, dU, da = gb.gfwa_bwd(Q, K, V, U, O, LSE, dO, s.w, O_f32=O32)
+    dQ, dK, dV, dU, da = gb.gfwa_bwd(Q, K, V, U, O, LSE, dO, s.w, O_lo=Olo)
     # fp32 round-off of sums of ~N w terms of size |dS| <= max|dU|
     bound = 1e-4 * dU.abs().max().item()
     assert dU.double().sum(-1).abs().max().item() <= bound
@@ -195,8 +195,8 @@ def _sampled_full_size(s: synth.AttnShape, seed: int, n_rows: int, bwd_slices, h
     Q, K, V, dO = synth.attn_inputs(s, seed=seed, device="cuda", dtype=torch.bfloat16)
     h, beta = synth.gate_inputs(s.B, s.nkv, s.H, seed=seed, device="cuda")
     U = gb.gfwa_gate_prefix(h, beta)
-    O, LSE, O32 = gb.gfwa_fwd(Q, K, V, U, s.w, want_o_f32=True)
-    dQ, dK, dV, dU, da = gb.gfwa_bwd(Q, K, V, U, O, LSE, dO, s.w, O_f32=O32)
+    O, LSE, Olo = gb.gfwa_fwd(Q, K, V, U, s.w, want_o_lo=True)
+    dQ, dK, dV, dU, da = gb.gfwa_bwd(Q, K, V, U, O, LSE, dO, s.w, O_lo=Olo)
     torch.cuda.synchronize()
     rng = np.random.default_rng(seed)
     rows = np.stack([rng.integers(0, s.B, n_rows), rng.integers(0, s.H, n_rows), rng.integers(0, s.N, n_rows)], 1)
@@ -245,12 +245,12 @@ def test_fwd_train_prepares_the_backward_workspace():
     Q, K, V, dO = synth.attn_inputs(s, seed=31, device="cuda", dtype=torch.bfloat16)
     h, beta = synth.gate_inputs(s.B, s.N, s.H, seed=32, device="cuda")
     U = gb.gfwa_gate_prefix(h, beta)
-    O, LSE, O32 = gb.gfwa_fwd(Q, K, V, U, s.w, want_o_f32=True)
-    ref = gb.gfwa_bwd(Q, K, V, U, O, LSE, dO, s.w, O_f32=O32)
-    O2, LSE2, O322 = gb.gfwa_fwd(Q, K, V, U, s.w, want_o_f32=True, prepare_bwd=True)
-    assert torch.equal(O, O2) and torch.equal(LSE, LSE2) and torch.equal(O32, O322)
-    got = gb.gfwa_bwd(Q, K, V, U, O2, LSE2, dO, s.w, O_f32=O322)
-    again = gb.gfwa_bwd(Q, K, V, U, O2, LSE2, dO, s.w, O_f32=O322)  # mark consumed: zeroes itself
+    O, LSE, Olo = gb.gfwa_fwd(Q, K, V, U, s.w, want_o_lo=True)
+    ref = gb.gfwa_bwd(Q, K, V, U, O, LSE, dO, s.w, O_lo=Olo)
+    O2, LSE2, Olo2 = gb.gfwa_fwd(Q, K, V, U, s.w, want_o_lo=True, prepare_bwd=True)
+    assert torch.equal(O, O2) and torch.equal(LSE, LSE2) and torch.equal(Olo, Olo2)
+    got = gb.gfwa_bwd(Q, K, V, U, O2, LSE2, dO, s.w, O_lo=Olo2)
+    again = gb.gfwa_bwd(Q, K, V, U, O2, LSE2, dO, s.w, O_lo=Olo2)  # mark consumed: zeroes itself
     torch.cuda.synchronize()
     for a, b, c in zip(ref[:4], got[:4], again[:4]):
         tol = 1e-2 * max(1.0, a.float().abs().max().item())  # fp32 reduce order only (bf16 outputs)
@@ -270,17 +270,17 @@ def test_fwd_train_interleaved_shapes_share_one_workspace():
         Q, K, V, dO = synth.attn_inputs(s, seed=seed, device="cuda", dtype=torch.bfloat16)
         h, beta = synth.gate_inputs(s.B, s.N, s.H, seed=seed + 1, device="cuda")
         U = gb.gfwa_gate_prefix(h, beta)
-        ref_o = gb.gfwa_fwd(Q, K, V, U, s.w, want_o_f32=True)
-        ref = gb.gfwa_bwd(Q, K, V, U, *ref_o[:2], dO, s.w, O_f32=ref_o[2])
+        ref_o = gb.gfwa_fwd(Q, K, V, U, s.w, want_o_lo=True)
+        ref = gb.gfwa_bwd(Q, K, V, U, *ref_o[:2], dO, s.w, O_lo=ref_o[2])
         out[name] = (Q, K, V, U, dO, s, [r.clone() for r in ref[:4]])
     prep = {}
     for name in ("X", "Y"):
         Q, K, V, U, dO, s, _ = out[name]
-        prep[name] = gb.gfwa_fwd(Q, K, V, U, s.w, want_o_f32=True, prepare_bwd=True)
+        prep[name] = gb.gfwa_fwd(Q, K, V, U, s.w, want_o_lo=True, prepare_bwd=True)
     for name in ("Y", "X"):
         Q, K, V, U, dO, s, ref = out[name]
-        O, LSE, O32 = prep[name]
-        got = gb.gfwa_bwd(Q, K, V, U, O, LSE, dO, s.w, O_f32=O32)
+        O, LSE, Olo = prep[name]
+        got = gb.gfwa_bwd(Q, K, V, U, O, LSE, dO, s.w, O_lo=Olo)
         torch.cuda.synchronize()
         for a, b in zip(ref, got[:4]):
             tol = 1e-2 * max(1.0, a.float().abs().max().item())  # fp32 reduce order only

@@ -19,8 +19,8 @@ def test_step_captures_and_replays_bit_exact():
 
     def step():
         U = gb.gfwa_gate_prefix(h, beta)
-        O, LSE, O32 = gb.gfwa_fwd(Q, K, V, U, s.w, want_o_f32=True)
-        dQ, dK, dV, dU, _ = gb.gfwa_bwd(Q, K, V, U, O, LSE, dO, s.w, O_f32=O32, want_dalpha=False)
+        O, LSE, Olo = gb.gfwa_fwd(Q, K, V, U, s.w, want_o_lo=True)
+        dQ, dK, dV, dU, _ = gb.gfwa_bwd(Q, K, V, U, O, LSE, dO, s.w, O_lo=Olo, want_dalpha=False)
         _, dh, dbeta = gb.gfwa_gate_prefix_bwd(dU, h, beta, want_dalpha=False)
         return U, O, LSE, dQ, dK, dV, dh, dbeta
 

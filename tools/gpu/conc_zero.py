@@ -14,7 +14,7 @@ def run(conc, zero):
     if zero and conc:
         ev.record(); side.wait_event(ev)
         with torch.cuda.stream(side): Z.zero_()
-    gb.gfwa_fwd(Q, K, V, U, s.w, want_o_f32=True)
+    gb.gfwa_fwd(Q, K, V, U, s.w, want_o_lo=True)
     if zero and not conc: Z.zero_()
     if zero and conc:
         e2 = torch.cuda.Event(); e2.record(side); torch.cuda.current_stream().wait_event(e2)

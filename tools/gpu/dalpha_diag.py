@@ -3,7 +3,7 @@
 For each (config, slice) print: max|dalpha - oracle| and where, max|dU - oracle|,
 sum_m dU_m of the kernel (telescoping: ~0), the kernel's dalpha vs the fp64
 reverse scan of its own dU, and the d-alpha error predicted by the kernel's D
-alone (exact P, dP; D taken from the kernel's O_f32), computed in fp64 numpy
+alone (exact P, dP; D taken from the kernel's O_lo), computed in fp64 numpy
 per 512-query block (test infrastructure: oracle + numpy, no product code).
 
     python tools/gpu/dalpha_diag.py [C2 C3_w512 dist C4s small]
@@ -48,8 +48,8 @@ def run(name, s, seed, slices, use_gate=True):
     Q, K, V, dO = synth.attn_inputs(s, seed=seed, device="cuda", dtype=torch.bfloat16)
     h, beta = synth.gate_inputs(s.B, s.nkv, s.H, seed=seed + 1, device="cuda")
     U = gb.gfwa_gate_prefix(h, beta)
-    O, LSE, O32 = gb.gfwa_fwd(Q, K, V, U, s.w, want_o_f32=True)
-    dQ, dK, dV, dU, da = gb.gfwa_bwd(Q, K, V, U, O, LSE, dO, s.w, O_f32=O32)
+    O, LSE, Olo = gb.gfwa_fwd(Q, K, V, U, s.w, want_o_lo=True)
+    dQ, dK, dV, dU, da = gb.gfwa_bwd(Q, K, V, U, O, LSE, dO, s.w, O_lo=Olo)
     torch.cuda.synchronize()
     h0 = s.nkv - s.N
     scale = 1.0 / np.sqrt(s.d)
@@ -68,8 +68,8 @@ def run(name, s, seed, slices, use_gate=True):
         v = sl(V)[0, :, 0].double().cpu().numpy()
         do = sl(dO)[0, :, 0].double().cpu().numpy()
         u = Ur[0, 0].double().cpu().numpy()
-        o32 = sl(O32)[0, :, 0].double().cpu().numpy()
-        Dk = (o32 * do).sum(1)
+        o_k = sl(O)[0, :, 0].double().cpu().numpy() + sl(Olo)[0, :, 0].double().cpu().numpy()
+        Dk = (o_k * do).sum(1)
         De = (Or[0, :, 0] * do).sum(1)
         _, da_D = band_dalpha(q, k, v, u, do, Dk, s.w, h0, scale)
         _, da_E = band_dalpha(q, k, v, u, do, De, s.w, h0, scale)

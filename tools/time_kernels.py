@@ -37,14 +37,14 @@ def main():
     Q, K, V, dO = synth.attn_inputs(s, seed=c["seed"], device="cuda", dtype=torch.bfloat16)
     h, beta = synth.gate_inputs(s.B, s.N, s.H, seed=c["seed"], device="cuda")
     U = gb.gfwa_gate_prefix(h, beta)
-    O, LSE, O32 = gb.gfwa_fwd(Q, K, V, U, s.w, want_o_f32=True)
+    O, LSE, Olo = gb.gfwa_fwd(Q, K, V, U, s.w, want_o_lo=True)
     fl = 4.0 * s.N * s.w * s.d * s.B * s.H
     tag = os.path.basename(os.environ.get("GFWA_LIB", "default"))
     if what in ("fwd", "both"):
-        ms = timeit(lambda: gb.gfwa_fwd(Q, K, V, U, s.w, want_o_f32=True))
+        ms = timeit(lambda: gb.gfwa_fwd(Q, K, V, U, s.w, want_o_lo=True))
         print(f"{tag} {wl} fwd {ms*1e3:8.1f} us  {fl/ms/1e9:7.1f} TFLOP/s")
     if what in ("bwd", "both"):
-        ms = timeit(lambda: gb.gfwa_bwd(Q, K, V, U, O, LSE, dO, s.w, O_f32=O32, want_dalpha=False))
+        ms = timeit(lambda: gb.gfwa_bwd(Q, K, V, U, O, LSE, dO, s.w, O_lo=Olo, want_dalpha=False))
         print(f"{tag} {wl} bwd {ms*1e3:8.1f} us  {2.5*fl/ms/1e9:7.1f} TFLOP/s")
 
 
