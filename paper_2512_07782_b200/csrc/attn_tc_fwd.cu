@@ -83,7 +83,7 @@ struct __align__(8) Bars {
     // a slot alternates K and V fills: each kind completes its own barrier, so a
     // consumer of one kind never sees a phase of the other (parity aliasing)
     uint64_t k_full[kSlots], v_full[kSlots], kv_empty[kSlots], v_ready[kSlots];
-    uint64_t s_full[2], p_ready[2], o_full[2], o_free[2], l_ready[2];
+    uint64_t s_full[2], p_ready[2], o_full[2], o_free[2], l_ready[2], l_free[2];
     uint32_t tmem;
 };
 static_assert(sizeof(Bars) <= 256, "barrier block");
@@ -187,6 +187,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&bars->o_full[i], 1);
             mbar_init(&bars->o_free[i], 4);
             mbar_init(&bars->l_ready[i], 4);
+            mbar_init(&bars->l_free[i], 4);  // the epilogue warps have read 1/l
         }
         for (int i = 0; i < kSlots; ++i) {
             mbar_init(&bars->k_full[i], 1);
@@ -386,7 +387,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         float* nbk = reinterpret_cast<float*>(smem + kOffNbk) + x * BN;
         float* linv = reinterpret_cast<float*>(smem + kOffLinv) + x * BM;
         const uint64_t sl2x2 = f2pack(p.sl2, p.sl2);
-        uint32_t cs = 0;
+        uint32_t cs = 0, nit = 0;
         for (int idx = blockIdx.x; idx < p.n_items; idx += gridDim.x) {
             const Item it = make_item(p, idx);
             if (!it.has(x)) continue;
@@ -542,7 +543,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (lane == 0) mbar_arrive(&bars->p_ready[x]);
                 if (r == 0) FTR(x, 3 * (int)cs + 2);
             }
-            // Alg. 2 l.19-20: 1/l for the epilogue, LSE = m + ln l (natural log, bias included)
+            // Alg. 2 l.19-20: 1/l for the epilogue, LSE = m + ln l (natural log, bias included).
+            // linv is reused per item: wait until the epilogue has read the previous
+            // item's (a tile with a single key tile could otherwise run a phase ahead)
+            mbar_wait_park(&bars->l_free[x], (nit & 1) ^ 1);
+            ++nit;
             linv[r] = l > 0.f ? 1.f / l : 0.f;
             if (valid) p.LSE[((int64_t)it.b * p.H + it.h) * p.Nq + t] = (m_used + bq + __log2f(l)) * kLn2;
             __syncwarp();
@@ -563,6 +568,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (r == 0) FTR(5, (int)(4 * (nit0 + nit1)) + 1);
             tc_fence_after();
             const float inv = linv_all[x * BM + r];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bars->l_free[x]);
             uint8_t* ehi = smem + kOffE;
             const uint32_t sbf = smem_u32(ehi), sf = smem_u32(ehi + kTile);
             const uint32_t o_col = 256 + 128 * x;
