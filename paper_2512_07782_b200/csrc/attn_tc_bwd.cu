@@ -23,8 +23,6 @@
 // transpose-reduce (after dS is handed to the MMA warp) and a cross-warp sum by
 // the drain warpgroup, so both sums see the same fp32 dS and sum_m dU_m
 // telescopes to zero.  dK, dV leave through smem + TMA stores.
-#include <vector>
-
 #include "attn_common.cuh"
 #include "sm100.cuh"
 #include "tma_host.cuh"
@@ -61,15 +59,8 @@ struct TcBwdParams {
     int64_t Nq, Nkv, h0, H;
     int w;
     float sl2, scale;
-    long long* trace;  // diagnostics only (GFWA_TRACE_BWD): per-CTA clock64 stamps
     unsigned long long* token;  // prepared-workspace token: consumed (cleared) by this kernel
 };
-
-#define GFWA_TR(slot)                                                                                         \
-    do {                                                                                                      \
-        if (p.trace)                                                                                          \
-            p.trace[((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 64 + (slot)] = clock64(); \
-    } while (0)
 
 struct __align__(8) Bars {
     uint64_t kv_full;
@@ -148,7 +139,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     // the pre kernel has read the token (stream order): clear it, so the next backward
     // on this workspace zeroes its accumulator unless a new gfwa_fwd_train prepares it
     if (p.token && threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) *p.token = 0ull;
-    if (threadIdx.x == 0) GFWA_TR(0);
 
     if (warp == 13) {
         // ------------------------------------------------ producer: TMA + per-step vectors
@@ -195,7 +185,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         auto mma2 = [&](int m) {  // gradients of step m
             const int bm = m & 1, sm = m % NQS;
             mbar_wait(&bars->ds_ready[bm], (m >> 1) & 1);
-            if (m < 8 && lane == 0) GFWA_TR(17 + m);
             tc_fence_after();
             if (elect_one()) {
                 const uint32_t buf = tmem + 128 * bm;
@@ -254,7 +243,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int bn = n & 1, s = n % NQS;
             const int64_t t0 = (qt_lo + n) * BMQ;
             mbar_wait(&bars->st_full[bn], (n >> 1) & 1);
-            if (n < 8 && threadIdx.x == 0) GFWA_TR(1 + n);
             tc_fence_after();
             const uint32_t scol = 128 * bn + 32 * wg;  // this WG's S^T columns (dP^T at +64)
             // keys in (g - w, g] of each query g = t + h0, as a column range
@@ -269,7 +257,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             const float* Dq = &s_D[s][32 * wg];
             float ds[32];
             uint32_t pk[16], dk[16];
-#pragma unroll
             uint32_t sall[32], dall[32];  // all four TMEM loads in flight before one wait
             tmem_ld32(lane_addr + scol, sall);
             tmem_ld32(lane_addr + scol + 64, dall);
@@ -279,8 +266,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_before();
             named_bar_sync(5, 256);
             tc_fence_after();
-            const bool trw = (n == 4 && threadIdx.x == 0);
-            if (trw) GFWA_TR(43);
             for (int h16 = 0; h16 < 32; h16 += 16) {
                 const uint32_t* s16 = sall + h16;
                 const uint32_t* d16 = dall + h16;
@@ -327,7 +312,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
             }
-            if (trw) GFWA_TR(44);
             tmem_st16(lane_addr + 128 * bn + 16 * wg, pk);       // P^T  -> columns [0,32)
             tmem_st16(lane_addr + 128 * bn + 32 + 16 * wg, dk);  // dS^T -> columns [32,64)
             {  // dS^T row -> smem (128B-swizzled MN-major: row = key, 16-B chunk of 8 queries ^ key%8)
@@ -337,14 +321,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                     sts128(sb + (((4 * wg + c) ^ (kr & 7)) * 16),
                            make_uint4(dk[4 * c], dk[4 * c + 1], dk[4 * c + 2], dk[4 * c + 3]));
             }
-            if (trw) GFWA_TR(45);
             tmem_wait_st();
             fence_proxy_async();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&bars->ds_ready[bn]);
-            if (n < 8 && threadIdx.x == 0) GFWA_TR(9 + n);
-            if (trw) GFWA_TR(46);
             // du^q partial over this warp's 32 keys, off the MMA's critical path (the
             // gradient contractions of step n are already running): butterfly
             // transpose-reduce -> lane l holds query 32 wg + l; the drain warpgroup
@@ -363,7 +344,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             s_red[bn][wg][warp & 3][lane] = ds[0];
             __syncwarp();
             if (lane == 0) mbar_arrive(&bars->red_ready[bn]);
-            if (trw) GFWA_TR(47);
         }
         {
             float c0, c1;
@@ -377,7 +357,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float mul = wg == 0 ? 1.f : p.scale;
         if (nsteps > 0) {
             mbar_wait(&bars->dkdv_full, 0);
-            if (threadIdx.x == 0) GFWA_TR(41);
             tc_fence_after();
         }
         // two halves of 64 columns: both TMEM loads of a half in flight before one
@@ -416,7 +395,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (kr == 0) {
             bulk_wait_read0();
-            if (wg == 0) GFWA_TR(42);
         }
     } else if (warp < 12) {
         // ------------------------------------------------ dQ drain: thread = head-dim lane
@@ -447,7 +425,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int bm = m & 1;
             const int64_t t0 = (qt_lo + m) * BMQ;
             mbar_wait(&bars->dq_full[bm], (m >> 1) & 1);
-            if (m < 8 && dl == 0) GFWA_TR(25 + m);
             tc_fence_after();
             uint32_t v[4][16];
 #pragma unroll
@@ -457,7 +434,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&bars->dq_drained[bm]);
-            if (m < 8 && dl == 0) GFWA_TR(33 + m);
             if (m > 0) combine_duq(m - 1);  // the previous step's partials are in smem by now
             // four rounds of 16 queries; row = query (128 B = this warp's 32 d),
             // 16-B chunk (d%32)/4 ^ (query%8), word d%4
@@ -476,7 +452,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                     bulk_commit();
                 }
             }
-            if (m < 8 && dl == 0) GFWA_TR(49 + m);
         }
         if (nsteps > 0) combine_duq(nsteps - 1);
         if (lane == 0) bulk_wait0();  // reductions complete before the CTA exits
@@ -650,25 +625,8 @@ gfwa_status_t tc_bwd(const AttnParams& pin, cudaStream_t st, void* ws) {
             cudaFuncSetAttribute(bwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes)))
         return s;
     dim3 grid((unsigned)((p.Nkv + BN - 1) / BN), (unsigned)p.H, (unsigned)p.B);
-    const char* trace_file = getenv("GFWA_TRACE_BWD");  // diagnostics (synchronous)
-    const size_t n_cta = (size_t)grid.x * grid.y * grid.z;
-    tp.trace = nullptr;
-    if (trace_file) {
-        cudaMalloc(&tp.trace, n_cta * 64 * sizeof(long long));
-        cudaMemsetAsync(tp.trace, 0, n_cta * 64 * sizeof(long long), st);
-    }
     bwd_tc_kernel<<<grid, kThreads, kSmemBytes, st>>>(mq, mk, mv, mdo, mdk, mdv, mdq, tp);
     note_launch();
-    if (trace_file) {
-        std::vector<long long> hbuf(n_cta * 64);
-        cudaStreamSynchronize(st);
-        cudaMemcpy(hbuf.data(), tp.trace, hbuf.size() * sizeof(long long), cudaMemcpyDeviceToHost);
-        cudaFree(tp.trace);
-        if (FILE* f = fopen(trace_file, "wb")) {
-            fwrite(hbuf.data(), sizeof(long long), hbuf.size(), f);
-            fclose(f);
-        }
-    }
     if (gfwa_status_t s = check_launch()) return s;
     stage_event(1, st);  // measurement hook: after the main kernel
     const bool dq_flat = p.qs[2] == D && p.qs[1] == p.H * D && p.qs[0] == p.Nq * p.H * D;

@@ -45,7 +45,22 @@ def main():
         print(f"{tag} {wl} fwd {ms*1e3:8.1f} us  {fl/ms/1e9:7.1f} TFLOP/s")
     if what in ("bwd", "both"):
         ms = timeit(lambda: gb.gfwa_bwd(Q, K, V, U, O, LSE, dO, s.w, O_lo=Olo, want_dalpha=False))
-        print(f"{tag} {wl} bwd {ms*1e3:8.1f} us  {2.5*fl/ms/1e9:7.1f} TFLOP/s")
+        # the main kernel alone (stage events recorded by the library between its kernels)
+        parts = []
+        for _ in range(10):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            sev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            for x in sev:
+                x.record()
+            a.record()
+            gb.debug_stage_events(sev)
+            gb.gfwa_bwd(Q, K, V, U, O, LSE, dO, s.w, O_lo=Olo, want_dalpha=False)
+            b.record()
+            torch.cuda.synchronize()
+            parts.append((a.elapsed_time(sev[0]), sev[0].elapsed_time(sev[1]), sev[1].elapsed_time(b)))
+        pre, main_, post = (sorted(x)[len(x) // 2] for x in zip(*parts))
+        print(f"{tag} {wl} bwd {ms*1e3:8.1f} us  {2.5*fl/ms/1e9:7.1f} TFLOP/s  (pre {pre*1e3:.1f}, main "
+              f"{main_*1e3:.1f} us = {2.5*fl/main_/1e9:.1f} TFLOP/s = {2.5*fl/main_/1e9/1627.2:.3f} of peak, post {post*1e3:.1f})")
 
 
 if __name__ == "__main__":
