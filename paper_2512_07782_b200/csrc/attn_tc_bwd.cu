@@ -9,9 +9,9 @@
 //   S^T  = K Q^T          SS  M=128 keys, N=64 queries   -> buf[n&1] cols [0,64)
 //   dP^T = V dO^T         SS                             -> buf[n&1] cols [64,128)
 //   (softmax-grad, 2 warpgroups x 32 queries, thread = key: P^T = exp(S - L),
-//    dS^T = P^T (dP^T - D); after both warpgroups hold their columns in
-//    registers, P^T and dS^T go back to TMEM as bf16, packed into [0,32) and
-//    [32,64), dS^T also to smem)
+//    dS^T = P^T (dP^T - D); each warpgroup packs its P^T and dS^T back to TMEM
+//    as bf16 over its own 32 S^T columns (P^T in the first 16, dS^T in the
+//    next 16: no cross-warpgroup barrier), dS^T also to smem)
 //   dQ^T = K^T dS^T       SS  M=128 (d), N=64             -> the freed [64,128)
 //   dV  += P^T dO         TS  (A = P^T from TMEM)         -> TMEM [256,384)
 //   dK  += dS^T Q         TS  (A = dS^T from TMEM)        -> TMEM [384,512)
@@ -195,13 +195,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mma_ss(buf + 64, sdesc_sw128(kb + kk * 2048, kKV / 2, 1024),
                            sdesc_sw128(sb + kk * 2048, 8192, 1024), id_dq, kk > 0 ? 1u : 0u);
                 tc_commit(&bars->dq_full[bm]);
-                // dV += P^T dO ; dK += dS^T Q   (P^T in columns [0,32), dS^T in [32,64):
-                // 16 queries = 8 TMEM columns per K step)
+                // dV += P^T dO ; dK += dS^T Q   (P^T and dS^T of queries [32 g, 32 g + 32) in
+                // columns [32 g, 32 g + 16) and [32 g + 16, 32 g + 32); 16 queries = 8 columns per K step)
 #pragma unroll
                 for (int kk = 0; kk < BMQ / 16; ++kk) {
                     const uint32_t acc = (m > 0 || kk > 0) ? 1u : 0u;
-                    mma_ts(tmem + 256, buf + 8 * kk, sdesc_sw128(ob + kk * 2048, kQT / 2, 1024), id_tm, acc);
-                    mma_ts(tmem + 384, buf + 32 + 8 * kk, sdesc_sw128(qb + kk * 2048, kQT / 2, 1024), id_tm, acc);
+                    // queries [16 kk, 16 kk + 16): warpgroup kk / 2's columns, half kk % 2
+                    const uint32_t pc = 32 * (kk >> 1) + 8 * (kk & 1);
+                    mma_ts(tmem + 256, buf + pc, sdesc_sw128(ob + kk * 2048, kQT / 2, 1024), id_tm, acc);
+                    mma_ts(tmem + 384, buf + pc + 16, sdesc_sw128(qb + kk * 2048, kQT / 2, 1024), id_tm, acc);
                 }
                 tc_commit(&bars->q_empty[sm]);
                 if (m == nsteps - 1) tc_commit(&bars->dkdv_full);
@@ -261,11 +263,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             tmem_ld32(lane_addr + scol, sall);
             tmem_ld32(lane_addr + scol + 64, dall);
             tmem_wait_ld();
-            // both warpgroups hold their S^T / dP^T columns in registers before
-            // either packs P^T, dS^T into [0,64): dQ^T then gets [64,128) whole
-            tc_fence_before();
-            named_bar_sync(5, 256);
-            tc_fence_after();
+            // each warpgroup packs its P^T, dS^T over its own S^T columns (no
+            // cross-warpgroup barrier); dQ^T then gets [64,128) whole
             for (int h16 = 0; h16 < 32; h16 += 16) {
                 const uint32_t* s16 = sall + h16;
                 const uint32_t* d16 = dall + h16;
@@ -312,8 +311,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
             }
-            tmem_st16(lane_addr + 128 * bn + 16 * wg, pk);       // P^T  -> columns [0,32)
-            tmem_st16(lane_addr + 128 * bn + 32 + 16 * wg, dk);  // dS^T -> columns [32,64)
+            tmem_st16(lane_addr + 128 * bn + 32 * wg, pk);       // P^T  -> columns [32 wg, 32 wg + 16)
+            tmem_st16(lane_addr + 128 * bn + 32 * wg + 16, dk);  // dS^T -> columns [32 wg + 16, 32 wg + 32)
             {  // dS^T row -> smem (128B-swizzled MN-major: row = key, 16-B chunk of 8 queries ^ key%8)
                 const uint32_t sb = smem_u32(dSs + bn * kDS) + kr * 128;
 #pragma unroll
