@@ -12,8 +12,6 @@
 //               the tile's last S MMA has read it), K_j and V_j through one ring
 //               of three tile slots (evict-last: re-read by ~w/128 neighbouring
 //               items);
-//               gfwa_fwd_train: also zeroes the item's rows of the backward's dQ
-//               accumulator with coalesced stores (the lanes are idle otherwise)
 //   warp 12     MMA issuer (one elected lane), ping-pong over the two tiles:
 //                 O_A += P_A V_{n-1};  S_A = Q_A K_n^T;
 //                 O_B += P_B V_{n-1};  S_B = Q_B K_n^T
@@ -33,7 +31,8 @@
 //               the training forward, its bf16 residual O_lo = bf16(O/l - O)
 //               (staged in a 32 KB buffer; O + O_lo carries O to ~2^-17, which
 //               is what the backward's D = rowsum(O dO) needs, reading C-12),
-//               written by TMA stores
+//               written by TMA stores; gfwa_fwd_train: it also zeroes the tile's
+//               rows of the backward's dQ accumulator (coalesced 512-byte rows)
 //   warps 14-15 training forward: the in-place fp16 conversion of every V tile
 //               (reading C-23: P and V in fp16 for the PV product, so the fp32 O
 //               that D = rowsum(O dO) is taken from carries 8x less P rounding
@@ -258,16 +257,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                     __syncwarp();
                 }
                 ++kc;
-            }
-            if (p.zero_acc) {
-                // gfwa_fwd_train: zero this item's rows of the backward's fp32 dQ
-                // accumulator [B, Nq, H, d] (one 512-byte row per warp store)
-                const int r1 = min(it.r0 + 2 * BM, (int)p.Nq);
-                for (int t = it.r0; t < r1; ++t) {
-                    float4* row = reinterpret_cast<float4*>(
-                        p.zero_acc + (((int64_t)it.b * p.Nq + t) * p.H + it.h) * D);
-                    row[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
-                }
             }
         }
         if (p.zero_acc && blockIdx.x == 0 && lane == 0) *p.token = p.token_val;
@@ -614,6 +603,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                         if (p.store_lo) tma_store_4d(&mol, ehi + kTile + hf * (kTile / 2), hf * 64, it.h, row0, it.b);
                         bulk_commit();
                     }
+                }
+            }
+            if (p.zero_acc) {
+                // gfwa_fwd_train: zero this tile's rows of the backward's fp32 dQ accumulator
+                // [B, Nq, H, d] while the stores drain (one 512-byte row per warp store;
+                // this warpgroup is otherwise idle between epilogues)
+                const int r1 = min(it.r0 + x * BM + BM, (int)p.Nq);
+                for (int t = it.r0 + x * BM + ew; t < r1; t += 4) {
+                    float4* row = reinterpret_cast<float4*>(p.zero_acc + (((int64_t)it.b * p.Nq + t) * p.H + it.h) * D);
+                    row[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
                 }
             }
             if (r == 0) {
