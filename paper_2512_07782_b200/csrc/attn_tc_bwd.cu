@@ -245,6 +245,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int bn = n & 1, s = n % NQS;
             const int64_t t0 = (qt_lo + n) * BMQ;
             mbar_wait(&bars->st_full[bn], (n >> 1) & 1);
+            // the producer's per-step vectors (s_cq, s_D): acquire them from its own
+            // arrive (already complete) rather than through the tensor core's commit
+            mbar_wait(&bars->q_full[s], (n / NQS) & 1);
             tc_fence_after();
             const uint32_t scol = 128 * bn + 32 * wg;  // this WG's S^T columns (dP^T at +64)
             // keys in (g - w, g] of each query g = t + h0, as a column range

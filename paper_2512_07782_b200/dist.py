@@ -34,7 +34,7 @@ import torch.distributed as dist
 
 @dataclass
 class Ops:
-    gate_prefix: Callable   # (h, beta, eps) -> U [B,H,S] fp32 (carry 0)
+    gate_prefix: Callable   # (h, beta, eps) -> (U [B,H,S] fp32 (carry 0), total = sum alpha [B,H] fp64)
     fwd: Callable           # (Q, K, V, U, w) -> (O, LSE, O_lo)
     bwd: Callable           # (Q, K, V, U, O, LSE, dO, w, O_lo) -> (dQ, dK, dV, dU)
     gate_bwd: Callable      # (dU, h, beta, eps, carry fp64 [B,H] | None) -> (dalpha, dh, dbeta)
@@ -62,7 +62,7 @@ def cuda_ops() -> Ops:
     def _fwd_into(Q, K, V, U, w, O_out, Olo_out):
         return gb.gfwa_fwd(Q, K, V, U, w, out=O_out, out_lo=Olo_out)[1]
 
-    return Ops(gate_prefix=lambda h, b, eps: gb.gfwa_gate_prefix(h, b, eps), fwd=_fwd, bwd=_bwd,
+    return Ops(gate_prefix=lambda h, b, eps: gb.gfwa_gate_prefix(h, b, eps, want_total=True), fwd=_fwd, bwd=_bwd,
                gate_bwd=_gate_bwd, fwd_into=_fwd_into)
 
 
@@ -123,6 +123,7 @@ class ShardResult:
     dh: torch.Tensor
     dbeta: torch.Tensor
     dU: torch.Tensor = None  # this rank's rows, halo contributions of rank r+1 added
+    U_offset: torch.Tensor = None  # P_r = sum of earlier ranks' gate totals [B,H] fp64: U = U_loc - P_r
 
 
 def halo_pack(K, V, U_loc, w: int):
@@ -132,14 +133,32 @@ def halo_pack(K, V, U_loc, w: int):
             (U_loc[..., S - w:] - U_loc[..., S - 1:S]).contiguous()]
 
 
-def global_offset(total: torch.Tensor, ring: Ring) -> torch.Tensor:
-    """P_r = sum of the earlier ranks' gate totals (exclusive scan, fp64)."""
-    allt = [torch.empty_like(total) for _ in range(ring.world)]
-    dist.all_gather(allt, total.contiguous(), group=ring.group)
-    out = torch.zeros_like(total)
+def global_offset_start(total: torch.Tensor, ring: Ring):
+    """Post the cross-rank exclusive scan of the gate totals (north_star's "running
+    gate-sum offset"): an all-gather of the [B,H] fp64 totals, asynchronous so it
+    overlaps the attention calls; finish with global_offset_finish."""
+    dev = total.device
+    t = total.detach().to(torch.float64).contiguous()
+    if ring.stage:  # gloo moves host tensors
+        t = t.cpu()
+    allt = [torch.empty_like(t) for _ in range(ring.world)]
+    work = dist.all_gather(allt, t, group=ring.group, async_op=True)
+    return work, allt, dev
+
+
+def global_offset_finish(handle, ring: Ring) -> torch.Tensor:
+    """P_r = sum_{r' < r} total_{r'} (exclusive prefix, fp64), on the totals' device."""
+    work, allt, dev = handle
+    work.wait()
+    out = torch.zeros_like(allt[0])
     for r in range(ring.rank):
         out += allt[r]
-    return out
+    return out.to(dev)
+
+
+def global_offset(total: torch.Tensor, ring: Ring) -> torch.Tensor:
+    """P_r = sum of the earlier ranks' gate totals (exclusive scan, fp64)."""
+    return global_offset_finish(global_offset_start(total, ring), ring)
 
 
 def alloc_kv_ext(K: torch.Tensor, V: torch.Tensor, w: int):
@@ -167,7 +186,10 @@ def sp_forward_backward(Q, K, V, h, beta, dO, w: int, ops: Ops, ring: Ring, eps:
     if w > S:
         raise ValueError(f"sequence sharding needs w <= rows per rank ({w} > {S})")
     r, P = ring.rank, ring.world
-    U_loc = ops.gate_prefix(h, beta, eps)
+    U_loc, total = ops.gate_prefix(h, beta, eps)
+    # the running gate-sum offset of this shard (global U = U_loc - P_r): posted now,
+    # collected after the backward (the attention only uses local frames, C-10)
+    scan = global_offset_start(total, ring) if P > 1 else None
     # forward halo r -> r+1 (K, V, u in the receiver's frame)
     like = halo_pack(K, V, U_loc, w)
     handle = ring.start(like if r < P - 1 else None, like, forward=True)
@@ -216,4 +238,5 @@ def sp_forward_backward(Q, K, V, h, beta, dO, w: int, ops: Ops, ring: Ring, eps:
         dU[..., S - w:] += back[2]
         carry = back[2].double().sum(-1)  # d-alpha carry = +sum_j dU_halo(j)
     dalpha, dh, dbeta = ops.gate_bwd(dU, h, beta, eps, carry)
-    return ShardResult(O, LSE, U_loc, dQ, dK, dV, dalpha, dh, dbeta, dU)
+    U_offset = global_offset_finish(scan, ring) if scan is not None else torch.zeros_like(total, dtype=torch.float64)
+    return ShardResult(O, LSE, U_loc, dQ, dK, dV, dalpha, dh, dbeta, dU, U_offset)

@@ -23,7 +23,8 @@ def _oracle_ops():
     t = lambda a: torch.from_numpy(np.asarray(a))  # noqa: E731
 
     def gate_prefix(h, beta, eps):
-        return t(oracle.gate_prefix_hbeta(h, beta, eps)[0])
+        U, total, _ = oracle.gate_prefix_hbeta(h, beta, eps)
+        return t(U), t(total)
 
     def fwd(Q, K, V, U, w):
         O, L = oracle.fwd(Q, K, V, U, w)
@@ -72,7 +73,8 @@ def _worker(rank, world, port, outdir, B, N, H, d, w, use_ext=False):
             kv_ext, Kl, Vl = alloc_kv_ext(Kl, Vl, w)
         res = sp_forward_backward(Q[:, sl], Kl, Vl, h[:, sl], beta[:, sl], dO[:, sl], w, _oracle_ops(),
                                   Ring(), kv_ext=kv_ext)
-        torch.save({k: getattr(res, k) for k in ("O", "LSE", "U_loc", "dQ", "dK", "dV", "dalpha", "dh", "dbeta")},
+        torch.save({k: getattr(res, k) for k in ("O", "LSE", "U_loc", "U_offset", "dQ", "dK", "dV", "dalpha", "dh",
+                                                 "dbeta")},
                    os.path.join(outdir, f"r{rank}.pt"))
     finally:
         dist.destroy_process_group()
@@ -102,9 +104,11 @@ def test_sequence_sharded_matches_unsharded(world, N, w, use_ext):
             assert np.allclose(res["dalpha"].numpy(), g["dalpha"][..., sl], atol=1e-10)
             assert np.allclose(res["dh"].numpy(), dh[:, sl], atol=1e-10)
             assert np.allclose(res["dbeta"].numpy(), db[:, sl], atol=1e-10)
-            # local frame: global U = U_loc - (earlier ranks' totals)
-            off = U[..., r * S - 1] if r > 0 else 0.0
-            assert np.allclose(res["U_loc"].numpy() + (off[..., None] if r > 0 else 0.0), U[..., sl], atol=1e-11)
+            # local frame: global U = U_loc - P_r, P_r = the cross-rank exclusive scan of
+            # the gate totals (returned by the step) = -U[r S - 1] of the unsharded scan
+            off = -U[..., r * S - 1] if r > 0 else np.zeros(U.shape[:2])
+            assert np.allclose(res["U_offset"].numpy(), off, atol=1e-11)
+            assert np.allclose(res["U_loc"].numpy() - res["U_offset"].numpy()[..., None], U[..., sl], atol=1e-11)
 
 
 def test_halo_larger_than_shard_is_rejected():

@@ -44,7 +44,9 @@ def _worker(rank, world, port, outdir, use_ext=False):
             kv_ext, Kl, Vl = alloc_kv_ext(Kl, Vl, W)
         res = sp_forward_backward(cu(Q), Kl, Vl, cu(h), cu(beta), cu(dO), W, cuda_ops(), Ring(), kv_ext=kv_ext)
         torch.cuda.synchronize()
-        torch.save({k: getattr(res, k).float().cpu() for k in ("O", "dQ", "dK", "dV", "dU", "dalpha")},
+        out = {k: getattr(res, k).float().cpu() for k in ("O", "dQ", "dK", "dV", "dU", "dalpha", "U_loc")}
+        out["U_offset"] = res.U_offset.double().cpu()
+        torch.save(out,
                    os.path.join(outdir, f"r{rank}.pt"))
     finally:
         dist.destroy_process_group()
@@ -68,6 +70,11 @@ def test_sequence_sharded_cuda_matches_oracle(use_ext):
             for k in ("dQ", "dK", "dV"):
                 assert np.abs(res[r][k].numpy() - g[k][:, sl]).max() <= TOL_BF16_GRAD, k
             assert np.abs(res[r]["dU"].numpy() - g["dU"][..., sl]).max() <= TOL_BF16_GRAD
+            # the cross-rank exclusive scan of the gate totals: global U = U_loc - P_r
+            off = -U[..., r * S - 1] if r > 0 else np.zeros(U.shape[:2])
+            assert np.abs(res[r]["U_offset"].numpy() - off).max() <= 1e-6 * max(1.0, np.abs(off).max())
+            U_glob = res[r]["U_loc"].double().numpy() - res[r]["U_offset"].numpy()[..., None]
+            assert np.abs(U_glob - U[..., sl]).max() <= 1e-6 * np.abs(U[..., sl]).max()
         # the sharded d-alpha must equal the exact (fp64) reverse scan of the
         # gathered dU -- which checks the cross-rank carry -- and the oracle's
         # d-alpha at north_star's gradient tolerance
