@@ -57,8 +57,7 @@ using namespace sm100;
 
 constexpr int BM = 128;  // query rows per tile (two tiles per item)
 constexpr int BN = 128;  // keys per tile
-constexpr int D = 128;   // head dim
-constexpr uint32_t kTile = BM * D * 2;  // 32 KB bf16 tile
+constexpr uint32_t kBox = BM * 64 * 2;  // one 16 KB TMA box: 128 rows x 64 bf16 (one 128-byte swizzle row)
 // 4 full warpgroups (setmaxnreg acts per warpgroup; the CTA register pool is
 // 512 x 128 = 64K): softmax A, softmax B, epilogue, {MMA, TMA, 2 V-convert warps}
 constexpr int kThreads = 512;
@@ -67,15 +66,19 @@ constexpr int kSoftmaxRegs = 184, kEpiRegs = 72, kOtherRegs = 72;  // 256*184 + 
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 constexpr int kPolyPairs = GFWA_FWD_POLY;  // of every 4 column pairs, how many use exp2_poly2
 
-// dynamic shared memory (1024-aligned base)
-constexpr uint32_t kOffQ = 0;                    // Q_A, Q_B
-constexpr uint32_t kOffKV = 2 * kTile;           // one K/V ring of 3 tile slots: K_0 V_0 K_1 V_1 ...
+// dynamic shared memory (1024-aligned base), per head dim D in {64, 128}
+template <int D>
+struct Lay {
+    static constexpr uint32_t kTile = BM * D * 2;           // one bf16 Q/K/V/O tile
+    static constexpr uint32_t kOffQ = 0;                    // Q_A, Q_B
+    static constexpr uint32_t kOffKV = 2 * kTile;           // one K/V ring of 3 tile slots: K_0 V_0 K_1 V_1 ...
+    static constexpr uint32_t kOffE = 5 * kTile;            // staging of the O tile, then of the O_lo tile
+    static constexpr uint32_t kOffNbk = 7 * kTile;          // [2 tiles][128] fp32 key biases
+    static constexpr uint32_t kOffLinv = kOffNbk + 2 * BN * 4;  // [2 tiles][128] 1/l
+    static constexpr uint32_t kOffBars = kOffLinv + 2 * BM * 4;
+    static constexpr size_t kSmemBytes = kOffBars + 256;
+};
 constexpr int kSlots = 3;
-constexpr uint32_t kOffE = 5 * kTile;            // 32 KB staging of the O tile, 32 KB of the O_lo tile
-constexpr uint32_t kOffNbk = 7 * kTile;          // [2 tiles][128] fp32 key biases
-constexpr uint32_t kOffLinv = kOffNbk + 2 * BN * 4;  // [2 tiles][128] 1/l
-constexpr uint32_t kOffBars = kOffLinv + 2 * BM * 4;
-constexpr size_t kSmemBytes = kOffBars + 256;
 
 struct __align__(8) Bars {
     uint64_t q_full[2], q_empty[2];
@@ -168,13 +171,17 @@ __device__ __forceinline__ Item make_item(const TcFwdParams& p, int idx) {
     return it;
 }
 
-template <bool kF16P>  // training forward (O_lo wanted): P, V in fp16 for the PV product (reading C-23)
+template <int D, bool kF16P>  // training forward (O_lo wanted): P, V in fp16 for the PV product (reading C-23)
 __global__ void __launch_bounds__(kThreads, 1)
     fwd_tc_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
                   const __grid_constant__ CUtensorMap mv, const __grid_constant__ CUtensorMap mo,
                   const __grid_constant__ CUtensorMap mol, const TcFwdParams p) {
     extern __shared__ __align__(1024) uint8_t smem[];
-    Bars* bars = (Bars*)(smem + kOffBars);
+    using L = Lay<D>;
+    constexpr uint32_t kTile = L::kTile, kOffQ = L::kOffQ, kOffKV = L::kOffKV, kOffE = L::kOffE,
+                       kOffNbk = L::kOffNbk, kOffLinv = L::kOffLinv;
+    constexpr int kHalves = D / 64;  // 64-column TMA boxes per tile row
+    Bars* bars = (Bars*)(smem + L::kOffBars);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         if (smem_u32(smem) & 1023u) __trap();  // the 128B-swizzle tiles need a 1024-aligned base
@@ -233,8 +240,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                         if (elect_one()) {
                             mbar_expect_tx(&bars->q_full[x], kTile);
                             uint8_t* dst = smem + kOffQ + x * kTile;
-                            for (int half = 0; half < 2; ++half)
-                                tma_load_4d(dst + half * (kTile / 2), &mq, &bars->q_full[x], half * 64, it.h,
+                            for (int half = 0; half < kHalves; ++half)
+                                tma_load_4d(dst + half * kBox, &mq, &bars->q_full[x], half * 64, it.h,
                                             it.r0 + x * BM, it.b);
                         }
                         __syncwarp();
@@ -250,8 +257,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (elect_one()) {
                         uint64_t* full = kv ? &bars->v_full[sl] : &bars->k_full[sl];
                         mbar_expect_tx(full, kTile);
-                        for (int half = 0; half < 2; ++half)
-                            tma_load_4d_hint(smem + kOffKV + sl * kTile + half * (kTile / 2), kv ? &mv : &mk, full,
+                        for (int half = 0; half < kHalves; ++half)
+                            tma_load_4d_hint(smem + kOffKV + sl * kTile + half * kBox, kv ? &mv : &mk, full,
                                              half * 64, it.h, j * BN, it.b, pol_kv);
                     }
                     __syncwarp();
@@ -295,7 +302,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                             for (int kk = 0; kk < BN / 16; ++kk)
                                 mma_ts(tmem + 256 + 128 * x, tmem + 128 * x + 8 * kk,
-                                       sdesc_sw128(vb + kk * 2048, kTile / 2, 1024), idesc_pv,
+                                       sdesc_sw128(vb + kk * 2048, kBox, 1024), idesc_pv,
                                        (!first_pv[x] || kk > 0) ? 1u : 0u);
                             if (j + 1 == it.jlo(x)) tc_commit(&bars->o_full[x]);
                         }
@@ -317,7 +324,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             const uint32_t kb = smem_u32(smem + kOffKV + sk * kTile);
 #pragma unroll
                             for (int kk = 0; kk < D / 16; ++kk) {
-                                const uint32_t off = (kk >> 2) * (kTile / 2) + (kk & 3) * 32;
+                                const uint32_t off = (kk >> 2) * kBox + (kk & 3) * 32;
                                 mma_ss(tmem + 128 * x, sdesc_sw128(qb + off, 16, 1024),
                                        sdesc_sw128(kb + off, 16, 1024), idesc_qk, kk > 0 ? 1u : 0u);
                             }
@@ -565,7 +572,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             // four rounds of 32 columns: O (bf16) into the Q slot, O_lo into E; each
             // 64-column half is stored as soon as it is staged
 #pragma unroll 1
-            for (int cq = 0; cq < 4; ++cq) {
+            for (int cq = 0; cq < D / 32; ++cq) {
                 uint32_t ob[32];
                 tmem_ld32(lane_addr + o_col + 32 * cq, ob);
                 tmem_wait_ld();
@@ -590,7 +597,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             lw[e] = pack_bf16x2(v0 - h0, v1 - h1);
                         }
                     }
-                    const uint32_t off = hf * (kTile / 2) + r * 128 + chunk * 16;
+                    const uint32_t off = hf * kBox + r * 128 + chunk * 16;
                     sts128(sbf + off, make_uint4(hw[0], hw[1], hw[2], hw[3]));
                     if (p.store_lo) sts128(sf + off, make_uint4(lw[0], lw[1], lw[2], lw[3]));
                 }
@@ -599,8 +606,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     named_bar_sync(3, 128);
                     if (r == 0) {
                         const int row0 = it.r0 + x * BM;
-                        tma_store_4d(&mo, ehi + hf * (kTile / 2), hf * 64, it.h, row0, it.b);
-                        if (p.store_lo) tma_store_4d(&mol, ehi + kTile + hf * (kTile / 2), hf * 64, it.h, row0, it.b);
+                        tma_store_4d(&mo, ehi + hf * kBox, hf * 64, it.h, row0, it.b);
+                        if (p.store_lo) tma_store_4d(&mol, ehi + kTile + hf * kBox, hf * 64, it.h, row0, it.b);
                         bulk_commit();
                     }
                 }
@@ -612,7 +619,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int r1 = min(it.r0 + x * BM + BM, (int)p.Nq);
                 for (int t = it.r0 + x * BM + ew; t < r1; t += 4) {
                     float4* row = reinterpret_cast<float4*>(p.zero_acc + (((int64_t)it.b * p.Nq + t) * p.H + it.h) * D);
-                    row[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (lane < D / 4) row[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
                 }
             }
             if (r == 0) {
@@ -650,13 +657,14 @@ extern "C" int gfwa_debug_fwd_trace(long long* host, size_t n) {
 #endif
 
 bool tc_fwd_supported(const AttnParams& p, gfwa_dtype_t dt) {
-    if (dt != GFWA_BF16 || p.d != D) return false;
+    if (dt != GFWA_BF16 || (p.d != 64 && p.d != 128)) return false;
     if (p.Nkv >= ((int64_t)1 << 31) || p.H >= 65536 || p.B >= 65536) return false;
     if (const char* e = getenv("GFWA_FORCE_SIMT")) return e[0] == '0';
     return true;
 }
 
-gfwa_status_t tc_fwd(const AttnParams& p, cudaStream_t st) {
+template <int D>
+static gfwa_status_t tc_fwd_d(const AttnParams& p, cudaStream_t st) {
     CUtensorMap mq, mk, mv, mo, mol;
     GFWA_REQUIRE(encode_bnhd_map(&mq, p.Q, p.B, p.Nq, p.H, D, p.qs, BM));
     GFWA_REQUIRE(encode_bnhd_map(&mk, p.K, p.B, p.Nkv, p.H, D, p.ks, BN));
@@ -687,7 +695,8 @@ gfwa_status_t tc_fwd(const AttnParams& p, cudaStream_t st) {
     int dev = 0, n_sm = 148;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
     // per launch: the attribute is per device (a process may drive several GPUs)
-    auto kern = tp.store_lo ? fwd_tc_kernel<true> : fwd_tc_kernel<false>;
+    auto kern = tp.store_lo ? fwd_tc_kernel<D, true> : fwd_tc_kernel<D, false>;
+    constexpr size_t kSmemBytes = Lay<D>::kSmemBytes;
     if (gfwa_status_t s = check_launch(
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes)))
         return s;
@@ -697,6 +706,10 @@ gfwa_status_t tc_fwd(const AttnParams& p, cudaStream_t st) {
     kern<<<grid, kThreads, kSmemBytes, st>>>(mq, mk, mv, mo, mol, tp);
     note_launch();
     return check_launch();
+}
+
+gfwa_status_t tc_fwd(const AttnParams& p, cudaStream_t st) {
+    return p.d == 64 ? tc_fwd_d<64>(p, st) : tc_fwd_d<128>(p, st);
 }
 
 }  // namespace gfwa

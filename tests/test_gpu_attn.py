@@ -75,6 +75,10 @@ BF16_SHAPES = [
     synth.AttnShape(B=1, H=2, N=300, d=128, w=250, N_kv=500),  # halo of 200 rows (not tile-aligned)
     synth.AttnShape(B=1, H=2, N=390, d=128, w=1000),      # w >= N with a ragged tail
     synth.AttnShape(B=1, H=2, N=129, d=128, w=129, N_kv=129 + 70),  # ragged halo, w = N
+    # head dim 64 (the paper's models: n_heads/d_head 12/64, 16/64) on tcgen05
+    synth.AttnShape(B=2, H=2, N=700, d=64, w=300),
+    synth.AttnShape(B=1, H=3, N=37, d=64, w=33),
+    synth.AttnShape(B=1, H=2, N=300, d=64, w=250, N_kv=500),
 ]
 
 
