@@ -576,7 +576,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 uint32_t ob[32];
                 tmem_ld32(lane_addr + o_col + 32 * cq, ob);
                 tmem_wait_ld();
-                if (cq == 3) {  // all of O_X has been read: release its columns
+                if (cq == D / 32 - 1) {  // all of O_X has been read: release its columns
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&bars->o_free[x]);
