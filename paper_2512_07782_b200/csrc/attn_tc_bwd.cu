@@ -34,12 +34,20 @@ using namespace sm100;
 
 constexpr int BN = 128;   // keys per CTA
 constexpr int BMQ = 64;   // queries per step
-constexpr int D = 128;
 constexpr int NQS = 3;    // Q/dO ring stages
 constexpr uint32_t kDQ = 32 * 128 * 4;    // 16 KB dQ staging: 4 warps x 2 x (16 queries x 32 d) fp32
 constexpr uint32_t kDQW = 16 * 32 * 4;    // 2 KB: one drain warp's box
-constexpr uint32_t kKV = 128 * 128 * 2;   // 32 KB K or V tile
-constexpr uint32_t kQT = 64 * 128 * 2;    // 16 KB Q or dO tile
+constexpr uint32_t kKVbox = 128 * 64 * 2;  // 16 KB: 128 key rows x 64 d (one 128-byte swizzle row)
+constexpr uint32_t kQTbox = 64 * 64 * 2;   // 8 KB: 64 query rows x 64 d
+// per head dim D in {64, 128}: the K slot is always 128 d wide (for D = 64 its
+// second half is zeros, so K^T is the M = 128 A operand of dQ^T = K^T dS^T and
+// dQ^T rows 64..127 come out zero); V, Q, dO tiles are D wide
+template <int D>
+struct BwdLay {
+    static constexpr uint32_t kKslot = 2 * kKVbox;  // 32 KB
+    static constexpr uint32_t kV = 128 * D * 2;
+    static constexpr uint32_t kQT = 64 * D * 2;      // Q or dO tile
+};
 constexpr uint32_t kDS = 128 * 64 * 2;    // 16 KB dS^T tile
 constexpr int kThreads = 448;             // 2 softmax-grad WGs, drain WG, MMA warp, TMA warp
 #ifndef GFWA_BWD_NODQ
@@ -80,6 +88,7 @@ __device__ __forceinline__ uint32_t range_bits(int lo, int hi, int base) {
     return upto_z & ~below_a;
 }
 
+template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
     bwd_tc_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
                   const __grid_constant__ CUtensorMap mv, const __grid_constant__ CUtensorMap mdo,
@@ -88,8 +97,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                   const TcBwdParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    constexpr uint32_t kKV = BwdLay<D>::kV, kQT = BwdLay<D>::kQT;
+    constexpr int kHalves = D / 64;      // 64-column TMA boxes per row
     uint8_t* Ks = smem;
-    uint8_t* Vs = Ks + kKV;
+    uint8_t* Vs = Ks + BwdLay<D>::kKslot;
     uint8_t* Qs = Vs + kKV;              // NQS stages of [Q tile | dO tile]
     uint8_t* dSs = Qs + NQS * 2 * kQT;   // 2 x dS^T tile
     uint8_t* dQs = dSs + 2 * kDS;        // dQ staging: per drain warp 2 x [16 queries][32 d] fp32, 128B swizzle
@@ -127,6 +138,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_init(&bars->dkdv_full, 1);
         fence_barrier_init();
     }
+    if (D < 128) {  // the zero second half of the K slot (K^T rows d >= D of the dQ^T MMA)
+        for (uint32_t i = threadIdx.x; i < kKVbox / 16; i += kThreads)
+            sts128(smem_u32(Ks + kKVbox) + i * 16, make_uint4(0u, 0u, 0u, 0u));
+        fence_proxy_async();
+    }
     if (warp == 12) {
         tmem_alloc(tmem_sh, 512);
         tmem_relinquish();
@@ -145,9 +161,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (nsteps > 0) {
             if (elect_one()) {
                 mbar_expect_tx(&bars->kv_full, 2 * kKV);
-                for (int half = 0; half < 2; ++half) {
-                    tma_load_4d(Ks + half * (kKV / 2), &mk, &bars->kv_full, half * 64, (int)h, (int)j0, (int)b);
-                    tma_load_4d(Vs + half * (kKV / 2), &mv, &bars->kv_full, half * 64, (int)h, (int)j0, (int)b);
+                for (int half = 0; half < kHalves; ++half) {
+                    tma_load_4d(Ks + half * kKVbox, &mk, &bars->kv_full, half * 64, (int)h, (int)j0, (int)b);
+                    tma_load_4d(Vs + half * kKVbox, &mv, &bars->kv_full, half * 64, (int)h, (int)j0, (int)b);
                 }
             }
             __syncwarp();
@@ -158,9 +174,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (elect_one()) {
                     mbar_expect_tx(&bars->q_full[s], 2 * kQT);
                     uint8_t* qd = Qs + s * 2 * kQT;
-                    for (int half = 0; half < 2; ++half) {
-                        tma_load_4d(qd + half * (kQT / 2), &mq, &bars->q_full[s], half * 64, (int)h, (int)t0, (int)b);
-                        tma_load_4d(qd + kQT + half * (kQT / 2), &mdo, &bars->q_full[s], half * 64, (int)h, (int)t0,
+                    for (int half = 0; half < kHalves; ++half) {
+                        tma_load_4d(qd + half * kQTbox, &mq, &bars->q_full[s], half * 64, (int)h, (int)t0, (int)b);
+                        tma_load_4d(qd + kQT + half * kQTbox, &mdo, &bars->q_full[s], half * 64, (int)h, (int)t0,
                                     (int)b);
                     }
                 }
@@ -192,7 +208,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // dQ^T = K^T dS^T, one N = 64 chain into the freed columns [64,128)
 #pragma unroll
                 for (int kk = 0; kk < BN / 16; ++kk)
-                    mma_ss(buf + 64, sdesc_sw128(kb + kk * 2048, kKV / 2, 1024),
+                    mma_ss(buf + 64, sdesc_sw128(kb + kk * 2048, kKVbox, 1024),
                            sdesc_sw128(sb + kk * 2048, 8192, 1024), id_dq, kk > 0 ? 1u : 0u);
                 tc_commit(&bars->dq_full[bm]);
                 // dV += P^T dO ; dK += dS^T Q   (P^T and dS^T of queries [32 g, 32 g + 32) in
@@ -202,8 +218,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint32_t acc = (m > 0 || kk > 0) ? 1u : 0u;
                     // queries [16 kk, 16 kk + 16): warpgroup kk / 2's columns, half kk % 2
                     const uint32_t pc = 32 * (kk >> 1) + 8 * (kk & 1);
-                    mma_ts(tmem + 256, buf + pc, sdesc_sw128(ob + kk * 2048, kQT / 2, 1024), id_tm, acc);
-                    mma_ts(tmem + 384, buf + pc + 16, sdesc_sw128(qb + kk * 2048, kQT / 2, 1024), id_tm, acc);
+                    mma_ts(tmem + 256, buf + pc, sdesc_sw128(ob + kk * 2048, kQTbox, 1024), id_tm, acc);
+                    mma_ts(tmem + 384, buf + pc + 16, sdesc_sw128(qb + kk * 2048, kQTbox, 1024), id_tm, acc);
                 }
                 tc_commit(&bars->q_empty[sm]);
                 if (m == nsteps - 1) tc_commit(&bars->dkdv_full);
@@ -220,8 +236,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t buf = tmem + 128 * bn;
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk) {
-                    const uint32_t ka = (kk >> 2) * (kKV / 2) + (kk & 3) * 32;
-                    const uint32_t qa = (kk >> 2) * (kQT / 2) + (kk & 3) * 32;
+                    const uint32_t ka = (kk >> 2) * kKVbox + (kk & 3) * 32;
+                    const uint32_t qa = (kk >> 2) * kQTbox + (kk & 3) * 32;
                     mma_ss(buf, sdesc_sw128(kb + ka, 16, 1024), sdesc_sw128(qb + qa, 16, 1024), id_st, kk > 0);
                     mma_ss(buf + 64, sdesc_sw128(vb + ka, 16, 1024), sdesc_sw128(ob + qa, 16, 1024), id_st, kk > 0);
                 }
@@ -364,7 +380,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // two halves of 64 columns: both TMEM loads of a half in flight before one
         // wait, each half's TMA store issued as soon as it is staged
 #pragma unroll 1
-        for (int hf = 0; hf < 2; ++hf) {
+        for (int hf = 0; hf < kHalves; ++hf) {
             uint32_t v2[2][32];
             if (nsteps > 0) {
                 tmem_ld32(lane_addr + acol + 64 * hf, v2[0]);
@@ -385,13 +401,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                     pkv.y = pack_bf16x2(__uint_as_float(v[8 * k + 2]) * mul, __uint_as_float(v[8 * k + 3]) * mul);
                     pkv.z = pack_bf16x2(__uint_as_float(v[8 * k + 4]) * mul, __uint_as_float(v[8 * k + 5]) * mul);
                     pkv.w = pack_bf16x2(__uint_as_float(v[8 * k + 6]) * mul, __uint_as_float(v[8 * k + 7]) * mul);
-                    sts128(sg + hf * (kKV / 2) + kr * 128 + chunk * 16, pkv);
+                    sts128(sg + hf * kKVbox + kr * 128 + chunk * 16, pkv);
                 }
             }
             fence_proxy_async();
             named_bar_sync(1 + wg, 128);
             if (kr == 0) {
-                tma_store_4d(wg == 0 ? &mdv : &mdk, stg + hf * (kKV / 2), hf * 64, (int)h, (int)j0, (int)b);
+                tma_store_4d(wg == 0 ? &mdv : &mdk, stg + hf * kKVbox, hf * 64, (int)h, (int)j0, (int)b);
                 bulk_commit();
             }
         }
@@ -428,10 +444,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int64_t t0 = (qt_lo + m) * BMQ;
             mbar_wait(&bars->dq_full[bm], (m >> 1) & 1);
             tc_fence_after();
+            const bool dlive = 32 * (warp & 3) < D;  // D = 64: dQ^T lanes 64..127 are the zero padding
             uint32_t v[4][16];
+            if (dlive) {
 #pragma unroll
-            for (int qq = 0; qq < 4; ++qq) tmem_ld16(lane_addr + 128 * bm + qcol[qq], v[qq]);
-            tmem_wait_ld();
+                for (int qq = 0; qq < 4; ++qq) tmem_ld16(lane_addr + 128 * bm + qcol[qq], v[qq]);
+                tmem_wait_ld();
+            }
             // all 64 queries are in registers: release the TMEM buffer first
             tc_fence_before();
             __syncwarp();
@@ -441,6 +460,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             // 16-B chunk (d%32)/4 ^ (query%8), word d%4
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
+                if (!dlive) break;
                 if (lane == 0) bulk_wait_read1();  // the reduce two rounds back has read this box
                 __syncwarp();
                 const uint32_t sq = smem_u32(wbox + (r & 1) * kDQW);
@@ -466,9 +486,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
-constexpr size_t kSmemBytes = 1024 + 2 * kKV + NQS * 2 * kQT + 2 * kDS + kDQ + sizeof(Bars) + 16;
+template <int D>
+constexpr size_t smem_bytes() {
+    return 1024 + BwdLay<D>::kKslot + BwdLay<D>::kV + NQS * 2 * BwdLay<D>::kQT + 2 * kDS + kDQ + sizeof(Bars) + 16;
+}
 
 // dQacc zeroing fused with D = rowsum(O dO)  (Alg. E.2 l.7; O + O_lo, C-12)
+template <int D>
 __global__ void __launch_bounds__(256) bwd_tc_pre_kernel(AttnParams p) {
     const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
@@ -478,7 +502,9 @@ __global__ void __launch_bounds__(256) bwd_tc_pre_kernel(AttnParams p) {
     const int64_t oo = b * p.os[0] + t * p.os[1] + h * p.os[2];
     const __nv_bfloat16* dO = (const __nv_bfloat16*)p.dO + oo;
     float acc = 0.f;
-    const int c = lane * 4;  // d = 128: 4 elements per lane
+    const int c = lane * 4;  // 4 elements per lane: lanes [0, D/4)
+    const bool act = lane < D / 4;
+    if (act) {
     const uint2 g2 = *reinterpret_cast<const uint2*>(dO + c);
     const float2 g01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&g2.x));
     const float2 g23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&g2.y));
@@ -495,14 +521,16 @@ __global__ void __launch_bounds__(256) bwd_tc_pre_kernel(AttnParams p) {
         o23.y += l23.y;
     }
     acc = o01.x * g01.x + o01.y * g01.y + o23.x * g23.x + o23.y * g23.y;
+    }
     acc = warp_sum(acc);
     if (lane == 0) p.Dv[(b * p.H + h) * p.Nq + t] = acc;
-    if (!(p.token && *p.token == p.token_val))  // not already zeroed by gfwa_fwd_train
+    if (act && !(p.token && *p.token == p.token_val))  // not already zeroed by gfwa_fwd_train
         *reinterpret_cast<float4*>(p.dQacc + ((b * p.Nq + t) * p.H + h) * D + c) = make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
 // D = rowsum((O + O_lo) dO) and zeroing of dQacc, fast path for contiguous O, O_lo, dO:
 // a warp per row (grid-stride, 32-bit index math), the zeroing as flat 32-byte stores
+template <int D>
 __global__ void __launch_bounds__(256) bwd_tc_pre_flat_kernel(const __nv_bfloat16* __restrict__ o,
                                                              const __nv_bfloat16* __restrict__ olo,
                                                              const __nv_bfloat16* __restrict__ dO,
@@ -522,17 +550,21 @@ __global__ void __launch_bounds__(256) bwd_tc_pre_flat_kernel(const __nv_bfloat1
         const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.y));
         return make_float4(a.x, a.y, b.x, b.y);
     };
+    const bool act = lane < D / 4;  // 4 elements per lane
     for (uint32_t row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < rows; row += nw) {
-        const float4 oh = f4(__ldcs(reinterpret_cast<const uint2*>(o + (size_t)row * D) + lane));
-        const float4 ol = f4(__ldcs(reinterpret_cast<const uint2*>(olo + (size_t)row * D) + lane));
-        const float4 g = f4(__ldcs(reinterpret_cast<const uint2*>(dO + (size_t)row * D) + lane));
-        float a = (oh.x + ol.x) * g.x + (oh.y + ol.y) * g.y + (oh.z + ol.z) * g.z + (oh.w + ol.w) * g.w;
+        float a = 0.f;
+        if (act) {
+            const float4 oh = f4(__ldcs(reinterpret_cast<const uint2*>(o + (size_t)row * D) + lane));
+            const float4 ol = f4(__ldcs(reinterpret_cast<const uint2*>(olo + (size_t)row * D) + lane));
+            const float4 g = f4(__ldcs(reinterpret_cast<const uint2*>(dO + (size_t)row * D) + lane));
+            a = (oh.x + ol.x) * g.x + (oh.y + ol.y) * g.y + (oh.z + ol.z) * g.z + (oh.w + ol.w) * g.w;
+        }
         a = warp_sum(a);
         if (lane == 0) {
             const uint32_t hh = row % H, bt = row / H, t = bt % Nq, b = bt / Nq;
             Dv[((size_t)b * H + hh) * Nq + t] = a;
         }
-        if (zero) reinterpret_cast<float4*>(acc + (size_t)row * D)[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (zero && act) reinterpret_cast<float4*>(acc + (size_t)row * D)[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
 }
 
@@ -553,6 +585,7 @@ __global__ void __launch_bounds__(256) bwd_tc_post_flat_kernel(const float* __re
 }
 
 // dQ = scale * dQacc -> bf16 (C-3), general strides
+template <int D>
 __global__ void __launch_bounds__(256) bwd_tc_post_kernel(AttnParams p) {
     const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
@@ -560,6 +593,7 @@ __global__ void __launch_bounds__(256) bwd_tc_post_kernel(AttnParams p) {
     if (row >= total) return;
     const int64_t h = row % p.H, t = (row / p.H) % p.Nq, b = row / (p.H * p.Nq);
     const int c = lane * 4;
+    if (lane >= D / 4) return;
     const float4 a = *reinterpret_cast<const float4*>(p.dQacc + ((b * p.Nq + t) * p.H + h) * D + c);
     uint2 o;
     o.x = pack_bf16x2(a.x * p.scale, a.y * p.scale);
@@ -570,15 +604,16 @@ __global__ void __launch_bounds__(256) bwd_tc_post_kernel(AttnParams p) {
 }  // namespace
 
 bool tc_bwd_supported(const AttnParams& p, gfwa_dtype_t dt) {
-    if (dt != GFWA_BF16 || p.d != D) return false;
+    if (dt != GFWA_BF16 || (p.d != 64 && p.d != 128)) return false;
     if (p.Nkv >= ((int64_t)1 << 31) || p.H >= 65536 || p.B >= 65536) return false;
     if (const char* e = getenv("GFWA_FORCE_SIMT")) return e[0] == '0';
     return true;
 }
 
-size_t tc_bwd_workspace(const AttnParams& p) { return (size_t)p.B * p.Nq * p.H * D * sizeof(float); }
+size_t tc_bwd_workspace(const AttnParams& p) { return (size_t)p.B * p.Nq * p.H * p.d * sizeof(float); }
 
-gfwa_status_t tc_bwd(const AttnParams& pin, cudaStream_t st, void* ws) {
+template <int D>
+static gfwa_status_t tc_bwd_d(const AttnParams& pin, cudaStream_t st, void* ws) {
     AttnParams p = pin;
     p.dQacc = (float*)ws;
     CUtensorMap mq, mk, mv, mdo, mdk, mdv, mdq;
@@ -598,12 +633,12 @@ gfwa_status_t tc_bwd(const AttnParams& pin, cudaStream_t st, void* ws) {
     const bool o_flat = p.Olo && p.os[2] == D && p.os[1] == p.H * D && p.os[0] == p.Nq * p.H * D &&
                         rows < ((int64_t)1 << 31) && n_du < ((int64_t)1 << 31);
     if (o_flat) {
-        bwd_tc_pre_flat_kernel<<<(unsigned)min64((rows + 7) / 8, (int64_t)n_sm * 16), 256, 0, st>>>(
+        bwd_tc_pre_flat_kernel<D><<<(unsigned)min64((rows + 7) / 8, (int64_t)n_sm * 16), 256, 0, st>>>(
             (const __nv_bfloat16*)p.O, (const __nv_bfloat16*)p.Olo, (const __nv_bfloat16*)p.dO, p.Dv, p.dQacc, (uint32_t)rows, (uint32_t)p.H, (uint32_t)p.Nq, p.dU,
             (uint32_t)n_du, p.token, p.token_val);
     } else {
         if (gfwa_status_t s = check_launch(cudaMemsetAsync(p.dU, 0, (size_t)n_du * sizeof(float), st))) return s;
-        bwd_tc_pre_kernel<<<rgrid, 256, 0, st>>>(p);
+        bwd_tc_pre_kernel<D><<<rgrid, 256, 0, st>>>(p);
     }
     note_launch();
     if (gfwa_status_t s = check_launch()) return s;
@@ -623,11 +658,12 @@ gfwa_status_t tc_bwd(const AttnParams& pin, cudaStream_t st, void* ws) {
     tp.scale = p.scale;
     tp.token = p.token;
     // per launch: the attribute is per device (a process may drive several GPUs)
+    constexpr size_t kSmemBytes = smem_bytes<D>();
     if (gfwa_status_t s = check_launch(
-            cudaFuncSetAttribute(bwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes)))
+            cudaFuncSetAttribute(bwd_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes)))
         return s;
     dim3 grid((unsigned)((p.Nkv + BN - 1) / BN), (unsigned)p.H, (unsigned)p.B);
-    bwd_tc_kernel<<<grid, kThreads, kSmemBytes, st>>>(mq, mk, mv, mdo, mdk, mdv, mdq, tp);
+    bwd_tc_kernel<D><<<grid, kThreads, kSmemBytes, st>>>(mq, mk, mv, mdo, mdk, mdv, mdq, tp);
     note_launch();
     if (gfwa_status_t s = check_launch()) return s;
     stage_event(1, st);  // measurement hook: after the main kernel
@@ -637,10 +673,14 @@ gfwa_status_t tc_bwd(const AttnParams& pin, cudaStream_t st, void* ws) {
         const unsigned g = (unsigned)min64((n8 + 255) / 256, (int64_t)n_sm * 8);
         bwd_tc_post_flat_kernel<<<g, 256, 0, st>>>(p.dQacc, (__nv_bfloat16*)p.dQ, n8, p.scale);
     } else {
-        bwd_tc_post_kernel<<<rgrid, 256, 0, st>>>(p);
+        bwd_tc_post_kernel<D><<<rgrid, 256, 0, st>>>(p);
     }
     note_launch();
     return check_launch();
+}
+
+gfwa_status_t tc_bwd(const AttnParams& p, cudaStream_t st, void* ws) {
+    return p.d == 64 ? tc_bwd_d<64>(p, st, ws) : tc_bwd_d<128>(p, st, ws);
 }
 
 }  // namespace gfwa
