@@ -309,9 +309,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) gate_prefix_kernel(
             if (total && c == g.n_chunks - 1) total[(int64_t)b * H + hh0 + j] = excl + agg;
         }
         const double carry = carry_in ? carry_in[(int64_t)b * H + hh0 + j] : 0.0;
-        // carry-side base in fp64; the final subtraction is done in fp64 too, so a
-        // result much smaller than the carry (cancellation) is rounded only once
+        // carry-side base in fp64, split once per run into hi + lo fp32 words: each
+        // U_t = hi + (lo - acc) then costs two fp32 adds, the first exact up to the
+        // small in-run prefix, so U_t is rounded once (as an fp64 subtraction would)
         const double cbase = carry - (excl + xs[i] - (double)run[i]);
+        const float chi = (float)cbase, clo = (float)(cbase - (double)chi);
         const float* row = sA + j * pitch + lane * (R + 1);
         float* urow = U + ((int64_t)b * H + hh0 + j) * N + t0 + tl;
         float acc = 0.f;
@@ -319,19 +321,19 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) gate_prefix_kernel(
             for (int k = 0; k < R; k += 4) {
                 float4 o;
                 acc += row[k];
-                o.x = (float)(cbase - (double)acc);
+                o.x = chi + (clo - acc);
                 acc += row[k + 1];
-                o.y = (float)(cbase - (double)acc);
+                o.y = chi + (clo - acc);
                 acc += row[k + 2];
-                o.z = (float)(cbase - (double)acc);
+                o.z = chi + (clo - acc);
                 acc += row[k + 3];
-                o.w = (float)(cbase - (double)acc);
+                o.w = chi + (clo - acc);
                 *reinterpret_cast<float4*>(urow + k) = o;
             }
         } else {
             for (int k = 0; k < R; ++k) {
                 acc += row[k];
-                if (tl + k < nt) urow[k] = (float)(cbase - (double)acc);
+                if (tl + k < nt) urow[k] = chi + (clo - acc);
             }
         }
     }
