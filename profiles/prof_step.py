@@ -25,7 +25,7 @@ def main():
     h, beta = h.bfloat16(), beta.bfloat16()
     for _ in range(2):
         U = gb.gfwa_gate_prefix(h, beta)
-        O, LSE, Olo = gb.gfwa_fwd(Q, K, V, U, s.w, want_o_lo=True)
+        O, LSE, Olo = gb.gfwa_fwd(Q, K, V, U, s.w, want_o_lo=True, prepare_bwd=True)
         dQ, dK, dV, dU, _ = gb.gfwa_bwd(Q, K, V, U, O, LSE, dO, s.w, O_lo=Olo, want_dalpha=False)
         gb.gfwa_gate_prefix_bwd(dU, h, beta, want_dalpha=False)
     torch.cuda.synchronize()

@@ -35,12 +35,13 @@ def main():
         print(f"{k:70s} {n:4d} {t / 1e3:10.2f} {rd / 1e6:9.2f} {wr / 1e6:9.2f} {(rd + wr) / t:8.1f}")
     if "--traffic" in sys.argv:
         path = sys.argv[sys.argv.index("--traffic") + 1]
-        call = {"fwd": ["fwd_tc_kernel"], "bwd": ["bwd_tc_pre_kernel", "bwd_tc_pre_flat_kernel", "bwd_tc_kernel",
-                                                  "bwd_tc_post_kernel", "bwd_tc_post_flat_kernel"]}
-        tr = {kind: sum(out[k]["dram_read"] + out[k]["dram_write"] for k in ks if k in out) for kind, ks in call.items()}
+        call = {"fwd": ["fwd_tc_kernel"], "bwd": ["bwd_tc_pre", "bwd_tc_kernel", "bwd_tc_post"],
+                "bwd_main": ["bwd_tc_kernel"]}
+        tr = {kind: sum(out[k]["dram_read"] + out[k]["dram_write"] for k in out if any(k.startswith(x) for x in ks))
+              for kind, ks in call.items()}
         tr = {k: int(v) for k, v in tr.items() if v}
-        tr["_note"] = ("dram__bytes_read.sum + dram__bytes_write.sum per launch of the gfwa_fwd / gfwa_bwd call "
-                       "(sum over the call's kernels), from " + sys.argv[1])
+        tr["_note"] = ("dram__bytes_read.sum + dram__bytes_write.sum per launch: fwd = fwd_tc_kernel, bwd = the "
+                       "gfwa_bwd call (pre + main + post), bwd_main = bwd_tc_kernel alone; from " + sys.argv[1])
         wl = sys.argv[sys.argv.index("--workload") + 1] if "--workload" in sys.argv else "C2"
         try:
             allt = json.load(open(path))
