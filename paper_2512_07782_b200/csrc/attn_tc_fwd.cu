@@ -8,18 +8,20 @@
 // are walked diagonal-first (descending j); the first one only feeds B (its
 // diagonal), the last only A (its window edge).
 //
-//   warp 13     TMA producer: Q_A, Q_B per item (a slot is refilled as soon as
+//   warp 21     TMA producer: Q_A, Q_B per item (a slot is refilled as soon as
 //               the tile's last S MMA has read it), K_j and V_j through one ring
 //               of three tile slots (evict-last: re-read by ~w/128 neighbouring
 //               items);
-//   warp 12     MMA issuer (one elected lane), ping-pong over the two tiles:
+//   warp 20     MMA issuer (one elected lane), ping-pong over the two tiles:
 //                 O_A += P_A V_{n-1};  S_A = Q_A K_n^T;
 //                 O_B += P_B V_{n-1};  S_B = Q_B K_n^T
 //               (P lives over its S columns, so a tile's next S is issued after
 //               its PV; while the tensor core runs one tile's pair the other
 //               tile's softmax runs)
-//   warps 0-3   softmax of tile A, warps 4-7 of tile B: one thread per query row
-//               holding its 128 S values in registers (one tcgen05.ld wait), the
+//   warps 0-7   softmax of tile A, warps 8-15 of tile B: two warpgroups per
+//               tile, each owning one 64-column half of every S row (one thread
+//               per row and half; the row max is exchanged through smem per key
+//               tile, the row sum per item), two passes over TMEM, the
 //               gate bias as an outer difference of two u vectors (P:377-380,
 //               nothing N x w is materialised), window masks only on diagonal /
 //               edge tiles with fully masked 32-key chunks skipped
@@ -27,13 +29,13 @@
 //               (the reference max moves only when it grows by > 2^8; the rare
 //               rescale of O runs in TMEM by the row's own thread), 16-bit P
 //               written back over the S columns.  LSE = m + ln l.
-//   warps 8-11  epilogue: O / l -> bf16 O (staged in a 32 KB buffer) and, in
+//   warps 16-19 epilogue: O / l -> bf16 O (staged per 64-column half) and, in
 //               the training forward, its bf16 residual O_lo = bf16(O/l - O)
 //               (staged in a 32 KB buffer; O + O_lo carries O to ~2^-17, which
 //               is what the backward's D = rowsum(O dO) needs, reading C-12),
 //               written by TMA stores; gfwa_fwd_train: it also zeroes the tile's
 //               rows of the backward's dQ accumulator (coalesced 512-byte rows)
-//   warps 14-15 training forward: the in-place fp16 conversion of every V tile
+//   warps 22-23 training forward: the in-place fp16 conversion of every V tile
 //               (reading C-23: P and V in fp16 for the PV product, so the fp32 O
 //               that D = rowsum(O dO) is taken from carries 8x less P rounding
 //               than with bf16 P)
@@ -58,11 +60,12 @@ using namespace sm100;
 constexpr int BM = 128;  // query rows per tile (two tiles per item)
 constexpr int BN = 128;  // keys per tile
 constexpr uint32_t kBox = BM * 64 * 2;  // one 16 KB TMA box: 128 rows x 64 bf16 (one 128-byte swizzle row)
-// 4 full warpgroups (setmaxnreg acts per warpgroup; the CTA register pool is
+// six warpgroups, 80 registers each (the CTA register file): softmax A (two
+// warpgroups, one per 64-column half of the S row), softmax B (two), epilogue,
+// {MMA, TMA, 2 V-convert warps}
 // 512 x 128 = 64K): softmax A, softmax B, epilogue, {MMA, TMA, 2 V-convert warps}
-constexpr int kThreads = 512;
-constexpr int kEpiWarp0 = 8, kMmaWarp = 12, kTmaWarp = 13, kCvtWarp0 = 14;
-constexpr int kSoftmaxRegs = 184, kEpiRegs = 72, kOtherRegs = 72;  // 256*184 + 128*72 + 128*72 = 65536
+constexpr int kThreads = 768;
+constexpr int kEpiWarp0 = 16, kMmaWarp = 20, kTmaWarp = 21, kCvtWarp0 = 22;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 constexpr int kPolyPairs = GFWA_FWD_POLY;  // of every 4 column pairs, how many use exp2_poly2
 
@@ -72,10 +75,12 @@ struct Lay {
     static constexpr uint32_t kTile = BM * D * 2;           // one bf16 Q/K/V/O tile
     static constexpr uint32_t kOffQ = 0;                    // Q_A, Q_B
     static constexpr uint32_t kOffKV = 2 * kTile;           // one K/V ring of 3 tile slots: K_0 V_0 K_1 V_1 ...
-    static constexpr uint32_t kOffE = 5 * kTile;            // staging of the O tile, then of the O_lo tile
-    static constexpr uint32_t kOffNbk = 7 * kTile;          // [2 tiles][128] fp32 key biases
+    static constexpr uint32_t kOffE = 5 * kTile;            // 32 KB: a 64-column box of O, then of O_lo
+    static constexpr uint32_t kOffNbk = kOffE + 2 * kBox;   // [2 tiles][128] fp32 key biases
     static constexpr uint32_t kOffLinv = kOffNbk + 2 * BN * 4;  // [2 tiles][128] 1/l
-    static constexpr uint32_t kOffBars = kOffLinv + 2 * BM * 4;
+    static constexpr uint32_t kOffXch = kOffLinv + 2 * BM * 4;  // [2 tiles][2 halves][128] row-max exchange
+    static constexpr uint32_t kOffXchL = kOffXch + 4 * BM * 4;  // [2 tiles][128] half 1's row sum
+    static constexpr uint32_t kOffBars = kOffXchL + 2 * BM * 4;
     static constexpr size_t kSmemBytes = kOffBars + 256;
 };
 constexpr int kSlots = 3;
@@ -189,7 +194,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&bars->q_full[i], 1);
             mbar_init(&bars->q_empty[i], 1);  // the tile's last S MMA
             mbar_init(&bars->s_full[i], 1);
-            mbar_init(&bars->p_ready[i], 4);
+            mbar_init(&bars->p_ready[i], 8);  // both softmax warpgroups of the tile
             mbar_init(&bars->o_full[i], 1);
             mbar_init(&bars->o_free[i], 4);
             mbar_init(&bars->l_ready[i], 4);
@@ -218,11 +223,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     const uint32_t tmem = bars->tmem;
 
-    if (warp >= kEpiWarp0 && warp < kMmaWarp) {
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kEpiRegs));
-    } else if (warp >= kMmaWarp) {
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kOtherRegs));
-    }
 
     if (warp == kTmaWarp) {
         // ------------------------------------------------------------ TMA producer
@@ -301,7 +301,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                             const uint32_t vb = smem_u32(smem + kOffKV + sv * kTile);
 #pragma unroll
                             for (int kk = 0; kk < BN / 16; ++kk)
-                                mma_ts(tmem + 256 + 128 * x, tmem + 128 * x + 8 * kk,
+                                // P of keys [16 kk, 16 kk + 16): S-row half kk / 4 holds its
+                                // 64 keys' P in its own first 32 columns
+                                mma_ts(tmem + 256 + 128 * x, tmem + 128 * x + 64 * (kk >> 2) + 8 * (kk & 3),
                                        sdesc_sw128(vb + kk * 2048, kBox, 1024), idesc_pv,
                                        (!first_pv[x] || kk > 0) ? 1u : 0u);
                             if (j + 1 == it.jlo(x)) tc_commit(&bars->o_full[x]);
@@ -374,14 +376,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp < kEpiWarp0) {
-        // ------------------------------------------------------------ softmax (tile x)
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kSoftmaxRegs));
-        const int x = warp >> 2;
+        // ------------------------------------------------------------ softmax (tile x, half hh)
+        // Two warpgroups per tile: half hh owns S columns [64 hh, 64 hh + 64) of every
+        // row (warps of both halves reach the same TMEM lanes: lane quarter = warp % 4),
+        // so each warp's serial chain per key tile is half as long.  The row max is
+        // exchanged through smem once per key tile, the row sum once per item.
+        const int x = warp >> 3, hh = (warp >> 2) & 1;
         const int r = threadIdx.x & 127;
         const uint32_t lane_addr = tmem + ((uint32_t)((warp & 3) * 32) << 16);
-        const uint32_t s_col = 128 * x, o_col = 256 + 128 * x;
-        float* nbk = reinterpret_cast<float*>(smem + kOffNbk) + x * BN;
+        const uint32_t s_col = 128 * x + 64 * hh, o_col = 256 + 128 * x + (D / 2) * hh;
+        float* nbk = reinterpret_cast<float*>(smem + kOffNbk) + x * BN + 64 * hh;  // this half's 64 keys
         float* linv = reinterpret_cast<float*>(smem + kOffLinv) + x * BM;
+        float* xch = reinterpret_cast<float*>(smem + L::kOffXch) + x * 2 * BM;    // [half][row]
+        const uint32_t bar_half = 1 + 2 * x + hh, bar_tile = 5 + x;             // named barrier ids
         const uint64_t sl2x2 = f2pack(p.sl2, p.sl2);
         uint32_t cs = 0, nit = 0;
         for (int idx = blockIdx.x; idx < p.n_items; idx += gridDim.x) {
@@ -397,50 +404,48 @@ __global__ void __launch_bounds__(kThreads, 1)
             // row constant (u_q - uref) cancels in the softmax and re-enters the LSE
             const float uref = Ubh[it.glo0];
             const float bq = valid ? (Ubh[g] - uref) * kLog2e : 0.f;
-            float m_used = -INFINITY, l = 0.f;
-            float u_next = jt * BN + r < Nkv ? Ubh[jt * BN + r] : 0.f;
+            float m_used = -INFINITY, l = 0.f;  // l: this half's partial row sum
+            const int kr = 64 * hh + (r & 63);    // key of this thread's nbk entry (threads r < 64)
+            float u_next = (r < 64 && jt * BN + kr < Nkv) ? Ubh[jt * BN + kr] : 0.f;
             for (int j = jt; j >= jlo_x; --j, ++cs) {
-                // -(u_k - uref) log2e of this key tile -> smem (WG-cooperative, after every
-                // thread finished the previous tile); the next tile's u is prefetched
-                float* nb_cur = nbk;
-                named_bar_sync(1 + x, 128);
-                nb_cur[r] = (uref - u_next) * kLog2e;
-                if (j > jlo_x) u_next = (j - 1) * BN + r < Nkv ? Ubh[(j - 1) * BN + r] : 0.f;
-                named_bar_sync(1 + x, 128);
+                // -(u_k - uref) log2e of this half's 64 keys -> smem (after every thread
+                // of the half finished the previous tile); the next tile's u is prefetched
+                named_bar_sync(bar_half, 128);
+                if (r < 64) nbk[r] = (uref - u_next) * kLog2e;
+                if (r < 64 && j > jlo_x) u_next = (j - 1) * BN + kr < Nkv ? Ubh[(j - 1) * BN + kr] : 0.f;
+                named_bar_sync(bar_half, 128);
                 if (r == 0) FTR(x, 3 * (int)cs);
                 mbar_wait_park(&bars->s_full[x], cs & 1);
                 if (r == 0) FTR(x, 3 * (int)cs + 1);
                 tc_fence_after();
                 const bool interior = (j * BN + BN - 1 <= glo_x) && (j * BN >= ghi_x - p.w + 1) && (j * BN + BN <= Nkv);
-                uint32_t keep[4] = {~0u, ~0u, ~0u, ~0u};
-                bool live[4] = {true, true, true, true};  // warp-uniform: chunk has a kept key in some row
+                uint32_t keep[2] = {~0u, ~0u};
+                bool live[2] = {true, true};  // warp-uniform: the 32-key chunk has a kept key in some row
                 if (!interior) {
                     // keys in (g - w, g] and < N_kv, as columns of this tile
                     const int kb = j * BN;
                     const int hi = min(min(g - kb, BN - 1), Nkv - 1 - kb);
                     const int lo = max(g - p.w + 1 - kb, 0);
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) {
-                        keep[c] = range_bits(lo, hi, 32 * c);
+                    for (int c = 0; c < 2; ++c) {
+                        keep[c] = range_bits(lo, hi, 64 * hh + 32 * c);
                         live[c] = __any_sync(0xffffffffu, keep[c] != 0u);
                     }
                 }
-                // two passes over the S row in TMEM, 64 columns in registers at a time (both
-                // softmax warpgroups fit the register file).  Pass 1 forms the logits
-                // x = scale*q.k - (u_k - uref) log2e (Alg. 2 l.12-15, masked to -inf
-                // outside the window), keeps the row max and writes x back over S;
-                // pass 2 reads x and only exponentiates.
+                const bool any = live[0] || live[1];
+                // pass 1: logits x = scale*q.k - (u_k - uref) log2e (Alg. 2 l.12-15, masked to
+                // -inf outside the window), the half-row max, x written back over S
                 float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-                for (int h2 = 0; h2 < 2; ++h2) {
-                    if (!(h2 ? (live[2] || live[3]) : (live[0] || live[1]))) continue;
-                    uint32_t raw[64];
-                    tmem_ld32(lane_addr + s_col + 64 * h2, *reinterpret_cast<uint32_t(*)[32]>(raw));
-                    tmem_ld32(lane_addr + s_col + 64 * h2 + 32, *reinterpret_cast<uint32_t(*)[32]>(raw + 32));
+                for (int cb = 0; cb < 2; ++cb) {  // 32 columns in registers at a time
+                    if (!(cb ? live[1] : live[0])) continue;  // masked for the whole warp: pass 2 skips it too
+                    uint32_t raw[32];
+                    tmem_ld32(lane_addr + s_col + 32 * cb, raw);
                     tmem_wait_ld();
+                    const uint32_t kw = cb ? keep[1] : keep[0];
 #pragma unroll
-                    for (int e = 0; e < 64; e += 4) {
-                        const float4 nbv = *reinterpret_cast<const float4*>(nb_cur + 64 * h2 + e);
+                    for (int e = 0; e < 32; e += 4) {
+                        const float4 nbv = *reinterpret_cast<const float4*>(nbk + 32 * cb + e);
                         const uint64_t x01 = ffma2(f2pack(__uint_as_float(raw[e]), __uint_as_float(raw[e + 1])),
                                                    sl2x2, f2pack(nbv.x, nbv.y));
                         const uint64_t x23 = ffma2(f2pack(__uint_as_float(raw[e + 2]), __uint_as_float(raw[e + 3])),
@@ -449,13 +454,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                         f2unpack(x01, a0, a1);
                         f2unpack(x23, a2, a3);
                         if (!interior) {
-                            const int c = 64 * h2 + e;
-                            const uint32_t kw = h2 ? ((e >> 5) ? keep[3] : keep[2]) : ((e >> 5) ? keep[1] : keep[0]);
-                            const int bit = c & 31;
-                            a0 = ((kw >> bit) & 1u) ? a0 : -INFINITY;
-                            a1 = ((kw >> (bit + 1)) & 1u) ? a1 : -INFINITY;
-                            a2 = ((kw >> (bit + 2)) & 1u) ? a2 : -INFINITY;
-                            a3 = ((kw >> (bit + 3)) & 1u) ? a3 : -INFINITY;
+                            a0 = ((kw >> e) & 1u) ? a0 : -INFINITY;
+                            a1 = ((kw >> (e + 1)) & 1u) ? a1 : -INFINITY;
+                            a2 = ((kw >> (e + 2)) & 1u) ? a2 : -INFINITY;
+                            a3 = ((kw >> (e + 3)) & 1u) ? a3 : -INFINITY;
                         }
                         mx[(e >> 2) & 3] = fmax3(mx[(e >> 2) & 3], fmaxf(a0, a1), fmaxf(a2, a3));
                         raw[e] = __float_as_uint(a0);
@@ -463,11 +465,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                         raw[e + 2] = __float_as_uint(a2);
                         raw[e + 3] = __float_as_uint(a3);
                     }
-                    tmem_st32(lane_addr + s_col + 64 * h2, *reinterpret_cast<uint32_t(*)[32]>(raw));
-                    tmem_st32(lane_addr + s_col + 64 * h2 + 32, *reinterpret_cast<uint32_t(*)[32]>(raw + 32));
+                    tmem_st32(lane_addr + s_col + 32 * cb, raw);
                 }
-                const float mt = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+                // the row max over both halves (exchange through smem)
+                xch[hh * BM + r] = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+                named_bar_sync(bar_tile, 256);
+                const float mt = fmaxf(xch[r], xch[BM + r]);
                 // lazy online softmax: move the reference max only when it grows by > 2^8
+                // (both halves take the same decision from the same values)
                 float corr = 1.f;
                 bool need = false;
                 if (mt > m_used + kRescaleThreshold) {
@@ -482,50 +487,45 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint64_t nm2 = f2pack(-mref, -mref);
                 float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
                 tmem_wait_st();  // pass 1's x is in TMEM
+                // pass 2: exponentials, the half-row sum, 16-bit P of the half's 64 keys
+                // into its own first 32 S columns (chunk cb's P lands on columns that
+                // chunk cb's x already left: [16 cb, 16 cb + 16) <= [32 cb, 32 cb + 32))
 #pragma unroll
-                for (int h2 = 0; h2 < 2; ++h2) {
-                    const bool any = h2 ? (live[2] || live[3]) : (live[0] || live[1]);
-                    uint32_t xr[64];
-                    if (any) {
-                        tmem_ld32(lane_addr + s_col + 64 * h2, *reinterpret_cast<uint32_t(*)[32]>(xr));
-                        tmem_ld32(lane_addr + s_col + 64 * h2 + 32, *reinterpret_cast<uint32_t(*)[32]>(xr + 32));
+                for (int cb = 0; cb < 2; ++cb) {
+                    uint32_t pk[16];
+                    if (cb ? live[1] : live[0]) {
+                        uint32_t xr[32];
+                        tmem_ld32(lane_addr + s_col + 32 * cb, xr);
                         tmem_wait_ld();
-                    }
 #pragma unroll
-                    for (int cb = 0; cb < 2; ++cb) {
-                        uint32_t pk[16];
-                        if (h2 ? (cb ? live[3] : live[2]) : (cb ? live[1] : live[0])) {
-#pragma unroll
-                            for (int e = 0; e < 16; ++e) {
-                                const int k = 32 * cb + 2 * e;
-                                const uint64_t d = fadd2(f2pack(__uint_as_float(xr[k]), __uint_as_float(xr[k + 1])), nm2);
-                                float p0, p1;
-                                if ((e & 3) < kPolyPairs) {
-                                    f2unpack(exp2_poly2(d), p0, p1);
-                                } else {
-                                    float d0, d1;
-                                    f2unpack(d, d0, d1);
-                                    p0 = ex2(d0);
-                                    p1 = ex2(d1);
-                                }
-                                acc[(2 * e) & 7] += p0;
-                                acc[(2 * e + 1) & 7] += p1;
-                                pk[e] = kF16P ? pack_f16x2(p0, p1) : pack_bf16x2(p0, p1);
+                        for (int e = 0; e < 16; ++e) {
+                            const uint64_t d = fadd2(f2pack(__uint_as_float(xr[2 * e]), __uint_as_float(xr[2 * e + 1])), nm2);
+                            float p0, p1;
+                            if ((e & 3) < kPolyPairs) {
+                                f2unpack(exp2_poly2(d), p0, p1);
+                            } else {
+                                float d0, d1;
+                                f2unpack(d, d0, d1);
+                                p0 = ex2(d0);
+                                p1 = ex2(d1);
                             }
-                        } else {
-#pragma unroll
-                            for (int e = 0; e < 16; ++e) pk[e] = 0u;
+                            acc[(2 * e) & 7] += p0;
+                            acc[(2 * e + 1) & 7] += p1;
+                            pk[e] = kF16P ? pack_f16x2(p0, p1) : pack_bf16x2(p0, p1);
                         }
-                        // P (16-bit) over the S columns: keys [64 h2 + 32 cb, +32) -> 16 columns
-                        tmem_st16(lane_addr + s_col + 32 * h2 + 16 * cb, pk);
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) pk[e] = 0u;
                     }
+                    tmem_st16(lane_addr + s_col + 16 * cb, pk);
                 }
                 l += ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
-                // rescale O (the PV of the previous step is complete: S_full certified it)
+                // rescale this half's O columns (the PV of the previous step is complete:
+                // S_full certified it)
                 if (__any_sync(0xffffffffu, need)) {
                     uint32_t ob[32];
 #pragma unroll 1
-                    for (int c = 0; c < D; c += 32) {
+                    for (int c = 0; c < D / 2; c += 32) {
                         tmem_ld32(lane_addr + o_col + c, ob);
                         tmem_wait_ld();
 #pragma unroll
@@ -539,15 +539,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (lane == 0) mbar_arrive(&bars->p_ready[x]);
                 if (r == 0) FTR(x, 3 * (int)cs + 2);
             }
-            // Alg. 2 l.19-20: 1/l for the epilogue, LSE = m + ln l (natural log, bias included).
-            // linv is reused per item: wait until the epilogue has read the previous
-            // item's (a tile with a single key tile could otherwise run a phase ahead)
-            mbar_wait_park(&bars->l_free[x], (nit & 1) ^ 1);
+            // Alg. 2 l.19-20: l = both halves' sums; 1/l for the epilogue, LSE = m + ln l
+            // (natural log, bias included).  linv is reused per item: wait until the
+            // epilogue has read the previous item's
+            float* xl = reinterpret_cast<float*>(smem + L::kOffXchL) + x * BM;
+            if (hh == 1) xl[r] = l;
+            named_bar_sync(bar_tile, 256);
+            if (hh == 0) {
+                const float lt = l + xl[r];
+                mbar_wait_park(&bars->l_free[x], (nit & 1) ^ 1);
+                linv[r] = lt > 0.f ? 1.f / lt : 0.f;
+                if (valid) p.LSE[((int64_t)it.b * p.H + it.h) * p.Nq + t] = (m_used + bq + __log2f(lt)) * kLn2;
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bars->l_ready[x]);
+            }
             ++nit;
-            linv[r] = l > 0.f ? 1.f / l : 0.f;
-            if (valid) p.LSE[((int64_t)it.b * p.H + it.h) * p.Nq + t] = (m_used + bq + __log2f(l)) * kLn2;
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&bars->l_ready[x]);
         }
     } else {
         // ------------------------------------------------------------ epilogue (+ V -> fp16)
@@ -566,8 +572,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const float inv = linv_all[x * BM + r];
             __syncwarp();
             if (lane == 0) mbar_arrive(&bars->l_free[x]);
-            uint8_t* ehi = smem + kOffE;
-            const uint32_t sbf = smem_u32(ehi), sf = smem_u32(ehi + kTile);
+            uint8_t* ehi = smem + kOffE;  // [O box | O_lo box] of one 64-column half
+            const uint32_t sbf = smem_u32(ehi), sf = smem_u32(ehi + kBox);
             const uint32_t o_col = 256 + 128 * x;
             // four rounds of 32 columns: O (bf16) into the Q slot, O_lo into E; each
             // 64-column half is stored as soon as it is staged
@@ -582,6 +588,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (lane == 0) mbar_arrive(&bars->o_free[x]);
                 }
                 const int hf = cq >> 1, cc = cq & 1;
+                if (cc == 0 && hf > 0) {  // the previous half's stores must have read the staging
+                    if (r == 0) bulk_wait_read0();
+                    named_bar_sync(7, 128);
+                }
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                     const int chunk = (cc * 4 + k) ^ (r & 7);
@@ -597,17 +607,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                             lw[e] = pack_bf16x2(v0 - h0, v1 - h1);
                         }
                     }
-                    const uint32_t off = hf * kBox + r * 128 + chunk * 16;
+                    const uint32_t off = r * 128 + chunk * 16;
                     sts128(sbf + off, make_uint4(hw[0], hw[1], hw[2], hw[3]));
                     if (p.store_lo) sts128(sf + off, make_uint4(lw[0], lw[1], lw[2], lw[3]));
                 }
                 if (cc == 1) {
                     fence_proxy_async();
-                    named_bar_sync(3, 128);
+                    named_bar_sync(7, 128);
                     if (r == 0) {
                         const int row0 = it.r0 + x * BM;
-                        tma_store_4d(&mo, ehi + hf * kBox, hf * 64, it.h, row0, it.b);
-                        if (p.store_lo) tma_store_4d(&mol, ehi + kTile + hf * kBox, hf * 64, it.h, row0, it.b);
+                        tma_store_4d(&mo, ehi, hf * 64, it.h, row0, it.b);
+                        if (p.store_lo) tma_store_4d(&mol, ehi + kBox, hf * 64, it.h, row0, it.b);
                         bulk_commit();
                     }
                 }
@@ -626,7 +636,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 bulk_wait_read0();  // the staging buffers are reusable once the stores have read them
                 FTR(5, (int)(4 * (nit0 + nit1)) + 2);
             }
-            named_bar_sync(3, 128);
+            named_bar_sync(7, 128);
             if (x)
                 ++nit1;
             else
