@@ -49,7 +49,13 @@ struct BwdLay {
     static constexpr uint32_t kQT = 64 * D * 2;      // Q or dO tile
 };
 constexpr uint32_t kDS = 128 * 64 * 2;    // 16 KB dS^T tile
-constexpr int kThreads = 448;             // 2 softmax-grad WGs, drain WG, MMA warp, TMA warp
+#ifndef GFWA_BWD_SWG
+#define GFWA_BWD_SWG 2
+#endif
+constexpr int kSWG = GFWA_BWD_SWG;        // softmax-grad warpgroups, each owning QPW queries of a step
+constexpr int QPW = 64 / kSWG;
+constexpr int kDrainWarp0 = 4 * kSWG, kMmaWarp = kDrainWarp0 + 4, kTmaWarp = kMmaWarp + 1;
+constexpr int kThreads = 32 * (kTmaWarp + 1);  // softmax-grad WGs, drain WG, MMA warp, TMA warp
 #ifndef GFWA_BWD_NODQ
 #define GFWA_BWD_NODQ 0  // experiment only: skip the dQ reductions
 #endif
@@ -108,7 +114,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t* tmem_sh = (uint32_t*)(bars + 1);
     __shared__ __align__(16) float s_cq[NQS][BMQ];    // (u_q - uref) log2e - L_q log2e
     __shared__ __align__(16) float s_D[NQS][BMQ];     // D_q = rowsum(O dO)
-    __shared__ float s_red[2][2][4][32];              // [parity][wg][warp][lane] du^q partials
+    __shared__ float s_red[2][kSWG][4][QPW];          // [parity][wg][warp][query] du^q partials
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t b = blockIdx.z, h = blockIdx.y;
@@ -129,10 +135,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&bars->st_full[i], 1);
-            mbar_init(&bars->ds_ready[i], 8);
+            mbar_init(&bars->ds_ready[i], 4 * kSWG);
             mbar_init(&bars->dq_full[i], 1);
             mbar_init(&bars->dq_drained[i], 4);
-            mbar_init(&bars->red_ready[i], 8);
+            mbar_init(&bars->red_ready[i], 4 * kSWG);
             mbar_init(&bars->red_free[i], 2);
         }
         mbar_init(&bars->dkdv_full, 1);
@@ -143,7 +149,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             sts128(smem_u32(Ks + kKVbox) + i * 16, make_uint4(0u, 0u, 0u, 0u));
         fence_proxy_async();
     }
-    if (warp == 12) {
+    if (warp == kMmaWarp) {
         tmem_alloc(tmem_sh, 512);
         tmem_relinquish();
     }
@@ -156,7 +162,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // on this workspace zeroes its accumulator unless a new gfwa_fwd_train prepares it
     if (p.token && threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) *p.token = 0ull;
 
-    if (warp == 13) {
+    if (warp == kTmaWarp) {
         // ------------------------------------------------ producer: TMA + per-step vectors
         if (nsteps > 0) {
             if (elect_one()) {
@@ -191,7 +197,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (lane == 0) mbar_arrive(&bars->q_full[s]);
             }
         }
-    } else if (warp == 12) {
+    } else if (warp == kMmaWarp) {
         // ------------------------------------------------ MMA issuer
         const uint32_t id_st = idesc_bf16(128, BMQ, false, false);  // S^T, dP^T
         const uint32_t id_tm = idesc_bf16(128, D, false, true);     // dV, dK (A in TMEM, B MN-major)
@@ -217,9 +223,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int kk = 0; kk < BMQ / 16; ++kk) {
                     const uint32_t acc = (m > 0 || kk > 0) ? 1u : 0u;
                     // queries [16 kk, 16 kk + 16): warpgroup kk / 2's columns, half kk % 2
-                    const uint32_t pc = 32 * (kk >> 1) + 8 * (kk & 1);
+                    const uint32_t pc = QPW * ((16 * kk) / QPW) + 8 * (kk % (QPW / 16));
                     mma_ts(tmem + 256, buf + pc, sdesc_sw128(ob + kk * 2048, kQTbox, 1024), id_tm, acc);
-                    mma_ts(tmem + 384, buf + pc + 16, sdesc_sw128(qb + kk * 2048, kQTbox, 1024), id_tm, acc);
+                    mma_ts(tmem + 384, buf + pc + QPW / 2, sdesc_sw128(qb + kk * 2048, kQTbox, 1024), id_tm, acc);
                 }
                 tc_commit(&bars->q_empty[sm]);
                 if (m == nsteps - 1) tc_commit(&bars->dkdv_full);
@@ -247,9 +253,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (n >= 1) mma2(n - 1);
         }
         if (nsteps > 0) mma2(nsteps - 1);
-    } else if (warp < 8) {
+    } else if (warp < kDrainWarp0) {
         // ------------------------------------------------ softmax-grad: thread = key, 32 queries per WG
-        const int wg = warp >> 2;  // query columns [32 wg, 32 wg + 32) of each step
+        const int wg = warp >> 2;  // query columns [QPW wg, QPW wg + QPW) of each step
         const int kr = threadIdx.x & 127;
         const int64_t j = j0 + kr;
         const bool kvalid = j < p.Nkv;
@@ -265,26 +271,31 @@ __global__ void __launch_bounds__(kThreads, 1)
             // arrive (already complete) rather than through the tensor core's commit
             mbar_wait(&bars->q_full[s], (n / NQS) & 1);
             tc_fence_after();
-            const uint32_t scol = 128 * bn + 32 * wg;  // this WG's S^T columns (dP^T at +64)
+            const uint32_t scol = 128 * bn + QPW * wg;  // this WG's S^T columns (dP^T at +64)
             // keys in (g - w, g] of each query g = t + h0, as a column range
             const bool interior = (j0 + BN - 1 <= t0 + p.h0) && (j0 > t0 + BMQ - 1 + p.h0 - p.w) &&
                                   (t0 + BMQ <= p.Nq) && (j0 + BN <= p.Nkv);
             uint32_t keep = ~0u;
             if (!interior) {
                 const int64_t qlo = j - p.h0 - t0, qhi = min64(j - p.h0 - t0 + p.w - 1, p.Nq - 1 - t0);
-                keep = kvalid ? range_bits((int)max64(qlo, -1), (int)min64(qhi, (int64_t)BMQ), 32 * wg) : 0u;
+                keep = kvalid ? range_bits((int)max64(qlo, -1), (int)min64(qhi, (int64_t)BMQ), QPW * wg) : 0u;
             }
-            const float* cq = &s_cq[s][32 * wg];
-            const float* Dq = &s_D[s][32 * wg];
-            float ds[32];
-            uint32_t pk[16], dk[16];
-            uint32_t sall[32], dall[32];  // all four TMEM loads in flight before one wait
-            tmem_ld32(lane_addr + scol, sall);
-            tmem_ld32(lane_addr + scol + 64, dall);
+            const float* cq = &s_cq[s][QPW * wg];
+            const float* Dq = &s_D[s][QPW * wg];
+            float ds[QPW];
+            uint32_t pk[QPW / 2], dk[QPW / 2];
+            uint32_t sall[QPW], dall[QPW];  // both TMEM loads in flight before one wait
+            if constexpr (QPW == 32) {
+                tmem_ld32(lane_addr + scol, *reinterpret_cast<uint32_t(*)[32]>(sall));
+                tmem_ld32(lane_addr + scol + 64, *reinterpret_cast<uint32_t(*)[32]>(dall));
+            } else {
+                tmem_ld16(lane_addr + scol, *reinterpret_cast<uint32_t(*)[16]>(sall));
+                tmem_ld16(lane_addr + scol + 64, *reinterpret_cast<uint32_t(*)[16]>(dall));
+            }
             tmem_wait_ld();
             // each warpgroup packs its P^T, dS^T over its own S^T columns (no
             // cross-warpgroup barrier); dQ^T then gets [64,128) whole
-            for (int h16 = 0; h16 < 32; h16 += 16) {
+            for (int h16 = 0; h16 < QPW; h16 += 16) {
                 const uint32_t* s16 = sall + h16;
                 const uint32_t* d16 = dall + h16;
 #pragma unroll
@@ -330,13 +341,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
             }
-            tmem_st16(lane_addr + 128 * bn + 32 * wg, pk);       // P^T  -> columns [32 wg, 32 wg + 16)
-            tmem_st16(lane_addr + 128 * bn + 32 * wg + 16, dk);  // dS^T -> columns [32 wg + 16, 32 wg + 32)
+            // P^T -> columns [QPW wg, QPW wg + QPW/2), dS^T -> [QPW wg + QPW/2, QPW wg + QPW)
+            if constexpr (QPW == 32) {
+                tmem_st16(lane_addr + 128 * bn + QPW * wg, *reinterpret_cast<const uint32_t(*)[16]>(pk));
+                tmem_st16(lane_addr + 128 * bn + QPW * wg + QPW / 2, *reinterpret_cast<const uint32_t(*)[16]>(dk));
+            } else {
+                tmem_st8(lane_addr + 128 * bn + QPW * wg, *reinterpret_cast<const uint32_t(*)[8]>(pk));
+                tmem_st8(lane_addr + 128 * bn + QPW * wg + QPW / 2, *reinterpret_cast<const uint32_t(*)[8]>(dk));
+            }
             {  // dS^T row -> smem (128B-swizzled MN-major: row = key, 16-B chunk of 8 queries ^ key%8)
                 const uint32_t sb = smem_u32(dSs + bn * kDS) + kr * 128;
 #pragma unroll
-                for (int c = 0; c < 4; ++c)
-                    sts128(sb + (((4 * wg + c) ^ (kr & 7)) * 16),
+                for (int c = 0; c < QPW / 8; ++c)
+                    sts128(sb + ((((QPW / 8) * wg + c) ^ (kr & 7)) * 16),
                            make_uint4(dk[4 * c], dk[4 * c + 1], dk[4 * c + 2], dk[4 * c + 3]));
             }
             tmem_wait_st();
@@ -349,7 +366,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             // transpose-reduce -> lane l holds query 32 wg + l; the drain warpgroup
             // sums the 4 warps' partials and issues the red.add (C-11)
 #pragma unroll
-            for (int sft = 16; sft >= 1; sft >>= 1) {
+            for (int sft = QPW / 2; sft >= 1; sft >>= 1) {
                 const bool up = lane & sft;
 #pragma unroll
                 for (int e = 0; e < sft; ++e) {
@@ -359,7 +376,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
             if (n >= 2) mbar_wait(&bars->red_free[bn], ((n - 2) >> 1) & 1);
-            s_red[bn][wg][warp & 3][lane] = ds[0];
+            if (QPW < 32) ds[0] += __shfl_xor_sync(0xffffffffu, ds[0], QPW);  // lane halves hold the same query
+            if (lane < QPW) s_red[bn][wg][warp & 3][lane] = ds[0];
             __syncwarp();
             if (lane == 0) mbar_arrive(&bars->red_ready[bn]);
         }
@@ -369,6 +387,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (kvalid && nsteps > 0) red_add(p.dU + (b * p.H + h) * p.Nkv + j, -(c0 + c1));  // du^k (C-4)
         }
         // epilogue: WG0 -> dV, WG1 -> dK (scale, C-3), via smem + TMA store
+        if (wg >= 2) goto done;
+        {
         uint8_t* stg = Qs + wg * 2 * kQT;  // the Q/dO stages are idle once dkdv_full fires
         const uint32_t sg = smem_u32(stg);
         const uint32_t acol = wg == 0 ? 256 : 384;
@@ -411,16 +431,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                 bulk_commit();
             }
         }
-        if (kr == 0) {
-            bulk_wait_read0();
+        if (kr == 0) bulk_wait_read0();
         }
-    } else if (warp < 12) {
+    } else if (warp < kMmaWarp) {
         // ------------------------------------------------ dQ drain: thread = head-dim lane
         // dQ^T (TMEM, lane = d) -> smem [16 queries][32 d] fp32 boxes (128B swizzle) ->
         // TMA bulk reduce-add into the fp32 dQ accumulator: the L2 does the adds, no
         // per-thread atomics.  Each drain warp stages its own 32 d (double-buffered
         // 2 KB boxes) and issues its own reduces, so no cross-warp barrier.
-        const int dl = threadIdx.x - 256;  // 0..127
+        const int dl = threadIdx.x - 32 * kDrainWarp0;  // 0..127
         const uint32_t lane_addr = tmem + ((uint32_t)((warp & 3) * 32) << 16);
         const uint32_t qcol[4] = {64, 80, 96, 112};  // dQ^T: columns [64,128) of the buffer
         uint8_t* wbox = dQs + (warp & 3) * 2 * kDQW;
@@ -430,7 +449,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (dl < BMQ) {
                 const int bq = mm & 1;
                 mbar_wait(&bars->red_ready[bq], (mm >> 1) & 1);
-                const int wq = dl >> 5, lq = dl & 31;
+                const int wq = dl / QPW, lq = dl % QPW;
                 const float rs =
                     s_red[bq][wq][0][lq] + s_red[bq][wq][1][lq] + s_red[bq][wq][2][lq] + s_red[bq][wq][3][lq];
                 __syncwarp();
@@ -478,9 +497,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (nsteps > 0) combine_duq(nsteps - 1);
         if (lane == 0) bulk_wait0();  // reductions complete before the CTA exits
     }
+done:
     tc_fence_before();
     __syncthreads();
-    if (warp == 12) {
+    if (warp == kMmaWarp) {
         tc_fence_after();
         tmem_dealloc(tmem, 512);
     }
