@@ -76,6 +76,23 @@ struct TcBwdParams {
     unsigned long long* token;  // prepared-workspace token: consumed (cleared) by this kernel
 };
 
+#ifndef GFWA_BWD_TRACE
+#define GFWA_BWD_TRACE 0  // diagnostics build only: clock64 stamps per role into a device array
+#endif
+#if GFWA_BWD_TRACE
+constexpr int kBTr = 256;  // stamps per (CTA, role), first 296 CTAs
+__device__ long long g_bwd_trace[296 * 8 * kBTr];
+#define BTR(role, k)                                                                                        \
+    do {                                                                                                    \
+        const int cta_ = (int)(blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z));              \
+        if ((k) < kBTr && cta_ < 296) g_bwd_trace[(cta_ * 8 + (role)) * kBTr + (k)] = clock64();            \
+    } while (0)
+#else
+#define BTR(role, k) \
+    do {             \
+    } while (0)
+#endif
+
 struct __align__(8) Bars {
     uint64_t kv_full;
     uint64_t q_full[NQS], q_empty[NQS];
@@ -127,6 +144,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int nsteps = t_lo <= t_hi ? (int)(t_hi / BMQ - qt_lo + 1) : 0;
     const float* Ubh = p.U + (b * p.H + h) * p.Nkv;
 
+    if (threadIdx.x == 0) BTR(5, 2);
     if (threadIdx.x == 0) {
         mbar_init(&bars->kv_full, 1);
         for (int s = 0; s < NQS; ++s) {
@@ -157,6 +175,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_sh;
+    if (threadIdx.x == 0) BTR(5, 0);
     const float uref = Ubh[j0];  // per-CTA bias reference (reading C-18)
     // the pre kernel has read the token (stream order): clear it, so the next backward
     // on this workspace zeroes its accumulator unless a new gfwa_fwd_train prepares it
@@ -177,6 +196,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int s = n % NQS;
                 const int64_t t0 = (qt_lo + n) * BMQ;
                 mbar_wait(&bars->q_empty[s], ((n / NQS) & 1) ^ 1);
+                if (lane == 0) BTR(3, n);
                 if (elect_one()) {
                     mbar_expect_tx(&bars->q_full[s], 2 * kQT);
                     uint8_t* qd = Qs + s * 2 * kQT;
@@ -228,6 +248,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mma_ts(tmem + 384, buf + pc + QPW / 2, sdesc_sw128(qb + kk * 2048, kQTbox, 1024), id_tm, acc);
                 }
                 tc_commit(&bars->q_empty[sm]);
+                BTR(1, 2 * m + 1);
                 if (m == nsteps - 1) tc_commit(&bars->dkdv_full);
             }
             __syncwarp();
@@ -248,6 +269,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mma_ss(buf + 64, sdesc_sw128(vb + ka, 16, 1024), sdesc_sw128(ob + qa, 16, 1024), id_st, kk > 0);
                 }
                 tc_commit(&bars->st_full[bn]);
+                BTR(1, 2 * n);
             }
             __syncwarp();
             if (n >= 1) mma2(n - 1);
@@ -267,6 +289,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int bn = n & 1, s = n % NQS;
             const int64_t t0 = (qt_lo + n) * BMQ;
             mbar_wait(&bars->st_full[bn], (n >> 1) & 1);
+            if (threadIdx.x == 0) BTR(0, 3 * n);
             // the producer's per-step vectors (s_cq, s_D): acquire them from its own
             // arrive (already complete) rather than through the tensor core's commit
             mbar_wait(&bars->q_full[s], (n / NQS) & 1);
@@ -361,6 +384,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&bars->ds_ready[bn]);
+            if (threadIdx.x == 0) BTR(0, 3 * n + 1);
             // du^q partial over this warp's 32 keys, off the MMA's critical path (the
             // gradient contractions of step n are already running): butterfly
             // transpose-reduce -> lane l holds query 32 wg + l; the drain warpgroup
@@ -380,6 +404,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (lane < QPW) s_red[bn][wg][warp & 3][lane] = ds[0];
             __syncwarp();
             if (lane == 0) mbar_arrive(&bars->red_ready[bn]);
+            if (threadIdx.x == 0) BTR(0, 3 * n + 2);
         }
         {
             float c0, c1;
@@ -395,6 +420,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float mul = wg == 0 ? 1.f : p.scale;
         if (nsteps > 0) {
             mbar_wait(&bars->dkdv_full, 0);
+            if (threadIdx.x == 0) BTR(4, 0);
             tc_fence_after();
         }
         // two halves of 64 columns: both TMEM loads of a half in flight before one
@@ -432,6 +458,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
         if (kr == 0) bulk_wait_read0();
+        if (threadIdx.x == 0) BTR(4, 1);
         }
     } else if (warp < kMmaWarp) {
         // ------------------------------------------------ dQ drain: thread = head-dim lane
@@ -462,6 +489,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int bm = m & 1;
             const int64_t t0 = (qt_lo + m) * BMQ;
             mbar_wait(&bars->dq_full[bm], (m >> 1) & 1);
+            if (dl == 0) BTR(2, 2 * m);
             tc_fence_after();
             const bool dlive = 32 * (warp & 3) < D;  // D = 64: dQ^T lanes 64..127 are the zero padding
             uint32_t v[4][16];
@@ -474,6 +502,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&bars->dq_drained[bm]);
+            if (dl == 0) BTR(2, 2 * m + 1);
             if (m > 0) combine_duq(m - 1);  // the previous step's partials are in smem by now
             // four rounds of 16 queries; row = query (128 B = this warp's 32 d),
             // 16-B chunk (d%32)/4 ^ (query%8), word d%4
@@ -500,6 +529,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 done:
     tc_fence_before();
     __syncthreads();
+    if (threadIdx.x == 0) BTR(5, 1);
     if (warp == kMmaWarp) {
         tc_fence_after();
         tmem_dealloc(tmem, 512);
@@ -698,6 +728,13 @@ static gfwa_status_t tc_bwd_d(const AttnParams& pin, cudaStream_t st, void* ws) 
     note_launch();
     return check_launch();
 }
+
+#if GFWA_BWD_TRACE
+extern "C" int gfwa_debug_bwd_trace(long long* host, size_t n) {
+    if (n > sizeof(g_bwd_trace) / sizeof(long long)) n = sizeof(g_bwd_trace) / sizeof(long long);
+    return (int)cudaMemcpyFromSymbol(host, g_bwd_trace, n * sizeof(long long));
+}
+#endif
 
 gfwa_status_t tc_bwd(const AttnParams& p, cudaStream_t st, void* ws) {
     return p.d == 64 ? tc_bwd_d<64>(p, st, ws) : tc_bwd_d<128>(p, st, ws);
