@@ -23,6 +23,8 @@
 // transpose-reduce (after dS is handed to the MMA warp) and a cross-warp sum by
 // the drain warpgroup, so both sums see the same fp32 dS and sum_m dU_m
 // telescopes to zero.  dK, dV leave through smem + TMA stores.
+#include <type_traits>
+
 #include "attn_common.cuh"
 #include "sm100.cuh"
 #include "tma_host.cuh"
@@ -49,6 +51,14 @@ struct BwdLay {
     static constexpr uint32_t kQT = 64 * D * 2;      // Q or dO tile
 };
 constexpr uint32_t kDS = 128 * 64 * 2;    // 16 KB dS^T tile
+// bias folding (reading C-25): the per-query terms of the exponent and of dP - D enter
+// the S^T and dP^T accumulators through one extra K = 16 slab each.  A side: one 1 KB
+// 128B-swizzle atom whose 8 rows are identical (read with SBO = 0 for all 128 key rows);
+// slab 0 = ones at k 0..2 (S^T), slab 1 = ones at k 3..5 (dP^T).  B side: per Q stage s,
+// slab s of a 64-row atom column holds [c'_hi, c'_mid, c'_lo, -D_hi, -D_mid, -D_lo, 0...]
+// per query, c' = ((u_q - uref) - L_q) / scale split into three bf16 (24 bits), so that
+// sl2 (S^T + c') = scale log2e q.k + (u_q - uref - L_q) log2e and dP^T + (-D) = dP - D.
+constexpr uint32_t kAugA = 1024, kAugB = 64 * 128;
 #ifndef GFWA_BWD_SWG
 #define GFWA_BWD_SWG 2
 #endif
@@ -59,10 +69,16 @@ constexpr int kThreads = 32 * (kTmaWarp + 1);  // softmax-grad WGs, drain WG, MM
 #ifndef GFWA_BWD_NODQ
 #define GFWA_BWD_NODQ 0  // experiment only: skip the dQ reductions
 #endif
-#ifndef GFWA_BWD_POLY
-#define GFWA_BWD_POLY 0
+#ifndef GFWA_BWD_NODUQ
+#define GFWA_BWD_NODUQ 0  // experiment only: skip the du^q butterfly (wrong dU)
 #endif
-constexpr int kBwdPoly = GFWA_BWD_POLY;  // of every 2 column pairs, how many use exp2_poly2
+#ifndef GFWA_BWD_L2PF
+#define GFWA_BWD_L2PF 0  // experiment: L2 prefetch distance (steps) of the Q/dO tiles
+#endif
+#ifndef GFWA_BWD_EXPT
+#define GFWA_BWD_EXPT 0  // experiment only (wrong results): 1 no grad MMAs, 2 no S/dP MMAs, 3 ex2 -> fmul, 5 no softmax math,
+
+#endif
 
 struct TcBwdParams {
     const float* U;
@@ -72,7 +88,7 @@ struct TcBwdParams {
     float* dU;     // [B, H, Nkv] fp32, zeroed before the launch
     int64_t Nq, Nkv, h0, H;
     int w;
-    float sl2, scale;
+    float sl2, scale, inv_scale;
     unsigned long long* token;  // prepared-workspace token: consumed (cleared) by this kernel
 };
 
@@ -104,6 +120,17 @@ __device__ __forceinline__ void red_add(float* addr, float a) {
     asm volatile("red.global.add.f32 [%0], %1;" ::"l"(addr), "f"(a) : "memory");
 }
 
+// x = hi + mid + lo to ~24 bits, each a bf16 (bit patterns in the low 16 bits)
+__device__ __forceinline__ void split3_bf16(float x, uint32_t& h, uint32_t& m, uint32_t& l) {
+    const __nv_bfloat16 bh = __float2bfloat16_rn(x);
+    const float r1 = x - __bfloat162float(bh);
+    const __nv_bfloat16 bm = __float2bfloat16_rn(r1);
+    const __nv_bfloat16 bl = __float2bfloat16_rn(r1 - __bfloat162float(bm));
+    h = __bfloat16_as_ushort(bh);
+    m = __bfloat16_as_ushort(bm);
+    l = __bfloat16_as_ushort(bl);
+}
+
 __device__ __forceinline__ uint32_t range_bits(int lo, int hi, int base) {
     const int a = min(max(lo - base, 0), 32), z = min(max(hi - base + 1, 0), 32);
     const uint32_t upto_z = z >= 32 ? 0xffffffffu : ((1u << z) - 1u);
@@ -127,10 +154,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* Qs = Vs + kKV;              // NQS stages of [Q tile | dO tile]
     uint8_t* dSs = Qs + NQS * 2 * kQT;   // 2 x dS^T tile
     uint8_t* dQs = dSs + 2 * kDS;        // dQ staging: per drain warp 2 x [16 queries][32 d] fp32, 128B swizzle
-    Bars* bars = (Bars*)(dQs + kDQ);
+    uint8_t* augA = dQs + kDQ;           // 1 KB, see kAugA
+    uint8_t* augB = augA + kAugA;        // 8 KB: 64 query rows x 4 slabs (slab s = Q stage s)
+    Bars* bars = (Bars*)(augB + kAugB);
     uint32_t* tmem_sh = (uint32_t*)(bars + 1);
-    __shared__ __align__(16) float s_cq[NQS][BMQ];    // (u_q - uref) log2e - L_q log2e
-    __shared__ __align__(16) float s_D[NQS][BMQ];     // D_q = rowsum(O dO)
     __shared__ float s_red[2][kSWG][4][QPW];          // [parity][wg][warp][query] du^q partials
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -165,8 +192,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (D < 128) {  // the zero second half of the K slot (K^T rows d >= D of the dQ^T MMA)
         for (uint32_t i = threadIdx.x; i < kKVbox / 16; i += kThreads)
             sts128(smem_u32(Ks + kKVbox) + i * 16, make_uint4(0u, 0u, 0u, 0u));
-        fence_proxy_async();
     }
+    {  // bias-folding slabs: B zero except the per-step chunk the producer writes; A constant
+        for (uint32_t i = threadIdx.x; i < kAugB / 16; i += kThreads)
+            sts128(smem_u32(augB) + i * 16, make_uint4(0u, 0u, 0u, 0u));
+        if (threadIdx.x < 64) {  // A atom: row r = tid / 8, 16-B chunk c = tid % 8 (physical)
+            const uint32_t r = threadIdx.x >> 3, c = threadIdx.x & 7, logical = c ^ r;
+            const uint32_t one = 0x3F80u;  // bf16 1.0
+            uint4 v = make_uint4(0u, 0u, 0u, 0u);
+            if (logical == 0) v = make_uint4(one | (one << 16), one, 0u, 0u);                  // k 0..2
+            if (logical == 2) v = make_uint4(0u, one << 16, one | (one << 16), 0u);            // k 16+3..16+5
+            sts128(smem_u32(augA) + r * 128 + c * 16, v);
+        }
+    }
+    fence_proxy_async();
     if (warp == kMmaWarp) {
         tmem_alloc(tmem_sh, 512);
         tmem_relinquish();
@@ -192,6 +231,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
             __syncwarp();
+            // the per-query vectors of step n + 1 are loaded while step n's stage is
+            // refilled (software pipelined: their global-load latency stays off q_full)
+            float vu[2], vl[2], vd[2];
+            auto fetch = [&](int n) {
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const int64_t t = (qt_lo + n) * BMQ + lane + 32 * i;
+                    const bool ok = n < nsteps && t < p.Nq;
+                    const int64_t vi = (b * p.H + h) * p.Nq + t;
+                    vu[i] = ok ? Ubh[t + p.h0] : 0.f;
+                    vl[i] = ok ? p.LSE[vi] : 0.f;
+                    vd[i] = ok ? p.Dv[vi] : 0.f;
+                }
+            };
+            fetch(0);
             for (int n = 0; n < nsteps; ++n) {
                 const int s = n % NQS;
                 const int64_t t0 = (qt_lo + n) * BMQ;
@@ -205,16 +259,31 @@ __global__ void __launch_bounds__(kThreads, 1)
                         tma_load_4d(qd + kQT + half * kQTbox, &mdo, &bars->q_full[s], half * 64, (int)h, (int)t0,
                                     (int)b);
                     }
+                    if (GFWA_BWD_L2PF > 0 && n + GFWA_BWD_L2PF < nsteps) {
+                        const int tp = (int)(t0 + GFWA_BWD_L2PF * BMQ);
+                        for (int half = 0; half < kHalves; ++half) {
+                            tma_prefetch_l2_4d(&mq, half * 64, (int)h, tp, (int)b);
+                            tma_prefetch_l2_4d(&mdo, half * 64, (int)h, tp, (int)b);
+                        }
+                    }
                 }
-                for (int q = lane; q < BMQ; q += 32) {
-                    const int64_t t = t0 + q;
-                    const bool ok = t < p.Nq;
-                    const int64_t vi = (b * p.H + h) * p.Nq + t;
-                    s_cq[s][q] = ok ? (Ubh[t + p.h0] - uref) * kLog2e - p.LSE[vi] * kLog2e : 0.f;
-                    s_D[s][q] = ok ? p.Dv[vi] : 0.f;
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const int q = lane + 32 * i;
+                    const bool ok = t0 + q < p.Nq;
+                    const float c = ok ? ((vu[i] - uref) - vl[i]) * p.inv_scale : 0.f;
+                    const float dv = ok ? -vd[i] : 0.f;
+                    uint32_t ch, cm, cl, dh, dm, dl;
+                    split3_bf16(c, ch, cm, cl);
+                    split3_bf16(dv, dh, dm, dl);
+                    // k 0..7 of the slab: [c_hi, c_mid, c_lo, -D_hi, -D_mid, -D_lo, 0, 0]
+                    const uint4 v = make_uint4(ch | (cm << 16), cl | (dh << 16), dm | (dl << 16), 0u);
+                    sts128(smem_u32(augB) + (q >> 3) * 1024 + (q & 7) * 128 + (((2 * s) ^ (q & 7)) * 16), v);
                 }
+                fence_proxy_async();  // generic-proxy writes -> the tensor core's async proxy
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bars->q_full[s]);
+                fetch(n + 1);
             }
         }
     } else if (warp == kMmaWarp) {
@@ -233,14 +302,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t qb = smem_u32(Qs + sm * 2 * kQT), ob = qb + kQT, sb = smem_u32(dSs + bm * kDS);
                 // dQ^T = K^T dS^T, one N = 64 chain into the freed columns [64,128)
 #pragma unroll
-                for (int kk = 0; kk < BN / 16; ++kk)
+                for (int kk = 0; kk < BN / 16 && GFWA_BWD_EXPT != 1; ++kk)
                     mma_ss(buf + 64, sdesc_sw128(kb + kk * 2048, kKVbox, 1024),
                            sdesc_sw128(sb + kk * 2048, 8192, 1024), id_dq, kk > 0 ? 1u : 0u);
                 tc_commit(&bars->dq_full[bm]);
                 // dV += P^T dO ; dK += dS^T Q   (P^T and dS^T of queries [32 g, 32 g + 32) in
                 // columns [32 g, 32 g + 16) and [32 g + 16, 32 g + 32); 16 queries = 8 columns per K step)
 #pragma unroll
-                for (int kk = 0; kk < BMQ / 16; ++kk) {
+                for (int kk = 0; kk < BMQ / 16 && GFWA_BWD_EXPT != 1; ++kk) {
                     const uint32_t acc = (m > 0 || kk > 0) ? 1u : 0u;
                     // queries [16 kk, 16 kk + 16): warpgroup kk / 2's columns, half kk % 2
                     const uint32_t pc = QPW * ((16 * kk) / QPW) + 8 * (kk % (QPW / 16));
@@ -256,18 +325,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int n = 0; n < nsteps; ++n) {
             const int bn = n & 1, s = n % NQS;
             mbar_wait(&bars->q_full[s], (n / NQS) & 1);
+            if (lane == 0) BTR(7, 2 * n);
             if (n >= 2) mbar_wait(&bars->dq_drained[bn], ((n - 2) >> 1) & 1);
+            if (lane == 0) BTR(7, 2 * n + 1);
             tc_fence_after();
             if (elect_one()) {
                 const uint32_t qb = smem_u32(Qs + s * 2 * kQT), ob = qb + kQT;
                 const uint32_t buf = tmem + 128 * bn;
 #pragma unroll
-                for (int kk = 0; kk < D / 16; ++kk) {
+                for (int kk = 0; kk < D / 16 && GFWA_BWD_EXPT != 2; ++kk) {
                     const uint32_t ka = (kk >> 2) * kKVbox + (kk & 3) * 32;
                     const uint32_t qa = (kk >> 2) * kQTbox + (kk & 3) * 32;
                     mma_ss(buf, sdesc_sw128(kb + ka, 16, 1024), sdesc_sw128(qb + qa, 16, 1024), id_st, kk > 0);
                     mma_ss(buf + 64, sdesc_sw128(vb + ka, 16, 1024), sdesc_sw128(ob + qa, 16, 1024), id_st, kk > 0);
                 }
+                // + the per-query bias slabs (C-25): A rows repeat (SBO = 0), B = stage s's slab
+                const uint64_t bslab = sdesc_sw128(smem_u32(augB) + 32 * s, 16, 1024);
+                mma_ss(buf, sdesc_sw128(smem_u32(augA), 16, 0), bslab, id_st, 1u);
+                mma_ss(buf + 64, sdesc_sw128(smem_u32(augA) + 32, 16, 0), bslab, id_st, 1u);
                 tc_commit(&bars->st_full[bn]);
                 BTR(1, 2 * n);
             }
@@ -286,13 +361,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t lane_addr = tmem + ((uint32_t)((warp & 3) * 32) << 16);
         uint64_t colsum2 = 0;  // packed (0.f, 0.f)
         for (int n = 0; n < nsteps; ++n) {
-            const int bn = n & 1, s = n % NQS;
+            const int bn = n & 1;
             const int64_t t0 = (qt_lo + n) * BMQ;
             mbar_wait(&bars->st_full[bn], (n >> 1) & 1);
             if (threadIdx.x == 0) BTR(0, 3 * n);
-            // the producer's per-step vectors (s_cq, s_D): acquire them from its own
-            // arrive (already complete) rather than through the tensor core's commit
-            mbar_wait(&bars->q_full[s], (n / NQS) & 1);
             tc_fence_after();
             const uint32_t scol = 128 * bn + QPW * wg;  // this WG's S^T columns (dP^T at +64)
             // keys in (g - w, g] of each query g = t + h0, as a column range
@@ -303,8 +375,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int64_t qlo = j - p.h0 - t0, qhi = min64(j - p.h0 - t0 + p.w - 1, p.Nq - 1 - t0);
                 keep = kvalid ? range_bits((int)max64(qlo, -1), (int)min64(qhi, (int64_t)BMQ), QPW * wg) : 0u;
             }
-            const float* cq = &s_cq[s][QPW * wg];
-            const float* Dq = &s_D[s][QPW * wg];
             float ds[QPW];
             uint32_t pk[QPW / 2], dk[QPW / 2];
             uint32_t sall[QPW], dall[QPW];  // both TMEM loads in flight before one wait
@@ -316,54 +386,53 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tmem_ld16(lane_addr + scol + 64, *reinterpret_cast<uint32_t(*)[16]>(dall));
             }
             tmem_wait_ld();
+            if (threadIdx.x == 0) BTR(6, 3 * n);
             // each warpgroup packs its P^T, dS^T over its own S^T columns (no
-            // cross-warpgroup barrier); dQ^T then gets [64,128) whole
-            for (int h16 = 0; h16 < QPW; h16 += 16) {
-                const uint32_t* s16 = sall + h16;
-                const uint32_t* d16 = dall + h16;
+            // cross-warpgroup barrier); dQ^T then gets [64,128) whole.  Two copies of
+            // the loop: interior steps (every (key, query) pair in the window) carry no
+            // per-element mask instructions at all
+            auto calc = [&](auto masked_tag) {
+                constexpr bool kMasked = decltype(masked_tag)::value;
 #pragma unroll
-                for (int e = 0; e < 16; e += 4) {
-                    const float4 c4 = *reinterpret_cast<const float4*>(cq + h16 + e);
-                    const float4 d4 = *reinterpret_cast<const float4*>(Dq + h16 + e);
+                for (int h16 = 0; h16 < QPW; h16 += 16) {
+                    const uint32_t* s16 = sall + h16;
+                    const uint32_t* d16 = dall + h16;
 #pragma unroll
-                    for (int u = 0; u < 2; ++u) {
-                    const int a = e + 2 * u, e2 = h16 + a;
-                    // P = exp(scale q.k + (u_q - u_k) - L_q), log2 units
-                    uint64_t x = ffma2(f2pack(__uint_as_float(s16[a]), __uint_as_float(s16[a + 1])), sl2x2,
-                                       u == 0 ? f2pack(c4.x, c4.y) : f2pack(c4.z, c4.w));
-                    x = fadd2(x, nuk2);
-                    float x0, x1;
-                    f2unpack(x, x0, x1);
-                    if (!interior) {
-                        x0 = ((keep >> e2) & 1u) ? x0 : -INFINITY;
-                        x1 = ((keep >> (e2 + 1)) & 1u) ? x1 : -INFINITY;
-                    }
-                    uint64_t pr;
-                    if (u < kBwdPoly) {
-                        // part of the exponentials on the FMA pipe: MUFU, SHFL and LDS
-                        // share the MIO queue, which bounds this loop
-                        pr = exp2_poly2(f2pack(x0, x1));
-                        if (!interior) {
-                            float q0, q1;
-                            f2unpack(pr, q0, q1);
-                            pr = f2pack(((keep >> e2) & 1u) ? q0 : 0.f, ((keep >> (e2 + 1)) & 1u) ? q1 : 0.f);
+                    for (int a = 0; a < 16; a += 2) {
+                        const int e2 = h16 + a;
+                        // P = exp(scale q.k + (u_q - u_k) - L_q), log2 units: the
+                        // per-query part is already in S^T (C-25), the per-key part is nuk
+                        const uint64_t x = ffma2(f2pack(__uint_as_float(s16[a]), __uint_as_float(s16[a + 1])), sl2x2,
+                                                 nuk2);
+                        float x0, x1;
+                        f2unpack(x, x0, x1);
+                        if constexpr (kMasked) {
+                            x0 = ((keep >> e2) & 1u) ? x0 : -INFINITY;
+                            x1 = ((keep >> (e2 + 1)) & 1u) ? x1 : -INFINITY;
                         }
-                    } else {
-                        pr = f2pack(ex2(x0), ex2(x1));
-                    }
-                    // dS = P (dP - D)
-                    const uint64_t dpd = fadd2(f2pack(__uint_as_float(d16[a]), __uint_as_float(d16[a + 1])),
-                                               u == 0 ? f2pack(-d4.x, -d4.y) : f2pack(-d4.z, -d4.w));
-                    const uint64_t dsv = fmul2(pr, dpd);
-                    colsum2 = fadd2(colsum2, dsv);  // du^k, fp32 (C-4)
-                    float p0, p1;
-                    f2unpack(pr, p0, p1);
-                    f2unpack(dsv, ds[e2], ds[e2 + 1]);
-                    pk[e2 / 2] = pack_bf16x2(p0, p1);
-                    dk[e2 / 2] = pack_bf16x2(ds[e2], ds[e2 + 1]);
+                        const uint64_t pr = GFWA_BWD_EXPT == 3 ? fmul2(f2pack(x0, x1), sl2x2) : f2pack(ex2(x0), ex2(x1));
+                        // dS = P (dP - D); dP^T already holds dP - D (C-25)
+                        const uint64_t dsv = fmul2(pr, f2pack(__uint_as_float(d16[a]), __uint_as_float(d16[a + 1])));
+                        colsum2 = fadd2(colsum2, dsv);  // du^k, fp32 (C-4)
+                        float p0, p1;
+                        f2unpack(pr, p0, p1);
+                        f2unpack(dsv, ds[e2], ds[e2 + 1]);
+                        pk[e2 / 2] = pack_bf16x2(p0, p1);
+                        dk[e2 / 2] = pack_bf16x2(ds[e2], ds[e2 + 1]);
                     }
                 }
+            };
+            if (GFWA_BWD_EXPT == 5) {
+#pragma unroll
+                for (int e = 0; e < QPW; ++e) ds[e] = __uint_as_float(sall[e] ^ dall[e]);
+#pragma unroll
+                for (int e = 0; e < QPW / 2; ++e) pk[e] = dk[e] = sall[e];
+            } else if (interior) {
+                calc(std::false_type{});
+            } else {
+                calc(std::true_type{});
             }
+            if (threadIdx.x == 0) BTR(6, 3 * n + 1);
             // P^T -> columns [QPW wg, QPW wg + QPW/2), dS^T -> [QPW wg + QPW/2, QPW wg + QPW)
             if constexpr (QPW == 32) {
                 tmem_st16(lane_addr + 128 * bn + QPW * wg, *reinterpret_cast<const uint32_t(*)[16]>(pk));
@@ -390,7 +459,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             // transpose-reduce -> lane l holds query 32 wg + l; the drain warpgroup
             // sums the 4 warps' partials and issues the red.add (C-11)
 #pragma unroll
-            for (int sft = QPW / 2; sft >= 1; sft >>= 1) {
+            for (int sft = QPW / 2; sft >= 1 && !GFWA_BWD_NODUQ && GFWA_BWD_EXPT != 5; sft >>= 1) {
                 const bool up = lane & sft;
 #pragma unroll
                 for (int e = 0; e < sft; ++e) {
@@ -399,6 +468,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ds[e] = keepv + __shfl_xor_sync(0xffffffffu, send, sft);
                 }
             }
+            if (threadIdx.x == 0) BTR(6, 3 * n + 2);
             if (n >= 2) mbar_wait(&bars->red_free[bn], ((n - 2) >> 1) & 1);
             if (QPW < 32) ds[0] += __shfl_xor_sync(0xffffffffu, ds[0], QPW);  // lane halves hold the same query
             if (lane < QPW) s_red[bn][wg][warp & 3][lane] = ds[0];
@@ -538,7 +608,8 @@ done:
 
 template <int D>
 constexpr size_t smem_bytes() {
-    return 1024 + BwdLay<D>::kKslot + BwdLay<D>::kV + NQS * 2 * BwdLay<D>::kQT + 2 * kDS + kDQ + sizeof(Bars) + 16;
+    return 1024 + BwdLay<D>::kKslot + BwdLay<D>::kV + NQS * 2 * BwdLay<D>::kQT + 2 * kDS + kDQ + kAugA + kAugB +
+           sizeof(Bars) + 16;
 }
 
 // dQacc zeroing fused with D = rowsum(O dO)  (Alg. E.2 l.7; O + O_lo, C-12)
@@ -706,6 +777,7 @@ static gfwa_status_t tc_bwd_d(const AttnParams& pin, cudaStream_t st, void* ws) 
     tp.w = p.w;
     tp.sl2 = p.scale * kLog2e;
     tp.scale = p.scale;
+    tp.inv_scale = 1.f / p.scale;
     tp.token = p.token;
     // per launch: the attribute is per device (a process may drive several GPUs)
     constexpr size_t kSmemBytes = smem_bytes<D>();

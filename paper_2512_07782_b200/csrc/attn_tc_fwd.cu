@@ -432,7 +432,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                         live[c] = __any_sync(0xffffffffu, keep[c] != 0u);
                     }
                 }
-                const bool any = live[0] || live[1];
                 // pass 1: logits x = scale*q.k - (u_k - uref) log2e (Alg. 2 l.12-15, masked to
                 // -inf outside the window), the half-row max, x written back over S
                 float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};

@@ -31,10 +31,12 @@ for cta in (150, 200):
     base = t[5, 2]
     rel = lambda v: int(v - base) if v > 0 else -1  # noqa: E731
     print(f"=== CTA {cta}: start->tmem {rel(t[5,0])}, end {rel(t[5,1])}, dkdv_full {rel(t[4,0])}, epi done {rel(t[4,1])}")
-    print(" n | Qload  S_iss  sm_beg  ds_rdy  bfly   grad_iss dq_full drained | sm_work  gap_S->sm")
+    print(" n | Qload  S_iss  sm_beg  ld_done calc  ds_rdy  bfly_end red_free grad_iss dq_full drained | ld calc st bfly | qfull drnd(n-2)")
     for n in range(12):
         if t[0, 3 * n] == 0:
             break
-        row = [rel(t[3, n]), rel(t[1, 2 * n]), rel(t[0, 3 * n]), rel(t[0, 3 * n + 1]), rel(t[0, 3 * n + 2]),
+        row = [rel(t[3, n]), rel(t[1, 2 * n]), rel(t[0, 3 * n]), rel(t[6, 3 * n]), rel(t[6, 3 * n + 1]),
+               rel(t[0, 3 * n + 1]), rel(t[6, 3 * n + 2]), rel(t[0, 3 * n + 2]),
                rel(t[1, 2 * n + 1]), rel(t[2, 2 * n]), rel(t[2, 2 * n + 1])]
-        print(f"{n:2d} | " + " ".join(f"{v:6d}" for v in row) + f" | {row[3]-row[2]:6d} {row[2]-row[1]:6d}")
+        d = [row[3] - row[2], row[4] - row[3], row[5] - row[4], row[6] - row[5]]
+        print(f"{n:2d} | " + " ".join(f"{v:6d}" for v in row) + " | " + " ".join(f"{v:5d}" for v in d) + f" | {rel(t[7, 2 * n]):6d} {rel(t[7, 2 * n + 1]):6d}")
