@@ -1,8 +1,12 @@
 // attn_tc_bwd.cu -- GatedFWA backward on the 5th-generation tensor cores
 // (sm_100a): Alg. E.2 with readings C-3, C-4, C-11, C-12.
 //
-// KV-major: one CTA owns a 128-key tile of one (b, h) (K and V resident in
-// smem) and walks the 64-query steps whose windows reach it.
+// KV-major and persistent: one CTA per SM walks work items, each a 128-key
+// tile of one (b, h) (K and V resident in smem) and the 64-query steps whose
+// windows reach it.  The next item's K, V and first Q/dO stage
+// are loaded into a rotating pool of shared-memory slots while the current
+// item's last steps run, and its dK/dV epilogue overlaps the next item's
+// first steps, so per-item prologue and epilogue latency is hidden.
 // All five contractions run on tcgen05 with TMEM accumulators, pipelined
 // across steps with two TMEM buffers (S^T/dP^T of step n are produced while
 // the gradients of step n-1 are contracted):
@@ -22,7 +26,8 @@
 // C-11) is a cross-thread sum over keys done in fp32 with a warp butterfly
 // transpose-reduce (after dS is handed to the MMA warp) and a cross-warp sum by
 // the drain warpgroup, so both sums see the same fp32 dS and sum_m dU_m
-// telescopes to zero.  dK, dV leave through smem + TMA stores.
+// telescopes to zero.  dK, dV are read out of TMEM by the drain warpgroup
+// (which then releases the accumulators) and stored as bf16 rows.
 #include <type_traits>
 
 #include "attn_common.cuh"
@@ -36,7 +41,6 @@ using namespace sm100;
 
 constexpr int BN = 128;   // keys per CTA
 constexpr int BMQ = 64;   // queries per step
-constexpr int NQS = 3;    // Q/dO ring stages
 constexpr uint32_t kDQ = 32 * 128 * 4;    // 16 KB dQ staging: 4 warps x 2 x (16 queries x 32 d) fp32
 constexpr uint32_t kDQW = 16 * 32 * 4;    // 2 KB: one drain warp's box
 constexpr uint32_t kKVbox = 128 * 64 * 2;  // 16 KB: 128 key rows x 64 d (one 128-byte swizzle row)
@@ -46,7 +50,6 @@ constexpr uint32_t kQTbox = 64 * 64 * 2;   // 8 KB: 64 query rows x 64 d
 // dQ^T rows 64..127 come out zero); V, Q, dO tiles are D wide
 template <int D>
 struct BwdLay {
-    static constexpr uint32_t kKslot = 2 * kKVbox;  // 32 KB
     static constexpr uint32_t kV = 128 * D * 2;
     static constexpr uint32_t kQT = 64 * D * 2;      // Q or dO tile
 };
@@ -54,8 +57,8 @@ constexpr uint32_t kDS = 128 * 64 * 2;    // 16 KB dS^T tile
 // bias folding (reading C-25): the per-query terms of the exponent and of dP - D enter
 // the S^T and dP^T accumulators through one extra K = 16 slab each.  A side: one 1 KB
 // 128B-swizzle atom whose 8 rows are identical (read with SBO = 0 for all 128 key rows);
-// slab 0 = ones at k 0..2 (S^T), slab 1 = ones at k 3..5 (dP^T).  B side: per Q stage s,
-// slab s of a 64-row atom column holds [c'_hi, c'_mid, c'_lo, -D_hi, -D_mid, -D_lo, 0...]
+// slab 0 = ones at k 0..2 (S^T), slab 1 = ones at k 3..5 (dP^T).  B side: per step g,
+// slab g % 4 of a 64-row atom column holds [c'_hi, c'_mid, c'_lo, -D_hi, -D_mid, -D_lo, 0...]
 // per query, c' = ((u_q - uref) - L_q) / scale split into three bf16 (24 bits), so that
 // sl2 (S^T + c') = scale log2e q.k + (u_q - uref - L_q) log2e and dP^T + (-D) = dP - D.
 constexpr uint32_t kAugA = 1024, kAugB = 64 * 128;
@@ -69,11 +72,11 @@ constexpr int kThreads = 32 * (kTmaWarp + 1);  // softmax-grad WGs, drain WG, MM
 #ifndef GFWA_BWD_NODQ
 #define GFWA_BWD_NODQ 0  // experiment only: skip the dQ reductions
 #endif
+#ifndef GFWA_BWD_DQRED
+#define GFWA_BWD_DQRED 0  // 1: dQ^T drained by per-query red.global.add instead of TMA bulk reductions
+#endif
 #ifndef GFWA_BWD_NODUQ
 #define GFWA_BWD_NODUQ 0  // experiment only: skip the du^q butterfly (wrong dU)
-#endif
-#ifndef GFWA_BWD_L2PF
-#define GFWA_BWD_L2PF 0  // experiment: L2 prefetch distance (steps) of the Q/dO tiles
 #endif
 #ifndef GFWA_BWD_EXPT
 #define GFWA_BWD_EXPT 0  // experiment only (wrong results): 1 no grad MMAs, 2 no S/dP MMAs, 3 ex2 -> fmul, 5 no softmax math,
@@ -84,10 +87,14 @@ struct TcBwdParams {
     const float* U;
     const float* LSE;
     const float* Dv;
-    float* dQacc;  // [B, Nq, H, d] fp32, zeroed by the preprocess kernel
+    float* dQacc;  // [B, Nq, H, d] fp32, zeroed by the preprocess kernel (or gfwa_fwd_train)
     float* dU;     // [B, H, Nkv] fp32, zeroed before the launch
+    __nv_bfloat16* dK;
+    __nv_bfloat16* dV;
+    int64_t ks[3], vs[3];  // dK / dV element strides over (b, n, h) (those of K / V)
     int64_t Nq, Nkv, h0, H;
     int w;
+    int n_kt, n_items;  // key tiles per (b, h); work items = key tiles x H x B
     float sl2, scale, inv_scale;
     unsigned long long* token;  // prepared-workspace token: consumed (cleared) by this kernel
 };
@@ -96,12 +103,11 @@ struct TcBwdParams {
 #define GFWA_BWD_TRACE 0  // diagnostics build only: clock64 stamps per role into a device array
 #endif
 #if GFWA_BWD_TRACE
-constexpr int kBTr = 256;  // stamps per (CTA, role), first 296 CTAs
-__device__ long long g_bwd_trace[296 * 8 * kBTr];
-#define BTR(role, k)                                                                                        \
-    do {                                                                                                    \
-        const int cta_ = (int)(blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z));              \
-        if ((k) < kBTr && cta_ < 296) g_bwd_trace[(cta_ * 8 + (role)) * kBTr + (k)] = clock64();            \
+constexpr int kBTr = 512;  // stamps per (CTA, role), first 148 CTAs
+__device__ long long g_bwd_trace[148 * 8 * kBTr];
+#define BTR(role, k)                                                                        \
+    do {                                                                                    \
+        if ((k) < kBTr && blockIdx.x < 148) g_bwd_trace[(blockIdx.x * 8 + (role)) * kBTr + (k)] = clock64(); \
     } while (0)
 #else
 #define BTR(role, k) \
@@ -109,11 +115,33 @@ __device__ long long g_bwd_trace[296 * 8 * kBTr];
     } while (0)
 #endif
 
+// Shared-memory slot pool: five 32 KB slots hold the current item's K and V and
+// the three Q/dO stages of its steps.  At an item boundary the roles rotate so
+// the NEXT item's K, V and first Q/dO stage are loaded while the current item's
+// last steps still run (its K is the last slot released, after the final
+// gradient MMAs; V is released once the last dP^T MMA has read it):
+//   K' = q[n % 3] (freed by step n-3), V' = V, q0' = q[(n+1) % 3] (step n-2),
+//   q1' = q[(n+2) % 3] (step n-1), q2' = K
+// Every role that touches the pool replays the same rotation, so no slot index
+// is ever communicated.
+constexpr int kPool = 5;
+constexpr uint32_t kSlot = 32768;
+struct Pool {
+    uint32_t s = 0u | (1u << 3) | (2u << 6) | (3u << 9) | (4u << 12);  // K, V, q0, q1, q2 (3 bits each)
+    __device__ __forceinline__ uint32_t f(int i) const { return (s >> (3 * i)) & 7u; }
+    __device__ __forceinline__ uint32_t K() const { return f(0); }
+    __device__ __forceinline__ uint32_t V() const { return f(1); }
+    __device__ __forceinline__ uint32_t Q(int m) const { return f(2 + m % 3); }
+    __device__ __forceinline__ void advance(int n) {
+        const uint32_t k = K(), v = V(), a = Q(n), b = Q(n + 1), c = Q(n + 2);
+        s = a | (v << 3) | (b << 6) | (c << 9) | (k << 12);
+    }
+};
+
 struct __align__(8) Bars {
-    uint64_t kv_full;
-    uint64_t q_full[NQS], q_empty[NQS];
+    uint64_t full[kPool], empty[kPool], aug_empty[4];
     uint64_t st_full[2], ds_ready[2], dq_full[2], dq_drained[2], red_ready[2], red_free[2];
-    uint64_t dkdv_full;
+    uint64_t dkdv_full, dkdv_free;
 };
 
 __device__ __forceinline__ void red_add(float* addr, float a) {
@@ -138,46 +166,52 @@ __device__ __forceinline__ uint32_t range_bits(int lo, int hi, int base) {
     return upto_z & ~below_a;
 }
 
+// One work item: a 128-key tile of one (b, h) and the 64-query steps whose
+// windows reach it (Alg. E.2 l.12-14)
+struct BItem {
+    int b, h, j0, qt_lo, nsteps;
+};
+__device__ __forceinline__ BItem make_bitem(const TcBwdParams& p, int idx) {
+    BItem it;
+    const int jt = idx % p.n_kt, bh = idx / p.n_kt;
+    it.h = bh % (int)p.H;
+    it.b = bh / (int)p.H;
+    it.j0 = jt * BN;
+    const int64_t j_last = min64((int64_t)it.j0 + BN, p.Nkv) - 1;
+    const int64_t t_lo = max64(0, (int64_t)it.j0 - p.h0);
+    const int64_t t_hi = min64(p.Nq - 1, j_last + p.w - 1 - p.h0);
+    it.qt_lo = (int)(t_lo / BMQ);
+    it.nsteps = t_lo <= t_hi ? (int)(t_hi / BMQ - it.qt_lo + 1) : 0;
+    return it;
+}
+
+// Persistent: one CTA per SM walks work items idx = blockIdx.x + k * gridDim.x.
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
     bwd_tc_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
                   const __grid_constant__ CUtensorMap mv, const __grid_constant__ CUtensorMap mdo,
                   const __grid_constant__ CUtensorMap mdk, const __grid_constant__ CUtensorMap mdv,
-                  const __grid_constant__ CUtensorMap mdq,
-                  const TcBwdParams p) {
+                  const __grid_constant__ CUtensorMap mdq, const TcBwdParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     constexpr uint32_t kKV = BwdLay<D>::kV, kQT = BwdLay<D>::kQT;
     constexpr int kHalves = D / 64;      // 64-column TMA boxes per row
-    uint8_t* Ks = smem;
-    uint8_t* Vs = Ks + BwdLay<D>::kKslot;
-    uint8_t* Qs = Vs + kKV;              // NQS stages of [Q tile | dO tile]
-    uint8_t* dSs = Qs + NQS * 2 * kQT;   // 2 x dS^T tile
+    uint8_t* pool_base = smem;           // kPool slots of kSlot bytes
+    uint8_t* dSs = pool_base + kPool * kSlot;  // 2 x dS^T tile
     uint8_t* dQs = dSs + 2 * kDS;        // dQ staging: per drain warp 2 x [16 queries][32 d] fp32, 128B swizzle
     uint8_t* augA = dQs + kDQ;           // 1 KB, see kAugA
-    uint8_t* augB = augA + kAugA;        // 8 KB: 64 query rows x 4 slabs (slab s = Q stage s)
+    uint8_t* augB = augA + kAugA;        // 8 KB: 64 query rows x 4 slabs (slab a = step g % 4)
     Bars* bars = (Bars*)(augB + kAugB);
     uint32_t* tmem_sh = (uint32_t*)(bars + 1);
     __shared__ float s_red[2][kSWG][4][QPW];          // [parity][wg][warp][query] du^q partials
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t b = blockIdx.z, h = blockIdx.y;
-    const int64_t j0 = (int64_t)blockIdx.x * BN;
-    const int64_t j_last = min64(j0 + BN, p.Nkv) - 1;
-    // Alg. E.2 l.12-14: queries whose window reaches this key tile
-    const int64_t t_lo = max64(0, j0 - p.h0);
-    const int64_t t_hi = min64(p.Nq - 1, j_last + p.w - 1 - p.h0);
-    const int64_t qt_lo = t_lo / BMQ;
-    const int nsteps = t_lo <= t_hi ? (int)(t_hi / BMQ - qt_lo + 1) : 0;
-    const float* Ubh = p.U + (b * p.H + h) * p.Nkv;
-
-    if (threadIdx.x == 0) BTR(5, 2);
     if (threadIdx.x == 0) {
-        mbar_init(&bars->kv_full, 1);
-        for (int s = 0; s < NQS; ++s) {
-            mbar_init(&bars->q_full[s], 2);  // TMA bytes + the vector stores
-            mbar_init(&bars->q_empty[s], 1);
+        for (int s = 0; s < kPool; ++s) {
+            mbar_init(&bars->full[s], 2);  // TMA bytes + the producer's own arrive (after its generic writes)
+            mbar_init(&bars->empty[s], 1);
         }
+        for (int a = 0; a < 4; ++a) mbar_init(&bars->aug_empty[a], 1);
         for (int i = 0; i < 2; ++i) {
             mbar_init(&bars->st_full[i], 1);
             mbar_init(&bars->ds_ready[i], 4 * kSWG);
@@ -187,11 +221,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&bars->red_free[i], 2);
         }
         mbar_init(&bars->dkdv_full, 1);
+        mbar_init(&bars->dkdv_free, 4);
         fence_barrier_init();
-    }
-    if (D < 128) {  // the zero second half of the K slot (K^T rows d >= D of the dQ^T MMA)
-        for (uint32_t i = threadIdx.x; i < kKVbox / 16; i += kThreads)
-            sts128(smem_u32(Ks + kKVbox) + i * 16, make_uint4(0u, 0u, 0u, 0u));
     }
     {  // bias-folding slabs: B zero except the per-step chunk the producer writes; A constant
         for (uint32_t i = threadIdx.x; i < kAugB / 16; i += kThreads)
@@ -214,63 +245,80 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_sh;
-    if (threadIdx.x == 0) BTR(5, 0);
-    const float uref = Ubh[j0];  // per-CTA bias reference (reading C-18)
     // the pre kernel has read the token (stream order): clear it, so the next backward
     // on this workspace zeroes its accumulator unless a new gfwa_fwd_train prepares it
-    if (p.token && threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) *p.token = 0ull;
+    if (p.token && threadIdx.x == 0 && blockIdx.x == 0) *p.token = 0ull;
 
     if (warp == kTmaWarp) {
         // ------------------------------------------------ producer: TMA + per-step vectors
-        if (nsteps > 0) {
-            if (elect_one()) {
-                mbar_expect_tx(&bars->kv_full, 2 * kKV);
-                for (int half = 0; half < kHalves; ++half) {
-                    tma_load_4d(Ks + half * kKVbox, &mk, &bars->kv_full, half * 64, (int)h, (int)j0, (int)b);
-                    tma_load_4d(Vs + half * kKVbox, &mv, &bars->kv_full, half * 64, (int)h, (int)j0, (int)b);
+        Pool pool;
+        uint32_t acq = 0;  // bit s: parity of the acquisitions of slot s so far
+        auto acquire = [&](uint32_t s) {
+            mbar_wait(&bars->empty[s], ((acq >> s) & 1u) ^ 1u);
+            acq ^= 1u << s;
+        };
+        int g = 0;
+        for (int idx = blockIdx.x; idx < p.n_items; idx += gridDim.x) {
+            const BItem it = make_bitem(p, idx);
+            if (it.nsteps == 0) continue;
+            const float* Ubh = p.U + ((int64_t)it.b * p.H + it.h) * p.Nkv;
+            const float uref = Ubh[it.j0];  // per-item bias reference (reading C-18)
+            // K and V of the item
+#pragma unroll 1
+            for (int kv = 0; kv < 2; ++kv) {
+                const uint32_t s = kv ? pool.V() : pool.K();
+                acquire(s);
+                uint8_t* dst = pool_base + s * kSlot;
+                if (D < 128 && kv == 0) {  // K^T rows d >= D of the dQ^T MMA (M = 128): zeros
+                    for (uint32_t i = lane; i < kKVbox / 16; i += 32)
+                        sts128(smem_u32(dst + kKVbox) + i * 16, make_uint4(0u, 0u, 0u, 0u));
+                    fence_proxy_async();
                 }
+                __syncwarp();
+                if (elect_one()) {
+                    mbar_expect_tx(&bars->full[s], kKV);
+                    for (int half = 0; half < kHalves; ++half)
+                        tma_load_4d(dst + half * kKVbox, kv ? &mv : &mk, &bars->full[s], half * 64, it.h, it.j0,
+                                    it.b);
+                    mbar_arrive(&bars->full[s]);
+                }
+                __syncwarp();
             }
-            __syncwarp();
-            // the per-query vectors of step n + 1 are loaded while step n's stage is
-            // refilled (software pipelined: their global-load latency stays off q_full)
+            // the per-query vectors of step m + 1 are loaded while step m's stage is
+            // refilled (software pipelined: their global-load latency stays off the full barrier)
             float vu[2], vl[2], vd[2];
-            auto fetch = [&](int n) {
+            auto fetch = [&](int m) {
 #pragma unroll
                 for (int i = 0; i < 2; ++i) {
-                    const int64_t t = (qt_lo + n) * BMQ + lane + 32 * i;
-                    const bool ok = n < nsteps && t < p.Nq;
-                    const int64_t vi = (b * p.H + h) * p.Nq + t;
+                    const int64_t t = (int64_t)(it.qt_lo + m) * BMQ + lane + 32 * i;
+                    const bool ok = m < it.nsteps && t < p.Nq;
+                    const int64_t vi = ((int64_t)it.b * p.H + it.h) * p.Nq + t;
                     vu[i] = ok ? Ubh[t + p.h0] : 0.f;
                     vl[i] = ok ? p.LSE[vi] : 0.f;
                     vd[i] = ok ? p.Dv[vi] : 0.f;
                 }
             };
             fetch(0);
-            for (int n = 0; n < nsteps; ++n) {
-                const int s = n % NQS;
-                const int64_t t0 = (qt_lo + n) * BMQ;
-                mbar_wait(&bars->q_empty[s], ((n / NQS) & 1) ^ 1);
-                if (lane == 0) BTR(3, n);
+            for (int m = 0; m < it.nsteps; ++m, ++g) {
+                const uint32_t s = pool.Q(m);
+                const int t0 = (it.qt_lo + m) * BMQ;
+                acquire(s);
+                if (lane == 0) BTR(3, g);
                 if (elect_one()) {
-                    mbar_expect_tx(&bars->q_full[s], 2 * kQT);
-                    uint8_t* qd = Qs + s * 2 * kQT;
+                    mbar_expect_tx(&bars->full[s], 2 * kQT);
+                    uint8_t* qd = pool_base + s * kSlot;
                     for (int half = 0; half < kHalves; ++half) {
-                        tma_load_4d(qd + half * kQTbox, &mq, &bars->q_full[s], half * 64, (int)h, (int)t0, (int)b);
-                        tma_load_4d(qd + kQT + half * kQTbox, &mdo, &bars->q_full[s], half * 64, (int)h, (int)t0,
-                                    (int)b);
-                    }
-                    if (GFWA_BWD_L2PF > 0 && n + GFWA_BWD_L2PF < nsteps) {
-                        const int tp = (int)(t0 + GFWA_BWD_L2PF * BMQ);
-                        for (int half = 0; half < kHalves; ++half) {
-                            tma_prefetch_l2_4d(&mq, half * 64, (int)h, tp, (int)b);
-                            tma_prefetch_l2_4d(&mdo, half * 64, (int)h, tp, (int)b);
-                        }
+                        tma_load_4d(qd + half * kQTbox, &mq, &bars->full[s], half * 64, it.h, t0, it.b);
+                        tma_load_4d(qd + kQT + half * kQTbox, &mdo, &bars->full[s], half * 64, it.h, t0, it.b);
                     }
                 }
+                // the bias slab of step g (slab g % 4, free once step g - 4's S^T/dP^T MMAs ran)
+                const int a = g & 3;
+                mbar_wait(&bars->aug_empty[a], ((g >> 2) & 1) ^ 1);
 #pragma unroll
                 for (int i = 0; i < 2; ++i) {
                     const int q = lane + 32 * i;
-                    const bool ok = t0 + q < p.Nq;
+                    const bool ok = (int64_t)t0 + q < p.Nq;
                     const float c = ok ? ((vu[i] - uref) - vl[i]) * p.inv_scale : 0.f;
                     const float dv = ok ? -vd[i] : 0.f;
                     uint32_t ch, cm, cl, dh, dm, dl;
@@ -278,28 +326,41 @@ __global__ void __launch_bounds__(kThreads, 1)
                     split3_bf16(dv, dh, dm, dl);
                     // k 0..7 of the slab: [c_hi, c_mid, c_lo, -D_hi, -D_mid, -D_lo, 0, 0]
                     const uint4 v = make_uint4(ch | (cm << 16), cl | (dh << 16), dm | (dl << 16), 0u);
-                    sts128(smem_u32(augB) + (q >> 3) * 1024 + (q & 7) * 128 + (((2 * s) ^ (q & 7)) * 16), v);
+                    sts128(smem_u32(augB) + (q >> 3) * 1024 + (q & 7) * 128 + (((2 * a) ^ (q & 7)) * 16), v);
                 }
                 fence_proxy_async();  // generic-proxy writes -> the tensor core's async proxy
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&bars->q_full[s]);
-                fetch(n + 1);
+                if (lane == 0) mbar_arrive(&bars->full[s]);
+                fetch(m + 1);
             }
+            pool.advance(it.nsteps);
         }
     } else if (warp == kMmaWarp) {
         // ------------------------------------------------ MMA issuer
         const uint32_t id_st = idesc_bf16(128, BMQ, false, false);  // S^T, dP^T
         const uint32_t id_tm = idesc_bf16(128, D, false, true);     // dV, dK (A in TMEM, B MN-major)
         const uint32_t id_dq = idesc_bf16(128, BMQ, true, true);    // dQ^T (A, B MN-major)
-        const uint32_t kb = smem_u32(Ks), vb = smem_u32(Vs);
-        if (nsteps > 0) mbar_wait(&bars->kv_full, 0);
-        auto mma2 = [&](int m) {  // gradients of step m
-            const int bm = m & 1, sm = m % NQS;
-            mbar_wait(&bars->ds_ready[bm], (m >> 1) & 1);
+        const uint32_t pb = smem_u32(pool_base);
+        Pool pool;
+        uint32_t fpar = 0;  // bit s: parity of the next fill of slot s to consume
+        auto wait_full = [&](uint32_t s) {
+            mbar_wait(&bars->full[s], (fpar >> s) & 1u);
+            fpar ^= 1u << s;
+        };
+        // the previous step, whose gradient MMAs are issued after this step's S^T / dP^T
+        int pg = -1, pm = 0, pn = 0, pitem = 0;
+        uint32_t ps = 0, pk = 0;
+        auto mma2 = [&]() {
+            const int bm = pg & 1;
+            mbar_wait(&bars->ds_ready[bm], (pg >> 1) & 1);
+            // the item's first gradient MMAs overwrite dV / dK: the epilogue must have read the last item's
+            if (pm == 0 && pitem > 0) mbar_wait(&bars->dkdv_free, (pitem - 1) & 1);
+            if (lane == 0) BTR(5, pg);
             tc_fence_after();
             if (elect_one()) {
                 const uint32_t buf = tmem + 128 * bm;
-                const uint32_t qb = smem_u32(Qs + sm * 2 * kQT), ob = qb + kQT, sb = smem_u32(dSs + bm * kDS);
+                const uint32_t qb = pb + ps * kSlot, ob = qb + kQT, kb = pb + pk * kSlot;
+                const uint32_t sb = smem_u32(dSs + bm * kDS);
                 // dQ^T = K^T dS^T, one N = 64 chain into the freed columns [64,128)
 #pragma unroll
                 for (int kk = 0; kk < BN / 16 && GFWA_BWD_EXPT != 1; ++kk)
@@ -310,239 +371,216 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // columns [32 g, 32 g + 16) and [32 g + 16, 32 g + 32); 16 queries = 8 columns per K step)
 #pragma unroll
                 for (int kk = 0; kk < BMQ / 16 && GFWA_BWD_EXPT != 1; ++kk) {
-                    const uint32_t acc = (m > 0 || kk > 0) ? 1u : 0u;
+                    const uint32_t acc = (pm > 0 || kk > 0) ? 1u : 0u;
                     // queries [16 kk, 16 kk + 16): warpgroup kk / 2's columns, half kk % 2
                     const uint32_t pc = QPW * ((16 * kk) / QPW) + 8 * (kk % (QPW / 16));
                     mma_ts(tmem + 256, buf + pc, sdesc_sw128(ob + kk * 2048, kQTbox, 1024), id_tm, acc);
                     mma_ts(tmem + 384, buf + pc + QPW / 2, sdesc_sw128(qb + kk * 2048, kQTbox, 1024), id_tm, acc);
                 }
-                tc_commit(&bars->q_empty[sm]);
-                BTR(1, 2 * m + 1);
-                if (m == nsteps - 1) tc_commit(&bars->dkdv_full);
+                tc_commit(&bars->empty[ps]);  // Q/dO stage free
+                // the item's K slot is released by the epilogue, which stages dV / dK in it
+                if (pm == pn - 1) tc_commit(&bars->dkdv_full);
             }
             __syncwarp();
         };
-        for (int n = 0; n < nsteps; ++n) {
-            const int bn = n & 1, s = n % NQS;
-            mbar_wait(&bars->q_full[s], (n / NQS) & 1);
-            if (lane == 0) BTR(7, 2 * n);
-            if (n >= 2) mbar_wait(&bars->dq_drained[bn], ((n - 2) >> 1) & 1);
-            if (lane == 0) BTR(7, 2 * n + 1);
-            tc_fence_after();
-            if (elect_one()) {
-                const uint32_t qb = smem_u32(Qs + s * 2 * kQT), ob = qb + kQT;
-                const uint32_t buf = tmem + 128 * bn;
-#pragma unroll
-                for (int kk = 0; kk < D / 16 && GFWA_BWD_EXPT != 2; ++kk) {
-                    const uint32_t ka = (kk >> 2) * kKVbox + (kk & 3) * 32;
-                    const uint32_t qa = (kk >> 2) * kQTbox + (kk & 3) * 32;
-                    mma_ss(buf, sdesc_sw128(kb + ka, 16, 1024), sdesc_sw128(qb + qa, 16, 1024), id_st, kk > 0);
-                    mma_ss(buf + 64, sdesc_sw128(vb + ka, 16, 1024), sdesc_sw128(ob + qa, 16, 1024), id_st, kk > 0);
+        int g = 0, nitem = 0;
+        for (int idx = blockIdx.x; idx < p.n_items; idx += gridDim.x) {
+            const BItem it = make_bitem(p, idx);
+            if (it.nsteps == 0) continue;
+            const uint32_t sK = pool.K(), sV = pool.V();
+            for (int m = 0; m < it.nsteps; ++m, ++g) {
+                const uint32_t s = pool.Q(m);
+                const int bn = g & 1;
+                if (m == 0) {
+                    wait_full(sK);
+                    wait_full(sV);
                 }
-                // + the per-query bias slabs (C-25): A rows repeat (SBO = 0), B = stage s's slab
-                const uint64_t bslab = sdesc_sw128(smem_u32(augB) + 32 * s, 16, 1024);
-                mma_ss(buf, sdesc_sw128(smem_u32(augA), 16, 0), bslab, id_st, 1u);
-                mma_ss(buf + 64, sdesc_sw128(smem_u32(augA) + 32, 16, 0), bslab, id_st, 1u);
-                tc_commit(&bars->st_full[bn]);
-                BTR(1, 2 * n);
+                wait_full(s);
+                if (g >= 2) mbar_wait(&bars->dq_drained[bn], ((g - 2) >> 1) & 1);
+                tc_fence_after();
+                if (lane == 0) BTR(1, g);
+                if (elect_one()) {
+                    const uint32_t qb = pb + s * kSlot, ob = qb + kQT;
+                    const uint32_t kb = pb + sK * kSlot, vb = pb + sV * kSlot;
+                    const uint32_t buf = tmem + 128 * bn;
+#pragma unroll
+                    for (int kk = 0; kk < D / 16 && GFWA_BWD_EXPT != 2; ++kk) {
+                        const uint32_t ka = (kk >> 2) * kKVbox + (kk & 3) * 32;
+                        const uint32_t qa = (kk >> 2) * kQTbox + (kk & 3) * 32;
+                        mma_ss(buf, sdesc_sw128(kb + ka, 16, 1024), sdesc_sw128(qb + qa, 16, 1024), id_st, kk > 0);
+                        mma_ss(buf + 64, sdesc_sw128(vb + ka, 16, 1024), sdesc_sw128(ob + qa, 16, 1024), id_st, kk > 0);
+                    }
+                    // + the per-query bias slabs (C-25): A rows repeat (SBO = 0), B = step g's slab
+                    const uint64_t bslab = sdesc_sw128(smem_u32(augB) + 32 * (g & 3), 16, 1024);
+                    mma_ss(buf, sdesc_sw128(smem_u32(augA), 16, 0), bslab, id_st, 1u);
+                    mma_ss(buf + 64, sdesc_sw128(smem_u32(augA) + 32, 16, 0), bslab, id_st, 1u);
+                    tc_commit(&bars->st_full[bn]);
+                    tc_commit(&bars->aug_empty[g & 3]);
+                    if (m == it.nsteps - 1) tc_commit(&bars->empty[sV]);  // V's last reader was this dP^T
+                }
+                __syncwarp();
+                if (pg >= 0) mma2();
+                pg = g;
+                pm = m;
+                pn = it.nsteps;
+                ps = s;
+                pk = sK;
+                pitem = nitem;
             }
-            __syncwarp();
-            if (n >= 1) mma2(n - 1);
+            pool.advance(it.nsteps);
+            ++nitem;
         }
-        if (nsteps > 0) mma2(nsteps - 1);
+        if (pg >= 0) mma2();
     } else if (warp < kDrainWarp0) {
-        // ------------------------------------------------ softmax-grad: thread = key, 32 queries per WG
+        // ------------------------------------------------ softmax-grad: thread = key, QPW queries per WG
         const int wg = warp >> 2;  // query columns [QPW wg, QPW wg + QPW) of each step
         const int kr = threadIdx.x & 127;
-        const int64_t j = j0 + kr;
-        const bool kvalid = j < p.Nkv;
-        const float nuk = kvalid ? -(Ubh[j] - uref) * kLog2e : 0.f;
-        const uint64_t sl2x2 = f2pack(p.sl2, p.sl2), nuk2 = f2pack(nuk, nuk);
+        const uint64_t sl2x2 = f2pack(p.sl2, p.sl2);
         const uint32_t lane_addr = tmem + ((uint32_t)((warp & 3) * 32) << 16);
-        uint64_t colsum2 = 0;  // packed (0.f, 0.f)
-        for (int n = 0; n < nsteps; ++n) {
-            const int bn = n & 1;
-            const int64_t t0 = (qt_lo + n) * BMQ;
-            mbar_wait(&bars->st_full[bn], (n >> 1) & 1);
-            if (threadIdx.x == 0) BTR(0, 3 * n);
-            tc_fence_after();
-            const uint32_t scol = 128 * bn + QPW * wg;  // this WG's S^T columns (dP^T at +64)
-            // keys in (g - w, g] of each query g = t + h0, as a column range
-            const bool interior = (j0 + BN - 1 <= t0 + p.h0) && (j0 > t0 + BMQ - 1 + p.h0 - p.w) &&
-                                  (t0 + BMQ <= p.Nq) && (j0 + BN <= p.Nkv);
-            uint32_t keep = ~0u;
-            if (!interior) {
-                const int64_t qlo = j - p.h0 - t0, qhi = min64(j - p.h0 - t0 + p.w - 1, p.Nq - 1 - t0);
-                keep = kvalid ? range_bits((int)max64(qlo, -1), (int)min64(qhi, (int64_t)BMQ), QPW * wg) : 0u;
-            }
-            float ds[QPW];
-            uint32_t pk[QPW / 2], dk[QPW / 2];
-            uint32_t sall[QPW], dall[QPW];  // both TMEM loads in flight before one wait
-            if constexpr (QPW == 32) {
-                tmem_ld32(lane_addr + scol, *reinterpret_cast<uint32_t(*)[32]>(sall));
-                tmem_ld32(lane_addr + scol + 64, *reinterpret_cast<uint32_t(*)[32]>(dall));
-            } else {
-                tmem_ld16(lane_addr + scol, *reinterpret_cast<uint32_t(*)[16]>(sall));
-                tmem_ld16(lane_addr + scol + 64, *reinterpret_cast<uint32_t(*)[16]>(dall));
-            }
-            tmem_wait_ld();
-            if (threadIdx.x == 0) BTR(6, 3 * n);
-            // each warpgroup packs its P^T, dS^T over its own S^T columns (no
-            // cross-warpgroup barrier); dQ^T then gets [64,128) whole.  Two copies of
-            // the loop: interior steps (every (key, query) pair in the window) carry no
-            // per-element mask instructions at all
-            auto calc = [&](auto masked_tag) {
-                constexpr bool kMasked = decltype(masked_tag)::value;
+        int g = 0;
+        for (int idx = blockIdx.x; idx < p.n_items; idx += gridDim.x) {
+            const BItem it = make_bitem(p, idx);
+            if (it.nsteps == 0) continue;
+            const float* Ubh = p.U + ((int64_t)it.b * p.H + it.h) * p.Nkv;
+            const int64_t j0 = it.j0, j = j0 + kr;
+            const bool kvalid = j < p.Nkv;
+            const float uref = Ubh[j0];
+            const float nuk = kvalid ? -(Ubh[j] - uref) * kLog2e : 0.f;
+            const uint64_t nuk2 = f2pack(nuk, nuk);
+            uint64_t colsum2 = 0;  // packed (0.f, 0.f)
+            for (int m = 0; m < it.nsteps; ++m, ++g) {
+                const int bn = g & 1;
+                const int64_t t0 = (int64_t)(it.qt_lo + m) * BMQ;
+                mbar_wait(&bars->st_full[bn], (g >> 1) & 1);
+                if (threadIdx.x == 0) BTR(0, g);
+                tc_fence_after();
+                const uint32_t scol = 128 * bn + QPW * wg;  // this WG's S^T columns (dP^T at +64)
+                // keys in (g - w, g] of each query g = t + h0, as a column range
+                const bool interior = (j0 + BN - 1 <= t0 + p.h0) && (j0 > t0 + BMQ - 1 + p.h0 - p.w) &&
+                                      (t0 + BMQ <= p.Nq) && (j0 + BN <= p.Nkv);
+                uint32_t keep = ~0u;
+                if (!interior) {
+                    const int64_t qlo = j - p.h0 - t0, qhi = min64(j - p.h0 - t0 + p.w - 1, p.Nq - 1 - t0);
+                    keep = kvalid ? range_bits((int)max64(qlo, -1), (int)min64(qhi, (int64_t)BMQ), QPW * wg) : 0u;
+                }
+                float ds[QPW];
+                uint32_t pk[QPW / 2], dk[QPW / 2];
+                uint32_t sall[QPW], dall[QPW];  // both TMEM loads in flight before one wait
+                if constexpr (QPW == 32) {
+                    tmem_ld32(lane_addr + scol, *reinterpret_cast<uint32_t(*)[32]>(sall));
+                    tmem_ld32(lane_addr + scol + 64, *reinterpret_cast<uint32_t(*)[32]>(dall));
+                } else {
+                    tmem_ld16(lane_addr + scol, *reinterpret_cast<uint32_t(*)[16]>(sall));
+                    tmem_ld16(lane_addr + scol + 64, *reinterpret_cast<uint32_t(*)[16]>(dall));
+                }
+                tmem_wait_ld();
+                // each warpgroup packs its P^T, dS^T over its own S^T columns (no
+                // cross-warpgroup barrier); dQ^T then gets [64,128) whole.  Two copies of
+                // the loop: interior steps (every (key, query) pair in the window) carry no
+                // per-element mask instructions at all
+                auto calc = [&](auto masked_tag) {
+                    constexpr bool kMasked = decltype(masked_tag)::value;
 #pragma unroll
-                for (int h16 = 0; h16 < QPW; h16 += 16) {
-                    const uint32_t* s16 = sall + h16;
-                    const uint32_t* d16 = dall + h16;
+                    for (int h16 = 0; h16 < QPW; h16 += 16) {
+                        const uint32_t* s16 = sall + h16;
+                        const uint32_t* d16 = dall + h16;
 #pragma unroll
-                    for (int a = 0; a < 16; a += 2) {
-                        const int e2 = h16 + a;
-                        // P = exp(scale q.k + (u_q - u_k) - L_q), log2 units: the
-                        // per-query part is already in S^T (C-25), the per-key part is nuk
-                        const uint64_t x = ffma2(f2pack(__uint_as_float(s16[a]), __uint_as_float(s16[a + 1])), sl2x2,
-                                                 nuk2);
-                        float x0, x1;
-                        f2unpack(x, x0, x1);
-                        if constexpr (kMasked) {
-                            x0 = ((keep >> e2) & 1u) ? x0 : -INFINITY;
-                            x1 = ((keep >> (e2 + 1)) & 1u) ? x1 : -INFINITY;
+                        for (int a = 0; a < 16; a += 2) {
+                            const int e2 = h16 + a;
+                            // P = exp(scale q.k + (u_q - u_k) - L_q), log2 units: the
+                            // per-query part is already in S^T (C-25), the per-key part is nuk
+                            const uint64_t x = ffma2(f2pack(__uint_as_float(s16[a]), __uint_as_float(s16[a + 1])),
+                                                     sl2x2, nuk2);
+                            float x0, x1;
+                            f2unpack(x, x0, x1);
+                            if constexpr (kMasked) {
+                                x0 = ((keep >> e2) & 1u) ? x0 : -INFINITY;
+                                x1 = ((keep >> (e2 + 1)) & 1u) ? x1 : -INFINITY;
+                            }
+                            const uint64_t pr = GFWA_BWD_EXPT == 3 ? fmul2(f2pack(x0, x1), sl2x2)
+                                                                   : f2pack(ex2(x0), ex2(x1));
+                            // dS = P (dP - D); dP^T already holds dP - D (C-25)
+                            const uint64_t dsv =
+                                fmul2(pr, f2pack(__uint_as_float(d16[a]), __uint_as_float(d16[a + 1])));
+                            colsum2 = fadd2(colsum2, dsv);  // du^k, fp32 (C-4)
+                            float p0, p1;
+                            f2unpack(pr, p0, p1);
+                            f2unpack(dsv, ds[e2], ds[e2 + 1]);
+                            pk[e2 / 2] = pack_bf16x2(p0, p1);
+                            dk[e2 / 2] = pack_bf16x2(ds[e2], ds[e2 + 1]);
                         }
-                        const uint64_t pr = GFWA_BWD_EXPT == 3 ? fmul2(f2pack(x0, x1), sl2x2) : f2pack(ex2(x0), ex2(x1));
-                        // dS = P (dP - D); dP^T already holds dP - D (C-25)
-                        const uint64_t dsv = fmul2(pr, f2pack(__uint_as_float(d16[a]), __uint_as_float(d16[a + 1])));
-                        colsum2 = fadd2(colsum2, dsv);  // du^k, fp32 (C-4)
-                        float p0, p1;
-                        f2unpack(pr, p0, p1);
-                        f2unpack(dsv, ds[e2], ds[e2 + 1]);
-                        pk[e2 / 2] = pack_bf16x2(p0, p1);
-                        dk[e2 / 2] = pack_bf16x2(ds[e2], ds[e2 + 1]);
+                    }
+                };
+                if (GFWA_BWD_EXPT == 5) {
+#pragma unroll
+                    for (int e = 0; e < QPW; ++e) ds[e] = __uint_as_float(sall[e] ^ dall[e]);
+#pragma unroll
+                    for (int e = 0; e < QPW / 2; ++e) pk[e] = dk[e] = sall[e];
+                } else if (interior) {
+                    calc(std::false_type{});
+                } else {
+                    calc(std::true_type{});
+                }
+                // P^T -> columns [QPW wg, QPW wg + QPW/2), dS^T -> [QPW wg + QPW/2, QPW wg + QPW)
+                if constexpr (QPW == 32) {
+                    tmem_st16(lane_addr + 128 * bn + QPW * wg, *reinterpret_cast<const uint32_t(*)[16]>(pk));
+                    tmem_st16(lane_addr + 128 * bn + QPW * wg + QPW / 2, *reinterpret_cast<const uint32_t(*)[16]>(dk));
+                } else {
+                    tmem_st8(lane_addr + 128 * bn + QPW * wg, *reinterpret_cast<const uint32_t(*)[8]>(pk));
+                    tmem_st8(lane_addr + 128 * bn + QPW * wg + QPW / 2, *reinterpret_cast<const uint32_t(*)[8]>(dk));
+                }
+                {  // dS^T row -> smem (128B-swizzled MN-major: row = key, 16-B chunk of 8 queries ^ key%8)
+                    const uint32_t sb = smem_u32(dSs + bn * kDS) + kr * 128;
+#pragma unroll
+                    for (int c = 0; c < QPW / 8; ++c)
+                        sts128(sb + ((((QPW / 8) * wg + c) ^ (kr & 7)) * 16),
+                               make_uint4(dk[4 * c], dk[4 * c + 1], dk[4 * c + 2], dk[4 * c + 3]));
+                }
+                tmem_wait_st();
+                fence_proxy_async();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bars->ds_ready[bn]);
+                if (threadIdx.x == 0) BTR(6, g);
+                // du^q partial over this warp's 32 keys, off the MMA's critical path (the
+                // gradient contractions of step g are already running): butterfly
+                // transpose-reduce -> lane l holds query QPW wg + l; the drain warpgroup
+                // sums the 4 warps' partials and issues the red.add (C-11)
+#pragma unroll
+                for (int sft = QPW / 2; sft >= 1 && !GFWA_BWD_NODUQ && GFWA_BWD_EXPT != 5; sft >>= 1) {
+                    const bool up = lane & sft;
+#pragma unroll
+                    for (int e = 0; e < sft; ++e) {
+                        const float send = up ? ds[e] : ds[e + sft];
+                        const float keepv = up ? ds[e + sft] : ds[e];
+                        ds[e] = keepv + __shfl_xor_sync(0xffffffffu, send, sft);
                     }
                 }
-            };
-            if (GFWA_BWD_EXPT == 5) {
-#pragma unroll
-                for (int e = 0; e < QPW; ++e) ds[e] = __uint_as_float(sall[e] ^ dall[e]);
-#pragma unroll
-                for (int e = 0; e < QPW / 2; ++e) pk[e] = dk[e] = sall[e];
-            } else if (interior) {
-                calc(std::false_type{});
-            } else {
-                calc(std::true_type{});
+                if (g >= 2) mbar_wait(&bars->red_free[bn], ((g - 2) >> 1) & 1);
+                if (QPW < 32) ds[0] += __shfl_xor_sync(0xffffffffu, ds[0], QPW);  // lane halves hold the same query
+                if (lane < QPW) s_red[bn][wg][warp & 3][lane] = ds[0];
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bars->red_ready[bn]);
             }
-            if (threadIdx.x == 0) BTR(6, 3 * n + 1);
-            // P^T -> columns [QPW wg, QPW wg + QPW/2), dS^T -> [QPW wg + QPW/2, QPW wg + QPW)
-            if constexpr (QPW == 32) {
-                tmem_st16(lane_addr + 128 * bn + QPW * wg, *reinterpret_cast<const uint32_t(*)[16]>(pk));
-                tmem_st16(lane_addr + 128 * bn + QPW * wg + QPW / 2, *reinterpret_cast<const uint32_t(*)[16]>(dk));
-            } else {
-                tmem_st8(lane_addr + 128 * bn + QPW * wg, *reinterpret_cast<const uint32_t(*)[8]>(pk));
-                tmem_st8(lane_addr + 128 * bn + QPW * wg + QPW / 2, *reinterpret_cast<const uint32_t(*)[8]>(dk));
-            }
-            {  // dS^T row -> smem (128B-swizzled MN-major: row = key, 16-B chunk of 8 queries ^ key%8)
-                const uint32_t sb = smem_u32(dSs + bn * kDS) + kr * 128;
-#pragma unroll
-                for (int c = 0; c < QPW / 8; ++c)
-                    sts128(sb + ((((QPW / 8) * wg + c) ^ (kr & 7)) * 16),
-                           make_uint4(dk[4 * c], dk[4 * c + 1], dk[4 * c + 2], dk[4 * c + 3]));
-            }
-            tmem_wait_st();
-            fence_proxy_async();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&bars->ds_ready[bn]);
-            if (threadIdx.x == 0) BTR(0, 3 * n + 1);
-            // du^q partial over this warp's 32 keys, off the MMA's critical path (the
-            // gradient contractions of step n are already running): butterfly
-            // transpose-reduce -> lane l holds query 32 wg + l; the drain warpgroup
-            // sums the 4 warps' partials and issues the red.add (C-11)
-#pragma unroll
-            for (int sft = QPW / 2; sft >= 1 && !GFWA_BWD_NODUQ && GFWA_BWD_EXPT != 5; sft >>= 1) {
-                const bool up = lane & sft;
-#pragma unroll
-                for (int e = 0; e < sft; ++e) {
-                    const float send = up ? ds[e] : ds[e + sft];
-                    const float keepv = up ? ds[e + sft] : ds[e];
-                    ds[e] = keepv + __shfl_xor_sync(0xffffffffu, send, sft);
-                }
-            }
-            if (threadIdx.x == 0) BTR(6, 3 * n + 2);
-            if (n >= 2) mbar_wait(&bars->red_free[bn], ((n - 2) >> 1) & 1);
-            if (QPW < 32) ds[0] += __shfl_xor_sync(0xffffffffu, ds[0], QPW);  // lane halves hold the same query
-            if (lane < QPW) s_red[bn][wg][warp & 3][lane] = ds[0];
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&bars->red_ready[bn]);
-            if (threadIdx.x == 0) BTR(0, 3 * n + 2);
-        }
-        {
             float c0, c1;
             f2unpack(colsum2, c0, c1);
-            if (kvalid && nsteps > 0) red_add(p.dU + (b * p.H + h) * p.Nkv + j, -(c0 + c1));  // du^k (C-4)
-        }
-        // epilogue: WG0 -> dV, WG1 -> dK (scale, C-3), via smem + TMA store
-        if (wg >= 2) goto done;
-        {
-        uint8_t* stg = Qs + wg * 2 * kQT;  // the Q/dO stages are idle once dkdv_full fires
-        const uint32_t sg = smem_u32(stg);
-        const uint32_t acol = wg == 0 ? 256 : 384;
-        const float mul = wg == 0 ? 1.f : p.scale;
-        if (nsteps > 0) {
-            mbar_wait(&bars->dkdv_full, 0);
-            if (threadIdx.x == 0) BTR(4, 0);
-            tc_fence_after();
-        }
-        // two halves of 64 columns: both TMEM loads of a half in flight before one
-        // wait, each half's TMA store issued as soon as it is staged
-#pragma unroll 1
-        for (int hf = 0; hf < kHalves; ++hf) {
-            uint32_t v2[2][32];
-            if (nsteps > 0) {
-                tmem_ld32(lane_addr + acol + 64 * hf, v2[0]);
-                tmem_ld32(lane_addr + acol + 64 * hf + 32, v2[1]);
-                tmem_wait_ld();
-            } else {
-#pragma unroll
-                for (int e = 0; e < 32; ++e) v2[0][e] = v2[1][e] = 0u;
-            }
-#pragma unroll
-            for (int cc = 0; cc < 2; ++cc) {
-                const uint32_t* v = v2[cc];
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const int chunk = (cc * 4 + k) ^ (kr & 7);
-                    uint4 pkv;
-                    pkv.x = pack_bf16x2(__uint_as_float(v[8 * k + 0]) * mul, __uint_as_float(v[8 * k + 1]) * mul);
-                    pkv.y = pack_bf16x2(__uint_as_float(v[8 * k + 2]) * mul, __uint_as_float(v[8 * k + 3]) * mul);
-                    pkv.z = pack_bf16x2(__uint_as_float(v[8 * k + 4]) * mul, __uint_as_float(v[8 * k + 5]) * mul);
-                    pkv.w = pack_bf16x2(__uint_as_float(v[8 * k + 6]) * mul, __uint_as_float(v[8 * k + 7]) * mul);
-                    sts128(sg + hf * kKVbox + kr * 128 + chunk * 16, pkv);
-                }
-            }
-            fence_proxy_async();
-            named_bar_sync(1 + wg, 128);
-            if (kr == 0) {
-                tma_store_4d(wg == 0 ? &mdv : &mdk, stg + hf * kKVbox, hf * 64, (int)h, (int)j0, (int)b);
-                bulk_commit();
-            }
-        }
-        if (kr == 0) bulk_wait_read0();
-        if (threadIdx.x == 0) BTR(4, 1);
+            if (kvalid) red_add(p.dU + ((int64_t)it.b * p.H + it.h) * p.Nkv + j, -(c0 + c1));  // du^k (C-4)
         }
     } else if (warp < kMmaWarp) {
-        // ------------------------------------------------ dQ drain: thread = head-dim lane
+        // ------------------------------------------------ dQ drain + dK/dV epilogue: thread = TMEM lane
         // dQ^T (TMEM, lane = d) -> smem [16 queries][32 d] fp32 boxes (128B swizzle) ->
         // TMA bulk reduce-add into the fp32 dQ accumulator: the L2 does the adds, no
         // per-thread atomics.  Each drain warp stages its own 32 d (double-buffered
-        // 2 KB boxes) and issues its own reduces, so no cross-warp barrier.
+        // 2 KB boxes) and issues its own reduces, so no cross-warp barrier.  After an
+        // item's last step the same threads (now lane = key) move dV, dK out of TMEM
+        // (releasing it for the next item's first gradient MMAs) and store them.
         const int dl = threadIdx.x - 32 * kDrainWarp0;  // 0..127
         const uint32_t lane_addr = tmem + ((uint32_t)((warp & 3) * 32) << 16);
         const uint32_t qcol[4] = {64, 80, 96, 112};  // dQ^T: columns [64,128) of the buffer
         uint8_t* wbox = dQs + (warp & 3) * 2 * kDQW;
         // du^q_t += rowsum(dS) at key position t + h0 (C-11): the 4 per-warp
         // partials of each softmax-grad warpgroup (threads dl < 64, one query each)
-        auto combine_duq = [&](int mm) {
+        auto combine_duq = [&](int mm, int64_t t0, int64_t bh) {
             if (dl < BMQ) {
                 const int bq = mm & 1;
                 mbar_wait(&bars->red_ready[bq], (mm >> 1) & 1);
@@ -551,55 +589,156 @@ __global__ void __launch_bounds__(kThreads, 1)
                     s_red[bq][wq][0][lq] + s_red[bq][wq][1][lq] + s_red[bq][wq][2][lq] + s_red[bq][wq][3][lq];
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bars->red_free[bq]);
-                const int64_t t = (qt_lo + mm) * BMQ + dl;
-                if (t < p.Nq) red_add(p.dU + (b * p.H + h) * p.Nkv + t + p.h0, rs);
+                const int64_t t = t0 + dl;
+                if (t < p.Nq) red_add(p.dU + bh * p.Nkv + t + p.h0, rs);
             }
         };
-        for (int m = 0; m < nsteps; ++m) {
-            const int bm = m & 1;
-            const int64_t t0 = (qt_lo + m) * BMQ;
-            mbar_wait(&bars->dq_full[bm], (m >> 1) & 1);
-            if (dl == 0) BTR(2, 2 * m);
-            tc_fence_after();
-            const bool dlive = 32 * (warp & 3) < D;  // D = 64: dQ^T lanes 64..127 are the zero padding
-            uint32_t v[4][16];
-            if (dlive) {
+        // dV (mul 1) and dK (mul scale, C-3) rows of key j -> global, bf16
+        auto store_row = [&](__nv_bfloat16* base, const uint32_t (&v)[32], int c0, float mul) {
+            uint4* dst = reinterpret_cast<uint4*>(base + c0);
 #pragma unroll
-                for (int qq = 0; qq < 4; ++qq) tmem_ld16(lane_addr + 128 * bm + qcol[qq], v[qq]);
-                tmem_wait_ld();
+            for (int k = 0; k < 4; ++k) {
+                uint4 o;
+                o.x = pack_bf16x2(__uint_as_float(v[8 * k + 0]) * mul, __uint_as_float(v[8 * k + 1]) * mul);
+                o.y = pack_bf16x2(__uint_as_float(v[8 * k + 2]) * mul, __uint_as_float(v[8 * k + 3]) * mul);
+                o.z = pack_bf16x2(__uint_as_float(v[8 * k + 4]) * mul, __uint_as_float(v[8 * k + 5]) * mul);
+                o.w = pack_bf16x2(__uint_as_float(v[8 * k + 6]) * mul, __uint_as_float(v[8 * k + 7]) * mul);
+                dst[k] = o;
             }
-            // all 64 queries are in registers: release the TMEM buffer first
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&bars->dq_drained[bm]);
-            if (dl == 0) BTR(2, 2 * m + 1);
-            if (m > 0) combine_duq(m - 1);  // the previous step's partials are in smem by now
-            // four rounds of 16 queries; row = query (128 B = this warp's 32 d),
-            // 16-B chunk (d%32)/4 ^ (query%8), word d%4
+        };
+        Pool pool;  // replica of the slot rotation (the epilogue stages in the item's K slot)
+        int g = 0, nitem = 0, pg = -1;
+        int64_t pt0 = 0, pbh = 0;
+        for (int idx = blockIdx.x; idx < p.n_items; idx += gridDim.x) {
+            const BItem it = make_bitem(p, idx);
+            const int64_t j = (int64_t)it.j0 + dl;
+            __nv_bfloat16* dvrow = p.dV + (int64_t)it.b * p.vs[0] + j * p.vs[1] + (int64_t)it.h * p.vs[2];
+            __nv_bfloat16* dkrow = p.dK + (int64_t)it.b * p.ks[0] + j * p.ks[1] + (int64_t)it.h * p.ks[2];
+            if (it.nsteps == 0) {  // no query reaches these keys: dK = dV = 0
+                if (j < p.Nkv) {
+                    uint32_t z[32];
 #pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                if (!dlive) break;
-                if (lane == 0) bulk_wait_read1();  // the reduce two rounds back has read this box
+                    for (int e = 0; e < 32; ++e) z[e] = 0u;
+#pragma unroll
+                    for (int c = 0; c < D; c += 32) {
+                        store_row(dvrow, z, c, 1.f);
+                        store_row(dkrow, z, c, 1.f);
+                    }
+                }
+                continue;
+            }
+            const int64_t bh = (int64_t)it.b * p.H + it.h;
+            for (int m = 0; m < it.nsteps; ++m, ++g) {
+                const int bm = g & 1;
+                const int64_t t0 = (int64_t)(it.qt_lo + m) * BMQ;
+                mbar_wait(&bars->dq_full[bm], (g >> 1) & 1);
+                if (dl == 0) BTR(2, g);
+                tc_fence_after();
+                const bool dlive = 32 * (warp & 3) < D;  // D = 64: dQ^T lanes 64..127 are the zero padding
+                uint32_t v[4][16];
+                if (dlive) {
+#pragma unroll
+                    for (int qq = 0; qq < 4; ++qq) tmem_ld16(lane_addr + 128 * bm + qcol[qq], v[qq]);
+                    tmem_wait_ld();
+                }
+                // all 64 queries are in registers: release the TMEM buffer first
+                tc_fence_before();
                 __syncwarp();
-                const uint32_t sq = smem_u32(wbox + (r & 1) * kDQW);
+                if (lane == 0) mbar_arrive(&bars->dq_drained[bm]);
+                if (dl == 0) BTR(7, g);
+                if (pg >= 0) combine_duq(pg, pt0, pbh);  // the previous step's partials are in smem by now
+                if (GFWA_BWD_DQRED) {
+                    // per query one coalesced 128-byte L2 reduction (lane = d): no staging
+                    if (dlive && !GFWA_BWD_NODQ) {
+                        float* acc = p.dQacc + (((int64_t)it.b * p.Nq + t0) * p.H + it.h) * D + 32 * (warp & 3) + lane;
+                        const int64_t qstride = p.H * D;
+                        const int nq = (int)min64(BMQ, p.Nq - t0);
 #pragma unroll
-                for (int e = 0; e < 16; ++e)
-                    sts32(sq + e * 128 + ((((lane >> 2) ^ e) & 7) << 4) + (lane & 3) * 4, __uint_as_float(v[r][e]));
+                        for (int r = 0; r < 4; ++r)
+#pragma unroll
+                            for (int e = 0; e < 16; ++e)
+                                if (16 * r + e < nq) red_add(acc + (16 * r + e) * qstride, __uint_as_float(v[r][e]));
+                    }
+                } else {
+                    // four rounds of 16 queries; row = query (128 B = this warp's 32 d),
+                    // 16-B chunk (d%32)/4 ^ (query%8), word d%4
+    #pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        if (!dlive) break;
+                        if (lane == 0) bulk_wait_read1();  // the reduce two rounds back has read this box
+                        __syncwarp();
+                        const uint32_t sq = smem_u32(wbox + (r & 1) * kDQW);
+    #pragma unroll
+                        for (int e = 0; e < 16; ++e)
+                            sts32(sq + e * 128 + ((((lane >> 2) ^ e) & 7) << 4) + (lane & 3) * 4, __uint_as_float(v[r][e]));
+                        fence_proxy_async();
+                        __syncwarp();
+                        if (lane == 0 && !GFWA_BWD_NODQ) {
+                            tma_reduce_add_4d(&mdq, wbox + (r & 1) * kDQW, 32 * (warp & 3), it.h, (int)(t0 + 16 * r),
+                                              it.b);
+                            bulk_commit();
+                        }
+                    }
+                }
+                pg = g;
+                pt0 = t0;
+                pbh = bh;
+            }
+            // epilogue of the item: dV, dK (TMEM lane = key) -> bf16, staged in the item's K
+            // slot (its last reader, dQ^T, has completed: dkdv_full) and written by TMA
+            // stores of [32 keys][64 d] boxes; the slot is released once they have read it
+            mbar_wait(&bars->dkdv_full, nitem & 1);
+            if (dl == 0) BTR(4, nitem);
+            tc_fence_after();
+            const uint32_t stg_off = pool.K() * kSlot + (warp & 3) * 8192;  // this warp's 8 KB
+            const uint32_t stg = smem_u32(pool_base) + stg_off;
+#pragma unroll 1
+            for (int tsr = 0; tsr < 2; ++tsr) {  // 0: dV (TMEM [256, 384)), 1: dK ([384, 512), times scale)
+                const float mul = tsr ? p.scale : 1.f;
+#pragma unroll 1
+                for (int hf = 0; hf < kHalves; ++hf) {
+                    uint32_t a[32], b[32];
+                    tmem_ld32(lane_addr + 256 + 128 * tsr + 64 * hf, a);
+                    tmem_ld32(lane_addr + 256 + 128 * tsr + 64 * hf + 32, b);
+                    tmem_wait_ld();
+                    if (tsr == 1 && hf == kHalves - 1) {  // every dV, dK column has been read: TMEM free
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&bars->dkdv_free);
+                    }
+                    const uint32_t row = stg + hf * 4096 + lane * 128;  // 128B swizzle: chunk ^ (key % 8)
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        const uint32_t* v = k < 4 ? a + 8 * k : b + 8 * (k - 4);
+                        uint4 o;
+                        o.x = pack_bf16x2(__uint_as_float(v[0]) * mul, __uint_as_float(v[1]) * mul);
+                        o.y = pack_bf16x2(__uint_as_float(v[2]) * mul, __uint_as_float(v[3]) * mul);
+                        o.z = pack_bf16x2(__uint_as_float(v[4]) * mul, __uint_as_float(v[5]) * mul);
+                        o.w = pack_bf16x2(__uint_as_float(v[6]) * mul, __uint_as_float(v[7]) * mul);
+                        sts128(row + ((k ^ (lane & 7)) << 4), o);
+                    }
+                }
                 fence_proxy_async();
                 __syncwarp();
-                if (lane == 0 && !GFWA_BWD_NODQ) {
-                    tma_reduce_add_4d(&mdq, wbox + (r & 1) * kDQW, 32 * (warp & 3), (int)h, (int)(t0 + 16 * r), (int)b);
+                if (lane == 0) {
+                    for (int hf = 0; hf < kHalves; ++hf)
+                        tma_store_4d(tsr ? &mdk : &mdv, pool_base + stg_off + hf * 4096, hf * 64, it.h,
+                                     it.j0 + 32 * (warp & 3), it.b);
                     bulk_commit();
+                    bulk_wait_read0();  // the staging is reusable / releasable once the stores have read it
                 }
+                __syncwarp();
             }
+            named_bar_sync(1, 128);  // all four drain warps' stores have read the slot
+            if (dl == 0) mbar_arrive(&bars->empty[pool.K()]);
+            pool.advance(it.nsteps);
+            ++nitem;
         }
-        if (nsteps > 0) combine_duq(nsteps - 1);
+        if (pg >= 0) combine_duq(pg, pt0, pbh);
         if (lane == 0) bulk_wait0();  // reductions complete before the CTA exits
     }
-done:
     tc_fence_before();
     __syncthreads();
-    if (threadIdx.x == 0) BTR(5, 1);
     if (warp == kMmaWarp) {
         tc_fence_after();
         tmem_dealloc(tmem, 512);
@@ -608,8 +747,7 @@ done:
 
 template <int D>
 constexpr size_t smem_bytes() {
-    return 1024 + BwdLay<D>::kKslot + BwdLay<D>::kV + NQS * 2 * BwdLay<D>::kQT + 2 * kDS + kDQ + kAugA + kAugB +
-           sizeof(Bars) + 16;
+    return 1024 + kPool * kSlot + 2 * kDS + kDQ + kAugA + kAugB + sizeof(Bars) + 16;
 }
 
 // dQacc zeroing fused with D = rowsum(O dO)  (Alg. E.2 l.7; O + O_lo, C-12)
@@ -742,8 +880,8 @@ static gfwa_status_t tc_bwd_d(const AttnParams& pin, cudaStream_t st, void* ws) 
     GFWA_REQUIRE(encode_bnhd_map(&mk, p.K, p.B, p.Nkv, p.H, D, p.ks, BN));
     GFWA_REQUIRE(encode_bnhd_map(&mv, p.V, p.B, p.Nkv, p.H, D, p.vs, BN));
     GFWA_REQUIRE(encode_bnhd_map(&mdo, p.dO, p.B, p.Nq, p.H, D, p.os, BMQ));
-    GFWA_REQUIRE(encode_bnhd_map(&mdk, p.dK, p.B, p.Nkv, p.H, D, p.ks, BN));
-    GFWA_REQUIRE(encode_bnhd_map(&mdv, p.dV, p.B, p.Nkv, p.H, D, p.vs, BN));
+    GFWA_REQUIRE(encode_bnhd_map(&mdk, p.dK, p.B, p.Nkv, p.H, D, p.ks, BN / 4));  // [32 keys][64 d] store boxes
+    GFWA_REQUIRE(encode_bnhd_map(&mdv, p.dV, p.B, p.Nkv, p.H, D, p.vs, BN / 4));
     const int64_t acc_s[3] = {p.Nq * p.H * D, p.H * D, D};  // dQacc [B, Nq, H, d] fp32
     GFWA_REQUIRE(encode_bnhd_map_f32(&mdq, p.dQacc, p.B, p.Nq, p.H, D, acc_s, 16));
     const int64_t rows = p.B * p.Nq * p.H;
@@ -779,12 +917,24 @@ static gfwa_status_t tc_bwd_d(const AttnParams& pin, cudaStream_t st, void* ws) 
     tp.scale = p.scale;
     tp.inv_scale = 1.f / p.scale;
     tp.token = p.token;
+    tp.dK = (__nv_bfloat16*)p.dK;
+    tp.dV = (__nv_bfloat16*)p.dV;
+    for (int i = 0; i < 3; ++i) {
+        tp.ks[i] = p.ks[i];
+        tp.vs[i] = p.vs[i];
+    }
+    tp.n_kt = (int)((p.Nkv + BN - 1) / BN);
+    const int64_t n_items = (int64_t)tp.n_kt * p.H * p.B;
+    if (n_items >= ((int64_t)1 << 31)) return GFWA_ERR_INVALID_ARGUMENT;
+    tp.n_items = (int)n_items;
     // per launch: the attribute is per device (a process may drive several GPUs)
     constexpr size_t kSmemBytes = smem_bytes<D>();
     if (gfwa_status_t s = check_launch(
             cudaFuncSetAttribute(bwd_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes)))
         return s;
-    dim3 grid((unsigned)((p.Nkv + BN - 1) / BN), (unsigned)p.H, (unsigned)p.B);
+    int64_t cap = n_sm;  // persistent: one CTA per SM
+    if (const char* e = getenv("GFWA_BWD_GRID")) cap = max64(1, atoll(e));  // diagnostics: fewer CTAs, more items each
+    const unsigned grid = (unsigned)min64(n_items, cap);
     bwd_tc_kernel<D><<<grid, kThreads, kSmemBytes, st>>>(mq, mk, mv, mdo, mdk, mdv, mdq, tp);
     note_launch();
     if (gfwa_status_t s = check_launch()) return s;
