@@ -104,10 +104,10 @@ struct TcBwdParams {
 #endif
 #if GFWA_BWD_TRACE
 constexpr int kBTr = 512;  // stamps per (CTA, role), first 148 CTAs
-__device__ long long g_bwd_trace[148 * 8 * kBTr];
+__device__ long long g_bwd_trace[148 * 12 * kBTr];
 #define BTR(role, k)                                                                        \
     do {                                                                                    \
-        if ((k) < kBTr && blockIdx.x < 148) g_bwd_trace[(blockIdx.x * 8 + (role)) * kBTr + (k)] = clock64(); \
+        if ((k) < kBTr && blockIdx.x < 148) g_bwd_trace[(blockIdx.x * 12 + (role)) * kBTr + (k)] = clock64(); \
     } while (0)
 #else
 #define BTR(role, k) \
@@ -146,17 +146,6 @@ struct __align__(8) Bars {
 
 __device__ __forceinline__ void red_add(float* addr, float a) {
     asm volatile("red.global.add.f32 [%0], %1;" ::"l"(addr), "f"(a) : "memory");
-}
-
-// x = hi + mid + lo to ~24 bits, each a bf16 (bit patterns in the low 16 bits)
-__device__ __forceinline__ void split3_bf16(float x, uint32_t& h, uint32_t& m, uint32_t& l) {
-    const __nv_bfloat16 bh = __float2bfloat16_rn(x);
-    const float r1 = x - __bfloat162float(bh);
-    const __nv_bfloat16 bm = __float2bfloat16_rn(r1);
-    const __nv_bfloat16 bl = __float2bfloat16_rn(r1 - __bfloat162float(bm));
-    h = __bfloat16_as_ushort(bh);
-    m = __bfloat16_as_ushort(bm);
-    l = __bfloat16_as_ushort(bl);
 }
 
 __device__ __forceinline__ uint32_t range_bits(int lo, int hi, int base) {
@@ -453,6 +442,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int64_t t0 = (int64_t)(it.qt_lo + m) * BMQ;
                 mbar_wait(&bars->st_full[bn], (g >> 1) & 1);
                 if (threadIdx.x == 0) BTR(0, g);
+                if (threadIdx.x == 128) BTR(9, g);
                 tc_fence_after();
                 const uint32_t scol = 128 * bn + QPW * wg;  // this WG's S^T columns (dP^T at +64)
                 // keys in (g - w, g] of each query g = t + h0, as a column range
@@ -542,6 +532,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bars->ds_ready[bn]);
                 if (threadIdx.x == 0) BTR(6, g);
+                if (threadIdx.x == 128) BTR(8, g);
+                if (threadIdx.x == 96) BTR(10, g);
+                if (threadIdx.x == 224) BTR(11, g);
                 // du^q partial over this warp's 32 keys, off the MMA's critical path (the
                 // gradient contractions of step g are already running): butterfly
                 // transpose-reduce -> lane l holds query QPW wg + l; the drain warpgroup

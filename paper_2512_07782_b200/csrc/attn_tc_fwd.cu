@@ -76,10 +76,13 @@ struct Lay {
     static constexpr uint32_t kOffQ = 0;                    // Q_A, Q_B
     static constexpr uint32_t kOffKV = 2 * kTile;           // one K/V ring of 3 tile slots: K_0 V_0 K_1 V_1 ...
     static constexpr uint32_t kOffE = 5 * kTile;            // 32 KB: a 64-column box of O, then of O_lo
-    static constexpr uint32_t kOffNbk = kOffE + 2 * kBox;   // [2 tiles][128] fp32 key biases
-    static constexpr uint32_t kOffLinv = kOffNbk + 2 * BN * 4;  // [2 tiles][128] 1/l
-    static constexpr uint32_t kOffXch = kOffLinv + 2 * BM * 4;  // [2 tiles][2 halves][128] row-max exchange
-    static constexpr uint32_t kOffXchL = kOffXch + 4 * BM * 4;  // [2 tiles][128] half 1's row sum
+    // gate-bias slabs (reading C-26): B side one 128-key x 128 B swizzle region whose 32-B
+    // column s holds ring slot s's per-key slab; A side one 1 KB atom of identical rows
+    static constexpr uint32_t kOffSlabK = kOffE + 2 * kBox;  // 16 KB
+    static constexpr uint32_t kOffSlabA = kOffSlabK + BN * 128;  // 1 KB
+    static constexpr uint32_t kOffLinv = kOffSlabA + 1024;    // [2 tiles][128] 1/l
+    static constexpr uint32_t kOffXch = kOffLinv + 2 * BM * 4;  // [2 tiles][2 parities][2 halves][128] row maxes
+    static constexpr uint32_t kOffXchL = kOffXch + 8 * BM * 4;  // [2 tiles][128] half 1's row sum
     static constexpr uint32_t kOffBars = kOffXchL + 2 * BM * 4;
     static constexpr size_t kSmemBytes = kOffBars + 256;
 };
@@ -106,6 +109,7 @@ struct TcFwdParams {
     unsigned long long* token;
     unsigned long long token_val;
     float sl2;  // scale * log2(e)
+    float inv_scale;
 };
 
 #if GFWA_FWD_TRACE
@@ -184,7 +188,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     extern __shared__ __align__(1024) uint8_t smem[];
     using L = Lay<D>;
     constexpr uint32_t kTile = L::kTile, kOffQ = L::kOffQ, kOffKV = L::kOffKV, kOffE = L::kOffE,
-                       kOffNbk = L::kOffNbk, kOffLinv = L::kOffLinv;
+ kOffLinv = L::kOffLinv;
     constexpr int kHalves = D / 64;  // 64-column TMA boxes per tile row
     Bars* bars = (Bars*)(smem + L::kOffBars);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -201,12 +205,22 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&bars->l_free[i], 4);  // the epilogue warps have read 1/l
         }
         for (int i = 0; i < kSlots; ++i) {
-            mbar_init(&bars->k_full[i], 1);
+            mbar_init(&bars->k_full[i], 2);  // TMA bytes + the producer's bias slab
             mbar_init(&bars->v_full[i], 1);
             mbar_init(&bars->kv_empty[i], 1);
             mbar_init(&bars->v_ready[i], 2);  // the two convert warps
         }
         fence_barrier_init();
+    }
+    {  // bias slabs: B region zero (k 8..15 of every slab stay zero), A atom = ones at k 0..2
+        for (uint32_t i = threadIdx.x; i < BN * 128 / 16; i += kThreads)
+            sts128(smem_u32(smem + L::kOffSlabK) + i * 16, make_uint4(0u, 0u, 0u, 0u));
+        if (threadIdx.x < 64) {  // row r = tid / 8, physical 16-B chunk c = tid % 8
+            const uint32_t r = threadIdx.x >> 3, c = threadIdx.x & 7, one = 0x3F80u;
+            sts128(smem_u32(smem + L::kOffSlabA) + r * 128 + c * 16,
+                   (c ^ r) == 0 ? make_uint4(one | (one << 16), one, 0u, 0u) : make_uint4(0u, 0u, 0u, 0u));
+        }
+        fence_proxy_async();
     }
     if (warp == kMmaWarp) {
         tmem_alloc(&bars->tmem, 512);
@@ -231,6 +245,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int idx = blockIdx.x; idx < p.n_items; idx += gridDim.x) {
             const Item it = make_item(p, idx);
             bool q_loaded[2] = {false, false};
+            const float* Ubh = p.U + ((int64_t)it.b * p.H + it.h) * p.Nkv;
+            const float uref = Ubh[it.glo0];  // the item's bias reference (reading C-18)
             for (int n = 0; n < it.nsteps; ++n) {
                 const int j = it.jtop - n;
 #pragma unroll
@@ -260,6 +276,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                         for (int half = 0; half < kHalves; ++half)
                             tma_load_4d_hint(smem + kOffKV + sl * kTile + half * kBox, kv ? &mv : &mk, full,
                                              half * 64, it.h, j * BN, it.b, pol_kv);
+                    }
+                    if (kv == 0) {
+                        // K_j's slab: b = (uref - u_k) / scale per key as hi + mid + lo bf16, so the
+                        // S MMA yields q.k + b and sl2 (q.k + b) = scale log2e q.k - (u_k - uref) log2e
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            const int r = lane + 32 * i, key = j * BN + r;
+                            const float bk = key < (int)p.Nkv ? (uref - Ubh[key]) * p.inv_scale : 0.f;
+                            uint32_t bh, bm, bl;
+                            split3_bf16(bk, bh, bm, bl);
+                            sts128(smem_u32(smem + L::kOffSlabK) + r * 128 + (((2 * sl) ^ (r & 7)) << 4),
+                                   make_uint4(bh | (bm << 16), bl, 0u, 0u));
+                        }
+                        fence_proxy_async();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&bars->k_full[sl]);
                     }
                     __syncwarp();
                 }
@@ -330,6 +362,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 mma_ss(tmem + 128 * x, sdesc_sw128(qb + off, 16, 1024),
                                        sdesc_sw128(kb + off, 16, 1024), idesc_qk, kk > 0 ? 1u : 0u);
                             }
+                            // + the per-key gate bias (C-26): ones (A, rows repeat: SBO = 0) x slab
+                            mma_ss(tmem + 128 * x, sdesc_sw128(smem_u32(smem + L::kOffSlabA), 16, 0),
+                                   sdesc_sw128(smem_u32(smem + L::kOffSlabK) + 32 * sk, 16, 1024), idesc_qk, 1u);
                             tc_commit(&bars->s_full[x]);
                             if (j == it.jlo(x)) tc_commit(&bars->q_empty[x]);
                         }
@@ -385,10 +420,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int r = threadIdx.x & 127;
         const uint32_t lane_addr = tmem + ((uint32_t)((warp & 3) * 32) << 16);
         const uint32_t s_col = 128 * x + 64 * hh, o_col = 256 + 128 * x + (D / 2) * hh;
-        float* nbk = reinterpret_cast<float*>(smem + kOffNbk) + x * BN + 64 * hh;  // this half's 64 keys
         float* linv = reinterpret_cast<float*>(smem + kOffLinv) + x * BM;
-        float* xch = reinterpret_cast<float*>(smem + L::kOffXch) + x * 2 * BM;    // [half][row]
-        const uint32_t bar_half = 1 + 2 * x + hh, bar_tile = 5 + x;             // named barrier ids
+        float* xch = reinterpret_cast<float*>(smem + L::kOffXch) + x * 4 * BM;    // [parity][half][row]
+        const uint32_t bar_tile = 5 + x;  // named barrier id of the tile's two softmax warpgroups
         const uint64_t sl2x2 = f2pack(p.sl2, p.sl2);
         uint32_t cs = 0, nit = 0;
         for (int idx = blockIdx.x; idx < p.n_items; idx += gridDim.x) {
@@ -405,15 +439,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const float uref = Ubh[it.glo0];
             const float bq = valid ? (Ubh[g] - uref) * kLog2e : 0.f;
             float m_used = -INFINITY, l = 0.f;  // l: this half's partial row sum
-            const int kr = 64 * hh + (r & 63);    // key of this thread's nbk entry (threads r < 64)
-            float u_next = (r < 64 && jt * BN + kr < Nkv) ? Ubh[jt * BN + kr] : 0.f;
             for (int j = jt; j >= jlo_x; --j, ++cs) {
-                // -(u_k - uref) log2e of this half's 64 keys -> smem (after every thread
-                // of the half finished the previous tile); the next tile's u is prefetched
-                named_bar_sync(bar_half, 128);
-                if (r < 64) nbk[r] = (uref - u_next) * kLog2e;
-                if (r < 64 && j > jlo_x) u_next = (j - 1) * BN + kr < Nkv ? Ubh[(j - 1) * BN + kr] : 0.f;
-                named_bar_sync(bar_half, 128);
                 if (r == 0) FTR(x, 3 * (int)cs);
                 mbar_wait_park(&bars->s_full[x], cs & 1);
                 if (r == 0) FTR(x, 3 * (int)cs + 1);
@@ -432,11 +458,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                         live[c] = __any_sync(0xffffffffu, keep[c] != 0u);
                     }
                 }
-                // pass 1: logits x = scale*q.k - (u_k - uref) log2e (Alg. 2 l.12-15, masked to
-                // -inf outside the window), the half-row max, x written back over S
+                // pass 1: the half-row max of S' = q.k - (u_k - uref) / scale (the gate bias is
+                // already in the accumulator, C-26; masked to -inf outside the window, Alg. 2
+                // l.12-15); x = sl2 S' is monotone in S', so the max is taken on S'
                 float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-                for (int cb = 0; cb < 2; ++cb) {  // 32 columns in registers at a time
+                for (int cb = 0; cb < 2; ++cb) {
                     if (!(cb ? live[1] : live[0])) continue;  // masked for the whole warp: pass 2 skips it too
                     uint32_t raw[32];
                     tmem_ld32(lane_addr + s_col + 32 * cb, raw);
@@ -444,14 +471,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint32_t kw = cb ? keep[1] : keep[0];
 #pragma unroll
                     for (int e = 0; e < 32; e += 4) {
-                        const float4 nbv = *reinterpret_cast<const float4*>(nbk + 32 * cb + e);
-                        const uint64_t x01 = ffma2(f2pack(__uint_as_float(raw[e]), __uint_as_float(raw[e + 1])),
-                                                   sl2x2, f2pack(nbv.x, nbv.y));
-                        const uint64_t x23 = ffma2(f2pack(__uint_as_float(raw[e + 2]), __uint_as_float(raw[e + 3])),
-                                                   sl2x2, f2pack(nbv.z, nbv.w));
-                        float a0, a1, a2, a3;
-                        f2unpack(x01, a0, a1);
-                        f2unpack(x23, a2, a3);
+                        float a0 = __uint_as_float(raw[e]), a1 = __uint_as_float(raw[e + 1]);
+                        float a2 = __uint_as_float(raw[e + 2]), a3 = __uint_as_float(raw[e + 3]);
                         if (!interior) {
                             a0 = ((kw >> e) & 1u) ? a0 : -INFINITY;
                             a1 = ((kw >> (e + 1)) & 1u) ? a1 : -INFINITY;
@@ -459,17 +480,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                             a3 = ((kw >> (e + 3)) & 1u) ? a3 : -INFINITY;
                         }
                         mx[(e >> 2) & 3] = fmax3(mx[(e >> 2) & 3], fmaxf(a0, a1), fmaxf(a2, a3));
-                        raw[e] = __float_as_uint(a0);
-                        raw[e + 1] = __float_as_uint(a1);
-                        raw[e + 2] = __float_as_uint(a2);
-                        raw[e + 3] = __float_as_uint(a3);
                     }
-                    tmem_st32(lane_addr + s_col + 32 * cb, raw);
                 }
-                // the row max over both halves (exchange through smem)
-                xch[hh * BM + r] = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+                // the row max over both halves (exchange through smem), in log2 units
+                // (double-buffered by key-tile parity: a half may run one tile ahead of the other)
+                float* xc = xch + (cs & 1) * 2 * BM;
+                xc[hh * BM + r] = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
                 named_bar_sync(bar_tile, 256);
-                const float mt = fmaxf(xch[r], xch[BM + r]);
+                const float mraw = fmaxf(xc[r], xc[BM + r]);
+                const float mt = mraw == -INFINITY ? -INFINITY : mraw * p.sl2;
                 // lazy online softmax: move the reference max only when it grows by > 2^8
                 // (both halves take the same decision from the same values)
                 float corr = 1.f;
@@ -485,10 +504,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const float mref = (m_used == -INFINITY) ? 0.f : m_used;
                 const uint64_t nm2 = f2pack(-mref, -mref);
                 float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-                tmem_wait_st();  // pass 1's x is in TMEM
-                // pass 2: exponentials, the half-row sum, 16-bit P of the half's 64 keys
-                // into its own first 32 S columns (chunk cb's P lands on columns that
-                // chunk cb's x already left: [16 cb, 16 cb + 16) <= [32 cb, 32 cb + 32))
+                // pass 2: exponentials 2^(sl2 S' - m), the half-row sum, 16-bit P of the half's 64
+                // keys into its own first 32 S columns (chunk cb's P lands on columns that
+                // chunk cb's S' already left: [16 cb, 16 cb + 16) <= [32 cb, 32 cb + 32))
 #pragma unroll
                 for (int cb = 0; cb < 2; ++cb) {
                     uint32_t pk[16];
@@ -496,15 +514,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                         uint32_t xr[32];
                         tmem_ld32(lane_addr + s_col + 32 * cb, xr);
                         tmem_wait_ld();
+                        const uint32_t kw = cb ? keep[1] : keep[0];
 #pragma unroll
                         for (int e = 0; e < 16; ++e) {
-                            const uint64_t d = fadd2(f2pack(__uint_as_float(xr[2 * e]), __uint_as_float(xr[2 * e + 1])), nm2);
-                            float p0, p1;
+                            const uint64_t d = ffma2(f2pack(__uint_as_float(xr[2 * e]), __uint_as_float(xr[2 * e + 1])),
+                                                     sl2x2, nm2);
+                            float d0, d1, p0, p1;
+                            f2unpack(d, d0, d1);
+                            if (!interior) {
+                                d0 = ((kw >> (2 * e)) & 1u) ? d0 : -INFINITY;
+                                d1 = ((kw >> (2 * e + 1)) & 1u) ? d1 : -INFINITY;
+                            }
                             if ((e & 3) < kPolyPairs) {
-                                f2unpack(exp2_poly2(d), p0, p1);
+                                f2unpack(exp2_poly2(f2pack(d0, d1)), p0, p1);
                             } else {
-                                float d0, d1;
-                                f2unpack(d, d0, d1);
                                 p0 = ex2(d0);
                                 p1 = ex2(d1);
                             }
@@ -697,6 +720,7 @@ static gfwa_status_t tc_fwd_d(const AttnParams& p, cudaStream_t st) {
     tp.token = p.token;
     tp.token_val = p.token_val;
     tp.sl2 = p.scale * kLog2e;
+    tp.inv_scale = 1.f / p.scale;
     tp.n_pairs = (int)((p.Nq + 2 * BM - 1) / (2 * BM));
     const int64_t n_items = (int64_t)tp.n_pairs * p.H * p.B;
     if (n_items >= ((int64_t)1 << 31) || p.Nkv + 2 * BM >= ((int64_t)1 << 31)) return GFWA_ERR_INVALID_ARGUMENT;

@@ -8,6 +8,7 @@
 #pragma once
 
 #include <cuda.h>
+#include <cuda_bf16.h>
 #include <stdint.h>
 
 namespace gfwa {
@@ -326,6 +327,17 @@ __device__ __forceinline__ uint32_t pack_f16x2(float lo, float hi) {
 // a packed bf16 pair -> a packed fp16 pair (RNE; exact for |x| in the fp16 normal range)
 __device__ __forceinline__ uint32_t bf16x2_to_f16x2(uint32_t w) {
     return pack_f16x2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
+}
+// x = hi + mid + lo to ~24 bits, each a bf16 (bit patterns in the low 16 bits): the
+// bias-folding slabs of the attention kernels carry fp32 values through bf16 MMAs
+__device__ __forceinline__ void split3_bf16(float x, uint32_t& h, uint32_t& m, uint32_t& l) {
+    const __nv_bfloat16 bh = __float2bfloat16_rn(x);
+    const float r1 = x - __bfloat162float(bh);
+    const __nv_bfloat16 bm = __float2bfloat16_rn(r1);
+    const __nv_bfloat16 bl = __float2bfloat16_rn(r1 - __bfloat162float(bm));
+    h = __bfloat16_as_ushort(bh);
+    m = __bfloat16_as_ushort(bm);
+    l = __bfloat16_as_ushort(bl);
 }
 __device__ __forceinline__ float ex2(float x) {
     float y;

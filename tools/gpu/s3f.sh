@@ -1,0 +1,3 @@
+for W in C2 C3_w512; do timeout 120 python tools/time_kernels.py $W bwd 2>&1 | tail -1; done
+timeout 600 python -m pytest tests/test_gpu_attn.py tests/test_gpu_dist.py tests/test_gpu_graph.py -x -q 2>&1 | tail -3
+timeout 300 python tools/gpu/dalpha_diag.py 2>&1 | tail -12

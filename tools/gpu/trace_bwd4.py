@@ -23,10 +23,10 @@ for _ in range(3):
 torch.cuda.synchronize()
 lib = gb.load()
 T = 512
-buf = np.zeros(148 * 8 * T, dtype=np.int64)
+buf = np.zeros(148 * 12 * T, dtype=np.int64)
 lib.gfwa_debug_bwd_trace.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
 assert lib.gfwa_debug_bwd_trace(buf.ctypes.data, buf.size) == 0
-tr = buf.reshape(148, 8, T).astype(np.float64)
+tr = buf.reshape(148, 12, T).astype(np.float64)
 for cta in (3, 77):
     t = tr[cta]
     base = t[3, 0]
@@ -50,6 +50,11 @@ ok = lambda *a: np.logical_and.reduce([x > 0 for x in a])
 for nm, a, b in (("A st issue -> softmax start", S, X), ("B softmax start -> ds_ready", X, R),
                  ("C ds_ready -> mma2 issue", R, M2), ("D mma2 issue -> drain sees dq_full", M2, D),
                  ("E drain sees -> drained", D, DR)):
+    m = ok(a, b)
+    q(nm, (b - a)[m])
+for nm, a, b in (("WG1 st_full seen - WG0's", X, tr[:, 9]), ("WG1 softmax (warp 4)", tr[:, 9], tr[:, 8]),
+                 ("ds_ready warp3 - warp0", R, tr[:, 10]), ("ds_ready warp7 - warp0", R, tr[:, 11]),
+                 ("last ds_ready (w0,3,4,7) -> mma2 issue", np.maximum.reduce([R, tr[:, 8], tr[:, 10], tr[:, 11]]), M2)):
     m = ok(a, b)
     q(nm, (b - a)[m])
 m = ok(DR[:, :-2], S[:, 2:])
