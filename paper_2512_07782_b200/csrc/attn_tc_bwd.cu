@@ -781,7 +781,9 @@ __global__ void __launch_bounds__(256) bwd_tc_pre_kernel(AttnParams p) {
 }
 
 // D = rowsum((O + O_lo) dO) and zeroing of dQacc, fast path for contiguous O, O_lo, dO:
-// a warp per row (grid-stride, 32-bit index math), the zeroing as flat 32-byte stores
+// each warp takes R rows per iteration (32 / (D / 8) lanes per row, 16-byte loads, all
+// 3R loads in flight before any use), grid-stride, 32-bit index math; the zeroing as
+// flat 16-byte stores
 template <int D>
 __global__ void __launch_bounds__(256) bwd_tc_pre_flat_kernel(const __nv_bfloat16* __restrict__ o,
                                                              const __nv_bfloat16* __restrict__ olo,
@@ -791,32 +793,60 @@ __global__ void __launch_bounds__(256) bwd_tc_pre_flat_kernel(const __nv_bfloat1
                                                              float* __restrict__ dU, uint32_t n_du,
                                                              const unsigned long long* __restrict__ token,
                                                              unsigned long long token_val) {
-    const uint32_t lane = threadIdx.x & 31;
+    constexpr int LPR = D / 8;           // lanes per row (8 bf16 = 16 B each)
+    constexpr int RPW = 32 / LPR;        // rows per warp load
+    constexpr int U = 2;                 // loads unrolled: U * RPW rows per iteration
+    const uint32_t lane = threadIdx.x & 31, sub = lane / LPR, cl = lane % LPR;
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
     // gfwa_fwd_train already zeroed the accumulator (its token is in the workspace)
     const bool zero = !(token && *token == token_val);
     // dU accumulates red.adds in the main kernel: zero it here (no separate memset launch)
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_du; i += gridDim.x * blockDim.x) dU[i] = 0.f;
-    auto f4 = [](uint2 v) {
-        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.x));
-        const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.y));
-        return make_float4(a.x, a.y, b.x, b.y);
+    auto dot8 = [](uint4 a, uint4 l, uint4 g) {
+        const uint32_t* av = &a.x;
+        const uint32_t* lv = &l.x;
+        const uint32_t* gv = &g.x;
+        float s = 0.f;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const float2 fa = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(av + k));
+            const float2 fl = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(lv + k));
+            const float2 fg = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(gv + k));
+            s = fmaf(fa.x + fl.x, fg.x, s);
+            s = fmaf(fa.y + fl.y, fg.y, s);
+        }
+        return s;
     };
-    const bool act = lane < D / 4;  // 4 elements per lane
-    for (uint32_t row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < rows; row += nw) {
-        float a = 0.f;
-        if (act) {
-            const float4 oh = f4(__ldcs(reinterpret_cast<const uint2*>(o + (size_t)row * D) + lane));
-            const float4 ol = f4(__ldcs(reinterpret_cast<const uint2*>(olo + (size_t)row * D) + lane));
-            const float4 g = f4(__ldcs(reinterpret_cast<const uint2*>(dO + (size_t)row * D) + lane));
-            a = (oh.x + ol.x) * g.x + (oh.y + ol.y) * g.y + (oh.z + ol.z) * g.z + (oh.w + ol.w) * g.w;
+    for (uint32_t r0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * (U * RPW); r0 < rows; r0 += nw * U * RPW) {
+        uint4 va[U], vl[U], vg[U];
+        bool ok[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t row = r0 + u * RPW + sub;
+            ok[u] = row < rows;
+            const size_t e = (size_t)(ok[u] ? row : 0) * D + cl * 8;
+            va[u] = __ldcs(reinterpret_cast<const uint4*>(o + e));
+            vl[u] = __ldcs(reinterpret_cast<const uint4*>(olo + e));
+            vg[u] = __ldcs(reinterpret_cast<const uint4*>(dO + e));
         }
-        a = warp_sum(a);
-        if (lane == 0) {
-            const uint32_t hh = row % H, bt = row / H, t = bt % Nq, b = bt / Nq;
-            Dv[((size_t)b * H + hh) * Nq + t] = a;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            float a = dot8(va[u], vl[u], vg[u]);
+#pragma unroll
+            for (int m = LPR / 2; m >= 1; m >>= 1) a += __shfl_xor_sync(0xffffffffu, a, m);
+            const uint32_t row = r0 + u * RPW + sub;
+            if (ok[u]) {
+                if (cl == 0) {
+                    const uint32_t hh = row % H, bt = row / H, t = bt % Nq, b = bt / Nq;
+                    Dv[((size_t)b * H + hh) * Nq + t] = a;
+                }
+                if (zero) {
+                    float4* z = reinterpret_cast<float4*>(acc + (size_t)row * D) + 2 * cl;
+                    z[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+            }
         }
-        if (zero && act) reinterpret_cast<float4*>(acc + (size_t)row * D)[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
 }
 
@@ -885,7 +915,7 @@ static gfwa_status_t tc_bwd_d(const AttnParams& pin, cudaStream_t st, void* ws) 
     const bool o_flat = p.Olo && p.os[2] == D && p.os[1] == p.H * D && p.os[0] == p.Nq * p.H * D &&
                         rows < ((int64_t)1 << 31) && n_du < ((int64_t)1 << 31);
     if (o_flat) {
-        bwd_tc_pre_flat_kernel<D><<<(unsigned)min64((rows + 7) / 8, (int64_t)n_sm * 16), 256, 0, st>>>(
+        bwd_tc_pre_flat_kernel<D><<<(unsigned)min64((rows + 8 * 512 / D - 1) / (8 * 512 / D), (int64_t)n_sm * 8), 256, 0, st>>>(
             (const __nv_bfloat16*)p.O, (const __nv_bfloat16*)p.Olo, (const __nv_bfloat16*)p.dO, p.Dv, p.dQacc, (uint32_t)rows, (uint32_t)p.H, (uint32_t)p.Nq, p.dU,
             (uint32_t)n_du, p.token, p.token_val);
     } else {

@@ -308,3 +308,25 @@ def test_d64_full_grid_many_items_per_cta():
         l_g = np64(LSE)[rows[:, 0], rows[:, 1], rows[:, 2]]
         assert np.abs(o_g - o_r).max() <= TOL_BF16_O
         assert np.abs(l_g - l_r).max() <= TOL_LSE
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_persistent_kernels_many_items_per_cta(d, monkeypatch):
+    """Forward and backward forced onto 2 / 3 CTAs (GFWA_FWD_GRID / GFWA_BWD_GRID,
+    read at every launch), so each CTA walks many work items: the backward's
+    rotating shared-memory slot pool (next item's K, V and first Q/dO stage
+    loaded during the current item's last steps, dK/dV staged in the item's K
+    slot), the dK/dV-accumulator hand-over between items, and items no query
+    reaches (a halo longer than w: those keys get dK = dV = 0)."""
+    monkeypatch.setenv("GFWA_FWD_GRID", "2")
+    monkeypatch.setenv("GFWA_BWD_GRID", "3")
+    for s in (synth.AttnShape(B=2, H=3, N=900, d=d, w=200),
+              synth.AttnShape(B=1, H=2, N=300, d=d, w=100, N_kv=300 + 450)):
+        got, ref = _run(s, torch.bfloat16, seed=7 * s.N + d)
+        assert max_abs(got["O"], ref["O"]) <= TOL_BF16_O
+        assert max_abs(got["LSE"], ref["LSE"]) <= TOL_LSE
+        for k in ("dQ", "dK", "dV", "dU", "dalpha"):
+            assert max_abs(got[k], ref[k]) <= TOL_BF16_GRAD, k
+        if s.nkv > s.N + s.w:  # keys before the first query's window: exact zeros
+            dead = s.nkv - s.N - s.w + 1
+            assert torch.count_nonzero(got["dK"][:, :dead]) == 0 and torch.count_nonzero(got["dV"][:, :dead]) == 0

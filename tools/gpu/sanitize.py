@@ -26,5 +26,15 @@ for Hk in (4, 1):
     Uc = torch.zeros(2, 4, 64, device=dev)
     pos = torch.full((2,), 70, dtype=torch.int64, device=dev)
     gb.gfwa_decode(q, k, v, a_new, Kc, Vc, Uc, pos)
+# persistent kernels with several items per CTA (slot-pool rotation, item boundaries), d = 64 and 128
+os.environ["GFWA_BWD_GRID"] = "3"
+os.environ["GFWA_FWD_GRID"] = "2"
+for d in (64, 128):
+    sm = synth.AttnShape(B=1, H=3, N=900, d=d, w=200)
+    Q, K, V, dO = synth.attn_inputs(sm, seed=6, device=dev, dtype=torch.bfloat16)
+    Um = gb.gfwa_gate_prefix(*synth.gate_inputs(1, sm.N, 3, seed=7, device=dev))
+    O, LSE, Olo = gb.gfwa_fwd(Q, K, V, Um, sm.w, want_o_lo=True, prepare_bwd=True)
+    gb.gfwa_bwd(Q, K, V, Um, O, LSE, dO, sm.w, O_lo=Olo)
+del os.environ["GFWA_BWD_GRID"], os.environ["GFWA_FWD_GRID"]
 torch.cuda.synchronize()
 print("sanitize workload done")
