@@ -183,3 +183,28 @@ def gate_chain(h, beta, dalpha, eps: float = 1e-6):
     _load().oracle_gate_chain(_p(h), _p(beta), _p(dalpha), _I64(B), _I64(N), _I64(H), ctypes.c_double(eps),
                               _p(dh), _p(db))
     return dh, db
+
+
+def normgate_fwd(O, g, gamma, eps: float = 1e-5):
+    """AttnLayer epilogue (reading C-27): Y = swish(g) * gamma * O * rstd
+    per (b, t, h) row, rstd = 1/sqrt(mean_c O_c^2 + eps).  O, g [B,Nq,H,d];
+    gamma [d].  Returns (Y [B,Nq,H,d], rstd [B,H,Nq])."""
+    O, g, gamma = _f64(O), _f64(g), _f64(gamma)
+    B, Nq, H, d = O.shape
+    Y = np.empty_like(O)
+    rstd = np.empty((B, H, Nq))
+    _load().oracle_normgate_fwd(_p(O), _p(g), _p(gamma), _I64(B), _I64(Nq), _I64(H), _I64(d),
+                                ctypes.c_double(eps), _p(Y), _p(rstd))
+    return Y, rstd
+
+
+def normgate_bwd(O, g, gamma, dY, eps: float = 1e-5):
+    """Chain rule of normgate_fwd: (dO, dg [B,Nq,H,d], dgamma [d])."""
+    O, g, gamma, dY = _f64(O), _f64(g), _f64(gamma), _f64(dY)
+    B, Nq, H, d = O.shape
+    dO = np.empty_like(O)
+    dg = np.empty_like(O)
+    dgamma = np.empty(d)
+    _load().oracle_normgate_bwd(_p(O), _p(g), _p(gamma), _p(dY), _I64(B), _I64(Nq), _I64(H), _I64(d),
+                                ctypes.c_double(eps), _p(dO), _p(dg), _p(dgamma))
+    return dO, dg, dgamma

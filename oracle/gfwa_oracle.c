@@ -334,3 +334,70 @@ void oracle_gate_chain(const double* h, const double* beta, const double* dalpha
                 dbeta[i] = da * (sigmoid(z) * h[i] * be - softplus(z)) / (be * be);
             }
 }
+
+/*
+ * AttnLayer output epilogue (§3 "(3) Block Structure"):
+ *   O~ = concat_h norm(O~^(h)),  G = swish(linear(X)),  out = (G (.) O~) W_O
+ * Reading C-27: norm is an RMSNorm over the head dim d with a per-channel
+ * weight gamma[d] shared by the heads, swish(x) = x sigmoid(x) is applied to
+ * the gate pre-activation g = linear(X) (given), and the W_O product is the
+ * caller's GEMM.  Per row (b, t, h) of O [B][Nq][H][d]:
+ *   r   = 1 / sqrt( (1/d) sum_c O_c^2 + eps )
+ *   n_c = gamma_c O_c r
+ *   Y_c = g_c sigmoid(g_c) n_c
+ * rstd [B][H][Nq] receives r.
+ */
+void oracle_normgate_fwd(const double* O, const double* g, const double* gamma, int64_t B, int64_t Nq,
+                         int64_t H, int64_t d, double eps, double* Y, double* rstd) {
+    for (int64_t b = 0; b < B; ++b)
+        for (int64_t t = 0; t < Nq; ++t)
+            for (int64_t hh = 0; hh < H; ++hh) {
+                const int64_t row = ((b * Nq + t) * H + hh) * d;
+                double ms = 0.0;
+                for (int64_t c = 0; c < d; ++c) ms += O[row + c] * O[row + c];
+                ms /= (double)d;
+                double r = 1.0 / sqrt(ms + eps);
+                rstd[(b * H + hh) * Nq + t] = r;
+                for (int64_t c = 0; c < d; ++c) {
+                    double n = gamma[c] * O[row + c] * r;
+                    double G = g[row + c] * sigmoid(g[row + c]);
+                    Y[row + c] = G * n;
+                }
+            }
+}
+
+/*
+ * Chain rule of oracle_normgate_fwd (C-27), given dY [B][Nq][H][d]:
+ *   dn_c     = dY_c G_c                     (n_c = gamma_c O_c r)
+ *   dg_c     = dY_c n_c (sigmoid(g_c) + g_c sigmoid(g_c) (1 - sigmoid(g_c)))
+ *   dgamma_c = sum over every row of dn_c O_c r
+ *   dO_k     = r gamma_k dn_k - (r^3 O_k / d) sum_c gamma_c dn_c O_c
+ * (dr/dO_k = -r^3 O_k / d).  dO feeds Alg. E.2 as the attention output's gradient.
+ */
+void oracle_normgate_bwd(const double* O, const double* g, const double* gamma, const double* dY, int64_t B,
+                         int64_t Nq, int64_t H, int64_t d, double eps, double* dO, double* dg, double* dgamma) {
+    for (int64_t c = 0; c < d; ++c) dgamma[c] = 0.0;
+    for (int64_t b = 0; b < B; ++b)
+        for (int64_t t = 0; t < Nq; ++t)
+            for (int64_t hh = 0; hh < H; ++hh) {
+                const int64_t row = ((b * Nq + t) * H + hh) * d;
+                double ms = 0.0;
+                for (int64_t c = 0; c < d; ++c) ms += O[row + c] * O[row + c];
+                ms /= (double)d;
+                double r = 1.0 / sqrt(ms + eps);
+                double s = 0.0; /* sum_c gamma_c dn_c O_c */
+                for (int64_t c = 0; c < d; ++c) {
+                    double sg = sigmoid(g[row + c]);
+                    double G = g[row + c] * sg;
+                    double n = gamma[c] * O[row + c] * r;
+                    double dn = dY[row + c] * G;
+                    dg[row + c] = dY[row + c] * n * (sg + g[row + c] * sg * (1.0 - sg));
+                    dgamma[c] += dn * O[row + c] * r;
+                    s += gamma[c] * dn * O[row + c];
+                }
+                for (int64_t k = 0; k < d; ++k) {
+                    double dn = dY[row + k] * g[row + k] * sigmoid(g[row + k]);
+                    dO[row + k] = r * gamma[k] * dn - r * r * r * O[row + k] / (double)d * s;
+                }
+            }
+}

@@ -403,3 +403,63 @@ def test_gate_chain_finite_differences():
     for idx in [(0, t, hh) for t in range(N) for hh in range(H)]:
         assert _fd(f_h, h, idx) == pytest.approx(dh[idx], rel=1e-6, abs=1e-9)
         assert _fd(f_b, beta, idx) == pytest.approx(db[idx], rel=1e-6, abs=1e-9)
+
+
+# --- AttnLayer epilogue (reading C-27): RMSNorm per head, swish gate ---
+
+
+def test_normgate_closed_forms():
+    """Constant rows: O_c = a for all c gives n_c = gamma_c a / sqrt(a^2 + eps); g = 0
+    gives Y = 0 (swish(0) = 0) and dg = dY n / 2 (sigmoid(0) = 1/2); with eps = 0
+    and gamma = 1 every row of n has mean square exactly 1."""
+    B, N, H, d = 1, 3, 2, 8
+    a = np.array([0.5, -2.0, 3.0]).reshape(1, N, 1, 1) * np.ones((B, N, H, d))
+    gamma = 1.0 + 0.1 * np.arange(d)
+    g = np.full((B, N, H, d), 40.0)  # swish(40) = 40 (sigmoid(40) = 1 - 4e-18)
+    Y, rstd = oracle.normgate_fwd(a, g, gamma, eps=1e-5)
+    expect = 40.0 * gamma * a / np.sqrt(a ** 2 + 1e-5)
+    assert np.allclose(Y, expect, rtol=1e-14)
+    assert np.allclose(rstd, 1.0 / np.sqrt(a[:, :, :, 0].transpose(0, 2, 1) ** 2 + 1e-5), rtol=1e-14)
+    O = _rand((B, N, H, d), 140)
+    dY = _rand((B, N, H, d), 141)
+    Y0, _ = oracle.normgate_fwd(O, np.zeros_like(O), gamma, eps=1e-5)
+    assert np.all(Y0 == 0.0)
+    _, dg0, _ = oracle.normgate_bwd(O, np.zeros_like(O), gamma, dY, eps=1e-5)
+    n = gamma * O / np.sqrt(np.mean(O ** 2, -1, keepdims=True) + 1e-5)
+    assert np.allclose(dg0, 0.5 * dY * n, rtol=1e-13, atol=1e-15)
+    Yn, _ = oracle.normgate_fwd(O, np.full_like(O, 40.0), np.ones(d), eps=0.0)
+    assert np.allclose(np.mean((Yn / 40.0) ** 2, -1), 1.0, rtol=1e-13)
+
+
+def test_normgate_bwd_finite_differences():
+    """dO, dg, dgamma of the epilogue vs central FD of sum(Y * dY)."""
+    B, N, H, d = 1, 2, 2, 5
+    O = _rand((B, N, H, d), 142)
+    g = _rand((B, N, H, d), 143, 2.0)
+    gamma = 1.0 + _rand((d,), 144, 0.3)
+    dY = _rand((B, N, H, d), 145)
+    dO, dg, dgamma = oracle.normgate_bwd(O, g, gamma, dY, eps=1e-3)
+    loss = lambda o, gg, ga: float(np.sum(oracle.normgate_fwd(o, gg, ga, eps=1e-3)[0] * dY))  # noqa: E731
+    for idx in [(0, t, hh, c) for t in range(N) for hh in range(H) for c in range(d)]:
+        assert _fd(lambda x: loss(x, g, gamma), O, idx) == pytest.approx(dO[idx], rel=1e-6, abs=1e-9)
+        assert _fd(lambda x: loss(O, x, gamma), g, idx) == pytest.approx(dg[idx], rel=1e-6, abs=1e-9)
+    for c in range(d):
+        assert _fd(lambda x: loss(O, g, x), gamma, (c,)) == pytest.approx(dgamma[c], rel=1e-6, abs=1e-9)
+
+
+def test_normgate_matches_torch_autograd():
+    """The same epilogue through torch's fp64 ops and autograd (a library routine,
+    independent of the oracle's loops): RMSNorm * weight, times g * sigmoid(g)."""
+    B, N, H, d = 2, 3, 2, 16
+    O = torch.from_numpy(_rand((B, N, H, d), 146)).requires_grad_(True)
+    g = torch.from_numpy(_rand((B, N, H, d), 147, 2.0)).requires_grad_(True)
+    gamma = torch.from_numpy(1.0 + _rand((d,), 148, 0.3)).requires_grad_(True)
+    dY = torch.from_numpy(_rand((B, N, H, d), 149))
+    Yt = torch.nn.functional.rms_norm(O, (d,), weight=gamma, eps=1e-5) * torch.nn.functional.silu(g)
+    Yt.backward(dY)
+    Y, rstd = oracle.normgate_fwd(O.detach(), g.detach(), gamma.detach(), eps=1e-5)
+    dO, dg, dgamma = oracle.normgate_bwd(O.detach(), g.detach(), gamma.detach(), dY, eps=1e-5)
+    assert np.allclose(Y, Yt.detach().numpy(), rtol=1e-12, atol=1e-14)
+    assert np.allclose(dO, O.grad.numpy(), rtol=1e-11, atol=1e-13)
+    assert np.allclose(dg, g.grad.numpy(), rtol=1e-11, atol=1e-13)
+    assert np.allclose(dgamma, gamma.grad.numpy(), rtol=1e-11, atol=1e-13)
