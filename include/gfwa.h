@@ -209,6 +209,52 @@ gfwa_status_t gfwa_bwd(const gfwa_attn_desc_t* desc, const void* Q, const void* 
                        const double* dalpha_carry, void* ws, size_t ws_bytes, gfwa_stream_t stream);
 
 /* ------------------------------------------------------------------------- */
+/* AttnLayer output epilogue fused into the attention kernels:     */
+/*   O~ = concat_h norm(GatedFWA_h),  G = swish(linear(X)),  out = (G . O~) W_O */
+/* Reading C-27: norm = RMSNorm over the head dim with a per-channel weight    */
+/* gamma[d] shared by the heads; swish(x) = x sigmoid(x) is applied to the     */
+/* gate pre-activation g = linear(X) given by the caller; the W_O GEMM stays   */
+/* the caller's.  Per (b, t, h) row:                                            */
+/*   rstd = 1 / sqrt(mean_c O_c^2 + eps),  Y_c = g_c sigmoid(g_c) gamma_c O_c rstd */
+/* ------------------------------------------------------------------------- */
+typedef struct {
+    const void* g;      /* [B,N_q,H,d] bf16, O's (packed) layout: gate pre-activation */
+    const float* gamma; /* [d] fp32 RMSNorm weight, shared by the heads */
+    float eps;          /* RMSNorm epsilon, > 0 */
+    float* rstd;        /* [B,H,N_q] fp32: written by the forward, read by the backward */
+} gfwa_normgate_t;
+
+/*
+ * gfwa_fwd_normgate -- gfwa_fwd (bwd_ws == NULL) or gfwa_fwd_train (bwd_ws given)
+ * whose epilogue also writes Y [B,N_q,H,d] bf16 (O's layout) and rstd from the
+ * fp32 attention output in registers: the normalised, gated layer output never
+ * makes a round trip through HBM as O.  O (the attention output O~, needed by
+ * the backward) and O_lo are still written.  BF16 tensor-core path only
+ * (UNSUPPORTED otherwise); O's layout must be packed [B,N_q,H,d]
+ * (INVALID_ARGUMENT otherwise); g, Y 16-byte aligned.
+ */
+gfwa_status_t gfwa_fwd_normgate(const gfwa_attn_desc_t* desc, const void* Q, const void* K, const void* V,
+                                const float* U, const gfwa_normgate_t* ng, void* O, void* O_lo, float* LSE,
+                                void* Y, void* bwd_ws, size_t bwd_ws_bytes, gfwa_stream_t stream);
+
+/*
+ * gfwa_bwd_normgate -- the layer backward from dY (the gradient of Y): the
+ * epilogue's chain rule runs inside the backward's preprocess pass,
+ *   dO~ = rstd gamma dn - (rstd^3 O~ / d) sum_c gamma_c dn_c O~_c,  dn = dY swish(g)
+ *   dg = dY n swish'(g) (n = gamma O~ rstd),  dgamma = sum over rows of dn O~ rstd
+ * with O~ = O + O_lo; dO~ is written to dO (bf16, O's layout: an OUTPUT here)
+ * and D = rowsum(O~ * dO~) is taken from those bf16 values (C-12), then Alg.
+ * E.2 proceeds exactly as gfwa_bwd.  dg [B,N_q,H,d] bf16; dgamma [d] fp32 is
+ * overwritten (zeroed, then accumulated by the call).  Layout and path
+ * requirements as gfwa_fwd_normgate; the other arguments as gfwa_bwd.
+ */
+gfwa_status_t gfwa_bwd_normgate(const gfwa_attn_desc_t* desc, const void* Q, const void* K, const void* V,
+                                const float* U, const void* O, const void* O_lo, const float* LSE,
+                                const gfwa_normgate_t* ng, const void* dY, void* dO, void* dg, float* dgamma,
+                                void* dQ, void* dK, void* dV, float* dU, float* dalpha,
+                                const double* dalpha_carry, void* ws, size_t ws_bytes, gfwa_stream_t stream);
+
+/* ------------------------------------------------------------------------- */
 /* Decode: one new token per sequence over a rolling w-entry cache.           */
 /* The paper claims O(wd) per step with a KV cache but gives no  */
 /* algorithm; reading C-16: decode(t) == row t of Eq. 12.                     */

@@ -65,6 +65,12 @@ class DecodeDesc(ctypes.Structure):
     ]
 
 
+class NormGate(ctypes.Structure):
+    """gfwa_normgate_t (include/gfwa.h): the AttnLayer epilogue's inputs (C-27)."""
+    _fields_ = [("g", ctypes.c_void_p), ("gamma", ctypes.c_void_p), ("eps", ctypes.c_float),
+                ("rstd", ctypes.c_void_p)]
+
+
 _lib = None
 _lock = threading.Lock()
 _VP = ctypes.c_void_p
@@ -91,6 +97,8 @@ EXPORTED = (
     "gfwa_version",
     "gfwa_launch_count",
     "gfwa_attn_path",
+    "gfwa_fwd_normgate",
+    "gfwa_bwd_normgate",
 )
 
 
@@ -127,6 +135,12 @@ def load() -> ctypes.CDLL:
         lib.gfwa_bwd_workspace_size.argtypes = [ctypes.POINTER(AttnDesc)]
         lib.gfwa_bwd.restype = ctypes.c_int
         lib.gfwa_bwd.argtypes = [ctypes.POINTER(AttnDesc)] + [_VP] * 15 + [sz, _VP]
+        lib.gfwa_fwd_normgate.restype = ctypes.c_int
+        lib.gfwa_fwd_normgate.argtypes = [ctypes.POINTER(AttnDesc)] + [_VP] * 4 + [ctypes.POINTER(NormGate)] + \
+            [_VP] * 5 + [sz, _VP]
+        lib.gfwa_bwd_normgate.restype = ctypes.c_int
+        lib.gfwa_bwd_normgate.argtypes = [ctypes.POINTER(AttnDesc)] + [_VP] * 7 + [ctypes.POINTER(NormGate)] + \
+            [_VP] * 11 + [sz, _VP]
         lib.gfwa_decode_workspace_size.restype = sz
         lib.gfwa_decode_workspace_size.argtypes = [ctypes.POINTER(DecodeDesc)]
         lib.gfwa_decode.restype = ctypes.c_int
@@ -352,6 +366,71 @@ def gfwa_bwd(Q, K, V, U, O, LSE, dO, w: int, scale: float | None = None, O_lo=No
                       _ptr(dalpha_carry), _ptr(ws), nbytes, _stream(dev))
     _check(st, "gfwa_bwd")
     return dQ, dK, dV, dU, dalpha
+
+
+def gfwa_fwd_normgate(Q, K, V, U, g, gamma, w: int, eps: float = 1e-5, scale: float | None = None,
+                      want_o_lo: bool = True, prepare_bwd: bool = False):
+    """AttnLayer forward (reading C-27): the attention of gfwa_fwd plus, in
+    its epilogue, Y = swish(g) * gamma * O * rstd per (b, t, h) row, rstd =
+    1/sqrt(mean_c O_c^2 + eps).  g [B,Nq,H,d] bf16 (the gate pre-activation
+    linear(X)); gamma [d] fp32.  Returns (Y, O, LSE, O_lo, rstd)."""
+    lib = load()
+    _need_cuda(Q, K, V, U, g, gamma)
+    B, Nq, H, d = Q.shape
+    dev = Q.device
+    O = torch.empty(B, Nq, H, d, dtype=Q.dtype, device=dev)
+    Y = torch.empty_like(O)
+    O_lo = torch.empty_like(O) if want_o_lo else None
+    LSE = torch.empty(B, H, Nq, dtype=torch.float32, device=dev)
+    rstd = torch.empty(B, H, Nq, dtype=torch.float32, device=dev)
+    g = g.contiguous()
+    gamma = gamma.to(torch.float32).contiguous()
+    ng = NormGate(_ptr(g), _ptr(gamma), float(eps), _ptr(rstd))
+    dsc = make_desc(Q, K, V, O, w, scale)
+    ws, nbytes = None, 0
+    if prepare_bwd:
+        nbytes = lib.gfwa_bwd_workspace_size(ctypes.byref(dsc))
+        ws = workspace(nbytes, dev, "bwd")
+    st = lib.gfwa_fwd_normgate(ctypes.byref(dsc), _ptr(Q), _ptr(K), _ptr(V), _ptr(U.contiguous()), ctypes.byref(ng),
+                               _ptr(O), _ptr(O_lo), _ptr(LSE), _ptr(Y), _ptr(ws), nbytes, _stream(dev))
+    _check(st, "gfwa_fwd_normgate")
+    return Y, O, LSE, O_lo, rstd
+
+
+def gfwa_bwd_normgate(Q, K, V, U, O, LSE, g, gamma, rstd, dY, w: int, eps: float = 1e-5,
+                      scale: float | None = None, O_lo=None, want_dalpha: bool = True, dalpha_carry=None):
+    """AttnLayer backward from dY: the epilogue's chain rule (dO~, dg, dgamma) fused into
+    the backward's preprocess, then Alg. E.2 on dO~.  Returns
+    (dQ, dK, dV, dU, dalpha, dg, dgamma, dO~)."""
+    lib = load()
+    _need_cuda(Q, K, V, U, O, LSE, g, gamma, rstd, dY)
+    B, Nq, H, d = Q.shape
+    Nkv = K.shape[1]
+    dev = Q.device
+    O = O.contiguous()
+    O_lo = None if O_lo is None else O_lo.contiguous()
+    g, dY = g.contiguous(), dY.contiguous()
+    gamma = gamma.to(torch.float32).contiguous()
+    dO = torch.empty_like(O)
+    dg = torch.empty_like(O)
+    dgamma = torch.empty(d, dtype=torch.float32, device=dev)
+    dQ = torch.empty_strided(Q.shape, Q.stride(), dtype=Q.dtype, device=dev)
+    dK = torch.empty_strided(K.shape, K.stride(), dtype=K.dtype, device=dev)
+    dV = torch.empty_strided(V.shape, V.stride(), dtype=V.dtype, device=dev)
+    dU = torch.empty(B, H, Nkv, dtype=torch.float32, device=dev)
+    dalpha = torch.empty(B, H, Nkv, dtype=torch.float32, device=dev) if want_dalpha else None
+    if dalpha_carry is not None:
+        dalpha_carry = dalpha_carry.to(torch.float64).contiguous()
+    ng = NormGate(_ptr(g), _ptr(gamma), float(eps), _ptr(rstd.contiguous()))
+    dsc = make_desc(Q, K, V, O, w, scale)
+    nbytes = lib.gfwa_bwd_workspace_size(ctypes.byref(dsc))
+    ws = workspace(nbytes, dev, "bwd")
+    st = lib.gfwa_bwd_normgate(ctypes.byref(dsc), _ptr(Q), _ptr(K), _ptr(V), _ptr(U.contiguous()), _ptr(O),
+                               _ptr(O_lo), _ptr(LSE), ctypes.byref(ng), _ptr(dY), _ptr(dO), _ptr(dg), _ptr(dgamma),
+                               _ptr(dQ), _ptr(dK), _ptr(dV), _ptr(dU), _ptr(dalpha), _ptr(dalpha_carry), _ptr(ws),
+                               nbytes, _stream(dev))
+    _check(st, "gfwa_bwd_normgate")
+    return dQ, dK, dV, dU, dalpha, dg, dgamma, dO
 
 
 def gfwa_attn_path(Q, K, V, w: int) -> int:

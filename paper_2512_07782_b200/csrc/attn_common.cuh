@@ -33,6 +33,17 @@ struct AttnParams {
     float* zero_acc;               // [B, Nq, H, d] fp32 region to zero (null: none)
     unsigned long long* token;     // prepared-workspace token slot (device)
     unsigned long long token_val;  // value identifying this problem's preparation
+    // AttnLayer output epilogue (reading C-27): Y = swish(g) * gamma * O * rstd,
+    // rstd = 1/sqrt(mean_c O_c^2 + eps) per (b, t, h) row; g, Y, dY, dg share O's strides
+    const void* ng_g;      // bf16 gate pre-activation (null: no epilogue)
+    const float* ng_gamma; // [d]
+    float ng_eps;
+    float* ng_rstd;        // [B,H,Nq] (forward output, backward input)
+    void* ng_Y;            // forward output
+    const void* ng_dY;     // backward input
+    void* ng_dg;           // backward output
+    float* ng_dgamma;      // backward output [d] (zeroed and accumulated by the call)
+    bool pre_done;         // backward: D, dO and the zeroing came from the fused epilogue pre kernel
 };
 
 // token marking a backward workspace whose dQ accumulator the forward already zeroed

@@ -850,6 +850,125 @@ __global__ void __launch_bounds__(256) bwd_tc_pre_flat_kernel(const __nv_bfloat1
     }
 }
 
+// AttnLayer epilogue backward fused with the preprocess (reading C-27): per
+// (b, t, h) row, from Y's gradient dY, the gate pre-activation g, gamma and the
+// forward's rstd r (O~ = O + O_lo, the fp32 attention output):
+//   dn = dY swish(g);  dg = dY n swish'(g) (n = gamma O~ r);  dgamma += dn O~ r
+//   dO~ = r gamma dn - (r^3 O~ / d) sum_c gamma_c dn_c O~_c   -> bf16 (the dP MMA operand)
+//   D = rowsum(O~ * bf16(dO~))   (C-12; the same dO values the main kernel contracts)
+// plus the zeroing of dU (and of the dQ accumulator unless gfwa_fwd_train prepared it).
+// Flat [rows, D] layouts; a warp takes 32 / (D / 8) rows per iteration (8 channels per
+// lane); dgamma is reduced per block in smem, then one atomic per channel per block.
+template <int D>
+__global__ void __launch_bounds__(256) bwd_tc_pre_normgate_kernel(
+    const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ olo, const __nv_bfloat16* __restrict__ g,
+    const __nv_bfloat16* __restrict__ dY, const float* __restrict__ gamma, const float* __restrict__ rstd,
+    __nv_bfloat16* __restrict__ dO, __nv_bfloat16* __restrict__ dg, float* __restrict__ dgamma,
+    float* __restrict__ Dv, float* __restrict__ acc, uint32_t rows, uint32_t H, uint32_t Nq, float* __restrict__ dU,
+    uint32_t n_du, const unsigned long long* __restrict__ token, unsigned long long token_val) {
+    constexpr int LPR = D / 8, RPW = 32 / LPR;
+    __shared__ float s_dg[8][D];
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, sub = lane / LPR, cl = lane % LPR;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    const bool zero = !(token && *token == token_val);
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_du; i += gridDim.x * blockDim.x) dU[i] = 0.f;
+    float gam[8], dga[8];
+    {
+        const float4 a = __ldg(reinterpret_cast<const float4*>(gamma + 8 * cl));
+        const float4 b = __ldg(reinterpret_cast<const float4*>(gamma + 8 * cl) + 1);
+        gam[0] = a.x; gam[1] = a.y; gam[2] = a.z; gam[3] = a.w;
+        gam[4] = b.x; gam[5] = b.y; gam[6] = b.z; gam[7] = b.w;
+    }
+#pragma unroll
+    for (int c = 0; c < 8; ++c) dga[c] = 0.f;
+    auto unpack8 = [](uint4 v, float (&f)[8]) {
+        const uint32_t* w = &v.x;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const float2 t = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(w + k));
+            f[2 * k] = t.x;
+            f[2 * k + 1] = t.y;
+        }
+    };
+    for (uint32_t r0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * RPW; r0 < rows; r0 += nw * RPW) {
+        const uint32_t row = r0 + sub;
+        const bool ok = row < rows;
+        const size_t e = (size_t)(ok ? row : 0) * D + cl * 8;
+        const uint32_t hh = (ok ? row : 0) % H, bt = (ok ? row : 0) / H, t = bt % Nq, b = bt / Nq;
+        const size_t vi = ((size_t)b * H + hh) * Nq + t;
+        float ov[8], gv[8], yv[8], dn[8];
+        unpack8(__ldcs(reinterpret_cast<const uint4*>(o + e)), ov);
+        if (olo) {
+            float lv[8];
+            unpack8(__ldcs(reinterpret_cast<const uint4*>(olo + e)), lv);
+#pragma unroll
+            for (int c = 0; c < 8; ++c) ov[c] += lv[c];
+        }
+        unpack8(__ldcs(reinterpret_cast<const uint4*>(g + e)), gv);
+        unpack8(__ldcs(reinterpret_cast<const uint4*>(dY + e)), yv);
+        if (!ok)  // a dummy load of row 0: contributes nothing to dgamma
+#pragma unroll
+            for (int c = 0; c < 8; ++c) yv[c] = 0.f;
+        const float r = __ldg(rstd + vi);
+        float s1 = 0.f;
+        uint32_t dgw[4];
+#pragma unroll
+        for (int c = 0; c < 8; c += 2) {
+            float dgc[2];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const float sg = 1.f / (1.f + __expf(-gv[c + q]));
+                const float G = gv[c + q] * sg;
+                dn[c + q] = yv[c + q] * G;
+                const float n = gam[c + q] * ov[c + q] * r;
+                dgc[q] = yv[c + q] * n * (sg + G * (1.f - sg));
+                dga[c + q] = fmaf(dn[c + q] * ov[c + q], r, dga[c + q]);
+                s1 = fmaf(gam[c + q] * dn[c + q], ov[c + q], s1);
+            }
+            dgw[c / 2] = pack_bf16x2(dgc[0], dgc[1]);
+        }
+#pragma unroll
+        for (int m = LPR / 2; m >= 1; m >>= 1) s1 += __shfl_xor_sync(0xffffffffu, s1, m);
+        const float k3 = r * r * r * s1 * (1.f / D);
+        uint32_t dow[4];
+        float dsum = 0.f;
+#pragma unroll
+        for (int c = 0; c < 8; c += 2) {
+            const float d0 = r * gam[c] * dn[c] - k3 * ov[c];
+            const float d1 = r * gam[c + 1] * dn[c + 1] - k3 * ov[c + 1];
+            dow[c / 2] = pack_bf16x2(d0, d1);
+            const float2 rb = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&dow[c / 2]));
+            dsum = fmaf(ov[c], rb.x, fmaf(ov[c + 1], rb.y, dsum));
+        }
+#pragma unroll
+        for (int m = LPR / 2; m >= 1; m >>= 1) dsum += __shfl_xor_sync(0xffffffffu, dsum, m);
+        if (ok) {
+            *reinterpret_cast<uint4*>(dO + e) = make_uint4(dow[0], dow[1], dow[2], dow[3]);
+            *reinterpret_cast<uint4*>(dg + e) = make_uint4(dgw[0], dgw[1], dgw[2], dgw[3]);
+            if (cl == 0) Dv[vi] = dsum;
+            if (zero) {
+                float4* z = reinterpret_cast<float4*>(acc + (size_t)row * D) + 2 * cl;
+                z[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+                z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        }
+    }
+    // dgamma: the warp's sub-rows (lanes with the same cl), then the block, then global
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+        for (int m = LPR; m < 32; m <<= 1) dga[c] += __shfl_xor_sync(0xffffffffu, dga[c], m);
+    if (sub == 0)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) s_dg[warp][8 * cl + c] = dga[c];
+    __syncthreads();
+    for (int c = threadIdx.x; c < D; c += blockDim.x) {
+        float v = 0.f;
+#pragma unroll
+        for (int w8 = 0; w8 < 8; ++w8) v += s_dg[w8][c];
+        atomicAdd(dgamma + c, v);
+    }
+}
+
 // dQ = scale * dQacc -> bf16 (C-3), flat fast path for a contiguous dQ: 8 elements
 // per thread (32-byte loads, 16-byte stores), grid-stride, no index division
 __global__ void __launch_bounds__(256) bwd_tc_post_flat_kernel(const float* __restrict__ acc,
@@ -914,7 +1033,15 @@ static gfwa_status_t tc_bwd_d(const AttnParams& pin, cudaStream_t st, void* ws) 
     const int64_t n_du = p.B * p.H * p.Nkv;
     const bool o_flat = p.Olo && p.os[2] == D && p.os[1] == p.H * D && p.os[0] == p.Nq * p.H * D &&
                         rows < ((int64_t)1 << 31) && n_du < ((int64_t)1 << 31);
-    if (o_flat) {
+    if (p.ng_dY) {  // AttnLayer epilogue backward fused with the preprocess (C-27); layouts checked by the caller
+        if (gfwa_status_t s = check_launch(cudaMemsetAsync(p.ng_dgamma, 0, D * sizeof(float), st))) return s;
+        bwd_tc_pre_normgate_kernel<D><<<(unsigned)min64((rows + 8 * 256 / D - 1) / (8 * 256 / D), (int64_t)n_sm * 8), 256,
+                                        0, st>>>(
+            (const __nv_bfloat16*)p.O, (const __nv_bfloat16*)p.Olo, (const __nv_bfloat16*)p.ng_g,
+            (const __nv_bfloat16*)p.ng_dY, p.ng_gamma, p.ng_rstd, (__nv_bfloat16*)p.dO, (__nv_bfloat16*)p.ng_dg,
+            p.ng_dgamma, p.Dv, p.dQacc, (uint32_t)rows, (uint32_t)p.H, (uint32_t)p.Nq, p.dU, (uint32_t)n_du, p.token,
+            p.token_val);
+    } else if (o_flat) {
         bwd_tc_pre_flat_kernel<D><<<(unsigned)min64((rows + 8 * 512 / D - 1) / (8 * 512 / D), (int64_t)n_sm * 8), 256, 0, st>>>(
             (const __nv_bfloat16*)p.O, (const __nv_bfloat16*)p.Olo, (const __nv_bfloat16*)p.dO, p.Dv, p.dQacc, (uint32_t)rows, (uint32_t)p.H, (uint32_t)p.Nq, p.dU,
             (uint32_t)n_du, p.token, p.token_val);

@@ -80,7 +80,8 @@ struct Lay {
     // column s holds ring slot s's per-key slab; A side one 1 KB atom of identical rows
     static constexpr uint32_t kOffSlabK = kOffE + 2 * kBox;  // 16 KB
     static constexpr uint32_t kOffSlabA = kOffSlabK + BN * 128;  // 1 KB
-    static constexpr uint32_t kOffLinv = kOffSlabA + 1024;    // [2 tiles][128] 1/l
+    static constexpr uint32_t kOffY = kOffSlabA + 1024;       // 8 KB: [128 rows][32 cols] bf16 Y box (C-27)
+    static constexpr uint32_t kOffLinv = kOffY + BM * 64;     // [2 tiles][128] 1/l
     static constexpr uint32_t kOffXch = kOffLinv + 2 * BM * 4;  // [2 tiles][2 parities][2 halves][128] row maxes
     static constexpr uint32_t kOffXchL = kOffXch + 8 * BM * 4;  // [2 tiles][128] half 1's row sum
     static constexpr uint32_t kOffBars = kOffXchL + 2 * BM * 4;
@@ -110,6 +111,12 @@ struct TcFwdParams {
     unsigned long long token_val;
     float sl2;  // scale * log2(e)
     float inv_scale;
+    // AttnLayer epilogue (reading C-27), active when ng_g is set
+    const __nv_bfloat16* ng_g;
+    const float* ng_gamma;
+    float* ng_rstd;
+    float ng_eps;
+    int64_t os[3];  // O's (= g's, Y's) element strides over (b, n, h)
 };
 
 #if GFWA_FWD_TRACE
@@ -184,7 +191,8 @@ template <int D, bool kF16P>  // training forward (O_lo wanted): P, V in fp16 fo
 __global__ void __launch_bounds__(kThreads, 1)
     fwd_tc_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
                   const __grid_constant__ CUtensorMap mv, const __grid_constant__ CUtensorMap mo,
-                  const __grid_constant__ CUtensorMap mol, const TcFwdParams p) {
+                  const __grid_constant__ CUtensorMap mol, const __grid_constant__ CUtensorMap my,
+                  const TcFwdParams p) {
     extern __shared__ __align__(1024) uint8_t smem[];
     using L = Lay<D>;
     constexpr uint32_t kTile = L::kTile, kOffQ = L::kOffQ, kOffKV = L::kOffKV, kOffE = L::kOffE,
@@ -597,6 +605,31 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint8_t* ehi = smem + kOffE;  // [O box | O_lo box] of one 64-column half
             const uint32_t sbf = smem_u32(ehi), sf = smem_u32(ehi + kBox);
             const uint32_t o_col = 256 + 128 * x;
+            const bool ng = p.ng_g != nullptr;
+            const int trow = it.r0 + x * BM + r;  // this thread's query row
+            const bool rvalid = trow < (int)p.Nq;
+            float rstd = 0.f;
+            const __nv_bfloat16* grow = nullptr;
+            if (ng) {
+                // AttnLayer epilogue (C-27): rstd = 1/sqrt(mean_c O_c^2 + eps) of
+                // the fp32 output row, one read pass over TMEM before the store rounds
+                float ss = 0.f;
+#pragma unroll 1
+                for (int cq = 0; cq < D / 32; ++cq) {
+                    uint32_t ob[32];
+                    tmem_ld32(lane_addr + o_col + 32 * cq, ob);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) {
+                        const float v = __uint_as_float(ob[e]) * inv;
+                        ss = fmaf(v, v, ss);
+                    }
+                }
+                rstd = rsqrtf(ss * (1.f / D) + p.ng_eps);
+                if (rvalid) p.ng_rstd[((int64_t)it.b * p.H + it.h) * p.Nq + trow] = rstd;
+                grow = p.ng_g + (int64_t)it.b * p.os[0] + (int64_t)(rvalid ? trow : 0) * p.os[1] +
+                       (int64_t)it.h * p.os[2];
+            }
             // four rounds of 32 columns: O (bf16) into the Q slot, O_lo into E; each
             // 64-column half is stored as soon as it is staged
 #pragma unroll 1
@@ -610,9 +643,32 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (lane == 0) mbar_arrive(&bars->o_free[x]);
                 }
                 const int hf = cq >> 1, cc = cq & 1;
-                if (cc == 0 && hf > 0) {  // the previous half's stores must have read the staging
+                if ((cc == 0 && hf > 0) || (ng && cq > 0)) {  // earlier stores must have read the staging
                     if (r == 0) bulk_wait_read0();
                     named_bar_sync(7, 128);
+                }
+                if (ng) {
+                    // Y = swish(g) * gamma * O * rstd for this round's 32 columns, staged in the
+                    // 64B-swizzled [128 rows][32 cols] Y box (sigmoid via tanh: one MUFU op)
+                    const uint32_t ybox = smem_u32(smem + L::kOffY) + r * 64;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const uint4 gq = __ldg(reinterpret_cast<const uint4*>(grow + 32 * cq) + k);
+                        const uint32_t* gw = &gq.x;
+                        uint32_t yw[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const float2 gam = __ldg(reinterpret_cast<const float2*>(p.ng_gamma + 32 * cq + 8 * k) + e);
+                            float g0, g1;
+                            f2unpack(bf2_to_f2(gw[e]), g0, g1);
+                            const float s0 = fmaf(0.5f, tanh_approx(0.5f * g0), 0.5f);
+                            const float s1 = fmaf(0.5f, tanh_approx(0.5f * g1), 0.5f);
+                            const float v0 = __uint_as_float(ob[8 * k + 2 * e]) * inv * rstd;
+                            const float v1 = __uint_as_float(ob[8 * k + 2 * e + 1]) * inv * rstd;
+                            yw[e] = pack_bf16x2(g0 * s0 * gam.x * v0, g1 * s1 * gam.y * v1);
+                        }
+                        sts128(ybox + ((k ^ ((r >> 1) & 3)) << 4), make_uint4(yw[0], yw[1], yw[2], yw[3]));
+                    }
                 }
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
@@ -633,13 +689,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                     sts128(sbf + off, make_uint4(hw[0], hw[1], hw[2], hw[3]));
                     if (p.store_lo) sts128(sf + off, make_uint4(lw[0], lw[1], lw[2], lw[3]));
                 }
-                if (cc == 1) {
+                if (cc == 1 || ng) {
                     fence_proxy_async();
                     named_bar_sync(7, 128);
                     if (r == 0) {
                         const int row0 = it.r0 + x * BM;
-                        tma_store_4d(&mo, ehi, hf * 64, it.h, row0, it.b);
-                        if (p.store_lo) tma_store_4d(&mol, ehi + kBox, hf * 64, it.h, row0, it.b);
+                        if (ng) tma_store_4d(&my, smem + L::kOffY, 32 * cq, it.h, row0, it.b);
+                        if (cc == 1) {
+                            tma_store_4d(&mo, ehi, hf * 64, it.h, row0, it.b);
+                            if (p.store_lo) tma_store_4d(&mol, ehi + kBox, hf * 64, it.h, row0, it.b);
+                        }
                         bulk_commit();
                     }
                 }
@@ -697,7 +756,7 @@ bool tc_fwd_supported(const AttnParams& p, gfwa_dtype_t dt) {
 
 template <int D>
 static gfwa_status_t tc_fwd_d(const AttnParams& p, cudaStream_t st) {
-    CUtensorMap mq, mk, mv, mo, mol;
+    CUtensorMap mq, mk, mv, mo, mol, my;
     GFWA_REQUIRE(encode_bnhd_map(&mq, p.Q, p.B, p.Nq, p.H, D, p.qs, BM));
     GFWA_REQUIRE(encode_bnhd_map(&mk, p.K, p.B, p.Nkv, p.H, D, p.ks, BN));
     GFWA_REQUIRE(encode_bnhd_map(&mv, p.V, p.B, p.Nkv, p.H, D, p.vs, BN));
@@ -706,6 +765,10 @@ static gfwa_status_t tc_fwd_d(const AttnParams& p, cudaStream_t st) {
         GFWA_REQUIRE(encode_bnhd_map(&mol, p.O_lo, p.B, p.Nq, p.H, D, p.os, BM));
     else
         mol = mo;  // unused
+    if (p.ng_g)
+        GFWA_REQUIRE(encode_bnhd_map_w32(&my, p.ng_Y, p.B, p.Nq, p.H, D, p.os, BM));
+    else
+        my = mo;  // unused
     TcFwdParams tp;
     tp.U = p.U;
     tp.LSE = p.LSE;
@@ -721,6 +784,11 @@ static gfwa_status_t tc_fwd_d(const AttnParams& p, cudaStream_t st) {
     tp.token_val = p.token_val;
     tp.sl2 = p.scale * kLog2e;
     tp.inv_scale = 1.f / p.scale;
+    tp.ng_g = (const __nv_bfloat16*)p.ng_g;
+    tp.ng_gamma = p.ng_gamma;
+    tp.ng_rstd = p.ng_rstd;
+    tp.ng_eps = p.ng_eps;
+    for (int i = 0; i < 3; ++i) tp.os[i] = p.os[i];
     tp.n_pairs = (int)((p.Nq + 2 * BM - 1) / (2 * BM));
     const int64_t n_items = (int64_t)tp.n_pairs * p.H * p.B;
     if (n_items >= ((int64_t)1 << 31) || p.Nkv + 2 * BM >= ((int64_t)1 << 31)) return GFWA_ERR_INVALID_ARGUMENT;
@@ -736,7 +804,7 @@ static gfwa_status_t tc_fwd_d(const AttnParams& p, cudaStream_t st) {
     int64_t cap = n_sm;
     if (const char* e = getenv("GFWA_FWD_GRID")) cap = max64(1, atoll(e));  // diagnostics: fewer CTAs, more items each
     const unsigned grid = (unsigned)min64(n_items, cap);
-    kern<<<grid, kThreads, kSmemBytes, st>>>(mq, mk, mv, mo, mol, tp);
+    kern<<<grid, kThreads, kSmemBytes, st>>>(mq, mk, mv, mo, mol, my, tp);
     note_launch();
     return check_launch();
 }

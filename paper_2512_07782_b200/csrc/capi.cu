@@ -1,3 +1,4 @@
+#include <initializer_list>
 // capi.cu -- argument validation, dispatch and helpers of the libgfwa C ABI
 // (include/gfwa.h).  No allocation, no synchronisation, no host reads of
 // device data; every launch goes onto the caller's stream.
@@ -57,6 +58,17 @@ struct Prepare {
     unsigned long long token_val = 0;
 };
 thread_local Prepare g_prepare;
+
+// gfwa_fwd_normgate / gfwa_bwd_normgate hand the AttnLayer epilogue (C-27) to the shared
+// gfwa_fwd / gfwa_bwd bodies (per thread)
+struct NormGate {
+    const gfwa_normgate_t* ng = nullptr;
+    void* Y = nullptr;         // forward output
+    const void* dY = nullptr;  // backward input
+    void* dg = nullptr;
+    float* dgamma = nullptr;
+};
+thread_local NormGate g_normgate;
 
 // per device (a process may drive several GPUs), race-free (relaxed atomics:
 // every thread computes the same value)
@@ -147,6 +159,14 @@ extern "C" gfwa_status_t gfwa_fwd(const gfwa_attn_desc_t* desc, const void* Q, c
     p.zero_acc = g_prepare.zero_acc;
     p.token = g_prepare.token;
     p.token_val = g_prepare.token_val;
+    if (g_normgate.ng) {  // gfwa_fwd_normgate (validated there; tensor-core path only)
+        if (!tc_fwd_supported(p, desc->dtype)) return GFWA_ERR_UNSUPPORTED;
+        p.ng_g = g_normgate.ng->g;
+        p.ng_gamma = g_normgate.ng->gamma;
+        p.ng_eps = g_normgate.ng->eps;
+        p.ng_rstd = g_normgate.ng->rstd;
+        p.ng_Y = g_normgate.Y;
+    }
     cudaStream_t st = (cudaStream_t)stream;
     gfwa_status_t s = tc_fwd_supported(p, desc->dtype) ? tc_fwd(p, st) : simt_fwd(p, desc->dtype, st);
     if (s != GFWA_OK || !check_finite_env()) return s;
@@ -243,6 +263,16 @@ extern "C" gfwa_status_t gfwa_bwd(const gfwa_attn_desc_t* desc, const void* Q, c
     p.dV = dV;
     p.dU = dU;
     p.Dv = (float*)((char*)ws + off_D);
+    if (g_normgate.ng) {  // gfwa_bwd_normgate: the fused epilogue backward replaces the preprocess
+        if (!tc_bwd_supported(p, desc->dtype)) return GFWA_ERR_UNSUPPORTED;
+        p.ng_g = g_normgate.ng->g;
+        p.ng_gamma = g_normgate.ng->gamma;
+        p.ng_eps = g_normgate.ng->eps;
+        p.ng_rstd = g_normgate.ng->rstd;
+        p.ng_dY = g_normgate.dY;
+        p.ng_dg = g_normgate.dg;
+        p.ng_dgamma = g_normgate.dgamma;
+    }
     cudaStream_t st = (cudaStream_t)stream;
     gfwa_status_t s;
     if (tc_bwd_supported(p, desc->dtype)) {
@@ -334,3 +364,54 @@ extern "C" void gfwa_debug_stage_events(void* const* events, int n) {
     for (int i = 0; i < 4; ++i) g_stage_ev[i] = (events && i < n) ? (cudaEvent_t)events[i] : nullptr;
 }
 extern "C" uint64_t gfwa_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+// ---------------------------------------------------------------------------
+// AttnLayer output epilogue (reading C-27)
+namespace {
+gfwa_status_t check_normgate(const gfwa_attn_desc_t* desc, const gfwa_normgate_t* ng, const void* O,
+                             const void* O_lo, std::initializer_list<const void*> bf16_rows) {
+    AttnParams p;
+    if (gfwa_status_t s = make_params(desc, p)) return s;
+    GFWA_REQUIRE(ng && ng->g && ng->gamma && ng->rstd && O);
+    GFWA_REQUIRE(ng->eps > 0.f && ng->eps == ng->eps);
+    if (desc->dtype != GFWA_BF16) return GFWA_ERR_UNSUPPORTED;
+    // every row tensor shares O's layout, which must be packed [B, N_q, H, d]
+    GFWA_REQUIRE(packed(p.os, p) && p.B * p.Nq * p.H < ((int64_t)1 << 31));
+    GFWA_REQUIRE(al16(ng->g) && al16(O) && (!O_lo || al16(O_lo)) && al16(ng->gamma));
+    for (const void* q : bf16_rows) GFWA_REQUIRE(q && al16(q));
+    return GFWA_OK;
+}
+}  // namespace
+
+extern "C" gfwa_status_t gfwa_fwd_normgate(const gfwa_attn_desc_t* desc, const void* Q, const void* K,
+                                           const void* V, const float* U, const gfwa_normgate_t* ng, void* O,
+                                           void* O_lo, float* LSE, void* Y, void* bwd_ws, size_t bwd_ws_bytes,
+                                           gfwa_stream_t stream) {
+    if (gfwa_status_t s = check_normgate(desc, ng, O, O_lo, {Y})) return s;
+    g_normgate = NormGate{};
+    g_normgate.ng = ng;
+    g_normgate.Y = Y;
+    const gfwa_status_t s = bwd_ws ? gfwa_fwd_train(desc, Q, K, V, U, O, O_lo, LSE, bwd_ws, bwd_ws_bytes, stream)
+                                   : gfwa_fwd(desc, Q, K, V, U, O, O_lo, LSE, stream);
+    g_normgate = NormGate{};
+    return s;
+}
+
+extern "C" gfwa_status_t gfwa_bwd_normgate(const gfwa_attn_desc_t* desc, const void* Q, const void* K,
+                                           const void* V, const float* U, const void* O, const void* O_lo,
+                                           const float* LSE, const gfwa_normgate_t* ng, const void* dY, void* dO,
+                                           void* dg, float* dgamma, void* dQ, void* dK, void* dV, float* dU,
+                                           float* dalpha, const double* dalpha_carry, void* ws, size_t ws_bytes,
+                                           gfwa_stream_t stream) {
+    if (gfwa_status_t s = check_normgate(desc, ng, O, O_lo, {dY, dO, dg})) return s;
+    GFWA_REQUIRE(dgamma);
+    g_normgate = NormGate{};
+    g_normgate.ng = ng;
+    g_normgate.dY = dY;
+    g_normgate.dg = dg;
+    g_normgate.dgamma = dgamma;
+    const gfwa_status_t s = gfwa_bwd(desc, Q, K, V, U, O, O_lo, LSE, dO, dQ, dK, dV, dU, dalpha, dalpha_carry, ws,
+                                     ws_bytes, stream);
+    g_normgate = NormGate{};
+    return s;
+}

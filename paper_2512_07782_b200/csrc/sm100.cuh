@@ -339,6 +339,11 @@ __device__ __forceinline__ void split3_bf16(float x, uint32_t& h, uint32_t& m, u
     m = __bfloat16_as_ushort(bm);
     l = __bfloat16_as_ushort(bl);
 }
+__device__ __forceinline__ float tanh_approx(float x) {
+    float y;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 __device__ __forceinline__ float ex2(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
