@@ -676,7 +676,58 @@ def run_aux(dev, peaks):
         "speedup_vs_pytorch": round(ms2 / ms, 2),
         "paper_context": ("A100 Triton: 1-pass 0.3 ms vs PyTorch 2.9 ms at N=64K (P:527); "
                           "1-pass ~28.5 vs Scan-Then-Propagate ~20.1 billion tokens/s (P:1061)")}
+    out["attn_layer_epilogue_C2"] = _attn_layer_epilogue(dev)
     return out
+
+
+def _attn_layer_epilogue(dev):
+    """the AttnLayer output epilogue (reading C-27: per-head
+    RMSNorm with weight gamma, then the swish gate) at C2, fused into the attention
+    kernels (gfwa_fwd_normgate + gfwa_bwd_normgate) vs the same math as separate
+    PyTorch ops around gfwa_fwd_train / gfwa_bwd (rms_norm * silu, autograd for its
+    backward).  Both: fwd + bwd of the layer from dY, inputs resident, eager."""
+    import torch
+    import torch.nn.functional as F
+
+    import synth
+    from paper_2512_07782_b200 import binding as gb
+
+    c = synth.CONFIGS["C2"]
+    s = synth.AttnShape(B=c["B"], H=c["H"], N=c["N"], d=c["d"], w=c["w"])
+    Q, K, V, dY = synth.attn_inputs(s, seed=c["seed"], device=dev, dtype=torch.bfloat16)
+    h, beta = synth.gate_inputs(s.B, s.N, s.H, seed=c["seed"], device=dev)
+    U = gb.gfwa_gate_prefix(h, beta)
+    g = torch.randn(s.B, s.N, s.H, s.d, device=dev).to(torch.bfloat16)
+    gamma = torch.ones(s.d, device=dev)
+
+    def fused():
+        Y, O, LSE, Olo, rstd = gb.gfwa_fwd_normgate(Q, K, V, U, g, gamma, s.w, prepare_bwd=True)
+        gb.gfwa_bwd_normgate(Q, K, V, U, O, LSE, g, gamma, rstd, dY, s.w, O_lo=Olo, want_dalpha=False)
+
+    def unfused():
+        O, LSE, Olo = gb.gfwa_fwd(Q, K, V, U, s.w, want_o_lo=True, prepare_bwd=True)
+        Ot = O.detach().requires_grad_(True)
+        gt = g.detach().requires_grad_(True)
+        gm = gamma.detach().requires_grad_(True)
+        Y = F.rms_norm(Ot, (s.d,), weight=gm, eps=1e-5) * F.silu(gt)
+        Y.backward(dY)
+        gb.gfwa_bwd(Q, K, V, U, O, LSE, Ot.grad, s.w, O_lo=Olo, want_dalpha=False)
+
+    res = {}
+    for name, fn in (("fused_ms", fused), ("unfused_torch_ms", unfused)):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(10):
+            fn()
+        e1.record()
+        torch.cuda.synchronize(dev)
+        res[name] = round(e0.elapsed_time(e1) / 10, 4)
+    res["speedup"] = round(res["unfused_torch_ms"] / res["fused_ms"], 3)
+    res["note"] = "layer fwd+bwd from dY at C2, eager; epilogue = RMSNorm(gamma) * swish(g) per head (C-27)"
+    return res
 
 
 # --------------------------------------------------------------------------- CPU oracle

@@ -46,14 +46,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // Wait with a suspend-time hint: the warp is parked until the phase completes
 // (or the 20 us hint expires) instead of re-issuing try_wait in a loop, so waiting
 // roles do not take issue slots from the working warps on the same SMSP.
+#ifndef GFWA_PARK_NS
+#define GFWA_PARK_NS 20000
+#endif
 __device__ __forceinline__ void mbar_wait_park(uint64_t* bar, uint32_t parity) {
+#if GFWA_PARK_NS == 0
+    mbar_wait(bar, parity);
+#else
     asm volatile(
         "{\n\t.reg .pred p;\n"
         "WAIT_%=:\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
         "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-        "r"(parity), "r"(20000)
+        "r"(parity), "r"(GFWA_PARK_NS)
         : "memory");
+#endif
 }
 
 // ------------------------------------------------------------------ TMA
