@@ -187,7 +187,9 @@ __device__ __forceinline__ Item make_item(const TcFwdParams& p, int idx) {
     return it;
 }
 
-template <int D, bool kF16P>  // training forward (O_lo wanted): P, V in fp16 for the PV product (reading C-23)
+// kF16P: training forward (O_lo wanted): P, V in fp16 for the PV product (reading C-23);
+// kNG: the AttnLayer epilogue (reading C-27) is fused into the store rounds
+template <int D, bool kF16P, bool kNG>
 __global__ void __launch_bounds__(kThreads, 1)
     fwd_tc_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
                   const __grid_constant__ CUtensorMap mv, const __grid_constant__ CUtensorMap mo,
@@ -605,7 +607,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint8_t* ehi = smem + kOffE;  // [O box | O_lo box] of one 64-column half
             const uint32_t sbf = smem_u32(ehi), sf = smem_u32(ehi + kBox);
             const uint32_t o_col = 256 + 128 * x;
-            const bool ng = p.ng_g != nullptr;
+            constexpr bool ng = kNG;
             const int trow = it.r0 + x * BM + r;  // this thread's query row
             const bool rvalid = trow < (int)p.Nq;
             float rstd = 0.f;
@@ -796,7 +798,8 @@ static gfwa_status_t tc_fwd_d(const AttnParams& p, cudaStream_t st) {
     int dev = 0, n_sm = 148;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
     // per launch: the attribute is per device (a process may drive several GPUs)
-    auto kern = tp.store_lo ? fwd_tc_kernel<D, true> : fwd_tc_kernel<D, false>;
+    auto kern = tp.ng_g ? (tp.store_lo ? fwd_tc_kernel<D, true, true> : fwd_tc_kernel<D, false, true>)
+                        : (tp.store_lo ? fwd_tc_kernel<D, true, false> : fwd_tc_kernel<D, false, false>);
     constexpr size_t kSmemBytes = Lay<D>::kSmemBytes;
     if (gfwa_status_t s = check_launch(
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes)))
