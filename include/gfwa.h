@@ -208,6 +208,24 @@ gfwa_status_t gfwa_bwd(const gfwa_attn_desc_t* desc, const void* Q, const void* 
                        const void* dO, void* dQ, void* dK, void* dV, float* dU, float* dalpha,
                        const double* dalpha_carry, void* ws, size_t ws_bytes, gfwa_stream_t stream);
 
+/*
+ * gfwa_bwd_rows_f32 -- gfwa_bwd that also writes fp32 copies of dK and dV (before
+ * their bf16 rounding) for the first head_rows and the last tail_rows key rows:
+ * dKV_head [2][B][head_rows][H][d] and dKV_tail [2][B][tail_rows][H][d] (dK in
+ * [0], dV in [1]; contiguous, 16-byte aligned).  Sequence sharding (SURVEY
+ * 8(e) step 2; BASELINE north_star): rank r's partial gradients of its w halo
+ * rows (its head rows) travel to rank r-1 in fp32 and are added there to that
+ * rank's fp32 tail rows, so the boundary rows are rounded to bf16 once.  The
+ * bf16 dK/dV of those rows are written as by gfwa_bwd.  Tensor-core path only
+ * (UNSUPPORTED otherwise); a count of 0 disables that side.
+ */
+gfwa_status_t gfwa_bwd_rows_f32(const gfwa_attn_desc_t* desc, const void* Q, const void* K, const void* V,
+                                const float* U, const void* O, const void* O_lo, const float* LSE,
+                                const void* dO, void* dQ, void* dK, void* dV, float* dU, float* dalpha,
+                                const double* dalpha_carry, int64_t head_rows, float* dKV_head,
+                                int64_t tail_rows, float* dKV_tail, void* ws, size_t ws_bytes,
+                                gfwa_stream_t stream);
+
 /* ------------------------------------------------------------------------- */
 /* AttnLayer output epilogue fused into the attention kernels:     */
 /*   O~ = concat_h norm(GatedFWA_h),  G = swish(linear(X)),  out = (G . O~) W_O */

@@ -99,6 +99,7 @@ EXPORTED = (
     "gfwa_attn_path",
     "gfwa_fwd_normgate",
     "gfwa_bwd_normgate",
+    "gfwa_bwd_rows_f32",
 )
 
 
@@ -135,6 +136,8 @@ def load() -> ctypes.CDLL:
         lib.gfwa_bwd_workspace_size.argtypes = [ctypes.POINTER(AttnDesc)]
         lib.gfwa_bwd.restype = ctypes.c_int
         lib.gfwa_bwd.argtypes = [ctypes.POINTER(AttnDesc)] + [_VP] * 15 + [sz, _VP]
+        lib.gfwa_bwd_rows_f32.restype = ctypes.c_int
+        lib.gfwa_bwd_rows_f32.argtypes = [ctypes.POINTER(AttnDesc)] + [_VP] * 14 + [_I64, _VP, _I64, _VP, _VP, sz, _VP]
         lib.gfwa_fwd_normgate.restype = ctypes.c_int
         lib.gfwa_fwd_normgate.argtypes = [ctypes.POINTER(AttnDesc)] + [_VP] * 4 + [ctypes.POINTER(NormGate)] + \
             [_VP] * 5 + [sz, _VP]
@@ -431,6 +434,36 @@ def gfwa_bwd_normgate(Q, K, V, U, O, LSE, g, gamma, rstd, dY, w: int, eps: float
                                nbytes, _stream(dev))
     _check(st, "gfwa_bwd_normgate")
     return dQ, dK, dV, dU, dalpha, dg, dgamma, dO
+
+
+def gfwa_bwd_rows_f32(Q, K, V, U, O, LSE, dO, w: int, head_rows: int, tail_rows: int,
+                      scale: float | None = None, O_lo=None):
+    """gfwa_bwd plus fp32 copies [2 (dK, dV), B, rows, H, d] of dK, dV for the first
+    head_rows and last tail_rows key rows (sequence sharding: the halo's partial
+    gradients travel and are added in fp32).  Returns (dQ, dK, dV, dU, head, tail)."""
+    lib = load()
+    _need_cuda(Q, K, V, U, O, LSE, dO)
+    if dO.stride() != O.stride() or (O_lo is not None and O_lo.stride() != O.stride()):
+        O, dO = O.contiguous(), dO.contiguous()
+        O_lo = None if O_lo is None else O_lo.contiguous()
+    B, Nq, H, d = Q.shape
+    Nkv = K.shape[1]
+    dev = Q.device
+    dQ = torch.empty_strided(Q.shape, Q.stride(), dtype=Q.dtype, device=dev)
+    dK = torch.empty_strided(K.shape, K.stride(), dtype=K.dtype, device=dev)
+    dV = torch.empty_strided(V.shape, V.stride(), dtype=V.dtype, device=dev)
+    dU = torch.empty(B, H, Nkv, dtype=torch.float32, device=dev)
+    head = torch.empty(2, B, head_rows, H, d, dtype=torch.float32, device=dev) if head_rows > 0 else None
+    tail = torch.empty(2, B, tail_rows, H, d, dtype=torch.float32, device=dev) if tail_rows > 0 else None
+    dsc = make_desc(Q, K, V, O, w, scale)
+    nbytes = lib.gfwa_bwd_workspace_size(ctypes.byref(dsc))
+    ws = workspace(nbytes, dev, "bwd")
+    st = lib.gfwa_bwd_rows_f32(ctypes.byref(dsc), _ptr(Q), _ptr(K), _ptr(V), _ptr(U.contiguous()), _ptr(O),
+                               _ptr(O_lo), _ptr(LSE), _ptr(dO), _ptr(dQ), _ptr(dK), _ptr(dV), _ptr(dU), None, None,
+                               int(head_rows), _ptr(head), int(tail_rows), _ptr(tail), _ptr(ws), nbytes,
+                               _stream(dev))
+    _check(st, "gfwa_bwd_rows_f32")
+    return dQ, dK, dV, dU, head, tail
 
 
 def gfwa_attn_path(Q, K, V, w: int) -> int:

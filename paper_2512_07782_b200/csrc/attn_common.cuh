@@ -44,6 +44,10 @@ struct AttnParams {
     void* ng_dg;           // backward output
     float* ng_dgamma;      // backward output [d] (zeroed and accumulated by the call)
     bool pre_done;         // backward: D, dO and the zeroing came from the fused epilogue pre kernel
+    // sequence sharding: fp32 copies of dK, dV of the first / last key rows ([2][B][rows][H][d])
+    float* f32_head;
+    float* f32_tail;
+    int64_t f32_head_rows, f32_tail_rows;
 };
 
 // token marking a backward workspace whose dQ accumulator the forward already zeroed

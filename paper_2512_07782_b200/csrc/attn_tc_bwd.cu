@@ -95,6 +95,12 @@ struct TcBwdParams {
     int64_t Nq, Nkv, h0, H;
     int w;
     int n_kt, n_items;  // key tiles per (b, h); work items = key tiles x H x B
+    int64_t B;
+    // sequence sharding: fp32 copies of dK, dV for the first head_rows
+    // and the last tail_rows key rows, [2 (dK, dV)][B][rows][H][d] (null: none)
+    float* f32_head;
+    float* f32_tail;
+    int64_t head_rows, tail_rows;
     float sl2, scale, inv_scale;
     unsigned long long* token;  // prepared-workspace token: consumed (cleared) by this kernel
 };
@@ -175,7 +181,8 @@ __device__ __forceinline__ BItem make_bitem(const TcBwdParams& p, int idx) {
 }
 
 // Persistent: one CTA per SM walks work items idx = blockIdx.x + k * gridDim.x.
-template <int D>
+// kRows: also write the fp32 copies of the boundary rows' dK, dV (sequence sharding)
+template <int D, bool kRows>
 __global__ void __launch_bounds__(kThreads, 1)
     bwd_tc_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
                   const __grid_constant__ CUtensorMap mv, const __grid_constant__ CUtensorMap mdo,
@@ -599,6 +606,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                 dst[k] = o;
             }
         };
+        // key j's row in the fp32 head / tail copy (the epilogue's tsr 0 is dV, 1 is dK; the
+        // buffers hold [dK, dV]), or null when j is outside that range
+        auto f32_row = [&](const BItem& it, int64_t j, int tsr, bool tail = false) -> float* {
+            float* base = tail ? p.f32_tail : p.f32_head;
+            const int64_t rows = tail ? p.tail_rows : p.head_rows;
+            const int64_t r = tail ? j - (p.Nkv - p.tail_rows) : j;
+            if (!base || r < 0 || r >= rows || j >= p.Nkv) return nullptr;
+            const int64_t which = tsr ? 0 : 1;  // dK first, then dV
+            return base + (((which * p.B + it.b) * rows + r) * p.H + it.h) * D;
+        };
         Pool pool;  // replica of the slot rotation (the epilogue stages in the item's K slot)
         int g = 0, nitem = 0, pg = -1;
         int64_t pt0 = 0, pbh = 0;
@@ -617,6 +634,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                         store_row(dvrow, z, c, 1.f);
                         store_row(dkrow, z, c, 1.f);
                     }
+#pragma unroll 1
+                    for (int tsr = 0; tsr < 2 && kRows; ++tsr)
+                        for (int c = 0; c < D; c += 4) {
+                            if (float* f = f32_row(it, j, tsr)) *reinterpret_cast<float4*>(f + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+                            if (float* f = f32_row(it, j, tsr, true)) *reinterpret_cast<float4*>(f + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+                        }
                 }
                 continue;
             }
@@ -698,6 +721,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                         tc_fence_before();
                         __syncwarp();
                         if (lane == 0) mbar_arrive(&bars->dkdv_free);
+                    }
+                    if (kRows) {  // the boundary rows' fp32 copies (sequence sharding)
+#pragma unroll 1
+                        for (int ht = 0; ht < 2; ++ht)
+                            if (float* f = f32_row(it, j, tsr, ht == 1)) {
+                                f += 64 * hf;
+#pragma unroll
+                                for (int e = 0; e < 32; e += 4) {
+                                    *reinterpret_cast<float4*>(f + e) =
+                                        make_float4(__uint_as_float(a[e]) * mul, __uint_as_float(a[e + 1]) * mul,
+                                                    __uint_as_float(a[e + 2]) * mul, __uint_as_float(a[e + 3]) * mul);
+                                    *reinterpret_cast<float4*>(f + 32 + e) =
+                                        make_float4(__uint_as_float(b[e]) * mul, __uint_as_float(b[e + 1]) * mul,
+                                                    __uint_as_float(b[e + 2]) * mul, __uint_as_float(b[e + 3]) * mul);
+                                }
+                            }
                     }
                     const uint32_t row = stg + hf * 4096 + lane * 128;  // 128B swizzle: chunk ^ (key % 8)
 #pragma unroll
@@ -1074,18 +1113,27 @@ static gfwa_status_t tc_bwd_d(const AttnParams& pin, cudaStream_t st, void* ws) 
         tp.vs[i] = p.vs[i];
     }
     tp.n_kt = (int)((p.Nkv + BN - 1) / BN);
+    tp.B = p.B;
+    tp.f32_head = p.f32_head;
+    tp.f32_tail = p.f32_tail;
+    tp.head_rows = p.f32_head_rows;
+    tp.tail_rows = p.f32_tail_rows;
     const int64_t n_items = (int64_t)tp.n_kt * p.H * p.B;
     if (n_items >= ((int64_t)1 << 31)) return GFWA_ERR_INVALID_ARGUMENT;
     tp.n_items = (int)n_items;
     // per launch: the attribute is per device (a process may drive several GPUs)
     constexpr size_t kSmemBytes = smem_bytes<D>();
     if (gfwa_status_t s = check_launch(
-            cudaFuncSetAttribute(bwd_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes)))
+            cudaFuncSetAttribute(bwd_tc_kernel<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes)))
+        return s;
+    if (gfwa_status_t s = check_launch(
+            cudaFuncSetAttribute(bwd_tc_kernel<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes)))
         return s;
     int64_t cap = n_sm;  // persistent: one CTA per SM
     if (const char* e = getenv("GFWA_BWD_GRID")) cap = max64(1, atoll(e));  // diagnostics: fewer CTAs, more items each
     const unsigned grid = (unsigned)min64(n_items, cap);
-    bwd_tc_kernel<D><<<grid, kThreads, kSmemBytes, st>>>(mq, mk, mv, mdo, mdk, mdv, mdq, tp);
+    auto kern = (tp.f32_head || tp.f32_tail) ? bwd_tc_kernel<D, true> : bwd_tc_kernel<D, false>;
+    kern<<<grid, kThreads, kSmemBytes, st>>>(mq, mk, mv, mdo, mdk, mdv, mdq, tp);
     note_launch();
     if (gfwa_status_t s = check_launch()) return s;
     stage_event(1, st);  // measurement hook: after the main kernel

@@ -70,6 +70,14 @@ struct NormGate {
 };
 thread_local NormGate g_normgate;
 
+// gfwa_bwd_rows_f32 hands its fp32 boundary-row outputs to the shared gfwa_bwd body
+struct RowsF32 {
+    float* head = nullptr;
+    float* tail = nullptr;
+    int64_t head_rows = 0, tail_rows = 0;
+};
+thread_local RowsF32 g_rows;
+
 // per device (a process may drive several GPUs), race-free (relaxed atomics:
 // every thread computes the same value)
 constexpr int kMaxDev = 64;
@@ -273,6 +281,14 @@ extern "C" gfwa_status_t gfwa_bwd(const gfwa_attn_desc_t* desc, const void* Q, c
         p.ng_dg = g_normgate.dg;
         p.ng_dgamma = g_normgate.dgamma;
     }
+    if (g_rows.head || g_rows.tail) {  // gfwa_bwd_rows_f32 (tensor-core path only)
+        if (!tc_bwd_supported(p, desc->dtype)) return GFWA_ERR_UNSUPPORTED;
+        GFWA_REQUIRE(g_rows.head_rows <= p.Nkv && g_rows.tail_rows <= p.Nkv);
+        p.f32_head = g_rows.head_rows > 0 ? g_rows.head : nullptr;
+        p.f32_tail = g_rows.tail_rows > 0 ? g_rows.tail : nullptr;
+        p.f32_head_rows = g_rows.head_rows;
+        p.f32_tail_rows = g_rows.tail_rows;
+    }
     cudaStream_t st = (cudaStream_t)stream;
     gfwa_status_t s;
     if (tc_bwd_supported(p, desc->dtype)) {
@@ -413,5 +429,26 @@ extern "C" gfwa_status_t gfwa_bwd_normgate(const gfwa_attn_desc_t* desc, const v
     const gfwa_status_t s = gfwa_bwd(desc, Q, K, V, U, O, O_lo, LSE, dO, dQ, dK, dV, dU, dalpha, dalpha_carry, ws,
                                      ws_bytes, stream);
     g_normgate = NormGate{};
+    return s;
+}
+
+// sequence sharding: gfwa_bwd plus fp32 copies of the boundary rows' dK, dV
+extern "C" gfwa_status_t gfwa_bwd_rows_f32(const gfwa_attn_desc_t* desc, const void* Q, const void* K,
+                                           const void* V, const float* U, const void* O, const void* O_lo,
+                                           const float* LSE, const void* dO, void* dQ, void* dK, void* dV,
+                                           float* dU, float* dalpha, const double* dalpha_carry,
+                                           int64_t head_rows, float* dKV_head, int64_t tail_rows, float* dKV_tail,
+                                           void* ws, size_t ws_bytes, gfwa_stream_t stream) {
+    GFWA_REQUIRE(head_rows >= 0 && tail_rows >= 0);
+    GFWA_REQUIRE((head_rows == 0 || dKV_head) && (tail_rows == 0 || dKV_tail));
+    GFWA_REQUIRE((!dKV_head || al16(dKV_head)) && (!dKV_tail || al16(dKV_tail)));
+    g_rows = RowsF32{};
+    g_rows.head = dKV_head;
+    g_rows.tail = dKV_tail;
+    g_rows.head_rows = head_rows;
+    g_rows.tail_rows = tail_rows;
+    const gfwa_status_t s = gfwa_bwd(desc, Q, K, V, U, O, O_lo, LSE, dO, dQ, dK, dV, dU, dalpha, dalpha_carry, ws,
+                                     ws_bytes, stream);
+    g_rows = RowsF32{};
     return s;
 }

@@ -41,6 +41,11 @@ class Ops:
     # (Q, K, V, U, w, O_out, Olo_out | None) -> LSE: the forward written into caller views
     # (lets the step run the interior queries while the halo is in flight); None: no split
     fwd_into: Callable | None = None
+    # (Q, K, V, U, O, LSE, dO, w, O_lo, head_rows, tail_rows) -> (dQ, dK, dV, dU, head, tail):
+    # bwd plus pre-rounding copies [2 (dK, dV), B, rows, H, d] of the first / last key rows'
+    # dK, dV, so the halo gradients travel and are added before their one rounding
+    # (fp32).  None: the halo rows travel in the gradients' dtype
+    bwd_rows: Callable | None = None
 
 
 def cuda_ops() -> Ops:
@@ -62,8 +67,13 @@ def cuda_ops() -> Ops:
     def _fwd_into(Q, K, V, U, w, O_out, Olo_out):
         return gb.gfwa_fwd(Q, K, V, U, w, out=O_out, out_lo=Olo_out)[1]
 
+    def _bwd_rows(Q, K, V, U, O, LSE, dO, w, Olo, head_rows, tail_rows):
+        if Q.dtype != torch.bfloat16:  # the fp32 parity path is exact: nothing to carry
+            return (*_bwd(Q, K, V, U, O, LSE, dO, w, Olo), None, None)
+        return gb.gfwa_bwd_rows_f32(Q, K, V, U, O, LSE, dO, w, head_rows, tail_rows, O_lo=Olo)
+
     return Ops(gate_prefix=lambda h, b, eps: gb.gfwa_gate_prefix(h, b, eps, want_total=True), fwd=_fwd, bwd=_bwd,
-               gate_bwd=_gate_bwd, fwd_into=_fwd_into)
+               gate_bwd=_gate_bwd, fwd_into=_fwd_into, bwd_rows=_bwd_rows)
 
 
 class Ring:
@@ -221,10 +231,25 @@ def sp_forward_backward(Q, K, V, h, beta, dO, w: int, ops: Ops, ring: Ring, eps:
                                     O[:, :w], None if Olo is None else Olo[:, :w])
     else:
         O, LSE, Olo = ops.fwd(Q, Kx, Vx, Ux, w)
-    dQ, dKx, dVx, dUx = ops.bwd(Q, Kx, Vx, Ux, O, LSE, dO, w, Olo)
-    # backward halo r -> r-1: gradients of the halo rows
-    back_like = [dKx[:, :w], dVx[:, :w], dUx[..., :w]]
-    back = ring.shift([t.contiguous() for t in back_like] if h0 else None, back_like, forward=False)
+    tail_rows = w if r < P - 1 else 0
+    head = tail = None
+    if ops.bwd_rows is not None:
+        dQ, dKx, dVx, dUx, head, tail = ops.bwd_rows(Q, Kx, Vx, Ux, O, LSE, dO, w, Olo, h0, tail_rows)
+    else:
+        dQ, dKx, dVx, dUx = ops.bwd(Q, Kx, Vx, Ux, O, LSE, dO, w, Olo)
+    # backward halo r -> r-1: gradients of the halo rows (dK, dV before their rounding when
+    # the backend provides them: [2, B, w, H, d] fp32)
+    # (every rank of a run takes the same branch: the same backend and dtype on all ranks)
+    exact = ops.bwd_rows is not None and (head is not None or tail is not None)
+    if exact:
+        ref = tail if tail is not None else head
+        back_like = [torch.empty(2, dKx.shape[0], w, dKx.shape[2], dKx.shape[3], dtype=ref.dtype,
+                                 device=dKx.device), dUx[..., :w]]
+        send = [head, dUx[..., :w].contiguous()] if h0 else None
+    else:
+        back_like = [dKx[:, :w], dVx[:, :w], dUx[..., :w]]
+        send = [t.contiguous() for t in back_like] if h0 else None
+    back = ring.shift(send, back_like, forward=False)
     if kv_ext is not None:
         dK, dV = dKx[:, h0:], dVx[:, h0:]  # views: no copy of the S local rows
     else:
@@ -233,10 +258,16 @@ def sp_forward_backward(Q, K, V, h, beta, dO, w: int, ops: Ops, ring: Ring, eps:
     dU = dUx[..., h0:].contiguous()
     carry = None
     if back is not None:
-        dK[:, S - w:] += back[0]
-        dV[:, S - w:] += back[1]
-        dU[..., S - w:] += back[2]
-        carry = back[2].double().sum(-1)  # d-alpha carry = +sum_j dU_halo(j)
+        if exact:  # own partial + received partial, both before rounding, rounded once
+            dK[:, S - w:] = (tail[0] + back[0][0]).to(dK.dtype)
+            dV[:, S - w:] = (tail[1] + back[0][1]).to(dV.dtype)
+            dU_halo = back[1]
+        else:
+            dK[:, S - w:] += back[0]
+            dV[:, S - w:] += back[1]
+            dU_halo = back[2]
+        dU[..., S - w:] += dU_halo
+        carry = dU_halo.double().sum(-1)  # d-alpha carry = +sum_j dU_halo(j)
     dalpha, dh, dbeta = ops.gate_bwd(dU, h, beta, eps, carry)
     U_offset = global_offset_finish(scan, ring) if scan is not None else torch.zeros_like(total, dtype=torch.float64)
     return ShardResult(O, LSE, U_loc, dQ, dK, dV, dalpha, dh, dbeta, dU, U_offset)

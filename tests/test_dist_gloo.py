@@ -17,7 +17,7 @@ import torch.multiprocessing as mp
 import oracle
 
 
-def _oracle_ops():
+def _oracle_ops(rows: bool = False):
     from paper_2512_07782_b200.dist import Ops
 
     t = lambda a: torch.from_numpy(np.asarray(a))  # noqa: E731
@@ -44,7 +44,15 @@ def _oracle_ops():
         O_out.copy_(t(O))
         return t(L)
 
-    return Ops(gate_prefix=gate_prefix, fwd=fwd, bwd=bwd, gate_bwd=gate_bwd, fwd_into=fwd_into)
+    def bwd_rows(Q, K, V, U, O, LSE, dO, w, Olo, head_rows, tail_rows):
+        dQ, dK, dV, dU = bwd(Q, K, V, U, O, LSE, dO, w, Olo)
+        n = dK.shape[1]
+        head = torch.stack([dK[:, :head_rows], dV[:, :head_rows]]).contiguous() if head_rows else None
+        tail = torch.stack([dK[:, n - tail_rows:], dV[:, n - tail_rows:]]).contiguous() if tail_rows else None
+        return dQ, dK, dV, dU, head, tail
+
+    return Ops(gate_prefix=gate_prefix, fwd=fwd, bwd=bwd, gate_bwd=gate_bwd, fwd_into=fwd_into,
+               bwd_rows=bwd_rows if rows else None)
 
 
 def _inputs(B, N, H, d, seed):
@@ -58,7 +66,7 @@ def _inputs(B, N, H, d, seed):
     return Q, K, V, dO, h, beta
 
 
-def _worker(rank, world, port, outdir, B, N, H, d, w, use_ext=False):
+def _worker(rank, world, port, outdir, B, N, H, d, w, use_ext=False, rows=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -71,7 +79,7 @@ def _worker(rank, world, port, outdir, B, N, H, d, w, use_ext=False):
         Kl, Vl, kv_ext = K[:, sl], V[:, sl], None
         if use_ext:  # [halo; local] buffers: the halo lands in place, no per-step concatenation
             kv_ext, Kl, Vl = alloc_kv_ext(Kl, Vl, w)
-        res = sp_forward_backward(Q[:, sl], Kl, Vl, h[:, sl], beta[:, sl], dO[:, sl], w, _oracle_ops(),
+        res = sp_forward_backward(Q[:, sl], Kl, Vl, h[:, sl], beta[:, sl], dO[:, sl], w, _oracle_ops(rows),
                                   Ring(), kv_ext=kv_ext)
         torch.save({k: getattr(res, k) for k in ("O", "LSE", "U_loc", "U_offset", "dQ", "dK", "dV", "dalpha", "dh",
                                                  "dbeta")},
@@ -80,13 +88,16 @@ def _worker(rank, world, port, outdir, B, N, H, d, w, use_ext=False):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,N,w,use_ext", [(2, 48, 10, False), (2, 40, 20, False), (3, 60, 7, False),
-                                               (2, 48, 10, True), (3, 60, 7, True)])
-def test_sequence_sharded_matches_unsharded(world, N, w, use_ext):
+@pytest.mark.parametrize("world,N,w,use_ext,rows", [(2, 48, 10, False, False), (2, 40, 20, False, False),
+                                                    (3, 60, 7, False, False), (2, 48, 10, True, False),
+                                                    (3, 60, 7, True, False),
+                                                    # halo dK/dV as pre-rounding [2, B, w, H, d] copies
+                                                    (2, 48, 10, True, True), (3, 60, 7, False, True)])
+def test_sequence_sharded_matches_unsharded(world, N, w, use_ext, rows):
     B, H, d = 1, 2, 8
-    port = 29500 + (os.getpid() % 2000) + (7 if use_ext else 0)
+    port = 29500 + (os.getpid() % 2000) + (7 if use_ext else 0) + (13 if rows else 0)
     with tempfile.TemporaryDirectory() as outdir:
-        mp.spawn(_worker, args=(world, port, outdir, B, N, H, d, w, use_ext), nprocs=world, join=True)
+        mp.spawn(_worker, args=(world, port, outdir, B, N, H, d, w, use_ext, rows), nprocs=world, join=True)
         Q, K, V, dO, h, beta = _inputs(B, N, H, d, 5)
         U, _, _ = oracle.gate_prefix_hbeta(h, beta)
         O, L = oracle.fwd(Q, K, V, U, w)

@@ -330,3 +330,24 @@ def test_persistent_kernels_many_items_per_cta(d, monkeypatch):
         if s.nkv > s.N + s.w:  # keys before the first query's window: exact zeros
             dead = s.nkv - s.N - s.w + 1
             assert torch.count_nonzero(got["dK"][:, :dead]) == 0 and torch.count_nonzero(got["dV"][:, :dead]) == 0
+
+
+def test_bwd_rows_f32_boundary_copies():
+    """gfwa_bwd_rows_f32 (sequence sharding): the fp32 copies of the
+    first / last key rows' dK, dV are the values the bf16 outputs were rounded from
+    (they round to them exactly) and match the oracle within the bf16 budget."""
+    s = synth.AttnShape(B=2, H=2, N=400, d=128, w=150, N_kv=400 + 150)
+    Q, K, V, dO = synth.attn_inputs(s, seed=71, dtype=torch.bfloat16)
+    U = _U(s.B, s.H, s.nkv, 72)
+    Qd, Kd, Vd, dOd, Ud = (x.cuda() for x in (Q, K, V, dO, U))
+    O, LSE, Olo = gb.gfwa_fwd(Qd, Kd, Vd, Ud, s.w, want_o_lo=True)
+    dQ, dK, dV, dU, head, tail = gb.gfwa_bwd_rows_f32(Qd, Kd, Vd, Ud, O, LSE, dOd, s.w, s.w, s.w, O_lo=Olo)
+    dQ2, dK2, dV2, dU2, _ = gb.gfwa_bwd(Qd, Kd, Vd, Ud, O, LSE, dOd, s.w, O_lo=Olo)
+    torch.cuda.synchronize()
+    assert torch.equal(dK, dK2) and torch.equal(dV, dV2) and torch.equal(dQ, dQ2)
+    w = s.w
+    for buf, rows in ((head, slice(0, w)), (tail, slice(s.nkv - w, s.nkv))):
+        assert torch.equal(buf[0].to(torch.bfloat16), dK[:, rows])
+        assert torch.equal(buf[1].to(torch.bfloat16), dV[:, rows])
+    g = oracle.bwd(Q, K, V, U, dO, s.w)
+    assert max_abs(head[0], g["dK"][:, :w]) <= TOL_BF16_GRAD and max_abs(tail[1], g["dV"][:, -w:]) <= TOL_BF16_GRAD

@@ -1,0 +1,5 @@
+for i in 1 2; do for v in default order2; do
+  if [ $v = default ]; then L=""; else L=paper_2512_07782_b200/variants/libgfwa_$v.so; fi
+  for W in C2 C3_w512; do GFWA_LIB=$L timeout 120 python tools/time_kernels.py $W bwd 2>&1 | tail -1; done
+done; done
+GFWA_LIB=paper_2512_07782_b200/variants/libgfwa_order2.so timeout 600 python -m pytest tests/test_gpu_attn.py -x -q -k "bf16 or many" 2>&1 | tail -2
