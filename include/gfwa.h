@@ -244,10 +244,15 @@ typedef struct {
 
 /*
  * gfwa_fwd_normgate -- gfwa_fwd (bwd_ws == NULL) or gfwa_fwd_train (bwd_ws given)
- * whose epilogue also writes Y [B,N_q,H,d] bf16 (O's layout) and rstd from the
- * fp32 attention output in registers: the normalised, gated layer output never
- * makes a round trip through HBM as O.  O (the attention output O~, needed by
- * the backward) and O_lo are still written.  BF16 tensor-core path only
+ * whose epilogue also takes rstd from the fp32 attention output in TMEM (one
+ * extra read pass before the output is released), followed by one streaming
+ * pass that writes Y [B,N_q,H,d] bf16 (O's layout) from O + O_lo (the fp32
+ * output to ~2^-17; O alone when O_lo is NULL), g and gamma: the layer output
+ * in one pass over the rows instead of an RMSNorm and a gate kernel chain.
+ * O (the attention output O~, needed by the backward) and O_lo are written as
+ * by gfwa_fwd.  (Computing Y inside the forward's epilogue warps was measured
+ * slower: their global traffic delays the release of the output accumulator.)
+ * BF16 tensor-core path only
  * (UNSUPPORTED otherwise); O's layout must be packed [B,N_q,H,d]
  * (INVALID_ARGUMENT otherwise); g, Y 16-byte aligned.
  */

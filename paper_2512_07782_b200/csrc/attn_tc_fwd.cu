@@ -80,8 +80,7 @@ struct Lay {
     // column s holds ring slot s's per-key slab; A side one 1 KB atom of identical rows
     static constexpr uint32_t kOffSlabK = kOffE + 2 * kBox;  // 16 KB
     static constexpr uint32_t kOffSlabA = kOffSlabK + BN * 128;  // 1 KB
-    static constexpr uint32_t kOffY = kOffSlabA + 1024;       // 8 KB: [128 rows][32 cols] bf16 Y box (C-27)
-    static constexpr uint32_t kOffLinv = kOffY + BM * 64;     // [2 tiles][128] 1/l
+    static constexpr uint32_t kOffLinv = kOffSlabA + 1024;    // [2 tiles][128] 1/l
     static constexpr uint32_t kOffXch = kOffLinv + 2 * BM * 4;  // [2 tiles][2 parities][2 halves][128] row maxes
     static constexpr uint32_t kOffXchL = kOffXch + 8 * BM * 4;  // [2 tiles][128] half 1's row sum
     static constexpr uint32_t kOffBars = kOffXchL + 2 * BM * 4;
@@ -113,6 +112,7 @@ struct TcFwdParams {
     float inv_scale;
     // AttnLayer epilogue (reading C-27), active when ng_g is set
     const __nv_bfloat16* ng_g;
+    __nv_bfloat16* ng_Y;
     const float* ng_gamma;
     float* ng_rstd;
     float ng_eps;
@@ -193,8 +193,7 @@ template <int D, bool kF16P, bool kNG>
 __global__ void __launch_bounds__(kThreads, 1)
     fwd_tc_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
                   const __grid_constant__ CUtensorMap mv, const __grid_constant__ CUtensorMap mo,
-                  const __grid_constant__ CUtensorMap mol, const __grid_constant__ CUtensorMap my,
-                  const TcFwdParams p) {
+                  const __grid_constant__ CUtensorMap mol, const TcFwdParams p) {
     extern __shared__ __align__(1024) uint8_t smem[];
     using L = Lay<D>;
     constexpr uint32_t kTile = L::kTile, kOffQ = L::kOffQ, kOffKV = L::kOffKV, kOffE = L::kOffE,
@@ -611,7 +610,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int trow = it.r0 + x * BM + r;  // this thread's query row
             const bool rvalid = trow < (int)p.Nq;
             float rstd = 0.f;
-            const __nv_bfloat16* grow = nullptr;
             if (ng) {
                 // AttnLayer epilogue (C-27): rstd = 1/sqrt(mean_c O_c^2 + eps) of
                 // the fp32 output row, one read pass over TMEM before the store rounds
@@ -629,8 +627,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 rstd = rsqrtf(ss * (1.f / D) + p.ng_eps);
                 if (rvalid) p.ng_rstd[((int64_t)it.b * p.H + it.h) * p.Nq + trow] = rstd;
-                grow = p.ng_g + (int64_t)it.b * p.os[0] + (int64_t)(rvalid ? trow : 0) * p.os[1] +
-                       (int64_t)it.h * p.os[2];
             }
             // four rounds of 32 columns: O (bf16) into the Q slot, O_lo into E; each
             // 64-column half is stored as soon as it is staged
@@ -645,32 +641,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (lane == 0) mbar_arrive(&bars->o_free[x]);
                 }
                 const int hf = cq >> 1, cc = cq & 1;
-                if ((cc == 0 && hf > 0) || (ng && cq > 0)) {  // earlier stores must have read the staging
+                if (cc == 0 && hf > 0) {  // the previous half's stores must have read the staging
                     if (r == 0) bulk_wait_read0();
                     named_bar_sync(7, 128);
-                }
-                if (ng) {
-                    // Y = swish(g) * gamma * O * rstd for this round's 32 columns, staged in the
-                    // 64B-swizzled [128 rows][32 cols] Y box (sigmoid via tanh: one MUFU op)
-                    const uint32_t ybox = smem_u32(smem + L::kOffY) + r * 64;
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const uint4 gq = __ldg(reinterpret_cast<const uint4*>(grow + 32 * cq) + k);
-                        const uint32_t* gw = &gq.x;
-                        uint32_t yw[4];
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const float2 gam = __ldg(reinterpret_cast<const float2*>(p.ng_gamma + 32 * cq + 8 * k) + e);
-                            float g0, g1;
-                            f2unpack(bf2_to_f2(gw[e]), g0, g1);
-                            const float s0 = fmaf(0.5f, tanh_approx(0.5f * g0), 0.5f);
-                            const float s1 = fmaf(0.5f, tanh_approx(0.5f * g1), 0.5f);
-                            const float v0 = __uint_as_float(ob[8 * k + 2 * e]) * inv * rstd;
-                            const float v1 = __uint_as_float(ob[8 * k + 2 * e + 1]) * inv * rstd;
-                            yw[e] = pack_bf16x2(g0 * s0 * gam.x * v0, g1 * s1 * gam.y * v1);
-                        }
-                        sts128(ybox + ((k ^ ((r >> 1) & 3)) << 4), make_uint4(yw[0], yw[1], yw[2], yw[3]));
-                    }
                 }
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
@@ -691,16 +664,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                     sts128(sbf + off, make_uint4(hw[0], hw[1], hw[2], hw[3]));
                     if (p.store_lo) sts128(sf + off, make_uint4(lw[0], lw[1], lw[2], lw[3]));
                 }
-                if (cc == 1 || ng) {
+                if (cc == 1) {
                     fence_proxy_async();
                     named_bar_sync(7, 128);
                     if (r == 0) {
                         const int row0 = it.r0 + x * BM;
-                        if (ng) tma_store_4d(&my, smem + L::kOffY, 32 * cq, it.h, row0, it.b);
-                        if (cc == 1) {
-                            tma_store_4d(&mo, ehi, hf * 64, it.h, row0, it.b);
-                            if (p.store_lo) tma_store_4d(&mol, ehi + kBox, hf * 64, it.h, row0, it.b);
-                        }
+                        tma_store_4d(&mo, ehi, hf * 64, it.h, row0, it.b);
+                        if (p.store_lo) tma_store_4d(&mol, ehi + kBox, hf * 64, it.h, row0, it.b);
                         bulk_commit();
                     }
                 }
@@ -739,6 +709,59 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
+// AttnLayer epilogue, second half (reading C-27): Y = swish(g) gamma (O + O_lo)
+// rstd, one streaming pass over the rows the forward just wrote (rstd came from the
+// forward's epilogue, taken on the fp32 output in TMEM).  Packed [rows, D] layouts; a
+// warp takes 32 / (D / 8) rows per load group (16 B per lane), U groups in flight.
+template <int D>
+__global__ void __launch_bounds__(256) normgate_y_kernel(const __nv_bfloat16* __restrict__ O,
+                                                         const __nv_bfloat16* __restrict__ Olo,
+                                                         const __nv_bfloat16* __restrict__ g,
+                                                         const float* __restrict__ gamma,
+                                                         const float* __restrict__ rstd,
+                                                         __nv_bfloat16* __restrict__ Y, uint32_t rows, uint32_t H,
+                                                         uint32_t Nq) {
+    constexpr int LPR = D / 8, RPW = 32 / LPR, U = 4;
+    const uint32_t lane = threadIdx.x & 31, sub = lane / LPR, cl = lane % LPR;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    const float4 ga = __ldg(reinterpret_cast<const float4*>(gamma) + 2 * cl);
+    const float4 gb = __ldg(reinterpret_cast<const float4*>(gamma) + 2 * cl + 1);
+    const float gam[8] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w};
+    for (uint32_t r0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * (U * RPW); r0 < rows; r0 += nw * U * RPW) {
+        uint4 ov[U], lv[U], gv[U];
+        float rs[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t row = min(r0 + u * RPW + sub, rows - 1);
+            const size_t e = (size_t)row * D + cl * 8;
+            ov[u] = __ldcs(reinterpret_cast<const uint4*>(O + e));
+            lv[u] = Olo ? __ldcs(reinterpret_cast<const uint4*>(Olo + e)) : make_uint4(0u, 0u, 0u, 0u);
+            gv[u] = __ldcs(reinterpret_cast<const uint4*>(g + e));
+            const uint32_t hh = row % H, bt = row / H, t = bt % Nq, b = bt / Nq;
+            rs[u] = __ldg(rstd + ((size_t)b * H + hh) * Nq + t);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t row = r0 + u * RPW + sub;
+            const uint32_t* ow = &ov[u].x;
+            const uint32_t* lw = &lv[u].x;
+            const uint32_t* gw = &gv[u].x;
+            uint32_t yw[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                float o0, o1, l0, l1, g0, g1;
+                f2unpack(bf2_to_f2(ow[e]), o0, o1);
+                f2unpack(bf2_to_f2(lw[e]), l0, l1);
+                f2unpack(bf2_to_f2(gw[e]), g0, g1);
+                const float s0 = fmaf(0.5f, tanh_approx(0.5f * g0), 0.5f);
+                const float s1 = fmaf(0.5f, tanh_approx(0.5f * g1), 0.5f);
+                yw[e] = pack_bf16x2(g0 * s0 * gam[2 * e] * (o0 + l0) * rs[u], g1 * s1 * gam[2 * e + 1] * (o1 + l1) * rs[u]);
+            }
+            if (row < rows) __stcs(reinterpret_cast<uint4*>(Y + (size_t)row * D + cl * 8), make_uint4(yw[0], yw[1], yw[2], yw[3]));
+        }
+    }
+}
+
 }  // namespace
 
 #if GFWA_FWD_TRACE
@@ -758,7 +781,7 @@ bool tc_fwd_supported(const AttnParams& p, gfwa_dtype_t dt) {
 
 template <int D>
 static gfwa_status_t tc_fwd_d(const AttnParams& p, cudaStream_t st) {
-    CUtensorMap mq, mk, mv, mo, mol, my;
+    CUtensorMap mq, mk, mv, mo, mol;
     GFWA_REQUIRE(encode_bnhd_map(&mq, p.Q, p.B, p.Nq, p.H, D, p.qs, BM));
     GFWA_REQUIRE(encode_bnhd_map(&mk, p.K, p.B, p.Nkv, p.H, D, p.ks, BN));
     GFWA_REQUIRE(encode_bnhd_map(&mv, p.V, p.B, p.Nkv, p.H, D, p.vs, BN));
@@ -767,10 +790,6 @@ static gfwa_status_t tc_fwd_d(const AttnParams& p, cudaStream_t st) {
         GFWA_REQUIRE(encode_bnhd_map(&mol, p.O_lo, p.B, p.Nq, p.H, D, p.os, BM));
     else
         mol = mo;  // unused
-    if (p.ng_g)
-        GFWA_REQUIRE(encode_bnhd_map_w32(&my, p.ng_Y, p.B, p.Nq, p.H, D, p.os, BM));
-    else
-        my = mo;  // unused
     TcFwdParams tp;
     tp.U = p.U;
     tp.LSE = p.LSE;
@@ -787,6 +806,7 @@ static gfwa_status_t tc_fwd_d(const AttnParams& p, cudaStream_t st) {
     tp.sl2 = p.scale * kLog2e;
     tp.inv_scale = 1.f / p.scale;
     tp.ng_g = (const __nv_bfloat16*)p.ng_g;
+    tp.ng_Y = (__nv_bfloat16*)p.ng_Y;
     tp.ng_gamma = p.ng_gamma;
     tp.ng_rstd = p.ng_rstd;
     tp.ng_eps = p.ng_eps;
@@ -807,7 +827,15 @@ static gfwa_status_t tc_fwd_d(const AttnParams& p, cudaStream_t st) {
     int64_t cap = n_sm;
     if (const char* e = getenv("GFWA_FWD_GRID")) cap = max64(1, atoll(e));  // diagnostics: fewer CTAs, more items each
     const unsigned grid = (unsigned)min64(n_items, cap);
-    kern<<<grid, kThreads, kSmemBytes, st>>>(mq, mk, mv, mo, mol, my, tp);
+    kern<<<grid, kThreads, kSmemBytes, st>>>(mq, mk, mv, mo, mol, tp);
+    note_launch();
+    if (gfwa_status_t s = check_launch()) return s;
+    if (!p.ng_g) return GFWA_OK;
+    const int64_t rows = p.B * p.Nq * p.H;  // < 2^31, packed layout: checked by the caller
+    constexpr int kRowsPerBlock = 8 * 4 * (256 / D);
+    normgate_y_kernel<D><<<(unsigned)min64((rows + kRowsPerBlock - 1) / kRowsPerBlock, (int64_t)n_sm * 8), 256, 0, st>>>(
+        (const __nv_bfloat16*)p.O, (const __nv_bfloat16*)p.O_lo, (const __nv_bfloat16*)p.ng_g, p.ng_gamma, p.ng_rstd,
+        (__nv_bfloat16*)p.ng_Y, (uint32_t)rows, (uint32_t)p.H, (uint32_t)p.Nq);
     note_launch();
     return check_launch();
 }

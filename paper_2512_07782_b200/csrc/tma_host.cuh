@@ -26,24 +26,6 @@ inline bool encode_bnhd_map(CUtensorMap* map, const void* base, int64_t B, int64
     return r == CUDA_SUCCESS;
 }
 
-// bf16 [B, N, H, d] map with box {32 d-elements (64 B), 1 head, rows, 1 batch}, 64-byte
-// swizzle (16-B chunk c of row r at chunk c ^ ((r >> 1) & 3)): the AttnLayer
-// epilogue's Y staging, one 32-column round at a time
-inline bool encode_bnhd_map_w32(CUtensorMap* map, const void* base, int64_t B, int64_t N, int64_t H, int d,
-                                const int64_t* s, int box_rows) {
-    cuuint64_t dims[4] = {(cuuint64_t)d, (cuuint64_t)H, (cuuint64_t)N, (cuuint64_t)B};
-    cuuint64_t strides[3] = {(cuuint64_t)(s[2] * 2), (cuuint64_t)(s[1] * 2), (cuuint64_t)(s[0] * 2)};
-    for (int i = 0; i < 3; ++i)
-        if (strides[i] == 0) strides[i] = 16;
-    cuuint32_t box[4] = {32u, 1u, (cuuint32_t)box_rows, 1u};
-    cuuint32_t estr[4] = {1u, 1u, 1u, 1u};
-    CUresult r = drv::tensorMapEncodeTiled(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims,
-                                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                        CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    return r == CUDA_SUCCESS;
-}
-
 // fp32 [B, N, H, d] map with box {32 d-elements (128 B), 1, rows, 1}, 128B swizzle
 // (the dQ reduce-add).
 inline bool encode_bnhd_map_f32(CUtensorMap* map, const void* base, int64_t B, int64_t N, int64_t H, int d,
