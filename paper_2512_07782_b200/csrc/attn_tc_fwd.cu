@@ -120,7 +120,7 @@ struct TcFwdParams {
 };
 
 #if GFWA_FWD_TRACE
-constexpr int kTrMax = 512;  // stamps per (CTA, role)
+constexpr int kTrMax = 1024;  // stamps per (CTA, role)
 __device__ long long g_fwd_trace[148 * 8 * kTrMax];
 #define FTR(role, k)                                                                          \
     do {                                                                                      \
@@ -449,9 +449,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             const float bq = valid ? (Ubh[g] - uref) * kLog2e : 0.f;
             float m_used = -INFINITY, l = 0.f;  // l: this half's partial row sum
             for (int j = jt; j >= jlo_x; --j, ++cs) {
-                if (r == 0) FTR(x, 3 * (int)cs);
+                if (r == 0) FTR(x, 6 * (int)cs);
                 mbar_wait_park(&bars->s_full[x], cs & 1);
-                if (r == 0) FTR(x, 3 * (int)cs + 1);
+                if (r == 0) FTR(x, 6 * (int)cs + 1);
                 tc_fence_after();
                 const bool interior = (j * BN + BN - 1 <= glo_x) && (j * BN >= ghi_x - p.w + 1) && (j * BN + BN <= Nkv);
                 uint32_t keep[2] = {~0u, ~0u};
@@ -491,12 +491,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                         mx[(e >> 2) & 3] = fmax3(mx[(e >> 2) & 3], fmaxf(a0, a1), fmaxf(a2, a3));
                     }
                 }
+                if (r == 0) FTR(x, 6 * (int)cs + 2);
                 // the row max over both halves (exchange through smem), in log2 units
                 // (double-buffered by key-tile parity: a half may run one tile ahead of the other)
                 float* xc = xch + (cs & 1) * 2 * BM;
                 xc[hh * BM + r] = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
                 named_bar_sync(bar_tile, 256);
                 const float mraw = fmaxf(xc[r], xc[BM + r]);
+                if (r == 0) FTR(x, 6 * (int)cs + 3);
                 const float mt = mraw == -INFINITY ? -INFINITY : mraw * p.sl2;
                 // lazy online softmax: move the reference max only when it grows by > 2^8
                 // (both halves take the same decision from the same values)
@@ -568,7 +570,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bars->p_ready[x]);
-                if (r == 0) FTR(x, 3 * (int)cs + 2);
+                if (r == 0) FTR(x, 6 * (int)cs + 5);
             }
             // Alg. 2 l.19-20: l = both halves' sums; 1/l for the epilogue, LSE = m + ln l
             // (natural log, bias included).  linv is reused per item: wait until the
