@@ -374,8 +374,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mma_ts(tmem + 384, buf + pc + QPW / 2, sdesc_sw128(qb + kk * 2048, kQTbox, 1024), id_tm, acc);
                 }
                 tc_commit(&bars->empty[ps]);  // Q/dO stage free
-                // the item's K slot is released by the epilogue, which stages dV / dK in it
-                if (pm == pn - 1) tc_commit(&bars->dkdv_full);
+                if (pm == pn - 1) {
+                    tc_commit(&bars->dkdv_full);
+                    tc_commit(&bars->empty[pk]);  // K free (its last reader was dQ^T)
+                }
             }
             __syncwarp();
         };
@@ -616,7 +618,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int64_t which = tsr ? 0 : 1;  // dK first, then dV
             return base + (((which * p.B + it.b) * rows + r) * p.H + it.h) * D;
         };
-        Pool pool;  // replica of the slot rotation (the epilogue stages in the item's K slot)
         int g = 0, nitem = 0, pg = -1;
         int64_t pt0 = 0, pbh = 0;
         for (int idx = blockIdx.x; idx < p.n_items; idx += gridDim.x) {
@@ -700,14 +701,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                 pt0 = t0;
                 pbh = bh;
             }
-            // epilogue of the item: dV, dK (TMEM lane = key) -> bf16, staged in the item's K
-            // slot (its last reader, dQ^T, has completed: dkdv_full) and written by TMA
-            // stores of [32 keys][64 d] boxes; the slot is released once they have read it
+            // epilogue of the item: dV, dK (TMEM lane = key) -> bf16 [32 keys][64 d] boxes,
+            // staged one at a time in this warp's 4 KB of the dQ staging and written by TMA
+            // stores (the item's K slot is released by the MMA warp right away, so the next
+            // item's Q/dO loads do not wait for the epilogue)
             mbar_wait(&bars->dkdv_full, nitem & 1);
             if (dl == 0) BTR(4, nitem);
             tc_fence_after();
-            const uint32_t stg_off = pool.K() * kSlot + (warp & 3) * 8192;  // this warp's 8 KB
-            const uint32_t stg = smem_u32(pool_base) + stg_off;
+            const uint32_t stg = smem_u32(wbox);
 #pragma unroll 1
             for (int tsr = 0; tsr < 2; ++tsr) {  // 0: dV (TMEM [256, 384)), 1: dK ([384, 512), times scale)
                 const float mul = tsr ? p.scale : 1.f;
@@ -738,7 +739,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 }
                             }
                     }
-                    const uint32_t row = stg + hf * 4096 + lane * 128;  // 128B swizzle: chunk ^ (key % 8)
+                    if (lane == 0) bulk_wait_read0();  // earlier stores / reductions have read the staging
+                    __syncwarp();
+                    const uint32_t row = stg + lane * 128;  // 128B swizzle: chunk ^ (key % 8)
 #pragma unroll
                     for (int k = 0; k < 8; ++k) {
                         const uint32_t* v = k < 4 ? a + 8 * k : b + 8 * (k - 4);
@@ -749,21 +752,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                         o.w = pack_bf16x2(__uint_as_float(v[6]) * mul, __uint_as_float(v[7]) * mul);
                         sts128(row + ((k ^ (lane & 7)) << 4), o);
                     }
+                    fence_proxy_async();
+                    __syncwarp();
+                    if (lane == 0) {
+                        tma_store_4d(tsr ? &mdk : &mdv, wbox, hf * 64, it.h, it.j0 + 32 * (warp & 3), it.b);
+                        bulk_commit();
+                    }
                 }
-                fence_proxy_async();
-                __syncwarp();
-                if (lane == 0) {
-                    for (int hf = 0; hf < kHalves; ++hf)
-                        tma_store_4d(tsr ? &mdk : &mdv, pool_base + stg_off + hf * 4096, hf * 64, it.h,
-                                     it.j0 + 32 * (warp & 3), it.b);
-                    bulk_commit();
-                    bulk_wait_read0();  // the staging is reusable / releasable once the stores have read it
-                }
-                __syncwarp();
             }
-            named_bar_sync(1, 128);  // all four drain warps' stores have read the slot
-            if (dl == 0) mbar_arrive(&bars->empty[pool.K()]);
-            pool.advance(it.nsteps);
+            if (lane == 0) bulk_wait_read0();  // the next step's dQ rounds reuse the staging
+            __syncwarp();
             ++nitem;
         }
         if (pg >= 0) combine_duq(pg, pt0, pbh);
