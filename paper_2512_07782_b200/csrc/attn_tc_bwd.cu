@@ -72,6 +72,9 @@ constexpr int kThreads = 32 * (kTmaWarp + 1);  // softmax-grad WGs, drain WG, MM
 #ifndef GFWA_BWD_NODQ
 #define GFWA_BWD_NODQ 0  // experiment only: skip the dQ reductions
 #endif
+#ifndef GFWA_PRE_U
+#define GFWA_PRE_U 4  // row groups in flight per warp in the backward's preprocess (2: 165, 4: 158 us at C2)
+#endif
 #ifndef GFWA_BWD_DQRED
 #define GFWA_BWD_DQRED 0  // 1: dQ^T drained by per-query red.global.add instead of TMA bulk reductions
 #endif
@@ -832,7 +835,7 @@ __global__ void __launch_bounds__(256) bwd_tc_pre_flat_kernel(const __nv_bfloat1
                                                              unsigned long long token_val) {
     constexpr int LPR = D / 8;           // lanes per row (8 bf16 = 16 B each)
     constexpr int RPW = 32 / LPR;        // rows per warp load
-    constexpr int U = 2;                 // loads unrolled: U * RPW rows per iteration
+    constexpr int U = GFWA_PRE_U;        // loads unrolled: U * RPW rows per iteration
     const uint32_t lane = threadIdx.x & 31, sub = lane / LPR, cl = lane % LPR;
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
     // gfwa_fwd_train already zeroed the accumulator (its token is in the workspace)
@@ -1079,7 +1082,7 @@ static gfwa_status_t tc_bwd_d(const AttnParams& pin, cudaStream_t st, void* ws) 
             p.ng_dgamma, p.Dv, p.dQacc, (uint32_t)rows, (uint32_t)p.H, (uint32_t)p.Nq, p.dU, (uint32_t)n_du, p.token,
             p.token_val);
     } else if (o_flat) {
-        bwd_tc_pre_flat_kernel<D><<<(unsigned)min64((rows + 8 * 512 / D - 1) / (8 * 512 / D), (int64_t)n_sm * 8), 256, 0, st>>>(
+        bwd_tc_pre_flat_kernel<D><<<(unsigned)min64((rows + 8 * 256 * GFWA_PRE_U / D - 1) / (8 * 256 * GFWA_PRE_U / D), (int64_t)n_sm * 8), 256, 0, st>>>(
             (const __nv_bfloat16*)p.O, (const __nv_bfloat16*)p.Olo, (const __nv_bfloat16*)p.dO, p.Dv, p.dQacc, (uint32_t)rows, (uint32_t)p.H, (uint32_t)p.Nq, p.dU,
             (uint32_t)n_du, p.token, p.token_val);
     } else {
