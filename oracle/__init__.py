@@ -12,6 +12,7 @@ See ``gfwa_oracle.c`` for the paper citations of every function.
 from __future__ import annotations
 
 import ctypes
+import math
 import os
 import subprocess
 
@@ -208,3 +209,61 @@ def normgate_bwd(O, g, gamma, dY, eps: float = 1e-5):
     _load().oracle_normgate_bwd(_p(O), _p(g), _p(gamma), _p(dY), _I64(B), _I64(Nq), _I64(H), _I64(d),
                                 ctypes.c_double(eps), _p(dO), _p(dg), _p(dgamma))
     return dO, dg, dgamma
+
+
+# --- NSA extension with GatedFWA as the local branch (App. B, C-28, C-29)
+
+
+def nsa_compress(K, V, blk: int):
+    """Block means Kc, Vc [B, N // blk, H, d] (C-28)."""
+    K, V = _f64(K), _f64(V)
+    B, N, H, d = K.shape
+    nb = N // blk
+    Kc, Vc = np.empty((B, nb, H, d)), np.empty((B, nb, H, d))
+    _load().oracle_nsa_compress(_p(K), _p(V), _I64(B), _I64(N), _I64(H), _I64(d), _I64(blk), _p(Kc), _p(Vc))
+    return Kc, Vc
+
+
+def nsa_cmp(Q, Kc, Vc, blk: int, scale: float | None = None):
+    """Compressed attention (O_cmp [B,N,H,d], scores [B,H,N,nb])."""
+    Q, Kc, Vc = _f64(Q), _f64(Kc), _f64(Vc)
+    B, N, H, d = Q.shape
+    nb = N // blk
+    scale = 1.0 / math.sqrt(d) if scale is None else scale
+    O = np.empty_like(Q)
+    sc = np.empty((B, H, N, max(nb, 1)))
+    _load().oracle_nsa_cmp(_p(Q), _p(Kc), _p(Vc), _I64(B), _I64(N), _I64(H), _I64(d), _I64(blk),
+                           ctypes.c_double(scale), _p(O), _p(sc))
+    return O, sc[..., :nb]
+
+
+def nsa_select(scores, N: int, blk: int, nsel: int):
+    """Selected blocks [B,H,N,nsel+1] (own block first, then top-nsel complete blocks; -1 pads)."""
+    sc = _f64(scores)
+    B, H = sc.shape[:2]
+    sel = np.empty((B, H, N, nsel + 1), dtype=np.int64)
+    _load().oracle_nsa_select(_p(sc), _I64(B), _I64(H), _I64(N), _I64(blk), _I64(nsel),
+                              sel.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)))
+    return sel
+
+
+def nsa_slc(Q, K, V, sel, blk: int, scale: float | None = None):
+    """Selected-block attention O_slc [B,N,H,d] over the given selection."""
+    Q, K, V = _f64(Q), _f64(K), _f64(V)
+    sel = np.ascontiguousarray(np.asarray(sel, dtype=np.int64))
+    B, N, H, d = Q.shape
+    nsel = sel.shape[-1] - 1
+    scale = 1.0 / math.sqrt(d) if scale is None else scale
+    O = np.empty_like(Q)
+    _load().oracle_nsa_slc(_p(Q), _p(K), _p(V), sel.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), _I64(B),
+                           _I64(N), _I64(H), _I64(d), _I64(blk), _I64(nsel), ctypes.c_double(scale), _p(O))
+    return O
+
+
+def nsa_combine(Ocmp, Oslc, Oloc, g):
+    """O = sigmoid(g0) O_cmp + sigmoid(g1) O_slc + sigmoid(g2) O_loc (P:700)."""
+    Ocmp, Oslc, Oloc, g = _f64(Ocmp), _f64(Oslc), _f64(Oloc), _f64(g)
+    B, N, H, d = Ocmp.shape
+    O = np.empty_like(Ocmp)
+    _load().oracle_nsa_combine(_p(Ocmp), _p(Oslc), _p(Oloc), _p(g), _I64(B), _I64(N), _I64(H), _I64(d), _p(O))
+    return O

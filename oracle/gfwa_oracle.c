@@ -401,3 +401,131 @@ void oracle_normgate_bwd(const double* O, const double* g, const double* gamma, 
                 }
             }
 }
+
+/*
+ * NSA extension with GatedFWA as the local branch (App. B; readings
+ * C-28, C-29).  Token compression: phi = the block MEAN (C-28: the
+ * learnable MLP replaced by its parameter-free mean, block length = stride =
+ * blk); compressed attention over the blocks that end at or before t; block
+ * selection by the compressed-attention score, top n_sel of those
+ * blocks plus the query's own block (C-29); selected attention over the tokens
+ * <= t of the selected blocks; output sum_c sigmoid(g_c) o_c.
+ */
+/* Kc, Vc [B][nb][H][d], nb = N / blk (complete blocks) */
+void oracle_nsa_compress(const double* K, const double* V, int64_t B, int64_t N, int64_t H, int64_t d, int64_t blk,
+                         double* Kc, double* Vc) {
+    const int64_t nb = N / blk;
+    for (int64_t b = 0; b < B; ++b)
+        for (int64_t i = 0; i < nb; ++i)
+            for (int64_t hh = 0; hh < H; ++hh)
+                for (int64_t c = 0; c < d; ++c) {
+                    double sk = 0.0, sv = 0.0;
+                    for (int64_t j = i * blk; j < (i + 1) * blk; ++j) {
+                        sk += K[((b * N + j) * H + hh) * d + c];
+                        sv += V[((b * N + j) * H + hh) * d + c];
+                    }
+                    Kc[((b * nb + i) * H + hh) * d + c] = sk / (double)blk;
+                    Vc[((b * nb + i) * H + hh) * d + c] = sv / (double)blk;
+                }
+}
+
+/* o_cmp [B][N][H][d]: softmax over the blocks i with (i+1) blk - 1 <= t of
+ * scale q.Kc_i (0 when t < blk - 1); scores [B][H][N][nb] (-inf for blocks not complete) */
+void oracle_nsa_cmp(const double* Q, const double* Kc, const double* Vc, int64_t B, int64_t N, int64_t H, int64_t d,
+                    int64_t blk, double scale, double* Ocmp, double* scores) {
+    const int64_t nb = N / blk;
+    for (int64_t b = 0; b < B; ++b)
+        for (int64_t hh = 0; hh < H; ++hh)
+            for (int64_t t = 0; t < N; ++t) {
+                const double* q = Q + ((b * N + t) * H + hh) * d;
+                double* sc = scores + ((b * H + hh) * N + t) * nb;
+                const int64_t nc = (t + 1) / blk;
+                double m = -INFINITY;
+                for (int64_t i = 0; i < nb; ++i) {
+                    sc[i] = -INFINITY;
+                    if (i >= nc) continue;
+                    double s = 0.0;
+                    for (int64_t c = 0; c < d; ++c) s += q[c] * Kc[((b * nb + i) * H + hh) * d + c];
+                    sc[i] = scale * s;
+                    if (sc[i] > m) m = sc[i];
+                }
+                double* o = Ocmp + ((b * N + t) * H + hh) * d;
+                for (int64_t c = 0; c < d; ++c) o[c] = 0.0;
+                if (nc == 0) continue;
+                double l = 0.0;
+                for (int64_t i = 0; i < nc; ++i) l += exp(sc[i] - m);
+                for (int64_t i = 0; i < nc; ++i) {
+                    const double p = exp(sc[i] - m) / l;
+                    for (int64_t c = 0; c < d; ++c) o[c] += p * Vc[((b * nb + i) * H + hh) * d + c];
+                }
+            }
+}
+
+/* sel [B][H][N][nsel + 1]: the query's own block t / blk first, then the n_sel
+ * complete blocks (other than its own) with the largest scores, ties to the lower
+ * index; -1 where fewer exist */
+void oracle_nsa_select(const double* scores, int64_t B, int64_t H, int64_t N, int64_t blk, int64_t nsel,
+                       int64_t* sel) {
+    const int64_t nb = N / blk;
+    for (int64_t bh = 0; bh < B * H; ++bh)
+        for (int64_t t = 0; t < N; ++t) {
+            const double* sc = scores + (bh * N + t) * nb;
+            int64_t* out = sel + (bh * N + t) * (nsel + 1);
+            const int64_t own = t / blk;
+            out[0] = own;
+            for (int64_t k = 1; k <= nsel; ++k) {
+                int64_t best = -1;
+                for (int64_t i = 0; i < nb; ++i) {
+                    if (i == own || sc[i] == -INFINITY) continue;
+                    int taken = 0;
+                    for (int64_t q = 1; q < k; ++q) taken |= out[q] == i;
+                    if (taken) continue;
+                    if (best < 0 || sc[i] > sc[best]) best = i;
+                }
+                out[k] = best;
+            }
+        }
+}
+
+/* o_slc [B][N][H][d]: softmax of scale q.k_j over the tokens j <= t of the selected blocks */
+void oracle_nsa_slc(const double* Q, const double* K, const double* V, const int64_t* sel, int64_t B, int64_t N,
+                    int64_t H, int64_t d, int64_t blk, int64_t nsel, double scale, double* Oslc) {
+    for (int64_t b = 0; b < B; ++b)
+        for (int64_t hh = 0; hh < H; ++hh)
+            for (int64_t t = 0; t < N; ++t) {
+                const double* q = Q + ((b * N + t) * H + hh) * d;
+                const int64_t* sl = sel + ((b * H + hh) * N + t) * (nsel + 1);
+                double m = -INFINITY;
+                for (int64_t k = 0; k <= nsel; ++k) {
+                    if (sl[k] < 0) continue;
+                    for (int64_t j = sl[k] * blk; j < (sl[k] + 1) * blk && j <= t; ++j) {
+                        double s = 0.0;
+                        for (int64_t c = 0; c < d; ++c) s += q[c] * K[((b * N + j) * H + hh) * d + c];
+                        if (scale * s > m) m = scale * s;
+                    }
+                }
+                double l = 0.0;
+                double* o = Oslc + ((b * N + t) * H + hh) * d;
+                for (int64_t c = 0; c < d; ++c) o[c] = 0.0;
+                for (int64_t k = 0; k <= nsel; ++k) {
+                    if (sl[k] < 0) continue;
+                    for (int64_t j = sl[k] * blk; j < (sl[k] + 1) * blk && j <= t; ++j) {
+                        double s = 0.0;
+                        for (int64_t c = 0; c < d; ++c) s += q[c] * K[((b * N + j) * H + hh) * d + c];
+                        const double e = exp(scale * s - m);
+                        l += e;
+                        for (int64_t c = 0; c < d; ++c) o[c] += e * V[((b * N + j) * H + hh) * d + c];
+                    }
+                }
+                for (int64_t c = 0; c < d; ++c) o[c] /= l;
+            }
+}
+
+/* o = sigmoid(g0) o_cmp + sigmoid(g1) o_slc + sigmoid(g2) o_loc; g [B][N][H][3] */
+void oracle_nsa_combine(const double* Ocmp, const double* Oslc, const double* Oloc, const double* g, int64_t B,
+                        int64_t N, int64_t H, int64_t d, double* O) {
+    for (int64_t r = 0; r < B * N * H; ++r) {
+        const double a = sigmoid(g[3 * r]), s = sigmoid(g[3 * r + 1]), l = sigmoid(g[3 * r + 2]);
+        for (int64_t c = 0; c < d; ++c) O[r * d + c] = a * Ocmp[r * d + c] + s * Oslc[r * d + c] + l * Oloc[r * d + c];
+    }
+}

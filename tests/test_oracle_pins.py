@@ -463,3 +463,69 @@ def test_normgate_matches_torch_autograd():
     assert np.allclose(dO, O.grad.numpy(), rtol=1e-11, atol=1e-13)
     assert np.allclose(dg, g.grad.numpy(), rtol=1e-11, atol=1e-13)
     assert np.allclose(dgamma, gamma.grad.numpy(), rtol=1e-11, atol=1e-13)
+
+
+# --- NSA extension (App. B; readings C-28 block-mean compression, C-29 selection) ---
+
+
+def _sdpa_causal(Q, K, V):
+    """fp64 torch SDPA, causal (a library routine independent of the oracle's loops)."""
+    q, k, v = (torch.from_numpy(np.ascontiguousarray(x)).permute(0, 2, 1, 3) for x in (Q, K, V))
+    return torch.nn.functional.scaled_dot_product_attention(q, k, v, is_causal=True).permute(0, 2, 1, 3).numpy()
+
+
+def test_nsa_compress_is_block_mean():
+    K, V = _rand((2, 40, 3, 8), 160), _rand((2, 40, 3, 8), 161)
+    Kc, Vc = oracle.nsa_compress(K, V, 8)
+    assert Kc.shape == (2, 5, 3, 8)
+    assert np.allclose(Kc, K.reshape(2, 5, 8, 3, 8).mean(2), atol=1e-15)
+    assert np.allclose(Vc, V.reshape(2, 5, 8, 3, 8).mean(2), atol=1e-15)
+
+
+def test_nsa_branches_reduce_to_causal_attention():
+    """blk = 1: every token is its own compressed block, so compressed attention is full
+    causal attention (but for the first row, whose own block is its only one, and
+    complete); with n_sel >= N the selection keeps every earlier block as well, so
+    selected attention is full causal attention too (torch SDPA, fp64)."""
+    B, N, H, d = 1, 12, 2, 8
+    Q, K, V = _rand((B, N, H, d), 162), _rand((B, N, H, d), 163), _rand((B, N, H, d), 164)
+    ref = _sdpa_causal(Q, K, V)
+    Kc, Vc = oracle.nsa_compress(K, V, 1)
+    Ocmp, sc = oracle.nsa_cmp(Q, Kc, Vc, 1)
+    assert np.allclose(Ocmp, ref, atol=1e-12)
+    sel = oracle.nsa_select(sc, N, 1, N)
+    Oslc = oracle.nsa_slc(Q, K, V, sel, 1)
+    assert np.allclose(Oslc, ref, atol=1e-12)
+
+
+def test_nsa_select_and_slc_by_hand():
+    """Selection = own block + the top n_sel complete blocks by compressed score (ties to
+    the lower index, C-29), checked against a direct argsort; o_slc of a selection that
+    is only the own block is causal attention inside that block."""
+    B, N, H, d, blk, nsel = 1, 64, 1, 4, 8, 2
+    rng = np.random.default_rng(165)
+    sc = rng.standard_normal((B, H, N, N // blk))
+    for t in range(N):  # blocks ending after t are not complete
+        sc[0, 0, t, (t + 1) // blk:] = -np.inf
+    sel = oracle.nsa_select(sc, N, blk, nsel)
+    for t in range(N):
+        own = t // blk
+        cand = [i for i in range((t + 1) // blk) if i != own]
+        top = sorted(cand, key=lambda i: (-sc[0, 0, t, i], i))[:nsel]
+        assert list(sel[0, 0, t]) == [own] + top + [-1] * (nsel - len(top))
+    Q, K, V = _rand((B, N, H, d), 166), _rand((B, N, H, d), 167), _rand((B, N, H, d), 168)
+    only_own = np.full((B, H, N, nsel + 1), -1, dtype=np.int64)
+    only_own[..., 0] = np.arange(N)[None, None, :] // blk
+    O = oracle.nsa_slc(Q, K, V, only_own, blk)
+    for i0 in range(0, N, blk):
+        blkref = _sdpa_causal(Q[:, i0:i0 + blk], K[:, i0:i0 + blk], V[:, i0:i0 + blk])
+        assert np.allclose(O[:, i0:i0 + blk], blkref, atol=1e-12)
+
+
+def test_nsa_combine_gates():
+    """sigmoid gates: g -> -inf removes a branch, g = 0 weighs it 1/2."""
+    shape = (1, 5, 2, 4)
+    a, s, l = _rand(shape, 169), _rand(shape, 170), _rand(shape, 171)
+    g = np.zeros(shape[:3] + (3,))
+    g[..., 0], g[..., 1], g[..., 2] = -800.0, 0.0, 800.0
+    assert np.allclose(oracle.nsa_combine(a, s, l, g), 0.5 * s + l, atol=1e-14)
