@@ -227,6 +227,39 @@ gfwa_status_t gfwa_bwd_rows_f32(const gfwa_attn_desc_t* desc, const void* Q, con
                                 gfwa_stream_t stream);
 
 /* ------------------------------------------------------------------------- */
+/* NSA extension with GatedFWA as the local branch (App. B)          */
+/* ------------------------------------------------------------------------- */
+typedef struct {
+    int64_t B, H, N;
+    int32_t d;          /* 64 or 128 */
+    int32_t w;          /* window of the local (GatedFWA) branch */
+    int32_t block;      /* compression / selection block length (length = stride) */
+    int32_t n_sel;      /* selected blocks besides the query's own block */
+    float scale;        /* <= 0 selects 1/sqrt(d) */
+    gfwa_dtype_t dtype; /* GFWA_BF16 */
+} gfwa_nsa_desc_t;
+
+/*
+ * gfwa_nsa_fwd -- forward of the hybrid:
+ *   O = sigmoid(g0) o_cmp + sigmoid(g1) o_slc + sigmoid(g2) o_loc
+ * with o_loc = gfwa_fwd(Q, K, V, U, w) (the GatedFWA local branch),
+ * o_cmp = softmax attention of q_t over the block means (reading C-28: the
+ * compression map phi is the block mean, block length = stride = `block`) of
+ * the blocks that end at or before t (0 for t < block - 1), and o_slc = softmax
+ * attention over the tokens <= t of the selected blocks: the query's own block
+ * plus the n_sel complete blocks with the largest compressed-attention scores
+ * scale q.Kc_i (reading C-29; ties to the lower index).  Q, K, V, O [B,N,H,d]
+ * bf16 packed; U [B,H,N] fp32; gates [B,N,H,3] fp32 logits.  Optional
+ * outputs (NULL to skip): O_cmp, O_slc [B,N,H,d] fp32, sel [B,H,N,n_sel+1]
+ * int32 (the own block first, -1 pads), O_loc [B,N,H,d] bf16.  N / block <=
+ * 512.  The compressed and selected branches run on CUDA-core kernels.
+ */
+size_t gfwa_nsa_workspace_size(const gfwa_nsa_desc_t* desc);
+gfwa_status_t gfwa_nsa_fwd(const gfwa_nsa_desc_t* desc, const void* Q, const void* K, const void* V,
+                           const float* U, const float* gates, void* O, float* O_cmp, float* O_slc,
+                           int32_t* sel, void* O_loc, void* ws, size_t ws_bytes, gfwa_stream_t stream);
+
+/* ------------------------------------------------------------------------- */
 /* AttnLayer output epilogue fused into the attention kernels:     */
 /*   O~ = concat_h norm(GatedFWA_h),  G = swish(linear(X)),  out = (G . O~) W_O */
 /* Reading C-27: norm = RMSNorm over the head dim with a per-channel weight    */

@@ -65,6 +65,13 @@ class DecodeDesc(ctypes.Structure):
     ]
 
 
+class NsaDesc(ctypes.Structure):
+    """gfwa_nsa_desc_t (include/gfwa.h): the NSA hybrid with GatedFWA as its local branch."""
+    _fields_ = [("B", ctypes.c_int64), ("H", ctypes.c_int64), ("N", ctypes.c_int64), ("d", ctypes.c_int32),
+                ("w", ctypes.c_int32), ("block", ctypes.c_int32), ("n_sel", ctypes.c_int32), ("scale", ctypes.c_float),
+                ("dtype", ctypes.c_int32)]
+
+
 class NormGate(ctypes.Structure):
     """gfwa_normgate_t (include/gfwa.h): the AttnLayer epilogue's inputs (C-27)."""
     _fields_ = [("g", ctypes.c_void_p), ("gamma", ctypes.c_void_p), ("eps", ctypes.c_float),
@@ -100,6 +107,8 @@ EXPORTED = (
     "gfwa_fwd_normgate",
     "gfwa_bwd_normgate",
     "gfwa_bwd_rows_f32",
+    "gfwa_nsa_fwd",
+    "gfwa_nsa_workspace_size",
 )
 
 
@@ -136,6 +145,10 @@ def load() -> ctypes.CDLL:
         lib.gfwa_bwd_workspace_size.argtypes = [ctypes.POINTER(AttnDesc)]
         lib.gfwa_bwd.restype = ctypes.c_int
         lib.gfwa_bwd.argtypes = [ctypes.POINTER(AttnDesc)] + [_VP] * 15 + [sz, _VP]
+        lib.gfwa_nsa_workspace_size.restype = sz
+        lib.gfwa_nsa_workspace_size.argtypes = [ctypes.POINTER(NsaDesc)]
+        lib.gfwa_nsa_fwd.restype = ctypes.c_int
+        lib.gfwa_nsa_fwd.argtypes = [ctypes.POINTER(NsaDesc)] + [_VP] * 11 + [sz, _VP]
         lib.gfwa_bwd_rows_f32.restype = ctypes.c_int
         lib.gfwa_bwd_rows_f32.argtypes = [ctypes.POINTER(AttnDesc)] + [_VP] * 14 + [_I64, _VP, _I64, _VP, _VP, sz, _VP]
         lib.gfwa_fwd_normgate.restype = ctypes.c_int
@@ -464,6 +477,34 @@ def gfwa_bwd_rows_f32(Q, K, V, U, O, LSE, dO, w: int, head_rows: int, tail_rows:
                                _stream(dev))
     _check(st, "gfwa_bwd_rows_f32")
     return dQ, dK, dV, dU, head, tail
+
+
+def gfwa_nsa_fwd(Q, K, V, U, gates, w: int, block: int = 64, n_sel: int = 16, scale: float | None = None,
+                 want_branches: bool = False):
+    """NSA hybrid forward with GatedFWA as the local branch (App. B; readings
+    C-28, C-29): O = sigmoid(g0) o_cmp + sigmoid(g1) o_slc + sigmoid(g2) o_gatedfwa.
+    Q, K, V [B,N,H,d] bf16; U [B,H,N]; gates [B,N,H,3] fp32 logits.  Returns O, or
+    (O, o_cmp, o_slc, sel, o_loc) with want_branches."""
+    lib = load()
+    _need_cuda(Q, K, V, U, gates)
+    B, N, H, d = Q.shape
+    dev = Q.device
+    Q, K, V = Q.contiguous(), K.contiguous(), V.contiguous()
+    O = torch.empty_like(Q)
+    oc = os_ = sel = ol = None
+    if want_branches:
+        oc = torch.empty(B, N, H, d, dtype=torch.float32, device=dev)
+        os_ = torch.empty_like(oc)
+        sel = torch.empty(B, H, N, n_sel + 1, dtype=torch.int32, device=dev)
+        ol = torch.empty_like(Q)
+    dsc = NsaDesc(B, H, N, d, w, block, n_sel, -1.0 if scale is None else float(scale), GFWA_BF16)
+    nbytes = lib.gfwa_nsa_workspace_size(ctypes.byref(dsc))
+    ws = workspace(nbytes, dev, "nsa")
+    U, gates = U.contiguous(), gates.float().contiguous()
+    st = lib.gfwa_nsa_fwd(ctypes.byref(dsc), _ptr(Q), _ptr(K), _ptr(V), _ptr(U), _ptr(gates), _ptr(O), _ptr(oc),
+                          _ptr(os_), _ptr(sel), _ptr(ol), _ptr(ws), nbytes, _stream(dev))
+    _check(st, "gfwa_nsa_fwd")
+    return (O, oc, os_, sel, ol) if want_branches else O
 
 
 def gfwa_attn_path(Q, K, V, w: int) -> int:

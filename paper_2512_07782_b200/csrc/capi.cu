@@ -452,3 +452,72 @@ extern "C" gfwa_status_t gfwa_bwd_rows_f32(const gfwa_attn_desc_t* desc, const v
     g_rows = RowsF32{};
     return s;
 }
+
+// ---------------------------------------------------------------------------
+// NSA extension (App. B; readings C-28, C-29), forward
+namespace gfwa {
+size_t nsa_workspace(int64_t B, int64_t N, int64_t H, int d, int blk, int nsel);
+gfwa_status_t nsa_fwd_branches(const void* Q, const void* K, const void* V, const float* g, int64_t B, int64_t N,
+                               int64_t H, int d, int blk, int nsel, float scale, float* Kc, float* Vc, float* Ocmp,
+                               float* Oslc, int* sel, const void* Oloc, void* O, cudaStream_t st);
+bool nsa_blocks_ok(int64_t N, int blk);
+}  // namespace gfwa
+
+namespace {
+bool nsa_desc_ok(const gfwa_nsa_desc_t* d) {
+    return d && d->B >= 1 && d->H >= 1 && d->N >= 1 && d->w >= 1 && d->block >= 1 && d->n_sel >= 0 &&
+           (d->d == 64 || d->d == 128) && d->dtype == GFWA_BF16 && nsa_blocks_ok(d->N, d->block) &&
+           d->B * d->N * d->H < ((int64_t)1 << 31) && d->scale == d->scale;
+}
+}  // namespace
+
+extern "C" size_t gfwa_nsa_workspace_size(const gfwa_nsa_desc_t* d) {
+    if (!nsa_desc_ok(d)) return 256;
+    return nsa_workspace(d->B, d->N, d->H, d->d, d->block, d->n_sel) + 256;
+}
+
+extern "C" gfwa_status_t gfwa_nsa_fwd(const gfwa_nsa_desc_t* d, const void* Q, const void* K, const void* V,
+                                      const float* U, const float* gates, void* O, float* O_cmp, float* O_slc,
+                                      int32_t* sel, void* O_loc, void* ws, size_t ws_bytes, gfwa_stream_t stream) {
+    if (!d) return GFWA_ERR_INVALID_ARGUMENT;
+    if (d->d != 64 && d->d != 128) return GFWA_ERR_UNSUPPORTED;
+    if (d->dtype != GFWA_BF16) return GFWA_ERR_UNSUPPORTED;
+    GFWA_REQUIRE(nsa_desc_ok(d));
+    GFWA_REQUIRE(Q && K && V && U && gates && O && ws && (uintptr_t)ws % 256 == 0);
+    GFWA_REQUIRE(al16(Q) && al16(K) && al16(V) && al16(O) && (!O_loc || al16(O_loc)));
+    if (ws_bytes < gfwa_nsa_workspace_size(d)) return GFWA_ERR_WORKSPACE;
+    const int64_t B = d->B, N = d->N, H = d->H, nb = N / d->block;
+    char* p = (char*)ws;
+    auto take = [&](size_t bytes) {
+        char* r = p;
+        p += (bytes + 255) & ~(size_t)255;
+        return (void*)r;
+    };
+    float* Kc = (float*)take((size_t)B * nb * H * d->d * 4);
+    float* Vc = Kc + (size_t)B * nb * H * d->d;
+    float* oc = (float*)take((size_t)B * N * H * d->d * 4 * 2);
+    float* os = oc + (size_t)B * N * H * d->d;
+    int* sl = (int*)take((size_t)B * H * N * (d->n_sel + 1) * 4);
+    void* ol = take((size_t)B * N * H * d->d * 2);
+    float* lse = (float*)take((size_t)B * H * N * 4);
+    if (O_cmp) oc = O_cmp;
+    if (O_slc) os = O_slc;
+    if (sel) sl = sel;
+    if (O_loc) ol = O_loc;
+    // the local branch: GatedFWA itself (gfwa_fwd)
+    gfwa_attn_desc_t ad{};
+    ad.B = B;
+    ad.H = H;
+    ad.N_q = N;
+    ad.N_kv = N;
+    ad.d = d->d;
+    ad.w = d->w;
+    ad.scale = d->scale;
+    ad.dtype = GFWA_BF16;
+    const int64_t st3[3] = {N * H * d->d, H * d->d, d->d};
+    for (int i = 0; i < 3; ++i) ad.q_stride[i] = ad.k_stride[i] = ad.v_stride[i] = ad.o_stride[i] = st3[i];
+    if (gfwa_status_t s = gfwa_fwd(&ad, Q, K, V, U, ol, nullptr, lse, stream)) return s;
+    const float scale = d->scale > 0.f ? d->scale : 1.f / std::sqrt((float)d->d);
+    return nsa_fwd_branches(Q, K, V, gates, B, N, H, d->d, d->block, d->n_sel, scale, Kc, Vc, oc, os, sl, ol, O,
+                            (cudaStream_t)stream);
+}
