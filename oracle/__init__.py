@@ -267,3 +267,28 @@ def nsa_combine(Ocmp, Oslc, Oloc, g):
     O = np.empty_like(Ocmp)
     _load().oracle_nsa_combine(_p(Ocmp), _p(Oslc), _p(Oloc), _p(g), _I64(B), _I64(N), _I64(H), _I64(d), _p(O))
     return O
+
+
+def nsa_bwd(Q, K, V, U, g, dO, sel, w: int, blk: int, scale: float | None = None):
+    """Chain rule of the NSA hybrid for a fixed selection: (dQ, dK, dV, dU, dgates)."""
+    Q, K, V, U, g, dO = (_f64(x) for x in (Q, K, V, U, g, dO))
+    sel = np.ascontiguousarray(np.asarray(sel, dtype=np.int64))
+    B, N, H, d = Q.shape
+    nsel = sel.shape[-1] - 1
+    scale = 1.0 / math.sqrt(d) if scale is None else scale
+    dQ, dK, dV = np.empty_like(Q), np.empty_like(K), np.empty_like(V)
+    dU = np.empty((B, H, N))
+    dg = np.empty_like(g)
+    _load().oracle_nsa_bwd(_p(Q), _p(K), _p(V), _p(U), _p(g), _p(dO), sel.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                           _I64(B), _I64(N), _I64(H), _I64(d), _I64(w), _I64(blk), _I64(nsel), ctypes.c_double(scale),
+                           _p(dQ), _p(dK), _p(dV), _p(dU), _p(dg))
+    return dQ, dK, dV, dU, dg
+
+
+def nsa_fwd_fixed(Q, K, V, U, g, sel, w: int, blk: int, scale: float | None = None):
+    """The NSA hybrid's output for a fixed selection (for finite differences)."""
+    Kc, Vc = nsa_compress(K, V, blk)
+    Oc, _ = nsa_cmp(Q, Kc, Vc, blk, scale)
+    Os = nsa_slc(Q, K, V, sel, blk, scale)
+    Ol, _ = fwd(Q, K, V, U, w, scale)
+    return nsa_combine(Oc, Os, Ol, g)

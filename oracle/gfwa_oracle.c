@@ -529,3 +529,137 @@ void oracle_nsa_combine(const double* Ocmp, const double* Oslc, const double* Ol
         for (int64_t c = 0; c < d; ++c) O[r * d + c] = a * Ocmp[r * d + c] + s * Oslc[r * d + c] + l * Oloc[r * d + c];
     }
 }
+
+/*
+ * Chain rule of the NSA hybrid for a FIXED selection sel (the top-n
+ * choice is piecewise constant, C-29): with dO_c = sigmoid(g_c) dO,
+ *   dg_c   = sigmoid(g_c) (1 - sigmoid(g_c)) dO . o_c
+ *   local  = Alg. E.2 on dO_loc (oracle_bwd), dU from it alone
+ *   cmp    p_i softmax over complete blocks, dS_i = p_i (dO_cmp . Vc_i - D),
+ *          D = sum_i p_i dO_cmp . Vc_i;  dq += scale dS_i Kc_i;  dKc_i += scale dS_i q;
+ *          dVc_i += p_i dO_cmp;  dK_j, dV_j += dKc_i / blk, dVc_i / blk for j in block i
+ *   slc    the same over the tokens <= t of the selected blocks, into dQ, dK, dV
+ * dQ, dK, dV, dg [B][N][H][3] overwritten; dU [B][H][N].
+ */
+void oracle_nsa_bwd(const double* Q, const double* K, const double* V, const double* U, const double* g,
+                    const double* dO, const int64_t* sel, int64_t B, int64_t N, int64_t H, int64_t d, int64_t w,
+                    int64_t blk, int64_t nsel, double scale, double* dQ, double* dK, double* dV, double* dU,
+                    double* dg) {
+    const int64_t nb = N / blk, rows = B * N * H, n = rows * d;
+    double* Kc = (double*)calloc((size_t)(B * (nb > 0 ? nb : 1) * H * d), sizeof(double));
+    double* Vc = (double*)calloc((size_t)(B * (nb > 0 ? nb : 1) * H * d), sizeof(double));
+    double* dKc = (double*)calloc((size_t)(B * (nb > 0 ? nb : 1) * H * d), sizeof(double));
+    double* dVc = (double*)calloc((size_t)(B * (nb > 0 ? nb : 1) * H * d), sizeof(double));
+    double* Oc = (double*)malloc(sizeof(double) * (size_t)n);
+    double* Os = (double*)malloc(sizeof(double) * (size_t)n);
+    double* Ol = (double*)malloc(sizeof(double) * (size_t)n);
+    double* L = (double*)malloc(sizeof(double) * (size_t)rows);
+    double* sc = (double*)malloc(sizeof(double) * (size_t)(B * H * N * (nb > 0 ? nb : 1)));
+    double* dOl = (double*)malloc(sizeof(double) * (size_t)n);
+    double* dQl = (double*)malloc(sizeof(double) * (size_t)n);
+    double* dKl = (double*)malloc(sizeof(double) * (size_t)n);
+    double* dVl = (double*)malloc(sizeof(double) * (size_t)n);
+    if (nb > 0) oracle_nsa_compress(K, V, B, N, H, d, blk, Kc, Vc);
+    oracle_nsa_cmp(Q, Kc, Vc, B, N, H, d, blk, scale, Oc, sc);
+    oracle_nsa_slc(Q, K, V, sel, B, N, H, d, blk, nsel, scale, Os);
+    oracle_fwd(B, H, N, N, d, w, scale, Q, K, V, U, Ol, L);
+    memset(dQ, 0, sizeof(double) * (size_t)n);
+    memset(dK, 0, sizeof(double) * (size_t)n);
+    memset(dV, 0, sizeof(double) * (size_t)n);
+    /* combination */
+    for (int64_t r = 0; r < rows; ++r) {
+        const double* o[3] = {Oc + r * d, Os + r * d, Ol + r * d};
+        for (int cix = 0; cix < 3; ++cix) {
+            const double sg = sigmoid(g[3 * r + cix]);
+            double dot = 0.0;
+            for (int64_t c = 0; c < d; ++c) dot += dO[r * d + c] * o[cix][c];
+            dg[3 * r + cix] = sg * (1.0 - sg) * dot;
+        }
+        const double sl = sigmoid(g[3 * r + 2]);
+        for (int64_t c = 0; c < d; ++c) dOl[r * d + c] = sl * dO[r * d + c];
+    }
+    /* local branch: Alg. E.2 */
+    oracle_bwd(B, H, N, N, d, w, scale, Q, K, V, U, dOl, dQl, dKl, dVl, dU, NULL, NULL);
+    for (int64_t e = 0; e < n; ++e) {
+        dQ[e] += dQl[e];
+        dK[e] += dKl[e];
+        dV[e] += dVl[e];
+    }
+    /* compressed and selected branches */
+    for (int64_t b = 0; b < B; ++b)
+        for (int64_t hh = 0; hh < H; ++hh)
+            for (int64_t t = 0; t < N; ++t) {
+                const int64_t r = (b * N + t) * H + hh;
+                const double* q = Q + r * d;
+                const double sgc = sigmoid(g[3 * r]), sgs = sigmoid(g[3 * r + 1]);
+                /* cmp */
+                const int64_t nc = (t + 1) / blk;
+                if (nc > 0) {
+                    const double* s = sc + ((b * H + hh) * N + t) * nb;
+                    double m = -INFINITY, l = 0.0, D = 0.0;
+                    for (int64_t i = 0; i < nc; ++i) m = s[i] > m ? s[i] : m;
+                    for (int64_t i = 0; i < nc; ++i) l += exp(s[i] - m);
+                    for (int64_t i = 0; i < nc; ++i) {
+                        double dp = 0.0;
+                        for (int64_t c = 0; c < d; ++c) dp += sgc * dO[r * d + c] * Vc[((b * nb + i) * H + hh) * d + c];
+                        D += exp(s[i] - m) / l * dp;
+                    }
+                    for (int64_t i = 0; i < nc; ++i) {
+                        const double p = exp(s[i] - m) / l;
+                        double dp = 0.0;
+                        for (int64_t c = 0; c < d; ++c) dp += sgc * dO[r * d + c] * Vc[((b * nb + i) * H + hh) * d + c];
+                        const double ds = p * (dp - D);
+                        for (int64_t c = 0; c < d; ++c) {
+                            dQ[r * d + c] += scale * ds * Kc[((b * nb + i) * H + hh) * d + c];
+                            dKc[((b * nb + i) * H + hh) * d + c] += scale * ds * q[c];
+                            dVc[((b * nb + i) * H + hh) * d + c] += p * sgc * dO[r * d + c];
+                        }
+                    }
+                }
+                /* slc */
+                const int64_t* sl = sel + ((b * H + hh) * N + t) * (nsel + 1);
+                double m = -INFINITY, l = 0.0, D = 0.0;
+                for (int64_t k = 0; k <= nsel; ++k)
+                    for (int64_t j = sl[k] * blk; sl[k] >= 0 && j < (sl[k] + 1) * blk && j <= t; ++j) {
+                        double s = 0.0;
+                        for (int64_t c = 0; c < d; ++c) s += q[c] * K[((b * N + j) * H + hh) * d + c];
+                        m = scale * s > m ? scale * s : m;
+                    }
+                for (int64_t k = 0; k <= nsel; ++k)
+                    for (int64_t j = sl[k] * blk; sl[k] >= 0 && j < (sl[k] + 1) * blk && j <= t; ++j) {
+                        double s = 0.0, dp = 0.0;
+                        for (int64_t c = 0; c < d; ++c) {
+                            s += q[c] * K[((b * N + j) * H + hh) * d + c];
+                            dp += sgs * dO[r * d + c] * V[((b * N + j) * H + hh) * d + c];
+                        }
+                        l += exp(scale * s - m);
+                        D += exp(scale * s - m) * dp;
+                    }
+                D /= l;
+                for (int64_t k = 0; k <= nsel; ++k)
+                    for (int64_t j = sl[k] * blk; sl[k] >= 0 && j < (sl[k] + 1) * blk && j <= t; ++j) {
+                        double s = 0.0, dp = 0.0;
+                        for (int64_t c = 0; c < d; ++c) {
+                            s += q[c] * K[((b * N + j) * H + hh) * d + c];
+                            dp += sgs * dO[r * d + c] * V[((b * N + j) * H + hh) * d + c];
+                        }
+                        const double p = exp(scale * s - m) / l, ds = p * (dp - D);
+                        for (int64_t c = 0; c < d; ++c) {
+                            dQ[r * d + c] += scale * ds * K[((b * N + j) * H + hh) * d + c];
+                            dK[((b * N + j) * H + hh) * d + c] += scale * ds * q[c];
+                            dV[((b * N + j) * H + hh) * d + c] += p * sgs * dO[r * d + c];
+                        }
+                    }
+            }
+    /* compression: block means spread back */
+    for (int64_t b = 0; b < B; ++b)
+        for (int64_t i = 0; i < nb; ++i)
+            for (int64_t hh = 0; hh < H; ++hh)
+                for (int64_t c = 0; c < d; ++c)
+                    for (int64_t j = i * blk; j < (i + 1) * blk; ++j) {
+                        dK[((b * N + j) * H + hh) * d + c] += dKc[((b * nb + i) * H + hh) * d + c] / (double)blk;
+                        dV[((b * N + j) * H + hh) * d + c] += dVc[((b * nb + i) * H + hh) * d + c] / (double)blk;
+                    }
+    free(Kc); free(Vc); free(dKc); free(dVc); free(Oc); free(Os); free(Ol); free(L); free(sc);
+    free(dOl); free(dQl); free(dKl); free(dVl);
+}

@@ -529,3 +529,26 @@ def test_nsa_combine_gates():
     g = np.zeros(shape[:3] + (3,))
     g[..., 0], g[..., 1], g[..., 2] = -800.0, 0.0, 800.0
     assert np.allclose(oracle.nsa_combine(a, s, l, g), 0.5 * s + l, atol=1e-14)
+
+
+def test_nsa_bwd_finite_differences():
+    """NSA chain rule for a fixed selection vs central FD of sum(O * W): dQ, dK, dV, dU
+    (through the local branch's gate), dgates."""
+    B, N, H, d, w, blk, nsel = 1, 12, 1, 4, 5, 3, 2
+    Q, K, V = _rand((B, N, H, d), 180), _rand((B, N, H, d), 181), _rand((B, N, H, d), 182)
+    U = -np.cumsum(0.2 + np.abs(_rand((B, H, N), 183)), -1)
+    g = _rand((B, N, H, 3), 184)
+    W = _rand((B, N, H, d), 185)
+    Kc, Vc = oracle.nsa_compress(K, V, blk)
+    _, sc = oracle.nsa_cmp(Q, Kc, Vc, blk)
+    sel = oracle.nsa_select(sc, N, blk, nsel)
+    dQ, dK, dV, dU, dg = oracle.nsa_bwd(Q, K, V, U, g, W, sel, w, blk)
+    loss = lambda q, k, v, u, gg: float(np.sum(oracle.nsa_fwd_fixed(q, k, v, u, gg, sel, w, blk) * W))  # noqa: E731
+    for idx in [(0, t, 0, c) for t in range(N) for c in range(d)]:
+        assert _fd(lambda x: loss(x, K, V, U, g), Q, idx) == pytest.approx(dQ[idx], rel=1e-6, abs=1e-8)
+        assert _fd(lambda x: loss(Q, x, V, U, g), K, idx) == pytest.approx(dK[idx], rel=1e-6, abs=1e-8)
+        assert _fd(lambda x: loss(Q, K, x, U, g), V, idx) == pytest.approx(dV[idx], rel=1e-6, abs=1e-8)
+    for idx in [(0, 0, t) for t in range(N)]:
+        assert _fd(lambda x: loss(Q, K, V, x, g), U, idx) == pytest.approx(dU[idx], rel=1e-6, abs=1e-8)
+    for idx in [(0, t, 0, c) for t in range(N) for c in range(3)]:
+        assert _fd(lambda x: loss(Q, K, V, U, x), g, idx) == pytest.approx(dg[idx], rel=1e-6, abs=1e-8)
