@@ -239,6 +239,19 @@ typedef struct {
     gfwa_dtype_t dtype; /* GFWA_BF16 */
 } gfwa_nsa_desc_t;
 
+/* Tensors the forward keeps for the backward (caller-owned; NULL members are
+ * kept in the workspace, i.e. not available to a later gfwa_nsa_bwd). */
+typedef struct {
+    float* O_cmp;   /* [B,N,H,d] fp32 compressed-branch output */
+    float* O_slc;   /* [B,N,H,d] fp32 selected-branch output */
+    float* LSE_cmp; /* [B,H,N] fp32 (-inf where no block is complete) */
+    float* LSE_slc; /* [B,H,N] fp32 */
+    int32_t* sel;   /* [B,H,N,n_sel+1] selected blocks: own block first, -1 pads */
+    void* O_loc;    /* [B,N,H,d] bf16 local (GatedFWA) branch output */
+    void* O_loc_lo; /* [B,N,H,d] bf16 residual of O_loc's cast (C-12) */
+    float* LSE_loc; /* [B,H,N] fp32 */
+} gfwa_nsa_saved_t;
+
 /*
  * gfwa_nsa_fwd -- forward of the hybrid:
  *   O = sigmoid(g0) o_cmp + sigmoid(g1) o_slc + sigmoid(g2) o_loc
@@ -249,15 +262,28 @@ typedef struct {
  * attention over the tokens <= t of the selected blocks: the query's own block
  * plus the n_sel complete blocks with the largest compressed-attention scores
  * scale q.Kc_i (reading C-29; ties to the lower index).  Q, K, V, O [B,N,H,d]
- * bf16 packed; U [B,H,N] fp32; gates [B,N,H,3] fp32 logits.  Optional
- * outputs (NULL to skip): O_cmp, O_slc [B,N,H,d] fp32, sel [B,H,N,n_sel+1]
- * int32 (the own block first, -1 pads), O_loc [B,N,H,d] bf16.  N / block <=
- * 512.  The compressed and selected branches run on CUDA-core kernels.
+ * bf16 packed; U [B,H,N] fp32; gates [B,N,H,3] fp32 logits.  `saved`
+ * (nullable) receives the tensors gfwa_nsa_bwd needs.  N / block <= 512.  The
+ * compressed and selected branches run on CUDA-core kernels.
  */
 size_t gfwa_nsa_workspace_size(const gfwa_nsa_desc_t* desc);
 gfwa_status_t gfwa_nsa_fwd(const gfwa_nsa_desc_t* desc, const void* Q, const void* K, const void* V,
-                           const float* U, const float* gates, void* O, float* O_cmp, float* O_slc,
-                           int32_t* sel, void* O_loc, void* ws, size_t ws_bytes, gfwa_stream_t stream);
+                           const float* U, const float* gates, void* O, const gfwa_nsa_saved_t* saved, void* ws,
+                           size_t ws_bytes, gfwa_stream_t stream);
+
+/*
+ * gfwa_nsa_bwd -- the chain rule of gfwa_nsa_fwd for its (fixed) selection:
+ * dgates [B,N,H,3] fp32 (sigmoid'(g_c) dO . o_c), the local branch by
+ * gfwa_bwd on sigmoid(g2) dO (dU [B,H,N] from it alone), the compressed branch
+ * (query side per query, block side per block, spread back through the block
+ * mean) and the selected branch (dK, dV of the selected tokens by fp32
+ * atomics); dQ, dK, dV [B,N,H,d] bf16 are the sums.  `saved` must hold every
+ * member, as written by gfwa_nsa_fwd on the same inputs.
+ */
+gfwa_status_t gfwa_nsa_bwd(const gfwa_nsa_desc_t* desc, const void* Q, const void* K, const void* V,
+                           const float* U, const float* gates, const void* dO, const gfwa_nsa_saved_t* saved,
+                           void* dQ, void* dK, void* dV, float* dU, float* dgates, void* ws, size_t ws_bytes,
+                           gfwa_stream_t stream);
 
 /* ------------------------------------------------------------------------- */
 /* AttnLayer output epilogue fused into the attention kernels:     */

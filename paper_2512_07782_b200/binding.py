@@ -72,6 +72,12 @@ class NsaDesc(ctypes.Structure):
                 ("dtype", ctypes.c_int32)]
 
 
+class NsaSaved(ctypes.Structure):
+    """gfwa_nsa_saved_t: the tensors gfwa_nsa_fwd keeps for gfwa_nsa_bwd."""
+    _fields_ = [(n, ctypes.c_void_p) for n in ("O_cmp", "O_slc", "LSE_cmp", "LSE_slc", "sel", "O_loc", "O_loc_lo",
+                                               "LSE_loc")]
+
+
 class NormGate(ctypes.Structure):
     """gfwa_normgate_t (include/gfwa.h): the AttnLayer epilogue's inputs (C-27)."""
     _fields_ = [("g", ctypes.c_void_p), ("gamma", ctypes.c_void_p), ("eps", ctypes.c_float),
@@ -108,6 +114,7 @@ EXPORTED = (
     "gfwa_bwd_normgate",
     "gfwa_bwd_rows_f32",
     "gfwa_nsa_fwd",
+    "gfwa_nsa_bwd",
     "gfwa_nsa_workspace_size",
 )
 
@@ -148,7 +155,10 @@ def load() -> ctypes.CDLL:
         lib.gfwa_nsa_workspace_size.restype = sz
         lib.gfwa_nsa_workspace_size.argtypes = [ctypes.POINTER(NsaDesc)]
         lib.gfwa_nsa_fwd.restype = ctypes.c_int
-        lib.gfwa_nsa_fwd.argtypes = [ctypes.POINTER(NsaDesc)] + [_VP] * 11 + [sz, _VP]
+        lib.gfwa_nsa_fwd.argtypes = [ctypes.POINTER(NsaDesc)] + [_VP] * 6 + [ctypes.POINTER(NsaSaved), _VP, sz, _VP]
+        lib.gfwa_nsa_bwd.restype = ctypes.c_int
+        lib.gfwa_nsa_bwd.argtypes = [ctypes.POINTER(NsaDesc)] + [_VP] * 6 + [ctypes.POINTER(NsaSaved)] + [_VP] * 6 + \
+            [sz, _VP]
         lib.gfwa_bwd_rows_f32.restype = ctypes.c_int
         lib.gfwa_bwd_rows_f32.argtypes = [ctypes.POINTER(AttnDesc)] + [_VP] * 14 + [_I64, _VP, _I64, _VP, _VP, sz, _VP]
         lib.gfwa_fwd_normgate.restype = ctypes.c_int
@@ -479,32 +489,54 @@ def gfwa_bwd_rows_f32(Q, K, V, U, O, LSE, dO, w: int, head_rows: int, tail_rows:
     return dQ, dK, dV, dU, head, tail
 
 
-def gfwa_nsa_fwd(Q, K, V, U, gates, w: int, block: int = 64, n_sel: int = 16, scale: float | None = None,
-                 want_branches: bool = False):
+def gfwa_nsa_fwd(Q, K, V, U, gates, w: int, block: int = 64, n_sel: int = 16, scale: float | None = None):
     """NSA hybrid forward with GatedFWA as the local branch (App. B; readings
     C-28, C-29): O = sigmoid(g0) o_cmp + sigmoid(g1) o_slc + sigmoid(g2) o_gatedfwa.
-    Q, K, V [B,N,H,d] bf16; U [B,H,N]; gates [B,N,H,3] fp32 logits.  Returns O, or
-    (O, o_cmp, o_slc, sel, o_loc) with want_branches."""
+    Q, K, V [B,N,H,d] bf16; U [B,H,N]; gates [B,N,H,3] fp32 logits.  Returns (O, saved):
+    saved is a dict of the tensors gfwa_nsa_bwd needs (o_cmp, o_slc, the LSEs, the
+    selection, the local branch's output and residual)."""
     lib = load()
     _need_cuda(Q, K, V, U, gates)
     B, N, H, d = Q.shape
     dev = Q.device
     Q, K, V = Q.contiguous(), K.contiguous(), V.contiguous()
+    U, gates = U.contiguous(), gates.float().contiguous()
     O = torch.empty_like(Q)
-    oc = os_ = sel = ol = None
-    if want_branches:
-        oc = torch.empty(B, N, H, d, dtype=torch.float32, device=dev)
-        os_ = torch.empty_like(oc)
-        sel = torch.empty(B, H, N, n_sel + 1, dtype=torch.int32, device=dev)
-        ol = torch.empty_like(Q)
+    f32 = lambda *sh: torch.empty(*sh, dtype=torch.float32, device=dev)  # noqa: E731
+    sv = {"O_cmp": f32(B, N, H, d), "O_slc": f32(B, N, H, d), "LSE_cmp": f32(B, H, N), "LSE_slc": f32(B, H, N),
+          "sel": torch.empty(B, H, N, n_sel + 1, dtype=torch.int32, device=dev), "O_loc": torch.empty_like(Q),
+          "O_loc_lo": torch.empty_like(Q), "LSE_loc": f32(B, H, N)}
+    saved = NsaSaved(*[_ptr(sv[n]) for n, _ in NsaSaved._fields_])
     dsc = NsaDesc(B, H, N, d, w, block, n_sel, -1.0 if scale is None else float(scale), GFWA_BF16)
     nbytes = lib.gfwa_nsa_workspace_size(ctypes.byref(dsc))
     ws = workspace(nbytes, dev, "nsa")
-    U, gates = U.contiguous(), gates.float().contiguous()
-    st = lib.gfwa_nsa_fwd(ctypes.byref(dsc), _ptr(Q), _ptr(K), _ptr(V), _ptr(U), _ptr(gates), _ptr(O), _ptr(oc),
-                          _ptr(os_), _ptr(sel), _ptr(ol), _ptr(ws), nbytes, _stream(dev))
+    st = lib.gfwa_nsa_fwd(ctypes.byref(dsc), _ptr(Q), _ptr(K), _ptr(V), _ptr(U), _ptr(gates), _ptr(O),
+                          ctypes.byref(saved), _ptr(ws), nbytes, _stream(dev))
     _check(st, "gfwa_nsa_fwd")
-    return (O, oc, os_, sel, ol) if want_branches else O
+    return O, sv
+
+
+def gfwa_nsa_bwd(Q, K, V, U, gates, dO, saved, w: int, block: int = 64, n_sel: int = 16,
+                 scale: float | None = None):
+    """The NSA hybrid's backward (fixed selection): (dQ, dK, dV, dU, dgates)."""
+    lib = load()
+    _need_cuda(Q, K, V, U, gates, dO)
+    B, N, H, d = Q.shape
+    dev = Q.device
+    Q, K, V, dO = Q.contiguous(), K.contiguous(), V.contiguous(), dO.contiguous()
+    U, gates = U.contiguous(), gates.float().contiguous()
+    dQ, dK, dV = torch.empty_like(Q), torch.empty_like(K), torch.empty_like(V)
+    dU = torch.empty(B, H, N, dtype=torch.float32, device=dev)
+    dg = torch.empty(B, N, H, 3, dtype=torch.float32, device=dev)
+    sv = NsaSaved(*[_ptr(saved[n]) for n, _ in NsaSaved._fields_])
+    dsc = NsaDesc(B, H, N, d, w, block, n_sel, -1.0 if scale is None else float(scale), GFWA_BF16)
+    nbytes = lib.gfwa_nsa_workspace_size(ctypes.byref(dsc))
+    ws = workspace(nbytes, dev, "nsa")
+    st = lib.gfwa_nsa_bwd(ctypes.byref(dsc), _ptr(Q), _ptr(K), _ptr(V), _ptr(U), _ptr(gates), _ptr(dO),
+                          ctypes.byref(sv), _ptr(dQ), _ptr(dK), _ptr(dV), _ptr(dU), _ptr(dg), _ptr(ws), nbytes,
+                          _stream(dev))
+    _check(st, "gfwa_nsa_bwd")
+    return dQ, dK, dV, dU, dg
 
 
 def gfwa_attn_path(Q, K, V, w: int) -> int:

@@ -454,12 +454,22 @@ extern "C" gfwa_status_t gfwa_bwd_rows_f32(const gfwa_attn_desc_t* desc, const v
 }
 
 // ---------------------------------------------------------------------------
-// NSA extension (App. B; readings C-28, C-29), forward
+// NSA extension (App. B; readings C-28, C-29)
 namespace gfwa {
 size_t nsa_workspace(int64_t B, int64_t N, int64_t H, int d, int blk, int nsel);
 gfwa_status_t nsa_fwd_branches(const void* Q, const void* K, const void* V, const float* g, int64_t B, int64_t N,
                                int64_t H, int d, int blk, int nsel, float scale, float* Kc, float* Vc, float* Ocmp,
-                               float* Oslc, int* sel, const void* Oloc, void* O, cudaStream_t st);
+                               float* Oslc, float* Lcmp, float* Lslc, int* sel, const void* Oloc, void* O,
+                               cudaStream_t st, bool compress_only = false);
+gfwa_status_t nsa_bwd_combine(const void* dO, const float* g, const float* Ocmp, const float* Oslc, const void* Oloc,
+                              const void* Ololo, float* dOc, float* dOs, void* dOl, float* dg, float* Dc, float* Ds,
+                              int64_t B, int64_t N, int64_t H, int d, cudaStream_t st);
+gfwa_status_t nsa_bwd_branches(const void* Q, const void* K, const void* V, const int* sel, const float* Kc,
+                               const float* Vc, const float* dOc, const float* dOs, const float* Lc, const float* Ls,
+                               const float* Dc, const float* Ds, float* dQacc, float* dKacc, float* dVacc, float* dKc,
+                               float* dVc, const void* dQl, const void* dKl, const void* dVl, void* dQ, void* dK,
+                               void* dV, int64_t B, int64_t N, int64_t H, int d, int blk, int nsel, float scale,
+                               cudaStream_t st);
 bool nsa_blocks_ok(int64_t N, int blk);
 }  // namespace gfwa
 
@@ -469,55 +479,135 @@ bool nsa_desc_ok(const gfwa_nsa_desc_t* d) {
            (d->d == 64 || d->d == 128) && d->dtype == GFWA_BF16 && nsa_blocks_ok(d->N, d->block) &&
            d->B * d->N * d->H < ((int64_t)1 << 31) && d->scale == d->scale;
 }
+gfwa_attn_desc_t nsa_local_desc(const gfwa_nsa_desc_t* d) {
+    gfwa_attn_desc_t ad{};
+    ad.B = d->B;
+    ad.H = d->H;
+    ad.N_q = d->N;
+    ad.N_kv = d->N;
+    ad.d = d->d;
+    ad.w = d->w;
+    ad.scale = d->scale;
+    ad.dtype = GFWA_BF16;
+    const int64_t st3[3] = {d->N * d->H * d->d, d->H * d->d, d->d};
+    for (int i = 0; i < 3; ++i) ad.q_stride[i] = ad.k_stride[i] = ad.v_stride[i] = ad.o_stride[i] = st3[i];
+    return ad;
+}
+// bump allocator over the caller's workspace (256-byte aligned pieces)
+struct Carve {
+    char* p;
+    void* take(size_t bytes) {
+        char* r = p;
+        p += (bytes + 255) & ~(size_t)255;
+        return r;
+    }
+};
+size_t nsa_bwd_bytes(const gfwa_nsa_desc_t* d) {
+    const size_t n = (size_t)d->B * d->N * d->H * d->d, rows = (size_t)d->B * d->N * d->H;
+    const size_t nbk = (size_t)d->B * (d->N / d->block) * d->H * d->d;
+    auto r = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    gfwa_attn_desc_t ad = nsa_local_desc(d);
+    return r(nbk * 4) * 4 + r(n * 4) * 5 + r(n * 2) * 4 + r(rows * 4) * 2 + r(gfwa_bwd_workspace_size(&ad));
+}
 }  // namespace
 
 extern "C" size_t gfwa_nsa_workspace_size(const gfwa_nsa_desc_t* d) {
     if (!nsa_desc_ok(d)) return 256;
-    return nsa_workspace(d->B, d->N, d->H, d->d, d->block, d->n_sel) + 256;
+    const size_t f = nsa_workspace(d->B, d->N, d->H, d->d, d->block, d->n_sel);
+    const size_t b = nsa_bwd_bytes(d);
+    return (f > b ? f : b) + 256;
 }
 
 extern "C" gfwa_status_t gfwa_nsa_fwd(const gfwa_nsa_desc_t* d, const void* Q, const void* K, const void* V,
-                                      const float* U, const float* gates, void* O, float* O_cmp, float* O_slc,
-                                      int32_t* sel, void* O_loc, void* ws, size_t ws_bytes, gfwa_stream_t stream) {
+                                      const float* U, const float* gates, void* O, const gfwa_nsa_saved_t* saved,
+                                      void* ws, size_t ws_bytes, gfwa_stream_t stream) {
     if (!d) return GFWA_ERR_INVALID_ARGUMENT;
     if (d->d != 64 && d->d != 128) return GFWA_ERR_UNSUPPORTED;
     if (d->dtype != GFWA_BF16) return GFWA_ERR_UNSUPPORTED;
     GFWA_REQUIRE(nsa_desc_ok(d));
     GFWA_REQUIRE(Q && K && V && U && gates && O && ws && (uintptr_t)ws % 256 == 0);
-    GFWA_REQUIRE(al16(Q) && al16(K) && al16(V) && al16(O) && (!O_loc || al16(O_loc)));
+    GFWA_REQUIRE(al16(Q) && al16(K) && al16(V) && al16(O));
     if (ws_bytes < gfwa_nsa_workspace_size(d)) return GFWA_ERR_WORKSPACE;
     const int64_t B = d->B, N = d->N, H = d->H, nb = N / d->block;
-    char* p = (char*)ws;
-    auto take = [&](size_t bytes) {
-        char* r = p;
-        p += (bytes + 255) & ~(size_t)255;
-        return (void*)r;
-    };
-    float* Kc = (float*)take((size_t)B * nb * H * d->d * 4);
+    Carve cv{(char*)ws};
+    float* Kc = (float*)cv.take((size_t)B * nb * H * d->d * 4 * 2);
     float* Vc = Kc + (size_t)B * nb * H * d->d;
-    float* oc = (float*)take((size_t)B * N * H * d->d * 4 * 2);
+    float* oc = (float*)cv.take((size_t)B * N * H * d->d * 4 * 2);
     float* os = oc + (size_t)B * N * H * d->d;
-    int* sl = (int*)take((size_t)B * H * N * (d->n_sel + 1) * 4);
-    void* ol = take((size_t)B * N * H * d->d * 2);
-    float* lse = (float*)take((size_t)B * H * N * 4);
-    if (O_cmp) oc = O_cmp;
-    if (O_slc) os = O_slc;
-    if (sel) sl = sel;
-    if (O_loc) ol = O_loc;
+    int* sl = (int*)cv.take((size_t)B * H * N * (d->n_sel + 1) * 4);
+    void* ol = cv.take((size_t)B * N * H * d->d * 2);
+    float* lse = (float*)cv.take((size_t)B * H * N * 4 * 3);
+    float *lc = lse + B * H * N, *ls = lc + B * H * N;
+    void* olo = nullptr;
+    if (saved) {
+        if (saved->O_cmp) oc = saved->O_cmp;
+        if (saved->O_slc) os = saved->O_slc;
+        if (saved->sel) sl = saved->sel;
+        if (saved->O_loc) ol = saved->O_loc;
+        if (saved->LSE_loc) lse = saved->LSE_loc;
+        if (saved->LSE_cmp) lc = saved->LSE_cmp;
+        if (saved->LSE_slc) ls = saved->LSE_slc;
+        olo = saved->O_loc_lo;
+        GFWA_REQUIRE(al16(ol) && (!olo || al16(olo)));
+    }
     // the local branch: GatedFWA itself (gfwa_fwd)
-    gfwa_attn_desc_t ad{};
-    ad.B = B;
-    ad.H = H;
-    ad.N_q = N;
-    ad.N_kv = N;
-    ad.d = d->d;
-    ad.w = d->w;
-    ad.scale = d->scale;
-    ad.dtype = GFWA_BF16;
-    const int64_t st3[3] = {N * H * d->d, H * d->d, d->d};
-    for (int i = 0; i < 3; ++i) ad.q_stride[i] = ad.k_stride[i] = ad.v_stride[i] = ad.o_stride[i] = st3[i];
-    if (gfwa_status_t s = gfwa_fwd(&ad, Q, K, V, U, ol, nullptr, lse, stream)) return s;
+    gfwa_attn_desc_t ad = nsa_local_desc(d);
+    if (gfwa_status_t s = gfwa_fwd(&ad, Q, K, V, U, ol, olo, lse, stream)) return s;
     const float scale = d->scale > 0.f ? d->scale : 1.f / std::sqrt((float)d->d);
-    return nsa_fwd_branches(Q, K, V, gates, B, N, H, d->d, d->block, d->n_sel, scale, Kc, Vc, oc, os, sl, ol, O,
-                            (cudaStream_t)stream);
+    return nsa_fwd_branches(Q, K, V, gates, B, N, H, d->d, d->block, d->n_sel, scale, Kc, Vc, oc, os, lc, ls, sl, ol,
+                            O, (cudaStream_t)stream);
+}
+
+extern "C" gfwa_status_t gfwa_nsa_bwd(const gfwa_nsa_desc_t* d, const void* Q, const void* K, const void* V,
+                                      const float* U, const float* gates, const void* dO,
+                                      const gfwa_nsa_saved_t* sv, void* dQ, void* dK, void* dV, float* dU,
+                                      float* dgates, void* ws, size_t ws_bytes, gfwa_stream_t stream) {
+    if (!d) return GFWA_ERR_INVALID_ARGUMENT;
+    if (d->d != 64 && d->d != 128) return GFWA_ERR_UNSUPPORTED;
+    if (d->dtype != GFWA_BF16) return GFWA_ERR_UNSUPPORTED;
+    GFWA_REQUIRE(nsa_desc_ok(d));
+    GFWA_REQUIRE(Q && K && V && U && gates && dO && sv && dQ && dK && dV && dU && dgates && ws);
+    GFWA_REQUIRE(sv->O_cmp && sv->O_slc && sv->LSE_cmp && sv->LSE_slc && sv->sel && sv->O_loc && sv->LSE_loc);
+    GFWA_REQUIRE((uintptr_t)ws % 256 == 0 && al16(Q) && al16(K) && al16(V) && al16(dO) && al16(dQ) && al16(dK) &&
+                 al16(dV) && al16(sv->O_loc) && (!sv->O_loc_lo || al16(sv->O_loc_lo)));
+    if (ws_bytes < gfwa_nsa_workspace_size(d)) return GFWA_ERR_WORKSPACE;
+    const int64_t B = d->B, N = d->N, H = d->H, nb = N / d->block;
+    const size_t n = (size_t)B * N * H * d->d, rows = (size_t)B * N * H, nbk = (size_t)B * nb * H * d->d;
+    cudaStream_t st = (cudaStream_t)stream;
+    Carve cv{(char*)ws};
+    float* Kc = (float*)cv.take(nbk * 4);
+    float* Vc = (float*)cv.take(nbk * 4);
+    float* dKc = (float*)cv.take(nbk * 4);
+    float* dVc = (float*)cv.take(nbk * 4);
+    float* dOc = (float*)cv.take(n * 4);
+    float* dOs = (float*)cv.take(n * 4);
+    float* dQacc = (float*)cv.take(n * 4);
+    float* dKacc = (float*)cv.take(n * 4);
+    float* dVacc = (float*)cv.take(n * 4);
+    void* dOl = cv.take(n * 2);
+    void* dQl = cv.take(n * 2);
+    void* dKl = cv.take(n * 2);
+    void* dVl = cv.take(n * 2);
+    float* Dc = (float*)cv.take(rows * 4);
+    float* Ds = (float*)cv.take(rows * 4);
+    gfwa_attn_desc_t ad = nsa_local_desc(d);
+    const size_t lws = gfwa_bwd_workspace_size(&ad);
+    void* lw = cv.take(lws);
+    const float scale = d->scale > 0.f ? d->scale : 1.f / std::sqrt((float)d->d);
+    gfwa_status_t s;
+    if ((s = nsa_bwd_combine(dO, gates, sv->O_cmp, sv->O_slc, sv->O_loc, sv->O_loc_lo, dOc, dOs, dOl, dgates, Dc, Ds,
+                             B, N, H, d->d, st)))
+        return s;
+    // the local branch: Alg. E.2 on sigmoid(g2) dO
+    if ((s = gfwa_bwd(&ad, Q, K, V, U, sv->O_loc, sv->O_loc_lo, sv->LSE_loc, dOl, dQl, dKl, dVl, dU, nullptr, nullptr,
+                      lw, lws, stream)))
+        return s;
+    // block means of K, V again (the compressed branch's keys and values)
+    if (nb > 0) {
+        if ((s = nsa_fwd_branches(Q, K, V, gates, B, N, H, d->d, d->block, 0, scale, Kc, Vc, nullptr, nullptr, nullptr,
+                                  nullptr, nullptr, nullptr, nullptr, st, true)))
+            return s;
+    }
+    return nsa_bwd_branches(Q, K, V, sv->sel, Kc, Vc, dOc, dOs, sv->LSE_cmp, sv->LSE_slc, Dc, Ds, dQacc, dKacc, dVacc,
+                            dKc, dVc, dQl, dKl, dVl, dQ, dK, dV, B, N, H, d->d, d->block, d->n_sel, scale, st);
 }

@@ -20,6 +20,11 @@ namespace gfwa {
 namespace {
 
 constexpr int kWarpsPerBlock = 8;
+
+__device__ __forceinline__ uint32_t pack_bf16x2_nsa(float lo, float hi) {
+    __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<uint32_t*>(&v);
+}
 constexpr int kMaxBlocks = 512;  // compressed blocks per sequence held in shared memory per warp
 
 __global__ void nsa_compress_kernel(const __nv_bfloat16* __restrict__ K, const __nv_bfloat16* __restrict__ V,
@@ -61,8 +66,8 @@ __device__ __forceinline__ void load_row(const __nv_bfloat16* p, int lane, float
 template <int D>
 __global__ void __launch_bounds__(32 * kWarpsPerBlock) nsa_cmp_select_kernel(
     const __nv_bfloat16* __restrict__ Q, const float* __restrict__ Kc, const float* __restrict__ Vc,
-    float* __restrict__ Ocmp, int* __restrict__ sel, int64_t B, int64_t N, int64_t H, int blk, int nsel,
-    float scale) {
+    float* __restrict__ Ocmp, float* __restrict__ Lcmp, int* __restrict__ sel, int64_t B, int64_t N, int64_t H,
+    int blk, int nsel, float scale) {
     constexpr int C = D / 32;
     __shared__ float s_sc[kWarpsPerBlock][kMaxBlocks];
     const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
@@ -96,6 +101,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) nsa_cmp_select_kernel(
     float* o = Ocmp + row * D + C * lane;
 #pragma unroll
     for (int c = 0; c < C; ++c) o[c] = nc > 0 ? acc[c] / l : 0.f;
+    if (lane == 0) Lcmp[(b * H + hh) * N + t] = nc > 0 ? m + __logf(l) : -INFINITY;
     __syncwarp();
     // selection (C-29): own block first, then n_sel arg-max rounds over the other complete blocks
     const int own = (int)(t / blk);
@@ -133,8 +139,8 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) nsa_cmp_select_kernel(
 template <int D>
 __global__ void __launch_bounds__(32 * kWarpsPerBlock) nsa_slc_kernel(
     const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __restrict__ K, const __nv_bfloat16* __restrict__ V,
-    const int* __restrict__ sel, float* __restrict__ Oslc, int64_t B, int64_t N, int64_t H, int blk, int nsel,
-    float scale) {
+    const int* __restrict__ sel, float* __restrict__ Oslc, float* __restrict__ Lslc, int64_t B, int64_t N, int64_t H,
+    int blk, int nsel, float scale) {
     constexpr int C = D / 32;
     const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
     const int64_t row = (int64_t)blockIdx.x * kWarpsPerBlock + wp;
@@ -170,6 +176,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) nsa_slc_kernel(
     float* o = Oslc + row * D + C * lane;
 #pragma unroll
     for (int c = 0; c < C; ++c) o[c] = acc[c] / l;  // the own block always holds token t: l > 0
+    if (lane == 0) Lslc[(b * H + hh) * N + t] = m + __logf(l);
 }
 
 __global__ void nsa_combine_kernel(const float* __restrict__ Ocmp, const float* __restrict__ Oslc,
@@ -184,6 +191,229 @@ __global__ void nsa_combine_kernel(const float* __restrict__ Ocmp, const float* 
     }
 }
 
+
+// ------------------------------------------------------------------ backward (fixed selection)
+
+// per row: the branch gradients of the gated sum and the rows' D terms
+template <int D>
+__global__ void __launch_bounds__(32 * kWarpsPerBlock) nsa_combine_bwd_kernel(
+    const __nv_bfloat16* __restrict__ dO, const float* __restrict__ g, const float* __restrict__ Ocmp,
+    const float* __restrict__ Oslc, const __nv_bfloat16* __restrict__ Oloc, const __nv_bfloat16* __restrict__ Ololo,
+    float* __restrict__ dOc, float* __restrict__ dOs, __nv_bfloat16* __restrict__ dOl, float* __restrict__ dg,
+    float* __restrict__ Dc, float* __restrict__ Ds, int64_t B, int64_t N, int64_t H) {
+    constexpr int C = D / 32;
+    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+    const int64_t row = (int64_t)blockIdx.x * kWarpsPerBlock + wp;
+    if (row >= B * N * H) return;
+    const int64_t hh = row % H, t = (row / H) % N, b = row / (H * N);
+    float go[C], ol[C], ll[C];
+    load_row<D>(dO + row * D, lane, go);
+    load_row<D>(Oloc + row * D, lane, ol);
+    if (Ololo) {
+        load_row<D>(Ololo + row * D, lane, ll);
+#pragma unroll
+        for (int c = 0; c < C; ++c) ol[c] += ll[c];
+    }
+    const float* oc = Ocmp + row * D + C * lane;
+    const float* os = Oslc + row * D + C * lane;
+    float sgm[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) sgm[k] = 1.f / (1.f + __expf(-g[3 * row + k]));
+    float dotc = 0.f, dots = 0.f, dotl = 0.f;
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+        dotc = fmaf(go[c], oc[c], dotc);
+        dots = fmaf(go[c], os[c], dots);
+        dotl = fmaf(go[c], ol[c], dotl);
+        dOc[row * D + C * lane + c] = sgm[0] * go[c];
+        dOs[row * D + C * lane + c] = sgm[1] * go[c];
+    }
+    if constexpr (C == 4) {
+        uint2 w;
+        w.x = pack_bf16x2_nsa(sgm[2] * go[0], sgm[2] * go[1]);
+        w.y = pack_bf16x2_nsa(sgm[2] * go[2], sgm[2] * go[3]);
+        *reinterpret_cast<uint2*>(dOl + row * D + 4 * lane) = w;
+    } else {
+        *reinterpret_cast<uint32_t*>(dOl + row * D + 2 * lane) = pack_bf16x2_nsa(sgm[2] * go[0], sgm[2] * go[1]);
+    }
+    dotc = warp_sum(dotc);
+    dots = warp_sum(dots);
+    dotl = warp_sum(dotl);
+    if (lane == 0) {
+        dg[3 * row] = sgm[0] * (1.f - sgm[0]) * dotc;
+        dg[3 * row + 1] = sgm[1] * (1.f - sgm[1]) * dots;
+        dg[3 * row + 2] = sgm[2] * (1.f - sgm[2]) * dotl;
+        // D = rowsum(o * dO_branch): dO_branch = sigmoid(g) dO
+        Dc[(b * H + hh) * N + t] = sgm[0] * dotc;
+        Ds[(b * H + hh) * N + t] = sgm[1] * dots;
+    }
+}
+
+// compressed branch, query side: dq = scale sum_i p_i (dO_cmp . Vc_i - D) Kc_i
+template <int D>
+__global__ void __launch_bounds__(32 * kWarpsPerBlock) nsa_cmp_dq_kernel(
+    const __nv_bfloat16* __restrict__ Q, const float* __restrict__ Kc, const float* __restrict__ Vc,
+    const float* __restrict__ dOc, const float* __restrict__ Lc, const float* __restrict__ Dc,
+    float* __restrict__ dQacc, int64_t B, int64_t N, int64_t H, int blk, float scale) {
+    constexpr int C = D / 32;
+    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+    const int64_t row = (int64_t)blockIdx.x * kWarpsPerBlock + wp;
+    if (row >= B * N * H) return;
+    const int64_t hh = row % H, t = (row / H) % N, b = row / (H * N);
+    const int64_t nb = N / blk;
+    const int nc = (int)((t + 1) / blk);
+    float q[C], go[C], dq[C];
+    load_row<D>(Q + row * D, lane, q);
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+        go[c] = dOc[row * D + C * lane + c];
+        dq[c] = 0.f;
+    }
+    const float L = Lc[(b * H + hh) * N + t], Dv = Dc[(b * H + hh) * N + t];
+    for (int i = 0; i < nc; ++i) {
+        const float* kr = Kc + ((b * nb + i) * H + hh) * D + C * lane;
+        const float* vr = Vc + ((b * nb + i) * H + hh) * D + C * lane;
+        float s = 0.f, dp = 0.f;
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            s = fmaf(q[c], kr[c], s);
+            dp = fmaf(go[c], vr[c], dp);
+        }
+        s = warp_sum(s) * scale;
+        dp = warp_sum(dp);
+        const float ds = __expf(s - L) * (dp - Dv);
+#pragma unroll
+        for (int c = 0; c < C; ++c) dq[c] = fmaf(scale * ds, kr[c], dq[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < C; ++c) dQacc[row * D + C * lane + c] = dq[c];
+}
+
+// compressed branch, block side (one warp per (b, block, h), every query that sees it):
+// dKc = scale sum_t dS q_t, dVc = sum_t p dO_cmp,t
+template <int D>
+__global__ void __launch_bounds__(32 * kWarpsPerBlock) nsa_cmp_dkv_kernel(
+    const __nv_bfloat16* __restrict__ Q, const float* __restrict__ Kc, const float* __restrict__ Vc,
+    const float* __restrict__ dOc, const float* __restrict__ Lc, const float* __restrict__ Dc,
+    float* __restrict__ dKc, float* __restrict__ dVc, int64_t B, int64_t N, int64_t H, int blk, float scale) {
+    constexpr int C = D / 32;
+    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+    const int64_t nb = N / blk;
+    const int64_t r = (int64_t)blockIdx.x * kWarpsPerBlock + wp;  // (b, i, h)
+    if (r >= B * nb * H) return;
+    const int64_t hh = r % H, i = (r / H) % nb, b = r / (H * nb);
+    float kc[C], vc[C], dk[C], dv[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+        kc[c] = Kc[r * D + C * lane + c];
+        vc[c] = Vc[r * D + C * lane + c];
+        dk[c] = 0.f;
+        dv[c] = 0.f;
+    }
+    for (int64_t t = (i + 1) * blk - 1; t < N; ++t) {
+        const int64_t row = (b * N + t) * H + hh;
+        float q[C], go[C];
+        load_row<D>(Q + row * D, lane, q);
+        float s = 0.f, dp = 0.f;
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            go[c] = dOc[row * D + C * lane + c];
+            s = fmaf(q[c], kc[c], s);
+            dp = fmaf(go[c], vc[c], dp);
+        }
+        s = warp_sum(s) * scale;
+        dp = warp_sum(dp);
+        const float p = __expf(s - Lc[(b * H + hh) * N + t]);
+        const float ds = p * (dp - Dc[(b * H + hh) * N + t]);
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            dk[c] = fmaf(scale * ds, q[c], dk[c]);
+            dv[c] = fmaf(p, go[c], dv[c]);
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+        dKc[r * D + C * lane + c] = dk[c];
+        dVc[r * D + C * lane + c] = dv[c];
+    }
+}
+
+// selected branch: dq into the query's row (added), dK / dV of the selected tokens by
+// fp32 atomics (a token is selected by a data-dependent set of queries)
+template <int D>
+__global__ void __launch_bounds__(32 * kWarpsPerBlock) nsa_slc_bwd_kernel(
+    const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __restrict__ K, const __nv_bfloat16* __restrict__ V,
+    const int* __restrict__ sel, const float* __restrict__ dOs, const float* __restrict__ Ls,
+    const float* __restrict__ Ds, float* __restrict__ dQacc, float* __restrict__ dKacc, float* __restrict__ dVacc,
+    int64_t B, int64_t N, int64_t H, int blk, int nsel, float scale) {
+    constexpr int C = D / 32;
+    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+    const int64_t row = (int64_t)blockIdx.x * kWarpsPerBlock + wp;
+    if (row >= B * N * H) return;
+    const int64_t hh = row % H, t = (row / H) % N, b = row / (H * N);
+    float q[C], go[C], dq[C];
+    load_row<D>(Q + row * D, lane, q);
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+        go[c] = dOs[row * D + C * lane + c];
+        dq[c] = 0.f;
+    }
+    const float L = Ls[(b * H + hh) * N + t], Dv = Ds[(b * H + hh) * N + t];
+    const int* sl = sel + ((b * H + hh) * N + t) * (nsel + 1);
+    for (int k = 0; k <= nsel; ++k) {
+        const int ib = sl[k];
+        if (ib < 0) continue;
+        const int64_t j1 = min64((int64_t)(ib + 1) * blk - 1, t);
+        for (int64_t j = (int64_t)ib * blk; j <= j1; ++j) {
+            const int64_t kr = (b * N + j) * H + hh;
+            float kv[C], vv[C];
+            load_row<D>(K + kr * D, lane, kv);
+            load_row<D>(V + kr * D, lane, vv);
+            float s = 0.f, dp = 0.f;
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                s = fmaf(q[c], kv[c], s);
+                dp = fmaf(go[c], vv[c], dp);
+            }
+            s = warp_sum(s) * scale;
+            dp = warp_sum(dp);
+            const float p = __expf(s - L), ds = p * (dp - Dv);
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                dq[c] = fmaf(scale * ds, kv[c], dq[c]);
+                atomicAdd(dKacc + kr * D + C * lane + c, scale * ds * q[c]);
+                atomicAdd(dVacc + kr * D + C * lane + c, p * go[c]);
+            }
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < C; ++c) dQacc[row * D + C * lane + c] += dq[c];
+}
+
+// dQ = dQ_loc + dQacc; dK = dK_loc + dKacc + dKc(block) / blk; dV likewise -> bf16
+__global__ void nsa_finalize_kernel(const __nv_bfloat16* __restrict__ dQl, const __nv_bfloat16* __restrict__ dKl,
+                                    const __nv_bfloat16* __restrict__ dVl, const float* __restrict__ dQacc,
+                                    const float* __restrict__ dKacc, const float* __restrict__ dVacc,
+                                    const float* __restrict__ dKc, const float* __restrict__ dVc,
+                                    __nv_bfloat16* __restrict__ dQ, __nv_bfloat16* __restrict__ dK,
+                                    __nv_bfloat16* __restrict__ dV, int64_t B, int64_t N, int64_t H, int d, int blk) {
+    const int64_t nb = N / blk, total = B * N * H * d;
+    const float inv = 1.f / (float)blk;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int c = (int)(e % d);
+        const int64_t r = e / d, hh = r % H, j = (r / H) % N, b = r / (H * N);
+        float kc = 0.f, vc = 0.f;
+        if (j / blk < nb) {
+            const int64_t x = ((b * nb + j / blk) * H + hh) * d + c;
+            kc = dKc[x] * inv;
+            vc = dVc[x] * inv;
+        }
+        dQ[e] = __float2bfloat16_rn(__bfloat162float(dQl[e]) + dQacc[e]);
+        dK[e] = __float2bfloat16_rn(__bfloat162float(dKl[e]) + dKacc[e] + kc);
+        dV[e] = __float2bfloat16_rn(__bfloat162float(dVl[e]) + dVacc[e] + vc);
+    }
+}
+
 }  // namespace
 
 size_t nsa_workspace(int64_t B, int64_t N, int64_t H, int d, int blk, int nsel) {
@@ -194,14 +424,15 @@ size_t nsa_workspace(int64_t B, int64_t N, int64_t H, int d, int blk, int nsel) 
     add((size_t)B * N * H * d * 4 * 2);     // o_cmp, o_slc
     add((size_t)B * H * N * (nsel + 1) * 4);  // selection
     add((size_t)B * N * H * d * 2);         // o_loc
-    add((size_t)B * H * N * 4);             // LSE of the local branch
+    add((size_t)B * H * N * 4 * 3);         // LSE of the local, compressed and selected branches
     return n;
 }
 
 // the branches and the combination; o_loc (bf16) was written by gfwa_fwd
 gfwa_status_t nsa_fwd_branches(const void* Q, const void* K, const void* V, const float* g, int64_t B, int64_t N,
                                int64_t H, int d, int blk, int nsel, float scale, float* Kc, float* Vc, float* Ocmp,
-                               float* Oslc, int* sel, const void* Oloc, void* O, cudaStream_t st) {
+                               float* Oslc, float* Lcmp, float* Lslc, int* sel, const void* Oloc, void* O,
+                               cudaStream_t st, bool compress_only) {
     int dev = 0, n_sm = 148;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
     const int64_t nb = N / blk;
@@ -210,20 +441,21 @@ gfwa_status_t nsa_fwd_branches(const void* Q, const void* K, const void* V, cons
             (const __nv_bfloat16*)K, (const __nv_bfloat16*)V, Kc, Vc, B, N, H, d, blk);
         note_launch();
     }
+    if (compress_only) return check_launch();
     const int64_t rows = B * N * H;
     const unsigned grid = (unsigned)((rows + kWarpsPerBlock - 1) / kWarpsPerBlock);
     if (d == 64) {
-        nsa_cmp_select_kernel<64><<<grid, 32 * kWarpsPerBlock, 0, st>>>((const __nv_bfloat16*)Q, Kc, Vc, Ocmp, sel, B,
-                                                                        N, H, blk, nsel, scale);
+        nsa_cmp_select_kernel<64><<<grid, 32 * kWarpsPerBlock, 0, st>>>((const __nv_bfloat16*)Q, Kc, Vc, Ocmp, Lcmp,
+                                                                        sel, B, N, H, blk, nsel, scale);
         nsa_slc_kernel<64><<<grid, 32 * kWarpsPerBlock, 0, st>>>((const __nv_bfloat16*)Q, (const __nv_bfloat16*)K,
-                                                                 (const __nv_bfloat16*)V, sel, Oslc, B, N, H, blk,
-                                                                 nsel, scale);
+                                                                 (const __nv_bfloat16*)V, sel, Oslc, Lslc, B, N, H,
+                                                                 blk, nsel, scale);
     } else {
-        nsa_cmp_select_kernel<128><<<grid, 32 * kWarpsPerBlock, 0, st>>>((const __nv_bfloat16*)Q, Kc, Vc, Ocmp, sel,
-                                                                         B, N, H, blk, nsel, scale);
+        nsa_cmp_select_kernel<128><<<grid, 32 * kWarpsPerBlock, 0, st>>>((const __nv_bfloat16*)Q, Kc, Vc, Ocmp, Lcmp,
+                                                                         sel, B, N, H, blk, nsel, scale);
         nsa_slc_kernel<128><<<grid, 32 * kWarpsPerBlock, 0, st>>>((const __nv_bfloat16*)Q, (const __nv_bfloat16*)K,
-                                                                  (const __nv_bfloat16*)V, sel, Oslc, B, N, H, blk,
-                                                                  nsel, scale);
+                                                                  (const __nv_bfloat16*)V, sel, Oslc, Lslc, B, N, H,
+                                                                  blk, nsel, scale);
     }
     note_launch(2);
     nsa_combine_kernel<<<(unsigned)min64((rows * d + 255) / 256, (int64_t)n_sm * 16), 256, 0, st>>>(
@@ -233,5 +465,63 @@ gfwa_status_t nsa_fwd_branches(const void* Q, const void* K, const void* V, cons
 }
 
 bool nsa_blocks_ok(int64_t N, int blk) { return N / blk <= kMaxBlocks; }
+
+// backward, phase 1: per-row gradients of the gated sum (dO_loc for gfwa_bwd, D terms)
+gfwa_status_t nsa_bwd_combine(const void* dO, const float* g, const float* Ocmp, const float* Oslc, const void* Oloc,
+                              const void* Ololo, float* dOc, float* dOs, void* dOl, float* dg, float* Dc, float* Ds,
+                              int64_t B, int64_t N, int64_t H, int d, cudaStream_t st) {
+    const unsigned grid = (unsigned)((B * N * H + kWarpsPerBlock - 1) / kWarpsPerBlock);
+    if (d == 64)
+        nsa_combine_bwd_kernel<64><<<grid, 32 * kWarpsPerBlock, 0, st>>>(
+            (const __nv_bfloat16*)dO, g, Ocmp, Oslc, (const __nv_bfloat16*)Oloc, (const __nv_bfloat16*)Ololo, dOc, dOs,
+            (__nv_bfloat16*)dOl, dg, Dc, Ds, B, N, H);
+    else
+        nsa_combine_bwd_kernel<128><<<grid, 32 * kWarpsPerBlock, 0, st>>>(
+            (const __nv_bfloat16*)dO, g, Ocmp, Oslc, (const __nv_bfloat16*)Oloc, (const __nv_bfloat16*)Ololo, dOc, dOs,
+            (__nv_bfloat16*)dOl, dg, Dc, Ds, B, N, H);
+    note_launch();
+    return check_launch();
+}
+
+// backward, phase 2: compressed and selected branches, then the sums with the local
+// branch's dQ, dK, dV (bf16, from gfwa_bwd)
+gfwa_status_t nsa_bwd_branches(const void* Q, const void* K, const void* V, const int* sel, const float* Kc,
+                               const float* Vc, const float* dOc, const float* dOs, const float* Lc, const float* Ls,
+                               const float* Dc, const float* Ds, float* dQacc, float* dKacc, float* dVacc, float* dKc,
+                               float* dVc, const void* dQl, const void* dKl, const void* dVl, void* dQ, void* dK,
+                               void* dV, int64_t B, int64_t N, int64_t H, int d, int blk, int nsel, float scale,
+                               cudaStream_t st) {
+    int dev = 0, n_sm = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t n = B * N * H * d, nb = N / blk;
+    if (gfwa_status_t s = check_launch(cudaMemsetAsync(dKacc, 0, n * sizeof(float), st))) return s;
+    if (gfwa_status_t s = check_launch(cudaMemsetAsync(dVacc, 0, n * sizeof(float), st))) return s;
+    const unsigned gq = (unsigned)((B * N * H + kWarpsPerBlock - 1) / kWarpsPerBlock);
+    const unsigned gb = (unsigned)((B * nb * H + kWarpsPerBlock - 1) / kWarpsPerBlock);
+    auto Qb = (const __nv_bfloat16*)Q;
+    if (d == 64) {
+        nsa_cmp_dq_kernel<64><<<gq, 32 * kWarpsPerBlock, 0, st>>>(Qb, Kc, Vc, dOc, Lc, Dc, dQacc, B, N, H, blk, scale);
+        if (nb > 0)
+            nsa_cmp_dkv_kernel<64><<<gb, 32 * kWarpsPerBlock, 0, st>>>(Qb, Kc, Vc, dOc, Lc, Dc, dKc, dVc, B, N, H, blk,
+                                                                       scale);
+        nsa_slc_bwd_kernel<64><<<gq, 32 * kWarpsPerBlock, 0, st>>>(Qb, (const __nv_bfloat16*)K,
+                                                                   (const __nv_bfloat16*)V, sel, dOs, Ls, Ds, dQacc,
+                                                                   dKacc, dVacc, B, N, H, blk, nsel, scale);
+    } else {
+        nsa_cmp_dq_kernel<128><<<gq, 32 * kWarpsPerBlock, 0, st>>>(Qb, Kc, Vc, dOc, Lc, Dc, dQacc, B, N, H, blk, scale);
+        if (nb > 0)
+            nsa_cmp_dkv_kernel<128><<<gb, 32 * kWarpsPerBlock, 0, st>>>(Qb, Kc, Vc, dOc, Lc, Dc, dKc, dVc, B, N, H,
+                                                                        blk, scale);
+        nsa_slc_bwd_kernel<128><<<gq, 32 * kWarpsPerBlock, 0, st>>>(Qb, (const __nv_bfloat16*)K,
+                                                                    (const __nv_bfloat16*)V, sel, dOs, Ls, Ds, dQacc,
+                                                                    dKacc, dVacc, B, N, H, blk, nsel, scale);
+    }
+    note_launch(nb > 0 ? 3 : 2);
+    nsa_finalize_kernel<<<(unsigned)min64((n + 255) / 256, (int64_t)n_sm * 16), 256, 0, st>>>(
+        (const __nv_bfloat16*)dQl, (const __nv_bfloat16*)dKl, (const __nv_bfloat16*)dVl, dQacc, dKacc, dVacc, dKc, dVc,
+        (__nv_bfloat16*)dQ, (__nv_bfloat16*)dK, (__nv_bfloat16*)dV, B, N, H, d, blk);
+    note_launch();
+    return check_launch();
+}
 
 }  // namespace gfwa

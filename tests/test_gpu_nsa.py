@@ -26,8 +26,8 @@ def test_nsa_fwd_matches_oracle(B, H, N, d, w, blk, nsel):
     g = torch.Generator().manual_seed(N)
     U = (-torch.cumsum(torch.nn.functional.softplus(torch.randn(B, H, N, generator=g)).double(), -1)).float()
     gates = torch.randn(B, N, H, 3, generator=g)
-    O, oc, osl, sel, ol = gb.gfwa_nsa_fwd(Q.cuda(), K.cuda(), V.cuda(), U.cuda(), gates.cuda(), w, block=blk,
-                                          n_sel=nsel, want_branches=True)
+    O, sv = gb.gfwa_nsa_fwd(Q.cuda(), K.cuda(), V.cuda(), U.cuda(), gates.cuda(), w, block=blk, n_sel=nsel)
+    oc, osl, sel, ol = sv["O_cmp"], sv["O_slc"], sv["sel"], sv["O_loc"]
     torch.cuda.synchronize()
     Kc, Vc = oracle.nsa_compress(K, V, blk)
     Ocr, sc = oracle.nsa_cmp(Q, Kc, Vc, blk)
@@ -53,3 +53,24 @@ def test_nsa_fwd_matches_oracle(B, H, N, d, w, blk, nsel):
     assert max_abs(ol, Olr) <= TOL_BF16_O
     Or = oracle.nsa_combine(Ocr, Oslr, Olr, gates)
     assert max_abs(O, Or) <= TOL_BF16_O
+
+
+@pytest.mark.parametrize("B,H,N,d,w,blk,nsel", [(1, 2, 300, 128, 96, 16, 4), (2, 2, 260, 64, 70, 32, 3),
+                                                 (1, 1, 40, 64, 8, 16, 3)])
+def test_nsa_bwd_matches_oracle(B, H, N, d, w, blk, nsel):
+    """gfwa_nsa_bwd vs the oracle's chain rule on the kernel's own selection; gradients at
+    north_star's bf16 budget (5e-2 abs), dgates likewise."""
+    s = synth.AttnShape(B=B, H=H, N=N, d=d, w=w)
+    Q, K, V, dO = synth.attn_inputs(s, seed=2 * N + d, dtype=torch.bfloat16)
+    g = torch.Generator().manual_seed(N + 1)
+    U = (-torch.cumsum(torch.nn.functional.softplus(torch.randn(B, H, N, generator=g)).double(), -1)).float()
+    gates = torch.randn(B, N, H, 3, generator=g)
+    dev = [x.cuda() for x in (Q, K, V, U, gates, dO)]
+    O, sv = gb.gfwa_nsa_fwd(*dev[:5], w, block=blk, n_sel=nsel)
+    dQ, dK, dV, dU, dg = gb.gfwa_nsa_bwd(*dev[:5], dev[5], sv, w, block=blk, n_sel=nsel)
+    torch.cuda.synchronize()
+    sel = sv["sel"].cpu().numpy().astype(np.int64)
+    rQ, rK, rV, rU, rg = oracle.nsa_bwd(Q, K, V, U, gates, dO, sel, w, blk)
+    from parity import TOL_BF16_GRAD
+    for name, got, ref in (("dQ", dQ, rQ), ("dK", dK, rK), ("dV", dV, rV), ("dU", dU, rU), ("dgates", dg, rg)):
+        assert max_abs(got, ref) <= TOL_BF16_GRAD, name
