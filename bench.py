@@ -679,6 +679,7 @@ def run_aux(dev, peaks):
         "paper_context": ("A100 Triton: 1-pass 0.3 ms vs PyTorch 2.9 ms at N=64K (P:527); "
                           "1-pass ~28.5 vs Scan-Then-Propagate ~20.1 billion tokens/s (P:1061)")}
     out["attn_layer_epilogue_C2"] = _attn_layer_epilogue(dev)
+    out["nsa_hybrid"] = _nsa_hybrid(dev)
     return out
 
 
@@ -730,6 +731,49 @@ def _attn_layer_epilogue(dev):
     res["speedup"] = round(res["unfused_torch_ms"] / res["fused_ms"], 3)
     res["note"] = "layer fwd+bwd from dY at C2, eager; epilogue = RMSNorm(gamma) * swish(g) per head (C-27)"
     return res
+
+
+def _nsa_hybrid(dev):
+    """the NSA hybrid with GatedFWA as the local branch (App. B; the
+    paper's NSA settings block 64, 16 selected blocks) at B=2, H=16,
+    N=4096, d=128, w=512: fwd and fwd+bwd time against the GatedFWA branch alone
+    (gfwa_fwd_train + gfwa_bwd), eager.  The compressed and selected branches are
+    CUDA-core kernels (the selected branch's dK/dV by fp32 atomics)."""
+    import torch
+
+    import synth
+    from paper_2512_07782_b200 import binding as gb
+
+    s = synth.AttnShape(B=2, H=16, N=4096, d=128, w=512)
+    Q, K, V, dO = synth.attn_inputs(s, seed=77, device=dev, dtype=torch.bfloat16)
+    h, beta = synth.gate_inputs(s.B, s.N, s.H, seed=78, device=dev)
+    U = gb.gfwa_gate_prefix(h, beta)
+    gates = torch.randn(s.B, s.N, s.H, 3, device=dev)
+
+    def t(fn, n=5):
+        for _ in range(2):
+            fn()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(n):
+            fn()
+        e1.record()
+        torch.cuda.synchronize(dev)
+        return round(e0.elapsed_time(e1) / n, 4)
+
+    O, sv = gb.gfwa_nsa_fwd(Q, K, V, U, gates, s.w, block=64, n_sel=16)
+    fwd = t(lambda: gb.gfwa_nsa_fwd(Q, K, V, U, gates, s.w, block=64, n_sel=16))
+    both = t(lambda: gb.gfwa_nsa_bwd(Q, K, V, U, gates, dO, gb.gfwa_nsa_fwd(Q, K, V, U, gates, s.w, 64, 16)[1], s.w,
+                                     64, 16))
+
+    def local():
+        O2, L2, Ol2 = gb.gfwa_fwd(Q, K, V, U, s.w, want_o_lo=True, prepare_bwd=True)
+        gb.gfwa_bwd(Q, K, V, U, O2, L2, dO, s.w, O_lo=Ol2, want_dalpha=False)
+
+    return {"config": "B=2, H=16, N=4096, d=128, w=512, block=64, n_sel=16", "nsa_fwd_ms": fwd,
+            "nsa_fwd_bwd_ms": both, "gatedfwa_local_fwd_bwd_ms": t(local),
+            "tokens_per_s_fwd_bwd": round(s.B * s.N / (both * 1e-3), 1)}
 
 
 # --------------------------------------------------------------------------- CPU oracle

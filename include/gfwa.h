@@ -233,7 +233,7 @@ typedef struct {
     int64_t B, H, N;
     int32_t d;          /* 64 or 128 */
     int32_t w;          /* window of the local (GatedFWA) branch */
-    int32_t block;      /* compression / selection block length (length = stride) */
+    int32_t block;      /* compression / selection block length (length = stride), 1..64 */
     int32_t n_sel;      /* selected blocks besides the query's own block */
     float scale;        /* <= 0 selects 1/sqrt(d) */
     gfwa_dtype_t dtype; /* GFWA_BF16 */

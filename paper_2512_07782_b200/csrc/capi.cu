@@ -469,13 +469,13 @@ gfwa_status_t nsa_bwd_branches(const void* Q, const void* K, const void* V, cons
                                const float* Dc, const float* Ds, float* dQacc, float* dKacc, float* dVacc, float* dKc,
                                float* dVc, const void* dQl, const void* dKl, const void* dVl, void* dQ, void* dK,
                                void* dV, int64_t B, int64_t N, int64_t H, int d, int blk, int nsel, float scale,
-                               cudaStream_t st);
+                               int* scnt, int* soff, int* scur, int* slist, cudaStream_t st);
 bool nsa_blocks_ok(int64_t N, int blk);
 }  // namespace gfwa
 
 namespace {
 bool nsa_desc_ok(const gfwa_nsa_desc_t* d) {
-    return d && d->B >= 1 && d->H >= 1 && d->N >= 1 && d->w >= 1 && d->block >= 1 && d->n_sel >= 0 &&
+    return d && d->B >= 1 && d->H >= 1 && d->N >= 1 && d->w >= 1 && d->block >= 1 && d->block <= 64 && d->n_sel >= 0 &&
            (d->d == 64 || d->d == 128) && d->dtype == GFWA_BF16 && nsa_blocks_ok(d->N, d->block) &&
            d->B * d->N * d->H < ((int64_t)1 << 31) && d->scale == d->scale;
 }
@@ -507,7 +507,9 @@ size_t nsa_bwd_bytes(const gfwa_nsa_desc_t* d) {
     const size_t nbk = (size_t)d->B * (d->N / d->block) * d->H * d->d;
     auto r = [](size_t b) { return (b + 255) & ~(size_t)255; };
     gfwa_attn_desc_t ad = nsa_local_desc(d);
-    return r(nbk * 4) * 4 + r(n * 4) * 5 + r(n * 2) * 4 + r(rows * 4) * 2 + r(gfwa_bwd_workspace_size(&ad));
+    const size_t nbp = (size_t)d->B * d->H * ((d->N + d->block - 1) / d->block);
+    return r(nbk * 4) * 4 + r(n * 4) * 5 + r(n * 2) * 4 + r(rows * 4) * 2 + r(gfwa_bwd_workspace_size(&ad)) +
+           r(nbp * 4) * 3 + r(rows * (d->n_sel + 1) * 4);
 }
 }  // namespace
 
@@ -593,6 +595,11 @@ extern "C" gfwa_status_t gfwa_nsa_bwd(const gfwa_nsa_desc_t* d, const void* Q, c
     gfwa_attn_desc_t ad = nsa_local_desc(d);
     const size_t lws = gfwa_bwd_workspace_size(&ad);
     void* lw = cv.take(lws);
+    const size_t nbp = (size_t)B * H * ((N + d->block - 1) / d->block);
+    int* scnt = (int*)cv.take(nbp * 4);
+    int* soff = (int*)cv.take(nbp * 4);
+    int* scur = (int*)cv.take(nbp * 4);
+    int* slist = (int*)cv.take(rows * (d->n_sel + 1) * 4);
     const float scale = d->scale > 0.f ? d->scale : 1.f / std::sqrt((float)d->d);
     gfwa_status_t s;
     if ((s = nsa_bwd_combine(dO, gates, sv->O_cmp, sv->O_slc, sv->O_loc, sv->O_loc_lo, dOc, dOs, dOl, dgates, Dc, Ds,
@@ -609,5 +616,6 @@ extern "C" gfwa_status_t gfwa_nsa_bwd(const gfwa_nsa_desc_t* d, const void* Q, c
             return s;
     }
     return nsa_bwd_branches(Q, K, V, sv->sel, Kc, Vc, dOc, dOs, sv->LSE_cmp, sv->LSE_slc, Dc, Ds, dQacc, dKacc, dVacc,
-                            dKc, dVc, dQl, dKl, dVl, dQ, dK, dV, B, N, H, d->d, d->block, d->n_sel, scale, st);
+                            dKc, dVc, dQl, dKl, dVl, dQ, dK, dV, B, N, H, d->d, d->block, d->n_sel, scale, scnt,
+                            soff, scur, slist, st);
 }

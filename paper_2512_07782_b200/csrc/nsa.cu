@@ -338,14 +338,13 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) nsa_cmp_dkv_kernel(
     }
 }
 
-// selected branch: dq into the query's row (added), dK / dV of the selected tokens by
-// fp32 atomics (a token is selected by a data-dependent set of queries)
+// selected branch, query side: dq into the query's row (added)
 template <int D>
 __global__ void __launch_bounds__(32 * kWarpsPerBlock) nsa_slc_bwd_kernel(
     const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __restrict__ K, const __nv_bfloat16* __restrict__ V,
     const int* __restrict__ sel, const float* __restrict__ dOs, const float* __restrict__ Ls,
-    const float* __restrict__ Ds, float* __restrict__ dQacc, float* __restrict__ dKacc, float* __restrict__ dVacc,
-    int64_t B, int64_t N, int64_t H, int blk, int nsel, float scale) {
+    const float* __restrict__ Ds, float* __restrict__ dQacc, int64_t B, int64_t N, int64_t H, int blk, int nsel,
+    float scale) {
     constexpr int C = D / 32;
     const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
     const int64_t row = (int64_t)blockIdx.x * kWarpsPerBlock + wp;
@@ -379,15 +378,122 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) nsa_slc_bwd_kernel(
             dp = warp_sum(dp);
             const float p = __expf(s - L), ds = p * (dp - Dv);
 #pragma unroll
-            for (int c = 0; c < C; ++c) {
-                dq[c] = fmaf(scale * ds, kv[c], dq[c]);
-                atomicAdd(dKacc + kr * D + C * lane + c, scale * ds * q[c]);
-                atomicAdd(dVacc + kr * D + C * lane + c, p * go[c]);
-            }
+            for (int c = 0; c < C; ++c) dq[c] = fmaf(scale * ds, kv[c], dq[c]);
         }
     }
 #pragma unroll
     for (int c = 0; c < C; ++c) dQacc[row * D + C * lane + c] += dq[c];
+}
+
+
+// selected branch, block side: the queries that selected each block are listed
+// (count, scan, fill), then one CTA per (b, h, block) accumulates the block's dK, dV
+// in registers over its queries -- no atomics on the gradients
+__global__ void nsa_sel_count_kernel(const int* __restrict__ sel, int* __restrict__ cnt, int64_t BH, int64_t N,
+                                     int nsel, int nbp) {
+    const int64_t total = BH * N * (nsel + 1);
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int ib = sel[e];
+        if (ib >= 0) atomicAdd(cnt + (e / ((int64_t)N * (nsel + 1))) * nbp + ib, 1);
+    }
+}
+// exclusive scan of the counts per (b, h): one warp per (b, h); cur = the fill cursors
+__global__ void nsa_sel_scan_kernel(const int* __restrict__ cnt, int* __restrict__ off, int* __restrict__ cur,
+                                    int64_t BH, int nbp) {
+    const int64_t bh = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (bh >= BH) return;
+    int run = 0;
+    for (int i0 = 0; i0 < nbp; i0 += 32) {
+        const int i = i0 + lane;
+        const int v = i < nbp ? cnt[bh * nbp + i] : 0;
+        int x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (i < nbp) {
+            off[bh * nbp + i] = run + x - v;
+            cur[bh * nbp + i] = run + x - v;
+        }
+        run += __shfl_sync(0xffffffffu, x, 31);
+    }
+}
+__global__ void nsa_sel_fill_kernel(const int* __restrict__ sel, int* __restrict__ cur, int* __restrict__ list,
+                                    int64_t BH, int64_t N, int nsel, int nbp) {
+    const int64_t total = BH * N * (nsel + 1);
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int ib = sel[e];
+        if (ib < 0) continue;
+        const int64_t bh = e / ((int64_t)N * (nsel + 1));
+        const int t = (int)((e / (nsel + 1)) % N);
+        list[bh * N * (nsel + 1) + atomicAdd(cur + bh * nbp + ib, 1)] = t;
+    }
+}
+
+// 256 threads: thread = (key kk = tid / 4 of the block's <= 64 keys, channels (tid % 4) + 4 m)
+template <int D>
+__global__ void __launch_bounds__(256) nsa_slc_dkv_kernel(
+    const __nv_bfloat16* __restrict__ Q, const __nv_bfloat16* __restrict__ K, const __nv_bfloat16* __restrict__ V,
+    const float* __restrict__ dOs, const float* __restrict__ Ls, const float* __restrict__ Ds,
+    const int* __restrict__ off, const int* __restrict__ cnt, const int* __restrict__ list,
+    float* __restrict__ dKacc, float* __restrict__ dVacc, int64_t B, int64_t N, int64_t H, int blk, int nsel,
+    int nbp, float scale) {
+    constexpr int M = D / 4;  // channels per thread
+    __shared__ float s_q[D], s_go[D];
+    const int64_t r = blockIdx.x;  // (b, h, block)
+    const int ib = (int)(r % nbp);
+    const int64_t bh = r / nbp, hh = bh % H, b = bh / H;
+    const int kk = threadIdx.x >> 2, sub = threadIdx.x & 3;
+    const int64_t j = (int64_t)ib * blk + kk;
+    const bool kvalid = kk < blk && j < N;
+    float kr[M], vr[M], dk[M], dv[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+        const int c = sub + 4 * m;
+        kr[m] = kvalid ? __bfloat162float(K[((b * N + j) * H + hh) * D + c]) : 0.f;
+        vr[m] = kvalid ? __bfloat162float(V[((b * N + j) * H + hh) * D + c]) : 0.f;
+        dk[m] = 0.f;
+        dv[m] = 0.f;
+    }
+    const int n = cnt[r], o0 = off[r];
+    const int* lst = list + bh * N * (nsel + 1) + o0;
+    for (int qi = 0; qi < n; ++qi) {
+        const int t = lst[qi];
+        const int64_t row = (b * N + t) * H + hh;
+        __syncthreads();  // the previous query's rows are consumed
+        for (int c = threadIdx.x; c < D; c += blockDim.x) {
+            s_q[c] = __bfloat162float(Q[row * D + c]);
+            s_go[c] = dOs[row * D + c];
+        }
+        __syncthreads();
+        float s = 0.f, dp = 0.f;
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+            s = fmaf(s_q[sub + 4 * m], kr[m], s);
+            dp = fmaf(s_go[sub + 4 * m], vr[m], dp);
+        }
+        s += __shfl_xor_sync(0xffffffffu, s, 1);
+        s += __shfl_xor_sync(0xffffffffu, s, 2);
+        dp += __shfl_xor_sync(0xffffffffu, dp, 1);
+        dp += __shfl_xor_sync(0xffffffffu, dp, 2);
+        if (!kvalid || j > t) continue;  // causal inside the block
+        const float p = __expf(s * scale - Ls[bh * N + t]);
+        const float ds = p * (dp - Ds[bh * N + t]);
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+            dk[m] = fmaf(scale * ds, s_q[sub + 4 * m], dk[m]);
+            dv[m] = fmaf(p, s_go[sub + 4 * m], dv[m]);
+        }
+    }
+    if (!kvalid) return;
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+        const int c = sub + 4 * m;
+        dKacc[((b * N + j) * H + hh) * D + c] = dk[m];
+        dVacc[((b * N + j) * H + hh) * D + c] = dv[m];
+    }
 }
 
 // dQ = dQ_loc + dQacc; dK = dK_loc + dKacc + dKc(block) / blk; dV likewise -> bf16
@@ -490,7 +596,7 @@ gfwa_status_t nsa_bwd_branches(const void* Q, const void* K, const void* V, cons
                                const float* Dc, const float* Ds, float* dQacc, float* dKacc, float* dVacc, float* dKc,
                                float* dVc, const void* dQl, const void* dKl, const void* dVl, void* dQ, void* dK,
                                void* dV, int64_t B, int64_t N, int64_t H, int d, int blk, int nsel, float scale,
-                               cudaStream_t st) {
+                               int* scnt, int* soff, int* scur, int* slist, cudaStream_t st) {
     int dev = 0, n_sm = 148;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
     const int64_t n = B * N * H * d, nb = N / blk;
@@ -498,6 +604,15 @@ gfwa_status_t nsa_bwd_branches(const void* Q, const void* K, const void* V, cons
     if (gfwa_status_t s = check_launch(cudaMemsetAsync(dVacc, 0, n * sizeof(float), st))) return s;
     const unsigned gq = (unsigned)((B * N * H + kWarpsPerBlock - 1) / kWarpsPerBlock);
     const unsigned gb = (unsigned)((B * nb * H + kWarpsPerBlock - 1) / kWarpsPerBlock);
+    // the queries of each selectable block (own blocks include the partial last one)
+    const int nbp = (int)((N + blk - 1) / blk);
+    const int64_t nsl = B * H * N * (nsel + 1);
+    if (gfwa_status_t s = check_launch(cudaMemsetAsync(scnt, 0, (size_t)B * H * nbp * sizeof(int), st))) return s;
+    const unsigned gs = (unsigned)min64((nsl + 255) / 256, (int64_t)n_sm * 16);
+    nsa_sel_count_kernel<<<gs, 256, 0, st>>>(sel, scnt, B * H, N, nsel, nbp);
+    nsa_sel_scan_kernel<<<(unsigned)((B * H + 7) / 8), 256, 0, st>>>(scnt, soff, scur, B * H, nbp);
+    nsa_sel_fill_kernel<<<gs, 256, 0, st>>>(sel, scur, slist, B * H, N, nsel, nbp);
+    note_launch(3);
     auto Qb = (const __nv_bfloat16*)Q;
     if (d == 64) {
         nsa_cmp_dq_kernel<64><<<gq, 32 * kWarpsPerBlock, 0, st>>>(Qb, Kc, Vc, dOc, Lc, Dc, dQacc, B, N, H, blk, scale);
@@ -506,7 +621,10 @@ gfwa_status_t nsa_bwd_branches(const void* Q, const void* K, const void* V, cons
                                                                        scale);
         nsa_slc_bwd_kernel<64><<<gq, 32 * kWarpsPerBlock, 0, st>>>(Qb, (const __nv_bfloat16*)K,
                                                                    (const __nv_bfloat16*)V, sel, dOs, Ls, Ds, dQacc,
-                                                                   dKacc, dVacc, B, N, H, blk, nsel, scale);
+                                                                   B, N, H, blk, nsel, scale);
+        nsa_slc_dkv_kernel<64><<<(unsigned)(B * H * nbp), 256, 0, st>>>(
+            Qb, (const __nv_bfloat16*)K, (const __nv_bfloat16*)V, dOs, Ls, Ds, soff, scnt, slist, dKacc, dVacc, B, N,
+            H, blk, nsel, nbp, scale);
     } else {
         nsa_cmp_dq_kernel<128><<<gq, 32 * kWarpsPerBlock, 0, st>>>(Qb, Kc, Vc, dOc, Lc, Dc, dQacc, B, N, H, blk, scale);
         if (nb > 0)
@@ -514,9 +632,12 @@ gfwa_status_t nsa_bwd_branches(const void* Q, const void* K, const void* V, cons
                                                                         blk, scale);
         nsa_slc_bwd_kernel<128><<<gq, 32 * kWarpsPerBlock, 0, st>>>(Qb, (const __nv_bfloat16*)K,
                                                                     (const __nv_bfloat16*)V, sel, dOs, Ls, Ds, dQacc,
-                                                                    dKacc, dVacc, B, N, H, blk, nsel, scale);
+                                                                    B, N, H, blk, nsel, scale);
+        nsa_slc_dkv_kernel<128><<<(unsigned)(B * H * nbp), 256, 0, st>>>(
+            Qb, (const __nv_bfloat16*)K, (const __nv_bfloat16*)V, dOs, Ls, Ds, soff, scnt, slist, dKacc, dVacc, B, N,
+            H, blk, nsel, nbp, scale);
     }
-    note_launch(nb > 0 ? 3 : 2);
+    note_launch(nb > 0 ? 4 : 3);
     nsa_finalize_kernel<<<(unsigned)min64((n + 255) / 256, (int64_t)n_sm * 16), 256, 0, st>>>(
         (const __nv_bfloat16*)dQl, (const __nv_bfloat16*)dKl, (const __nv_bfloat16*)dVl, dQacc, dKacc, dVacc, dKc, dVc,
         (__nv_bfloat16*)dQ, (__nv_bfloat16*)dK, (__nv_bfloat16*)dV, B, N, H, d, blk);
