@@ -249,14 +249,19 @@ def sp_forward_backward(Q, K, V, h, beta, dO, w: int, ops: Ops, ring: Ring, eps:
     else:
         back_like = [dKx[:, :w], dVx[:, :w], dUx[..., :w]]
         send = [t.contiguous() for t in back_like] if h0 else None
-    back = ring.shift(send, back_like, forward=False)
+    handle = ring.start(send, back_like, forward=False)
     if kv_ext is not None:
         dK, dV = dKx[:, h0:], dVx[:, h0:]  # views: no copy of the S local rows
     else:
         dK = dKx[:, h0:].contiguous()
         dV = dVx[:, h0:].contiguous()
     dU = dUx[..., h0:].contiguous()
-    carry = None
+    # the gate backward of the whole shard runs while the halo gradients travel: with
+    # carry = +sum_j dU_halo(j), dalpha_q = carry - sum_{m >= q} dU_m needs no received
+    # value for q < S - w (the halo additions to the last w rows cancel the carry), so
+    # the local scan with carry 0 is exact there; the last w rows are redone below
+    dalpha, dh, dbeta = ops.gate_bwd(dU, h, beta, eps, None)
+    back = ring.finish(handle)
     if back is not None:
         if exact:  # own partial + received partial, both before rounding, rounded once
             dK[:, S - w:] = (tail[0] + back[0][0]).to(dK.dtype)
@@ -268,6 +273,10 @@ def sp_forward_backward(Q, K, V, h, beta, dO, w: int, ops: Ops, ring: Ring, eps:
             dU_halo = back[2]
         dU[..., S - w:] += dU_halo
         carry = dU_halo.double().sum(-1)  # d-alpha carry = +sum_j dU_halo(j)
-    dalpha, dh, dbeta = ops.gate_bwd(dU, h, beta, eps, carry)
+        da_t, dh_t, db_t = ops.gate_bwd(dU[..., S - w:].contiguous(), h[:, S - w:].contiguous(),
+                                        beta[:, S - w:].contiguous(), eps, carry)
+        dalpha[..., S - w:] = da_t
+        dh[:, S - w:] = dh_t
+        dbeta[:, S - w:] = db_t
     U_offset = global_offset_finish(scan, ring) if scan is not None else torch.zeros_like(total, dtype=torch.float64)
     return ShardResult(O, LSE, U_loc, dQ, dK, dV, dalpha, dh, dbeta, dU, U_offset)
