@@ -73,3 +73,23 @@ def test_normgate_plain_forward_is_unchanged():
     Y, O, LSE, Olo, _ = gb.gfwa_fwd_normgate(Q, K, V, U, g, gamma, s.w)
     O2, LSE2, Olo2 = gb.gfwa_fwd(Q, K, V, U, s.w, want_o_lo=True)
     assert torch.equal(O, O2) and torch.equal(LSE, LSE2) and torch.equal(Olo, Olo2)
+
+
+def test_normgate_inference_without_residual():
+    """Inference form (no O_lo, no backward workspace): Y from the bf16 O alone stays
+    within the same budget at d = 64."""
+    s = synth.AttnShape(B=1, H=2, N=333, d=64, w=128)
+    Q, K, V, _ = synth.attn_inputs(s, seed=91, dtype=torch.bfloat16)
+    gen = torch.Generator().manual_seed(92)
+    g = torch.randn(1, s.N, 2, s.d, generator=gen).to(torch.bfloat16)
+    gamma = (1.0 + 0.1 * torch.randn(s.d, generator=gen)).float()
+    U = _U(1, 2, s.N, 93)
+    Y, O, LSE, Olo, rstd = gb.gfwa_fwd_normgate(Q.cuda(), K.cuda(), V.cuda(), U.cuda(), g.cuda(), gamma.cuda(), s.w,
+                                               eps=EPS, want_o_lo=False)
+    torch.cuda.synchronize()
+    assert Olo is None
+    Or, _ = oracle.fwd(Q, K, V, U, s.w)
+    Yr, rr = oracle.normgate_fwd(Or, g, gamma, eps=EPS)
+    gf = np64(g)
+    L = float(np.max(np.abs(gf / (1.0 + np.exp(-gf)) * np64(gamma) * rr.transpose(0, 2, 1)[..., None])))
+    assert max_abs(Y, Yr) <= TOL_BF16_O * max(1.0, L) + 2.0 ** -7 * np.abs(Yr).max()
