@@ -48,6 +48,9 @@
 #ifndef GFWA_FWD_POLY
 #define GFWA_FWD_POLY 0
 #endif
+#ifndef GFWA_FWD_LD16
+#define GFWA_FWD_LD16 1  // softmax passes in 16-column chunks with the next TMEM load in flight
+#endif
 #ifndef GFWA_FWD_TRACE
 #define GFWA_FWD_TRACE 0  // diagnostics build only: clock64 stamps per role into a device array
 #endif
@@ -185,6 +188,40 @@ __device__ __forceinline__ Item make_item(const TcFwdParams& p, int idx) {
     it.jtop = it.has1 ? it.jhi1 : it.jhi0;
     it.nsteps = it.jtop - it.jlo0 + 1;
     return it;
+}
+
+// softmax pass helpers on 16-column chunks (GFWA_FWD_LD16)
+__device__ __forceinline__ void max_chunk16(const uint32_t (&raw)[16], uint32_t kw, bool interior, float (&mx)[4]) {
+#pragma unroll
+    for (int e = 0; e < 16; e += 4) {
+        float a0 = __uint_as_float(raw[e]), a1 = __uint_as_float(raw[e + 1]);
+        float a2 = __uint_as_float(raw[e + 2]), a3 = __uint_as_float(raw[e + 3]);
+        if (!interior) {
+            a0 = ((kw >> e) & 1u) ? a0 : -INFINITY;
+            a1 = ((kw >> (e + 1)) & 1u) ? a1 : -INFINITY;
+            a2 = ((kw >> (e + 2)) & 1u) ? a2 : -INFINITY;
+            a3 = ((kw >> (e + 3)) & 1u) ? a3 : -INFINITY;
+        }
+        mx[(e >> 2) & 3] = fmax3(mx[(e >> 2) & 3], fmaxf(a0, a1), fmaxf(a2, a3));
+    }
+}
+template <bool kF16P>
+__device__ __forceinline__ void exp_chunk16(const uint32_t (&xr)[16], uint32_t kw, bool interior, uint64_t sl2x2,
+                                            uint64_t nm2, float (&acc)[8], uint32_t (&pk)[8]) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const uint64_t dd = ffma2(f2pack(__uint_as_float(xr[2 * e]), __uint_as_float(xr[2 * e + 1])), sl2x2, nm2);
+        float d0, d1;
+        f2unpack(dd, d0, d1);
+        if (!interior) {
+            d0 = ((kw >> (2 * e)) & 1u) ? d0 : -INFINITY;
+            d1 = ((kw >> (2 * e + 1)) & 1u) ? d1 : -INFINITY;
+        }
+        const float p0 = ex2(d0), p1 = ex2(d1);
+        acc[(2 * e) & 7] += p0;
+        acc[(2 * e + 1) & 7] += p1;
+        pk[e] = kF16P ? pack_f16x2(p0, p1) : pack_bf16x2(p0, p1);
+    }
 }
 
 // kF16P: training forward (O_lo wanted): P, V in fp16 for the PV product (reading C-23);
@@ -471,6 +508,29 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // already in the accumulator, C-26; masked to -inf outside the window, Alg. 2
                 // l.12-15); x = sl2 S' is monotone in S', so the max is taken on S'
                 float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#if GFWA_FWD_LD16
+                {
+                    // four 16-column chunks, the next chunk's TMEM load in flight while the
+                    // current one is reduced (TMEM load latency under load is hundreds of cycles)
+                    uint32_t ra[16], rb[16];
+                    const uint32_t kw0 = keep[0], kw1 = keep[1];
+                    const bool l0 = live[0], l1 = live[1];
+                    // (loads of fully masked chunks are issued anyway: no data-dependent merges
+                    // of the in-flight registers; only their reduction is skipped)
+                    tmem_ld16(lane_addr + s_col, ra);
+                    tmem_wait_ld();
+                    tmem_ld16(lane_addr + s_col + 16, rb);
+                    if (l0) max_chunk16(ra, kw0 & 0xffffu, interior, mx);
+                    tmem_wait_ld();
+                    tmem_ld16(lane_addr + s_col + 32, ra);
+                    if (l0) max_chunk16(rb, kw0 >> 16, interior, mx);
+                    tmem_wait_ld();
+                    tmem_ld16(lane_addr + s_col + 48, rb);
+                    if (l1) max_chunk16(ra, kw1 & 0xffffu, interior, mx);
+                    tmem_wait_ld();
+                    if (l1) max_chunk16(rb, kw1 >> 16, interior, mx);
+                }
+#else
 #pragma unroll
                 for (int cb = 0; cb < 2; ++cb) {
                     if (!(cb ? live[1] : live[0])) continue;  // masked for the whole warp: pass 2 skips it too
@@ -491,6 +551,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         mx[(e >> 2) & 3] = fmax3(mx[(e >> 2) & 3], fmaxf(a0, a1), fmaxf(a2, a3));
                     }
                 }
+#endif
                 if (r == 0) FTR(x, 6 * (int)cs + 2);
                 // the row max over both halves (exchange through smem), in log2 units
                 // (double-buffered by key-tile parity: a half may run one tile ahead of the other)
@@ -518,6 +579,48 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // pass 2: exponentials 2^(sl2 S' - m), the half-row sum, 16-bit P of the half's 64
                 // keys into its own first 32 S columns (chunk cb's P lands on columns that
                 // chunk cb's S' already left: [16 cb, 16 cb + 16) <= [32 cb, 32 cb + 32))
+#if GFWA_FWD_LD16
+                {
+                    // four 16-column chunks with the next chunk's load in flight; chunk q's P
+                    // lands on columns [8 q, 8 q + 8), below every S' column still to be read
+                    uint32_t xa[16], xb[16], pk[8];
+                    const uint32_t kw0 = keep[0], kw1 = keep[1];
+                    const bool l0 = live[0], l1 = live[1];
+                    const uint32_t z8[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+                    tmem_ld16(lane_addr + s_col, xa);
+                    tmem_wait_ld();
+                    tmem_ld16(lane_addr + s_col + 16, xb);
+                    if (l0) {
+                        exp_chunk16<kF16P>(xa, kw0 & 0xffffu, interior, sl2x2, nm2, acc, pk);
+                        tmem_st8(lane_addr + s_col, pk);
+                    } else {
+                        tmem_st8(lane_addr + s_col, z8);
+                    }
+                    tmem_wait_ld();
+                    tmem_ld16(lane_addr + s_col + 32, xa);
+                    if (l0) {
+                        exp_chunk16<kF16P>(xb, kw0 >> 16, interior, sl2x2, nm2, acc, pk);
+                        tmem_st8(lane_addr + s_col + 8, pk);
+                    } else {
+                        tmem_st8(lane_addr + s_col + 8, z8);
+                    }
+                    tmem_wait_ld();
+                    tmem_ld16(lane_addr + s_col + 48, xb);
+                    if (l1) {
+                        exp_chunk16<kF16P>(xa, kw1 & 0xffffu, interior, sl2x2, nm2, acc, pk);
+                        tmem_st8(lane_addr + s_col + 16, pk);
+                    } else {
+                        tmem_st8(lane_addr + s_col + 16, z8);
+                    }
+                    tmem_wait_ld();
+                    if (l1) {
+                        exp_chunk16<kF16P>(xb, kw1 >> 16, interior, sl2x2, nm2, acc, pk);
+                        tmem_st8(lane_addr + s_col + 24, pk);
+                    } else {
+                        tmem_st8(lane_addr + s_col + 24, z8);
+                    }
+                }
+#else
 #pragma unroll
                 for (int cb = 0; cb < 2; ++cb) {
                     uint32_t pk[16];
@@ -552,6 +655,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     tmem_st16(lane_addr + s_col + 16 * cb, pk);
                 }
+#endif
                 l += ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
                 // rescale this half's O columns (the PV of the previous step is complete:
                 // S_full certified it)
