@@ -19,7 +19,8 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("B,H,N,d,w,blk,nsel", [(1, 2, 300, 128, 96, 16, 4), (2, 3, 520, 64, 200, 32, 5),
-                                                 (1, 2, 1024, 128, 512, 64, 16), (1, 1, 40, 64, 8, 16, 3)])
+                                                 (1, 2, 1024, 128, 512, 64, 16), (1, 1, 40, 64, 8, 16, 3),
+                                                 (1, 2, 10, 128, 4, 16, 2)])  # N < block: no complete block
 def test_nsa_fwd_matches_oracle(B, H, N, d, w, blk, nsel):
     s = synth.AttnShape(B=B, H=H, N=N, d=d, w=w)
     Q, K, V, _ = synth.attn_inputs(s, seed=N + d, dtype=torch.bfloat16)
@@ -56,7 +57,7 @@ def test_nsa_fwd_matches_oracle(B, H, N, d, w, blk, nsel):
 
 
 @pytest.mark.parametrize("B,H,N,d,w,blk,nsel", [(1, 2, 300, 128, 96, 16, 4), (2, 2, 260, 64, 70, 32, 3),
-                                                 (1, 1, 40, 64, 8, 16, 3)])
+                                                 (1, 1, 40, 64, 8, 16, 3), (1, 2, 10, 128, 4, 16, 2)])
 def test_nsa_bwd_matches_oracle(B, H, N, d, w, blk, nsel):
     """gfwa_nsa_bwd vs the oracle's chain rule on the kernel's own selection; gradients at
     north_star's bf16 budget (5e-2 abs), dgates likewise."""
