@@ -680,7 +680,49 @@ def run_aux(dev, peaks):
                           "1-pass ~28.5 vs Scan-Then-Propagate ~20.1 billion tokens/s (P:1061)")}
     out["attn_layer_epilogue_C2"] = _attn_layer_epilogue(dev)
     out["nsa_hybrid"] = _nsa_hybrid(dev)
+    out["gqa_C2"] = _gqa_c2(dev, peaks)
     return out
+
+
+def _gqa_c2(dev, peaks):
+    """Grouped-query attention (gfwa_attn_desc_t.H_kv; the NSA configuration's GQA,
+    P:1209-1211) at C2's query shape: H = 16 query heads over H_kv = 16 (MHA), 4, 1 K/V
+    heads.  fwd (gfwa_fwd_train) + bwd (gfwa_bwd) per layer, inputs resident, eager;
+    the in-window FLOPs are those of the 16 query heads whatever H_kv."""
+    import torch
+
+    import synth
+    from paper_2512_07782_b200 import binding as gb
+
+    c = synth.CONFIGS["C2"]
+    s = synth.AttnShape(B=c["B"], H=c["H"], N=c["N"], d=c["d"], w=c["w"])
+    Q, K, V, dO = synth.attn_inputs(s, seed=c["seed"], device=dev, dtype=torch.bfloat16)
+    h, beta = synth.gate_inputs(s.B, s.N, s.H, seed=c["seed"], device=dev)
+    U = gb.gfwa_gate_prefix(h, beta)
+    fl = 14.0 * s.N * s.w * s.d * s.B * s.H
+    res = {}
+    for hkv in (s.H, 4, 1):
+        Kg, Vg = K[:, :, :hkv].contiguous(), V[:, :, :hkv].contiguous()
+
+        def step():
+            O, LSE, Olo = gb.gfwa_fwd(Q, Kg, Vg, U, s.w, want_o_lo=True, prepare_bwd=True)
+            gb.gfwa_bwd(Q, Kg, Vg, U, O, LSE, dO, s.w, O_lo=Olo, want_dalpha=False)
+
+        for _ in range(3):
+            step()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(10):
+            step()
+        e1.record()
+        torch.cuda.synchronize(dev)
+        ms = e0.elapsed_time(e1) / 10
+        res[f"H_kv={hkv}"] = {"ms": round(ms, 4), "tflops_in_window": round(fl / (ms * 1e-3) / 1e12, 1),
+                              "pct_bf16_peak": round(fl / (ms * 1e-3) / 1e12 / peaks["bf16"], 4)}
+        del Kg, Vg
+    res["note"] = "C2 queries (B=8, H=16, N=4096, d=128, w=512), fwd+bwd eager, no dalpha scan"
+    return res
 
 
 def _attn_layer_epilogue(dev):

@@ -139,6 +139,13 @@ gfwa_status_t gfwa_gate_prefix_variant(int variant, gfwa_dtype_t in_dtype, const
  * Gradients share the layout of their primal: dQ uses q_stride, dK k_stride,
  * dV v_stride, dO and O use o_stride.  For the BF16 path every stride and
  * base pointer must be 16-byte aligned (TMA).
+ * Grouped-query attention (the NSA configuration's GQA): with
+ * H_kv > 0, K, V, dK, dV have H_kv heads and query head hh reads K/V head
+ * hh / (H / H_kv); U, LSE, dU, dalpha stay per query head, so every query
+ * head keeps its own gate (Eq. 7 is per head).  dK, dV of a K/V head sum
+ * the gradients of its H / H_kv query heads.  H % H_kv == 0 is required;
+ * H_kv != H runs on the BF16 tensor-core path only (UNSUPPORTED otherwise).
+ * H_kv = 0 means H_kv = H (multi-head attention).
  */
 typedef struct {
     int64_t B, H, N_q, N_kv;
@@ -147,6 +154,7 @@ typedef struct {
     float scale;        /* <= 0 selects 1/sqrt(d) */
     gfwa_dtype_t dtype; /* dtype of Q, K, V, O, dO, dQ, dK, dV */
     int64_t q_stride[3], k_stride[3], v_stride[3], o_stride[3];
+    int64_t H_kv;       /* K/V heads (GQA), H % H_kv == 0; 0 = H */
 } gfwa_attn_desc_t;
 
 /*
@@ -211,8 +219,8 @@ gfwa_status_t gfwa_bwd(const gfwa_attn_desc_t* desc, const void* Q, const void* 
 /*
  * gfwa_bwd_rows_f32 -- gfwa_bwd that also writes fp32 copies of dK and dV (before
  * their bf16 rounding) for the first head_rows and the last tail_rows key rows:
- * dKV_head [2][B][head_rows][H][d] and dKV_tail [2][B][tail_rows][H][d] (dK in
- * [0], dV in [1]; contiguous, 16-byte aligned).  Sequence sharding (SURVEY
+ * dKV_head [2][B][head_rows][H_kv][d] and dKV_tail [2][B][tail_rows][H_kv][d] (dK
+ * in [0], dV in [1]; contiguous, 16-byte aligned; H_kv = H without GQA).  Sequence sharding (SURVEY
  * 8(e) step 2; BASELINE north_star): rank r's partial gradients of its w halo
  * rows (its head rows) travel to rank r-1 in fp32 and are added there to that
  * rank's fp32 tail rows, so the boundary rows are rounded to bf16 once.  The

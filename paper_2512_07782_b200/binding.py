@@ -48,6 +48,7 @@ class AttnDesc(ctypes.Structure):
         ("k_stride", ctypes.c_int64 * 3),
         ("v_stride", ctypes.c_int64 * 3),
         ("o_stride", ctypes.c_int64 * 3),
+        ("H_kv", ctypes.c_int64),
     ]
 
 
@@ -248,6 +249,7 @@ def make_desc(Q, K, V, O_like, w: int, scale: float | None) -> AttnDesc:
     dsc.k_stride[:] = _bnh_strides(K)
     dsc.v_stride[:] = _bnh_strides(V)
     dsc.o_stride[:] = _bnh_strides(O_like)
+    dsc.H_kv = K.shape[2] if K.shape[2] != H else 0  # GQA: K/V heads (0 = H)
     return dsc
 
 
@@ -461,7 +463,7 @@ def gfwa_bwd_normgate(Q, K, V, U, O, LSE, g, gamma, rstd, dY, w: int, eps: float
 
 def gfwa_bwd_rows_f32(Q, K, V, U, O, LSE, dO, w: int, head_rows: int, tail_rows: int,
                       scale: float | None = None, O_lo=None):
-    """gfwa_bwd plus fp32 copies [2 (dK, dV), B, rows, H, d] of dK, dV for the first
+    """gfwa_bwd plus fp32 copies [2 (dK, dV), B, rows, H_kv, d] of dK, dV for the first
     head_rows and last tail_rows key rows (sequence sharding: the halo's partial
     gradients travel and are added in fp32).  Returns (dQ, dK, dV, dU, head, tail)."""
     lib = load()
@@ -476,8 +478,9 @@ def gfwa_bwd_rows_f32(Q, K, V, U, O, LSE, dO, w: int, head_rows: int, tail_rows:
     dK = torch.empty_strided(K.shape, K.stride(), dtype=K.dtype, device=dev)
     dV = torch.empty_strided(V.shape, V.stride(), dtype=V.dtype, device=dev)
     dU = torch.empty(B, H, Nkv, dtype=torch.float32, device=dev)
-    head = torch.empty(2, B, head_rows, H, d, dtype=torch.float32, device=dev) if head_rows > 0 else None
-    tail = torch.empty(2, B, tail_rows, H, d, dtype=torch.float32, device=dev) if tail_rows > 0 else None
+    Hkv = K.shape[2]  # GQA: the copies have K's heads
+    head = torch.empty(2, B, head_rows, Hkv, d, dtype=torch.float32, device=dev) if head_rows > 0 else None
+    tail = torch.empty(2, B, tail_rows, Hkv, d, dtype=torch.float32, device=dev) if tail_rows > 0 else None
     dsc = make_desc(Q, K, V, O, w, scale)
     nbytes = lib.gfwa_bwd_workspace_size(ctypes.byref(dsc))
     ws = workspace(nbytes, dev, "bwd")

@@ -7,6 +7,7 @@ namespace gfwa {
 struct AttnParams {
     // problem
     int64_t B, H, Nq, Nkv, h0;  // h0 = Nkv - Nq halo rows
+    int64_t Hkv;                // K/V heads (GQA): query head h reads K/V head h / (H / Hkv)
     int d, w;
     float scale;
     // element strides over (b, n, h); d contiguous

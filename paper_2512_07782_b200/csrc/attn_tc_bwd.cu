@@ -95,12 +95,13 @@ struct TcBwdParams {
     __nv_bfloat16* dK;
     __nv_bfloat16* dV;
     int64_t ks[3], vs[3];  // dK / dV element strides over (b, n, h) (those of K / V)
-    int64_t Nq, Nkv, h0, H;
+    int64_t Nq, Nkv, h0, H, Hkv;
     int w;
-    int n_kt, n_items;  // key tiles per (b, h); work items = key tiles x H x B
+    int G;              // query heads per K/V head (GQA; 1 = MHA)
+    int n_kt, n_items;  // key tiles per (b, K/V head); work items = key tiles x Hkv x B
     int64_t B;
     // sequence sharding: fp32 copies of dK, dV for the first head_rows
-    // and the last tail_rows key rows, [2 (dK, dV)][B][rows][H][d] (null: none)
+    // and the last tail_rows key rows, [2 (dK, dV)][B][rows][Hkv][d] (null: none)
     float* f32_head;
     float* f32_tail;
     int64_t head_rows, tail_rows;
@@ -164,22 +165,25 @@ __device__ __forceinline__ uint32_t range_bits(int lo, int hi, int base) {
     return upto_z & ~below_a;
 }
 
-// One work item: a 128-key tile of one (b, h) and the 64-query steps whose
-// windows reach it (Alg. E.2 l.12-14)
+// One work item: a 128-key tile of one (b, K/V head h) and the 64-query steps whose
+// windows reach it (Alg. E.2 l.12-14), for each of the G query heads
+// h G + gi reading that K/V head (GQA): tot = G nsteps steps, head-major, all
+// accumulating into the same dK / dV
 struct BItem {
-    int b, h, j0, qt_lo, nsteps;
+    int b, h, j0, qt_lo, nsteps, tot;
 };
 __device__ __forceinline__ BItem make_bitem(const TcBwdParams& p, int idx) {
     BItem it;
     const int jt = idx % p.n_kt, bh = idx / p.n_kt;
-    it.h = bh % (int)p.H;
-    it.b = bh / (int)p.H;
+    it.h = bh % (int)p.Hkv;
+    it.b = bh / (int)p.Hkv;
     it.j0 = jt * BN;
     const int64_t j_last = min64((int64_t)it.j0 + BN, p.Nkv) - 1;
     const int64_t t_lo = max64(0, (int64_t)it.j0 - p.h0);
     const int64_t t_hi = min64(p.Nq - 1, j_last + p.w - 1 - p.h0);
     it.qt_lo = (int)(t_lo / BMQ);
     it.nsteps = t_lo <= t_hi ? (int)(t_hi / BMQ - it.qt_lo + 1) : 0;
+    it.tot = it.nsteps * p.G;
     return it;
 }
 
@@ -260,8 +264,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int idx = blockIdx.x; idx < p.n_items; idx += gridDim.x) {
             const BItem it = make_bitem(p, idx);
             if (it.nsteps == 0) continue;
-            const float* Ubh = p.U + ((int64_t)it.b * p.H + it.h) * p.Nkv;
-            const float uref = Ubh[it.j0];  // per-item bias reference (reading C-18)
             // K and V of the item
 #pragma unroll 1
             for (int kv = 0; kv < 2; ++kv) {
@@ -283,32 +285,40 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 __syncwarp();
             }
-            // the per-query vectors of step m + 1 are loaded while step m's stage is
-            // refilled (software pipelined: their global-load latency stays off the full barrier)
-            float vu[2], vl[2], vd[2];
-            auto fetch = [&](int m) {
+            // the per-query vectors of step f + 1 are loaded while step f's stage is
+            // refilled (software pipelined: their global-load latency stays off the full barrier).
+            // Step f = gi nsteps + m: query head h G + gi, query tile qt_lo + m
+            float vu[2], vl[2], vd[2], vref = 0.f;
+            auto fetch = [&](int f) {
+                const int gi = f / it.nsteps, m = f - gi * it.nsteps;
+                const int64_t bh = (int64_t)it.b * p.H + (int64_t)it.h * p.G + gi;
+                const float* Ubh = p.U + bh * p.Nkv;
+                if (f < it.tot) vref = Ubh[it.j0];  // per-(item, query head) bias reference (reading C-18)
 #pragma unroll
                 for (int i = 0; i < 2; ++i) {
                     const int64_t t = (int64_t)(it.qt_lo + m) * BMQ + lane + 32 * i;
-                    const bool ok = m < it.nsteps && t < p.Nq;
-                    const int64_t vi = ((int64_t)it.b * p.H + it.h) * p.Nq + t;
+                    const bool ok = f < it.tot && t < p.Nq;
+                    const int64_t vi = bh * p.Nq + t;
                     vu[i] = ok ? Ubh[t + p.h0] : 0.f;
                     vl[i] = ok ? p.LSE[vi] : 0.f;
                     vd[i] = ok ? p.Dv[vi] : 0.f;
                 }
             };
             fetch(0);
-            for (int m = 0; m < it.nsteps; ++m, ++g) {
-                const uint32_t s = pool.Q(m);
+            for (int f = 0; f < it.tot; ++f, ++g) {
+                const uint32_t s = pool.Q(f);
+                const int gi = f / it.nsteps, m = f - gi * it.nsteps;
+                const int hq = it.h * p.G + gi;
                 const int t0 = (it.qt_lo + m) * BMQ;
+                const float uref = vref;
                 acquire(s);
                 if (lane == 0) BTR(3, g);
                 if (elect_one()) {
                     mbar_expect_tx(&bars->full[s], 2 * kQT);
                     uint8_t* qd = pool_base + s * kSlot;
                     for (int half = 0; half < kHalves; ++half) {
-                        tma_load_4d(qd + half * kQTbox, &mq, &bars->full[s], half * 64, it.h, t0, it.b);
-                        tma_load_4d(qd + kQT + half * kQTbox, &mdo, &bars->full[s], half * 64, it.h, t0, it.b);
+                        tma_load_4d(qd + half * kQTbox, &mq, &bars->full[s], half * 64, hq, t0, it.b);
+                        tma_load_4d(qd + kQT + half * kQTbox, &mdo, &bars->full[s], half * 64, hq, t0, it.b);
                     }
                 }
                 // the bias slab of step g (slab g % 4, free once step g - 4's S^T/dP^T MMAs ran)
@@ -330,9 +340,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 fence_proxy_async();  // generic-proxy writes -> the tensor core's async proxy
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bars->full[s]);
-                fetch(m + 1);
+                fetch(f + 1);
             }
-            pool.advance(it.nsteps);
+            pool.advance(it.tot);
         }
     } else if (warp == kMmaWarp) {
         // ------------------------------------------------ MMA issuer
@@ -389,7 +399,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const BItem it = make_bitem(p, idx);
             if (it.nsteps == 0) continue;
             const uint32_t sK = pool.K(), sV = pool.V();
-            for (int m = 0; m < it.nsteps; ++m, ++g) {
+            for (int m = 0; m < it.tot; ++m, ++g) {  // m: flat step (query head major)
                 const uint32_t s = pool.Q(m);
                 const int bn = g & 1;
                 if (m == 0) {
@@ -417,18 +427,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mma_ss(buf + 64, sdesc_sw128(smem_u32(augA) + 32, 16, 0), bslab, id_st, 1u);
                     tc_commit(&bars->st_full[bn]);
                     tc_commit(&bars->aug_empty[g & 3]);
-                    if (m == it.nsteps - 1) tc_commit(&bars->empty[sV]);  // V's last reader was this dP^T
+                    if (m == it.tot - 1) tc_commit(&bars->empty[sV]);  // V's last reader was this dP^T
                 }
                 __syncwarp();
                 if (pg >= 0) mma2();
                 pg = g;
                 pm = m;
-                pn = it.nsteps;
+                pn = it.tot;
                 ps = s;
                 pk = sK;
                 pitem = nitem;
             }
-            pool.advance(it.nsteps);
+            pool.advance(it.tot);
             ++nitem;
         }
         if (pg >= 0) mma2();
@@ -442,9 +452,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int idx = blockIdx.x; idx < p.n_items; idx += gridDim.x) {
             const BItem it = make_bitem(p, idx);
             if (it.nsteps == 0) continue;
-            const float* Ubh = p.U + ((int64_t)it.b * p.H + it.h) * p.Nkv;
             const int64_t j0 = it.j0, j = j0 + kr;
             const bool kvalid = j < p.Nkv;
+#pragma unroll 1
+            for (int gi = 0; gi < p.G; ++gi) {  // query heads of this K/V head (GQA)
+            const int64_t bhq = (int64_t)it.b * p.H + (int64_t)it.h * p.G + gi;
+            const float* Ubh = p.U + bhq * p.Nkv;
             const float uref = Ubh[j0];
             const float nuk = kvalid ? -(Ubh[j] - uref) * kLog2e : 0.f;
             const uint64_t nuk2 = f2pack(nuk, nuk);
@@ -569,7 +582,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             float c0, c1;
             f2unpack(colsum2, c0, c1);
-            if (kvalid) red_add(p.dU + ((int64_t)it.b * p.H + it.h) * p.Nkv + j, -(c0 + c1));  // du^k (C-4)
+            if (kvalid) red_add(p.dU + bhq * p.Nkv + j, -(c0 + c1));  // du^k (C-4)
+            }
         }
     } else if (warp < kMmaWarp) {
         // ------------------------------------------------ dQ drain + dK/dV epilogue: thread = TMEM lane
@@ -619,7 +633,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int64_t r = tail ? j - (p.Nkv - p.tail_rows) : j;
             if (!base || r < 0 || r >= rows || j >= p.Nkv) return nullptr;
             const int64_t which = tsr ? 0 : 1;  // dK first, then dV
-            return base + (((which * p.B + it.b) * rows + r) * p.H + it.h) * D;
+            return base + (((which * p.B + it.b) * rows + r) * p.Hkv + it.h) * D;
         };
         int g = 0, nitem = 0, pg = -1;
         int64_t pt0 = 0, pbh = 0;
@@ -647,7 +661,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 continue;
             }
-            const int64_t bh = (int64_t)it.b * p.H + it.h;
+#pragma unroll 1
+            for (int gi = 0; gi < p.G; ++gi) {  // query heads of this K/V head (GQA)
+            const int hq = it.h * p.G + gi;
+            const int64_t bh = (int64_t)it.b * p.H + hq;
             for (int m = 0; m < it.nsteps; ++m, ++g) {
                 const int bm = g & 1;
                 const int64_t t0 = (int64_t)(it.qt_lo + m) * BMQ;
@@ -670,7 +687,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (GFWA_BWD_DQRED) {
                     // per query one coalesced 128-byte L2 reduction (lane = d): no staging
                     if (dlive && !GFWA_BWD_NODQ) {
-                        float* acc = p.dQacc + (((int64_t)it.b * p.Nq + t0) * p.H + it.h) * D + 32 * (warp & 3) + lane;
+                        float* acc = p.dQacc + (((int64_t)it.b * p.Nq + t0) * p.H + hq) * D + 32 * (warp & 3) + lane;
                         const int64_t qstride = p.H * D;
                         const int nq = (int)min64(BMQ, p.Nq - t0);
 #pragma unroll
@@ -694,7 +711,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         fence_proxy_async();
                         __syncwarp();
                         if (lane == 0 && !GFWA_BWD_NODQ) {
-                            tma_reduce_add_4d(&mdq, wbox + (r & 1) * kDQW, 32 * (warp & 3), it.h, (int)(t0 + 16 * r),
+                            tma_reduce_add_4d(&mdq, wbox + (r & 1) * kDQW, 32 * (warp & 3), hq, (int)(t0 + 16 * r),
                                               it.b);
                             bulk_commit();
                         }
@@ -703,6 +720,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 pg = g;
                 pt0 = t0;
                 pbh = bh;
+            }
             }
             // epilogue of the item: dV, dK (TMEM lane = key) -> bf16 [32 keys][64 d] boxes,
             // staged one at a time in this warp's 4 KB of the dQ staging and written by TMA
@@ -1059,11 +1077,11 @@ static gfwa_status_t tc_bwd_d(const AttnParams& pin, cudaStream_t st, void* ws) 
     p.dQacc = (float*)ws;
     CUtensorMap mq, mk, mv, mdo, mdk, mdv, mdq;
     GFWA_REQUIRE(encode_bnhd_map(&mq, p.Q, p.B, p.Nq, p.H, D, p.qs, BMQ));
-    GFWA_REQUIRE(encode_bnhd_map(&mk, p.K, p.B, p.Nkv, p.H, D, p.ks, BN));
-    GFWA_REQUIRE(encode_bnhd_map(&mv, p.V, p.B, p.Nkv, p.H, D, p.vs, BN));
+    GFWA_REQUIRE(encode_bnhd_map(&mk, p.K, p.B, p.Nkv, p.Hkv, D, p.ks, BN));
+    GFWA_REQUIRE(encode_bnhd_map(&mv, p.V, p.B, p.Nkv, p.Hkv, D, p.vs, BN));
     GFWA_REQUIRE(encode_bnhd_map(&mdo, p.dO, p.B, p.Nq, p.H, D, p.os, BMQ));
-    GFWA_REQUIRE(encode_bnhd_map(&mdk, p.dK, p.B, p.Nkv, p.H, D, p.ks, BN / 4));  // [32 keys][64 d] store boxes
-    GFWA_REQUIRE(encode_bnhd_map(&mdv, p.dV, p.B, p.Nkv, p.H, D, p.vs, BN / 4));
+    GFWA_REQUIRE(encode_bnhd_map(&mdk, p.dK, p.B, p.Nkv, p.Hkv, D, p.ks, BN / 4));  // [32 keys][64 d] store boxes
+    GFWA_REQUIRE(encode_bnhd_map(&mdv, p.dV, p.B, p.Nkv, p.Hkv, D, p.vs, BN / 4));
     const int64_t acc_s[3] = {p.Nq * p.H * D, p.H * D, D};  // dQacc [B, Nq, H, d] fp32
     GFWA_REQUIRE(encode_bnhd_map_f32(&mdq, p.dQacc, p.B, p.Nq, p.H, D, acc_s, 16));
     const int64_t rows = p.B * p.Nq * p.H;
@@ -1102,6 +1120,8 @@ static gfwa_status_t tc_bwd_d(const AttnParams& pin, cudaStream_t st, void* ws) 
     tp.Nkv = p.Nkv;
     tp.h0 = p.h0;
     tp.H = p.H;
+    tp.Hkv = p.Hkv;
+    tp.G = (int)(p.H / p.Hkv);
     tp.w = p.w;
     tp.sl2 = p.scale * kLog2e;
     tp.scale = p.scale;
@@ -1119,7 +1139,7 @@ static gfwa_status_t tc_bwd_d(const AttnParams& pin, cudaStream_t st, void* ws) 
     tp.f32_tail = p.f32_tail;
     tp.head_rows = p.f32_head_rows;
     tp.tail_rows = p.f32_tail_rows;
-    const int64_t n_items = (int64_t)tp.n_kt * p.H * p.B;
+    const int64_t n_items = (int64_t)tp.n_kt * p.Hkv * p.B;
     if (n_items >= ((int64_t)1 << 31)) return GFWA_ERR_INVALID_ARGUMENT;
     tp.n_items = (int)n_items;
     // per launch: the attribute is per device (a process may drive several GPUs)

@@ -106,6 +106,7 @@ struct TcFwdParams {
     float* LSE;
     int64_t Nq, Nkv, h0, H, B;
     int w;
+    int G;  // query heads per K/V head (GQA; 1 = MHA)
     int store_lo;
     int n_items, n_pairs;
     float* zero_acc;  // gfwa_fwd_train: the dQ accumulator [B, Nq, H, d] whose item rows are zeroed
@@ -321,7 +322,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         mbar_expect_tx(full, kTile);
                         for (int half = 0; half < kHalves; ++half)
                             tma_load_4d_hint(smem + kOffKV + sl * kTile + half * kBox, kv ? &mv : &mk, full,
-                                             half * 64, it.h, j * BN, it.b, pol_kv);
+                                             half * 64, it.h / p.G, j * BN, it.b, pol_kv);
                     }
                     if (kv == 0) {
                         // K_j's slab: b = (uref - u_k) / scale per key as hi + mid + lo bf16, so the
@@ -889,8 +890,8 @@ template <int D>
 static gfwa_status_t tc_fwd_d(const AttnParams& p, cudaStream_t st) {
     CUtensorMap mq, mk, mv, mo, mol;
     GFWA_REQUIRE(encode_bnhd_map(&mq, p.Q, p.B, p.Nq, p.H, D, p.qs, BM));
-    GFWA_REQUIRE(encode_bnhd_map(&mk, p.K, p.B, p.Nkv, p.H, D, p.ks, BN));
-    GFWA_REQUIRE(encode_bnhd_map(&mv, p.V, p.B, p.Nkv, p.H, D, p.vs, BN));
+    GFWA_REQUIRE(encode_bnhd_map(&mk, p.K, p.B, p.Nkv, p.Hkv, D, p.ks, BN));
+    GFWA_REQUIRE(encode_bnhd_map(&mv, p.V, p.B, p.Nkv, p.Hkv, D, p.vs, BN));
     GFWA_REQUIRE(encode_bnhd_map(&mo, p.O, p.B, p.Nq, p.H, D, p.os, BM));
     if (p.O_lo)
         GFWA_REQUIRE(encode_bnhd_map(&mol, p.O_lo, p.B, p.Nq, p.H, D, p.os, BM));
@@ -905,6 +906,7 @@ static gfwa_status_t tc_fwd_d(const AttnParams& p, cudaStream_t st) {
     tp.H = p.H;
     tp.B = p.B;
     tp.w = p.w;
+    tp.G = (int)(p.H / p.Hkv);
     tp.store_lo = p.O_lo != nullptr;
     tp.zero_acc = p.zero_acc;
     tp.token = p.token;

@@ -47,7 +47,7 @@ bool packed(const int64_t* st, const AttnParams& p) {
     return st[2] == p.d && st[1] == p.H * p.d && st[0] == p.Nq * p.H * p.d;
 }
 bool packed_kv(const int64_t* st, const AttnParams& p) {
-    return st[2] == p.d && st[1] == p.H * p.d && st[0] == p.Nkv * p.H * p.d;
+    return st[2] == p.d && st[1] == p.Hkv * p.d && st[0] == p.Nkv * p.Hkv * p.d;
 }
 bool check_finite_env();
 
@@ -109,6 +109,8 @@ gfwa_status_t make_params(const gfwa_attn_desc_t* d, AttnParams& p) {
     p = AttnParams{};
     p.B = d->B;
     p.H = d->H;
+    if (d->H_kv < 0 || (d->H_kv > 0 && d->H % d->H_kv != 0)) return GFWA_ERR_INVALID_ARGUMENT;
+    p.Hkv = d->H_kv > 0 ? d->H_kv : d->H;
     p.Nq = d->N_q;
     p.Nkv = d->N_kv;
     p.h0 = d->N_kv - d->N_q;
@@ -176,6 +178,7 @@ extern "C" gfwa_status_t gfwa_fwd(const gfwa_attn_desc_t* desc, const void* Q, c
         p.ng_Y = g_normgate.Y;
     }
     cudaStream_t st = (cudaStream_t)stream;
+    if (p.Hkv != p.H && !tc_fwd_supported(p, desc->dtype)) return GFWA_ERR_UNSUPPORTED;  // GQA: tensor-core path
     gfwa_status_t s = tc_fwd_supported(p, desc->dtype) ? tc_fwd(p, st) : simt_fwd(p, desc->dtype, st);
     if (s != GFWA_OK || !check_finite_env()) return s;
     // opt-in debug check (GFWA_CHECK_FINITE=1): LSE, and O when it is packed
@@ -290,6 +293,7 @@ extern "C" gfwa_status_t gfwa_bwd(const gfwa_attn_desc_t* desc, const void* Q, c
         p.f32_tail_rows = g_rows.tail_rows;
     }
     cudaStream_t st = (cudaStream_t)stream;
+    if (p.Hkv != p.H && !tc_bwd_supported(p, desc->dtype)) return GFWA_ERR_UNSUPPORTED;  // GQA: tensor-core path
     gfwa_status_t s;
     if (tc_bwd_supported(p, desc->dtype)) {
         s = tc_bwd(p, st, (char*)ws + off_tc);  // D, dQ/dU zeroing fused in its own pre kernel
@@ -302,7 +306,7 @@ extern "C" gfwa_status_t gfwa_bwd(const gfwa_attn_desc_t* desc, const void* Q, c
         if ((s = gfwa_check_finite(GFWA_F32, dU, p.B * p.H * p.Nkv, stream)) != GFWA_OK) return s;
         if (packed(p.qs, p) && (s = gfwa_check_finite(desc->dtype, dQ, p.B * p.Nq * p.H * p.d, stream)) != GFWA_OK)
             return s;
-        const int64_t nkv = p.B * p.Nkv * p.H * p.d;
+        const int64_t nkv = p.B * p.Nkv * p.Hkv * p.d;
         if (packed_kv(p.ks, p) && (s = gfwa_check_finite(desc->dtype, dK, nkv, stream)) != GFWA_OK) return s;
         if (packed_kv(p.vs, p) && (s = gfwa_check_finite(desc->dtype, dV, nkv, stream)) != GFWA_OK) return s;
     }
