@@ -95,6 +95,40 @@ def test_bf16_path_matches_oracle(s):
         assert max_abs(got[k], ref[k]) <= TOL_BF16_GRAD, k
 
 
+@pytest.mark.parametrize("d", [128, 64])
+def test_bf16_late_max_growth(d):
+    """Keys far back in the window that outscore every key of the query's own tile by
+    2^11-2^16 (alpha = 0: no decay).  The forward walks key tiles diagonal-first, so
+    these keys arrive after a row's reference max is set and force the lazy rescale
+    of O and l (Alg. 2 l. "o <- diag(e^{m_old - m_new}) o + p v"; the kernel
+    moves its reference only when the row max grows by > 2^8).  dO is scaled by 1/16: the
+    spiked keys collect nearly all of the ~600 queries' probability, and dV at those
+    rows would otherwise reach ~25, where one bf16 ulp alone exceeds 5e-2."""
+    s = synth.AttnShape(B=1, H=2, N=640, d=d, w=640)
+    Q, K, V, dO = synth.attn_inputs(s, seed=11, dtype=torch.float32)
+    g = torch.Generator().manual_seed(12)
+    for h in range(s.H):
+        u = Q[0, 0, h] / Q[0, 0, h].norm() * d ** 0.5
+        Q[0, :, h] = u + 0.3 * torch.randn(s.N, d, generator=g)
+        K[0, 40, h] = u          # column 40: half 0, third 16-key chunk
+        K[0, 120, h] = 0.7 * u   # column 120: half 1, last chunk
+        K[0, 300, h] = 0.9 * u   # a spike in a middle tile as well
+    dO = dO / 16
+    Q, K, V, dO = (x.to(torch.bfloat16) for x in (Q, K, V, dO))
+    U = torch.zeros(s.B, s.H, s.N)
+    Qd, Kd, Vd, dOd, Ud = (x.cuda() for x in (Q, K, V, dO, U))
+    O, LSE, Olo = gb.gfwa_fwd(Qd, Kd, Vd, Ud, s.w, want_o_lo=True)
+    dQ, dK, dV, dU, da = gb.gfwa_bwd(Qd, Kd, Vd, Ud, O, LSE, dOd, s.w, O_lo=Olo)
+    torch.cuda.synchronize()
+    Or, Lr = oracle.fwd(Q, K, V, U, s.w)
+    ref = oracle.bwd(Q, K, V, U, dO, s.w)
+    assert max_abs(O, Or) <= TOL_BF16_O
+    assert max_abs(LSE, Lr) <= TOL_LSE
+    got = dict(dQ=dQ, dK=dK, dV=dV, dU=dU, dalpha=da)
+    for k in got:
+        assert max_abs(got[k], ref[k]) <= TOL_BF16_GRAD, k
+
+
 def test_end_to_end_from_gate_inputs():
     """gate scan -> attention -> backward -> gate chain vs the oracle chain."""
     from paper_2512_07782_b200 import gated_fwa
