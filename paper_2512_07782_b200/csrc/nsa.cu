@@ -14,12 +14,17 @@
 // The local branch o_loc is gfwa_fwd (the tensor-core GatedFWA kernel).
 // These are CUDA-core kernels: the compressed branch is ~N/blk keys per query and
 // the selected branch (n_sel + 1) blk keys, a small multiple of the local window.
+// The per-query / per-block walks take kU keys (queries) per round: their rows are
+// loaded together and the kU warp reductions interleaved, so a round pays one
+// load latency and one reduction latency instead of kU (the serial per-key walk
+// was latency-bound).
 #include "common.cuh"
 
 namespace gfwa {
 namespace {
 
 constexpr int kWarpsPerBlock = 8;
+constexpr int kU = 8;  // keys per round in the selected-branch kernels (loads in flight, interleaved reductions)
 
 __device__ __forceinline__ uint32_t pack_bf16x2_nsa(float lo, float hi) {
     __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
@@ -62,6 +67,20 @@ __device__ __forceinline__ void load_row(const __nv_bfloat16* p, int lane, float
         v[1] = __uint_as_float(w & 0xffff0000u);
     }
 }
+
+// the same row left packed (C / 2 words of bf16 pairs), unpacked at use
+template <int D>
+__device__ __forceinline__ void load_raw(const __nv_bfloat16* p, int lane, uint32_t (&w)[D / 64]) {
+    if constexpr (D / 64 == 2) {
+        const uint2 x = *reinterpret_cast<const uint2*>(p + 4 * lane);
+        w[0] = x.x;
+        w[1] = x.y;
+    } else {
+        w[0] = *reinterpret_cast<const uint32_t*>(p + 2 * lane);
+    }
+}
+__device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
 
 template <int D>
 __global__ void __launch_bounds__(32 * kWarpsPerBlock) nsa_cmp_select_kernel(
@@ -156,20 +175,50 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) nsa_slc_kernel(
         const int ib = sl[k];
         if (ib < 0) continue;
         const int64_t j1 = min64((int64_t)(ib + 1) * blk - 1, t);
-        for (int64_t j = (int64_t)ib * blk; j <= j1; ++j) {
-            float kv[C];
-            load_row<D>(K + ((b * N + j) * H + hh) * D, lane, kv);
-            float s = 0.f;
+        // kU keys per round: their K and V rows loaded together, the kU dot products
+        // reduced across the warp interleaved, one online-softmax update per round
+        for (int64_t j = (int64_t)ib * blk; j <= j1; j += kU) {
+            const int nk = (int)min64(kU, j1 - j + 1);
+            float kv[kU][C], sc[kU];
+            uint32_t vv[kU][C / 2];
 #pragma unroll
-            for (int c = 0; c < C; ++c) s = fmaf(q[c], kv[c], s);
-            s = warp_sum(s) * scale;
-            const float mn = fmaxf(m, s);
-            const float corr = __expf(m - mn), p = __expf(s - mn);
-            float vv[C];
-            load_row<D>(V + ((b * N + j) * H + hh) * D, lane, vv);
+            for (int u = 0; u < kU; ++u) {
+                const int64_t ju = u < nk ? j + u : j;  // tail: re-read row j, masked below
+                load_row<D>(K + ((b * N + ju) * H + hh) * D, lane, kv[u]);
+                load_raw<D>(V + ((b * N + ju) * H + hh) * D, lane, vv[u]);
+            }
 #pragma unroll
-            for (int c = 0; c < C; ++c) acc[c] = acc[c] * corr + p * vv[c];
-            l = l * corr + p;
+            for (int u = 0; u < kU; ++u) {
+                float x = 0.f;
+#pragma unroll
+                for (int c = 0; c < C; ++c) x = fmaf(q[c], kv[u][c], x);
+                sc[u] = x;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                for (int u = 0; u < kU; ++u) sc[u] += __shfl_xor_sync(0xffffffffu, sc[u], o);
+            float mx = -INFINITY;
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                sc[u] = u < nk ? sc[u] * scale : -INFINITY;
+                mx = fmaxf(mx, sc[u]);
+            }
+            const float mn = fmaxf(m, mx);  // finite: nk >= 1
+            const float corr = __expf(m - mn);
+            l *= corr;
+#pragma unroll
+            for (int c = 0; c < C; ++c) acc[c] *= corr;
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const float pu = __expf(sc[u] - mn);
+                l += pu;
+#pragma unroll
+                for (int c = 0; c < C; c += 2) {
+                    acc[c] = fmaf(pu, bf_lo(vv[u][c / 2]), acc[c]);
+                    acc[c + 1] = fmaf(pu, bf_hi(vv[u][c / 2]), acc[c + 1]);
+                }
+            }
             m = mn;
         }
     }
@@ -270,20 +319,37 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) nsa_cmp_dq_kernel(
         dq[c] = 0.f;
     }
     const float L = Lc[(b * H + hh) * N + t], Dv = Dc[(b * H + hh) * N + t];
-    for (int i = 0; i < nc; ++i) {
-        const float* kr = Kc + ((b * nb + i) * H + hh) * D + C * lane;
-        const float* vr = Vc + ((b * nb + i) * H + hh) * D + C * lane;
-        float s = 0.f, dp = 0.f;
+    for (int i0 = 0; i0 < nc; i0 += kU) {
+        const int ni = min(kU, nc - i0);
+        float kr[kU][C], sc[kU], dp[kU];
 #pragma unroll
-        for (int c = 0; c < C; ++c) {
-            s = fmaf(q[c], kr[c], s);
-            dp = fmaf(go[c], vr[c], dp);
+        for (int u = 0; u < kU; ++u) {
+            const int i = u < ni ? i0 + u : i0;
+            const float* kp = Kc + ((b * nb + i) * H + hh) * D + C * lane;
+            const float* vp = Vc + ((b * nb + i) * H + hh) * D + C * lane;
+            float x = 0.f, y = 0.f;
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                kr[u][c] = kp[c];
+                x = fmaf(q[c], kr[u][c], x);
+                y = fmaf(go[c], vp[c], y);
+            }
+            sc[u] = x;
+            dp[u] = y;
         }
-        s = warp_sum(s) * scale;
-        dp = warp_sum(dp);
-        const float ds = __expf(s - L) * (dp - Dv);
 #pragma unroll
-        for (int c = 0; c < C; ++c) dq[c] = fmaf(scale * ds, kr[c], dq[c]);
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                sc[u] += __shfl_xor_sync(0xffffffffu, sc[u], o);
+                dp[u] += __shfl_xor_sync(0xffffffffu, dp[u], o);
+            }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const float ds = u < ni ? __expf(sc[u] * scale - L) * (dp[u] - Dv) : 0.f;
+#pragma unroll
+            for (int c = 0; c < C; ++c) dq[c] = fmaf(scale * ds, kr[u][c], dq[c]);
+        }
     }
 #pragma unroll
     for (int c = 0; c < C; ++c) dQacc[row * D + C * lane + c] = dq[c];
@@ -310,25 +376,47 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) nsa_cmp_dkv_kernel(
         dk[c] = 0.f;
         dv[c] = 0.f;
     }
-    for (int64_t t = (i + 1) * blk - 1; t < N; ++t) {
-        const int64_t row = (b * N + t) * H + hh;
-        float q[C], go[C];
-        load_row<D>(Q + row * D, lane, q);
-        float s = 0.f, dp = 0.f;
+    // kU queries per round: their rows, L and D loaded together, reductions interleaved
+    for (int64_t t0 = (i + 1) * blk - 1; t0 < N; t0 += kU) {
+        const int nt = (int)min64(kU, N - t0);
+        float q[kU][C], go[kU][C], sc[kU], dp[kU], Lt[kU], Dt[kU];
 #pragma unroll
-        for (int c = 0; c < C; ++c) {
-            go[c] = dOc[row * D + C * lane + c];
-            s = fmaf(q[c], kc[c], s);
-            dp = fmaf(go[c], vc[c], dp);
+        for (int u = 0; u < kU; ++u) {
+            const int64_t t = u < nt ? t0 + u : t0;
+            const int64_t row = (b * N + t) * H + hh;
+            load_row<D>(Q + row * D, lane, q[u]);
+#pragma unroll
+            for (int c = 0; c < C; ++c) go[u][c] = dOc[row * D + C * lane + c];
+            Lt[u] = Lc[(b * H + hh) * N + t];
+            Dt[u] = Dc[(b * H + hh) * N + t];
         }
-        s = warp_sum(s) * scale;
-        dp = warp_sum(dp);
-        const float p = __expf(s - Lc[(b * H + hh) * N + t]);
-        const float ds = p * (dp - Dc[(b * H + hh) * N + t]);
 #pragma unroll
-        for (int c = 0; c < C; ++c) {
-            dk[c] = fmaf(scale * ds, q[c], dk[c]);
-            dv[c] = fmaf(p, go[c], dv[c]);
+        for (int u = 0; u < kU; ++u) {
+            float x = 0.f, y = 0.f;
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                x = fmaf(q[u][c], kc[c], x);
+                y = fmaf(go[u][c], vc[c], y);
+            }
+            sc[u] = x;
+            dp[u] = y;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                sc[u] += __shfl_xor_sync(0xffffffffu, sc[u], o);
+                dp[u] += __shfl_xor_sync(0xffffffffu, dp[u], o);
+            }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const float p = u < nt ? __expf(sc[u] * scale - Lt[u]) : 0.f;
+            const float ds = p * (dp[u] - Dt[u]);
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                dk[c] = fmaf(scale * ds, q[u][c], dk[c]);
+                dv[c] = fmaf(p, go[u][c], dv[c]);
+            }
         }
     }
 #pragma unroll
@@ -363,22 +451,37 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) nsa_slc_bwd_kernel(
         const int ib = sl[k];
         if (ib < 0) continue;
         const int64_t j1 = min64((int64_t)(ib + 1) * blk - 1, t);
-        for (int64_t j = (int64_t)ib * blk; j <= j1; ++j) {
-            const int64_t kr = (b * N + j) * H + hh;
-            float kv[C], vv[C];
-            load_row<D>(K + kr * D, lane, kv);
-            load_row<D>(V + kr * D, lane, vv);
-            float s = 0.f, dp = 0.f;
+        for (int64_t j = (int64_t)ib * blk; j <= j1; j += kU) {
+            const int nk = (int)min64(kU, j1 - j + 1);
+            float kv[kU][C], sc[kU], dp[kU];
 #pragma unroll
-            for (int c = 0; c < C; ++c) {
-                s = fmaf(q[c], kv[c], s);
-                dp = fmaf(go[c], vv[c], dp);
+            for (int u = 0; u < kU; ++u) {
+                const int64_t kr = (b * N + (u < nk ? j + u : j)) * H + hh;
+                float vv[C];
+                load_row<D>(K + kr * D, lane, kv[u]);
+                load_row<D>(V + kr * D, lane, vv);
+                float x = 0.f, y = 0.f;
+#pragma unroll
+                for (int c = 0; c < C; ++c) {
+                    x = fmaf(q[c], kv[u][c], x);
+                    y = fmaf(go[c], vv[c], y);
+                }
+                sc[u] = x;
+                dp[u] = y;
             }
-            s = warp_sum(s) * scale;
-            dp = warp_sum(dp);
-            const float p = __expf(s - L), ds = p * (dp - Dv);
 #pragma unroll
-            for (int c = 0; c < C; ++c) dq[c] = fmaf(scale * ds, kv[c], dq[c]);
+            for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                for (int u = 0; u < kU; ++u) {
+                    sc[u] += __shfl_xor_sync(0xffffffffu, sc[u], o);
+                    dp[u] += __shfl_xor_sync(0xffffffffu, dp[u], o);
+                }
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const float p = u < nk ? __expf(sc[u] * scale - L) : 0.f, ds = p * (dp[u] - Dv);
+#pragma unroll
+                for (int c = 0; c < C; ++c) dq[c] = fmaf(scale * ds, kv[u][c], dq[c]);
+            }
         }
     }
 #pragma unroll
@@ -441,7 +544,9 @@ __global__ void __launch_bounds__(256) nsa_slc_dkv_kernel(
     float* __restrict__ dKacc, float* __restrict__ dVacc, int64_t B, int64_t N, int64_t H, int blk, int nsel,
     int nbp, float scale) {
     constexpr int M = D / 4;  // channels per thread
-    __shared__ float s_q[D], s_go[D];
+    constexpr int kQB = 16;
+    __shared__ float s_q[kQB][D], s_go[kQB][D], s_L[kQB], s_D[kQB];
+    __shared__ int s_t[kQB];
     const int64_t r = blockIdx.x;  // (b, h, block)
     const int ib = (int)(r % nbp);
     const int64_t bh = r / nbp, hh = bh % H, b = bh / H;
@@ -459,32 +564,42 @@ __global__ void __launch_bounds__(256) nsa_slc_dkv_kernel(
     }
     const int n = cnt[r], o0 = off[r];
     const int* lst = list + bh * N * (nsel + 1) + o0;
-    for (int qi = 0; qi < n; ++qi) {
-        const int t = lst[qi];
-        const int64_t row = (b * N + t) * H + hh;
-        __syncthreads();  // the previous query's rows are consumed
-        for (int c = threadIdx.x; c < D; c += blockDim.x) {
-            s_q[c] = __bfloat162float(Q[row * D + c]);
-            s_go[c] = dOs[row * D + c];
+    // kQB listed queries staged per round (their Q / dO rows, L, D loaded together)
+    for (int q0 = 0; q0 < n; q0 += kQB) {
+        const int nq = min(kQB, n - q0);
+        __syncthreads();  // the previous round's rows are consumed
+        for (int e = threadIdx.x; e < nq * D; e += blockDim.x) {
+            const int qi = e / D, c = e % D;
+            const int64_t row = (b * N + lst[q0 + qi]) * H + hh;
+            s_q[qi][c] = __bfloat162float(Q[row * D + c]);
+            s_go[qi][c] = dOs[row * D + c];
+        }
+        if (threadIdx.x < nq) {
+            const int t = lst[q0 + threadIdx.x];
+            s_t[threadIdx.x] = t;
+            s_L[threadIdx.x] = Ls[bh * N + t];
+            s_D[threadIdx.x] = Ds[bh * N + t];
         }
         __syncthreads();
-        float s = 0.f, dp = 0.f;
+        for (int qi = 0; qi < nq; ++qi) {
+            float s = 0.f, dp = 0.f;
 #pragma unroll
-        for (int m = 0; m < M; ++m) {
-            s = fmaf(s_q[sub + 4 * m], kr[m], s);
-            dp = fmaf(s_go[sub + 4 * m], vr[m], dp);
-        }
-        s += __shfl_xor_sync(0xffffffffu, s, 1);
-        s += __shfl_xor_sync(0xffffffffu, s, 2);
-        dp += __shfl_xor_sync(0xffffffffu, dp, 1);
-        dp += __shfl_xor_sync(0xffffffffu, dp, 2);
-        if (!kvalid || j > t) continue;  // causal inside the block
-        const float p = __expf(s * scale - Ls[bh * N + t]);
-        const float ds = p * (dp - Ds[bh * N + t]);
+            for (int m = 0; m < M; ++m) {
+                s = fmaf(s_q[qi][sub + 4 * m], kr[m], s);
+                dp = fmaf(s_go[qi][sub + 4 * m], vr[m], dp);
+            }
+            s += __shfl_xor_sync(0xffffffffu, s, 1);
+            s += __shfl_xor_sync(0xffffffffu, s, 2);
+            dp += __shfl_xor_sync(0xffffffffu, dp, 1);
+            dp += __shfl_xor_sync(0xffffffffu, dp, 2);
+            if (!kvalid || j > s_t[qi]) continue;  // causal inside the block
+            const float p = __expf(s * scale - s_L[qi]);
+            const float ds = p * (dp - s_D[qi]);
 #pragma unroll
-        for (int m = 0; m < M; ++m) {
-            dk[m] = fmaf(scale * ds, s_q[sub + 4 * m], dk[m]);
-            dv[m] = fmaf(p, s_go[sub + 4 * m], dv[m]);
+            for (int m = 0; m < M; ++m) {
+                dk[m] = fmaf(scale * ds, s_q[qi][sub + 4 * m], dk[m]);
+                dv[m] = fmaf(p, s_go[qi][sub + 4 * m], dv[m]);
+            }
         }
     }
     if (!kvalid) return;
