@@ -470,6 +470,30 @@ def measure_seq(steps, warmup, dist, rank, world, local, dev, sample_clocks=Fals
         out["clocks"] = clk.summary()
     launches = gb.launch_count() - n0
     ms = _max_over_ranks(dist, e0.elapsed_time(e1) / steps, dev)
+    # e2e: the same sharded step with this rank's inputs copied from pinned host memory
+    # and its results (O, dQ, dK, dV, dh, dbeta) copied back every step, pipelined on
+    # copy streams like the dense path's; each device input set has its own halo slot
+    ext_sets = []
+
+    def alloc_set():
+        Qb, dOb = torch.empty_like(Q), torch.empty_like(dO)
+        (Kx, Vx), Kb, Vb = alloc_kv_ext(torch.empty_like(K), torch.empty_like(V), s.w)
+        ext_sets.append(((Kx, Vx), Kb.data_ptr()))
+        return [Qb, Kb, Vb, dOb, torch.empty_like(h), torch.empty_like(beta)]
+
+    def compute_set(bufs):
+        Qb, Kb, Vb, dOb, hb, bb = bufs
+        ext = next(e for e, ptr in ext_sets if ptr == Kb.data_ptr())
+        res = sp_forward_backward(Qb, Kb, Vb, hb, bb, dOb, s.w, ops, ring, kv_ext=ext)
+        return (res.O, res.dQ, res.dK, res.dV, res.dh, res.dbeta)
+
+    class _A:  # run_e2e reads args.steps only
+        pass
+    a = _A()
+    a.steps = steps
+    out["e2e"] = run_e2e(a, s, Q, K, V, dO, h, beta, None, dev, world, dist, compute_fn=compute_set,
+                         alloc_fn=alloc_set)
+    del ext_sets
     fl = 14.0 * Ng * s.w * s.d * s.B * s.H  # fwd 4 + bwd 10 (north_star in-window count)
     out.update({
         "ms_per_step": round(ms, 4), "tokens_per_s": round(s.B * Ng / (ms * 1e-3), 1),
@@ -492,7 +516,7 @@ def _traffic_from_profiles(kind: str, workload: str):
         return None
 
 
-def run_e2e(args, s, Q, K, V, dO, h, beta, step_fn, dev, world, dist):
+def run_e2e(args, s, Q, K, V, dO, h, beta, step_fn, dev, world, dist, compute_fn=None, alloc_fn=None):
     """The step end to end through the public API with host buffers: every step
     copies its inputs from pinned host memory (H2D) and its results back (D2H).
     Copies run on their own streams (the two copy engines, PCIe full duplex) and
@@ -504,7 +528,10 @@ def run_e2e(args, s, Q, K, V, dO, h, beta, step_fn, dev, world, dist):
     from paper_2512_07782_b200 import binding as gb
 
     host_in = [x.cpu().pin_memory() for x in (Q, K, V, dO, h, beta)]
-    dev_in = [[torch.empty_like(x, device=dev) for x in host_in] for _ in range(2)]
+    if alloc_fn is None:
+        dev_in = [[torch.empty_like(x, device=dev) for x in host_in] for _ in range(2)]
+    else:  # the caller's device buffers (e.g. K/V views behind a halo slot)
+        dev_in = [alloc_fn() for _ in range(2)]
     outs_host = None
     comp = torch.cuda.current_stream(dev)
     s_h2d, s_d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
@@ -513,6 +540,8 @@ def run_e2e(args, s, Q, K, V, dO, h, beta, step_fn, dev, world, dist):
     n = max(8, min(2 * args.steps, 24))
 
     def compute(bufs):
+        if compute_fn is not None:
+            return compute_fn(bufs)
         Qd, Kd, Vd, dOd, hd, bd = bufs
         U = gb.gfwa_gate_prefix(hd, bd)
         O, LSE, Olo = gb.gfwa_fwd(Qd, Kd, Vd, U, s.w, want_o_lo=True, prepare_bwd=True)
