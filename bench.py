@@ -123,7 +123,8 @@ def _dist():
         import torch
         import torch.distributed as dist
 
-        dist.init_process_group(os.environ.get("GFWA_BENCH_BACKEND", "nccl"))
+        if not dist.is_initialized():  # run_ours hands the N > 1 headline to run_seq
+            dist.init_process_group(os.environ.get("GFWA_BENCH_BACKEND", "nccl"))
         local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
         return dist, dist.get_rank(), ws, local
     return None, 0, 1, 0
@@ -499,7 +500,8 @@ def measure_seq(steps, warmup, dist, rank, world, local, dev, sample_clocks=Fals
         "ms_per_step": round(ms, 4), "tokens_per_s": round(s.B * Ng / (ms * 1e-3), 1),
         "tflops_in_window": round(fl / (ms * 1e-3) / 1e12, 2), "gpu_launches": launches, "steps": steps,
         "config": {"workload": "C4 (BASELINE configs[3])", "B": s.B, "H": s.H, "N": Ng, "rows_per_rank": S,
-                   "d": s.d, "w": s.w, "parallelism": f"sequence-sharded x{world} (w-row K/V/u halo, NCCL P2P)",
+                   "d": s.d, "w": s.w, "parallelism": f"sequence-sharded x{world} (w-row K/V/u halo, "
+                                  f"{(dist.get_backend().upper() + ' P2P') if dist else 'no exchange'})",
                    "l2": "inputs larger than L2, no flush"}})
     del Q, K, V, dO, h, beta, kv_ext
     torch.cuda.empty_cache()
