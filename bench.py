@@ -418,7 +418,7 @@ def run_seq(args, aux_c2: bool = False):
         "data": "synthetic (synth.py seeded per rank)",
         "config": r["config"],
         "tflops_in_window": r["tflops_in_window"], "pct_bf16_peak": round(r["tflops_in_window"] / peaks["bf16"], 4),
-        "gpu_launches": r["gpu_launches"], "clocks": r.get("clocks"),
+        "roofline": r.get("roofline"), "gpu_launches": r["gpu_launches"], "clocks": r.get("clocks"),
         "e2e": r.get("e2e"), "aux": aux,
     }), flush=True)
 
@@ -487,6 +487,34 @@ def measure_seq(steps, warmup, dist, rank, world, local, dev, sample_clocks=Fals
         ext = next(e for e, ptr in ext_sets if ptr == Kb.data_ptr())
         res = sp_forward_backward(Qb, Kb, Vb, hb, bb, dOb, s.w, ops, ring, kv_ext=ext)
         return (res.O, res.dQ, res.dK, res.dV, res.dh, res.dbeta)
+
+    # roofline of the dominant kernel: this rank's backward main kernel on its [halo; local]
+    # rows, timed by the library's stage events on the launching stream (max over ranks)
+    hx, bx = (torch.cat([h[:, :s.w], h], 1), torch.cat([beta[:, :s.w], beta], 1)) if rank > 0 else (h, beta)
+    Kr, Vr = kv_ext if rank > 0 else (K, V)
+    Ux = gb.gfwa_gate_prefix(hx, bx)
+    O_, LSE_, Olo_ = gb.gfwa_fwd(Q, Kr, Vr, Ux, s.w, want_o_lo=True, prepare_bwd=True)
+    mains = []
+    for _ in range(3):
+        sev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        for x in sev:
+            x.record(st)
+        gb.debug_stage_events(sev)
+        gb.gfwa_bwd(Q, Kr, Vr, Ux, O_, LSE_, dO, s.w, O_lo=Olo_, want_dalpha=False)
+        torch.cuda.synchronize(dev)
+        mains.append(sev[0].elapsed_time(sev[1]))
+        gb.gfwa_fwd(Q, Kr, Vr, Ux, s.w, want_o_lo=True, prepare_bwd=True)  # re-prepare the dQ accumulator
+    main_ms = _max_over_ranks(dist, sorted(mains)[1], dev)
+    del O_, LSE_, Olo_, Ux, hx, bx
+    peaks = _peaks()
+    fl_b = 10.0 * S * s.w * s.d * s.B * s.H
+    ach = fl_b / (main_ms * 1e-3) / 1e12
+    out["roofline"] = {"kernel": "bwd_tc_kernel", "bound": "tensor", "achieved": round(ach, 2),
+                       "peak": peaks["bf16"], "unit": "TFLOP/s", "frac": round(ach / peaks["bf16"], 4),
+                       "traffic": None, "kernel_ms": round(main_ms, 4),
+                       "peak_src": f"{peaks['src']} bf16 burst (MEASURED_PEAKS.json bf16_tflops)",
+                       "algorithmic": f"10*S*w*d*B*H = {fl_b:.4g} FLOP/launch per rank (S = N/P rows; "
+                                      "north_star in-window count)"}
 
     class _A:  # run_e2e reads args.steps only
         pass

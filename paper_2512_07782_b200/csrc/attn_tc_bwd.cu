@@ -78,6 +78,9 @@ constexpr int kThreads = 32 * (kTmaWarp + 1);  // softmax-grad WGs, drain WG, MM
 #ifndef GFWA_BWD_DQRED
 #define GFWA_BWD_DQRED 0  // 1: dQ^T drained by per-query red.global.add instead of TMA bulk reductions
 #endif
+#ifndef GFWA_BWD_SFIRST
+#define GFWA_BWD_SFIRST 0  // issue S^T(g) before waiting for the drain of dQ^T(g-2) (only dP^T(g) needs it)
+#endif
 #ifndef GFWA_BWD_NODUQ
 #define GFWA_BWD_NODUQ 0  // experiment only: skip the du^q butterfly (wrong dU)
 #endif
@@ -407,6 +410,46 @@ __global__ void __launch_bounds__(kThreads, 1)
                     wait_full(sV);
                 }
                 wait_full(s);
+#if GFWA_BWD_SFIRST
+                // S^T(g) writes columns [0,64) of buffer g&1 (P^T / dS^T of step g-2, read by
+                // gradient MMAs already issued ahead of it); only dP^T(g), in [64,128), needs
+                // dQ^T(g-2) drained -- so S^T(g) runs on the tensor core during the drain
+                tc_fence_after();
+                if (elect_one()) {
+                    const uint32_t qb = pb + s * kSlot;
+                    const uint32_t kb = pb + sK * kSlot;
+                    const uint32_t buf = tmem + 128 * bn;
+#pragma unroll
+                    for (int kk = 0; kk < D / 16 && GFWA_BWD_EXPT != 2; ++kk) {
+                        const uint32_t ka = (kk >> 2) * kKVbox + (kk & 3) * 32;
+                        const uint32_t qa = (kk >> 2) * kQTbox + (kk & 3) * 32;
+                        mma_ss(buf, sdesc_sw128(kb + ka, 16, 1024), sdesc_sw128(qb + qa, 16, 1024), id_st, kk > 0);
+                    }
+                    const uint64_t bslab = sdesc_sw128(smem_u32(augB) + 32 * (g & 3), 16, 1024);
+                    mma_ss(buf, sdesc_sw128(smem_u32(augA), 16, 0), bslab, id_st, 1u);
+                }
+                __syncwarp();
+                if (g >= 2) mbar_wait(&bars->dq_drained[bn], ((g - 2) >> 1) & 1);
+                tc_fence_after();
+                if (lane == 0) BTR(1, g);
+                if (elect_one()) {
+                    const uint32_t qb = pb + s * kSlot, ob = qb + kQT;
+                    const uint32_t vb = pb + sV * kSlot;
+                    const uint32_t buf = tmem + 128 * bn;
+#pragma unroll
+                    for (int kk = 0; kk < D / 16 && GFWA_BWD_EXPT != 2; ++kk) {
+                        const uint32_t ka = (kk >> 2) * kKVbox + (kk & 3) * 32;
+                        const uint32_t qa = (kk >> 2) * kQTbox + (kk & 3) * 32;
+                        mma_ss(buf + 64, sdesc_sw128(vb + ka, 16, 1024), sdesc_sw128(ob + qa, 16, 1024), id_st, kk > 0);
+                    }
+                    const uint64_t bslab = sdesc_sw128(smem_u32(augB) + 32 * (g & 3), 16, 1024);
+                    mma_ss(buf + 64, sdesc_sw128(smem_u32(augA) + 32, 16, 0), bslab, id_st, 1u);
+                    tc_commit(&bars->st_full[bn]);
+                    tc_commit(&bars->aug_empty[g & 3]);
+                    if (m == it.tot - 1) tc_commit(&bars->empty[sV]);  // V's last reader was this dP^T
+                }
+                __syncwarp();
+#else
                 if (g >= 2) mbar_wait(&bars->dq_drained[bn], ((g - 2) >> 1) & 1);
                 tc_fence_after();
                 if (lane == 0) BTR(1, g);
@@ -430,6 +473,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (m == it.tot - 1) tc_commit(&bars->empty[sV]);  // V's last reader was this dP^T
                 }
                 __syncwarp();
+#endif
                 if (pg >= 0) mma2();
                 pg = g;
                 pm = m;
