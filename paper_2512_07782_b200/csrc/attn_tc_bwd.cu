@@ -79,7 +79,7 @@ constexpr int kThreads = 32 * (kTmaWarp + 1);  // softmax-grad WGs, drain WG, MM
 #define GFWA_BWD_DQRED 0  // 1: dQ^T drained by per-query red.global.add instead of TMA bulk reductions
 #endif
 #ifndef GFWA_BWD_SFIRST
-#define GFWA_BWD_SFIRST 0  // issue S^T(g) before waiting for the drain of dQ^T(g-2) (only dP^T(g) needs it)
+#define GFWA_BWD_SFIRST 1  // issue S^T(g) before waiting for the drain of dQ^T(g-2) (only dP^T(g) needs it)
 #endif
 #ifndef GFWA_BWD_NODUQ
 #define GFWA_BWD_NODUQ 0  // experiment only: skip the du^q butterfly (wrong dU)
