@@ -155,6 +155,29 @@ typedef struct {
     gfwa_dtype_t dtype; /* dtype of Q, K, V, O, dO, dQ, dK, dV */
     int64_t q_stride[3], k_stride[3], v_stride[3], o_stride[3];
     int64_t H_kv;       /* K/V heads (GQA), H % H_kv == 0; 0 = H */
+    /*
+     * In-kernel halo (SURVEY 8(e)'s B200 refinement, 8(f) f3): halo_rows > 0 makes
+     * the attention kernels TMA-load key rows [0, halo_rows) straight from K_halo /
+     * V_halo -- typically the previous sequence shard's last rows in that rank's own
+     * memory, mapped into this process (CUDA IPC / NVLink peer pointer), so the
+     * halo never needs a copy or a send -- and rows [halo_rows, N_kv) from K / V,
+     * which then hold N_kv - halo_rows rows ([B, N_kv - halo_rows, H_kv, d] with
+     * k_stride / v_stride).  K_halo / V_halo are [B, halo_rows, H_kv, d] with
+     * kh_stride / vh_stride (elements, 16-byte aligned) and must stay valid and
+     * unchanged until the call's work completes on the stream.  Requirements:
+     * BF16, the tensor-core path, halo_rows % 128 == 0, halo_rows <= N_kv - N_q
+     * (the halo lies in front of every query); INVALID_ARGUMENT / UNSUPPORTED
+     * otherwise.  Results equal the same call on one contiguous [halo; local] K / V;
+     * gradients (dK, dV, dU) still cover all N_kv rows in the caller's buffers,
+     * dK / dV with K's / V's strides (so with B > 1 the batch stride of K / V must
+     * span N_kv rows, e.g. K / V views of the local rows of [B, N_kv, H_kv, d]
+     * buffers).
+     * halo_rows = 0 (a zero-initialised tail): K / V hold all N_kv rows.
+     */
+    int64_t halo_rows;
+    const void* K_halo;
+    const void* V_halo;
+    int64_t kh_stride[3], vh_stride[3];
 } gfwa_attn_desc_t;
 
 /*

@@ -49,6 +49,11 @@ class AttnDesc(ctypes.Structure):
         ("v_stride", ctypes.c_int64 * 3),
         ("o_stride", ctypes.c_int64 * 3),
         ("H_kv", ctypes.c_int64),
+        ("halo_rows", ctypes.c_int64),
+        ("K_halo", ctypes.c_void_p),
+        ("V_halo", ctypes.c_void_p),
+        ("kh_stride", ctypes.c_int64 * 3),
+        ("vh_stride", ctypes.c_int64 * 3),
     ]
 
 
@@ -238,9 +243,30 @@ def _bnh_strides(t: torch.Tensor):
     return (t.stride(0), t.stride(1), t.stride(2))
 
 
-def make_desc(Q, K, V, O_like, w: int, scale: float | None) -> AttnDesc:
+def _grad_kv(K, V, Nkv: int):
+    """dK, dV over all Nkv key rows: K's layout when K holds them all, else contiguous
+    [B, Nkv, H_kv, d] (the in-kernel halo: K holds only the local rows)."""
+    if K.shape[1] == Nkv:
+        return (torch.empty_strided(K.shape, K.stride(), dtype=K.dtype, device=K.device),
+                torch.empty_strided(V.shape, V.stride(), dtype=V.dtype, device=V.device))
+    # the ABI gives dK / dV K's / V's strides: a batch stride must cover all Nkv rows
+    # (B = 1, or K a view of the local rows of a [B, Nkv, H_kv, d] buffer)
+    shp = (K.shape[0], Nkv, K.shape[2], K.shape[3])
+    out = []
+    for T in (K, V):
+        if T.shape[0] > 1 and T.stride(0) < Nkv * T.stride(1):
+            raise GfwaError("kv_halo with B > 1: K / V must be views of [B, N_kv, H_kv, d] buffers")
+        out.append(torch.empty_strided(shp, T.stride(), dtype=T.dtype, device=T.device))
+    return out[0], out[1]
+
+
+def make_desc(Q, K, V, O_like, w: int, scale: float | None, kv_halo=None) -> AttnDesc:
+    """kv_halo = (K_halo, V_halo): the in-kernel halo (include/gfwa.h): key rows
+    [0, halo) are read from these tensors (e.g. CUDA-IPC / peer-mapped views of the
+    previous shard's last rows) and K, V hold the remaining rows."""
     B, Nq, H, d = Q.shape
-    Nkv = K.shape[1]
+    hr = 0 if kv_halo is None else kv_halo[0].shape[1]
+    Nkv = K.shape[1] + hr
     dsc = AttnDesc()
     dsc.B, dsc.H, dsc.N_q, dsc.N_kv, dsc.d, dsc.w = B, H, Nq, Nkv, d, int(w)
     dsc.scale = float(scale) if scale is not None else 0.0
@@ -250,6 +276,14 @@ def make_desc(Q, K, V, O_like, w: int, scale: float | None) -> AttnDesc:
     dsc.v_stride[:] = _bnh_strides(V)
     dsc.o_stride[:] = _bnh_strides(O_like)
     dsc.H_kv = K.shape[2] if K.shape[2] != H else 0  # GQA: K/V heads (0 = H)
+    if kv_halo is not None:
+        Kh, Vh = kv_halo
+        if Kh.shape != Vh.shape or Kh.shape[0] != B or Kh.shape[2:] != K.shape[2:] or Kh.dtype != K.dtype:
+            raise GfwaError("kv_halo tensors must be [B, halo_rows, H_kv, d] like K")
+        dsc.halo_rows = hr
+        dsc.K_halo, dsc.V_halo = Kh.data_ptr(), Vh.data_ptr()
+        dsc.kh_stride[:] = _bnh_strides(Kh)
+        dsc.vh_stride[:] = _bnh_strides(Vh)
     return dsc
 
 
@@ -331,14 +365,16 @@ def gfwa_gate_prefix_bwd(dU: torch.Tensor, h: torch.Tensor | None = None, beta: 
 
 
 def gfwa_fwd(Q, K, V, U, w: int, scale: float | None = None, want_o_lo: bool = False, out=None, out_lo=None,
-             prepare_bwd: bool = False):
+             prepare_bwd: bool = False, kv_halo=None):
     """O [B,Nq,H,d], LSE [B,H,Nq] (+ O_lo) per Eq. 12 / Alg. 2.
     O_lo (bf16 only; None for fp32, whose O is exact): the bf16 residual of the
     output cast, bf16(O_exact - O), for the backward's D (reading C-12).
     out / out_lo: caller tensors (views allowed) receiving O and O_lo; O_lo must
     share O's element strides (the ABI's one stride set).
     prepare_bwd: gfwa_fwd_train on the workspace gfwa_bwd will use (the forward
-    zeroes the backward's dQ accumulator; the next gfwa_bwd skips that pass)."""
+    zeroes the backward's dQ accumulator; the next gfwa_bwd skips that pass).
+    kv_halo = (K_halo, V_halo): the first key rows come from these tensors (the
+    in-kernel halo of include/gfwa.h); K, V hold the rest and U covers all rows."""
     lib = load()
     _need_cuda(Q, K, V, U)
     U = U.contiguous()
@@ -353,7 +389,7 @@ def gfwa_fwd(Q, K, V, U, w: int, scale: float | None = None, want_o_lo: bool = F
         elif want_o_lo:
             O_lo = torch.empty_strided(O.shape, O.stride(), dtype=torch.bfloat16, device=Q.device)
     LSE = torch.empty(B, H, Nq, dtype=torch.float32, device=Q.device)
-    dsc = make_desc(Q, K, V, O, w, scale)
+    dsc = make_desc(Q, K, V, O, w, scale, kv_halo)
     if prepare_bwd:
         nbytes = lib.gfwa_bwd_workspace_size(ctypes.byref(dsc))
         ws = workspace(nbytes, Q.device, "bwd")  # the tensor gfwa_bwd below takes
@@ -368,8 +404,9 @@ def gfwa_fwd(Q, K, V, U, w: int, scale: float | None = None, want_o_lo: bool = F
 
 
 def gfwa_bwd(Q, K, V, U, O, LSE, dO, w: int, scale: float | None = None, O_lo=None, want_dalpha: bool = True,
-             dalpha_carry=None):
-    """dQ, dK, dV, dU (+ dalpha) per Alg. E.2; D = rowsum((O + O_lo) dO)."""
+             dalpha_carry=None, kv_halo=None):
+    """dQ, dK, dV, dU (+ dalpha) per Alg. E.2; D = rowsum((O + O_lo) dO).
+    kv_halo: as in gfwa_fwd; dK, dV then cover all N_kv rows (halo rows first)."""
     lib = load()
     _need_cuda(Q, K, V, U, O, LSE, dO)
     if dO.stride() != O.stride() or (O_lo is not None and O_lo.stride() != O.stride()):
@@ -377,16 +414,15 @@ def gfwa_bwd(Q, K, V, U, O, LSE, dO, w: int, scale: float | None = None, O_lo=No
         O, dO = O.contiguous(), dO.contiguous()
         O_lo = None if O_lo is None else O_lo.contiguous()
     B, Nq, H, d = Q.shape
-    Nkv = K.shape[1]
     dev = Q.device
+    dsc = make_desc(Q, K, V, O, w, scale, kv_halo)
+    Nkv = dsc.N_kv
     dQ = torch.empty_strided(Q.shape, Q.stride(), dtype=Q.dtype, device=dev)
-    dK = torch.empty_strided(K.shape, K.stride(), dtype=K.dtype, device=dev)
-    dV = torch.empty_strided(V.shape, V.stride(), dtype=V.dtype, device=dev)
+    dK, dV = _grad_kv(K, V, Nkv)
     dU = torch.empty(B, H, Nkv, dtype=torch.float32, device=dev)
     dalpha = torch.empty(B, H, Nkv, dtype=torch.float32, device=dev) if want_dalpha else None
     if dalpha_carry is not None:
         dalpha_carry = dalpha_carry.to(torch.float64).contiguous()
-    dsc = make_desc(Q, K, V, O, w, scale)
     nbytes = lib.gfwa_bwd_workspace_size(ctypes.byref(dsc))
     ws = workspace(nbytes, dev, "bwd")
     st = lib.gfwa_bwd(ctypes.byref(dsc), _ptr(Q), _ptr(K), _ptr(V), _ptr(U.contiguous()), _ptr(O), _ptr(O_lo),
@@ -462,7 +498,7 @@ def gfwa_bwd_normgate(Q, K, V, U, O, LSE, g, gamma, rstd, dY, w: int, eps: float
 
 
 def gfwa_bwd_rows_f32(Q, K, V, U, O, LSE, dO, w: int, head_rows: int, tail_rows: int,
-                      scale: float | None = None, O_lo=None):
+                      scale: float | None = None, O_lo=None, kv_halo=None):
     """gfwa_bwd plus fp32 copies [2 (dK, dV), B, rows, H_kv, d] of dK, dV for the first
     head_rows and last tail_rows key rows (sequence sharding: the halo's partial
     gradients travel and are added in fp32).  Returns (dQ, dK, dV, dU, head, tail)."""
@@ -472,16 +508,15 @@ def gfwa_bwd_rows_f32(Q, K, V, U, O, LSE, dO, w: int, head_rows: int, tail_rows:
         O, dO = O.contiguous(), dO.contiguous()
         O_lo = None if O_lo is None else O_lo.contiguous()
     B, Nq, H, d = Q.shape
-    Nkv = K.shape[1]
     dev = Q.device
+    dsc = make_desc(Q, K, V, O, w, scale, kv_halo)
+    Nkv = dsc.N_kv
     dQ = torch.empty_strided(Q.shape, Q.stride(), dtype=Q.dtype, device=dev)
-    dK = torch.empty_strided(K.shape, K.stride(), dtype=K.dtype, device=dev)
-    dV = torch.empty_strided(V.shape, V.stride(), dtype=V.dtype, device=dev)
+    dK, dV = _grad_kv(K, V, Nkv)
     dU = torch.empty(B, H, Nkv, dtype=torch.float32, device=dev)
     Hkv = K.shape[2]  # GQA: the copies have K's heads
     head = torch.empty(2, B, head_rows, Hkv, d, dtype=torch.float32, device=dev) if head_rows > 0 else None
     tail = torch.empty(2, B, tail_rows, Hkv, d, dtype=torch.float32, device=dev) if tail_rows > 0 else None
-    dsc = make_desc(Q, K, V, O, w, scale)
     nbytes = lib.gfwa_bwd_workspace_size(ctypes.byref(dsc))
     ws = workspace(nbytes, dev, "bwd")
     st = lib.gfwa_bwd_rows_f32(ctypes.byref(dsc), _ptr(Q), _ptr(K), _ptr(V), _ptr(U.contiguous()), _ptr(O),

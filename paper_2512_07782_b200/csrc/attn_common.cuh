@@ -12,6 +12,11 @@ struct AttnParams {
     float scale;
     // element strides over (b, n, h); d contiguous
     int64_t qs[3], ks[3], vs[3], os[3];
+    // in-kernel halo: key rows [0, hrows) from Kh / Vh (strides khs / vhs), the rest from K / V
+    int64_t hrows;
+    const void* Kh;
+    const void* Vh;
+    int64_t khs[3], vhs[3];
     // forward
     const void* Q;
     const void* K;

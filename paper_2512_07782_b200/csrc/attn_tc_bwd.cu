@@ -110,6 +110,7 @@ struct TcBwdParams {
     int64_t head_rows, tail_rows;
     float sl2, scale, inv_scale;
     unsigned long long* token;  // prepared-workspace token: consumed (cleared) by this kernel
+    int hrows;                  // in-kernel halo: key tiles below hrows come from the halo maps
 };
 
 #ifndef GFWA_BWD_TRACE
@@ -197,7 +198,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     bwd_tc_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
                   const __grid_constant__ CUtensorMap mv, const __grid_constant__ CUtensorMap mdo,
                   const __grid_constant__ CUtensorMap mdk, const __grid_constant__ CUtensorMap mdv,
-                  const __grid_constant__ CUtensorMap mdq, const TcBwdParams p) {
+                  const __grid_constant__ CUtensorMap mdq, const __grid_constant__ CUtensorMap mkh,
+                  const __grid_constant__ CUtensorMap mvh, const TcBwdParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     constexpr uint32_t kKV = BwdLay<D>::kV, kQT = BwdLay<D>::kQT;
@@ -281,9 +283,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 __syncwarp();
                 if (elect_one()) {
                     mbar_expect_tx(&bars->full[s], kKV);
+                    // in-kernel halo: key tiles below hrows from the halo's own (e.g. peer) memory
+                    const bool hz = it.j0 < p.hrows;
+                    const CUtensorMap* km = kv ? (hz ? &mvh : &mv) : (hz ? &mkh : &mk);
                     for (int half = 0; half < kHalves; ++half)
-                        tma_load_4d(dst + half * kKVbox, kv ? &mv : &mk, &bars->full[s], half * 64, it.h, it.j0,
-                                    it.b);
+                        tma_load_4d(dst + half * kKVbox, km, &bars->full[s], half * 64, it.h,
+                                    hz ? it.j0 : it.j0 - p.hrows, it.b);
                     mbar_arrive(&bars->full[s]);
                 }
                 __syncwarp();
@@ -1121,8 +1126,14 @@ static gfwa_status_t tc_bwd_d(const AttnParams& pin, cudaStream_t st, void* ws) 
     p.dQacc = (float*)ws;
     CUtensorMap mq, mk, mv, mdo, mdk, mdv, mdq;
     GFWA_REQUIRE(encode_bnhd_map(&mq, p.Q, p.B, p.Nq, p.H, D, p.qs, BMQ));
-    GFWA_REQUIRE(encode_bnhd_map(&mk, p.K, p.B, p.Nkv, p.Hkv, D, p.ks, BN));
-    GFWA_REQUIRE(encode_bnhd_map(&mv, p.V, p.B, p.Nkv, p.Hkv, D, p.vs, BN));
+    // K / V hold key rows [hrows, Nkv); rows [0, hrows) come from the halo maps (in-kernel halo)
+    GFWA_REQUIRE(encode_bnhd_map(&mk, p.K, p.B, p.Nkv - p.hrows, p.Hkv, D, p.ks, BN));
+    GFWA_REQUIRE(encode_bnhd_map(&mv, p.V, p.B, p.Nkv - p.hrows, p.Hkv, D, p.vs, BN));
+    CUtensorMap mkh = mk, mvh = mv;
+    if (p.hrows) {
+        GFWA_REQUIRE(encode_bnhd_map(&mkh, p.Kh, p.B, p.hrows, p.Hkv, D, p.khs, BN));
+        GFWA_REQUIRE(encode_bnhd_map(&mvh, p.Vh, p.B, p.hrows, p.Hkv, D, p.vhs, BN));
+    }
     GFWA_REQUIRE(encode_bnhd_map(&mdo, p.dO, p.B, p.Nq, p.H, D, p.os, BMQ));
     GFWA_REQUIRE(encode_bnhd_map(&mdk, p.dK, p.B, p.Nkv, p.Hkv, D, p.ks, BN / 4));  // [32 keys][64 d] store boxes
     GFWA_REQUIRE(encode_bnhd_map(&mdv, p.dV, p.B, p.Nkv, p.Hkv, D, p.vs, BN / 4));
@@ -1171,6 +1182,7 @@ static gfwa_status_t tc_bwd_d(const AttnParams& pin, cudaStream_t st, void* ws) 
     tp.scale = p.scale;
     tp.inv_scale = 1.f / p.scale;
     tp.token = p.token;
+    tp.hrows = (int)p.hrows;
     tp.dK = (__nv_bfloat16*)p.dK;
     tp.dV = (__nv_bfloat16*)p.dV;
     for (int i = 0; i < 3; ++i) {
@@ -1198,7 +1210,7 @@ static gfwa_status_t tc_bwd_d(const AttnParams& pin, cudaStream_t st, void* ws) 
     if (const char* e = getenv("GFWA_BWD_GRID")) cap = max64(1, atoll(e));  // diagnostics: fewer CTAs, more items each
     const unsigned grid = (unsigned)min64(n_items, cap);
     auto kern = (tp.f32_head || tp.f32_tail) ? bwd_tc_kernel<D, true> : bwd_tc_kernel<D, false>;
-    kern<<<grid, kThreads, kSmemBytes, st>>>(mq, mk, mv, mdo, mdk, mdv, mdq, tp);
+    kern<<<grid, kThreads, kSmemBytes, st>>>(mq, mk, mv, mdo, mdk, mdv, mdq, mkh, mvh, tp);
     note_launch();
     if (gfwa_status_t s = check_launch()) return s;
     stage_event(1, st);  // measurement hook: after the main kernel

@@ -121,6 +121,7 @@ struct TcFwdParams {
     float* ng_rstd;
     float ng_eps;
     int64_t os[3];  // O's (= g's, Y's) element strides over (b, n, h)
+    int hrows;      // in-kernel halo: key tiles below hrows come from the halo maps
 };
 
 #if GFWA_FWD_TRACE
@@ -231,7 +232,8 @@ template <int D, bool kF16P, bool kNG>
 __global__ void __launch_bounds__(kThreads, 1)
     fwd_tc_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
                   const __grid_constant__ CUtensorMap mv, const __grid_constant__ CUtensorMap mo,
-                  const __grid_constant__ CUtensorMap mol, const TcFwdParams p) {
+                  const __grid_constant__ CUtensorMap mol, const __grid_constant__ CUtensorMap mkh,
+                  const __grid_constant__ CUtensorMap mvh, const TcFwdParams p) {
     extern __shared__ __align__(1024) uint8_t smem[];
     using L = Lay<D>;
     constexpr uint32_t kTile = L::kTile, kOffQ = L::kOffQ, kOffKV = L::kOffKV, kOffE = L::kOffE,
@@ -320,9 +322,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (elect_one()) {
                         uint64_t* full = kv ? &bars->v_full[sl] : &bars->k_full[sl];
                         mbar_expect_tx(full, kTile);
+                        // in-kernel halo: tiles below hrows from the halo's own (e.g. peer) memory
+                        const bool hz = j * BN < p.hrows;
+                        const CUtensorMap* km = kv ? (hz ? &mvh : &mv) : (hz ? &mkh : &mk);
                         for (int half = 0; half < kHalves; ++half)
-                            tma_load_4d_hint(smem + kOffKV + sl * kTile + half * kBox, kv ? &mv : &mk, full,
-                                             half * 64, it.h / p.G, j * BN, it.b, pol_kv);
+                            tma_load_4d_hint(smem + kOffKV + sl * kTile + half * kBox, km, full, half * 64,
+                                             it.h / p.G, hz ? j * BN : j * BN - p.hrows, it.b, pol_kv);
                     }
                     if (kv == 0) {
                         // K_j's slab: b = (uref - u_k) / scale per key as hi + mid + lo bf16, so the
@@ -890,8 +895,14 @@ template <int D>
 static gfwa_status_t tc_fwd_d(const AttnParams& p, cudaStream_t st) {
     CUtensorMap mq, mk, mv, mo, mol;
     GFWA_REQUIRE(encode_bnhd_map(&mq, p.Q, p.B, p.Nq, p.H, D, p.qs, BM));
-    GFWA_REQUIRE(encode_bnhd_map(&mk, p.K, p.B, p.Nkv, p.Hkv, D, p.ks, BN));
-    GFWA_REQUIRE(encode_bnhd_map(&mv, p.V, p.B, p.Nkv, p.Hkv, D, p.vs, BN));
+    // K / V hold key rows [hrows, Nkv); rows [0, hrows) come from the halo maps (in-kernel halo)
+    GFWA_REQUIRE(encode_bnhd_map(&mk, p.K, p.B, p.Nkv - p.hrows, p.Hkv, D, p.ks, BN));
+    GFWA_REQUIRE(encode_bnhd_map(&mv, p.V, p.B, p.Nkv - p.hrows, p.Hkv, D, p.vs, BN));
+    CUtensorMap mkh = mk, mvh = mv;
+    if (p.hrows) {
+        GFWA_REQUIRE(encode_bnhd_map(&mkh, p.Kh, p.B, p.hrows, p.Hkv, D, p.khs, BN));
+        GFWA_REQUIRE(encode_bnhd_map(&mvh, p.Vh, p.B, p.hrows, p.Hkv, D, p.vhs, BN));
+    }
     GFWA_REQUIRE(encode_bnhd_map(&mo, p.O, p.B, p.Nq, p.H, D, p.os, BM));
     if (p.O_lo)
         GFWA_REQUIRE(encode_bnhd_map(&mol, p.O_lo, p.B, p.Nq, p.H, D, p.os, BM));
@@ -919,6 +930,7 @@ static gfwa_status_t tc_fwd_d(const AttnParams& p, cudaStream_t st) {
     tp.ng_rstd = p.ng_rstd;
     tp.ng_eps = p.ng_eps;
     for (int i = 0; i < 3; ++i) tp.os[i] = p.os[i];
+    tp.hrows = (int)p.hrows;
     tp.n_pairs = (int)((p.Nq + 2 * BM - 1) / (2 * BM));
     const int64_t n_items = (int64_t)tp.n_pairs * p.H * p.B;
     if (n_items >= ((int64_t)1 << 31) || p.Nkv + 2 * BM >= ((int64_t)1 << 31)) return GFWA_ERR_INVALID_ARGUMENT;
@@ -935,7 +947,7 @@ static gfwa_status_t tc_fwd_d(const AttnParams& p, cudaStream_t st) {
     int64_t cap = n_sm;
     if (const char* e = getenv("GFWA_FWD_GRID")) cap = max64(1, atoll(e));  // diagnostics: fewer CTAs, more items each
     const unsigned grid = (unsigned)min64(n_items, cap);
-    kern<<<grid, kThreads, kSmemBytes, st>>>(mq, mk, mv, mo, mol, tp);
+    kern<<<grid, kThreads, kSmemBytes, st>>>(mq, mk, mv, mo, mol, mkh, mvh, tp);
     note_launch();
     if (gfwa_status_t s = check_launch()) return s;
     if (!p.ng_g) return GFWA_OK;

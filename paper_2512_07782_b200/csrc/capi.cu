@@ -124,6 +124,20 @@ gfwa_status_t make_params(const gfwa_attn_desc_t* d, AttnParams& p) {
         p.os[i] = d->o_stride[i];
     }
     if (d->H > 65535 || d->B > 65535) return GFWA_ERR_INVALID_ARGUMENT;
+    p.hrows = d->halo_rows;
+    if (p.hrows != 0) {  // in-kernel halo: BF16 tensor-core path (checked at dispatch)
+        if (p.hrows < 0 || p.hrows % 128 != 0 || p.hrows > p.h0 || d->dtype != GFWA_BF16 || !d->K_halo ||
+            !d->V_halo || ((uintptr_t)d->K_halo % 16) || ((uintptr_t)d->V_halo % 16))
+            return GFWA_ERR_INVALID_ARGUMENT;
+        p.Kh = d->K_halo;
+        p.Vh = d->V_halo;
+        for (int i = 0; i < 3; ++i) {
+            p.khs[i] = d->kh_stride[i];
+            p.vhs[i] = d->vh_stride[i];
+            if (p.khs[i] < 0 || p.vhs[i] < 0 || (p.khs[i] * 2) % 16 || (p.vhs[i] * 2) % 16)
+                return GFWA_ERR_INVALID_ARGUMENT;
+        }
+    }
     return GFWA_OK;
 }
 
@@ -146,6 +160,22 @@ bool strides_ok(const int64_t* s, size_t esize) {
 
 bool al16(const void* p) { return ((uintptr_t)p % 16) == 0; }
 
+// in-kernel halo on another GPU's memory (a peer-mapped pointer): the kernels' TMA reads
+// it over NVLink, which needs peer access from the current device (IPC mappings opened
+// with lazy peer access have it already; "already enabled" is not an error)
+void ensure_peer_access(const void* ptr) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+        cudaGetLastError();
+        return;
+    }
+    int cur = 0, can = 0;
+    if (cudaGetDevice(&cur) != cudaSuccess || a.device < 0 || a.device == cur) return;
+    if (cudaDeviceCanAccessPeer(&can, cur, a.device) == cudaSuccess && can &&
+        cudaDeviceEnablePeerAccess(a.device, 0) != cudaSuccess)
+        cudaGetLastError();  // cudaErrorPeerAccessAlreadyEnabled
+}
+
 }  // namespace
 
 extern "C" gfwa_status_t gfwa_fwd(const gfwa_attn_desc_t* desc, const void* Q, const void* K, const void* V,
@@ -159,6 +189,10 @@ extern "C" gfwa_status_t gfwa_fwd(const gfwa_attn_desc_t* desc, const void* Q, c
     if (!al16(Q) || !al16(K) || !al16(V) || !al16(O) || (O_lo && !al16(O_lo))) return GFWA_ERR_INVALID_ARGUMENT;
     if (O_lo && desc->dtype != GFWA_BF16) return GFWA_ERR_INVALID_ARGUMENT;  // an fp32 O is exact already
     bind_context(Q);
+    if (p.hrows) {
+        ensure_peer_access(p.Kh);
+        ensure_peer_access(p.Vh);
+    }
     p.Q = Q;
     p.K = K;
     p.V = V;
@@ -178,7 +212,8 @@ extern "C" gfwa_status_t gfwa_fwd(const gfwa_attn_desc_t* desc, const void* Q, c
         p.ng_Y = g_normgate.Y;
     }
     cudaStream_t st = (cudaStream_t)stream;
-    if (p.Hkv != p.H && !tc_fwd_supported(p, desc->dtype)) return GFWA_ERR_UNSUPPORTED;  // GQA: tensor-core path
+    if ((p.Hkv != p.H || p.hrows) && !tc_fwd_supported(p, desc->dtype))
+        return GFWA_ERR_UNSUPPORTED;  // GQA, in-kernel halo: tensor-core path
     gfwa_status_t s = tc_fwd_supported(p, desc->dtype) ? tc_fwd(p, st) : simt_fwd(p, desc->dtype, st);
     if (s != GFWA_OK || !check_finite_env()) return s;
     // opt-in debug check (GFWA_CHECK_FINITE=1): LSE, and O when it is packed
@@ -261,6 +296,10 @@ extern "C" gfwa_status_t gfwa_bwd(const gfwa_attn_desc_t* desc, const void* Q, c
     p.token = tc_bwd_supported(p, desc->dtype) ? (unsigned long long*)((char*)ws + off_tok) : nullptr;
     p.token_val = prep_token(p);
     bind_context(Q);
+    if (p.hrows) {
+        ensure_peer_access(p.Kh);
+        ensure_peer_access(p.Vh);
+    }
     p.Q = Q;
     p.K = K;
     p.V = V;
@@ -293,7 +332,8 @@ extern "C" gfwa_status_t gfwa_bwd(const gfwa_attn_desc_t* desc, const void* Q, c
         p.f32_tail_rows = g_rows.tail_rows;
     }
     cudaStream_t st = (cudaStream_t)stream;
-    if (p.Hkv != p.H && !tc_bwd_supported(p, desc->dtype)) return GFWA_ERR_UNSUPPORTED;  // GQA: tensor-core path
+    if ((p.Hkv != p.H || p.hrows) && !tc_bwd_supported(p, desc->dtype))
+        return GFWA_ERR_UNSUPPORTED;  // GQA, in-kernel halo: tensor-core path
     gfwa_status_t s;
     if (tc_bwd_supported(p, desc->dtype)) {
         s = tc_bwd(p, st, (char*)ws + off_tc);  // D, dQ/dU zeroing fused in its own pre kernel

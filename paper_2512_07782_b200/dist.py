@@ -46,6 +46,10 @@ class Ops:
     # dK, dV, so the halo gradients travel and are added before their one rounding
     # (fp32).  None: the halo rows travel in the gradients' dtype
     bwd_rows: Callable | None = None
+    # in-kernel peer halo (SURVEY 8(e) refinement, f3): fwd / bwd_rows with kv_halo = the
+    # previous rank's last w K/V rows read by TMA straight from its memory (map_peer_halo)
+    fwd_halo: Callable | None = None      # (Q, K, V, U, w, kv_halo) -> (O, LSE, O_lo)
+    bwd_rows_halo: Callable | None = None  # bwd_rows(..., kv_halo) -> as bwd_rows
 
 
 def cuda_ops() -> Ops:
@@ -72,8 +76,15 @@ def cuda_ops() -> Ops:
             return (*_bwd(Q, K, V, U, O, LSE, dO, w, Olo), None, None)
         return gb.gfwa_bwd_rows_f32(Q, K, V, U, O, LSE, dO, w, head_rows, tail_rows, O_lo=Olo)
 
+    def _fwd_halo(Q, K, V, U, w, kv_halo):
+        return gb.gfwa_fwd(Q, K, V, U, w, want_o_lo=True, prepare_bwd=True, kv_halo=kv_halo)
+
+    def _bwd_rows_halo(Q, K, V, U, O, LSE, dO, w, Olo, head_rows, tail_rows, kv_halo):
+        return gb.gfwa_bwd_rows_f32(Q, K, V, U, O, LSE, dO, w, head_rows, tail_rows, O_lo=Olo, kv_halo=kv_halo)
+
     return Ops(gate_prefix=lambda h, b, eps: gb.gfwa_gate_prefix(h, b, eps, want_total=True), fwd=_fwd, bwd=_bwd,
-               gate_bwd=_gate_bwd, fwd_into=_fwd_into, bwd_rows=_bwd_rows)
+               gate_bwd=_gate_bwd, fwd_into=_fwd_into, bwd_rows=_bwd_rows, fwd_halo=_fwd_halo,
+               bwd_rows_halo=_bwd_rows_halo)
 
 
 class Ring:
@@ -136,6 +147,38 @@ class ShardResult:
     U_offset: torch.Tensor = None  # P_r = sum of earlier ranks' gate totals [B,H] fp64: U = U_loc - P_r
 
 
+@dataclass
+class PeerHalo:
+    """map_peer_halo's result: kv = views of the previous rank's last w K / V rows in
+    its memory (None on rank 0); every rank passes its PeerHalo to sp_forward_backward."""
+    kv: tuple | None
+    mapped: tuple | None = None  # the mapped allocations (kept referenced)
+
+
+def map_peer_halo(K: torch.Tensor, V: torch.Tensor, w: int, ring: "Ring") -> PeerHalo:
+    """The in-kernel peer halo's mapping (SURVEY 8(e)'s B200 refinement): every rank
+    publishes CUDA IPC handles of its local K, V (torch's tensor reductions, exchanged
+    once through the process group) and rank r maps rank r-1's allocation into its
+    own address space -- over NVLink on a multi-GPU box (peer access), the same device
+    in the one-GPU tests.  Returns a PeerHalo with views of rank r-1's last w rows
+    for kv_halo (none on rank 0).  The caller keeps K, V alive and unchanged while a
+    neighbour's step may read them (the step's inputs are read-only)."""
+    from torch.multiprocessing.reductions import reduce_tensor
+
+    if K.device.type != "cuda" or K.dtype != torch.bfloat16:
+        raise ValueError("the in-kernel peer halo needs bf16 CUDA tensors")
+    mine = (reduce_tensor(K), reduce_tensor(V), K.shape[1])
+    objs = [None] * ring.world
+    dist.all_gather_object(objs, mine, group=ring.group)
+    if ring.rank == 0:
+        return PeerHalo(None)
+    (fk, ak), (fv, av), S_prev = objs[ring.rank - 1]
+    if w > S_prev:
+        raise ValueError(f"sequence sharding needs w <= rows per rank ({w} > {S_prev})")
+    Kp, Vp = fk(*ak), fv(*av)  # the previous rank's tensors, IPC-mapped
+    return PeerHalo((Kp[:, S_prev - w:], Vp[:, S_prev - w:]), (Kp, Vp))
+
+
 def halo_pack(K, V, U_loc, w: int):
     """Last w K/V rows and their u in the receiver's frame (U_loc[S-1] -> 0)."""
     S = K.shape[1]
@@ -185,13 +228,16 @@ def alloc_kv_ext(K: torch.Tensor, V: torch.Tensor, w: int):
 
 
 def sp_forward_backward(Q, K, V, h, beta, dO, w: int, ops: Ops, ring: Ring, eps: float = 1e-6,
-                        kv_ext=None) -> ShardResult:
+                        kv_ext=None, peer=None) -> ShardResult:
     """One sequence-sharded training step on this rank's S rows.
 
     Q, K, V, dO [B,S,H,d]; h, beta [B,S,H] (this rank's contiguous rows).
     Requires w <= S (one-hop halo).  kv_ext = (K_ext, V_ext) from alloc_kv_ext
     (K, V then being their local views) avoids copying the local rows every step;
-    dK, dV are then returned as views of the backward's [halo; local] outputs."""
+    dK, dV are then returned as views of the backward's [halo; local] outputs.
+    peer = map_peer_halo(K, V, w, ring), passed on every rank, selects the
+    in-kernel peer halo: the kernels TMA-load the previous rank's last w K/V rows
+    from its memory, so only the w u values travel forward (all ranks must agree)."""
     S = K.shape[1]
     if w > S:
         raise ValueError(f"sequence sharding needs w <= rows per rank ({w} > {S})")
@@ -200,10 +246,14 @@ def sp_forward_backward(Q, K, V, h, beta, dO, w: int, ops: Ops, ring: Ring, eps:
     # the running gate-sum offset of this shard (global U = U_loc - P_r): posted now,
     # collected after the backward (the attention only uses local frames, C-10)
     scan = global_offset_start(total, ring) if P > 1 else None
-    # forward halo r -> r+1 (K, V, u in the receiver's frame)
+    use_peer = peer is not None and P > 1
+    kv_peer = peer.kv if use_peer else None
+    # forward halo r -> r+1 (K, V, u in the receiver's frame; u only with the peer halo)
     like = halo_pack(K, V, U_loc, w)
+    if use_peer:
+        like = like[2:]
     handle = ring.start(like if r < P - 1 else None, like, forward=True)
-    split = kv_ext is not None and ops.fwd_into is not None and r > 0 and 2 * w <= S
+    split = kv_ext is not None and ops.fwd_into is not None and r > 0 and 2 * w <= S and not use_peer
     if split:
         # queries [w, S) see only local keys: run them while the halo is in flight,
         # then the first w queries over [halo; local[:w]] (the ABI's halo convention)
@@ -214,7 +264,11 @@ def sp_forward_backward(Q, K, V, h, beta, dO, w: int, ops: Ops, ring: Ring, eps:
         LSE = torch.empty(Q.shape[0], Q.shape[2], S, dtype=torch.float32, device=Q.device)
         LSE[..., w:] = ops.fwd_into(Q[:, w:], K, V, U_loc, w, O[:, w:], None if Olo is None else Olo[:, w:])
     recv = ring.finish(handle)
-    if recv is not None:
+    if recv is not None and use_peer:  # K / V halo read in-kernel from rank r-1's memory
+        Kx, Vx = K, V
+        Ux = torch.cat([recv[0], U_loc], -1).contiguous()
+        h0 = w
+    elif recv is not None:
         if kv_ext is not None:
             Kx, Vx = kv_ext  # the w halo rows land in front of the resident local rows
             Kx[:, :w].copy_(recv[0])
@@ -229,11 +283,16 @@ def sp_forward_backward(Q, K, V, h, beta, dO, w: int, ops: Ops, ring: Ring, eps:
     if split:
         LSE[..., :w] = ops.fwd_into(Q[:, :w], Kx[:, :2 * w], Vx[:, :2 * w], Ux[..., :2 * w].contiguous(), w,
                                     O[:, :w], None if Olo is None else Olo[:, :w])
+    elif use_peer and h0:
+        O, LSE, Olo = ops.fwd_halo(Q, Kx, Vx, Ux, w, kv_peer)
     else:
         O, LSE, Olo = ops.fwd(Q, Kx, Vx, Ux, w)
     tail_rows = w if r < P - 1 else 0
     head = tail = None
-    if ops.bwd_rows is not None:
+    if use_peer and h0:
+        dQ, dKx, dVx, dUx, head, tail = ops.bwd_rows_halo(Q, Kx, Vx, Ux, O, LSE, dO, w, Olo, h0, tail_rows,
+                                                          kv_peer)
+    elif ops.bwd_rows is not None:
         dQ, dKx, dVx, dUx, head, tail = ops.bwd_rows(Q, Kx, Vx, Ux, O, LSE, dO, w, Olo, h0, tail_rows)
     else:
         dQ, dKx, dVx, dUx = ops.bwd(Q, Kx, Vx, Ux, O, LSE, dO, w, Olo)

@@ -27,12 +27,12 @@ def _inputs():
     return Q, K, V, dO, h, beta
 
 
-def _worker(rank, world, port, outdir, use_ext=False):
+def _worker(rank, world, port, outdir, use_ext=False, use_peer=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from paper_2512_07782_b200.dist import Ring, alloc_kv_ext, cuda_ops, sp_forward_backward
+        from paper_2512_07782_b200.dist import Ring, alloc_kv_ext, cuda_ops, map_peer_halo, sp_forward_backward
 
         torch.cuda.set_device(0)
         Q, K, V, dO, h, beta = _inputs()
@@ -42,8 +42,13 @@ def _worker(rank, world, port, outdir, use_ext=False):
         Kl, Vl, kv_ext = cu(K), cu(V), None
         if use_ext:  # [halo; local] resident buffers (the bench's C4 path)
             kv_ext, Kl, Vl = alloc_kv_ext(Kl, Vl, W)
-        res = sp_forward_backward(cu(Q), Kl, Vl, cu(h), cu(beta), cu(dO), W, cuda_ops(), Ring(), kv_ext=kv_ext)
+        ring = Ring()
+        # in-kernel peer halo: rank r-1's K / V mapped by CUDA IPC, read by the kernels' TMA
+        peer = map_peer_halo(Kl, Vl, W, ring) if use_peer else None
+        res = sp_forward_backward(cu(Q), Kl, Vl, cu(h), cu(beta), cu(dO), W, cuda_ops(), ring, kv_ext=kv_ext,
+                                  peer=peer)
         torch.cuda.synchronize()
+        dist.barrier()  # rank r-1's K / V stay alive until rank r's kernels are done
         out = {k: getattr(res, k).float().cpu() for k in ("O", "dQ", "dK", "dV", "dU", "dalpha", "U_loc")}
         out["U_offset"] = res.U_offset.double().cpu()
         torch.save(out,
@@ -52,12 +57,12 @@ def _worker(rank, world, port, outdir, use_ext=False):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("use_ext", [False, True])
-def test_sequence_sharded_cuda_matches_oracle(use_ext):
+@pytest.mark.parametrize("use_ext,use_peer", [(False, False), (True, False), (True, True)])
+def test_sequence_sharded_cuda_matches_oracle(use_ext, use_peer):
     world = 2
-    port = 31500 + (os.getpid() % 2000) + (11 if use_ext else 0)
+    port = 31500 + (os.getpid() % 2000) + (11 if use_ext else 0) + (23 if use_peer else 0)
     with tempfile.TemporaryDirectory() as outdir:
-        mp.spawn(_worker, args=(world, port, outdir, use_ext), nprocs=world, join=True)
+        mp.spawn(_worker, args=(world, port, outdir, use_ext, use_peer), nprocs=world, join=True)
         Q, K, V, dO, h, beta = _inputs()
         U, _, _ = oracle.gate_prefix_hbeta(h, beta)
         O, _ = oracle.fwd(Q, K, V, U, W)
