@@ -740,6 +740,7 @@ def run_aux(dev, peaks):
     out["attn_layer_epilogue_C2"] = _attn_layer_epilogue(dev)
     out["nsa_hybrid"] = _nsa_hybrid(dev)
     out["gqa_C2"] = _gqa_c2(dev, peaks)
+    out["in_kernel_halo_C4_shard"] = _halo_c4_shard(dev)
     return out
 
 
@@ -781,6 +782,44 @@ def _gqa_c2(dev, peaks):
                               "pct_bf16_peak": round(fl / (ms * 1e-3) / 1e12 / peaks["bf16"], 4)}
         del Kg, Vg
     res["note"] = "C2 queries (B=8, H=16, N=4096, d=128, w=512), fwd+bwd eager, no dalpha scan"
+    return res
+
+
+def _halo_c4_shard(dev):
+    """The in-kernel halo (gfwa_attn_desc_t.halo_rows, f3) at one rank's shape of the
+    8-way sharded C4 step (S = 16384 query rows after a w = 2048 halo, H = 32, d = 128):
+    fwd (gfwa_fwd_train) + bwd with the halo tiles TMA-loaded from a separate buffer (as
+    from the previous rank's memory) vs the same call on one contiguous [halo; local]
+    K / V -- the halo costs no copy and no extra time."""
+    import torch
+
+    import synth
+    from paper_2512_07782_b200 import binding as gb
+
+    c = synth.CONFIGS["C4"]
+    w, S = c["w"], c["N"] // 8
+    s = synth.AttnShape(B=c["B"], H=c["H"], N=S, d=c["d"], w=w, N_kv=S + w)
+    Q, K, V, dO = synth.attn_inputs(s, seed=c["seed"], device=dev, dtype=torch.bfloat16)
+    h, beta = synth.gate_inputs(s.B, S + w, s.H, seed=c["seed"], device=dev)
+    U = gb.gfwa_gate_prefix(h, beta)
+    Kh, Vh = K[:, :w].clone(), V[:, :w].clone()
+    res = {}
+    for name, kv, halo in (("contiguous_ms", (K, V), None), ("kv_halo_ms", (K[:, w:], V[:, w:]), (Kh, Vh))):
+        def step():
+            O, LSE, Olo = gb.gfwa_fwd(Q, kv[0], kv[1], U, w, want_o_lo=True, prepare_bwd=True, kv_halo=halo)
+            gb.gfwa_bwd(Q, kv[0], kv[1], U, O, LSE, dO, w, O_lo=Olo, want_dalpha=False, kv_halo=halo)
+
+        for _ in range(3):
+            step()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(5):
+            step()
+        e1.record()
+        torch.cuda.synchronize(dev)
+        res[name] = round(e0.elapsed_time(e1) / 5, 4)
+    res["config"] = f"B=1, H={s.H}, S={S} query rows + {w}-row halo, d={s.d}, w={w}, fwd+bwd eager"
     return res
 
 
