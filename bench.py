@@ -430,7 +430,7 @@ def measure_seq(steps, warmup, dist, rank, world, local, dev, sample_clocks=Fals
 
     import synth
     from paper_2512_07782_b200 import binding as gb
-    from paper_2512_07782_b200.dist import Ring, alloc_kv_ext, cuda_ops, sp_forward_backward
+    from paper_2512_07782_b200.dist import Ring, alloc_kv_ext, cuda_ops, map_peer_halo, sp_forward_backward
 
     c = synth.CONFIGS["C4"]
     Ng = c["N"]
@@ -444,9 +444,13 @@ def measure_seq(steps, warmup, dist, rank, world, local, dev, sample_clocks=Fals
     ops = cuda_ops()
     st = torch.cuda.current_stream(dev)
     kv_ext, K, V = alloc_kv_ext(K, V, s.w)  # K/V resident behind a w-row halo slot
+    # opt-in (GFWA_PEER_HALO=1): the in-kernel peer halo -- rank r-1's K/V rows mapped by
+    # CUDA IPC and read by the kernels' TMA, only the u halo sent (not the default: it has
+    # not run across GPUs in this environment)
+    peer = map_peer_halo(K, V, s.w, ring) if world > 1 and os.environ.get("GFWA_PEER_HALO") == "1" else None
 
     def step():
-        return sp_forward_backward(Q, K, V, h, beta, dO, s.w, ops, ring, kv_ext=kv_ext)
+        return sp_forward_backward(Q, K, V, h, beta, dO, s.w, ops, ring, kv_ext=kv_ext, peer=peer)
 
     clk = ClockSampler(local).start() if sample_clocks else None
     if clk:
@@ -528,10 +532,11 @@ def measure_seq(steps, warmup, dist, rank, world, local, dev, sample_clocks=Fals
         "ms_per_step": round(ms, 4), "tokens_per_s": round(s.B * Ng / (ms * 1e-3), 1),
         "tflops_in_window": round(fl / (ms * 1e-3) / 1e12, 2), "gpu_launches": launches, "steps": steps,
         "config": {"workload": "C4 (BASELINE configs[3])", "B": s.B, "H": s.H, "N": Ng, "rows_per_rank": S,
-                   "d": s.d, "w": s.w, "parallelism": f"sequence-sharded x{world} (w-row K/V/u halo, "
+                   "d": s.d, "w": s.w, "halo": "in-kernel peer (CUDA IPC)" if peer is not None else "sent",
+                   "parallelism": f"sequence-sharded x{world} (w-row K/V/u halo, "
                                   f"{(dist.get_backend().upper() + ' P2P') if dist else 'no exchange'})",
                    "l2": "inputs larger than L2, no flush"}})
-    del Q, K, V, dO, h, beta, kv_ext
+    del Q, K, V, dO, h, beta, kv_ext, peer
     torch.cuda.empty_cache()
     return out
 
