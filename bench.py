@@ -537,6 +537,8 @@ def measure_seq(steps, warmup, dist, rank, world, local, dev, sample_clocks=Fals
                                   f"{(dist.get_backend().upper() + ' P2P') if dist else 'no exchange'})",
                    "l2": "inputs larger than L2, no flush"}})
     del Q, K, V, dO, h, beta, kv_ext, peer
+    if dist:
+        dist.barrier()  # every mapping of a neighbour's K/V is released before its owner frees it
     torch.cuda.empty_cache()
     return out
 
