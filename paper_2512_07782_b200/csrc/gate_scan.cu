@@ -166,19 +166,8 @@ template <typename Tin>
 __device__ __forceinline__ float load_in(const Tin* p) { return to_f32<Tin>(*p); }
 
 // alpha_t = softplus(beta_t h_t) / (beta_t + eps)  (Eq. 9, Alg. 1 l.6)
-#ifndef GFWA_GATE_LG2
-#define GFWA_GATE_LG2 0  // experiment: softplus from MUFU.EX2 + MUFU.LG2 (3 MUFU, ~10 instructions)
-#endif
 __device__ __forceinline__ float alpha_of(float hv, float bv, float eps) {
-#if GFWA_GATE_LG2
-    const float z = bv * hv;
-    float u, l;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(u) : "f"(-fabsf(z) * 1.4426950408889634f));
-    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l) : "f"(1.f + u));
-    return __fdividef(fmaf(l, 0.6931471805599453f, fmaxf(z, 0.f)), bv + eps);
-#else
     return __fdividef(softplus_fast(bv * hv), bv + eps);
-#endif
 }
 
 // smem index of token tt in a head row: one pad word per run of R tokens
