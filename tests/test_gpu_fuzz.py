@@ -46,3 +46,36 @@ def test_random_shapes_match_oracle(k, monkeypatch):
     assert max_abs(LSE, Lr) <= TOL_LSE
     for name, t in (("dQ", dQ), ("dK", dK), ("dV", dV), ("dU", dU), ("dalpha", da)):
         assert max_abs(t, ref[name]) <= TOL_BF16_GRAD, name
+
+
+@pytest.mark.parametrize("k", range(8))
+def test_random_shapes_kv_halo_match_oracle(k, monkeypatch):
+    """The in-kernel halo (gfwa_attn_desc_t.halo_rows) on random shapes: the first
+    halo_rows (a multiple of 128, <= the halo in front of the queries) key rows come
+    from a separate buffer, the rest of the halo (if any) from K / V; forced small grids."""
+    r = np.random.default_rng(9500 + k)
+    N = int(r.choice([1, 65, 200, 257, 511]))
+    hr = 128 * int(r.integers(1, 4))
+    extra = int(r.choice([0, 0, 37, 128]))  # halo rows beyond the in-kernel part, read from K
+    w = int(r.choice([1, 100, 300, 513, 1200]))
+    d = int(r.choice([64, 128]))
+    B, H = int(r.integers(1, 3)), int(r.integers(1, 4))
+    if r.integers(0, 2):
+        monkeypatch.setenv("GFWA_FWD_GRID", "2")
+        monkeypatch.setenv("GFWA_BWD_GRID", "3")
+    s = synth.AttnShape(B=B, H=H, N=N, d=d, w=w, N_kv=N + hr + extra)
+    Q, K, V, dO = synth.attn_inputs(s, seed=300 + k, dtype=torch.bfloat16)
+    g = torch.Generator().manual_seed(400 + k)
+    U = (-torch.cumsum(torch.nn.functional.softplus(torch.randn(s.B, s.H, s.nkv, generator=g)).double(), -1)).float()
+    Qd, Kd, Vd, dOd, Ud = (x.cuda() for x in (Q, K, V, dO, U))
+    halo = (Kd[:, :hr].clone(), Vd[:, :hr].clone())
+    O, LSE, Olo = gb.gfwa_fwd(Qd, Kd[:, hr:], Vd[:, hr:], Ud, s.w, want_o_lo=True, prepare_bwd=bool(k % 2),
+                              kv_halo=halo)
+    dQ, dK, dV, dU, da = gb.gfwa_bwd(Qd, Kd[:, hr:], Vd[:, hr:], Ud, O, LSE, dOd, s.w, O_lo=Olo, kv_halo=halo)
+    torch.cuda.synchronize()
+    Or, Lr = oracle.fwd(Q, K, V, U, s.w)
+    ref = oracle.bwd(Q, K, V, U, dO, s.w)
+    assert max_abs(O, Or) <= TOL_BF16_O
+    assert max_abs(LSE, Lr) <= TOL_LSE
+    for name, t in (("dQ", dQ), ("dK", dK), ("dV", dV), ("dU", dU), ("dalpha", da)):
+        assert max_abs(t, ref[name]) <= TOL_BF16_GRAD, name
